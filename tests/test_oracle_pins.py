@@ -1,0 +1,417 @@
+"""Pins for the CPU oracle against what the paper and the mathematics fix.
+
+Every test here checks oracle/ against something other than itself: values
+printed in PAPER.md (tests/golden), closed forms derived by hand in the
+docstrings, invariants (mass, symmetry, partition of unity), an independent
+route (FFT convolution, brute-force counting) or the paper's own formulas for
+quantities the oracle computes a different way (moments vs Eq. (4)).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SQ5 = math.sqrt(5.0)
+
+
+def _read_golden(name):
+    rows = []
+    with open(os.path.join(GOLD, name)) as fh:
+        for line in fh:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line.split())
+    return rows
+
+
+def _fine_moments(basis, r, a, N):
+    """Mass, first and second moments of beta by sampling on the lattice Z^2/N.
+
+    For a box spline the aliasing error of this rule decays like (pi N a)^-4r,
+    so it is an independent (spectral) route to the continuous moments."""
+    hx, hy = O.support_halfwidths(basis, r, a)
+    xs = np.arange(-math.ceil(hx * N) - 1, math.ceil(hx * N) + 2) / N
+    ys = np.arange(-math.ceil(hy * N) - 1, math.ceil(hy * N) + 2) / N
+    X, Y = np.meshgrid(xs, ys)
+    v = O.beta(basis, r, a, X.ravel(), Y.ravel()).reshape(X.shape) / N**2
+    return v.sum(), (v * X).sum(), (v * Y).sum(), (v * X * X).sum(), (v * X * Y).sum(), (v * Y * Y).sum(), v
+
+
+def _eq4_theta(a):
+    """Eq. (4), retyped here from the paper."""
+    a1, a2, a3, a4 = np.asarray(a) ** 2
+    return np.array([2 * a1 + a2 + a4, a2 - a4, 2 * a3 + a2 + a4]) / 24.0
+
+
+def _cov_theta_prime(a):
+    """PAPER.md:411-416, retyped here from the paper."""
+    a1, a2, a3, a4 = np.asarray(a) ** 2
+    return np.array([4 * a1 + a2 + a3 + 4 * a4, 2 * (a1 + a2 - a3 - a4), a1 + 4 * a2 + 4 * a3 + a4]) / 60.0
+
+
+# ----------------------------------------------------------------------------
+# Kernel evaluator
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+@pytest.mark.parametrize("r", [1, 2])
+def test_kernel_mass_and_covariance(basis, r):
+    """Unit mass and covariance r*C_a (Prop. 1) with C_a
+    from Eq. (4) (Theta) or PAPER.md:413-416 (Theta')."""
+    rng = np.random.default_rng(10 * basis + r)
+    ref = _eq4_theta if basis == O.THETA else _cov_theta_prime
+    for _ in range(2):
+        a = rng.uniform(1.5, 3.5, 4)
+        m, mx, my, cxx, cxy, cyy, _v = _fine_moments(basis, r, a, 64 if r == 1 else 8)
+        C = r * ref(a)
+        tol = 1e-6 if r == 1 else 1e-9  # aliasing of the N-lattice rule
+        assert abs(m - 1) < tol
+        assert abs(mx) < 1e-12 and abs(my) < 1e-12
+        np.testing.assert_allclose([cxx, cxy, cyy], C, atol=tol * max(C))
+    # oracle's own covariance map agrees with the retyped formulas
+    np.testing.assert_allclose(O.cov_of_scales(basis, a), ref(a), rtol=1e-14)
+
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+@pytest.mark.parametrize("zero", [0, 1, 2, 3])
+def test_kernel_with_zero_scale(basis, zero):
+    """One zero scale: still a unit-mass kernel with covariance C_a."""
+    rng = np.random.default_rng(7 + zero)
+    a = rng.uniform(2.0, 3.5, 4)
+    a[zero] = 0.0
+    ref = _eq4_theta if basis == O.THETA else _cov_theta_prime
+    for r in (1, 2):
+        m, mx, my, cxx, cxy, cyy, _ = _fine_moments(basis, r, a, 64 if r == 1 else 16)
+        tol = 5e-5 if r == 1 else 1e-7  # 3-direction kernel: slower aliasing decay
+        assert abs(m - 1) < tol
+        np.testing.assert_allclose([cxx, cxy, cyy], r * ref(a), atol=tol * max(r * ref(a)))
+
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+def test_kernel_symmetric_nonnegative(basis):
+    rng = np.random.default_rng(3)
+    for r in (1, 2, 3):
+        a = rng.uniform(1.0, 3.0, 4)
+        x = rng.uniform(-6, 6, 60)
+        y = rng.uniform(-6, 6, 60)
+        v = O.beta(basis, r, a, x, y)
+        w = O.beta(basis, r, a, -x, -y)
+        np.testing.assert_allclose(v, w, rtol=1e-12, atol=1e-15)
+        assert (v >= -1e-15).all()
+
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+def test_r1_polygon_equals_nested_integral(basis):
+    """Two independent evaluators at r = 1: rectangle overlap
+    and the nested Gauss-Legendre integral of Eq. (2)."""
+    rng = np.random.default_rng(5)
+    for _ in range(4):
+        a = rng.uniform(0.7, 5, 4)
+        x = rng.uniform(-5, 5, 300)
+        y = rng.uniform(-5, 5, 300)
+        p = O.beta(basis, 1, a, x, y, polygon=True)
+        g = O.beta(basis, 1, a, x, y, polygon=False)
+        np.testing.assert_allclose(p, g, atol=1e-13)
+
+
+def test_unit_kernel_value_at_origin():
+    """Hand-derived closed forms.
+
+    Theta': b = (sqrt5,)*4.  beta'_b(0) = |R13 n R24| / 25 with R13, R24
+    concentric squares of side sqrt5 rotated by theta, cos theta = u1.u2 = 4/5.
+    Each corner of one square is cut by the other along a right triangle with
+    legs h(1 - tan(theta/2)) and h(cos + sin - 1)/cos, h = sqrt5/2,
+    tan(theta/2) = 1/3: area h^2/6 = 5/24.  Overlap 5 - 4*5/24 = 25/6,
+    so beta'_b(0) = 1/6.
+    Theta: b = (1, sqrt2, 1, sqrt2).  R13 = unit square, R24 = the diamond
+    |x|+|y| <= 1 which contains it: overlap 1, beta_b(0) = 1/(1*2*1) = 1/2.
+    """
+    assert O.beta(O.THETA_PRIME, 1, [SQ5] * 4, 0.0, 0.0)[0] == pytest.approx(1 / 6, abs=1e-15)
+    assert O.beta(O.THETA, 1, [1, math.sqrt(2), 1, math.sqrt(2)], 0.0, 0.0)[0] == pytest.approx(0.5, abs=1e-15)
+
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+@pytest.mark.parametrize("r", [1, 2, 3])
+def test_unit_lattice_partition_of_unity(basis, r):
+    """The box spline whose scales equal the lattice step lengths (the
+    interpolation kernel of Eq. (11), r-fold) sums to one
+    over the integer translates: sum_q beta_h(x - q) = 1."""
+    h = np.linalg.norm(O.steps(basis).astype(float), axis=1)
+    rng = np.random.default_rng(r)
+    R = 3 * r + 2
+    qs = np.arange(-R, R + 1)
+    QX, QY = np.meshgrid(qs, qs)
+    for _ in range(5 if r < 3 else 2):
+        x, y = rng.uniform(0, 1, 2)
+        v = O.beta(basis, r, h, x - QX.ravel(), y - QY.ravel())
+        assert abs(v.sum() - 1) < 1e-13
+
+
+@pytest.mark.parametrize("r", [1, 2])
+def test_table2_isotropic_error(r):
+    """Table 2 isotropic columns: 10.8% and 4.9%."""
+    gold = {int(o): float(e) for o, e in _read_golden("table2_isotropic.txt")}
+    a, _ = O.solve_scales(O.THETA, np.array([1.0, 0.0, 1.0]) / r)
+    h, L = 0.04, 6.0
+    xs = np.arange(-L, L + h / 2, h)
+    X, Y = np.meshgrid(xs, xs)
+    v = O.beta(O.THETA, r, a, X.ravel(), Y.ravel()).reshape(X.shape)
+    G = np.exp(-(X**2 + Y**2) / 2) / (2 * np.pi)
+    err = 100 * math.sqrt(((v - G) ** 2).sum() / (G**2).sum())
+    assert round(err, 1) == gold[r]
+
+
+# ----------------------------------------------------------------------------
+# Scale solver
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+def test_isotropic_scales_sqrt6_sigma(basis):
+    """C = sigma^2 I -> every a_k = sqrt(6) sigma."""
+    for s in (0.5, 1.0, 3.0, 17.0):
+        a, _ = O.solve_scales(basis, [s * s, 0.0, s * s])
+        np.testing.assert_allclose(a, math.sqrt(6) * s, rtol=1e-13)
+
+
+def test_solver_hand_derived_diag41():
+    """C = diag(4, 1).
+    Theta': P = 16C11 - 4C22 = 60, Q = 16C22 - 4C11 = 0 forces t = 0 and
+    u = (30, 0, 0, 30): a = (sqrt30, 0, 0, sqrt30).
+    Theta: u = (48 - s, s, 12 - s, s), s in [0, 12], J = M11^2 + M22^2 with
+    M11 = (48-s)^2 + s^2, M22 = (12-s)^2 + s^2 decreasing on [0, 12], so
+    s = 12 and a = (6, sqrt12, 0, sqrt12)."""
+    a, _ = O.solve_scales(O.THETA_PRIME, [4.0, 0.0, 1.0])
+    np.testing.assert_allclose(a, [math.sqrt(30), 0, 0, math.sqrt(30)], atol=1e-7)
+    a, _ = O.solve_scales(O.THETA, [4.0, 0.0, 1.0])
+    np.testing.assert_allclose(a, [6, math.sqrt(12), 0, math.sqrt(12)], atol=1e-7)
+
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+def test_solver_roundtrip_and_optimality(basis):
+    """C_{a(C)} = C (against the retyped paper formulas) and J(t*) is the
+    minimum of a 10,001-point sweep of the family; homogeneity a(lC) = sqrt(l) a(C)."""
+    ref = _eq4_theta if basis == O.THETA else _cov_theta_prime
+    rng = np.random.default_rng(11 + basis)
+    n = 0
+    while n < 60:
+        smaj = rng.uniform(1, 20)
+        rho = rng.uniform(1, 6)
+        th = rng.uniform(0, math.pi)
+        sx, sy = smaj, smaj / math.sqrt(rho)
+        phi, rho2 = O.orient(sx, sy, th)
+        if rho2 > 0.95 * O.bound_rho(basis, phi):
+            continue
+        n += 1
+        C = O.decode(sx, sy, th)
+        a, t = O.solve_scales(basis, C)
+        np.testing.assert_allclose(ref(a), C, rtol=1e-11, atol=1e-12 * C[0])
+        st, lo, hi = O.family_range(basis, C)
+        ts = np.linspace(lo, hi, 10001)
+        J = np.array([O.family_J(basis, C, x) for x in ts])
+        Jt = O.family_J(basis, C, t)
+        assert Jt <= J.min() * (1 + 1e-12)
+        a2, _ = O.solve_scales(basis, 4.0 * C)
+        np.testing.assert_allclose(a2, 2 * a, rtol=1e-9, atol=1e-9 * a.max())
+
+
+# ----------------------------------------------------------------------------
+# Elongation bounds and basis selection
+# ----------------------------------------------------------------------------
+
+def test_table4_previous_bound_row():
+    """Eq. (6) reproduces Table 4 row 2; erratum at 30 deg."""
+    for deg, val, status in _read_golden("table4_previous_bound.txt"):
+        phi = math.radians(float(deg))
+        if val == "inf":
+            assert O.bound_rho(O.THETA, phi) > 1e12
+            continue
+        rho = O.eq6_rho(phi)
+        if status == "ok":
+            assert round(rho, 1) == float(val)
+        else:
+            assert round(rho, 2) == 6.46  # Eq. (6) at 30 deg; paper prints 6.1
+        # the rewritten bound used by the oracle equals Eq. (6) verbatim
+        assert O.bound_rho(O.THETA, phi) == pytest.approx(rho, rel=1e-12)
+
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+def test_bound_equals_solver_feasibility(basis):
+    """The closed-form bound is exactly where the scale family becomes empty."""
+    rng = np.random.default_rng(20 + basis)
+    for _ in range(200):
+        phi = rng.uniform(0, math.pi)
+        rb = O.bound_rho(basis, phi)
+        if not np.isfinite(rb) or rb > 1e6:
+            continue
+        for f, expect in ((0.99, 0), (1.01, -1)):
+            rho = f * rb
+            s = 2.0
+            C = O.decode(s, s / math.sqrt(rho), phi)
+            st, lo, hi = O.family_range(basis, C)
+            assert (st == 0) == (expect == 0), (phi, rho, rb)
+
+
+def test_dual_sector_switch_angles():
+    """Theta' is chosen iff its bound is larger (R8).  On [0, 45)
+    deg, 0.6/cos2phi = 1/(sin2phi+cos2phi) at tan 2phi = 2/3 and
+    0.8/sin2phi = 1/(sin2phi+cos2phi) at tan 2phi = 4 (hand-derived), so the
+    Theta' sector is (atan(2/3)/2, atan(4)/2) = (16.85, 37.98) deg, where the
+    dual bound is (1 + sqrt13/5)/(1 - sqrt13/5) = 6.171."""
+    lo, hi = math.atan(2 / 3) / 2, math.atan(4) / 2
+    for phi, expect in ((lo - 1e-6, 0), (lo + 1e-6, 1), (hi - 1e-6, 1), (hi + 1e-6, 0), (math.radians(30), 1)):
+        assert O.select(O.DUAL, 3.0, 1.5, phi) == expect
+    e = math.sqrt(13) / 5
+    assert O.bound_rho(O.THETA, lo) == pytest.approx((1 + e) / (1 - e), rel=1e-12)
+    assert O.select(O.DUAL, 2.0, 2.0, 0.5) == O.THETA  # isotropic -> Theta
+
+
+def test_clamp_keeps_trace_and_orientation():
+    phi = math.radians(22.5)
+    rb = O.bound_rho(O.THETA, phi)
+    sx, sy = 4.0, 4.0 / math.sqrt(2 * rb)
+    st, C = O.pixel_cov(O.THETA, 1, sx, sy, phi)
+    assert st == 1
+    assert C[0] + C[2] == pytest.approx(sx * sx + sy * sy, rel=1e-14)
+    w, V = np.linalg.eigh(np.array([[C[0], C[1]], [C[1], C[2]]]))
+    assert w[1] / w[0] == pytest.approx(0.95 * rb, rel=1e-10)
+    assert abs(abs(V[0, 1] * math.cos(phi) + V[1, 1] * math.sin(phi)) - 1) < 1e-12
+    st, _ = O.pixel_cov(O.THETA, 0, sx, sy, phi)
+    assert st == -1
+
+
+# ----------------------------------------------------------------------------
+# The filter (direct sum)
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("policy", [O.THETA, O.THETA_PRIME])
+def test_impulse_response_is_sampled_kernel(policy):
+    """Fig. 6 idea: an impulse image returns the sampled
+    kernel at p - q0."""
+    H = W = 31
+    img = np.zeros((H, W))
+    img[15, 14] = 1.0
+    sx, sy, th = 2.5, 1.4, 0.7
+    ys, xs = np.mgrid[0:H, 0:W]
+    out, bas, cl, sc = O.filter_points(img, xs.ravel(), ys.ravel(), sx, sy, th, policy=policy, r=1)
+    a = sc[0]
+    ref = O.beta(policy, 1, a, (xs - 14).ravel().astype(float), (ys - 15).ravel().astype(float))
+    np.testing.assert_allclose(out, ref, atol=1e-15)
+    assert abs(out.sum() - 1) < 2e-2  # sampled mass ~ 1 (not exact, R12)
+
+
+@pytest.mark.parametrize("policy,r", [(O.THETA_PRIME, 1), (O.THETA, 2)])
+def test_constant_covariance_equals_fft_convolution(policy, r):
+    """Constant covariance: the space-variant filter is a plain convolution
+    with the sampled kernel; compare with a zero-padded FFT convolution."""
+    rng = np.random.default_rng(4)
+    H, W = 24, 20
+    img = rng.uniform(0, 1, (H, W))
+    sx, sy, th = 2.2, 1.3, 0.4
+    ys, xs = np.mgrid[0:H, 0:W]
+    out, bas, cl, sc = O.filter_points(img, xs.ravel(), ys.ravel(), sx, sy, th, policy=policy, r=r)
+    a = sc[0]
+    R = 14
+    ks = np.arange(-R, R + 1).astype(float)
+    KX, KY = np.meshgrid(ks, ks)
+    K = O.beta(policy, r, a, KX.ravel(), KY.ravel()).reshape(KX.shape)
+    assert K[0, :].max() == 0 and K[:, 0].max() == 0
+    SH, SW = H + 2 * R + 1, W + 2 * R + 1
+    F = np.fft.rfft2(img, (SH, SW)) * np.fft.rfft2(K, (SH, SW))
+    full = np.fft.irfft2(F, (SH, SW))
+    ref = full[R:R + H, R:R + W]
+    np.testing.assert_allclose(out.reshape(H, W), ref, atol=1e-12)
+
+
+def test_filter_linearity_and_view():
+    rng = np.random.default_rng(8)
+    H, W = 40, 44
+    f1 = rng.uniform(0, 1, (H, W))
+    f2 = rng.uniform(0, 1, (H, W))
+    px = rng.integers(0, W, 30)
+    py = rng.integers(0, H, 30)
+    sx = rng.uniform(1, 3, 30)
+    sy = rng.uniform(1, 3, 30)
+    th = rng.uniform(0, math.pi, 30)
+    kw = dict(policy=O.DUAL, r=1)
+    o1 = O.filter_points(f1, px, py, sx, sy, th, **kw)[0]
+    o2 = O.filter_points(f2, px, py, sx, sy, th, **kw)[0]
+    o3 = O.filter_points(2 * f1 - 3 * f2, px, py, sx, sy, th, **kw)[0]
+    np.testing.assert_allclose(o3, 2 * o1 - 3 * o2, atol=1e-12)
+    # a sub-view that still covers every support gives the same result
+    sel = (px >= 1 + 12) & (py >= 2 + 12)
+    assert sel.sum() >= 2
+    o4 = O.filter_points(f1[2:, 1:], px[sel], py[sel], sx[sel], sy[sel], th[sel], full_shape=(H, W),
+                         origin=(1, 2), **kw)
+    np.testing.assert_allclose(o4[0], o1[sel], atol=0)
+    with pytest.raises(ValueError):
+        O.filter_points(f1[2:, 1:], [0], [0], 2.0, 2.0, 0.0, full_shape=(H, W), origin=(1, 2), **kw)
+
+
+# ----------------------------------------------------------------------------
+# Integer pre-integration reference
+# ----------------------------------------------------------------------------
+
+def _count_reps(steps_order, r, maxv):
+    """N(v) = #{j in N^{4r} : sum j_i s_i = v} by multiplying the generating
+    functions of the 4r one-dimensional rays (independent of the scan)."""
+    import collections
+    cur = collections.Counter({(0, 0): 1})
+    for _rep in range(r):
+        for sx, sy in steps_order:
+            nxt = collections.Counter()
+            for (vx, vy), c in cur.items():
+                j = 0
+                while True:
+                    wx, wy = vx + j * sx, vy + j * sy
+                    if abs(wx) > maxv[0] or wy > maxv[1] or (sx == 0 and sy == 0):
+                        break
+                    nxt[(wx, wy)] += c
+                    j += 1
+            cur = nxt
+    return cur
+
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+@pytest.mark.parametrize("r", [1, 2])
+def test_preintegration_counts(basis, r):
+    """Without domain truncation g(q) = sum_q' f(q') N(q - q'), N = number of
+    representations of q - q' by the running-sum steps."""
+    rng = np.random.default_rng(9)
+    H, W = 3, 4
+    f = rng.integers(0, 256, (H, W)).astype(np.uint8)
+    Pb = 4
+    GH = H + Pb
+    P = 2 * GH + 2  # lines cannot leave the domain sideways: no truncation
+    g = O.preintegrate_u8(f, basis, r, P, Pb)
+    N = _count_reps([tuple(s) for s in O.steps(basis)], r, (W + 2 * P, GH))
+    ref = np.zeros_like(g, dtype=object)
+    for (vx, vy), c in N.items():
+        for y in range(H):
+            for x in range(W):
+                Y, X = y + vy, x + vx + P
+                if 0 <= Y < GH and 0 <= X < W + 2 * P:
+                    ref[Y, X] += int(f[y, x]) * c
+    ref = np.array([[int(v) % 2**64 for v in row] for row in ref], dtype=np.uint64)
+    # only points whose whole backward cone stays inside [-P, W+P) are pinned
+    ok = np.zeros(g.shape, dtype=bool)
+    for Y in range(GH):
+        for X in range(W + 2 * P):
+            ok[Y, X] = (X - P) - 2 * Y >= -P and (X - P) + 2 * Y < W + P
+    assert ok.sum() > 20
+    np.testing.assert_array_equal(g[ok], ref[ok])
+
+
+def test_preintegration_impulse_single_level_ray():
+    """One level along s from an impulse is the ray {q0 + j s} (S:379 idea)."""
+    f = np.zeros((6, 5), dtype=np.uint8)
+    f[1, 2] = 7
+    g = O.preintegrate_u8(f, O.THETA, 1, 12, 3)
+    # the first Theta level is (1,0): row 1 from x=2 on; total mass after all
+    # levels at the bottom-right corner region is positive; check level-1
+    # semantics through a constant image instead: g on the first row with
+    # W = 5 counts lattice points of the cone.
+    assert g[1, 12 + 2] >= 7 and g[0].sum() == 0
