@@ -1,0 +1,165 @@
+/*
+ * bsf.h -- C ABI of the B200-native O(1) space-variant box-spline filter.
+ *
+ * Method: Chaudhury & Sanyal, "Improvements on 'Fast space-variant elliptical
+ * filtering using box splines'" (arXiv 1109.5114), cited PAPER.md:<line>.
+ *
+ *   out(p) = sum_q f(q) beta^{(r)}_{a(p)}(p - q)
+ *
+ * computed the paper's way: one global pre-integration of the image (running
+ * sums along the four grid directions of the box spline, each repeated r
+ * times; Alg. 3 step 2 PAPER.md:395-399) followed
+ * by a per-pixel local finite difference (the (r+1)^4-tap mesh of Table 1,
+ * PAPER.md:355-373, shifts of Eq. (10)) whose taps are read
+ * from the running sum with the interpolation of Eq. (11).
+ * The per-pixel scales a(p) come from the pixel's covariance (sigma_x,
+ * sigma_y, theta) by the minimum-kurtosis rule on
+ * C(p)/r (Prop. 1); basis Theta, Theta' or the per-pixel
+ * dual choice of Algorithm 2.  DESIGN.md lists every
+ * reading taken where the paper is silent.
+ *
+ * Conventions
+ *  - Images are row-major, x fastest; the paper's (m, n) is (x, y).
+ *  - All buffers are owned by the caller (device buffers from PyTorch unless a
+ *    function says "host").  The library never frees caller memory.  The plan
+ *    owns its workspace and its interpolation tables.
+ *  - Every call that takes a stream is asynchronous on that stream
+ *    (cudaStream_t passed as void*; NULL = legacy default stream).  Argument
+ *    errors are returned synchronously; device-side conditions (margin
+ *    violation, infeasible covariance with clamp = 0) raise flags read by
+ *    bsf_get_stats(), which synchronises the stream.
+ *  - Thread safety: a plan may be used by one host thread at a time.
+ */
+#ifndef BSF_H
+#define BSF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bsf_plan_s *bsf_plan_t;
+
+typedef enum {
+    BSF_OK = 0,
+    BSF_EINVAL = 1,      /* bad argument or descriptor field                  */
+    BSF_ENOMEM = 2,      /* device or host allocation failed                  */
+    BSF_ECUDA = 3,       /* CUDA runtime error (see bsf_last_error())          */
+    BSF_EINFEASIBLE = 4, /* covariance outside the basis' elongation bound    */
+    BSF_ERANGE = 5,      /* kernel reach exceeds the plan margins             */
+    BSF_ENCCL = 6,       /* collective/transport error                        */
+    BSF_EUNSUPPORTED = 7 /* valid request not implemented by this build       */
+} bsf_status;
+
+typedef enum { BSF_U8 = 0, BSF_F32 = 1, BSF_F64 = 2, BSF_I64 = 3, BSF_DD = 4 } bsf_dtype;
+
+typedef enum {
+    BSF_THETA = 0,       /* {0, 45, 90, 135} deg, steps (1,0),(1,1),(0,1),(-1,1) */
+    BSF_THETA_PRIME = 1, /* {26.6, 63.4, 116.6, 153.4} deg, steps (2,1),(1,2),(-1,2),(-2,1) */
+    BSF_DUAL = 2         /* Algorithm 2: per-pixel choice of the basis with the larger bound */
+} bsf_basis;
+
+typedef enum {
+    BSF_PREC_FP64 = 0,   /* fp64 taps and weights: fast, ill-conditioned for large images */
+    BSF_PREC_DD = 1      /* double-double taps, weights and accumulation (default)                             */
+} bsf_precision;
+
+typedef struct {
+    int width, height;   /* image size W, H (pixels)                                          */
+    int batch;           /* number of covariance fields (independent images / frames)         */
+    int channels;        /* images per covariance field (e.g. 3 for RGB); image b*C+c uses    */
+                         /* covariance field b                                                */
+    bsf_dtype in_dtype;  /* BSF_U8 or BSF_F32                                                 */
+    bsf_dtype out_dtype; /* BSF_F64 or BSF_F32                                                */
+    int order;           /* r >= 1: each direction repeated r times (north star)              */
+    bsf_basis basis;
+    float max_sigma;     /* upper bound of sigma_x, sigma_y over the covariance field         */
+    int margin_x;        /* P: domain columns [-P, W+P); 0 = derive from max_sigma            */
+    int margin_y;        /* Pb: domain rows [0, H+Pb); 0 = derive from max_sigma              */
+    int clamp;           /* 1: rho <- min(rho, 0.95 rho_B(phi)) at fixed trace/orientation    */
+                         /* 0: infeasible pixels give NaN and raise BSF_EINFEASIBLE            */
+    bsf_precision precision;
+    int device;          /* CUDA device ordinal                                               */
+} bsf_plan_desc;
+
+typedef struct {
+    int margin_x, margin_y;  /* P, Pb actually used                                          */
+    int g_width, g_height;   /* W + 2P, H + Pb                                                */
+    int nbases;              /* running-sum sets per image: 2 for BSF_DUAL, else 1             */
+    size_t g_bytes;          /* bytes of the pre-integrated buffer bsf_preintegrate writes    */
+    size_t g_exact_bytes;    /* bytes of the bit-exact int64 buffer (u8 input only, else 0)   */
+} bsf_geometry;
+
+typedef struct {
+    long long pixels;        /* pixels filtered since the last reset                          */
+    long long clamped;       /* pixels whose elongation was clamped                           */
+    long long zero_scale;    /* pixels with one scale treated as exactly zero (R5)  */
+    long long theta_prime;   /* pixels filtered with basis Theta'                             */
+    long long flags;         /* bit0 margin violation, bit1 infeasible, bit2 two zero scales  */
+} bsf_stats;
+
+/* Create a plan: validates the descriptor, derives the margins, loads the
+ * interpolation tables for (basis, order) from `lut_dir` (directory holding
+ * bsf_lut_b{basis}_r{order}.bin) and allocates the workspace.  No device work
+ * is launched.  Errors: BSF_EINVAL (descriptor), BSF_ERANGE (explicit margins
+ * smaller than the reach bound), BSF_ENOMEM, BSF_ECUDA, BSF_EUNSUPPORTED
+ * (order without tables).                                                    */
+bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut_dir, bsf_plan_t *out);
+bsf_status bsf_plan_destroy(bsf_plan_t plan);
+bsf_status bsf_plan_geometry(bsf_plan_t plan, bsf_geometry *geom);
+
+/* Pre-integration (the "running sum"): for every image of
+ * the batch and every basis in use, the 4r nested running sums
+ *   g <- g(q) + g(q - s_k)   (integer steps, no sqrt5 factor: DESIGN.md R3)
+ * on the domain x in [-P, W+P), y in [0, H+Pb) with zero state outside it.
+ *   f_dev: [batch*channels][H][W] of in_dtype.
+ *   g_dev: geometry.g_bytes; layout [nbases][batch*channels][H+Pb][W+2P] of
+ *          double-double (double2 {hi, lo}); opaque to callers except through
+ *          bsf_filter.  Exact for u8 input while the sums are below 2^106.   */
+bsf_status bsf_preintegrate(bsf_plan_t plan, const void *f_dev, void *g_dev, void *stream);
+
+/* Bit-exact integer pre-integration of a u8 image (the contract checked
+ * against the oracle): same sums, int64 arithmetic wrapping modulo 2^64.
+ *   g_dev: geometry.g_exact_bytes; layout [nbases][batch*channels][H+Pb][W+2P]
+ *          of int64, element (y, x) at [y][x + P].  Level order: Theta
+ *          (1,0),(1,1),(0,1),(-1,1); Theta' (1,2),(2,1),(-1,2),(-2,1)
+ *          (Alg. 3 (a)-(d)); repeated r times.  BSF_EINVAL for f32 input.   */
+bsf_status bsf_preintegrate_exact(bsf_plan_t plan, const void *f_dev, void *g_dev, void *stream);
+
+/* Local finite difference for every pixel (Alg. 3 step 3, PAPER.md:400-403,
+ * generalised to order r and to Algorithm 2's basis choice).
+ *   g_dev:   output of bsf_preintegrate.
+ *   cov_dev: [batch][3][H][W] float32 planes (sigma_x, sigma_y, theta); theta
+ *            is the angle of the sigma_x axis from the x axis, in radians.
+ *   out_dev: [batch*channels][H][W] of out_dtype.                            */
+bsf_status bsf_filter(bsf_plan_t plan, const void *g_dev, const void *cov_dev, void *out_dev, void *stream);
+
+/* Same computation for an explicit pixel list (parity at full size):
+ *   pts_dev: int32 triples (image, x, y) * npts;  out_dev: float64[npts].    */
+bsf_status bsf_filter_points(bsf_plan_t plan, const void *g_dev, const void *cov_dev, const int *pts_dev,
+                             int npts, double *out_dev, void *stream);
+
+/* bsf_preintegrate + bsf_filter with the plan's own g workspace.            */
+bsf_status bsf_run(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, void *stream);
+
+/* End to end from HOST buffers (pinned for overlap): copies f and cov to the
+ * device, runs bsf_run, copies out back, all on `stream`.  Returns after
+ * enqueueing; synchronise the stream before reading out_host.               */
+bsf_status bsf_run_host(bsf_plan_t plan, const void *f_host, const void *cov_host, void *out_host, void *stream);
+
+/* Statistics since the last reset (synchronises the plan's last stream). */
+bsf_status bsf_get_stats(bsf_plan_t plan, bsf_stats *stats, int reset);
+
+/* Number of library kernels launched through this plan since creation. */
+long long bsf_launch_count(bsf_plan_t plan);
+
+const char *bsf_status_str(bsf_status s);
+const char *bsf_last_error(void);
+int bsf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSF_H */

@@ -1,0 +1,219 @@
+"""Thin Python binding of the C-ABI library ``libbsf.so`` (include/bsf.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  PyTorch provides device memory and streams.  There is no CPU
+fallback: if the extension is missing, ``lib()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbsf.so")
+LUT_DIR = os.path.join(HERE, "lut")
+
+BSF_U8, BSF_F32, BSF_F64, BSF_I64, BSF_DD = 0, 1, 2, 3, 4
+BSF_THETA, BSF_THETA_PRIME, BSF_DUAL = 0, 1, 2
+BSF_PREC_FP64, BSF_PREC_DD = 0, 1
+
+STATUS = {0: "ok", 1: "invalid argument", 2: "out of memory", 3: "CUDA error", 4: "infeasible covariance",
+          5: "kernel reach exceeds plan margins", 6: "communication error", 7: "unsupported"}
+
+
+class BsfError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("%s (%d): %s" % (STATUS.get(status, "?"), status, msg))
+        self.status = status
+
+
+class bsf_plan_desc(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int), ("height", ctypes.c_int), ("batch", ctypes.c_int),
+                ("channels", ctypes.c_int), ("in_dtype", ctypes.c_int), ("out_dtype", ctypes.c_int),
+                ("order", ctypes.c_int), ("basis", ctypes.c_int), ("max_sigma", ctypes.c_float),
+                ("margin_x", ctypes.c_int), ("margin_y", ctypes.c_int), ("clamp", ctypes.c_int),
+                ("precision", ctypes.c_int), ("device", ctypes.c_int)]
+
+
+class bsf_geometry(ctypes.Structure):
+    _fields_ = [("margin_x", ctypes.c_int), ("margin_y", ctypes.c_int), ("g_width", ctypes.c_int),
+                ("g_height", ctypes.c_int), ("nbases", ctypes.c_int), ("g_bytes", ctypes.c_size_t),
+                ("g_exact_bytes", ctypes.c_size_t)]
+
+
+class bsf_stats(ctypes.Structure):
+    _fields_ = [("pixels", ctypes.c_longlong), ("clamped", ctypes.c_longlong), ("zero_scale", ctypes.c_longlong),
+                ("theta_prime", ctypes.c_longlong), ("flags", ctypes.c_longlong)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libbsf.so (built in-tree by build.py / __graft_entry__.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError("libbsf.so not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i, st = ctypes.c_void_p, ctypes.c_int, ctypes.c_int
+        L.bsf_plan_create.restype = st
+        L.bsf_plan_create.argtypes = [ctypes.POINTER(bsf_plan_desc), ctypes.c_char_p, ctypes.POINTER(vp)]
+        L.bsf_plan_destroy.restype = st
+        L.bsf_plan_destroy.argtypes = [vp]
+        L.bsf_plan_geometry.restype = st
+        L.bsf_plan_geometry.argtypes = [vp, ctypes.POINTER(bsf_geometry)]
+        for name in ("bsf_preintegrate", "bsf_preintegrate_exact"):
+            getattr(L, name).restype = st
+            getattr(L, name).argtypes = [vp, vp, vp, vp]
+        L.bsf_filter.restype = st
+        L.bsf_filter.argtypes = [vp, vp, vp, vp, vp]
+        L.bsf_filter_points.restype = st
+        L.bsf_filter_points.argtypes = [vp, vp, vp, vp, i, vp, vp]
+        L.bsf_run.restype = st
+        L.bsf_run.argtypes = [vp, vp, vp, vp, vp]
+        L.bsf_run_host.restype = st
+        L.bsf_run_host.argtypes = [vp, vp, vp, vp, vp]
+        L.bsf_get_stats.restype = st
+        L.bsf_get_stats.argtypes = [vp, ctypes.POINTER(bsf_stats), i]
+        L.bsf_launch_count.restype = ctypes.c_longlong
+        L.bsf_launch_count.argtypes = [vp]
+        L.bsf_status_str.restype = ctypes.c_char_p
+        L.bsf_status_str.argtypes = [st]
+        L.bsf_last_error.restype = ctypes.c_char_p
+        L.bsf_last_error.argtypes = []
+        L.bsf_version.restype = i
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise BsfError(status, lib().bsf_last_error().decode())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return ctypes.c_void_p(t)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Plan:
+    """A bsf_plan_t.  Methods mirror the C functions of include/bsf.h."""
+
+    def __init__(self, width, height, *, batch=1, channels=1, in_dtype=BSF_F32, out_dtype=BSF_F64, order=1,
+                 basis=BSF_DUAL, max_sigma=1.0, margin_x=0, margin_y=0, clamp=1, precision=BSF_PREC_DD,
+                 device=0, lut_dir=LUT_DIR):
+        self.desc = bsf_plan_desc(width, height, batch, channels, in_dtype, out_dtype, order, basis,
+                                  float(max_sigma), margin_x, margin_y, clamp, precision, device)
+        h = ctypes.c_void_p()
+        _check(lib().bsf_plan_create(ctypes.byref(self.desc), lut_dir.encode(), ctypes.byref(h)))
+        self.handle = h
+        g = bsf_geometry()
+        _check(lib().bsf_plan_geometry(self.handle, ctypes.byref(g)))
+        self.geometry = g
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().bsf_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --- allocation helpers (PyTorch owns device memory) ---------------------
+    def empty_g(self):
+        import torch
+        return torch.empty(self.geometry.g_bytes // 8, dtype=torch.float64, device="cuda:%d" % self.desc.device)
+
+    def empty_g_exact(self):
+        import torch
+        n = self.geometry.g_exact_bytes // 8
+        g = self.geometry
+        return torch.empty(n, dtype=torch.int64, device="cuda:%d" % self.desc.device).view(
+            g.nbases, self.desc.batch * self.desc.channels, g.g_height, g.g_width)
+
+    # --- C-ABI calls ------------------------------------------------------------
+    def preintegrate(self, f, g, stream=None):
+        _check(lib().bsf_preintegrate(self.handle, _ptr(f), _ptr(g), _stream(stream)))
+
+    def preintegrate_exact(self, f, g, stream=None):
+        _check(lib().bsf_preintegrate_exact(self.handle, _ptr(f), _ptr(g), _stream(stream)))
+
+    def filter(self, g, cov, out, stream=None):
+        _check(lib().bsf_filter(self.handle, _ptr(g), _ptr(cov), _ptr(out), _stream(stream)))
+
+    def filter_points(self, g, cov, pts, out, stream=None):
+        n = pts.numel() // 3
+        _check(lib().bsf_filter_points(self.handle, _ptr(g), _ptr(cov), _ptr(pts), n, _ptr(out), _stream(stream)))
+
+    def run(self, f, cov, out, stream=None):
+        _check(lib().bsf_run(self.handle, _ptr(f), _ptr(cov), _ptr(out), _stream(stream)))
+
+    def run_host(self, f_host, cov_host, out_host, stream=None):
+        _check(lib().bsf_run_host(self.handle, _ptr(f_host), _ptr(cov_host), _ptr(out_host), _stream(stream)))
+
+    def stats(self, reset=False):
+        s = bsf_stats()
+        st = lib().bsf_get_stats(self.handle, ctypes.byref(s), 1 if reset else 0)
+        d = {k: getattr(s, k) for k, _ in bsf_stats._fields_}
+        d["status"] = st
+        return d
+
+    def launch_count(self):
+        return lib().bsf_launch_count(self.handle)
+
+
+# C-ABI names, re-exported (the binding keeps the library's vocabulary)
+def bsf_plan_create(**kw):
+    return Plan(**kw)
+
+
+def bsf_preintegrate(plan, f, g, stream=None):
+    plan.preintegrate(f, g, stream)
+
+
+def bsf_preintegrate_exact(plan, f, g, stream=None):
+    plan.preintegrate_exact(f, g, stream)
+
+
+def bsf_filter(plan, g, cov, out, stream=None):
+    plan.filter(g, cov, out, stream)
+
+
+def bsf_filter_points(plan, g, cov, pts, out, stream=None):
+    plan.filter_points(g, cov, pts, out, stream)
+
+
+def bsf_run(plan, f, cov, out, stream=None):
+    plan.run(f, cov, out, stream)
+
+
+def bsf_run_host(plan, f_host, cov_host, out_host, stream=None):
+    plan.run_host(f_host, cov_host, out_host, stream)
+
+
+def bsf_get_stats(plan, reset=False):
+    return plan.stats(reset)
+
+
+def exported_symbols():
+    """Function names declared in include/bsf.h."""
+    import re
+    hdr = os.path.join(os.path.dirname(HERE), "include", "bsf.h")
+    src = open(hdr).read()
+    return sorted(set(re.findall(r"\b(bsf_[a-z_]+)\s*\(", src)))

@@ -1,0 +1,377 @@
+// C-ABI of the library (include/bsf.h): plans, table loading, dispatch.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "bsf_internal.h"
+
+using namespace bsf;
+
+static thread_local std::string g_last_error;
+
+static bsf_status set_err(bsf_status s, const std::string &msg) {
+    g_last_error = msg;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return set_err(BSF_ECUDA, std::string(#expr ": ") + cudaGetErrorString(e_));      \
+    } while (0)
+
+struct bsf_plan_s {
+    bsf_plan_desc d;
+    Geometry geo;
+    int bases[2];           // basis of each running-sum slot
+    std::vector<void *> dev_allocs;
+    LutBasis *luts_dev = nullptr;  // [2], indexed by basis id
+    void *scan_ws = nullptr;
+    size_t scan_ws_bytes = 0;
+    double2 *g_ws = nullptr;       // for bsf_run
+    void *f_stage = nullptr, *cov_stage = nullptr, *out_stage = nullptr;
+    unsigned long long *stats = nullptr;
+    long long nlaunch = 0;
+    cudaStream_t last = nullptr;
+};
+
+static size_t g_bytes(const bsf_plan_s *p) {
+    return (size_t)p->geo.nbases * p->geo.nimg * p->geo.GH * p->geo.GW * sizeof(double2);
+}
+
+static int required_disp(float max_sigma, int order) {
+    // |tap - p| <= (r/2) sum_k a_k <= sigma_max sqrt(24 r)
+    return (int)ceil((double)max_sigma * sqrt(24.0 * order)) + 1;
+}
+
+// ---------------------------------------------------------------------------
+// interpolation tables
+// ---------------------------------------------------------------------------
+static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *out) {
+    char path[4096];
+    snprintf(path, sizeof path, "%s/bsf_lut_b%d_r%d.bin", dir ? dir : ".", basis, p->d.order);
+    FILE *fh = fopen(path, "rb");
+    if (!fh) return set_err(BSF_EUNSUPPORTED, std::string("missing interpolation table ") + path);
+    std::vector<char> buf;
+    fseek(fh, 0, SEEK_END);
+    long n = ftell(fh);
+    fseek(fh, 0, SEEK_SET);
+    buf.resize(n);
+    size_t got = fread(buf.data(), 1, n, fh);
+    fclose(fh);
+    if ((long)got != n) return set_err(BSF_EINVAL, "short read " + std::string(path));
+    size_t off = 0;
+    auto take = [&](void *dst, size_t sz) -> bool {
+        if (off + sz > buf.size()) return false;
+        memcpy(dst, buf.data() + off, sz);
+        off += sz;
+        return true;
+    };
+    uint32_t hdr[5], nreg;
+    if (!take(hdr, sizeof hdr) || hdr[0] != 0x4C465342u || (int)hdr[2] != basis || (int)hdr[3] != p->d.order ||
+        hdr[4] != NVAR || !take(&nreg, 4) || nreg > MAX_REG)
+        return set_err(BSF_EINVAL, "bad table header " + std::string(path));
+    memset(out, 0, sizeof *out);
+    out->nreg = nreg;
+    for (int k = 0; k < 4; ++k) {
+        int nv[2];
+        take(nv, 8);
+        out->normal[k] = make_int2(nv[0], nv[1]);
+    }
+    std::vector<int> keys(4 * nreg);
+    for (uint32_t r = 0; r < nreg; ++r) {
+        take(&keys[4 * r], 16);
+        double c[2];
+        take(c, 16);
+        out->centre[r] = make_double2(c[0], c[1]);
+    }
+    int kmax[4];
+    for (int k = 0; k < 4; ++k) {
+        out->kmin[k] = 1 << 30;
+        kmax[k] = -(1 << 30);
+        for (uint32_t r = 0; r < nreg; ++r) {
+            out->kmin[k] = keys[4 * r + k] < out->kmin[k] ? keys[4 * r + k] : out->kmin[k];
+            kmax[k] = keys[4 * r + k] > kmax[k] ? keys[4 * r + k] : kmax[k];
+        }
+        out->radix[k] = kmax[k] - out->kmin[k] + 1;
+    }
+    if (out->radix[0] * out->radix[1] * out->radix[2] * out->radix[3] > 81)
+        return set_err(BSF_EINVAL, "region key space too large");
+    memset(out->table, -1, sizeof out->table);
+    for (uint32_t r = 0; r < nreg; ++r) {
+        int idx = 0, mul = 1;
+        for (int k = 0; k < 4; ++k) {
+            idx += (keys[4 * r + k] - out->kmin[k]) * mul;
+            mul *= out->radix[k];
+        }
+        out->table[idx] = (signed char)r;
+    }
+    for (int v = 0; v < NVAR; ++v) {
+        int hv[4];
+        if (!take(hv, 16)) return set_err(BSF_EINVAL, "truncated table");
+        LutVar &V = out->var[v];
+        V.deg = hv[1];
+        V.nmon = hv[2];
+        V.nmax = hv[3];
+        std::vector<int> counts(nreg);
+        std::vector<int2> offs((size_t)nreg * V.nmax);
+        std::vector<double2> coef((size_t)nreg * V.nmax * V.nmon);
+        for (uint32_t r = 0; r < nreg; ++r) {
+            take(&counts[r], 4);
+            for (int s = 0; s < V.nmax; ++s) {
+                int o[2];
+                take(o, 8);
+                offs[(size_t)r * V.nmax + s] = make_int2(o[0], o[1]);
+                if (!take(&coef[((size_t)r * V.nmax + s) * V.nmon], 16 * (size_t)V.nmon))
+                    return set_err(BSF_EINVAL, "truncated table");
+            }
+        }
+        void *d_counts, *d_offs, *d_coef;
+        CUDA_TRY(cudaMalloc(&d_counts, counts.size() * sizeof(int)));
+        p->dev_allocs.push_back(d_counts);
+        CUDA_TRY(cudaMalloc(&d_offs, offs.size() * sizeof(int2)));
+        p->dev_allocs.push_back(d_offs);
+        CUDA_TRY(cudaMalloc(&d_coef, coef.size() * sizeof(double2)));
+        p->dev_allocs.push_back(d_coef);
+        CUDA_TRY(cudaMemcpy(d_counts, counts.data(), counts.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(d_offs, offs.data(), offs.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(d_coef, coef.data(), coef.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        V.counts = (const int *)d_counts;
+        V.offs = (const int2 *)d_offs;
+        V.coef = (const double2 *)d_coef;
+    }
+    return BSF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut_dir, bsf_plan_t *out) {
+    if (!desc || !out) return set_err(BSF_EINVAL, "null argument");
+    *out = nullptr;
+    const bsf_plan_desc &d = *desc;
+    if (d.width < 1 || d.height < 1 || d.batch < 1 || d.channels < 1)
+        return set_err(BSF_EINVAL, "image size, batch and channels must be >= 1");
+    if (d.in_dtype != BSF_U8 && d.in_dtype != BSF_F32) return set_err(BSF_EINVAL, "in_dtype must be U8 or F32");
+    if (d.out_dtype != BSF_F64 && d.out_dtype != BSF_F32) return set_err(BSF_EINVAL, "out_dtype must be F64 or F32");
+    if (d.order < 1 || d.order > 4) return set_err(BSF_EINVAL, "order must be 1..4");
+    if (d.basis < BSF_THETA || d.basis > BSF_DUAL) return set_err(BSF_EINVAL, "bad basis");
+    if (!(d.max_sigma > 0) || !isfinite(d.max_sigma)) return set_err(BSF_EINVAL, "max_sigma must be > 0");
+    if (d.precision != BSF_PREC_FP64 && d.precision != BSF_PREC_DD) return set_err(BSF_EINVAL, "bad precision");
+    if (d.margin_x < 0 || d.margin_y < 0) return set_err(BSF_EINVAL, "negative margin");
+    int disp = required_disp(d.max_sigma, d.order);
+    int needP = disp + 3 * d.order + 2, needPb = disp + 2;
+    if ((d.margin_x && d.margin_x < needP) || (d.margin_y && d.margin_y < needPb))
+        return set_err(BSF_ERANGE, "margins smaller than the kernel reach (need P >= " + std::to_string(needP) +
+                                       ", Pb >= " + std::to_string(needPb) + ")");
+    CUDA_TRY(cudaSetDevice(d.device));
+    bsf_plan_s *p = new bsf_plan_s();
+    p->d = d;
+    Geometry &g = p->geo;
+    g.W = d.width;
+    g.H = d.height;
+    g.P = d.margin_x ? d.margin_x : needP;
+    g.Pb = d.margin_y ? d.margin_y : needPb;
+    g.GW = g.W + 2 * g.P;
+    g.GH = g.H + g.Pb;
+    g.nimg = d.batch * d.channels;
+    g.nbases = d.basis == BSF_DUAL ? 2 : 1;
+    p->bases[0] = d.basis == BSF_DUAL ? BSF_THETA : d.basis;
+    p->bases[1] = BSF_THETA_PRIME;
+    LutBasis host[2];
+    memset(host, 0, sizeof host);
+    for (int b = 0; b < 2; ++b) {
+        bool used = d.basis == BSF_DUAL || d.basis == b;
+        if (!used) continue;
+        bsf_status s = load_lut(p, lut_dir, b, &host[b]);
+        if (s != BSF_OK) {
+            bsf_plan_destroy(p);
+            return s;
+        }
+    }
+    auto dmalloc = [&](void **ptr, size_t n) -> cudaError_t {
+        cudaError_t e = cudaMalloc(ptr, n);
+        if (e == cudaSuccess) p->dev_allocs.push_back(*ptr);
+        return e;
+    };
+    if (dmalloc((void **)&p->luts_dev, sizeof host) != cudaSuccess ||
+        cudaMemcpy(p->luts_dev, host, sizeof host, cudaMemcpyHostToDevice) != cudaSuccess) {
+        bsf_plan_destroy(p);
+        return set_err(BSF_ENOMEM, "table upload failed");
+    }
+    p->scan_ws_bytes = scan_workspace_bytes(g);
+    if (dmalloc(&p->scan_ws, p->scan_ws_bytes) != cudaSuccess ||
+        dmalloc((void **)&p->stats, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+        bsf_plan_destroy(p);
+        return set_err(BSF_ENOMEM, "workspace allocation failed");
+    }
+    cudaMemset(p->stats, 0, 8 * sizeof(unsigned long long));
+    *out = p;
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_plan_destroy(bsf_plan_t p) {
+    if (!p) return BSF_OK;
+    for (void *q : p->dev_allocs) cudaFree(q);
+    delete p;
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_plan_geometry(bsf_plan_t p, bsf_geometry *geom) {
+    if (!p || !geom) return set_err(BSF_EINVAL, "null argument");
+    geom->margin_x = p->geo.P;
+    geom->margin_y = p->geo.Pb;
+    geom->g_width = p->geo.GW;
+    geom->g_height = p->geo.GH;
+    geom->nbases = p->geo.nbases;
+    geom->g_bytes = g_bytes(p);
+    geom->g_exact_bytes = p->d.in_dtype == BSF_U8 ? g_bytes(p) / 2 : 0;
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, void *stream) {
+    if (!p || !f || !g) return set_err(BSF_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last = st;
+    double2 *gd = (double2 *)g;
+    CUDA_TRY(launch_fill_dd(f, p->d.in_dtype == BSF_U8, gd, p->geo, p->geo.nbases, st, &p->nlaunch));
+    size_t slot = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW;
+    for (int s = 0; s < p->geo.nbases; ++s)
+        CUDA_TRY(launch_scan_dd(gd + s * slot, p->geo, p->bases[s], p->d.order, p->scan_ws, p->scan_ws_bytes, st,
+                                &p->nlaunch));
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_preintegrate_exact(bsf_plan_t p, const void *f, void *g, void *stream) {
+    if (!p || !f || !g) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.in_dtype != BSF_U8) return set_err(BSF_EINVAL, "exact pre-integration needs u8 input");
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last = st;
+    unsigned long long *gd = (unsigned long long *)g;
+    CUDA_TRY(launch_fill_i64((const uint8_t *)f, gd, p->geo, p->geo.nbases, st, &p->nlaunch));
+    size_t slot = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW;
+    for (int s = 0; s < p->geo.nbases; ++s)
+        CUDA_TRY(launch_scan_i64(gd + s * slot, p->geo, p->bases[s], p->d.order, p->scan_ws, p->scan_ws_bytes, st,
+                                 &p->nlaunch));
+    return BSF_OK;
+}
+
+static GatherArgs gather_args(bsf_plan_s *p, const void *g, const void *cov, void *out) {
+    GatherArgs a;
+    memset(&a, 0, sizeof a);
+    a.geo = p->geo;
+    a.policy = p->d.basis;
+    a.clamp = p->d.clamp;
+    a.channels = p->d.channels;
+    a.out_f32 = p->d.out_dtype == BSF_F32;
+    a.g = (const double2 *)g;
+    a.cov = (const float *)cov;
+    a.out = out;
+    a.stats = p->stats;
+    return a;
+}
+
+extern "C" bsf_status bsf_filter(bsf_plan_t p, const void *g, const void *cov, void *out, void *stream) {
+    if (!p || !g || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last = st;
+    GatherArgs a = gather_args(p, g, cov, out);
+    CUDA_TRY(launch_gather_impl(a, p->d.order, p->d.precision, st, p->luts_dev, &p->nlaunch));
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_filter_points(bsf_plan_t p, const void *g, const void *cov, const int *pts, int npts,
+                                        double *out, void *stream) {
+    if (!p || !g || !cov || !out || (!pts && npts)) return set_err(BSF_EINVAL, "null argument");
+    if (npts < 0) return set_err(BSF_EINVAL, "npts < 0");
+    if (npts == 0) return BSF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last = st;
+    GatherArgs a = gather_args(p, g, cov, out);
+    a.out_f32 = 0;
+    a.pts = pts;
+    a.npts = npts;
+    CUDA_TRY(launch_gather_impl(a, p->d.order, p->d.precision, st, p->luts_dev, &p->nlaunch));
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void *out, void *stream) {
+    if (!p) return set_err(BSF_EINVAL, "null plan");
+    if (!p->g_ws) {
+        void *q;
+        if (cudaMalloc(&q, g_bytes(p)) != cudaSuccess) return set_err(BSF_ENOMEM, "g workspace");
+        p->dev_allocs.push_back(q);
+        p->g_ws = (double2 *)q;
+    }
+    bsf_status s = bsf_preintegrate(p, f, p->g_ws, stream);
+    if (s != BSF_OK) return s;
+    return bsf_filter(p, p->g_ws, cov, out, stream);
+}
+
+extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void *cov_host, void *out_host,
+                                   void *stream) {
+    if (!p || !f_host || !cov_host || !out_host) return set_err(BSF_EINVAL, "null argument");
+    const Geometry &g = p->geo;
+    size_t fb = (size_t)g.nimg * g.H * g.W * (p->d.in_dtype == BSF_U8 ? 1 : 4);
+    size_t cb = (size_t)p->d.batch * 3 * g.H * g.W * 4;
+    size_t ob = (size_t)g.nimg * g.H * g.W * (p->d.out_dtype == BSF_F32 ? 4 : 8);
+    if (!p->f_stage) {
+        void *a, *b, *c;
+        if (cudaMalloc(&a, fb) != cudaSuccess || cudaMalloc(&b, cb) != cudaSuccess || cudaMalloc(&c, ob) != cudaSuccess)
+            return set_err(BSF_ENOMEM, "staging buffers");
+        p->dev_allocs.push_back(a);
+        p->dev_allocs.push_back(b);
+        p->dev_allocs.push_back(c);
+        p->f_stage = a;
+        p->cov_stage = b;
+        p->out_stage = c;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemcpyAsync(p->f_stage, f_host, fb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(p->cov_stage, cov_host, cb, cudaMemcpyHostToDevice, st));
+    bsf_status s = bsf_run(p, p->f_stage, p->cov_stage, p->out_stage, stream);
+    if (s != BSF_OK) return s;
+    CUDA_TRY(cudaMemcpyAsync(out_host, p->out_stage, ob, cudaMemcpyDeviceToHost, st));
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_get_stats(bsf_plan_t p, bsf_stats *s, int reset) {
+    if (!p || !s) return set_err(BSF_EINVAL, "null argument");
+    CUDA_TRY(cudaStreamSynchronize(p->last));
+    unsigned long long h[8];
+    CUDA_TRY(cudaMemcpy(h, p->stats, sizeof h, cudaMemcpyDeviceToHost));
+    s->pixels = (long long)h[0];
+    s->clamped = (long long)h[1];
+    s->zero_scale = (long long)h[2];
+    s->theta_prime = (long long)h[3];
+    s->flags = (long long)h[4];
+    if (reset) CUDA_TRY(cudaMemset(p->stats, 0, sizeof h));
+    if (s->flags & FLAG_RANGE_H) return set_err(BSF_ERANGE, "a tap window left the pre-integration domain");
+    if (s->flags & FLAG_INFEASIBLE_H) return set_err(BSF_EINFEASIBLE, "covariance outside the elongation bound");
+    return BSF_OK;
+}
+
+extern "C" long long bsf_launch_count(bsf_plan_t p) { return p ? p->nlaunch : 0; }
+
+extern "C" const char *bsf_status_str(bsf_status s) {
+    switch (s) {
+        case BSF_OK: return "ok";
+        case BSF_EINVAL: return "invalid argument";
+        case BSF_ENOMEM: return "out of memory";
+        case BSF_ECUDA: return "CUDA error";
+        case BSF_EINFEASIBLE: return "infeasible covariance";
+        case BSF_ERANGE: return "kernel reach exceeds plan margins";
+        case BSF_ENCCL: return "communication error";
+        case BSF_EUNSUPPORTED: return "unsupported";
+    }
+    return "unknown status";
+}
+
+extern "C" const char *bsf_last_error(void) { return g_last_error.c_str(); }
+extern "C" int bsf_version(void) { return 100; }

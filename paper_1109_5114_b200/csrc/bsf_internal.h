@@ -1,0 +1,66 @@
+// Internal declarations shared by bsf_api.cu and bsf_kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bsf.h"
+
+namespace bsf {
+
+constexpr int MAX_REG = 32;
+// device-side condition flags (also in bsf_pixel.cuh)
+enum { FLAG_RANGE_H = 1, FLAG_INFEASIBLE_H = 2, FLAG_TWO_ZERO_H = 4, FLAG_SOLVER_H = 8 };
+constexpr int NVAR = 5;  // full kernel + one per dropped direction
+
+// One interpolation table (basis, order, variant) in device memory.
+struct LutVar {
+    int deg, nmon, nmax;
+    const int2 *offs;      // [nreg][nmax]
+    const int *counts;     // [nreg]
+    const double2 *coef;   // [nreg][nmax][nmon] double-double
+};
+
+struct LutBasis {
+    int nreg;
+    int2 normal[4];        // knot-line normals n_k = perp(s_k)
+    int kmin[4];           // min floor(n_k . phi) over the unit cell
+    int radix[4];
+    signed char table[81]; // mixed-radix key -> region (or -1)
+    double2 centre[MAX_REG];
+    LutVar var[NVAR];
+};
+
+struct Geometry {
+    int W, H, P, Pb, GW, GH;
+    int nimg;     // batch * channels
+    int nbases;
+};
+
+struct GatherArgs {
+    Geometry geo;
+    int policy;   // BSF_THETA / BSF_THETA_PRIME / BSF_DUAL
+    int clamp;
+    int channels;
+    int out_f32;
+    const double2 *g;       // [nbases][nimg][GH][GW]
+    const float *cov;       // [batch][3][H][W]
+    void *out;              // [nimg][H][W]
+    const int *pts;         // optional (img, x, y) triples
+    int npts;
+    unsigned long long *stats;  // [5]: pixels, clamped, zero, theta', flags(or)
+};
+
+// launchers (bsf_kernels.cu)
+cudaError_t launch_fill_dd(const void *f, int u8, double2 *g, const Geometry &geo, int nbasis_copy,
+                           cudaStream_t st, long long *nlaunch);
+cudaError_t launch_fill_i64(const uint8_t *f, unsigned long long *g, const Geometry &geo, int nbasis_copy,
+                            cudaStream_t st, long long *nlaunch);
+cudaError_t launch_scan_dd(double2 *g, const Geometry &geo, int basis, int order, void *ws, size_t ws_bytes,
+                           cudaStream_t st, long long *nlaunch);
+cudaError_t launch_scan_i64(unsigned long long *g, const Geometry &geo, int basis, int order, void *ws,
+                            size_t ws_bytes, cudaStream_t st, long long *nlaunch);
+size_t scan_workspace_bytes(const Geometry &geo);
+cudaError_t launch_gather_impl(const GatherArgs &a, int order, int precision, cudaStream_t st,
+                               const LutBasis *luts_dev, long long *nlaunch);
+
+}  // namespace bsf
