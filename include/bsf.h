@@ -141,6 +141,13 @@ bsf_status bsf_filter(bsf_plan_t plan, const void *g_dev, const void *cov_dev, v
 bsf_status bsf_filter_points(bsf_plan_t plan, const void *g_dev, const void *cov_dev, const int *pts_dev,
                              int npts, double *out_dev, void *stream);
 
+/* As bsf_filter_points, also writing per-point diagnostics (for decision
+ * parity with the oracle): aux_dev float64[8 * npts] =
+ *   {basis, zero-scale direction (-1 none), clamped, flags, a'_1..a'_4}
+ * with a'_k = a_k / |s_k| the scale in lattice steps.                        */
+bsf_status bsf_filter_points_aux(bsf_plan_t plan, const void *g_dev, const void *cov_dev, const int *pts_dev,
+                                 int npts, double *out_dev, double *aux_dev, void *stream);
+
 /* bsf_preintegrate + bsf_filter with the plan's own g workspace.            */
 bsf_status bsf_run(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, void *stream);
 

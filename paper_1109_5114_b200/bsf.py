@@ -70,6 +70,8 @@ def lib():
         L.bsf_filter.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_filter_points.restype = st
         L.bsf_filter_points.argtypes = [vp, vp, vp, vp, i, vp, vp]
+        L.bsf_filter_points_aux.restype = st
+        L.bsf_filter_points_aux.argtypes = [vp, vp, vp, vp, i, vp, vp, vp]
         L.bsf_run.restype = st
         L.bsf_run.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_run_host.restype = st
@@ -160,6 +162,11 @@ class Plan:
     def filter_points(self, g, cov, pts, out, stream=None):
         n = pts.numel() // 3
         _check(lib().bsf_filter_points(self.handle, _ptr(g), _ptr(cov), _ptr(pts), n, _ptr(out), _stream(stream)))
+
+    def filter_points_aux(self, g, cov, pts, out, aux, stream=None):
+        n = pts.numel() // 3
+        _check(lib().bsf_filter_points_aux(self.handle, _ptr(g), _ptr(cov), _ptr(pts), n, _ptr(out), _ptr(aux),
+                                           _stream(stream)))
 
     def run(self, f, cov, out, stream=None):
         _check(lib().bsf_run(self.handle, _ptr(f), _ptr(cov), _ptr(out), _stream(stream)))

@@ -288,6 +288,11 @@ extern "C" bsf_status bsf_filter(bsf_plan_t p, const void *g, const void *cov, v
 
 extern "C" bsf_status bsf_filter_points(bsf_plan_t p, const void *g, const void *cov, const int *pts, int npts,
                                         double *out, void *stream) {
+    return bsf_filter_points_aux(p, g, cov, pts, npts, out, nullptr, stream);
+}
+
+extern "C" bsf_status bsf_filter_points_aux(bsf_plan_t p, const void *g, const void *cov, const int *pts, int npts,
+                                            double *out, double *aux, void *stream) {
     if (!p || !g || !cov || !out || (!pts && npts)) return set_err(BSF_EINVAL, "null argument");
     if (npts < 0) return set_err(BSF_EINVAL, "npts < 0");
     if (npts == 0) return BSF_OK;
@@ -297,6 +302,7 @@ extern "C" bsf_status bsf_filter_points(bsf_plan_t p, const void *g, const void 
     a.out_f32 = 0;
     a.pts = pts;
     a.npts = npts;
+    a.aux = aux;
     CUDA_TRY(launch_gather_impl(a, p->d.order, p->d.precision, st, p->luts_dev, &p->nlaunch));
     return BSF_OK;
 }

@@ -75,7 +75,10 @@ __device__ __forceinline__ double dd_to_d(dd a) { return __dadd_rn(a.hi, a.lo); 
 __device__ __forceinline__ double dd_floor(dd a, dd *frac) {
     double f = floor(a.hi);
     if (f == a.hi && a.lo < 0.0) f -= 1.0;
-    *frac = two_sum(__dadd_rn(a.hi, -f), a.lo);
+    // a.hi - f is not exact for a.hi in (-1, 0) (no Sterbenz), so keep its error
+    dd t = two_sum(a.hi, -f);
+    t.lo = __dadd_rn(t.lo, a.lo);
+    *frac = fast_two_sum(t.hi, t.lo);
     return f;
 }
 

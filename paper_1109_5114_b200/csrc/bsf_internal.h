@@ -47,6 +47,7 @@ struct GatherArgs {
     void *out;              // [nimg][H][W]
     const int *pts;         // optional (img, x, y) triples
     int npts;
+    double *aux;            // optional per-point diagnostics [8 * npts]
     unsigned long long *stats;  // [5]: pixels, clamped, zero, theta', flags(or)
 };
 

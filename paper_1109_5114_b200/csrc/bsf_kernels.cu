@@ -384,6 +384,9 @@ __device__ __forceinline__ typename Ar::V interp(const double2 *__restrict__ g, 
 }
 
 // out(p) = prod_k (1/a'_k)^R sum_j c_j F(p + sum_k (R/2 - j_k) a'_k s_k)
+#ifdef BSF_TAP_DUMP
+__device__ double *g_tap_dump;
+#endif
 template <int R, class Ar>
 __device__ double mesh(const double2 *__restrict__ g, const Geometry &geo, const LutBasis &L, const PixelScales &ps,
                        int x, int y, int *flags) {
@@ -411,6 +414,16 @@ __device__ double mesh(const double2 *__restrict__ g, const Geometry &geo, const
             Yy = dd_add(Yy, two_prod(m * c_steps[ps.basis][k][1], ps.ap[k]));
         }
         Val F = interp<R, Ar>(g, geo, L, V, Yx, Yy, ps.drop, sdrop, flags);
+#ifdef BSF_TAP_DUMP
+        if (g_tap_dump && x == 0 && y == 23) {
+            double *o = g_tap_dump + 8 * t;
+            dd fx, fy;
+            o[0] = dd_floor(Yx, &fx);
+            o[1] = dd_floor(Yy, &fy);
+            o[2] = fx.hi; o[3] = fx.lo; o[4] = fy.hi; o[5] = fy.lo;
+            if constexpr (sizeof(Val) == 16) { o[6] = F.hi; o[7] = F.lo; } else { o[6] = F; o[7] = 0; }
+        }
+#endif
         acc = Ar::add(acc, Ar::muli(F, coef));
     }
     double norm = 1.0;
@@ -461,6 +474,14 @@ __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a, const LutBasi
         const double2 *g = a.g + ((size_t)slot * geo.nimg + img) * geo.GH * geo.GW;
         res = mesh<R, Ar>(g, geo, luts[ps.basis], ps, x, y, &flags);
     }
+    if (a.aux) {
+        double *ax = a.aux + 8 * oidx;
+        ax[0] = ps.basis;
+        ax[1] = ps.drop;
+        ax[2] = ps.clamped;
+        ax[3] = flags;
+        for (int k = 0; k < 4; ++k) ax[4 + k] = ps.ap[k];
+    }
     if (a.out_f32)
         ((float *)a.out)[oidx] = (float)res;
     else
@@ -487,6 +508,9 @@ static void launch_r(const GatherArgs &a, int prec, cudaStream_t st, const LutBa
         gather_kernel<R, ArD><<<grid, block, 0, st>>>(a, luts);
 }
 
+#ifdef BSF_TAP_DUMP
+extern "C" void bsf_debug_set_dump(double *p) { cudaMemcpyToSymbol(g_tap_dump, &p, sizeof p); }
+#endif
 cudaError_t launch_gather_impl(const GatherArgs &a, int order, int prec, cudaStream_t st, const LutBasis *luts,
                                long long *nl) {
     switch (order) {
