@@ -167,6 +167,7 @@ def main():
     ap.add_argument("--order", type=int, default=0)
     ap.add_argument("--impl", default="bsf")
     ap.add_argument("--precision", default="dd", choices=["dd", "fp64"])
+    ap.add_argument("--anchor", default="global", choices=["global", "tile"])
     ap.add_argument("--ref-points", type=int, default=24)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,7 +200,8 @@ def main():
     prec = bsf.BSF_PREC_DD if args.precision == "dd" else bsf.BSF_PREC_FP64
     plan = bsf.Plan(w.width, w.height, batch=1, channels=1,
                     in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" else bsf.BSF_F32, out_dtype=bsf.BSF_F64,
-                    order=w.order, basis=w.basis, max_sigma=w.max_sigma, precision=prec, device=local)
+                    order=w.order, basis=w.basis, max_sigma=w.max_sigma, precision=prec, device=local,
+                    anchor=bsf.BSF_ANCHOR_TILE if args.anchor == "tile" else bsf.BSF_ANCHOR_GLOBAL)
     img = synth.make_image(w, frame=rank, device=dev).contiguous()
     cov = synth.make_cov(w, device=dev).contiguous()
     out = torch.empty((1, w.height, w.width), dtype=torch.float64, device=dev)
@@ -208,7 +210,12 @@ def main():
     stream = torch.cuda.current_stream()
     npx = w.width * w.height
 
+    tile = args.anchor == "tile"
+
     def one_step():
+        if tile:
+            plan.run(img, cov, out, stream)
+            return
         plan.preintegrate(img, g, stream)
         plan.filter(g, cov, out, stream)
 
@@ -229,9 +236,13 @@ def main():
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             starts[i].record(stream)
-            plan.preintegrate(img, g, stream)
-            mids[i].record(stream)
-            plan.filter(g, cov, out, stream)
+            if tile:
+                mids[i].record(stream)
+                plan.run(img, cov, out, stream)
+            else:
+                plan.preintegrate(img, g, stream)
+                mids[i].record(stream)
+                plan.filter(g, cov, out, stream)
             ends[i].record(stream)
             flush.zero_()
         torch.cuda.synchronize()
@@ -294,7 +305,7 @@ def main():
     in_b = 1 if w.in_dtype == "u8" else 4
     # algorithmic bytes of the pre-integration: read f once, write g (dd) once per basis
     pre_bytes = npx * in_b + nb * gh * gw * 16
-    roof = {"bound": "alu", "kernel": "gather_kernel", "achieved": achieved, "peak": fp64_peak,
+    roof = {"bound": "alu", "kernel": "tile_kernel (fused pre-integration + gather)" if tile else "gather_kernel", "achieved": achieved, "peak": fp64_peak,
             "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
             "peak_source": "148 SM x 64 DFMA/clk x 2 x %.0f MHz (sm_max, %s)" % (sm_mhz, src),
             "algorithmic_fma_per_px": fma_px, "gather_ms": gat,
@@ -311,6 +322,7 @@ def main():
             "config": {"workload": w.name, "width": w.width, "height": w.height, "order": w.order,
                        "basis": "dual" if w.basis == 2 else str(w.basis), "in_dtype": w.in_dtype,
                        "precision": "double-double" if prec == bsf.BSF_PREC_DD else "fp64",
+                       "anchor": args.anchor,
                        "l2": "flushed between steps (256 MB write, untimed)", "parallelism": "dp%d" % world},
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -66,6 +66,11 @@ typedef enum {
     BSF_PREC_DD = 1      /* double-double taps, weights and accumulation (default)                             */
 } bsf_precision;
 
+typedef enum {
+    BSF_ANCHOR_GLOBAL = 0, /* one pre-integration of the whole image (bsf_preintegrate + bsf_filter) */
+    BSF_ANCHOR_TILE = 1    /* fused: sums restarted per 16x16 output tile on its halo (R18) */
+} bsf_anchor;
+
 typedef struct {
     int width, height;   /* image size W, H (pixels)                                          */
     int batch;           /* number of covariance fields (independent images / frames)         */
@@ -82,6 +87,7 @@ typedef struct {
                          /* 0: infeasible pixels give NaN and raise BSF_EINFEASIBLE            */
     bsf_precision precision;
     int device;          /* CUDA device ordinal                                               */
+    bsf_anchor anchor;   /* how bsf_run anchors the running sums                              */
 } bsf_plan_desc;
 
 typedef struct {
@@ -148,7 +154,17 @@ bsf_status bsf_filter_points(bsf_plan_t plan, const void *g_dev, const void *cov
 bsf_status bsf_filter_points_aux(bsf_plan_t plan, const void *g_dev, const void *cov_dev, const int *pts_dev,
                                  int npts, double *out_dev, double *aux_dev, void *stream);
 
-/* bsf_preintegrate + bsf_filter with the plan's own g workspace.            */
+/* The tile-anchored fused path for an explicit pixel list (parity at full
+ * size): each point's 16x16 tile is pre-integrated on its halo and the point
+ * gathered; results are identical to those of bsf_run with BSF_ANCHOR_TILE.
+ *   f_dev, cov_dev as bsf_run; pts_dev int32 (image, x, y) * npts;
+ *   out_dev float64[npts]; aux_dev NULL or float64[8 * npts] (see _aux).    */
+bsf_status bsf_run_points(bsf_plan_t plan, const void *f_dev, const void *cov_dev, const int *pts_dev, int npts,
+                          double *out_dev, double *aux_dev, void *stream);
+
+/* The whole hot path: BSF_ANCHOR_GLOBAL = bsf_preintegrate + bsf_filter with
+ * the plan's own g workspace; BSF_ANCHOR_TILE = the fused tile kernel (no
+ * global g).                                                                 */
 bsf_status bsf_run(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, void *stream);
 
 /* End to end from HOST buffers (pinned for overlap): copies f and cov to the

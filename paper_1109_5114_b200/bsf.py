@@ -16,6 +16,7 @@ LUT_DIR = os.path.join(HERE, "lut")
 BSF_U8, BSF_F32, BSF_F64, BSF_I64, BSF_DD = 0, 1, 2, 3, 4
 BSF_THETA, BSF_THETA_PRIME, BSF_DUAL = 0, 1, 2
 BSF_PREC_FP64, BSF_PREC_DD = 0, 1
+BSF_ANCHOR_GLOBAL, BSF_ANCHOR_TILE = 0, 1
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "out of memory", 3: "CUDA error", 4: "infeasible covariance",
           5: "kernel reach exceeds plan margins", 6: "communication error", 7: "unsupported"}
@@ -32,7 +33,7 @@ class bsf_plan_desc(ctypes.Structure):
                 ("channels", ctypes.c_int), ("in_dtype", ctypes.c_int), ("out_dtype", ctypes.c_int),
                 ("order", ctypes.c_int), ("basis", ctypes.c_int), ("max_sigma", ctypes.c_float),
                 ("margin_x", ctypes.c_int), ("margin_y", ctypes.c_int), ("clamp", ctypes.c_int),
-                ("precision", ctypes.c_int), ("device", ctypes.c_int)]
+                ("precision", ctypes.c_int), ("device", ctypes.c_int), ("anchor", ctypes.c_int)]
 
 
 class bsf_geometry(ctypes.Structure):
@@ -72,6 +73,8 @@ def lib():
         L.bsf_filter_points.argtypes = [vp, vp, vp, vp, i, vp, vp]
         L.bsf_filter_points_aux.restype = st
         L.bsf_filter_points_aux.argtypes = [vp, vp, vp, vp, i, vp, vp, vp]
+        L.bsf_run_points.restype = st
+        L.bsf_run_points.argtypes = [vp, vp, vp, vp, i, vp, vp, vp]
         L.bsf_run.restype = st
         L.bsf_run.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_run_host.restype = st
@@ -116,9 +119,9 @@ class Plan:
 
     def __init__(self, width, height, *, batch=1, channels=1, in_dtype=BSF_F32, out_dtype=BSF_F64, order=1,
                  basis=BSF_DUAL, max_sigma=1.0, margin_x=0, margin_y=0, clamp=1, precision=BSF_PREC_DD,
-                 device=0, lut_dir=LUT_DIR):
+                 device=0, anchor=BSF_ANCHOR_GLOBAL, lut_dir=LUT_DIR):
         self.desc = bsf_plan_desc(width, height, batch, channels, in_dtype, out_dtype, order, basis,
-                                  float(max_sigma), margin_x, margin_y, clamp, precision, device)
+                                  float(max_sigma), margin_x, margin_y, clamp, precision, device, anchor)
         h = ctypes.c_void_p()
         _check(lib().bsf_plan_create(ctypes.byref(self.desc), lut_dir.encode(), ctypes.byref(h)))
         self.handle = h
@@ -168,6 +171,11 @@ class Plan:
         _check(lib().bsf_filter_points_aux(self.handle, _ptr(g), _ptr(cov), _ptr(pts), n, _ptr(out), _ptr(aux),
                                            _stream(stream)))
 
+    def run_points(self, f, cov, pts, out, aux=None, stream=None):
+        n = pts.numel() // 3
+        _check(lib().bsf_run_points(self.handle, _ptr(f), _ptr(cov), _ptr(pts), n, _ptr(out), _ptr(aux),
+                                    _stream(stream)))
+
     def run(self, f, cov, out, stream=None):
         _check(lib().bsf_run(self.handle, _ptr(f), _ptr(cov), _ptr(out), _stream(stream)))
 
@@ -204,6 +212,10 @@ def bsf_filter(plan, g, cov, out, stream=None):
 
 def bsf_filter_points(plan, g, cov, pts, out, stream=None):
     plan.filter_points(g, cov, pts, out, stream)
+
+
+def bsf_run_points(plan, f, cov, pts, out, aux=None, stream=None):
+    plan.run_points(f, cov, pts, out, aux, stream)
 
 
 def bsf_run(plan, f, cov, out, stream=None):

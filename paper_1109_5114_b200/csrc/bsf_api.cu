@@ -37,6 +37,11 @@ struct bsf_plan_s {
     double2 *g_ws = nullptr;       // for bsf_run
     void *f_stage = nullptr, *cov_stage = nullptr, *out_stage = nullptr;
     unsigned long long *stats = nullptr;
+    LutBasis host_luts[2];
+    double2 *tile_scratch = nullptr;
+    size_t tile_cap = 0;
+    int tile_nslots = 0;
+    int *tile_counter = nullptr;
     long long nlaunch = 0;
     cudaStream_t last = nullptr;
 };
@@ -79,6 +84,8 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         return set_err(BSF_EINVAL, "bad table header " + std::string(path));
     memset(out, 0, sizeof *out);
     out->nreg = nreg;
+    out->wxmin = out->wymin = 1 << 30;
+    out->wxmax = out->wymax = -(1 << 30);
     for (int k = 0; k < 4; ++k) {
         int nv[2];
         take(nv, 8);
@@ -90,6 +97,8 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         double c[2];
         take(c, 16);
         out->centre[r] = make_double2(c[0], c[1]);
+        if (c[0] != 0.0 || c[1] != 0.0)  // the gather evaluates at phi itself (R17)
+            return set_err(BSF_EINVAL, "table expanded around a non-zero centre (regenerate): " + std::string(path));
     }
     int kmax[4];
     for (int k = 0; k < 4; ++k) {
@@ -142,6 +151,14 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         CUDA_TRY(cudaMemcpy(d_counts, counts.data(), counts.size() * sizeof(int), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(d_offs, offs.data(), offs.size() * sizeof(int2), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(d_coef, coef.data(), coef.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        for (uint32_t r = 0; r < nreg; ++r)
+            for (int s2 = 0; s2 < counts[r]; ++s2) {
+                int2 o = offs[(size_t)r * V.nmax + s2];
+                out->wxmin = o.x < out->wxmin ? o.x : out->wxmin;
+                out->wxmax = o.x > out->wxmax ? o.x : out->wxmax;
+                out->wymin = o.y < out->wymin ? o.y : out->wymin;
+                out->wymax = o.y > out->wymax ? o.y : out->wymax;
+            }
         V.counts = (const int *)d_counts;
         V.offs = (const int2 *)d_offs;
         V.coef = (const double2 *)d_coef;
@@ -165,6 +182,7 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     if (!(d.max_sigma > 0) || !isfinite(d.max_sigma)) return set_err(BSF_EINVAL, "max_sigma must be > 0");
     if (d.precision != BSF_PREC_FP64 && d.precision != BSF_PREC_DD) return set_err(BSF_EINVAL, "bad precision");
     if (d.margin_x < 0 || d.margin_y < 0) return set_err(BSF_EINVAL, "negative margin");
+    if (d.anchor != BSF_ANCHOR_GLOBAL && d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EINVAL, "bad anchor");
     int disp = required_disp(d.max_sigma, d.order);
     int needP = disp + 3 * d.order + 2, needPb = disp + 2;
     if ((d.margin_x && d.margin_x < needP) || (d.margin_y && d.margin_y < needPb))
@@ -200,6 +218,7 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
         if (e == cudaSuccess) p->dev_allocs.push_back(*ptr);
         return e;
     };
+    memcpy(p->host_luts, host, sizeof host);
     if (dmalloc((void **)&p->luts_dev, sizeof host) != cudaSuccess ||
         cudaMemcpy(p->luts_dev, host, sizeof host, cudaMemcpyHostToDevice) != cudaSuccess) {
         bsf_plan_destroy(p);
@@ -307,8 +326,75 @@ extern "C" bsf_status bsf_filter_points_aux(bsf_plan_t p, const void *g, const v
     return BSF_OK;
 }
 
+static bsf_status ensure_tile_ws(bsf_plan_s *p) {
+    if (p->tile_scratch) return BSF_OK;
+    int mask = p->d.basis == BSF_DUAL ? 3 : (1 << p->d.basis);
+    p->tile_cap = tile_capacity(p->d.order, p->d.max_sigma, p->host_luts, mask);
+    p->tile_nslots = tile_slots();
+    void *q;
+    size_t bytes = (size_t)p->tile_nslots * 2 * p->tile_cap * sizeof(double2);
+    if (cudaMalloc(&q, bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "tile scratch " + std::to_string(bytes));
+    p->dev_allocs.push_back(q);
+    p->tile_scratch = (double2 *)q;
+    if (cudaMalloc(&q, sizeof(int)) != cudaSuccess) return set_err(BSF_ENOMEM, "tile counter");
+    p->dev_allocs.push_back(q);
+    p->tile_counter = (int *)q;
+    return BSF_OK;
+}
+
+static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *out) {
+    TileArgs a;
+    memset(&a, 0, sizeof a);
+    a.W = p->geo.W;
+    a.H = p->geo.H;
+    a.nimg = p->geo.nimg;
+    a.channels = p->d.channels;
+    a.policy = p->d.basis;
+    a.clamp = p->d.clamp;
+    a.out_f32 = p->d.out_dtype == BSF_F32;
+    a.in_u8 = p->d.in_dtype == BSF_U8;
+    a.f = f;
+    a.cov = (const float *)cov;
+    a.out = out;
+    a.scratch = p->tile_scratch;
+    a.cap = (long long)p->tile_cap;
+    a.counter = p->tile_counter;
+    a.ntx = (p->geo.W + TILE - 1) / TILE;
+    a.nty = (p->geo.H + TILE - 1) / TILE;
+    a.stats = p->stats;
+    return a;
+}
+
+extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *cov, const int *pts, int npts,
+                                     double *out, double *aux, void *stream) {
+    if (!p || !f || !cov || !out || (!pts && npts)) return set_err(BSF_EINVAL, "null argument");
+    if (npts < 0) return set_err(BSF_EINVAL, "npts < 0");
+    if (npts == 0) return BSF_OK;
+    bsf_status s = ensure_tile_ws(p);
+    if (s != BSF_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last = st;
+    TileArgs a = tile_args(p, f, cov, out);
+    a.pts = pts;
+    a.npts = npts;
+    a.aux = aux;
+    a.out_f32 = 0;
+    CUDA_TRY(launch_tile_impl(a, p->d.order, p->d.precision, p->tile_nslots, st, p->luts_dev, &p->nlaunch));
+    return BSF_OK;
+}
+
 extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void *out, void *stream) {
     if (!p) return set_err(BSF_EINVAL, "null plan");
+    if (p->d.anchor == BSF_ANCHOR_TILE) {
+        if (!f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+        bsf_status s = ensure_tile_ws(p);
+        if (s != BSF_OK) return s;
+        cudaStream_t st = (cudaStream_t)stream;
+        p->last = st;
+        TileArgs a = tile_args(p, f, cov, out);
+        CUDA_TRY(launch_tile_impl(a, p->d.order, p->d.precision, p->tile_nslots, st, p->luts_dev, &p->nlaunch));
+        return BSF_OK;
+    }
     if (!p->g_ws) {
         void *q;
         if (cudaMalloc(&q, g_bytes(p)) != cudaSuccess) return set_err(BSF_ENOMEM, "g workspace");

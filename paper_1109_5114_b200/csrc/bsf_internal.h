@@ -27,6 +27,7 @@ struct LutBasis {
     int radix[4];
     signed char table[81]; // mixed-radix key -> region (or -1)
     double2 centre[MAX_REG];
+    int wxmin, wxmax, wymin, wymax;  // window offset extents over all variants
     LutVar var[NVAR];
 };
 
@@ -50,6 +51,29 @@ struct GatherArgs {
     double *aux;            // optional per-point diagnostics [8 * npts]
     unsigned long long *stats;  // [5]: pixels, clamped, zero, theta', flags(or)
 };
+
+// Tile-anchored fused path: per 16x16 output tile, local running sums on the
+// tile's halo (zero state), then the gather from them.
+struct TileArgs {
+    int W, H, nimg, channels;
+    int policy, clamp, out_f32, in_u8;
+    const void *f;          // [nimg][H][W]
+    const float *cov;       // [batch][3][H][W]
+    void *out;              // [nimg][H][W] (or float64[npts] with pts)
+    const int *pts;         // optional (img, x, y) triples
+    int npts;
+    double *aux;            // optional per-point diagnostics
+    double2 *scratch;       // [slots][2][cap]
+    long long cap;          // points per basis per slot
+    int *counter;           // work counter (zeroed before launch)
+    int ntx, nty;
+    unsigned long long *stats;
+};
+constexpr int TILE = 16;
+size_t tile_capacity(int order, float max_sigma, const LutBasis *host_luts, int basis_mask);
+int tile_slots();
+cudaError_t launch_tile_impl(const TileArgs &a, int order, int precision, int slots, cudaStream_t st,
+                             const LutBasis *luts_dev, long long *nlaunch);
 
 // launchers (bsf_kernels.cu)
 cudaError_t launch_fill_dd(const void *f, int u8, double2 *g, const Geometry &geo, int nbasis_copy,

@@ -22,6 +22,7 @@ namespace bsf {
 // ---------------------------------------------------------------------------
 __constant__ int c_steps[2][4][2] = {{{1, 0}, {1, 1}, {0, 1}, {-1, 1}}, {{2, 1}, {1, 2}, {-1, 2}, {-2, 1}}};
 static const int h_scan_order[2][4][2] = {{{1, 0}, {1, 1}, {0, 1}, {-1, 1}}, {{1, 2}, {2, 1}, {-1, 2}, {-2, 1}}};
+__constant__ int c_scan_order[2][4][2] = {{{1, 0}, {1, 1}, {0, 1}, {-1, 1}}, {{1, 2}, {2, 1}, {-1, 2}, {-2, 1}}};
 
 // ---------------------------------------------------------------------------
 // element types for the scans
@@ -255,28 +256,6 @@ cudaError_t launch_scan_i64(unsigned long long *g, const Geometry &geo, int basi
 // Gather
 // ---------------------------------------------------------------------------
 
-// arithmetic policies: double-double or plain fp64
-struct ArDD {
-    typedef dd V;
-    __device__ static V zero() { return {0.0, 0.0}; }
-    __device__ static V from(double2 c) { return {c.x, c.y}; }
-    __device__ static V fma(V a, V b, V c) { return dd_fma(a, b, c); }
-    __device__ static V add(V a, V b) { return dd_add(a, b); }
-    __device__ static V mul(V a, V b) { return dd_mul(a, b); }
-    __device__ static V muli(V a, int k) { return dd_mul_d(a, (double)k); }
-    __device__ static double to_d(V a) { return dd_to_d(a); }
-};
-struct ArD {
-    typedef double V;
-    __device__ static V zero() { return 0.0; }
-    __device__ static V from(double2 c) { return c.x + c.y; }
-    __device__ static V fma(V a, V b, V c) { return ::fma(a, b, c); }
-    __device__ static V add(V a, V b) { return a + b; }
-    __device__ static V mul(V a, V b) { return a * b; }
-    __device__ static V muli(V a, int k) { return a * (double)k; }
-    __device__ static double to_d(V a) { return a; }
-};
-
 __device__ __forceinline__ int binom_small(int n, int k) {
     int r = 1;
     for (int i = 0; i < k; ++i) r = r * (n - i) / (i + 1);
@@ -312,85 +291,135 @@ __device__ __forceinline__ int classify(const LutBasis &L, double x, double y) {
     return 0;
 }
 
-template <class Ar>
-__device__ __forceinline__ typename Ar::V horner2(const double2 *__restrict__ c, int deg, typename Ar::V px,
-                                                  typename Ar::V py) {
-    typedef typename Ar::V V;
+// ---------------------------------------------------------------------------
+// Interpolation weights M(phi - d): polynomials in phi (exact doubles, R17)
+// with double-double coefficients.
+// ---------------------------------------------------------------------------
+
+// plain fp64 2D Horner (BSF_PREC_FP64)
+__device__ __forceinline__ double horner2_d(const double2 *__restrict__ c, int deg, double x, double y) {
     int idx = 0;
-    V ax = Ar::zero();
+    double ax = 0.0;
     for (int i = deg; i >= 0; --i) {
-        V ay = Ar::from(__ldg(c + idx++));
-        for (int j = deg - i - 1; j >= 0; --j) ay = Ar::fma(ay, py, Ar::from(__ldg(c + idx++)));
-        ax = (i == deg) ? ay : Ar::fma(ax, px, ay);
+        double2 c0 = __ldg(c + idx++);
+        double ay = c0.x + c0.y;
+        for (int j = deg - i - 1; j >= 0; --j) {
+            double2 cj = __ldg(c + idx++);
+            ay = fma(ay, y, cj.x + cj.y);
+        }
+        ax = (i == deg) ? ay : fma(ax, x, ay);
     }
     return ax;
 }
 
-template <class Ar>
-__device__ __forceinline__ typename Ar::V load_g(const double2 *__restrict__ g, const Geometry &geo, int qx, int qy,
-                                                 int *flags) {
-    if (qy < 0) return Ar::zero();  // above the image every running sum is zero
-    int gx = qx + geo.P;
-    if (gx < 0 || gx >= geo.GW || qy >= geo.GH) {
-        *flags |= FLAG_RANGE;
-        return Ar::zero();
-    }
-    return Ar::from(__ldg(g + (size_t)qy * geo.GW + gx));
+// One compensated Horner step (Graillat-Langlois-Louvet): value (h + l) <-
+// (h + l) * x + (ch + cl), with the rounding errors of h*x and of the sum
+// carried in l.  11 fp64 instructions; result accurate to ~u^2 * cond.
+__device__ __forceinline__ void comp_step(double &h, double &l, double x, double ch, double cl) {
+    double p = __dmul_rn(h, x);
+    double pe = __fma_rn(h, x, -p);
+    double s = __dadd_rn(p, ch);
+    double bb = __dadd_rn(s, -p);
+    double se = __dadd_rn(__dadd_rn(p, -__dadd_rn(s, -bb)), __dadd_rn(ch, -bb));
+    l = __fma_rn(l, x, __dadd_rn(__dadd_rn(pe, se), cl));
+    h = s;
 }
 
-// F(Y) = sum_d G'(floor(Y) + d) M(frac(Y) - d)   (Eq. 11, r-fold, R4/R5)
-template <int R, class Ar>
-__device__ __forceinline__ typename Ar::V interp(const double2 *__restrict__ g, const Geometry &geo,
-                                                 const LutBasis &L, const LutVar &V, dd Yx, dd Yy, int drop,
-                                                 int2 sdrop, int *flags) {
-    typedef typename Ar::V Val;
-    dd fx, fy;
-    int bx = (int)dd_floor(Yx, &fx);
-    int by = (int)dd_floor(Yy, &fy);
-    int reg = classify(L, fx.hi, fy.hi);
-    double2 c = L.centre[reg];
-    Val px, py;
-    if constexpr (sizeof(Val) == 16) {
-        px = dd_add_d(fx, -c.x);
-        py = dd_add_d(fy, -c.y);
-    } else {
-        px = (fx.hi - c.x) + fx.lo;
-        py = (fy.hi - c.y) + fy.lo;
+// compensated 2D Horner with double-double coefficients at an exact point
+__device__ __forceinline__ void horner2_comp(const double2 *__restrict__ c, int deg, double x, double y, double &wh,
+                                             double &wl) {
+    int idx = 0;
+    double ah = 0.0, al = 0.0;
+    for (int i = deg; i >= 0; --i) {
+        double2 c0 = __ldg(c + idx++);
+        double sh = c0.x, sl = c0.y;
+        for (int j = deg - i - 1; j >= 0; --j) {
+            double2 cj = __ldg(c + idx++);
+            comp_step(sh, sl, y, cj.x, cj.y);
+        }
+        if (i == deg) {
+            ah = sh;
+            al = sl;
+        } else {
+            comp_step(ah, al, x, sh, sl);
+        }
     }
+    wh = ah;
+    wl = al;
+}
+
+// Where the running sums are read from: the global domain (bsf_filter) or a
+// tile's local domain (tile path).  Points above Y0 are zero (no image above);
+// other points outside the stored domain are a margin violation.
+struct GView {
+    const double2 *g;
+    int X0, Y0, NX, NY;
+};
+
+__device__ __forceinline__ double2 load_g2(const GView &v, int qx, int qy, int *flags) {
+    int ly = qy - v.Y0, lx = qx - v.X0;
+    if (ly < 0) return make_double2(0.0, 0.0);  // above the rows that hold any image
+    if (lx < 0 || lx >= v.NX || ly >= v.NY) {
+        *flags |= FLAG_RANGE;
+        return make_double2(0.0, 0.0);
+    }
+    return v.g[(size_t)ly * v.NX + lx];  // plain load: tile scratch is written in-kernel
+}
+
+// G' = (1 - T_{s_drop})^R G  (exact lattice difference, R5), double-double
+template <int R>
+__device__ __forceinline__ double2 load_gp(const GView &v, int qx, int qy, int drop, int2 sdrop, int *flags) {
+    if (drop < 0) return load_g2(v, qx, qy, flags);
+    dd G = {0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i <= R; ++i) {
+        double2 t = load_g2(v, qx - i * sdrop.x, qy - i * sdrop.y, flags);
+        int cb = binom_small(R, i) * ((i & 1) ? -1 : 1);
+        G = dd_add(G, dd_mul_d({t.x, t.y}, (double)cb));
+    }
+    return make_double2(G.hi, G.lo);
+}
+
+// F(b + phi) = sum_d G'(b + d) M(phi - d)   (Eq. 11, r-fold, R4/R5)
+// Double-double: weights by compensated Horner, products by TwoProd, the
+// large partial sum by TwoSum, all small terms in one fp64 accumulator.
+template <int R, bool DD>
+__device__ __forceinline__ dd interp(const GView &gv, const LutBasis &L, const LutVar &V, int bx, int by, double fx,
+                                     double fy, int drop, int2 sdrop, int *flags) {
+    int reg = classify(L, fx, fy);
     int n = __ldg(V.counts + reg);
     const int2 *offs = V.offs + reg * V.nmax;
     const double2 *cf = V.coef + (size_t)reg * V.nmax * V.nmon;
-    Val F = Ar::zero();
+    double Fh = 0.0, Fl = 0.0;
     for (int s = 0; s < n; ++s) {
         int2 d = __ldg(offs + s);
-        int qx = bx + d.x, qy = by + d.y;
-        Val G;
-        if (drop < 0) {
-            G = load_g<Ar>(g, geo, qx, qy, flags);
+        double2 G = load_gp<R>(gv, bx + d.x, by + d.y, drop, sdrop, flags);
+        if (DD) {
+            double wh, wl;
+            horner2_comp(cf + (size_t)s * V.nmon, V.deg, fx, fy, wh, wl);
+            double p = __dmul_rn(G.x, wh);
+            double pe = __fma_rn(G.x, wh, -p);
+            double t = __dadd_rn(Fh, p);
+            double bb = __dadd_rn(t, -Fh);
+            double te = __dadd_rn(__dadd_rn(Fh, -__dadd_rn(t, -bb)), __dadd_rn(p, -bb));
+            Fh = t;
+            Fl = __fma_rn(G.x, wl, __fma_rn(G.y, wh, __dadd_rn(Fl, __dadd_rn(te, pe))));
         } else {
-            // G' = (1 - T_{s_drop})^R G  (exact lattice difference, R5)
-            G = Ar::zero();
-#pragma unroll
-            for (int i = 0; i <= R; ++i) {
-                Val t = load_g<Ar>(g, geo, qx - i * sdrop.x, qy - i * sdrop.y, flags);
-                int cb = binom_small(R, i) * ((i & 1) ? -1 : 1);
-                G = Ar::add(G, Ar::muli(t, cb));
-            }
+            double w = horner2_d(cf + (size_t)s * V.nmon, V.deg, fx, fy);
+            Fh = fma(G.x + G.y, w, Fh);
         }
-        Val w = horner2<Ar>(cf + (size_t)s * V.nmon, V.deg, px, py);
-        F = Ar::fma(G, w, F);
     }
-    return F;
+    return fast_two_sum(Fh, Fl);
 }
 
 // out(p) = prod_k (1/a'_k)^R sum_j c_j F(p + sum_k (R/2 - j_k) a'_k s_k)
+// a'_k lies on the 2^-40 grid (R17), so each displacement and their sum are
+// exact doubles: the tap's lattice base b and fractional offset phi are exact.
 #ifdef BSF_TAP_DUMP
 __device__ double *g_tap_dump;
 #endif
-template <int R, class Ar>
-__device__ double mesh(const double2 *__restrict__ g, const Geometry &geo, const LutBasis &L, const PixelScales &ps,
-                       int x, int y, int *flags) {
-    typedef typename Ar::V Val;
+template <int R, bool DD>
+__device__ double mesh(const GView &gv, const LutBasis &L, const PixelScales &ps, int x, int y, int *flags) {
     int dirs[4];
     int ns = 0;
     for (int k = 0; k < 4; ++k)
@@ -400,38 +429,36 @@ __device__ double mesh(const double2 *__restrict__ g, const Geometry &geo, const
     if (ps.drop >= 0) sdrop = make_int2(c_steps[ps.basis][ps.drop][0], c_steps[ps.basis][ps.drop][1]);
     int ntap = 1;
     for (int q = 0; q < ns; ++q) ntap *= (R + 1);
-    Val acc = Ar::zero();
+    dd acc = {0.0, 0.0};
     for (int t = 0; t < ntap; ++t) {
         int tt = t, coef = 1;
-        dd Yx = dd_make((double)x), Yy = dd_make((double)y);
+        double Dx = 0.0, Dy = 0.0;
         for (int q = 0; q < ns; ++q) {
             int j = tt % (R + 1);
             tt /= (R + 1);
             coef *= binom_small(R, j) * ((j & 1) ? -1 : 1);
             int k = dirs[q];
-            double m = 0.5 * R - j;  // half-integer: m * s exact
-            Yx = dd_add(Yx, two_prod(m * c_steps[ps.basis][k][0], ps.ap[k]));
-            Yy = dd_add(Yy, two_prod(m * c_steps[ps.basis][k][1], ps.ap[k]));
+            double m = 0.5 * R - j;  // half-integer
+            Dx += (m * c_steps[ps.basis][k][0]) * ps.ap[k];  // exact (R17)
+            Dy += (m * c_steps[ps.basis][k][1]) * ps.ap[k];
         }
-        Val F = interp<R, Ar>(g, geo, L, V, Yx, Yy, ps.drop, sdrop, flags);
+        double flx = floor(Dx), fly = floor(Dy);
+        double fx = Dx - flx, fy = Dy - fly;  // exact
+        dd F = interp<R, DD>(gv, L, V, x + (int)flx, y + (int)fly, fx, fy, ps.drop, sdrop, flags);
 #ifdef BSF_TAP_DUMP
         if (g_tap_dump && x == 0 && y == 23) {
             double *o = g_tap_dump + 8 * t;
-            dd fx, fy;
-            o[0] = dd_floor(Yx, &fx);
-            o[1] = dd_floor(Yy, &fy);
-            o[2] = fx.hi; o[3] = fx.lo; o[4] = fy.hi; o[5] = fy.lo;
-            if constexpr (sizeof(Val) == 16) { o[6] = F.hi; o[7] = F.lo; } else { o[6] = F; o[7] = 0; }
+            o[0] = x + flx; o[1] = y + fly; o[2] = fx; o[3] = 0; o[4] = fy; o[5] = 0; o[6] = F.hi; o[7] = F.lo;
         }
 #endif
-        acc = Ar::add(acc, Ar::muli(F, coef));
+        acc = dd_add(acc, dd_mul_d(F, (double)coef));
     }
     double norm = 1.0;
     for (int q = 0; q < ns; ++q) {
         double ia = 1.0 / ps.ap[dirs[q]];
         for (int i = 0; i < R; ++i) norm *= ia;
     }
-    return Ar::to_d(acc) * norm;
+    return dd_to_d(acc) * norm;
 }
 
 __device__ __forceinline__ void warp_count(unsigned long long *ctr, bool pred) {
@@ -441,7 +468,7 @@ __device__ __forceinline__ void warp_count(unsigned long long *ctr, bool pred) {
     if ((int)(threadIdx.x & 31) == leader && b) atomicAdd(ctr, (unsigned long long)__popc(b));
 }
 
-template <int R, class Ar>
+template <int R, bool DD>
 __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a, const LutBasis *__restrict__ luts) {
     int img, x, y;
     long long oidx;
@@ -471,8 +498,8 @@ __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a, const LutBasi
         res = __longlong_as_double(0x7ff8000000000000LL);
     } else {
         int slot = geo.nbases == 2 ? ps.basis : 0;
-        const double2 *g = a.g + ((size_t)slot * geo.nimg + img) * geo.GH * geo.GW;
-        res = mesh<R, Ar>(g, geo, luts[ps.basis], ps, x, y, &flags);
+        GView gv = {a.g + ((size_t)slot * geo.nimg + img) * geo.GH * geo.GW, -geo.P, 0, geo.GW, geo.GH};
+        res = mesh<R, DD>(gv, luts[ps.basis], ps, x, y, &flags);
     }
     if (a.aux) {
         double *ax = a.aux + 8 * oidx;
@@ -495,6 +522,215 @@ __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a, const LutBasi
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Tile-anchored fused path.
+//
+// Restarting the running sums at zero on a window that contains the kernel
+// supports of a tile's pixels (plus the windows of their taps) leaves the
+// filter output unchanged (the output only depends on f inside the supports,
+// and truncating the sum domain adds only functions constant along a sum
+// direction, which the mesh annihilates: SURVEY F9, R18).  It bounds
+// the sums' magnitude by the tile's own reach (conditioning) and
+// keeps the sums in an L2-resident per-CTA scratch instead of an HBM image.
+// ---------------------------------------------------------------------------
+struct TileDomain {
+    int X0, Y0, NX, NY;
+};
+
+__device__ __forceinline__ TileDomain tile_domain(const LutBasis &L, int R, int x0, int y0, int EX, int EY) {
+    TileDomain d;
+    d.X0 = x0 - EX + L.wxmin - 2 * R - 1;  // zero-scale lattice difference reaches back R|s_x| <= 2R
+    int X1 = x0 + TILE - 1 + EX + L.wxmax + 2 * R + 1;
+    d.Y0 = y0 - EY;                        // no kernel support above: zero state
+    int Y1 = y0 + TILE - 1 + EY + L.wymax + 1;
+    d.NX = X1 - d.X0 + 1;
+    d.NY = Y1 - d.Y0 + 1;
+    return d;
+}
+
+// one running-sum level along (sx, sy) on the NX x NY local domain; threads own lines
+__device__ __forceinline__ void tile_scan_level(double2 *__restrict__ G, int NX, int NY, int sx, int sy) {
+    int nlines = sy == 0 ? NY : sy * NX + abs(sx) * (NY - sy);
+    for (int l = threadIdx.x; l < nlines; l += blockDim.x) {
+        int xs, ys;
+        if (sy == 0) {
+            xs = 0;
+            ys = l;
+        } else if (l < sy * NX) {
+            xs = l % NX;
+            ys = l / NX;
+        } else {
+            int q = l - sy * NX, as = abs(sx);
+            ys = sy + q / as;
+            xs = sx > 0 ? q % as : NX - 1 - q % as;
+        }
+        dd acc = {0.0, 0.0};
+        for (int xx = xs, yy = ys; xx >= 0 && xx < NX && yy < NY; xx += sx, yy += sy) {
+            double2 v = G[(size_t)yy * NX + xx];
+            acc = dd_add(acc, {v.x, v.y});
+            G[(size_t)yy * NX + xx] = make_double2(acc.hi, acc.lo);
+        }
+    }
+}
+
+template <int R, bool DD>
+__global__ void __launch_bounds__(256) tile_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
+    __shared__ int s_item, s_ex[2], s_ey[2], s_used, s_bad;
+    const int tid = threadIdx.x;
+    double2 *scr = a.scratch + (size_t)blockIdx.x * 2 * a.cap;
+    const int tiles_per_img = a.ntx * a.nty;
+    const int nitems = a.pts ? a.npts : tiles_per_img * a.nimg;
+    for (;;) {
+        if (tid == 0) {
+            s_item = atomicAdd(a.counter, 1);
+            s_ex[0] = s_ex[1] = s_ey[0] = s_ey[1] = 0;
+            s_used = 0;
+            s_bad = 0;
+        }
+        __syncthreads();
+        const int item = s_item;
+        if (item >= nitems) break;
+        int img, x0, y0, want = -1;
+        if (a.pts) {
+            img = a.pts[3 * item];
+            int px = a.pts[3 * item + 1], py = a.pts[3 * item + 2];
+            x0 = px & ~(TILE - 1);
+            y0 = py & ~(TILE - 1);
+            want = (px - x0) + TILE * (py - y0);
+        } else {
+            img = item / tiles_per_img;
+            int rem = item % tiles_per_img;
+            x0 = (rem % a.ntx) * TILE;
+            y0 = (rem / a.ntx) * TILE;
+        }
+        const int x = x0 + (tid % TILE), y = y0 + tid / TILE;
+        const bool valid = x < a.W && y < a.H;
+        PixelScales ps;
+        ps.flags = 0;
+        ps.basis = 0;
+        ps.drop = -1;
+        ps.clamped = 0;
+        if (valid) {
+            size_t plane = (size_t)a.H * a.W;
+            const float *cv = a.cov + (size_t)(img / a.channels) * 3 * plane + (size_t)y * a.W + x;
+            pixel_scales(__ldg(cv), __ldg(cv + plane), __ldg(cv + 2 * plane), a.policy, a.clamp, R, ps);
+        }
+        const bool live = valid && !(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
+        if (live) {
+            double ex = 0.0, ey = 0.0;
+            for (int k = 0; k < 4; ++k) {
+                ex += ps.ap[k] * abs(c_steps[ps.basis][k][0]);
+                ey += ps.ap[k] * c_steps[ps.basis][k][1];
+            }
+            atomicMax(&s_ex[ps.basis], (int)ceil(0.5 * R * ex));
+            atomicMax(&s_ey[ps.basis], (int)ceil(0.5 * R * ey));
+            atomicOr(&s_used, 1 << ps.basis);
+        }
+        __syncthreads();
+        const int used = s_used;
+        const size_t ipl = (size_t)a.H * a.W;
+        for (int b = 0; b < 2; ++b) {
+            if (!(used & (1 << b))) continue;
+            TileDomain d = tile_domain(luts[b], R, x0, y0, s_ex[b], s_ey[b]);
+            if ((long long)d.NX * d.NY > a.cap) {
+                if (tid == 0) s_bad = 1;
+                continue;
+            }
+            double2 *G = scr + (size_t)b * a.cap;
+            const int n = d.NX * d.NY;
+            for (int i = tid; i < n; i += blockDim.x) {
+                int X = d.X0 + i % d.NX, Y = d.Y0 + i / d.NX;
+                double v = 0.0;
+                if (X >= 0 && X < a.W && Y >= 0 && Y < a.H) {
+                    size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
+                    v = a.in_u8 ? (double)((const uint8_t *)a.f)[o] : (double)((const float *)a.f)[o];
+                }
+                G[i] = make_double2(v, 0.0);
+            }
+            __syncthreads();
+            for (int rep = 0; rep < R; ++rep)
+                for (int lv = 0; lv < 4; ++lv) {
+                    tile_scan_level(G, d.NX, d.NY, c_scan_order[b][lv][0], c_scan_order[b][lv][1]);
+                    __syncthreads();
+                }
+        }
+        __syncthreads();
+        int flags = ps.flags | (s_bad ? FLAG_RANGE : 0);
+        const bool mine = a.pts ? (tid == want) : valid;
+        if (mine) {
+            double res = __longlong_as_double(0x7ff8000000000000LL);
+            if (live && !s_bad) {
+                TileDomain d = tile_domain(luts[ps.basis], R, x0, y0, s_ex[ps.basis], s_ey[ps.basis]);
+                GView gv = {scr + (size_t)ps.basis * a.cap, d.X0, d.Y0, d.NX, d.NY};
+                res = mesh<R, DD>(gv, luts[ps.basis], ps, x, y, &flags);
+            }
+            long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
+            if (a.aux) {
+                double *ax = a.aux + 8 * oidx;
+                ax[0] = ps.basis;
+                ax[1] = ps.drop;
+                ax[2] = ps.clamped;
+                ax[3] = flags;
+                for (int k = 0; k < 4; ++k) ax[4 + k] = ps.ap[k];
+            }
+            if (a.out_f32 && !a.pts)
+                ((float *)a.out)[oidx] = (float)res;
+            else
+                ((double *)a.out)[oidx] = res;
+            if (a.stats) {
+                atomicAdd(a.stats + 0, 1ull);
+                if (ps.clamped) atomicAdd(a.stats + 1, 1ull);
+                if (ps.drop >= 0) atomicAdd(a.stats + 2, 1ull);
+                if (ps.basis == BASIS_THETA_PRIME) atomicAdd(a.stats + 3, 1ull);
+                if (flags) atomicOr(a.stats + 4, (unsigned long long)flags);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+size_t tile_capacity(int order, float max_sigma, const LutBasis *L, int basis_mask) {
+    int E = (int)ceil((double)max_sigma * sqrt(24.0 * order)) + 1;  // (r/2) sum_k a'_k |s_k| bound
+    size_t cap = 0;
+    for (int b = 0; b < 2; ++b) {
+        if (!(basis_mask & (1 << b))) continue;
+        size_t nx = TILE + 2 * E + (L[b].wxmax - L[b].wxmin) + 4 * order + 4;
+        size_t ny = TILE + 2 * E + L[b].wymax + 2;
+        cap = nx * ny > cap ? nx * ny : cap;
+    }
+    return cap;
+}
+
+int tile_slots() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return 2 * sms;
+}
+
+template <int R>
+static void launch_tile_r(const TileArgs &a, int prec, int slots, cudaStream_t st, const LutBasis *luts) {
+    if (prec == BSF_PREC_DD)
+        tile_kernel<R, true><<<slots, 256, 0, st>>>(a, luts);
+    else
+        tile_kernel<R, false><<<slots, 256, 0, st>>>(a, luts);
+}
+
+cudaError_t launch_tile_impl(const TileArgs &a, int order, int prec, int slots, cudaStream_t st,
+                             const LutBasis *luts, long long *nl) {
+    cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+    switch (order) {
+        case 1: launch_tile_r<1>(a, prec, slots, st, luts); break;
+        case 2: launch_tile_r<2>(a, prec, slots, st, luts); break;
+        case 3: launch_tile_r<3>(a, prec, slots, st, luts); break;
+        case 4: launch_tile_r<4>(a, prec, slots, st, luts); break;
+        default: return cudaErrorInvalidValue;
+    }
+    ++*nl;
+    return cudaGetLastError();
+}
+
 template <int R>
 static void launch_r(const GatherArgs &a, int prec, cudaStream_t st, const LutBasis *luts) {
     dim3 grid, block(128);
@@ -503,9 +739,9 @@ static void launch_r(const GatherArgs &a, int prec, cudaStream_t st, const LutBa
     else
         grid = dim3((a.geo.W + 15) / 16, (a.geo.H + 7) / 8, a.geo.nimg);
     if (prec == BSF_PREC_DD)
-        gather_kernel<R, ArDD><<<grid, block, 0, st>>>(a, luts);
+        gather_kernel<R, true><<<grid, block, 0, st>>>(a, luts);
     else
-        gather_kernel<R, ArD><<<grid, block, 0, st>>>(a, luts);
+        gather_kernel<R, false><<<grid, block, 0, st>>>(a, luts);
 }
 
 #ifdef BSF_TAP_DUMP

@@ -204,6 +204,14 @@ __device__ __forceinline__ void pixel_scales(float sxf, float syf, float thf, in
             ++nz;
         }
     if (nz > 1) ps.flags |= FLAG_TWO_ZERO;
+    // R17: put a'_k on the 2^-40 grid.  Then every tap displacement
+    // (R/2 - j) a'_k s_k is a multiple of 2^-41 below 2^12 in magnitude, so
+    // displacements, their sums, lattice bases and fractional offsets are
+    // exact doubles.  Scale change <= 2^-41 (lattice units).
+    for (int k = 0; k < 4; ++k) {
+        ps.ap[k] = rint(ps.ap[k] * 0x1p40) * 0x1p-40;
+        if (ps.ap[k] == 0.0 && k != ps.drop) ps.flags |= FLAG_TWO_ZERO;  // sigma below ~1e-12
+    }
 }
 
 }  // namespace bsf

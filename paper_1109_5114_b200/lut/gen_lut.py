@@ -19,7 +19,7 @@ piece M is one polynomial in the local coordinate phi = x - (i, j).
 
 Output table per (basis, r, variant): for each region rho of the unit cell,
 the window offsets d with M(phi - d) != 0 and the coefficients of
-M(phi - d) as a polynomial in (phi - c_rho), c_rho a rational point of rho.
+M(phi - d) as a polynomial in phi (expansion centre c_rho = 0).
 Coefficients are stored as double-double (hi, lo) pairs.
 """
 from __future__ import annotations
@@ -151,8 +151,9 @@ def unit_regions(basis, n=400):
         cx += 0.00131
         cy += 0.00071
         assert region_key(basis, cx, cy) == k
-        # rational centre on a 1/64 grid (any point works as expansion centre)
-        rc = (Fr(round(cx * 64), 64), Fr(round(cy * 64), 64))
+        # expansion centre: the cell origin, so that psi = phi is exact on the
+        # GPU (fractional tap offsets are exact doubles, R17)
+        rc = (Fr(0), Fr(0))
         regs.append({"key": k, "rep": (cx, cy), "centre": rc, "area": cnt / n / n})
     return regs
 
@@ -194,8 +195,74 @@ def base_parallelogram(basis, sa, sb):
     return P
 
 
-def integrate_dir(P, xi):
-    """M'(x) = int_0^1 M(x - t xi) dt, piece by piece."""
+_W = {}  # worker globals (fork)
+
+
+def _integrate_piece(key):
+    P, xi, fams = _W["P"], _W["xi"], _W["fams"]
+    Gcache = _W.setdefault("Gcache", {})
+    i, j, ri = key
+    reg = P.regs[ri]
+    px, py = i + reg["rep"][0], j + reg["rep"][1]
+    cuts = []  # (t, nvec, c)
+    for nx, ny in fams:
+        nd = nx * xi[0] + ny * xi[1]
+        if nd == 0:
+            continue
+        v0 = nx * px + ny * py
+        v1 = v0 - nd  # value at t = 1
+        lo, hi = min(v0, v1), max(v0, v1)
+        for c in range(math.ceil(lo), math.floor(hi) + 1):
+            t = (v0 - c) / nd
+            if 1e-12 < t < 1 - 1e-12:
+                cuts.append((t, (nx, ny), c, nd))
+    cuts.sort()
+    bounds = [(0.0, None)] + [(t, (n, c, nd)) for t, n, c, nd in cuts] + [(1.0, None)]
+    total = {}
+    for m in range(len(bounds) - 1):
+        ta, ba = bounds[m]
+        tb, bb = bounds[m + 1]
+        if tb - ta < 1e-9:
+            raise RuntimeError("degenerate crossing order at a representative point")
+        tm = 0.5 * (ta + tb)
+        si, sj, sr = P.locate(px - tm * xi[0], py - tm * xi[1])
+        src = P.pieces.get((si, sj, sr))
+        if not src:
+            continue
+        # G: antiderivative of src (in its local coords) along xi
+        gk = (si, sj, sr)
+        if gk not in Gcache:
+            Gcache[gk] = antideriv_along(src, xi)
+        G = Gcache[gk]
+        # int_{ta}^{tb} src(z - t xi) dt = G(z - ta xi) - G(z - tb xi)
+        # with z = phi + (i - si, j - sj) in the source's local coords.
+        dx, dy = i - si, j - sj
+
+        def tpoly(b):
+            if b is None:
+                return None
+            (nx, ny), c, nd = b
+            # t(phi) = (n.(phi + (i,j)) - c) / nd
+            return lin(Fr(nx, nd), Fr(ny, nd), Fr(nx * i + ny * j - c, nd))
+
+        def at(tb_, tconst):
+            if tb_ is None:
+                X = lin(1, 0, dx - tconst * xi[0])
+                Y = lin(0, 1, dy - tconst * xi[1])
+            else:
+                # phi + d - t(phi) xi
+                X = padd(lin(1, 0, dx), {k: -xi[0] * v for k, v in tb_.items()})
+                Y = padd(lin(0, 1, dy), {k: -xi[1] * v for k, v in tb_.items()})
+            return compose(G, X, Y)
+
+        Ga = at(tpoly(ba), Fr(0) if ba is None and m == 0 else None)
+        Gb = at(tpoly(bb), Fr(1) if bb is None else None)
+        total = padd(total, padd(Ga, Gb, -1))
+    return key, total
+
+
+def integrate_dir(P, xi, workers=None):
+    """M'(x) = int_0^1 M(x - t xi) dt, piece by piece (pieces in parallel)."""
     basis = P.basis
     Q = PPoly(basis)
     Q.regs, Q.key2reg = P.regs, P.key2reg
@@ -210,67 +277,19 @@ def integrate_dir(P, xi):
     for nx, ny in normals(basis) + [(1, 0), (0, 1)]:
         if (nx, ny) not in fams and (-nx, -ny) not in fams:
             fams.append((nx, ny))
-    Gcache = {}
-    for i in range(i0, i1 + 1):
-        for j in range(j0, j1 + 1):
-            for ri, reg in enumerate(P.regs):
-                px, py = i + reg["rep"][0], j + reg["rep"][1]
-                cuts = []  # (t, nvec, c)
-                for nx, ny in fams:
-                    nd = nx * xi[0] + ny * xi[1]
-                    if nd == 0:
-                        continue
-                    v0 = nx * px + ny * py
-                    v1 = v0 - nd  # value at t = 1
-                    lo, hi = min(v0, v1), max(v0, v1)
-                    for c in range(math.ceil(lo), math.floor(hi) + 1):
-                        t = (v0 - c) / nd
-                        if 1e-12 < t < 1 - 1e-12:
-                            cuts.append((t, (nx, ny), c, nd))
-                cuts.sort()
-                bounds = [(0.0, None)] + [(t, (n, c, nd)) for t, n, c, nd in cuts] + [(1.0, None)]
-                total = {}
-                for m in range(len(bounds) - 1):
-                    ta, ba = bounds[m]
-                    tb, bb = bounds[m + 1]
-                    if tb - ta < 1e-9:
-                        raise RuntimeError("degenerate crossing order at a representative point")
-                    tm = 0.5 * (ta + tb)
-                    si, sj, sr = P.locate(px - tm * xi[0], py - tm * xi[1])
-                    src = P.pieces.get((si, sj, sr))
-                    if not src:
-                        continue
-                    # G: antiderivative of src (in its local coords) along xi
-                    gk = (si, sj, sr)
-                    if gk not in Gcache:
-                        Gcache[gk] = antideriv_along(src, xi)
-                    G = Gcache[gk]
-                    # int_{ta}^{tb} src(z - t xi) dt = -(G(z - tb xi) - G(z - ta xi))
-                    # with z = phi + (i - si, j - sj) in the source's local coords.
-                    dx, dy = i - si, j - sj
-
-                    def tpoly(b):
-                        if b is None:
-                            return None
-                        (nx, ny), c, nd = b
-                        # t(phi) = (n.(phi + (i,j)) - c) / nd
-                        return lin(Fr(nx, nd), Fr(ny, nd), Fr(nx * i + ny * j - c, nd))
-
-                    def at(tb_, tconst):
-                        if tb_ is None:
-                            X = lin(1, 0, dx - tconst * xi[0])
-                            Y = lin(0, 1, dy - tconst * xi[1])
-                        else:
-                            # phi + d - t(phi) xi
-                            X = padd(lin(1, 0, dx), {k: -xi[0] * v for k, v in tb_.items()})
-                            Y = padd(lin(0, 1, dy), {k: -xi[1] * v for k, v in tb_.items()})
-                        return compose(G, X, Y)
-
-                    Ga = at(tpoly(ba), Fr(0) if ba is None and m == 0 else None)
-                    Gb = at(tpoly(bb), Fr(1) if bb is None else None)
-                    total = padd(total, padd(Ga, Gb, -1))
-                if total:
-                    Q.pieces[(i, j, ri)] = total
+    keys = [(i, j, ri) for i in range(i0, i1 + 1) for j in range(j0, j1 + 1) for ri in range(len(P.regs))]
+    _W.clear()
+    _W.update(P=P, xi=xi, fams=fams)
+    workers = workers or int(os.environ.get("BSF_LUT_WORKERS", "0")) or (os.cpu_count() or 1)
+    if workers > 1 and len(keys) > 64:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(workers) as pool:
+            results = pool.map(_integrate_piece, keys, chunksize=max(1, len(keys) // (8 * workers)))
+    else:
+        results = [_integrate_piece(k) for k in keys]
+    for key, total in results:
+        if total:
+            Q.pieces[key] = total
     return Q
 
 

@@ -12,11 +12,11 @@ DT = {"u8": bsf.BSF_U8, "f32": bsf.BSF_F32}
 
 
 def make_plan(w: synth.Workload, *, policy=None, order=None, precision=bsf.BSF_PREC_DD, clamp=1, out_f32=False,
-              margin_x=0, margin_y=0, batch=None):
+              margin_x=0, margin_y=0, batch=None, anchor=bsf.BSF_ANCHOR_GLOBAL):
     return bsf.Plan(w.width, w.height, batch=batch or w.batch, channels=w.channels, in_dtype=DT[w.in_dtype],
                     out_dtype=bsf.BSF_F32 if out_f32 else bsf.BSF_F64, order=order or w.order,
                     basis=w.basis if policy is None else policy, max_sigma=w.max_sigma, margin_x=margin_x,
-                    margin_y=margin_y, clamp=clamp, precision=precision)
+                    margin_y=margin_y, clamp=clamp, precision=precision, anchor=anchor)
 
 
 def gpu_full(plan: bsf.Plan, img: torch.Tensor, cov: torch.Tensor, out_dtype=torch.float64) -> torch.Tensor:
@@ -41,6 +41,15 @@ def gpu_points(plan: bsf.Plan, img: torch.Tensor, cov: torch.Tensor, pts: torch.
     plan.filter_points(g, c, p, out)
     torch.cuda.synchronize()
     return out.cpu()
+
+
+def tile_points(plan: bsf.Plan, img: torch.Tensor, cov: torch.Tensor, pts: torch.Tensor, aux=False):
+    dev = torch.device("cuda:0")
+    out = torch.empty(pts.shape[0], dtype=torch.float64, device=dev)
+    ax = torch.empty(pts.shape[0] * 8, dtype=torch.float64, device=dev) if aux else None
+    plan.run_points(img.to(dev).contiguous(), cov.to(dev).contiguous(), pts.to(dev).contiguous(), out, ax)
+    torch.cuda.synchronize()
+    return (out.cpu(), ax.cpu().view(-1, 8)) if aux else out.cpu()
 
 
 def oracle_points(img: np.ndarray, cov: np.ndarray, xs, ys, *, policy, r, clamp=1, nthreads=0):
