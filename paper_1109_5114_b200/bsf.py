@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbsf.so")
+LIB_PATH = os.environ.get("BSF_LIB") or os.path.join(HERE, "libbsf.so")
 LUT_DIR = os.path.join(HERE, "lut")
 
 BSF_U8, BSF_F32, BSF_F64, BSF_I64, BSF_DD = 0, 1, 2, 3, 4

@@ -325,27 +325,46 @@ __device__ __forceinline__ void comp_step(double &h, double &l, double x, double
     h = s;
 }
 
-// compensated 2D Horner with double-double coefficients at an exact point
-__device__ __forceinline__ void horner2_comp(const double2 *__restrict__ c, int deg, double x, double y, double &wh,
-                                             double &wl) {
+// compensated 2D Horner with double-double coefficients at an exact point;
+// NW independent polynomials (window points) are evaluated in lock-step so the
+// serial dependency chain of each is interleaved with the others (ILP).
+template <int NW>
+__device__ __forceinline__ void horner2_comp_n(const double2 *__restrict__ c, int nmon, int deg, double x, double y,
+                                               double *wh, double *wl) {
+    double ah[NW], al[NW];
     int idx = 0;
-    double ah = 0.0, al = 0.0;
     for (int i = deg; i >= 0; --i) {
-        double2 c0 = __ldg(c + idx++);
-        double sh = c0.x, sl = c0.y;
-        for (int j = deg - i - 1; j >= 0; --j) {
-            double2 cj = __ldg(c + idx++);
-            comp_step(sh, sl, y, cj.x, cj.y);
+        double sh[NW], sl[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            double2 c0 = __ldg(c + w * nmon + idx);
+            sh[w] = c0.x;
+            sl[w] = c0.y;
         }
-        if (i == deg) {
-            ah = sh;
-            al = sl;
-        } else {
-            comp_step(ah, al, x, sh, sl);
+        ++idx;
+        for (int j = deg - i - 1; j >= 0; --j) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                double2 cj = __ldg(c + w * nmon + idx);
+                comp_step(sh[w], sl[w], y, cj.x, cj.y);
+            }
+            ++idx;
+        }
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            if (i == deg) {
+                ah[w] = sh[w];
+                al[w] = sl[w];
+            } else {
+                comp_step(ah[w], al[w], x, sh[w], sl[w]);
+            }
         }
     }
-    wh = ah;
-    wl = al;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        wh[w] = ah[w];
+        wl[w] = al[w];
+    }
 }
 
 // Where the running sums are read from: the global domain (bsf_filter) or a
@@ -391,19 +410,36 @@ __device__ __forceinline__ dd interp(const GView &gv, const LutBasis &L, const L
     const int2 *offs = V.offs + reg * V.nmax;
     const double2 *cf = V.coef + (size_t)reg * V.nmax * V.nmon;
     double Fh = 0.0, Fl = 0.0;
-    for (int s = 0; s < n; ++s) {
+    // F += G * w with w = wh + wl: TwoProd for G.hi * wh, TwoSum into Fh, all
+    // small terms (product error, sum error, G.hi*wl, G.lo*wh) into Fl.
+    auto accum = [&](double2 G, double wh, double wl) {
+        double p = __dmul_rn(G.x, wh);
+        double pe = __fma_rn(G.x, wh, -p);
+        double t = __dadd_rn(Fh, p);
+        double bb = __dadd_rn(t, -Fh);
+        double te = __dadd_rn(__dadd_rn(Fh, -__dadd_rn(t, -bb)), __dadd_rn(p, -bb));
+        Fh = t;
+        Fl = __fma_rn(G.x, wl, __fma_rn(G.y, wh, __dadd_rn(Fl, __dadd_rn(te, pe))));
+    };
+    int s = 0;
+    if (DD) {
+        for (; s + 2 <= n; s += 2) {
+            int2 d0 = __ldg(offs + s), d1 = __ldg(offs + s + 1);
+            double2 G0 = load_gp<R>(gv, bx + d0.x, by + d0.y, drop, sdrop, flags);
+            double2 G1 = load_gp<R>(gv, bx + d1.x, by + d1.y, drop, sdrop, flags);
+            double wh[2], wl[2];
+            horner2_comp_n<2>(cf + (size_t)s * V.nmon, V.nmon, V.deg, fx, fy, wh, wl);
+            accum(G0, wh[0], wl[0]);
+            accum(G1, wh[1], wl[1]);
+        }
+    }
+    for (; s < n; ++s) {
         int2 d = __ldg(offs + s);
         double2 G = load_gp<R>(gv, bx + d.x, by + d.y, drop, sdrop, flags);
         if (DD) {
             double wh, wl;
-            horner2_comp(cf + (size_t)s * V.nmon, V.deg, fx, fy, wh, wl);
-            double p = __dmul_rn(G.x, wh);
-            double pe = __fma_rn(G.x, wh, -p);
-            double t = __dadd_rn(Fh, p);
-            double bb = __dadd_rn(t, -Fh);
-            double te = __dadd_rn(__dadd_rn(Fh, -__dadd_rn(t, -bb)), __dadd_rn(p, -bb));
-            Fh = t;
-            Fl = __fma_rn(G.x, wl, __fma_rn(G.y, wh, __dadd_rn(Fl, __dadd_rn(te, pe))));
+            horner2_comp_n<1>(cf + (size_t)s * V.nmon, V.nmon, V.deg, fx, fy, &wh, &wl);
+            accum(G, wh, wl);
         } else {
             double w = horner2_d(cf + (size_t)s * V.nmon, V.deg, fx, fy);
             Fh = fma(G.x + G.y, w, Fh);
@@ -469,7 +505,10 @@ __device__ __forceinline__ void warp_count(unsigned long long *ctr, bool pred) {
 }
 
 template <int R, bool DD>
-__global__ void __launch_bounds__(128) gather_kernel(GatherArgs a, const LutBasis *__restrict__ luts) {
+#ifndef BSF_GATHER_MINB
+#define BSF_GATHER_MINB 6
+#endif
+__global__ void __launch_bounds__(128, BSF_GATHER_MINB) gather_kernel(GatherArgs a, const LutBasis *__restrict__ luts) {
     int img, x, y;
     long long oidx;
     if (a.pts) {
@@ -575,7 +614,10 @@ __device__ __forceinline__ void tile_scan_level(double2 *__restrict__ G, int NX,
 }
 
 template <int R, bool DD>
-__global__ void __launch_bounds__(256) tile_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
+#ifndef BSF_TILE_MINB
+#define BSF_TILE_MINB 3
+#endif
+__global__ void __launch_bounds__(256, BSF_TILE_MINB) tile_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
     __shared__ int s_item, s_ex[2], s_ey[2], s_used, s_bad;
     const int tid = threadIdx.x;
     double2 *scr = a.scratch + (size_t)blockIdx.x * 2 * a.cap;
@@ -706,7 +748,7 @@ int tile_slots() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return 2 * sms;
+    return BSF_TILE_MINB * sms;
 }
 
 template <int R>

@@ -1,0 +1,125 @@
+"""Multi-GPU partitioning: one process per GPU.
+
+* Independent images / frames (config 4, and bench's weak scaling): each rank
+  filters its own contiguous range of frames; no collective on the data path.
+* One huge image (config 5): row strips.  The filtered value at p depends only
+  on f inside p's kernel support (half-extent <= R_s = sigma_max sqrt(24 r)),
+  so each rank receives the input rows [y0 - R_s, y0) and [y1, y1 + R_s) from
+  its neighbours (one NCCL send/recv pair per neighbour) and runs the
+  tile-anchored kernel on its block.  Strip and halo boundaries are multiples
+  of the 16-row tile, so every kept tile sees exactly the data and domain it
+  sees in a single-GPU run: the outputs are bit-identical.  No scan carries
+  are exchanged (the tile path restarts its sums per tile).
+
+Only plumbing lives here (partition arithmetic, halo exchange through
+torch.distributed); the compute is the C-ABI library.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+TILE = 16
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous balanced split of n units: [start, stop) for `rank`."""
+    base, extra = divmod(n, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def halo_rows(max_sigma: float, order: int) -> int:
+    """Kernel-support half-extent bound in rows, rounded up to whole tiles."""
+    rs = int(math.ceil(max_sigma * math.sqrt(24.0 * order))) + 1
+    return TILE * ((rs + TILE - 1) // TILE)
+
+
+@dataclass
+class Strip:
+    rank: int
+    world: int
+    y0: int      # first output row of this rank
+    y1: int      # one past the last output row
+    b0: int      # first row of the local block (input incl. halo)
+    b1: int      # one past the last row of the local block
+    halo: int
+
+    @property
+    def rows(self):
+        return self.b1 - self.b0
+
+    @property
+    def out_slice(self):
+        """Rows of the local block that are this rank's outputs."""
+        return slice(self.y0 - self.b0, self.y1 - self.b0)
+
+
+def strip_plan(H: int, rank: int, world: int, halo: int) -> Strip:
+    """Row strips aligned to the tile grid (every strip but the last has a
+    multiple of 16 rows)."""
+    ntiles = (H + TILE - 1) // TILE
+    t0, t1 = shard_range(ntiles, rank, world)
+    y0, y1 = t0 * TILE, min(H, t1 * TILE)
+    return Strip(rank, world, y0, y1, max(0, y0 - halo), min(H, y1 + halo), halo)
+
+
+def exchange_halos(own: torch.Tensor, strip: Strip, H: int, group=None) -> torch.Tensor:
+    """Assemble the local block [b0, b1) from this rank's rows [y0, y1)
+    (`own`, shape (..., y1 - y0, W)) and the neighbours' boundary rows, with
+    point-to-point sends/receives (NCCL over NVLink for CUDA tensors, gloo on
+    CPU).  Assumes every strip is at least `halo` rows tall (else a halo would
+    span two neighbours)."""
+    import torch.distributed as dist
+    r, n = strip.rank, strip.world
+    lead = own.shape[:-2]
+    W = own.shape[-1]
+    block = own.new_zeros(lead + (strip.rows, W))
+    block[..., strip.out_slice, :] = own
+    ops = []
+    top = strip.y0 - strip.b0          # rows needed from rank - 1
+    bot = strip.b1 - strip.y1          # rows needed from rank + 1
+    if r > 0:
+        prev = strip_plan(H, r - 1, n, strip.halo)
+        send_up = prev.b1 - prev.y1    # rows rank-1 needs from me
+        ops.append(dist.P2POp(dist.isend, own[..., :send_up, :].contiguous(), r - 1, group))
+        recv_top = block.new_empty(lead + (top, W))
+        ops.append(dist.P2POp(dist.irecv, recv_top, r - 1, group))
+    if r < n - 1:
+        nxt = strip_plan(H, r + 1, n, strip.halo)
+        send_dn = nxt.y0 - nxt.b0      # rows rank+1 needs from me
+        ops.append(dist.P2POp(dist.isend, own[..., own.shape[-2] - send_dn:, :].contiguous(), r + 1, group))
+        recv_bot = block.new_empty(lead + (bot, W))
+        ops.append(dist.P2POp(dist.irecv, recv_bot, r + 1, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if r > 0:
+        block[..., :top, :] = recv_top
+    if r < n - 1:
+        block[..., strip.rows - bot:, :] = recv_bot
+    return block
+
+
+def filter_strip(plan_factory, f_own: torch.Tensor, cov_own: torch.Tensor, strip: Strip, H: int, group=None,
+                 stream=None) -> torch.Tensor:
+    """Filter this rank's strip of one image: exchange input halos, run the
+    tile-anchored library path on the block, keep the own rows.
+
+    plan_factory(height) -> a bsf.Plan for a W x height block (anchor TILE)
+    f_own (y1 - y0, W); cov_own (3, y1 - y0, W) -- this rank's rows only.
+    The covariance of halo rows is never used (their outputs are discarded),
+    so it is not exchanged."""
+    f_blk = exchange_halos(f_own, strip, H, group)
+    cov_blk = cov_own.new_zeros((3, strip.rows, cov_own.shape[-1]))
+    cov_blk[:, strip.out_slice, :] = cov_own
+    if strip.y0 > strip.b0:
+        cov_blk[:, :strip.y0 - strip.b0, :] = 1.0  # placeholder sigma for discarded halo outputs
+    if strip.b1 > strip.y1:
+        cov_blk[:, strip.rows - (strip.b1 - strip.y1):, :] = 1.0
+    plan = plan_factory(strip.rows)
+    out = torch.empty((1, strip.rows, f_own.shape[-1]), dtype=torch.float64, device=f_own.device)
+    plan.run(f_blk.contiguous(), cov_blk.contiguous(), out, stream)
+    return out[0, strip.out_slice, :]
