@@ -74,22 +74,71 @@ def lin(cx, cy, c0):
     return p
 
 
+def _mul_lin_int(A, a, b, c):
+    """(a x + b y + c) * A for a dense integer array A[i, j] (x^i y^j)."""
+    import numpy as np
+    n = A.shape[0]
+    R = np.zeros((n + 1, n + 1), dtype=object)
+    if c:
+        R[:n, :n] += A * c
+    if a:
+        R[1:, :n] += A * a
+    if b:
+        R[:n, 1:] += A * b
+    return R
+
+
+def _lcm(a, b):
+    return a // math.gcd(a, b) * b
+
+
 def compose(P, X, Y, cache=None):
-    """P(X(phi), Y(phi)) for linear polynomials X, Y."""
+    """P(X(phi), Y(phi)) for linear polynomials X, Y, exactly.
+
+    Integer Horner on dense arrays: with X = Xh/dX, Y = Yh/dY (Xh, Yh integer
+    linear forms) and C = den * P integer,
+      dX^D dY^D den P(X, Y) = sum_i Xh^i dX^(D-i) dY^i T_i,
+      T_i = dY^(D-i) Q_i(Y) = sum_j C_ij Yh^j dY^(D-i-j)."""
     if not P:
         return {}
+    import numpy as np
     deg = max(i + j for i, j in P)
-    xp = [{(0, 0): Fr(1)}]
-    yp = [{(0, 0): Fr(1)}]
-    for _ in range(deg):
-        xp.append(pmul(xp[-1], X))
-        yp.append(pmul(yp[-1], Y))
+    den = 1
+    for v in P.values():
+        den = _lcm(den, Fr(v).denominator)
+
+    def intlin(L):
+        a, b, c = Fr(L.get((1, 0), 0)), Fr(L.get((0, 1), 0)), Fr(L.get((0, 0), 0))
+        d = _lcm(_lcm(a.denominator, b.denominator), c.denominator)
+        return int(a * d), int(b * d), int(c * d), d
+
+    ax, bx, cx, dX = intlin(X)
+    ay, by, cy, dY = intlin(Y)
+    C = {k: int(Fr(v) * den) for k, v in P.items()}
+    acc = None
+    for i in range(deg, -1, -1):
+        m = deg - i
+        q = np.zeros((1, 1), dtype=object)
+        q[0, 0] = C.get((i, m), 0)
+        for j in range(m - 1, -1, -1):
+            q = _mul_lin_int(q, ay, by, cy)
+            q[0, 0] += C.get((i, j), 0) * dY ** (m - j)
+        w = dX ** (deg - i) * dY ** i
+        if acc is None:
+            acc = q * w
+        else:
+            acc = _mul_lin_int(acc, ax, bx, cx)
+            n = q.shape[0]
+            acc[:n, :n] += q * w
+    scale = den * dX ** deg * dY ** deg
     out = {}
-    for (i, j), v in P.items():
-        t = pmul(xp[i], yp[j])
-        for k, w in t.items():
-            out[k] = out.get(k, 0) + v * w
-    return {k: v for k, v in out.items() if v != 0}
+    n = acc.shape[0]
+    for i in range(n):
+        for j in range(n - i):
+            v = acc[i, j]
+            if v != 0:
+                out[(i, j)] = Fr(int(v), scale)
+    return out
 
 
 def peval(P, x, y):
@@ -130,9 +179,14 @@ def region_key(basis, x, y):
     return tuple(math.floor(nx * x + ny * y) for nx, ny in normals(basis))
 
 
+_REG_CACHE = {}
+
+
 def unit_regions(basis, n=400):
     """Distinct cells of the knot-line arrangement inside [0,1)^2, with a
     floating representative point (sample centroid) and a rational centre."""
+    if (basis, n) in _REG_CACHE:
+        return _REG_CACHE[(basis, n)]
     acc = {}
     for a in range(n):
         for b in range(n):
@@ -155,6 +209,7 @@ def unit_regions(basis, n=400):
         # GPU (fractional tap offsets are exact doubles, R17)
         rc = (Fr(0), Fr(0))
         regs.append({"key": k, "rep": (cx, cy), "centre": rc, "area": cnt / n / n})
+    _REG_CACHE[(basis, n)] = regs
     return regs
 
 
