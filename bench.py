@@ -166,7 +166,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--order", type=int, default=0)
     ap.add_argument("--impl", default="bsf")
-    ap.add_argument("--precision", default="dd", choices=["dd", "fp64"])
+    ap.add_argument("--precision", default="dd", choices=["dd", "fp64", "auto"])
     ap.add_argument("--anchor", default="global", choices=["global", "tile"])
     ap.add_argument("--ref-points", type=int, default=24)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
@@ -197,7 +197,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
 
-    prec = bsf.BSF_PREC_DD if args.precision == "dd" else bsf.BSF_PREC_FP64
+    prec = {"dd": bsf.BSF_PREC_DD, "fp64": bsf.BSF_PREC_FP64, "auto": bsf.BSF_PREC_AUTO}[args.precision]
     plan = bsf.Plan(w.width, w.height, batch=1, channels=1,
                     in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" else bsf.BSF_F32, out_dtype=bsf.BSF_F64,
                     order=w.order, basis=w.basis, max_sigma=w.max_sigma, precision=prec, device=local,
@@ -321,12 +321,14 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "width": w.width, "height": w.height, "order": w.order,
                        "basis": "dual" if w.basis == 2 else str(w.basis), "in_dtype": w.in_dtype,
-                       "precision": "double-double" if prec == bsf.BSF_PREC_DD else "fp64",
+                       "precision": {"dd": "double-double", "fp64": "fp64",
+                                     "auto": "fp64 + a-posteriori bound, double-double fallback"}[args.precision],
                        "anchor": args.anchor,
                        "l2": "flushed between steps (256 MB write, untimed)", "parallelism": "dp%d" % world},
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
-            "stats": {k: stats[k] for k in ("pixels", "clamped", "zero_scale", "theta_prime", "flags")}}
+            "stats": {k: stats[k] for k in ("pixels", "clamped", "zero_scale", "theta_prime", "flags",
+                                            "double_double")}}
     print(json.dumps(line))
     if pg:
         pg.destroy_process_group()

@@ -63,7 +63,9 @@ typedef enum {
 
 typedef enum {
     BSF_PREC_FP64 = 0,   /* fp64 taps and weights: fast, ill-conditioned for large images */
-    BSF_PREC_DD = 1      /* double-double taps, weights and accumulation (default)                             */
+    BSF_PREC_DD = 1,     /* double-double taps, weights and accumulation                                      */
+    BSF_PREC_AUTO = 2    /* fp64 with an a-posteriori error bound; pixels whose bound exceeds 1e-11 are        */
+                         /* recomputed in double-double                                */
 } bsf_precision;
 
 typedef enum {
@@ -104,6 +106,7 @@ typedef struct {
     long long zero_scale;    /* pixels with one scale treated as exactly zero (R5)  */
     long long theta_prime;   /* pixels filtered with basis Theta'                             */
     long long flags;         /* bit0 margin violation, bit1 infeasible, bit2 two zero scales  */
+    long long double_double; /* pixels computed (or recomputed) in double-double              */
 } bsf_stats;
 
 /* Create a plan: validates the descriptor, derives the margins, loads the
@@ -148,8 +151,10 @@ bsf_status bsf_filter_points(bsf_plan_t plan, const void *g_dev, const void *cov
                              int npts, double *out_dev, void *stream);
 
 /* As bsf_filter_points, also writing per-point diagnostics (for decision
- * parity with the oracle): aux_dev float64[8 * npts] =
- *   {basis, zero-scale direction (-1 none), clamped, flags, a'_1..a'_4}
+ * parity with the oracle): aux_dev float64[12 * npts] =
+ *   {basis, zero-scale direction (-1 none), clamped, flags, a'_1..a'_4,
+ *    computed in double-double (0/1), sum_j |c_j F_j| / |S|,
+ *    sum_j |c_j| sum_d |G_d| / |S| (fp64 paths; cancellation ratios), 0}
  * with a'_k = a_k / |s_k| the scale in lattice steps.                        */
 bsf_status bsf_filter_points_aux(bsf_plan_t plan, const void *g_dev, const void *cov_dev, const int *pts_dev,
                                  int npts, double *out_dev, double *aux_dev, void *stream);
@@ -158,7 +163,7 @@ bsf_status bsf_filter_points_aux(bsf_plan_t plan, const void *g_dev, const void 
  * size): each point's 16x16 tile is pre-integrated on its halo and the point
  * gathered; results are identical to those of bsf_run with BSF_ANCHOR_TILE.
  *   f_dev, cov_dev as bsf_run; pts_dev int32 (image, x, y) * npts;
- *   out_dev float64[npts]; aux_dev NULL or float64[8 * npts] (see _aux).    */
+ *   out_dev float64[npts]; aux_dev NULL or float64[12 * npts] (see _aux).    */
 bsf_status bsf_run_points(bsf_plan_t plan, const void *f_dev, const void *cov_dev, const int *pts_dev, int npts,
                           double *out_dev, double *aux_dev, void *stream);
 

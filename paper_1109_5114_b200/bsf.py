@@ -15,7 +15,7 @@ LUT_DIR = os.path.join(HERE, "lut")
 
 BSF_U8, BSF_F32, BSF_F64, BSF_I64, BSF_DD = 0, 1, 2, 3, 4
 BSF_THETA, BSF_THETA_PRIME, BSF_DUAL = 0, 1, 2
-BSF_PREC_FP64, BSF_PREC_DD = 0, 1
+BSF_PREC_FP64, BSF_PREC_DD, BSF_PREC_AUTO = 0, 1, 2
 BSF_ANCHOR_GLOBAL, BSF_ANCHOR_TILE = 0, 1
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "out of memory", 3: "CUDA error", 4: "infeasible covariance",
@@ -44,7 +44,8 @@ class bsf_geometry(ctypes.Structure):
 
 class bsf_stats(ctypes.Structure):
     _fields_ = [("pixels", ctypes.c_longlong), ("clamped", ctypes.c_longlong), ("zero_scale", ctypes.c_longlong),
-                ("theta_prime", ctypes.c_longlong), ("flags", ctypes.c_longlong)]
+                ("theta_prime", ctypes.c_longlong), ("flags", ctypes.c_longlong),
+                ("double_double", ctypes.c_longlong)]
 
 
 _lib = None

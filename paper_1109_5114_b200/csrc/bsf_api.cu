@@ -153,6 +153,9 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         CUDA_TRY(cudaMemcpy(d_coef, coef.data(), coef.size() * sizeof(double2), cudaMemcpyHostToDevice));
         for (uint32_t r = 0; r < nreg; ++r)
             for (int s2 = 0; s2 < counts[r]; ++s2) {
+                double sb = 0.0;
+                for (int m = 0; m < V.nmon; ++m) sb += fabs(coef[((size_t)r * V.nmax + s2) * V.nmon + m].x);
+                out->hornerB = sb > out->hornerB ? sb : out->hornerB;
                 int2 o = offs[(size_t)r * V.nmax + s2];
                 out->wxmin = o.x < out->wxmin ? o.x : out->wxmin;
                 out->wxmax = o.x > out->wxmax ? o.x : out->wxmax;
@@ -180,7 +183,8 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     if (d.order < 1 || d.order > 4) return set_err(BSF_EINVAL, "order must be 1..4");
     if (d.basis < BSF_THETA || d.basis > BSF_DUAL) return set_err(BSF_EINVAL, "bad basis");
     if (!(d.max_sigma > 0) || !isfinite(d.max_sigma)) return set_err(BSF_EINVAL, "max_sigma must be > 0");
-    if (d.precision != BSF_PREC_FP64 && d.precision != BSF_PREC_DD) return set_err(BSF_EINVAL, "bad precision");
+    if (d.precision != BSF_PREC_FP64 && d.precision != BSF_PREC_DD && d.precision != BSF_PREC_AUTO)
+        return set_err(BSF_EINVAL, "bad precision");
     if (d.margin_x < 0 || d.margin_y < 0) return set_err(BSF_EINVAL, "negative margin");
     if (d.anchor != BSF_ANCHOR_GLOBAL && d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EINVAL, "bad anchor");
     int disp = required_disp(d.max_sigma, d.order);
@@ -443,6 +447,7 @@ extern "C" bsf_status bsf_get_stats(bsf_plan_t p, bsf_stats *s, int reset) {
     s->zero_scale = (long long)h[2];
     s->theta_prime = (long long)h[3];
     s->flags = (long long)h[4];
+    s->double_double = (long long)h[5];
     if (reset) CUDA_TRY(cudaMemset(p->stats, 0, sizeof h));
     if (s->flags & FLAG_RANGE_H) return set_err(BSF_ERANGE, "a tap window left the pre-integration domain");
     if (s->flags & FLAG_INFEASIBLE_H) return set_err(BSF_EINFEASIBLE, "covariance outside the elongation bound");

@@ -8,6 +8,7 @@
 namespace bsf {
 
 constexpr int MAX_REG = 32;
+constexpr int BSF_AUX = 12;  // doubles of per-point diagnostics
 // device-side condition flags (also in bsf_pixel.cuh)
 enum { FLAG_RANGE_H = 1, FLAG_INFEASIBLE_H = 2, FLAG_TWO_ZERO_H = 4, FLAG_SOLVER_H = 8 };
 constexpr int NVAR = 5;  // full kernel + one per dropped direction
@@ -28,6 +29,7 @@ struct LutBasis {
     signed char table[81]; // mixed-radix key -> region (or -1)
     double2 centre[MAX_REG];
     int wxmin, wxmax, wymin, wymax;  // window offset extents over all variants
+    double hornerB;                  // max over all weights of sum_mu |c_mu| (Horner bound on [0,1]^2)
     LutVar var[NVAR];
 };
 
@@ -49,7 +51,7 @@ struct GatherArgs {
     const int *pts;         // optional (img, x, y) triples
     int npts;
     double *aux;            // optional per-point diagnostics [8 * npts]
-    unsigned long long *stats;  // [5]: pixels, clamped, zero, theta', flags(or)
+    unsigned long long *stats;  // [6]: pixels, clamped, zero, theta', flags(or), double-double
 };
 
 // Tile-anchored fused path: per 16x16 output tile, local running sums on the

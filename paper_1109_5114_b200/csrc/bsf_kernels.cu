@@ -404,7 +404,7 @@ __device__ __forceinline__ double2 load_gp(const GView &v, int qx, int qy, int d
 // large partial sum by TwoSum, all small terms in one fp64 accumulator.
 template <int R, bool DD>
 __device__ __forceinline__ dd interp(const GView &gv, const LutBasis &L, const LutVar &V, int bx, int by, double fx,
-                                     double fy, int drop, int2 sdrop, int *flags) {
+                                     double fy, int drop, int2 sdrop, int *flags, double *sumG) {
     int reg = classify(L, fx, fy);
     int n = __ldg(V.counts + reg);
     const int2 *offs = V.offs + reg * V.nmax;
@@ -442,7 +442,9 @@ __device__ __forceinline__ dd interp(const GView &gv, const LutBasis &L, const L
             accum(G, wh, wl);
         } else {
             double w = horner2_d(cf + (size_t)s * V.nmon, V.deg, fx, fy);
-            Fh = fma(G.x + G.y, w, Fh);
+            double g = G.x + G.y;
+            Fh = fma(g, w, Fh);
+            *sumG += fabs(g);
         }
     }
     return fast_two_sum(Fh, Fl);
@@ -454,8 +456,11 @@ __device__ __forceinline__ dd interp(const GView &gv, const LutBasis &L, const L
 #ifdef BSF_TAP_DUMP
 __device__ double *g_tap_dump;
 #endif
+// err (fp64 path only): a-posteriori estimate of |computed - exact| / |result|
+// (BSF_PREC_AUTO).
 template <int R, bool DD>
-__device__ double mesh(const GView &gv, const LutBasis &L, const PixelScales &ps, int x, int y, int *flags) {
+__device__ double mesh(const GView &gv, const LutBasis &L, const PixelScales &ps, int x, int y, int *flags,
+                       double *err = nullptr, double *ratios = nullptr) {
     int dirs[4];
     int ns = 0;
     for (int k = 0; k < 4; ++k)
@@ -466,6 +471,7 @@ __device__ double mesh(const GView &gv, const LutBasis &L, const PixelScales &ps
     int ntap = 1;
     for (int q = 0; q < ns; ++q) ntap *= (R + 1);
     dd acc = {0.0, 0.0};
+    double sumCG = 0.0, sumCF = 0.0;
     for (int t = 0; t < ntap; ++t) {
         int tt = t, coef = 1;
         double Dx = 0.0, Dy = 0.0;
@@ -480,7 +486,12 @@ __device__ double mesh(const GView &gv, const LutBasis &L, const PixelScales &ps
         }
         double flx = floor(Dx), fly = floor(Dy);
         double fx = Dx - flx, fy = Dy - fly;  // exact
-        dd F = interp<R, DD>(gv, L, V, x + (int)flx, y + (int)fly, fx, fy, ps.drop, sdrop, flags);
+        double sumG = 0.0;
+        dd F = interp<R, DD>(gv, L, V, x + (int)flx, y + (int)fly, fx, fy, ps.drop, sdrop, flags, &sumG);
+        if (!DD) {
+            sumCG += abs(coef) * sumG;
+            sumCF += fabs(coef * F.hi);
+        }
 #ifdef BSF_TAP_DUMP
         if (g_tap_dump && x == 0 && y == 23) {
             double *o = g_tap_dump + 8 * t;
@@ -494,7 +505,32 @@ __device__ double mesh(const GView &gv, const LutBasis &L, const PixelScales &ps
         double ia = 1.0 / ps.ap[dirs[q]];
         for (int i = 0; i < R; ++i) norm *= ia;
     }
-    return dd_to_d(acc) * norm;
+    double S = dd_to_d(acc);
+    if (!DD && err) {
+        // error estimate 4 u sum_j |c_j| sum_d |G_d| / |S|.  Calibrated on
+        // 200k config-2 pixels against double-double (profiles/
+        // r01_auto_calibration.md): the true fp64 error never exceeded
+        // 0.12 u sum|c||G| / |S|, so this estimate carries >= 30x headroom.
+        const double u = 1.1102230246251565e-16;
+        *err = 4.0 * u * sumCG / fabs(S);
+    }
+    if (!DD && ratios) {
+        ratios[0] = sumCF / fabs(S);
+        ratios[1] = sumCG / fabs(S);
+    }
+    return S * norm;
+}
+
+// BSF_PREC_AUTO: fp64 first; recompute in double-double when the estimate
+// exceeds 1e-9 (the fp64 results kept were within 1.6e-11 in calibration).
+template <int R>
+__device__ __forceinline__ double mesh_auto(const GView &gv, const LutBasis &L, const PixelScales &ps, int x, int y,
+                                            int *flags, int *used_dd, double *ratios = nullptr) {
+    double err = 1.0;
+    double v = mesh<R, false>(gv, L, ps, x, y, flags, &err, ratios);
+    *used_dd = !(err <= 1e-9);
+    if (*used_dd) v = mesh<R, true>(gv, L, ps, x, y, flags);
+    return v;
 }
 
 __device__ __forceinline__ void warp_count(unsigned long long *ctr, bool pred) {
@@ -504,7 +540,7 @@ __device__ __forceinline__ void warp_count(unsigned long long *ctr, bool pred) {
     if ((int)(threadIdx.x & 31) == leader && b) atomicAdd(ctr, (unsigned long long)__popc(b));
 }
 
-template <int R, bool DD>
+template <int R, int MODE>
 #ifndef BSF_GATHER_MINB
 #define BSF_GATHER_MINB 6
 #endif
@@ -533,20 +569,29 @@ __global__ void __launch_bounds__(128, BSF_GATHER_MINB) gather_kernel(GatherArgs
     pixel_scales(__ldg(cv), __ldg(cv + plane), __ldg(cv + 2 * plane), a.policy, a.clamp, R, ps);
     double res;
     int flags = ps.flags;
+    int used_dd = MODE == BSF_PREC_DD;
+    double ratios[2] = {0.0, 0.0};
     if (flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO)) {
         res = __longlong_as_double(0x7ff8000000000000LL);
     } else {
         int slot = geo.nbases == 2 ? ps.basis : 0;
         GView gv = {a.g + ((size_t)slot * geo.nimg + img) * geo.GH * geo.GW, -geo.P, 0, geo.GW, geo.GH};
-        res = mesh<R, DD>(gv, luts[ps.basis], ps, x, y, &flags);
+        if (MODE == BSF_PREC_AUTO)
+            res = mesh_auto<R>(gv, luts[ps.basis], ps, x, y, &flags, &used_dd, ratios);
+        else
+            res = mesh<R, MODE == BSF_PREC_DD>(gv, luts[ps.basis], ps, x, y, &flags, nullptr, ratios);
     }
     if (a.aux) {
-        double *ax = a.aux + 8 * oidx;
+        double *ax = a.aux + BSF_AUX * oidx;
         ax[0] = ps.basis;
         ax[1] = ps.drop;
         ax[2] = ps.clamped;
         ax[3] = flags;
         for (int k = 0; k < 4; ++k) ax[4 + k] = ps.ap[k];
+        ax[8] = used_dd;
+        ax[9] = ratios[0];
+        ax[10] = ratios[1];
+        ax[11] = 0.0;
     }
     if (a.out_f32)
         ((float *)a.out)[oidx] = (float)res;
@@ -557,6 +602,7 @@ __global__ void __launch_bounds__(128, BSF_GATHER_MINB) gather_kernel(GatherArgs
         warp_count(a.stats + 1, ps.clamped != 0);
         warp_count(a.stats + 2, ps.drop >= 0);
         warp_count(a.stats + 3, ps.basis == BASIS_THETA_PRIME);
+        warp_count(a.stats + 5, used_dd != 0);
         if (flags) atomicOr(a.stats + 4, (unsigned long long)flags);
     }
 }
@@ -613,7 +659,7 @@ __device__ __forceinline__ void tile_scan_level(double2 *__restrict__ G, int NX,
     }
 }
 
-template <int R, bool DD>
+template <int R, int MODE>
 #ifndef BSF_TILE_MINB
 #define BSF_TILE_MINB 3
 #endif
@@ -700,21 +746,64 @@ __global__ void __launch_bounds__(256, BSF_TILE_MINB) tile_kernel(TileArgs a, co
         __syncthreads();
         int flags = ps.flags | (s_bad ? FLAG_RANGE : 0);
         const bool mine = a.pts ? (tid == want) : valid;
-        if (mine) {
-            double res = __longlong_as_double(0x7ff8000000000000LL);
-            if (live && !s_bad) {
-                TileDomain d = tile_domain(luts[ps.basis], R, x0, y0, s_ex[ps.basis], s_ey[ps.basis]);
-                GView gv = {scr + (size_t)ps.basis * a.cap, d.X0, d.Y0, d.NX, d.NY};
-                res = mesh<R, DD>(gv, luts[ps.basis], ps, x, y, &flags);
+        double res = __longlong_as_double(0x7ff8000000000000LL);
+        int used_dd = MODE == BSF_PREC_DD;
+        double ratios[2] = {0.0, 0.0};
+        if (mine && live && !s_bad) {
+            TileDomain d = tile_domain(luts[ps.basis], R, x0, y0, s_ex[ps.basis], s_ey[ps.basis]);
+            GView gv = {scr + (size_t)ps.basis * a.cap, d.X0, d.Y0, d.NX, d.NY};
+            if (MODE == BSF_PREC_AUTO) {
+                double err = 1.0;
+                res = mesh<R, false>(gv, luts[ps.basis], ps, x, y, &flags, &err, ratios);
+                used_dd = !(err <= 1e-9);
+            } else {
+                res = mesh<R, MODE == BSF_PREC_DD>(gv, luts[ps.basis], ps, x, y, &flags, nullptr, ratios);
             }
+        }
+        if (MODE == BSF_PREC_AUTO) {
+            // recompute the rejected pixels in double-double, packed densely
+            // onto the first threads so warps do not run it with idle lanes
+            __shared__ int s_nrej;
+            __shared__ short s_rej[256];
+            __shared__ PixelScales s_ps[256];
+            __shared__ double s_res[256];
+            __shared__ int s_flags[256];
+            if (tid == 0) s_nrej = 0;
+            __syncthreads();
+            if (used_dd && mine && live && !s_bad) {
+                int k = atomicAdd(&s_nrej, 1);
+                s_rej[k] = (short)tid;
+                s_ps[tid] = ps;
+            }
+            __syncthreads();
+            if (tid < s_nrej) {
+                int src = s_rej[tid];
+                PixelScales q = s_ps[src];
+                int qx = x0 + (src % TILE), qy = y0 + src / TILE, qf = 0;
+                TileDomain d = tile_domain(luts[q.basis], R, x0, y0, s_ex[q.basis], s_ey[q.basis]);
+                GView gv = {scr + (size_t)q.basis * a.cap, d.X0, d.Y0, d.NX, d.NY};
+                s_res[src] = mesh<R, true>(gv, luts[q.basis], q, qx, qy, &qf);
+                s_flags[src] = qf;
+            }
+            __syncthreads();
+            if (used_dd && mine && live && !s_bad) {
+                res = s_res[tid];
+                flags |= s_flags[tid];
+            }
+        }
+        if (mine) {
             long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
             if (a.aux) {
-                double *ax = a.aux + 8 * oidx;
+                double *ax = a.aux + BSF_AUX * oidx;
                 ax[0] = ps.basis;
                 ax[1] = ps.drop;
                 ax[2] = ps.clamped;
                 ax[3] = flags;
                 for (int k = 0; k < 4; ++k) ax[4 + k] = ps.ap[k];
+                ax[8] = used_dd;
+                ax[9] = ratios[0];
+                ax[10] = ratios[1];
+                ax[11] = 0.0;
             }
             if (a.out_f32 && !a.pts)
                 ((float *)a.out)[oidx] = (float)res;
@@ -725,6 +814,7 @@ __global__ void __launch_bounds__(256, BSF_TILE_MINB) tile_kernel(TileArgs a, co
                 if (ps.clamped) atomicAdd(a.stats + 1, 1ull);
                 if (ps.drop >= 0) atomicAdd(a.stats + 2, 1ull);
                 if (ps.basis == BASIS_THETA_PRIME) atomicAdd(a.stats + 3, 1ull);
+                if (used_dd) atomicAdd(a.stats + 5, 1ull);
                 if (flags) atomicOr(a.stats + 4, (unsigned long long)flags);
             }
         }
@@ -754,9 +844,11 @@ int tile_slots() {
 template <int R>
 static void launch_tile_r(const TileArgs &a, int prec, int slots, cudaStream_t st, const LutBasis *luts) {
     if (prec == BSF_PREC_DD)
-        tile_kernel<R, true><<<slots, 256, 0, st>>>(a, luts);
+        tile_kernel<R, BSF_PREC_DD><<<slots, 256, 0, st>>>(a, luts);
+    else if (prec == BSF_PREC_AUTO)
+        tile_kernel<R, BSF_PREC_AUTO><<<slots, 256, 0, st>>>(a, luts);
     else
-        tile_kernel<R, false><<<slots, 256, 0, st>>>(a, luts);
+        tile_kernel<R, BSF_PREC_FP64><<<slots, 256, 0, st>>>(a, luts);
 }
 
 cudaError_t launch_tile_impl(const TileArgs &a, int order, int prec, int slots, cudaStream_t st,
@@ -781,9 +873,11 @@ static void launch_r(const GatherArgs &a, int prec, cudaStream_t st, const LutBa
     else
         grid = dim3((a.geo.W + 15) / 16, (a.geo.H + 7) / 8, a.geo.nimg);
     if (prec == BSF_PREC_DD)
-        gather_kernel<R, true><<<grid, block, 0, st>>>(a, luts);
+        gather_kernel<R, BSF_PREC_DD><<<grid, block, 0, st>>>(a, luts);
+    else if (prec == BSF_PREC_AUTO)
+        gather_kernel<R, BSF_PREC_AUTO><<<grid, block, 0, st>>>(a, luts);
     else
-        gather_kernel<R, false><<<grid, block, 0, st>>>(a, luts);
+        gather_kernel<R, BSF_PREC_FP64><<<grid, block, 0, st>>>(a, luts);
 }
 
 #ifdef BSF_TAP_DUMP

@@ -46,10 +46,10 @@ def gpu_points(plan: bsf.Plan, img: torch.Tensor, cov: torch.Tensor, pts: torch.
 def tile_points(plan: bsf.Plan, img: torch.Tensor, cov: torch.Tensor, pts: torch.Tensor, aux=False):
     dev = torch.device("cuda:0")
     out = torch.empty(pts.shape[0], dtype=torch.float64, device=dev)
-    ax = torch.empty(pts.shape[0] * 8, dtype=torch.float64, device=dev) if aux else None
+    ax = torch.empty(pts.shape[0] * 12, dtype=torch.float64, device=dev) if aux else None
     plan.run_points(img.to(dev).contiguous(), cov.to(dev).contiguous(), pts.to(dev).contiguous(), out, ax)
     torch.cuda.synchronize()
-    return (out.cpu(), ax.cpu().view(-1, 8)) if aux else out.cpu()
+    return (out.cpu(), ax.cpu().view(-1, 12)) if aux else out.cpu()
 
 
 def oracle_points(img: np.ndarray, cov: np.ndarray, xs, ys, *, policy, r, clamp=1, nthreads=0):

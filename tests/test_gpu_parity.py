@@ -98,15 +98,16 @@ def _small_smooth(H, W, smax, seed=7):
     return w, img, cov
 
 
+@pytest.mark.parametrize("precision", [bsf.BSF_PREC_DD, bsf.BSF_PREC_AUTO])
 @pytest.mark.parametrize("policy", [0, 1, 2])
 @pytest.mark.parametrize("r", [1, 2])
-def test_filter_small_ragged_all_pixels(policy, r):
+def test_filter_small_ragged_all_pixels(policy, r, precision):
     """Ragged size (not a multiple of the 16x8 tile), space-variant field
     spanning isotropic to elongation 6, all orientations, zero scales and the
     clamp: every pixel."""
     H, W = 45, 53
     w, img, cov = _small_smooth(H, W, 3.0)
-    plan = make_plan(w, policy=policy, order=r)
+    plan = make_plan(w, policy=policy, order=r, precision=precision)
     out = gpu_full(plan, img, cov)[0].numpy()
     ys, xs = np.mgrid[0:H, 0:W]
     ref, bas, cl, sc = oracle_points(img.numpy(), cov.numpy(), xs.ravel(), ys.ravel(), policy=policy, r=r)
@@ -168,10 +169,11 @@ def test_reject_mode_flags_infeasible():
 # ---------------------------------------------------------------------------
 # full-size configs: sampled outputs in the launch configuration bench times
 # ---------------------------------------------------------------------------
-def test_config2_full_size_sampled():
+@pytest.mark.parametrize("precision", [bsf.BSF_PREC_DD, bsf.BSF_PREC_AUTO])
+def test_config2_full_size_sampled(precision):
     w = synth.workload(2)
     img, cov = synth.make_image(w), synth.make_cov(w)
-    plan = make_plan(w)
+    plan = make_plan(w, precision=precision)
     out = gpu_full(plan, img, cov)[0]
     pts = synth.sample_points(w, 160, seed=2)
     xs, ys = pts[:, 1].numpy(), pts[:, 2].numpy()

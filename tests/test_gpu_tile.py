@@ -29,12 +29,13 @@ def test_tile_c1_all_pixels(policy):
     assert st["pixels"] == w.width * w.height and st["flags"] == 0
 
 
+@pytest.mark.parametrize("precision", [bsf.BSF_PREC_DD, bsf.BSF_PREC_AUTO])
 @pytest.mark.parametrize("policy", [0, 1, 2])
 @pytest.mark.parametrize("r", [1, 2])
-def test_tile_small_ragged_all_pixels(policy, r):
+def test_tile_small_ragged_all_pixels(policy, r, precision):
     H, W = 45, 53
     w, img, cov = _small_smooth(H, W, 3.0)
-    plan = make_plan(w, policy=policy, order=r, anchor=TILE)
+    plan = make_plan(w, policy=policy, order=r, anchor=TILE, precision=precision)
     out = gpu_full(plan, img, cov)[0].numpy()
     ys, xs = np.mgrid[0:H, 0:W]
     ref, *_ = oracle_points(img.numpy(), cov.numpy(), xs.ravel(), ys.ravel(), policy=policy, r=r)
@@ -69,10 +70,11 @@ def test_tile_batch_channels_f32_out():
         assert max_rel(out[i].ravel(), ref) <= 1e-4
 
 
-def test_tile_config2_full_size_sampled():
+@pytest.mark.parametrize("precision", [bsf.BSF_PREC_DD, bsf.BSF_PREC_AUTO])
+def test_tile_config2_full_size_sampled(precision):
     w = synth.workload(2)
     img, cov = synth.make_image(w), synth.make_cov(w)
-    plan = make_plan(w, anchor=TILE)
+    plan = make_plan(w, anchor=TILE, precision=precision)
     out = gpu_full(plan, img, cov)[0]
     pts = synth.sample_points(w, 160, seed=2)
     xs, ys = pts[:, 1].numpy(), pts[:, 2].numpy()
