@@ -41,6 +41,7 @@ struct bsf_plan_s {
     double2 *tile_scratch = nullptr;
     size_t tile_cap = 0;
     int tile_nslots = 0;
+    bool fused = false;
     int *tile_counter = nullptr;
     long long nlaunch = 0;
     cudaStream_t last = nullptr;
@@ -79,7 +80,8 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         return true;
     };
     uint32_t hdr[5], nreg;
-    if (!take(hdr, sizeof hdr) || hdr[0] != 0x4C465342u || (int)hdr[2] != basis || (int)hdr[3] != p->d.order ||
+    if (!take(hdr, sizeof hdr) || hdr[0] != 0x4C465342u || hdr[1] != 2u || (int)hdr[2] != basis ||
+        (int)hdr[3] != p->d.order ||
         hdr[4] != NVAR || !take(&nreg, 4) || nreg > MAX_REG)
         return set_err(BSF_EINVAL, "bad table header " + std::string(path));
     memset(out, 0, sizeof *out);
@@ -128,29 +130,65 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         V.deg = hv[1];
         V.nmon = hv[2];
         V.nmax = hv[3];
+        uint64_t Lden;
+        if (!take(&Lden, 8) || Lden == 0 || Lden >= (1ull << 53)) return set_err(BSF_EINVAL, "bad denominator");
+        const double L = (double)Lden;
         std::vector<int> counts(nreg);
         std::vector<int2> offs((size_t)nreg * V.nmax);
-        std::vector<double2> coef((size_t)nreg * V.nmax * V.nmon);
+        std::vector<double> num((size_t)nreg * V.nmax * V.nmon);
         for (uint32_t r = 0; r < nreg; ++r) {
             take(&counts[r], 4);
             for (int s = 0; s < V.nmax; ++s) {
                 int o[2];
                 take(o, 8);
                 offs[(size_t)r * V.nmax + s] = make_int2(o[0], o[1]);
-                if (!take(&coef[((size_t)r * V.nmax + s) * V.nmon], 16 * (size_t)V.nmon))
+                if (!take(&num[((size_t)r * V.nmax + s) * V.nmon], 8 * (size_t)V.nmon))
                     return set_err(BSF_EINVAL, "truncated table");
             }
         }
-        void *d_counts, *d_offs, *d_coef;
+        // double-double coefficients n / L, correctly rounded: hi = fl(n/L);
+        // n - hi*L is exact in one fma (it is a multiple of ulp(hi) below L*ulp(hi)),
+        // lo = fl((n - hi*L)/L).
+        std::vector<double2> coef(num.size());
+        for (size_t i = 0; i < num.size(); ++i) {
+            double hi = num[i] / L;
+            double rem = fma(-hi, L, num[i]);
+            coef[i] = make_double2(hi, rem / L);
+        }
+        // integer table for the exact split contraction in the padded chunk layout
+        V.nmonp = bsf_chunk_off(V.deg, -1);
+        std::vector<double> nump((size_t)nreg * V.nmax * V.nmonp, 0.0);
+        for (int ihi = V.deg; ihi >= 0; ihi = bsf_chunk_lo(V.deg, ihi) - 1) {
+            int m0 = bsf_row_start(V.deg, ihi), n = bsf_chunk_len(V.deg, ihi), o = bsf_chunk_off(V.deg, ihi);
+            for (size_t rs = 0; rs < (size_t)nreg * V.nmax; ++rs)
+                for (int m = 0; m < n; ++m) nump[rs * V.nmonp + o + m] = num[rs * V.nmon + m0 + m];
+        }
+        double colmax = 0.0;  // max over (region, monomial) of sum_s |n|
+        for (uint32_t r = 0; r < nreg; ++r)
+            for (int m = 0; m < V.nmon; ++m) {
+                double cs = 0.0;
+                for (int s = 0; s < V.nmax; ++s) cs += fabs(num[((size_t)r * V.nmax + s) * V.nmon + m]);
+                colmax = cs > colmax ? cs : colmax;
+            }
+        // sums of G1 * n stay exact while |G1| sum|n| <= 2^53
+        int cm = 0;
+        while (ldexp(1.0, cm) < colmax) ++cm;
+        V.kbits = 53 - cm;
+        V.L = L;
+        void *d_counts, *d_offs, *d_coef, *d_num;
         CUDA_TRY(cudaMalloc(&d_counts, counts.size() * sizeof(int)));
         p->dev_allocs.push_back(d_counts);
         CUDA_TRY(cudaMalloc(&d_offs, offs.size() * sizeof(int2)));
         p->dev_allocs.push_back(d_offs);
         CUDA_TRY(cudaMalloc(&d_coef, coef.size() * sizeof(double2)));
         p->dev_allocs.push_back(d_coef);
+        CUDA_TRY(cudaMalloc(&d_num, nump.size() * sizeof(double)));
+        p->dev_allocs.push_back(d_num);
         CUDA_TRY(cudaMemcpy(d_counts, counts.data(), counts.size() * sizeof(int), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(d_offs, offs.data(), offs.size() * sizeof(int2), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(d_coef, coef.data(), coef.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(d_num, nump.data(), nump.size() * sizeof(double), cudaMemcpyHostToDevice));
+        V.num = (const double *)d_num;
         for (uint32_t r = 0; r < nreg; ++r)
             for (int s2 = 0; s2 < counts[r]; ++s2) {
                 double sb = 0.0;
@@ -330,13 +368,30 @@ extern "C" bsf_status bsf_filter_points_aux(bsf_plan_t p, const void *g, const v
     return BSF_OK;
 }
 
+// The exact split contraction (bsf_fused.cuh) serves the tile path whenever
+// every table in use keeps an exact limb of >= KBITS_MIN bits; otherwise (and
+// for BSF_PREC_FP64, or BSF_FUSED=0 in the environment) the per-thread
+// double-double tile kernel runs.
+static bool use_fused(const bsf_plan_s *p) {
+    if (p->d.precision == BSF_PREC_FP64) return false;
+    const char *env = getenv("BSF_FUSED");
+    if (env && env[0] == '0') return false;
+    for (int b = 0; b < 2; ++b) {
+        if (!(p->d.basis == BSF_DUAL || p->d.basis == b)) continue;
+        for (int v = 0; v < NVAR; ++v)
+            if (p->host_luts[b].var[v].kbits < KBITS_MIN) return false;
+    }
+    return true;
+}
+
 static bsf_status ensure_tile_ws(bsf_plan_s *p) {
     if (p->tile_scratch) return BSF_OK;
     int mask = p->d.basis == BSF_DUAL ? 3 : (1 << p->d.basis);
     p->tile_cap = tile_capacity(p->d.order, p->d.max_sigma, p->host_luts, mask);
-    p->tile_nslots = tile_slots();
+    p->fused = use_fused(p);
+    p->tile_nslots = p->fused ? fused_slots() : tile_slots();
     void *q;
-    size_t bytes = (size_t)p->tile_nslots * 2 * p->tile_cap * sizeof(double2);
+    size_t bytes = (size_t)p->tile_nslots * (p->fused ? NPLANE_MAX : 2) * p->tile_cap * sizeof(double2);
     if (cudaMalloc(&q, bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "tile scratch " + std::to_string(bytes));
     p->dev_allocs.push_back(q);
     p->tile_scratch = (double2 *)q;
@@ -369,6 +424,11 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     return a;
 }
 
+static cudaError_t launch_tile(bsf_plan_s *p, const TileArgs &a, cudaStream_t st) {
+    if (p->fused) return launch_fused_impl(a, p->d.order, p->tile_nslots, st, p->luts_dev, &p->nlaunch);
+    return launch_tile_impl(a, p->d.order, p->d.precision, p->tile_nslots, st, p->luts_dev, &p->nlaunch);
+}
+
 extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *cov, const int *pts, int npts,
                                      double *out, double *aux, void *stream) {
     if (!p || !f || !cov || !out || (!pts && npts)) return set_err(BSF_EINVAL, "null argument");
@@ -383,7 +443,7 @@ extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *co
     a.npts = npts;
     a.aux = aux;
     a.out_f32 = 0;
-    CUDA_TRY(launch_tile_impl(a, p->d.order, p->d.precision, p->tile_nslots, st, p->luts_dev, &p->nlaunch));
+    CUDA_TRY(launch_tile(p, a, st));
     return BSF_OK;
 }
 
@@ -396,7 +456,7 @@ extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void
         cudaStream_t st = (cudaStream_t)stream;
         p->last = st;
         TileArgs a = tile_args(p, f, cov, out);
-        CUDA_TRY(launch_tile_impl(a, p->d.order, p->d.precision, p->tile_nslots, st, p->luts_dev, &p->nlaunch));
+        CUDA_TRY(launch_tile(p, a, st));
         return BSF_OK;
     }
     if (!p->g_ws) {

@@ -880,6 +880,8 @@ static void launch_r(const GatherArgs &a, int prec, cudaStream_t st, const LutBa
         gather_kernel<R, BSF_PREC_FP64><<<grid, block, 0, st>>>(a, luts);
 }
 
+#include "bsf_fused.cuh"
+
 #ifdef BSF_TAP_DUMP
 extern "C" void bsf_debug_set_dump(double *p) { cudaMemcpyToSymbol(g_tap_dump, &p, sizeof p); }
 #endif

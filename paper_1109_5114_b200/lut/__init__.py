@@ -25,7 +25,18 @@ def ensure(basis: int, r: int) -> str:
     return p
 
 
+def _dd_of_ratio(n: np.ndarray, L: int):
+    """Correctly rounded double-double of n / L (n exact integers in float64)."""
+    from fractions import Fraction as Fr
+    hi = n / float(L)
+    lo = np.zeros_like(hi)
+    for idx in zip(*np.nonzero(n)):
+        lo[idx] = float(Fr(int(n[idx]), L) - Fr(float(hi[idx])))
+    return hi, lo
+
+
 def load(basis: int, r: int):
+    """Parse a version-2 table: coefficients n / L with integer numerators."""
     with open(ensure(basis, r), "rb") as fh:
         buf = fh.read()
     off = 0
@@ -37,7 +48,7 @@ def load(basis: int, r: int):
         return v
 
     magic, ver, b, rr, nvar = take("<IIIII")
-    assert magic == 0x4C465342 and b == basis and rr == r
+    assert magic == 0x4C465342 and ver == 2 and b == basis and rr == r
     (nreg,) = take("<I")
     normals = [take("<ii") for _ in range(4)]
     keys, centres = [], []
@@ -47,15 +58,19 @@ def load(basis: int, r: int):
     variants = []
     for _ in range(nvar):
         drop, deg, nmon, nmax = take("<iiii")
+        (L,) = take("<Q")
         counts = np.zeros(nreg, dtype=np.int32)
         offs = np.zeros((nreg, nmax, 2), dtype=np.int32)
-        coef = np.zeros((nreg, nmax, nmon, 2))
+        num = np.zeros((nreg, nmax, nmon))
         for ri in range(nreg):
             (counts[ri],) = take("<i")
             for s in range(nmax):
                 offs[ri, s] = take("<ii")
-                coef[ri, s] = np.array(take("<%dd" % (2 * nmon))).reshape(nmon, 2)
-        variants.append(dict(drop=drop, deg=deg, nmon=nmon, nmax=nmax, counts=counts, offs=offs, coef=coef))
+                num[ri, s] = np.array(take("<%dd" % nmon))
+        hi, lo = _dd_of_ratio(num, L)
+        coef = np.stack([hi, lo], axis=-1)
+        variants.append(dict(drop=drop, deg=deg, nmon=nmon, nmax=nmax, counts=counts, offs=offs, coef=coef,
+                             num=num, L=L))
     return dict(basis=basis, r=r, normals=normals, keys=keys, centres=np.array(centres), variants=variants)
 
 

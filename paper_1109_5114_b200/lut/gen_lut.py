@@ -401,13 +401,32 @@ def monomials(deg):
 
 
 MAGIC = 0x4C465342  # 'BSFL'
+VERSION = 2
+
+
+def integer_table(table, nmon_list):
+    """Common denominator L and integer numerators n = L * c of every
+    coefficient of one variant (the GPU contracts with the integers exactly,
+    DESIGN.md "Exact split contraction")."""
+    L = 1
+    for win in table:
+        for _, poly in win:
+            for v in poly.values():
+                L = _lcm(L, Fr(v).denominator)
+    return L
 
 
 def write_bin(path, basis, r, variants):
-    """variants: list of (drop, deg, table, regs)."""
+    """variants: list of (drop, deg, table, regs).
+
+    Version 2 layout (little endian): header MAGIC, 2, basis, r, nvar; nreg;
+    4 knot-line normals; per region key[4] and centre[2]; per variant
+    (drop, deg, nmon, nmax), L (uint64, common denominator), then per region
+    count and per window slot (dx, dy) and nmon numerators n (float64, exact
+    integers |n| < 2^53): coefficient = n / L."""
     regs = variants[0][3]
     out = bytearray()
-    out += struct.pack("<IIIII", MAGIC, 1, basis, r, len(variants))
+    out += struct.pack("<IIIII", MAGIC, VERSION, basis, r, len(variants))
     nreg = len(regs)
     out += struct.pack("<I", nreg)
     nrm = normals(basis)
@@ -419,7 +438,10 @@ def write_bin(path, basis, r, variants):
     for drop, deg, table, _ in variants:
         mons = monomials(deg)
         nmax = max(len(w) for w in table)
+        L = integer_table(table, len(mons))
+        assert L < 2**53
         out += struct.pack("<iiii", -1 if drop is None else drop, deg, len(mons), nmax)
+        out += struct.pack("<Q", L)
         for win in table:
             out += struct.pack("<i", len(win))
             for slot in range(nmax):
@@ -429,10 +451,67 @@ def write_bin(path, basis, r, variants):
                     (dx, dy), poly = (0, 0), {}
                 out += struct.pack("<ii", dx, dy)
                 for (i, j) in mons:
-                    hi, lo = to_dd(poly.get((i, j), Fr(0)))
-                    out += struct.pack("<dd", hi, lo)
+                    n = poly.get((i, j), Fr(0)) * L
+                    assert n.denominator == 1 and abs(n.numerator) < 2**53
+                    out += struct.pack("<d", float(n.numerator))
     with open(path, "wb") as fh:
         fh.write(out)
+
+
+def upgrade_v1(path):
+    """Rewrite a version-1 table (double-double coefficients) as version 2.
+
+    Each coefficient is a rational with denominator < 2^50; it is recovered
+    exactly from its 106-bit double-double value (continued fractions), and
+    the recovered value is checked against the stored pair."""
+    buf = open(path, "rb").read()
+    off = 0
+
+    def take(fmt):
+        nonlocal off
+        v = struct.unpack_from(fmt, buf, off)
+        off += struct.calcsize(fmt)
+        return v
+
+    magic, ver, basis, r, nvar = take("<IIIII")
+    assert magic == MAGIC and ver == 1, (path, ver)
+    (nreg,) = take("<I")
+    nrm = [take("<ii") for _ in range(4)]
+    regs = []
+    for _ in range(nreg):
+        key = take("<4i")
+        c = take("<dd")
+        regs.append({"key": key, "centre": c})
+    variants = []
+    for _ in range(nvar):
+        drop, deg, nmon, nmax = take("<iiii")
+        mons = monomials(deg)
+        assert len(mons) == nmon
+        table = []
+        for _ in range(nreg):
+            (cnt,) = take("<i")
+            win = []
+            for s in range(nmax):
+                d = take("<ii")
+                vals = take("<%dd" % (2 * nmon))
+                if s >= cnt:
+                    continue
+                poly = {}
+                for m, (i, j) in enumerate(mons):
+                    hi, lo = vals[2 * m], vals[2 * m + 1]
+                    if hi == 0.0 and lo == 0.0:
+                        continue
+                    exact = Fr(hi) + Fr(lo)
+                    f = exact.limit_denominator(2**50)
+                    assert abs(f - exact) <= abs(exact) * Fr(1, 2**100), (path, f, exact)
+                    assert to_dd(f) == (hi, lo), (path, f)
+                    poly[(i, j)] = f
+                win.append((d, poly))
+            table.append(win)
+        variants.append((None if drop < 0 else drop, deg, table, regs))
+    assert off == len(buf)
+    assert [tuple(v) for v in nrm] == [tuple(v) for v in normals(basis)]
+    write_bin(path, basis, r, variants)
 
 
 def generate(basis, r, outdir):
@@ -447,6 +526,11 @@ def generate(basis, r, outdir):
 
 if __name__ == "__main__":
     outdir = os.path.dirname(os.path.abspath(__file__))
+    if sys.argv[1:2] == ["upgrade"]:
+        for p in sys.argv[2:]:
+            upgrade_v1(p)
+            print("upgraded", p)
+        sys.exit(0)
     orders = [int(a) for a in sys.argv[1:]] or [1, 2]
     for r in orders:
         for basis in (0, 1):
