@@ -183,6 +183,16 @@ bsf_status bsf_get_stats(bsf_plan_t plan, bsf_stats *stats, int reset);
 /* Number of library kernels launched through this plan since creation. */
 long long bsf_launch_count(bsf_plan_t plan);
 
+/* Diagnostics.  bsf_debug_phase_cycles: the first call enables per-phase
+ * cycle counters in the tile path (adds one clock read per phase per tile);
+ * later calls copy the 8 counters (SM cycles summed over tiles: scales,
+ * pre-integration, exact split, sort, gather, accumulation) to host `out`
+ * (may be NULL) after synchronising the plan's last stream, and zero them when
+ * `reset`.  bsf_uses_fused: 1 when the tile path runs the exact split
+ * contraction kernel (known after the first tile-path call), else 0.        */
+bsf_status bsf_debug_phase_cycles(bsf_plan_t plan, unsigned long long *out, int reset);
+int bsf_uses_fused(bsf_plan_t plan);
+
 const char *bsf_status_str(bsf_status s);
 const char *bsf_last_error(void);
 int bsf_version(void);

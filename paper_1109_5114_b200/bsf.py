@@ -84,6 +84,10 @@ def lib():
         L.bsf_get_stats.argtypes = [vp, ctypes.POINTER(bsf_stats), i]
         L.bsf_launch_count.restype = ctypes.c_longlong
         L.bsf_launch_count.argtypes = [vp]
+        L.bsf_debug_phase_cycles.restype = st
+        L.bsf_debug_phase_cycles.argtypes = [vp, vp, i]
+        L.bsf_uses_fused.restype = i
+        L.bsf_uses_fused.argtypes = [vp]
         L.bsf_status_str.restype = ctypes.c_char_p
         L.bsf_status_str.argtypes = [st]
         L.bsf_last_error.restype = ctypes.c_char_p
@@ -189,6 +193,15 @@ class Plan:
         d = {k: getattr(s, k) for k, _ in bsf_stats._fields_}
         d["status"] = st
         return d
+
+    def phase_cycles(self, reset=False):
+        """Per-phase SM cycles of the fused tile kernel (enables counting on first call)."""
+        buf = (ctypes.c_ulonglong * 8)()
+        _check(lib().bsf_debug_phase_cycles(self.handle, buf, int(reset)))
+        return list(buf)
+
+    def uses_fused(self):
+        return bool(lib().bsf_uses_fused(self.handle))
 
     def launch_count(self):
         return lib().bsf_launch_count(self.handle)

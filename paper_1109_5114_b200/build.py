@@ -1,14 +1,15 @@
 """Build libbsf.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = [os.path.join(HERE, "csrc", f) for f in ("bsf_api.cu", "bsf_kernels.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("bsf_dd.cuh", "bsf_pixel.cuh", "bsf_internal.h")] + [
-    os.path.join(os.path.dirname(HERE), "include", "bsf.h")]
+DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*"))) + [os.path.join(os.path.dirname(HERE), "include", "bsf.h"),
+                                                             os.path.abspath(__file__)]
 OUT = os.path.join(HERE, "libbsf.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -42,6 +42,7 @@ struct bsf_plan_s {
     size_t tile_cap = 0;
     int tile_nslots = 0;
     bool fused = false;
+    unsigned long long *prof = nullptr;  // phase cycles of the fused kernel (diagnostics)
     int *tile_counter = nullptr;
     long long nlaunch = 0;
     cudaStream_t last = nullptr;
@@ -134,7 +135,7 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         if (!take(&Lden, 8) || Lden == 0 || Lden >= (1ull << 53)) return set_err(BSF_EINVAL, "bad denominator");
         const double L = (double)Lden;
         std::vector<int> counts(nreg);
-        std::vector<int2> offs((size_t)nreg * V.nmax);
+        std::vector<int2> offs((size_t)nreg * V.nmax, make_int2(0, 0));
         std::vector<double> num((size_t)nreg * V.nmax * V.nmon);
         for (uint32_t r = 0; r < nreg; ++r) {
             take(&counts[r], 4);
@@ -155,14 +156,20 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
             double rem = fma(-hi, L, num[i]);
             coef[i] = make_double2(hi, rem / L);
         }
-        // integer table for the exact split contraction in the padded chunk layout
-        V.nmonp = bsf_chunk_off(V.deg, -1);
-        std::vector<double> nump((size_t)nreg * V.nmax * V.nmonp, 0.0);
-        for (int ihi = V.deg; ihi >= 0; ihi = bsf_chunk_lo(V.deg, ihi) - 1) {
-            int m0 = bsf_row_start(V.deg, ihi), n = bsf_chunk_len(V.deg, ihi), o = bsf_chunk_off(V.deg, ihi);
-            for (size_t rs = 0; rs < (size_t)nreg * V.nmax; ++rs)
-                for (int m = 0; m < n; ++m) nump[rs * V.nmonp + o + m] = num[rs * V.nmon + m0 + m];
-        }
+        // integer table for the exact split contraction (bsf_fused.cuh, FP64
+        // tensor-core fragments): per region nslot4 = nmax rounded up to 4 window
+        // slots, per slot nmonp = nmon rounded up to 8 monomials (zero padded),
+        // monomials in the gen_lut order; offsets padded alike with (0, 0).
+        V.nmonp = (V.nmon + 7) & ~7;
+        V.nslot4 = (V.nmax + 3) & ~3;
+        std::vector<double> nump((size_t)nreg * V.nslot4 * V.nmonp, 0.0);
+        std::vector<int2> offs4((size_t)nreg * V.nslot4, make_int2(0, 0));
+        for (uint32_t r = 0; r < nreg; ++r)
+            for (int sl = 0; sl < V.nmax; ++sl) {
+                offs4[(size_t)r * V.nslot4 + sl] = offs[(size_t)r * V.nmax + sl];
+                for (int m = 0; m < V.nmon; ++m)
+                    nump[((size_t)r * V.nslot4 + sl) * V.nmonp + m] = num[((size_t)r * V.nmax + sl) * V.nmon + m];
+            }
         double colmax = 0.0;  // max over (region, monomial) of sum_s |n|
         for (uint32_t r = 0; r < nreg; ++r)
             for (int m = 0; m < V.nmon; ++m) {
@@ -175,7 +182,11 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         while (ldexp(1.0, cm) < colmax) ++cm;
         V.kbits = 53 - cm;
         V.L = L;
-        void *d_counts, *d_offs, *d_coef, *d_num;
+        void *d_counts, *d_offs, *d_coef, *d_num, *d_offs4;
+        CUDA_TRY(cudaMalloc(&d_offs4, offs4.size() * sizeof(int2)));
+        p->dev_allocs.push_back(d_offs4);
+        CUDA_TRY(cudaMemcpy(d_offs4, offs4.data(), offs4.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        V.offs4 = (const int2 *)d_offs4;
         CUDA_TRY(cudaMalloc(&d_counts, counts.size() * sizeof(int)));
         p->dev_allocs.push_back(d_counts);
         CUDA_TRY(cudaMalloc(&d_offs, offs.size() * sizeof(int2)));
@@ -421,6 +432,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.ntx = (p->geo.W + TILE - 1) / TILE;
     a.nty = (p->geo.H + TILE - 1) / TILE;
     a.stats = p->stats;
+    a.prof = p->prof;
     return a;
 }
 
@@ -515,6 +527,25 @@ extern "C" bsf_status bsf_get_stats(bsf_plan_t p, bsf_stats *s, int reset) {
 }
 
 extern "C" long long bsf_launch_count(bsf_plan_t p) { return p ? p->nlaunch : 0; }
+
+extern "C" bsf_status bsf_debug_phase_cycles(bsf_plan_t p, unsigned long long *out, int reset) {
+    if (!p) return set_err(BSF_EINVAL, "null plan");
+    if (!p->prof) {
+        void *q;
+        CUDA_TRY(cudaMalloc(&q, 8 * sizeof(unsigned long long)));
+        p->dev_allocs.push_back(q);
+        p->prof = (unsigned long long *)q;
+        CUDA_TRY(cudaMemset(q, 0, 8 * sizeof(unsigned long long)));
+    }
+    if (out) {
+        CUDA_TRY(cudaStreamSynchronize(p->last));
+        CUDA_TRY(cudaMemcpy(out, p->prof, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    }
+    if (reset) CUDA_TRY(cudaMemset(p->prof, 0, 8 * sizeof(unsigned long long)));
+    return BSF_OK;
+}
+
+extern "C" int bsf_uses_fused(bsf_plan_t p) { return p && p->fused ? 1 : 0; }
 
 extern "C" const char *bsf_status_str(bsf_status s) {
     switch (s) {

@@ -29,15 +29,23 @@ constexpr int NPLANE = 2 * NVAR;              // (basis, variant)
 constexpr uint16_t NOKEY = 0xFFFF;
 
 template <int R> struct FusedCfg;
-template <> struct FusedCfg<1> { static constexpr int NTAP = 16, P = 256; };
-template <> struct FusedCfg<2> { static constexpr int NTAP = 81, P = 64; };
-template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 16; };
-template <> struct FusedCfg<4> { static constexpr int NTAP = 625, P = 8; };
+// NTAP taps per pixel, P pixels per chunk, MT 8-item m-tiles per group
+template <> struct FusedCfg<1> { static constexpr int NTAP = 16, P = 256, MT = 2; };
+template <> struct FusedCfg<2> { static constexpr int NTAP = 81, P = 64, MT = 2; };
+template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 16, MT = 1; };
+template <> struct FusedCfg<4> { static constexpr int NTAP = 625, P = 4, MT = 1; };
+
+template <int R>
+constexpr size_t fused_escratch_doubles() {  // per warp: [limb][mu][item], item stride GS + 1
+    return (size_t)2 * ((((4 * R - 1) * (4 * R) / 2) + 7) / 8 * 8) * (8 * FusedCfg<R>::MT + 1);
+}
 
 template <int R>
 constexpr size_t fused_smem_bytes() {
     constexpr size_t ITEMS = (size_t)FusedCfg<R>::P * FusedCfg<R>::NTAP;
-    return ITEMS * 16 + FT * 4 * 8 + ITEMS * 2 + (ITEMS + 16 * NKEY) * 2 + 2 * NKEY * 4 + FT * 4;
+    constexpr size_t GS = 8 * FusedCfg<R>::MT;
+    return ITEMS * 16 + (FT / 32) * fused_escratch_doubles<R>() * 8 + FT * 4 * 8 + ITEMS * 2 +
+           (ITEMS + GS * NKEY) * 2 + (FT / 32) * NKEY * 4 + FT * 4;
 }
 
 // pixel info word: bit0 basis, bits1-3 variant (drop + 1), bit4 live, bit5 clamped, bits 8.. flags
@@ -65,88 +73,167 @@ __device__ __forceinline__ void fused_tap(const double *ap, int basis, int drop,
     }
 }
 
-// One chunk of rows [IHI .. ILO] of the contraction + compensated Horner.
-template <int DEG, int IHI>
-__device__ __forceinline__ void fused_chunk(const double2 *__restrict__ G, int NX, int NY, int bx, int by,
-                                            const int2 *__restrict__ offs, const double *__restrict__ num, int nmonp,
-                                            int n, double fx, double fy, double &ah, double &al, int &flags) {
-    constexpr int ILO = bsf_chunk_lo(DEG, IHI);
-    constexpr int NM = bsf_chunk_len(DEG, IHI);
-    constexpr int NMP = (NM + 1) & ~1;
-    constexpr int OFF = bsf_chunk_off(DEG, IHI);
-    double A[NMP], B[NMP];
+// split running sum (G1, G0) at domain point (lx, ly); zero above the domain.
+// Branch-free: the load always reads a valid address and the value is
+// selected afterwards (no divergence barriers in the MMA loop).
+__device__ __forceinline__ double2 load_split(const double2 *__restrict__ G, int NX, int NY, int lx, int ly,
+                                              int &flags) {
+    const bool inside = lx >= 0 && lx < NX && ly >= 0 && ly < NY;
+    flags |= (ly >= 0 && !inside) ? FLAG_RANGE : 0;
+    const double2 v = G[inside ? (size_t)ly * NX + lx : 0];
+    return inside ? v : make_double2(0.0, 0.0);
+}
+
+// binomial sign weight of tap t: prod_k (-1)^{j_k} C(R, j_k)
+template <int R>
+__device__ __forceinline__ int tap_coef(int t, int drop) {
+    int c = 1;
 #pragma unroll
-    for (int m = 0; m < NMP; ++m) {
-        A[m] = 0.0;
-        B[m] = 0.0;
+    for (int k = 0; k < 4; ++k) {
+        if (k == drop) continue;
+        const int j = t % (R + 1);
+        t /= (R + 1);
+        c *= binom_small(R, j) * ((j & 1) ? -1 : 1);
     }
-#pragma unroll 2
-    for (int s = 0; s < n; ++s) {
-        const int2 d = __ldg(offs + s);
-        const int lx = bx + d.x, ly = by + d.y;
-        double2 g = make_double2(0.0, 0.0);
-        if (ly >= 0) {  // above the domain: zero state
-            if (lx >= 0 && lx < NX && ly < NY)
-                g = G[(size_t)ly * NX + lx];
-            else
-                flags |= FLAG_RANGE;
-        }
-        const double2 *c = reinterpret_cast<const double2 *>(num + (size_t)s * nmonp + OFF);
-#pragma unroll
-        for (int m = 0; m < NMP / 2; ++m) {
-            const double2 cc = __ldg(c + m);
-            A[2 * m] = fma(g.x, cc.x, A[2 * m]);  // exact: integers below 2^53
-            B[2 * m] = fma(g.y, cc.x, B[2 * m]);
-            A[2 * m + 1] = fma(g.x, cc.y, A[2 * m + 1]);
-            B[2 * m + 1] = fma(g.y, cc.y, B[2 * m + 1]);
-        }
-    }
-#pragma unroll
-    for (int i = IHI; i >= ILO; --i) {
-        const int base = bsf_row_start(DEG, i) - bsf_row_start(DEG, IHI);
-        double rh = 0.0, rl = 0.0;
-#pragma unroll
-        for (int j = DEG - i; j >= 0; --j) {
-            const int m = base + (DEG - i - j);
-            const dd E = two_sum(A[m], B[m]);
-            if (j == DEG - i) {
-                rh = E.hi;
-                rl = E.lo;
-            } else {
-                comp_step(rh, rl, fy, E.hi, E.lo);
-            }
-        }
-        if (i == DEG) {
-            ah = rh;
-            al = rl;
-        } else {
-            comp_step(ah, al, fx, rh, rl);
-        }
-    }
-    if constexpr (ILO > 0)
-        fused_chunk<DEG, ILO - 1>(G, NX, NY, bx, by, offs, num, nmonp, n, fx, fy, ah, al, flags);
+    return c;
+}
+
+// FP64 tensor-core MMA (DMMA): D(8x8) += A(8x4) B(4x8).  Fragments (PTX ISA,
+// m8n8k4 .f64): lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4)+{0,1}].
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
 }
 
 template <int DEG>
-__device__ __forceinline__ void fused_item(const double2 *__restrict__ G, int NX, int NY, int bx, int by,
-                                           const LutVar &V, int reg, double fx, double fy, double &Fh, double &Fl,
-                                           int &flags) {
-    const int n = __ldg(V.counts + reg);
-    fused_chunk<DEG, DEG>(G, NX, NY, bx, by, V.offs + (size_t)reg * V.nmax, V.num + (size_t)reg * V.nmax * V.nmonp,
-                          V.nmonp, n, fx, fy, Fh, Fl, flags);
+struct DegCfg {
+    static constexpr int NMON = (DEG + 1) * (DEG + 2) / 2;
+    static constexpr int NT = (NMON + 7) / 8;  // 8-monomial n-tiles
+};
+
+// Contraction of one group of GS = 8 MT items sharing a key, on the FP64
+// tensor cores: for every item (M), window slot (K) and monomial (N)
+//   E_mu = sum_s G1_s n_{s,mu}  (exact)   and   sum_s G0_s n_{s,mu},
+// the two limbs as separate accumulators.  (bx_t, by_t): tap base of the
+// item this lane feeds in m-tile t; the result goes to the warp's scratch
+// E[limb][mu][item] (item stride GS + 1).
+template <int DEG, int MT>
+__device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
+                                            const int (&byt)[MT], const int2 *__restrict__ offs,
+                                            const double *__restrict__ num, int nmonp, int n4, double *E,
+                                            int &flags) {
+    constexpr int NT = DegCfg<DEG>::NT, GS = 8 * MT, ES = GS + 1;
+    const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
+    double C[MT][2][NT][2];
+#pragma unroll
+    for (int t = 0; t < MT; ++t)
+#pragma unroll
+        for (int L = 0; L < 2; ++L)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) C[t][L][j][0] = C[t][L][j][1] = 0.0;
+    // Software pipeline over k-steps of 4 window slots, unrolled by two with
+    // ping-pong operand sets (A for even steps, B for odd): while one step's
+    // MMAs issue, the other set is loaded for the next step, and the window
+    // offsets one step further ahead.  No loaded value crosses the loop edge
+    // through a register copy.
+    const int nsteps = n4 >> 2;
+    const double *cs = num + kq * nmonp + gq;
+    const int cstep = 4 * nmonp;
+    double2 aA[MT], aB[MT];
+    double bA[NT], bB[NT];
+    int2 dA = __ldg(offs + kq), dB = make_int2(0, 0);
+#pragma unroll
+    for (int t = 0; t < MT; ++t) aA[t] = load_split(G, NX, NY, bxt[t] + dA.x, byt[t] + dA.y, flags);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) bA[j] = __ldg(cs + 8 * j);
+    if (nsteps > 1) dB = __ldg(offs + 4 + kq);
+    for (int st = 0; st < nsteps; st += 2) {
+        if (st + 1 < nsteps) {
+#pragma unroll
+            for (int t = 0; t < MT; ++t) aB[t] = load_split(G, NX, NY, bxt[t] + dB.x, byt[t] + dB.y, flags);
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bB[j] = __ldg(cs + (size_t)(st + 1) * cstep + 8 * j);
+        }
+        if (st + 2 < nsteps) dA = __ldg(offs + 4 * (st + 2) + kq);
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+                dmma(C[t][0][j], aA[t].x, bA[j]);  // exact: integers below 2^53
+                dmma(C[t][1][j], aA[t].y, bA[j]);
+            }
+        if (st + 1 >= nsteps) break;
+        if (st + 2 < nsteps) {
+#pragma unroll
+            for (int t = 0; t < MT; ++t) aA[t] = load_split(G, NX, NY, bxt[t] + dA.x, byt[t] + dA.y, flags);
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bA[j] = __ldg(cs + (size_t)(st + 2) * cstep + 8 * j);
+        }
+        if (st + 3 < nsteps) dB = __ldg(offs + 4 * (st + 3) + kq);
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+                dmma(C[t][0][j], aB[t].x, bB[j]);
+                dmma(C[t][1][j], aB[t].y, bB[j]);
+            }
+    }
+    const int NMP = NT * 8;
+#pragma unroll
+    for (int t = 0; t < MT; ++t)
+#pragma unroll
+        for (int L = 0; L < 2; ++L)
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    E[(L * NMP + 8 * j + 2 * kq + q) * ES + gq + 8 * t] = C[t][L][j][q];
+}
+
+// F = sum_mu (E1_mu + E0_mu) phi^mu for one item (monomials x-major, i
+// descending, j descending: the gen_lut order), compensated: first the DEG+1
+// independent row polynomials R_i(phi_y) (interleaved, so their dependency
+// chains overlap), then the Horner scheme in phi_x over the rows.
+template <int DEG, int GS>
+__device__ __forceinline__ dd fused_horner(const double *E, int item, double fx, double fy) {
+    constexpr int NMP = DegCfg<DEG>::NT * 8, ES = GS + 1;
+    double rh[DEG + 1], rl[DEG + 1];
+    // highest y power of every row first
+#pragma unroll
+    for (int i = 0; i <= DEG; ++i) {
+        const int m = (DEG - i) * (DEG - i + 1) / 2;  // row i starts with phi_y^(DEG-i)
+        const dd e = two_sum(E[m * ES + item], E[(NMP + m) * ES + item]);
+        rh[i] = e.hi;
+        rl[i] = e.lo;
+    }
+#pragma unroll
+    for (int k = 1; k <= DEG; ++k)
+#pragma unroll
+        for (int i = 0; i <= DEG - k; ++i) {  // row i has DEG - i + 1 terms
+            const int m = (DEG - i) * (DEG - i + 1) / 2 + k;
+            const dd e = two_sum(E[m * ES + item], E[(NMP + m) * ES + item]);
+            comp_step(rh[i], rl[i], fy, e.hi, e.lo);
+        }
+    double ah = rh[DEG], al = rl[DEG];
+#pragma unroll
+    for (int i = DEG - 1; i >= 0; --i) comp_step(ah, al, fx, rh[i], rl[i]);
+    return fast_two_sum(ah, al);
 }
 
 template <int R>
 __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
     constexpr int NTAP = FusedCfg<R>::NTAP, P = FusedCfg<R>::P, ITEMS = P * NTAP;
+    constexpr int MT = FusedCfg<R>::MT, GS = 8 * MT;
+    constexpr int ESZ = (int)fused_escratch_doubles<R>();
     extern __shared__ __align__(16) unsigned char smem[];
     double2 *s_F = reinterpret_cast<double2 *>(smem);
-    double *s_ap = reinterpret_cast<double *>(s_F + ITEMS);
+    double *s_E = reinterpret_cast<double *>(s_F + ITEMS);  // [warp][ESZ]
+    double *s_ap = s_E + (FT / 32) * ESZ;
     uint16_t *s_key = reinterpret_cast<uint16_t *>(s_ap + FT * 4);
     uint16_t *s_sorted = s_key + ITEMS;
-    int *s_cnt = reinterpret_cast<int *>(s_sorted + ITEMS + 16 * NKEY);
-    int *s_start = s_cnt + NKEY;
-    int *s_info = s_start + NKEY;
+    int *s_hist = reinterpret_cast<int *>(s_sorted + ITEMS + GS * NKEY);  // [warp][key]
+    int *s_info = s_hist + (FT / 32) * NKEY;
     __shared__ int s_item, s_ex[2], s_ey[2], s_vmask[2], s_bad, s_npad, s_any;
     __shared__ int s_dom[2][4];
     __shared__ long long s_poff[NPLANE];
@@ -154,6 +241,15 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     __shared__ unsigned long long s_pmax[NPLANE];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // optional phase timing (TileArgs::prof, diagnostics only): thread 0 adds
+    // the SM cycles spent in each phase
+    long long ph_t = clock64();
+#define FUSED_PHASE(k)                                        \
+    if (a.prof && tid == 0) {                                 \
+        const long long t_ = clock64();                       \
+        atomicAdd(a.prof + (k), (unsigned long long)(t_ - ph_t)); \
+        ph_t = t_;                                            \
+    }
     double2 *scr = a.scratch + (size_t)blockIdx.x * NPLANE * a.cap;
     const int tiles_per_img = a.ntx * a.nty;
     const int nitems = a.pts ? a.npts : tiles_per_img * a.nimg;
@@ -170,6 +266,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         __syncthreads();
         const int item = s_item;
         if (item >= nitems) break;
+        if (a.prof && tid == 0) ph_t = clock64();
         int img, x0, y0, want = -1;
         if (a.pts) {
             img = a.pts[3 * item];
@@ -215,6 +312,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             }
         }
         __syncthreads();
+        FUSED_PHASE(0);
 
         // ---- 2. pre-integration planes ------------------------------------------
         if (tid == 0) {
@@ -291,6 +389,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             }
         }
         __syncthreads();
+        FUSED_PHASE(1);
 
         // ---- 3. exact split G = 2^e (G1 + G0) of every plane that is read --------
         for (int pi = 0; pi < NPLANE; ++pi) {
@@ -324,41 +423,56 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             }
         }
         __syncthreads();
+        FUSED_PHASE(2);
 
         // ---- 4-5. taps bucketed by key, gather, per-pixel sums -------------------
+        // Items are numbered tap-major, i = t * P + p (p the pixel within the
+        // chunk), and bucketed by a STABLE counting sort, so a 16-lane group
+        // holds the same tap of neighbouring pixels: their G reads are adjacent.
+        constexpr int WPR = ((ITEMS + FT / 32 - 1) / (FT / 32) + 31) & ~31;  // items per warp range
         for (int c0 = 0; c0 < FT; c0 += P) {
             if (tid == 0) s_any = 0;
             __syncthreads();
             if (tid >= c0 && tid < c0 + P && info_live(s_info[tid]) && (!a.pts || tid == want)) s_any = 1;
-            for (int k = tid; k < NKEY; k += FT) s_cnt[k] = 0;
+            for (int k = tid; k < (FT / 32) * NKEY; k += FT) s_hist[k] = 0;
             __syncthreads();
             if (!s_any) continue;  // uniform
-            // keys
-            for (int i = tid; i < ITEMS; i += FT) {
-                const int p = c0 + i / NTAP, t = i % NTAP;
-                const int w = s_info[p];
+            // keys, per-warp histograms (warp w owns items [w*WPR, (w+1)*WPR))
+            for (int base = warp * WPR; base < min(ITEMS, (warp + 1) * WPR); base += 32) {
+                const int i = base + lane;
                 uint16_t key = NOKEY;
-                const int var = info_var(w);
-                const int ntap = var ? NTAP / (R + 1) : NTAP;
-                if (info_live(w) && (!a.pts || p == want) && t < ntap) {
-                    const int b = info_basis(w);
-                    double Dx, Dy;
-                    int cf;
-                    fused_tap<R>(s_ap + 4 * p, b, var - 1, t, Dx, Dy, cf);
-                    const double fx = Dx - floor(Dx), fy = Dy - floor(Dy);
-                    const int reg = classify(luts[b], fx, fy);
-                    key = (uint16_t)((b * NVAR + var) * MAX_REG + reg);
-                    atomicAdd(&s_cnt[key], 1);
+                if (i < ITEMS) {
+                    const int t = i / P, p = c0 + i % P;
+                    const int w = s_info[p];
+                    const int var = info_var(w);
+                    const int ntap = var ? NTAP / (R + 1) : NTAP;
+                    if (info_live(w) && (!a.pts || p == want) && t < ntap) {
+                        const int b = info_basis(w);
+                        double Dx, Dy;
+                        int cf;
+                        fused_tap<R>(s_ap + 4 * p, b, var - 1, t, Dx, Dy, cf);
+                        const double fx = Dx - floor(Dx), fy = Dy - floor(Dy);
+                        const int reg = classify(luts[b], fx, fy);
+                        key = (uint16_t)((b * NVAR + var) * MAX_REG + reg);
+                    }
+                    s_key[i] = key;
                 }
-                s_key[i] = key;
+                const unsigned m = __match_any_sync(0xffffffffu, key);
+                if (key != NOKEY && lane == __ffs(m) - 1) s_hist[warp * NKEY + key] += __popc(m);
+                __syncwarp();
             }
             __syncthreads();
-            // bucket starts, each bucket padded to a multiple of 16 (warp 0)
+            // bucket starts (each bucket padded to a multiple of GS) and per-warp offsets
             if (warp == 0) {
                 constexpr int PER = NKEY / 32;
                 int loc = 0;
 #pragma unroll
-                for (int q = 0; q < PER; ++q) loc += (s_cnt[lane * PER + q] + 15) & ~15;
+                for (int q = 0; q < PER; ++q) {
+                    int tot = 0;
+#pragma unroll
+                    for (int w = 0; w < FT / 32; ++w) tot += s_hist[w * NKEY + lane * PER + q];
+                    loc += (tot + GS - 1) / GS * GS;
+                }
                 int inc = loc;
                 for (int o = 1; o < 32; o <<= 1) {
                     const int t = __shfl_up_sync(0xffffffffu, inc, o);
@@ -367,9 +481,15 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 int run = inc - loc;
 #pragma unroll
                 for (int q = 0; q < PER; ++q) {
-                    s_start[lane * PER + q] = run;
-                    run += (s_cnt[lane * PER + q] + 15) & ~15;
-                    s_cnt[lane * PER + q] = 0;
+                    const int k = lane * PER + q;
+                    int o = run;
+#pragma unroll
+                    for (int w = 0; w < FT / 32; ++w) {
+                        const int h = s_hist[w * NKEY + k];
+                        s_hist[w * NKEY + k] = o;
+                        o += h;
+                    }
+                    run += (o - run + GS - 1) / GS * GS;
                 }
                 if (lane == 31) s_npad = inc;
             }
@@ -377,68 +497,98 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             const int npad = s_npad;
             for (int i = tid; i < npad; i += FT) s_sorted[i] = NOKEY;
             __syncthreads();
-            for (int i = tid; i < ITEMS; i += FT) {
-                const uint16_t key = s_key[i];
-                if (key != NOKEY) s_sorted[s_start[key] + atomicAdd(&s_cnt[key], 1)] = (uint16_t)i;
+            for (int base = warp * WPR; base < min(ITEMS, (warp + 1) * WPR); base += 32) {
+                const int i = base + lane;
+                const uint16_t key = i < ITEMS ? s_key[i] : NOKEY;
+                const unsigned m = __match_any_sync(0xffffffffu, key);
+                const int rank = __popc(m & ((1u << lane) - 1u));
+                if (key != NOKEY) s_sorted[s_hist[warp * NKEY + key] + rank] = (uint16_t)i;
+                __syncwarp();
+                if (key != NOKEY && lane == __ffs(m) - 1) s_hist[warp * NKEY + key] += __popc(m);
+                __syncwarp();
             }
             __syncthreads();
-            // gather: half-warp groups of 16 items sharing one key
+            FUSED_PHASE(3);
+            // gather: groups of GS items sharing one key, one warp per group,
+            // contraction on the FP64 tensor cores, Horner on lanes < GS
             {
-                const int ngroups = npad >> 4, npairs = (ngroups + 1) >> 1, half = lane >> 4;
+                const int ngroups = npad / GS;
+                double *E = s_E + warp * ESZ;
                 int flags = 0;
-                for (int k = warp; k < npairs; k += FT / 32) {
-                    const int g = 2 * k + half;
-                    if (g >= ngroups) continue;
-                    const int i0 = s_sorted[g * 16];
-                    int idx = s_sorted[g * 16 + (lane & 15)];
-                    const bool real = idx != NOKEY;
-                    if (!real) idx = i0;  // dummy lanes repeat the group's first item
+                for (int g = warp; g < ngroups; g += FT / 32) {
+                    const int i0 = s_sorted[g * GS];
                     const int key = s_key[i0];
                     const int b = key / (NVAR * MAX_REG), var = (key / MAX_REG) % NVAR, reg = key % MAX_REG;
-                    const int p = c0 + idx / NTAP, t = idx % NTAP;
+                    int idx = lane < GS ? s_sorted[g * GS + lane] : NOKEY;
+                    const bool real = idx != NOKEY;
+                    if (!real) idx = i0;  // dummy lanes repeat the group's first item
+                    const int p = c0 + idx % P, t = idx / P;
                     double Dx, Dy;
                     int cf;
                     fused_tap<R>(s_ap + 4 * p, b, var - 1, t, Dx, Dy, cf);
                     const double flx = floor(Dx), fly = floor(Dy);
-                    const int x = x0 + (p % TILE), y = y0 + p / TILE;
-                    const int bx = x + (int)flx - s_dom[b][0], by = y + (int)fly - s_dom[b][1];
-                    const double2 *G = scr + s_poff[b * NVAR + var];
-                    double Fh, Fl;
-                    int fl = 0;
-                    if (var == 0)
-                        fused_item<4 * R - 2>(G, s_dom[b][2], s_dom[b][3], bx, by, luts[b].var[0], reg, Dx - flx,
-                                              Dy - fly, Fh, Fl, fl);
-                    else
-                        fused_item<3 * R - 2>(G, s_dom[b][2], s_dom[b][3], bx, by, luts[b].var[var], reg, Dx - flx,
-                                              Dy - fly, Fh, Fl, fl);
-                    if (real) {
-                        s_F[idx] = make_double2(Fh, Fl);
-                        flags |= fl;
+                    const int bx = x0 + (p % TILE) + (int)flx - s_dom[b][0];
+                    const int by = y0 + p / TILE + (int)fly - s_dom[b][1];
+                    int bxt[MT], byt[MT];
+#pragma unroll
+                    for (int q = 0; q < MT; ++q) {
+                        bxt[q] = __shfl_sync(0xffffffffu, bx, (lane >> 2) + 8 * q);
+                        byt[q] = __shfl_sync(0xffffffffu, by, (lane >> 2) + 8 * q);
                     }
+                    const double2 *G = scr + s_poff[b * NVAR + var];
+                    const LutVar &V = luts[b].var[var];
+                    const int n4 = (__ldg(V.counts + reg) + 3) & ~3;
+                    const int NX = s_dom[b][2], NY = s_dom[b][3];
+                    dd F;
+                    long long tq0 = 0;
+                    if (a.prof && lane == 0) tq0 = clock64();
+                    if (var == 0) {
+                        fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, V.offs4 + (size_t)reg * V.nslot4,
+                                                   V.num + (size_t)reg * V.nslot4 * V.nmonp, V.nmonp, n4, E, flags);
+                        __syncwarp();
+                        if (a.prof && lane == 0) atomicAdd(a.prof + 7, (unsigned long long)(clock64() - tq0));
+                        if (lane < GS) F = fused_horner<4 * R - 2, GS>(E, lane, Dx - flx, Dy - fly);
+                    } else {
+                        fused_group<3 * R - 2, MT>(G, NX, NY, bxt, byt, V.offs4 + (size_t)reg * V.nslot4,
+                                                   V.num + (size_t)reg * V.nslot4 * V.nmonp, V.nmonp, n4, E, flags);
+                        __syncwarp();
+                        if (lane < GS) F = fused_horner<3 * R - 2, GS>(E, lane, Dx - flx, Dy - fly);
+                    }
+                    if (lane < GS && real) s_F[idx] = make_double2(F.hi, F.lo);
+                    __syncwarp();
+                    if (a.prof && lane == 0) atomicAdd(a.prof + 6, (unsigned long long)(clock64() - tq0));
                 }
                 if (flags && a.stats) atomicOr(a.stats + 4, (unsigned long long)flags);
             }
             __syncthreads();
-            // per-pixel signed accumulation and normalisation (a7)
-            if (tid < P) {
-                const int p = c0 + tid;
+            FUSED_PHASE(4);
+            // per-pixel signed accumulation and normalisation (a7): TPP threads per
+            // pixel sum interleaved taps in double-double, combined by shuffles
+            {
+                constexpr int TPP = FT / P;
+                const int pl = tid / TPP, sub = tid % TPP;
+                const int p = c0 + pl;
                 const int w = s_info[p];
+                const int b = info_basis(w), var = info_var(w);
+                dd S = {0.0, 0.0};
+                if (info_live(w)) {
+                    const int ntap = var ? NTAP / (R + 1) : NTAP;
+                    for (int t = sub; t < ntap; t += TPP) {
+                        const double2 F = s_F[t * P + pl];
+                        S = dd_add(S, dd_mul_d({F.x, F.y}, (double)tap_coef<R>(t, var - 1)));
+                    }
+                }
+#pragma unroll
+                for (int o = 1; o < TPP; o <<= 1) {
+                    const dd T = {__shfl_xor_sync(0xffffffffu, S.hi, o), __shfl_xor_sync(0xffffffffu, S.lo, o)};
+                    S = dd_add(S, T);
+                }
                 const int x = x0 + (p % TILE), y = y0 + p / TILE;
                 const bool valid = x < a.W && y < a.H;
-                const bool mine = a.pts ? (p == want) : valid;
+                const bool mine = sub == 0 && (a.pts ? (p == want) : valid);
                 if (mine) {
                     double res = __longlong_as_double(0x7ff8000000000000LL);
-                    const int b = info_basis(w), var = info_var(w);
                     if (info_live(w)) {
-                        const int ntap = var ? NTAP / (R + 1) : NTAP;
-                        dd S = {0.0, 0.0};
-                        for (int t = 0; t < ntap; ++t) {
-                            double Dx, Dy;
-                            int cf;
-                            fused_tap<R>(s_ap + 4 * p, b, var - 1, t, Dx, Dy, cf);
-                            const double2 F = s_F[tid * NTAP + t];
-                            S = dd_add(S, dd_mul_d({F.x, F.y}, (double)cf));
-                        }
                         double norm = 1.0;
                         for (int k = 0; k < 4; ++k) {
                             if (k == var - 1) continue;
@@ -472,6 +622,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 }
             }
             __syncthreads();
+            FUSED_PHASE(5);
         }
     }
 }

@@ -13,42 +13,16 @@ constexpr int BSF_AUX = 12;  // doubles of per-point diagnostics
 enum { FLAG_RANGE_H = 1, FLAG_INFEASIBLE_H = 2, FLAG_TWO_ZERO_H = 4, FLAG_SOLVER_H = 8 };
 constexpr int NVAR = 5;  // full kernel + one per dropped direction
 
-// Monomial chunks of the exact split contraction (bsf_fused.cuh).  Monomials
-// phi_x^i phi_y^j of degree <= deg are ordered x-major, i descending, j
-// descending (gen_lut.monomials); a chunk is a run of whole rows i with at
-// most BSF_CH monomials, stored padded to an even length so the kernel reads
-// coefficient pairs with 16-byte loads.
-constexpr int BSF_CH = 28;
-__host__ __device__ constexpr int bsf_row_start(int deg, int i) { return (deg - i) * (deg - i + 1) / 2; }
-__host__ __device__ constexpr int bsf_chunk_lo(int deg, int ihi) {
-    int tot = 0, i = ihi;
-    while (i >= 0 && tot + (deg - i + 1) <= BSF_CH) {
-        tot += deg - i + 1;
-        --i;
-    }
-    return i == ihi ? ihi : i + 1;
-}
-__host__ __device__ constexpr int bsf_chunk_len(int deg, int ihi) {
-    return bsf_row_start(deg, bsf_chunk_lo(deg, ihi)) + (deg - bsf_chunk_lo(deg, ihi) + 1) - bsf_row_start(deg, ihi);
-}
-// offset (padded layout) of the chunk that starts at row ihi; ihi = -1 gives the padded total
-__host__ __device__ constexpr int bsf_chunk_off(int deg, int ihi) {
-    int off = 0, i = deg;
-    while (i > ihi) {
-        off += (bsf_chunk_len(deg, i) + 1) & ~1;
-        i = bsf_chunk_lo(deg, i) - 1;
-    }
-    return off;
-}
-
 // One interpolation table (basis, order, variant) in device memory.
 struct LutVar {
     int deg, nmon, nmax;
     const int2 *offs;      // [nreg][nmax]
     const int *counts;     // [nreg]
     const double2 *coef;   // [nreg][nmax][nmon] double-double (n / L)
-    const double *num;     // [nreg][nmax][nmonp] integer numerators n (exact doubles), chunk layout
-    int nmonp;             // bsf_chunk_off(deg, -1)
+    const double *num;     // [nreg][nslot4][nmonp] integer numerators n (exact doubles), zero padded
+    const int2 *offs4;     // [nreg][nslot4] window offsets, padded with (0, 0)
+    int nmonp;             // nmon rounded up to 8 (FP64 MMA n-tiles)
+    int nslot4;            // nmax rounded up to 4 (FP64 MMA k-steps)
     int kbits;             // |G1| <= 2^kbits keeps sum_s G1 * n exact in fp64
     double L;              // common denominator
 };
@@ -102,6 +76,7 @@ struct TileArgs {
     int *counter;           // work counter (zeroed before launch)
     int ntx, nty;
     unsigned long long *stats;
+    unsigned long long *prof;  // optional [8] phase cycles (bsf_debug_phase_cycles)
 };
 constexpr int TILE = 16;
 size_t tile_capacity(int order, float max_sigma, const LutBasis *host_luts, int basis_mask);

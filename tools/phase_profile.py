@@ -1,0 +1,38 @@
+"""Phase breakdown of the fused tile kernel on a BASELINE config (GPU).
+
+python tools/phase_profile.py [--config 2] [--order R]
+Prints the share of SM cycles per phase (diagnostic counters, one clock read
+per phase per tile; see bsf_debug_phase_cycles)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1109_5114_b200 import bsf  # noqa: E402
+
+PHASES = ["scales", "pre-integration", "exact split", "keys+sort", "gather", "accumulate"]
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--order", type=int, default=0)
+args = ap.parse_args()
+w = synth.workload(args.config, order=args.order) if args.order else synth.workload(args.config)
+dev = torch.device("cuda:0")
+plan = bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" else bsf.BSF_F32, order=w.order,
+                basis=w.basis, max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_TILE)
+img = synth.make_image(w, device=dev).contiguous()
+cov = synth.make_cov(w, device=dev).contiguous()
+out = torch.empty((1, w.height, w.width), dtype=torch.float64, device=dev)
+plan.run(img, cov, out)
+plan.phase_cycles(reset=True)
+plan.run(img, cov, out)
+cyc = plan.phase_cycles()
+tot = sum(cyc[:6])
+print("workload", w.name, "fused", plan.uses_fused())
+for n, c in zip(PHASES, cyc):
+    print("%-16s %6.1f%%  %.3e cycles" % (n, 100.0 * c / tot, c))
+print("gather groups: warp-cycles total %.3e, full-variant MMA loop %.3e (per-CTA wall equivalent /8: %.3e, %.3e)"
+      % (cyc[6], cyc[7], cyc[6] / 8, cyc[7] / 8))
