@@ -398,8 +398,8 @@ static bool use_fused(const bsf_plan_s *p) {
 static bsf_status ensure_tile_ws(bsf_plan_s *p) {
     if (p->tile_scratch) return BSF_OK;
     int mask = p->d.basis == BSF_DUAL ? 3 : (1 << p->d.basis);
-    p->tile_cap = tile_capacity(p->d.order, p->d.max_sigma, p->host_luts, mask);
     p->fused = use_fused(p);
+    p->tile_cap = tile_capacity(p->d.order, p->d.max_sigma, p->host_luts, mask, p->fused ? 2 * TILE : TILE);
     p->tile_nslots = p->fused ? fused_slots() : tile_slots();
     void *q;
     size_t bytes = (size_t)p->tile_nslots * (p->fused ? NPLANE_MAX : 2) * p->tile_cap * sizeof(double2);

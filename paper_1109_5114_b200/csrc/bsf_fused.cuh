@@ -23,7 +23,8 @@
 //       F    = sum_mu E_mu phi^mu                   (compensated Horner, rows)
 //  5. a7: per pixel S = sum_j c_j F_j in double-double, out = 2^e S w^r / L.
 
-constexpr int FT = 256;                       // threads per CTA = pixels per tile
+constexpr int FT = 256;                       // threads per CTA = pixels per sub-tile
+constexpr int STILE = 2 * TILE;               // super-tile: the running sums' anchor
 constexpr int NKEY = 2 * NVAR * MAX_REG;      // (basis, variant, region)
 constexpr int NPLANE = 2 * NVAR;              // (basis, variant)
 constexpr uint16_t NOKEY = 0xFFFF;
@@ -82,6 +83,18 @@ __device__ __forceinline__ double2 load_split(const double2 *__restrict__ G, int
     flags |= (ly >= 0 && !inside) ? FLAG_RANGE : 0;
     const double2 v = G[inside ? (size_t)ly * NX + lx : 0];
     return inside ? v : make_double2(0.0, 0.0);
+}
+
+// Halo domain of a super-tile (as tile_domain, for STILE x STILE outputs).
+__device__ __forceinline__ TileDomain fused_domain(const LutBasis &L, int R, int x0, int y0, int EX, int EY) {
+    TileDomain d;
+    d.X0 = x0 - EX + L.wxmin - 2 * R - 1;  // zero-scale lattice difference reaches back R|s_x| <= 2R
+    const int X1 = x0 + STILE - 1 + EX + L.wxmax + 2 * R + 1;
+    d.Y0 = y0 - EY;  // no kernel support above: zero state
+    const int Y1 = y0 + STILE - 1 + EY + L.wymax + 1;
+    d.NX = X1 - d.X0 + 1;
+    d.NY = Y1 - d.Y0 + 1;
+    return d;
 }
 
 // binomial sign weight of tap t: prod_k (-1)^{j_k} C(R, j_k)
@@ -251,8 +264,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         ph_t = t_;                                            \
     }
     double2 *scr = a.scratch + (size_t)blockIdx.x * NPLANE * a.cap;
-    const int tiles_per_img = a.ntx * a.nty;
-    const int nitems = a.pts ? a.npts : tiles_per_img * a.nimg;
+    const int nstx = (a.W + STILE - 1) / STILE, nsty = (a.H + STILE - 1) / STILE;
+    const int stiles_per_img = nstx * nsty;
+    const int nitems = a.pts ? a.npts : stiles_per_img * a.nimg;
     const size_t ipl = (size_t)a.H * a.W;
 
     for (;;) {
@@ -267,48 +281,41 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         const int item = s_item;
         if (item >= nitems) break;
         if (a.prof && tid == 0) ph_t = clock64();
-        int img, x0, y0, want = -1;
+        // super-tile origin (X0s, Y0s): the running sums are anchored on its
+        // halo domain; its four TILE x TILE sub-tiles are gathered in turn
+        int img, X0s, Y0s, want = -1, qwant = -1;
         if (a.pts) {
             img = a.pts[3 * item];
             const int px = a.pts[3 * item + 1], py = a.pts[3 * item + 2];
-            x0 = px & ~(TILE - 1);
-            y0 = py & ~(TILE - 1);
-            want = (px - x0) + TILE * (py - y0);
+            X0s = px & ~(STILE - 1);
+            Y0s = py & ~(STILE - 1);
+            qwant = ((px - X0s) >= TILE ? 1 : 0) + ((py - Y0s) >= TILE ? 2 : 0);
+            want = (px & (TILE - 1)) + TILE * (py & (TILE - 1));
         } else {
-            img = item / tiles_per_img;
-            const int rem = item % tiles_per_img;
-            x0 = (rem % a.ntx) * TILE;
-            y0 = (rem / a.ntx) * TILE;
+            img = item / stiles_per_img;
+            const int rem = item % stiles_per_img;
+            X0s = (rem % nstx) * STILE;
+            Y0s = (rem / nstx) * STILE;
         }
 
-        // ---- 1. per-pixel scales ------------------------------------------------
-        {
-            const int x = x0 + (tid % TILE), y = y0 + tid / TILE;
-            PixelScales ps;
-            ps.flags = 0;
-            ps.basis = 0;
-            ps.drop = -1;
-            ps.clamped = 0;
-            ps.ap[0] = ps.ap[1] = ps.ap[2] = ps.ap[3] = 0.0;
-            const bool valid = x < a.W && y < a.H;
-            if (valid) {
+        // ---- 1. reach of every pixel of the super-tile (a1-a4) -------------------
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+            const int x = X0s + TILE * (q & 1) + (tid % TILE), y = Y0s + TILE * (q >> 1) + tid / TILE;
+            if (x < a.W && y < a.H) {
+                PixelScales ps;
                 const float *cv = a.cov + (size_t)(img / a.channels) * 3 * ipl + (size_t)y * a.W + x;
                 pixel_scales(__ldg(cv), __ldg(cv + ipl), __ldg(cv + 2 * ipl), a.policy, a.clamp, R, ps);
-            }
-            const bool live = valid && !(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
-            const int var = ps.drop + 1;
-            s_info[tid] = ps.basis | (var << 1) | (live ? 16 : 0) | (ps.clamped ? 32 : 0) | (ps.flags << 8);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) s_ap[tid * 4 + k] = ps.ap[k];
-            if (live) {
-                double ex = 0.0, ey = 0.0;
-                for (int k = 0; k < 4; ++k) {
-                    ex += ps.ap[k] * abs(c_steps[ps.basis][k][0]);
-                    ey += ps.ap[k] * c_steps[ps.basis][k][1];
+                if (!(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO))) {
+                    double ex = 0.0, ey = 0.0;
+                    for (int k = 0; k < 4; ++k) {
+                        ex += ps.ap[k] * abs(c_steps[ps.basis][k][0]);
+                        ey += ps.ap[k] * c_steps[ps.basis][k][1];
+                    }
+                    atomicMax(&s_ex[ps.basis], (int)ceil(0.5 * R * ex));
+                    atomicMax(&s_ey[ps.basis], (int)ceil(0.5 * R * ey));
+                    atomicOr(&s_vmask[ps.basis], 1 << (ps.drop + 1));
                 }
-                atomicMax(&s_ex[ps.basis], (int)ceil(0.5 * R * ex));
-                atomicMax(&s_ey[ps.basis], (int)ceil(0.5 * R * ey));
-                atomicOr(&s_vmask[ps.basis], 1 << var);
             }
         }
         __syncthreads();
@@ -318,7 +325,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (tid == 0) {
             int np = 0;
             for (int b = 0; b < 2; ++b) {
-                TileDomain d = tile_domain(luts[b], R, x0, y0, s_ex[b], s_ey[b]);
+                TileDomain d = fused_domain(luts[b], R, X0s, Y0s, s_ex[b], s_ey[b]);
                 s_dom[b][0] = d.X0;
                 s_dom[b][1] = d.Y0;
                 s_dom[b][2] = d.NX;
@@ -333,17 +340,19 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         }
         __syncthreads();
         if (s_bad) {
-            // domain exceeds the plan's capacity: flag every pixel (cannot happen
-            // when max_sigma bounds the covariance field)
-            const int x = x0 + (tid % TILE), y = y0 + tid / TILE;
-            const bool mine = a.pts ? (tid == want) : (x < a.W && y < a.H);
-            if (mine) {
-                const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
-                if (a.out_f32 && !a.pts)
-                    ((float *)a.out)[oidx] = __int_as_float(0x7fc00000);
-                else
-                    ((double *)a.out)[oidx] = __longlong_as_double(0x7ff8000000000000LL);
-                if (a.stats) atomicOr(a.stats + 4, (unsigned long long)FLAG_RANGE);
+            // domain exceeds the plan's capacity: NaN for every pixel (cannot
+            // happen when max_sigma bounds the covariance field)
+            for (int q = 0; q < 4; ++q) {
+                const int x = X0s + TILE * (q & 1) + (tid % TILE), y = Y0s + TILE * (q >> 1) + tid / TILE;
+                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H);
+                if (mine) {
+                    const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
+                    if (a.out_f32 && !a.pts)
+                        ((float *)a.out)[oidx] = __int_as_float(0x7fc00000);
+                    else
+                        ((double *)a.out)[oidx] = __longlong_as_double(0x7ff8000000000000LL);
+                    if (a.stats) atomicOr(a.stats + 4, (unsigned long long)FLAG_RANGE);
+                }
             }
             __syncthreads();
             continue;
@@ -425,6 +434,30 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         __syncthreads();
         FUSED_PHASE(2);
 
+        // ---- sub-tiles: per-pixel scales, then 4-5 ------------------------------
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+        if (a.pts && q != qwant) continue;
+        const int x0 = X0s + TILE * (q & 1), y0 = Y0s + TILE * (q >> 1);
+        {
+            const int x = x0 + (tid % TILE), y = y0 + tid / TILE;
+            PixelScales ps;
+            ps.flags = 0;
+            ps.basis = 0;
+            ps.drop = -1;
+            ps.clamped = 0;
+            ps.ap[0] = ps.ap[1] = ps.ap[2] = ps.ap[3] = 0.0;
+            const bool valid = x < a.W && y < a.H;
+            if (valid) {
+                const float *cv = a.cov + (size_t)(img / a.channels) * 3 * ipl + (size_t)y * a.W + x;
+                pixel_scales(__ldg(cv), __ldg(cv + ipl), __ldg(cv + 2 * ipl), a.policy, a.clamp, R, ps);
+            }
+            const bool live = valid && !(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
+            s_info[tid] = ps.basis | ((ps.drop + 1) << 1) | (live ? 16 : 0) | (ps.clamped ? 32 : 0) | (ps.flags << 8);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s_ap[tid * 4 + k] = ps.ap[k];
+        }
+        __syncthreads();
         // ---- 4-5. taps bucketed by key, gather, per-pixel sums -------------------
         // Items are numbered tap-major, i = t * P + p (p the pixel within the
         // chunk), and bucketed by a STABLE counting sort, so a 16-lane group
@@ -624,6 +657,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             __syncthreads();
             FUSED_PHASE(5);
         }
+        }  // sub-tiles
     }
 }
 

@@ -79,7 +79,7 @@ struct TileArgs {
     unsigned long long *prof;  // optional [8] phase cycles (bsf_debug_phase_cycles)
 };
 constexpr int TILE = 16;
-size_t tile_capacity(int order, float max_sigma, const LutBasis *host_luts, int basis_mask);
+size_t tile_capacity(int order, float max_sigma, const LutBasis *host_luts, int basis_mask, int tile);
 int tile_slots();
 cudaError_t launch_tile_impl(const TileArgs &a, int order, int precision, int slots, cudaStream_t st,
                              const LutBasis *luts_dev, long long *nlaunch);

@@ -822,13 +822,13 @@ __global__ void __launch_bounds__(256, BSF_TILE_MINB) tile_kernel(TileArgs a, co
     }
 }
 
-size_t tile_capacity(int order, float max_sigma, const LutBasis *L, int basis_mask) {
+size_t tile_capacity(int order, float max_sigma, const LutBasis *L, int basis_mask, int tile) {
     int E = (int)ceil((double)max_sigma * sqrt(24.0 * order)) + 1;  // (r/2) sum_k a'_k |s_k| bound
     size_t cap = 0;
     for (int b = 0; b < 2; ++b) {
         if (!(basis_mask & (1 << b))) continue;
-        size_t nx = TILE + 2 * E + (L[b].wxmax - L[b].wxmin) + 4 * order + 4;
-        size_t ny = TILE + 2 * E + L[b].wymax + 2;
+        size_t nx = tile + 2 * E + (L[b].wxmax - L[b].wxmin) + 4 * order + 4;
+        size_t ny = tile + 2 * E + L[b].wymax + 2;
         cap = nx * ny > cap ? nx * ny : cap;
     }
     return cap;
