@@ -1,15 +1,17 @@
 """Benchmark: megapixels/s of (pre-integration + space-variant filter).
 
-python bench.py --gpus N --steps K --warmup W [--config 2] [--impl reference]
+python bench.py --gpus N --steps K --warmup W [--config 2] [--anchor tile|global] [--impl reference]
 
-One step = one pass of the whole hot path (bsf_run: pre-integration of every
-basis in use + the per-pixel finite-difference gather) over the config's
-synthetic input, already resident in HBM.  Default workload: config 2 of
-BASELINE.json (1024^2 f32, order 2, dual basis).  For N > 1 (torchrun, one
-rank per GPU) every rank filters its own image (independent problems: weak
-scaling); time = max over ranks.  The L2 (126 MB) is flushed between timed
-steps (the working set, ~65 MB, would fit); each step is timed with CUDA
-events on the launching stream, flush excluded.
+One step = one pass of the whole hot path over the config's synthetic input,
+already resident in HBM.  Default (--anchor tile): bsf_run with the running
+sums anchored per 32x32 super-tile and the exact split contraction on the FP64
+tensor cores, ONE fused kernel.  --anchor global: the paper's
+single global pre-integration (bsf_preintegrate) + bsf_filter.  Default
+workload: config 2 of BASELINE.json (1024^2 f32, order 2, dual basis).  For
+N > 1 (torchrun, one rank per GPU) every rank filters its own image
+(independent problems: weak scaling); time = max over ranks.  The L2 (126 MB)
+is flushed between timed steps; each step is timed with CUDA events on the
+launching stream, flush excluded.
 
 --impl reference times the CPU oracle (the deliberately slow reference arm of
 this tier) on bounded pixel samples of the same workload, on rank 0 only.
@@ -91,6 +93,11 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def _fp64_peak():
+    with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as fh:
+        return json.load(fh)
+
+
 def algorithmic_fma_per_px(order: int, basis_counts) -> float:
     """(r+1)^4 taps x N_r window x (M_r coefficients + 1)
     multiply-adds per pixel, weighted by the basis mix."""
@@ -167,7 +174,7 @@ def main():
     ap.add_argument("--order", type=int, default=0)
     ap.add_argument("--impl", default="bsf")
     ap.add_argument("--precision", default="dd", choices=["dd", "fp64", "auto"])
-    ap.add_argument("--anchor", default="global", choices=["global", "tile"])
+    ap.add_argument("--anchor", default="tile", choices=["global", "tile"])
     ap.add_argument("--ref-points", type=int, default=24)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -291,28 +298,50 @@ def main():
             pg.destroy_process_group()
         return
 
-    # --- roofline of the dominant kernel (the gather) ------------------------
+    # --- roofline of the dominant kernel ---------------------------------------
     peaks, src = _peaks()
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s: 64 DFMA/clk/SM
-    tp = stats["theta_prime"] / max(stats["pixels"], 1)
-    fma_px = algorithmic_fma_per_px(w.order, {0: 1 - tp, 1: tp})
-    gat = sum(gat_ms) / len(gat_ms)
-    achieved = 2 * fma_px * npx / (gat * 1e-3) / 1e12
-    pre = sum(pre_ms) / len(pre_ms)
     gh, gw = plan.geometry.g_height, plan.geometry.g_width
     nb = plan.geometry.nbases
     in_b = 1 if w.in_dtype == "u8" else 4
-    # algorithmic bytes of the pre-integration: read f once, write g (dd) once per basis
-    pre_bytes = npx * in_b + nb * gh * gw * 16
-    roof = {"bound": "alu", "kernel": "tile_kernel (fused pre-integration + gather)" if tile else "gather_kernel", "achieved": achieved, "peak": fp64_peak,
-            "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
-            "peak_source": "148 SM x 64 DFMA/clk x 2 x %.0f MHz (sm_max, %s)" % (sm_mhz, src),
-            "algorithmic_fma_per_px": fma_px, "gather_ms": gat,
-            "share_of_step": gat / ms if ms else None,
-            "preintegration": {"bound": "hbm", "ms": pre, "achieved_gbs": pre_bytes / (pre * 1e-3) / 1e9,
-                               "peak_gbs": peaks.get("hbm_gbs"), "frac": pre_bytes / (pre * 1e-3) / 1e9 /
-                               peaks.get("hbm_gbs", 6650.0), "algorithmic_bytes": pre_bytes}}
+    gat = sum(gat_ms) / len(gat_ms)
+    pre = sum(pre_ms) / len(pre_ms)
+    if tile and plan.uses_fused():
+        # one fused kernel (pre-integration + exact split contraction on the FP64
+        # tensor cores); algorithmic work = the interpolation multiply-adds of
+        # Eq. (11) the kernel counted (window x monomials per tap, no padding)
+        fp = _fp64_peak()
+        macs_px = stats["macs"] / max(stats["pixels"], 1)
+        achieved = 2.0 * macs_px * npx / (gat * 1e-3) / 1e12
+        plan.phase_cycles(reset=True)  # enables the counters (diagnostic pass, untimed)
+        plan.run(img, cov, out, stream)
+        plan.phase_cycles(reset=True)
+        plan.run(img, cov, out, stream)
+        cyc = plan.phase_cycles()
+        tot = float(sum(cyc[:6])) or 1.0
+        names = ["scales", "pre_integration", "exact_split", "keys_sort", "gather", "accumulate"]
+        roof = {"bound": "fp64-tensor", "kernel": "fused_kernel (pre-integration + gather, DMMA m8n8k4)",
+                "achieved": achieved, "peak": fp["fp64_tensor_peak_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / fp["fp64_tensor_peak_tflops"], "traffic": None,
+                "peak_source": "measured: tools/fp64_peak.cu DMMA m8n8k4 (profiles/r01_fp64_peak.json)",
+                "algorithmic_macs_per_px": macs_px, "executed_limbs": 2, "kernel_ms": gat,
+                "share_of_step": gat / ms if ms else None,
+                "phase_share": {n: c / tot for n, c in zip(names, cyc)}}
+    else:
+        fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s: 64 DFMA/clk/SM
+        tp = stats["theta_prime"] / max(stats["pixels"], 1)
+        fma_px = algorithmic_fma_per_px(w.order, {0: 1 - tp, 1: tp})
+        achieved = 2 * fma_px * npx / (gat * 1e-3) / 1e12
+        # algorithmic bytes of the pre-integration: read f once, write g (dd) once per basis
+        pre_bytes = npx * in_b + nb * gh * gw * 16
+        roof = {"bound": "alu", "kernel": "tile_kernel (dd, fused)" if tile else "gather_kernel",
+                "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                "traffic": None, "peak_source": "148 SM x 64 DFMA/clk x 2 x %.0f MHz (sm_max, %s)" % (sm_mhz, src),
+                "algorithmic_fma_per_px": fma_px, "gather_ms": gat,
+                "share_of_step": gat / ms if ms else None,
+                "preintegration": {"bound": "hbm", "ms": pre, "achieved_gbs": pre_bytes / (pre * 1e-3) / 1e9,
+                                   "peak_gbs": peaks.get("hbm_gbs"), "frac": pre_bytes / (pre * 1e-3) / 1e9 /
+                                   peaks.get("hbm_gbs", 6650.0), "algorithmic_bytes": pre_bytes}}
     cb = None
     if not args.no_cpu_baseline:
         cb = cpu_baseline(w, args.cpu_budget, 400)
@@ -321,14 +350,15 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "width": w.width, "height": w.height, "order": w.order,
                        "basis": "dual" if w.basis == 2 else str(w.basis), "in_dtype": w.in_dtype,
-                       "precision": {"dd": "double-double", "fp64": "fp64",
-                                     "auto": "fp64 + a-posteriori bound, double-double fallback"}[args.precision],
+                       "precision": ("exact split contraction (2 fp64 limbs)" if tile and plan.uses_fused() else
+                                     {"dd": "double-double", "fp64": "fp64",
+                                      "auto": "fp64 + a-posteriori bound, double-double fallback"}[args.precision]),
                        "anchor": args.anchor,
                        "l2": "flushed between steps (256 MB write, untimed)", "parallelism": "dp%d" % world},
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
             "stats": {k: stats[k] for k in ("pixels", "clamped", "zero_scale", "theta_prime", "flags",
-                                            "double_double")}}
+                                            "double_double", "macs")}}
     print(json.dumps(line))
     if pg:
         pg.destroy_process_group()

@@ -107,6 +107,8 @@ typedef struct {
     long long theta_prime;   /* pixels filtered with basis Theta'                             */
     long long flags;         /* bit0 margin violation, bit1 infeasible, bit2 two zero scales  */
     long long double_double; /* pixels computed (or recomputed) in double-double              */
+    long long macs;          /* algorithmic multiply-adds of the interpolation (Eq. 11) in the */
+                             /* exact split path: sum over taps of window x monomials          */
 } bsf_stats;
 
 /* Create a plan: validates the descriptor, derives the margins, loads the

@@ -45,7 +45,7 @@ class bsf_geometry(ctypes.Structure):
 class bsf_stats(ctypes.Structure):
     _fields_ = [("pixels", ctypes.c_longlong), ("clamped", ctypes.c_longlong), ("zero_scale", ctypes.c_longlong),
                 ("theta_prime", ctypes.c_longlong), ("flags", ctypes.c_longlong),
-                ("double_double", ctypes.c_longlong)]
+                ("double_double", ctypes.c_longlong), ("macs", ctypes.c_longlong)]
 
 
 _lib = None

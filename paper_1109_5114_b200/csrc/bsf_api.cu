@@ -160,15 +160,22 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         // tensor-core fragments): per region nslot4 = nmax rounded up to 4 window
         // slots, per slot nmonp = nmon rounded up to 8 monomials (zero padded),
         // monomials in the gen_lut order; offsets padded alike with (0, 0).
-        V.nmonp = (V.nmon + 7) & ~7;
+        if (bsf_nt(V.deg) < 0) return set_err(BSF_EUNSUPPORTED, "no MMA column layout for this table degree");
+        V.nmonp = 8 * bsf_nt(V.deg);
         V.nslot4 = (V.nmax + 3) & ~3;
+        std::vector<int> col(V.nmon);
+        {
+            int m = 0;
+            for (int i = V.deg; i >= 0; --i)  // gen_lut order: x-major, i and j descending
+                for (int j = V.deg - i; j >= 0; --j) col[m++] = bsf_mono_col(V.deg, i, j);
+        }
         std::vector<double> nump((size_t)nreg * V.nslot4 * V.nmonp, 0.0);
         std::vector<int2> offs4((size_t)nreg * V.nslot4, make_int2(0, 0));
         for (uint32_t r = 0; r < nreg; ++r)
             for (int sl = 0; sl < V.nmax; ++sl) {
                 offs4[(size_t)r * V.nslot4 + sl] = offs[(size_t)r * V.nmax + sl];
                 for (int m = 0; m < V.nmon; ++m)
-                    nump[((size_t)r * V.nslot4 + sl) * V.nmonp + m] = num[((size_t)r * V.nmax + sl) * V.nmon + m];
+                    nump[((size_t)r * V.nslot4 + sl) * V.nmonp + col[m]] = num[((size_t)r * V.nmax + sl) * V.nmon + m];
             }
         double colmax = 0.0;  // max over (region, monomial) of sum_s |n|
         for (uint32_t r = 0; r < nreg; ++r)
@@ -177,6 +184,18 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
                 for (int s = 0; s < V.nmax; ++s) cs += fabs(num[((size_t)r * V.nmax + s) * V.nmon + m]);
                 colmax = cs > colmax ? cs : colmax;
             }
+        // a-posteriori bound of the G0 limb (bsf_fused.cuh): |F^ - F| <= gamma_{n+1} 0.5 sum_s,mu |n_s,mu|
+        {
+            double worst = 0.0;
+            for (uint32_t r = 0; r < nreg; ++r) {
+                double t = 0.0;
+                for (int sl = 0; sl < V.nmax; ++sl)
+                    for (int m = 0; m < V.nmon; ++m) t += fabs(num[((size_t)r * V.nmax + sl) * V.nmon + m]);
+                worst = t > worst ? t : worst;
+            }
+            const double u = 1.1102230246251565e-16, nn = V.nslot4 + 1;
+            V.bnd = (nn * u / (1.0 - nn * u)) * 0.5 * worst;
+        }
         // sums of G1 * n stay exact while |G1| sum|n| <= 2^53
         int cm = 0;
         while (ldexp(1.0, cm) < colmax) ++cm;
@@ -433,6 +452,9 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.nty = (p->geo.H + TILE - 1) / TILE;
     a.stats = p->stats;
     a.prof = p->prof;
+    // BSF_SPLIT_TOL (environment, diagnostics): override the fallback threshold
+    const char *tol = getenv("BSF_SPLIT_TOL");
+    a.split_tol = tol ? atof(tol) : BSF_SPLIT_TOL_DEFAULT;
     return a;
 }
 
@@ -520,6 +542,7 @@ extern "C" bsf_status bsf_get_stats(bsf_plan_t p, bsf_stats *s, int reset) {
     s->theta_prime = (long long)h[3];
     s->flags = (long long)h[4];
     s->double_double = (long long)h[5];
+    s->macs = (long long)h[6];
     if (reset) CUDA_TRY(cudaMemset(p->stats, 0, sizeof h));
     if (s->flags & FLAG_RANGE_H) return set_err(BSF_ERANGE, "a tap window left the pre-integration domain");
     if (s->flags & FLAG_INFEASIBLE_H) return set_err(BSF_EINFEASIBLE, "covariance outside the elongation bound");

@@ -29,6 +29,7 @@ constexpr int NKEY = 2 * NVAR * MAX_REG;      // (basis, variant, region)
 constexpr int NPLANE = 2 * NVAR;              // (basis, variant)
 constexpr uint16_t NOKEY = 0xFFFF;
 
+
 template <int R> struct FusedCfg;
 // NTAP taps per pixel, P pixels per chunk, MT 8-item m-tiles per group
 template <> struct FusedCfg<1> { static constexpr int NTAP = 16, P = 256, MT = 2; };
@@ -37,15 +38,10 @@ template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 16, MT = 1
 template <> struct FusedCfg<4> { static constexpr int NTAP = 625, P = 4, MT = 1; };
 
 template <int R>
-constexpr size_t fused_escratch_doubles() {  // per warp: [limb][mu][item], item stride GS + 1
-    return (size_t)2 * ((((4 * R - 1) * (4 * R) / 2) + 7) / 8 * 8) * (8 * FusedCfg<R>::MT + 1);
-}
-
-template <int R>
 constexpr size_t fused_smem_bytes() {
     constexpr size_t ITEMS = (size_t)FusedCfg<R>::P * FusedCfg<R>::NTAP;
     constexpr size_t GS = 8 * FusedCfg<R>::MT;
-    return ITEMS * 16 + (FT / 32) * fused_escratch_doubles<R>() * 8 + FT * 4 * 8 + ITEMS * 2 +
+    return ITEMS * 16 + FT * 4 * 8 + ITEMS * 2 +
            (ITEMS + GS * NKEY) * 2 + (FT / 32) * NKEY * 4 + FT * 4;
 }
 
@@ -122,21 +118,65 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 template <int DEG>
 struct DegCfg {
     static constexpr int NMON = (DEG + 1) * (DEG + 2) / 2;
-    static constexpr int NT = (NMON + 7) / 8;  // 8-monomial n-tiles
+    static constexpr int NT = bsf_nt(DEG);  // 8-column n-tiles (bsf_mono_col layout)
 };
+
+// Row polynomials R_i(phi_y) owned by lane LANE of the quad (compensated
+// Horner over the accumulator slots of row i, highest y power first).
+template <int DEG, int NT, int LANE, int I>
+__device__ __forceinline__ void fused_rows(const double (&C)[2][NT][2], double fy, double (&Rh)[DEG + 1],
+                                           double (&Rl)[DEG + 1]) {
+    if constexpr (I <= DEG) {
+        if constexpr (bsf_row_lane(DEG, I) == LANE) {
+            constexpr int S0 = bsf_row_slot(DEG, I);
+            double rh = 0.0, rl = 0.0;
+#pragma unroll
+            for (int k = 0; k <= DEG - I; ++k) {
+                const int sl = S0 + k;
+                const dd e = two_sum(C[0][sl >> 1][sl & 1], C[1][sl >> 1][sl & 1]);
+                if (k == 0) {
+                    rh = e.hi;
+                    rl = e.lo;
+                } else {
+                    comp_step(rh, rl, fy, e.hi, e.lo);
+                }
+            }
+            Rh[I] = rh;
+            Rl[I] = rl;
+        }
+        fused_rows<DEG, NT, LANE, I + 1>(C, fy, Rh, Rl);
+    }
+}
+
+// Horner scheme in phi_x over the rows, gathered from the quad's lanes.
+template <int DEG, int I>
+__device__ __forceinline__ void fused_xhorner(const double (&Rh)[DEG + 1], const double (&Rl)[DEG + 1], double fx,
+                                              double &ah, double &al) {
+    constexpr int SRC = bsf_row_lane(DEG, I);
+    const int src = (threadIdx.x & 28) | SRC;
+    const double h = __shfl_sync(0xffffffffu, Rh[I], src), l = __shfl_sync(0xffffffffu, Rl[I], src);
+    if constexpr (I == DEG) {
+        ah = h;
+        al = l;
+    } else {
+        comp_step(ah, al, fx, h, l);
+    }
+    if constexpr (I > 0) fused_xhorner<DEG, I - 1>(Rh, Rl, fx, ah, al);
+}
 
 // Contraction of one group of GS = 8 MT items sharing a key, on the FP64
 // tensor cores: for every item (M), window slot (K) and monomial (N)
 //   E_mu = sum_s G1_s n_{s,mu}  (exact)   and   sum_s G0_s n_{s,mu},
-// the two limbs as separate accumulators.  (bx_t, by_t): tap base of the
-// item this lane feeds in m-tile t; the result goes to the warp's scratch
-// E[limb][mu][item] (item stride GS + 1).
+// the two limbs as separate accumulators; then F = sum_mu E_mu phi^mu straight
+// from the accumulator fragments (rows per lane in phi_y, then phi_x across
+// the quad), compensated.  Lane l feeds and receives item l/4 + 8t of m-tile
+// t; (bxt, byt, fxt, fyt) are that item's tap base and fractional offset.
 template <int DEG, int MT>
 __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
-                                            const int (&byt)[MT], const int2 *__restrict__ offs,
-                                            const double *__restrict__ num, int nmonp, int n4, double *E,
-                                            int &flags) {
-    constexpr int NT = DegCfg<DEG>::NT, GS = 8 * MT, ES = GS + 1;
+                                            const int (&byt)[MT], const double (&fxt)[MT], const double (&fyt)[MT],
+                                            const int2 *__restrict__ offs, const double *__restrict__ num, int nmonp,
+                                            int n4, double (&Fh)[MT], double (&Fl)[MT], int &flags) {
+    constexpr int NT = DegCfg<DEG>::NT;
     const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
     double C[MT][2][NT][2];
 #pragma unroll
@@ -192,62 +232,38 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
                 dmma(C[t][1][j], aB[t].y, bB[j]);
             }
     }
-    const int NMP = NT * 8;
 #pragma unroll
-    for (int t = 0; t < MT; ++t)
+    for (int t = 0; t < MT; ++t) {
+        double Rh[DEG + 1], Rl[DEG + 1];
 #pragma unroll
-        for (int L = 0; L < 2; ++L)
-#pragma unroll
-            for (int j = 0; j < NT; ++j)
-#pragma unroll
-                for (int q = 0; q < 2; ++q)
-                    E[(L * NMP + 8 * j + 2 * kq + q) * ES + gq + 8 * t] = C[t][L][j][q];
-}
-
-// F = sum_mu (E1_mu + E0_mu) phi^mu for one item (monomials x-major, i
-// descending, j descending: the gen_lut order), compensated: first the DEG+1
-// independent row polynomials R_i(phi_y) (interleaved, so their dependency
-// chains overlap), then the Horner scheme in phi_x over the rows.
-template <int DEG, int GS>
-__device__ __forceinline__ dd fused_horner(const double *E, int item, double fx, double fy) {
-    constexpr int NMP = DegCfg<DEG>::NT * 8, ES = GS + 1;
-    double rh[DEG + 1], rl[DEG + 1];
-    // highest y power of every row first
-#pragma unroll
-    for (int i = 0; i <= DEG; ++i) {
-        const int m = (DEG - i) * (DEG - i + 1) / 2;  // row i starts with phi_y^(DEG-i)
-        const dd e = two_sum(E[m * ES + item], E[(NMP + m) * ES + item]);
-        rh[i] = e.hi;
-        rl[i] = e.lo;
-    }
-#pragma unroll
-    for (int k = 1; k <= DEG; ++k)
-#pragma unroll
-        for (int i = 0; i <= DEG - k; ++i) {  // row i has DEG - i + 1 terms
-            const int m = (DEG - i) * (DEG - i + 1) / 2 + k;
-            const dd e = two_sum(E[m * ES + item], E[(NMP + m) * ES + item]);
-            comp_step(rh[i], rl[i], fy, e.hi, e.lo);
+        for (int i = 0; i <= DEG; ++i) Rh[i] = Rl[i] = 0.0;
+        switch (kq) {
+            case 0: fused_rows<DEG, NT, 0, 0>(C[t], fyt[t], Rh, Rl); break;
+            case 1: fused_rows<DEG, NT, 1, 0>(C[t], fyt[t], Rh, Rl); break;
+            case 2: fused_rows<DEG, NT, 2, 0>(C[t], fyt[t], Rh, Rl); break;
+            default: fused_rows<DEG, NT, 3, 0>(C[t], fyt[t], Rh, Rl); break;
         }
-    double ah = rh[DEG], al = rl[DEG];
-#pragma unroll
-    for (int i = DEG - 1; i >= 0; --i) comp_step(ah, al, fx, rh[i], rl[i]);
-    return fast_two_sum(ah, al);
+        double ah, al;
+        fused_xhorner<DEG, DEG>(Rh, Rl, fxt[t], ah, al);
+        const dd F = fast_two_sum(ah, al);
+        Fh[t] = F.hi;
+        Fl[t] = F.lo;
+    }
 }
 
 template <int R>
 __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
     constexpr int NTAP = FusedCfg<R>::NTAP, P = FusedCfg<R>::P, ITEMS = P * NTAP;
     constexpr int MT = FusedCfg<R>::MT, GS = 8 * MT;
-    constexpr int ESZ = (int)fused_escratch_doubles<R>();
     extern __shared__ __align__(16) unsigned char smem[];
     double2 *s_F = reinterpret_cast<double2 *>(smem);
-    double *s_E = reinterpret_cast<double *>(s_F + ITEMS);  // [warp][ESZ]
-    double *s_ap = s_E + (FT / 32) * ESZ;
+    double *s_ap = reinterpret_cast<double *>(s_F + ITEMS);
     uint16_t *s_key = reinterpret_cast<uint16_t *>(s_ap + FT * 4);
     uint16_t *s_sorted = s_key + ITEMS;
     int *s_hist = reinterpret_cast<int *>(s_sorted + ITEMS + GS * NKEY);  // [warp][key]
     int *s_info = s_hist + (FT / 32) * NKEY;
-    __shared__ int s_item, s_ex[2], s_ey[2], s_vmask[2], s_bad, s_npad, s_any;
+    __shared__ int s_item, s_ex[2], s_ey[2], s_vmask[2], s_bad, s_npad, s_any, s_nfb;
+    __shared__ short s_fb[FT];
     __shared__ int s_dom[2][4];
     __shared__ long long s_poff[NPLANE];
     __shared__ int s_pe[NPLANE];
@@ -277,6 +293,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             s_bad = 0;
         }
         if (tid < NPLANE) s_pmax[tid] = 0ull;
+        if (tid == 0) s_nfb = 0;
         __syncthreads();
         const int item = s_item;
         if (item >= nitems) break;
@@ -543,10 +560,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             __syncthreads();
             FUSED_PHASE(3);
             // gather: groups of GS items sharing one key, one warp per group,
-            // contraction on the FP64 tensor cores, Horner on lanes < GS
+            // contraction on the FP64 tensor cores, polynomial from the fragments
             {
                 const int ngroups = npad / GS;
-                double *E = s_E + warp * ESZ;
                 int flags = 0;
                 for (int g = warp; g < ngroups; g += FT / 32) {
                     const int i0 = s_sorted[g * GS];
@@ -562,34 +578,49 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     const double flx = floor(Dx), fly = floor(Dy);
                     const int bx = x0 + (p % TILE) + (int)flx - s_dom[b][0];
                     const int by = y0 + p / TILE + (int)fly - s_dom[b][1];
-                    int bxt[MT], byt[MT];
+                    const double fx = Dx - flx, fy = Dy - fly;
+                    int bxt[MT], byt[MT], idt[MT];
+                    double fxt[MT], fyt[MT];
+                    bool realt[MT];
 #pragma unroll
                     for (int q = 0; q < MT; ++q) {
-                        bxt[q] = __shfl_sync(0xffffffffu, bx, (lane >> 2) + 8 * q);
-                        byt[q] = __shfl_sync(0xffffffffu, by, (lane >> 2) + 8 * q);
+                        const int src = (lane >> 2) + 8 * q;
+                        bxt[q] = __shfl_sync(0xffffffffu, bx, src);
+                        byt[q] = __shfl_sync(0xffffffffu, by, src);
+                        fxt[q] = __shfl_sync(0xffffffffu, fx, src);
+                        fyt[q] = __shfl_sync(0xffffffffu, fy, src);
+                        idt[q] = __shfl_sync(0xffffffffu, idx, src);
+                        realt[q] = __shfl_sync(0xffffffffu, (int)real, src) != 0;
                     }
                     const double2 *G = scr + s_poff[b * NVAR + var];
                     const LutVar &V = luts[b].var[var];
                     const int n4 = (__ldg(V.counts + reg) + 3) & ~3;
                     const int NX = s_dom[b][2], NY = s_dom[b][3];
-                    dd F;
+                    const int2 *offs = V.offs4 + (size_t)reg * V.nslot4;
+                    const double *num = V.num + (size_t)reg * V.nslot4 * V.nmonp;
+                    double Fh[MT], Fl[MT];
+                    if (a.stats) {  // algorithmic work: window x monomials per real item
+                        const unsigned nreal = __popc(__ballot_sync(0xffffffffu, real));
+                        if (lane == 0)
+                            atomicAdd(a.stats + 6, (unsigned long long)nreal * __ldg(V.counts + reg) *
+                                                       (var == 0 ? DegCfg<4 * R - 2>::NMON : DegCfg<3 * R - 2>::NMON));
+                    }
                     long long tq0 = 0;
                     if (a.prof && lane == 0) tq0 = clock64();
-                    if (var == 0) {
-                        fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, V.offs4 + (size_t)reg * V.nslot4,
-                                                   V.num + (size_t)reg * V.nslot4 * V.nmonp, V.nmonp, n4, E, flags);
-                        __syncwarp();
-                        if (a.prof && lane == 0) atomicAdd(a.prof + 7, (unsigned long long)(clock64() - tq0));
-                        if (lane < GS) F = fused_horner<4 * R - 2, GS>(E, lane, Dx - flx, Dy - fly);
-                    } else {
-                        fused_group<3 * R - 2, MT>(G, NX, NY, bxt, byt, V.offs4 + (size_t)reg * V.nslot4,
-                                                   V.num + (size_t)reg * V.nslot4 * V.nmonp, V.nmonp, n4, E, flags);
-                        __syncwarp();
-                        if (lane < GS) F = fused_horner<3 * R - 2, GS>(E, lane, Dx - flx, Dy - fly);
+                    if (var == 0)
+                        fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.nmonp, n4, Fh, Fl, flags);
+                    else
+                        fused_group<3 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.nmonp, n4, Fh, Fl, flags);
+                    if ((lane & 3) == 0) {
+#pragma unroll
+                        for (int q = 0; q < MT; ++q)
+                            if (realt[q]) s_F[idt[q]] = make_double2(Fh[q], Fl[q]);
                     }
-                    if (lane < GS && real) s_F[idx] = make_double2(F.hi, F.lo);
-                    __syncwarp();
-                    if (a.prof && lane == 0) atomicAdd(a.prof + 6, (unsigned long long)(clock64() - tq0));
+                    if (a.prof && lane == 0) {
+                        const unsigned long long dt = clock64() - tq0;
+                        atomicAdd(a.prof + 6, dt);
+                        if (var == 0) atomicAdd(a.prof + 7, dt);
+                    }
                 }
                 if (flags && a.stats) atomicOr(a.stats + 4, (unsigned long long)flags);
             }
@@ -604,23 +635,28 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 const int w = s_info[p];
                 const int b = info_basis(w), var = info_var(w);
                 dd S = {0.0, 0.0};
+                double sumCF = 0.0;  // sum_j |c_j F_j| (for the double-double rounding term)
                 if (info_live(w)) {
                     const int ntap = var ? NTAP / (R + 1) : NTAP;
                     for (int t = sub; t < ntap; t += TPP) {
                         const double2 F = s_F[t * P + pl];
-                        S = dd_add(S, dd_mul_d({F.x, F.y}, (double)tap_coef<R>(t, var - 1)));
+                        const double c = (double)tap_coef<R>(t, var - 1);
+                        S = dd_add(S, dd_mul_d({F.x, F.y}, c));
+                        sumCF += fabs(c * F.x);
                     }
                 }
 #pragma unroll
                 for (int o = 1; o < TPP; o <<= 1) {
                     const dd T = {__shfl_xor_sync(0xffffffffu, S.hi, o), __shfl_xor_sync(0xffffffffu, S.lo, o)};
                     S = dd_add(S, T);
+                    sumCF += __shfl_xor_sync(0xffffffffu, sumCF, o);
                 }
                 const int x = x0 + (p % TILE), y = y0 + p / TILE;
                 const bool valid = x < a.W && y < a.H;
                 const bool mine = sub == 0 && (a.pts ? (p == want) : valid);
                 if (mine) {
                     double res = __longlong_as_double(0x7ff8000000000000LL);
+                    double erel = 0.0;
                     if (info_live(w)) {
                         double norm = 1.0;
                         for (int k = 0; k < 4; ++k) {
@@ -628,7 +664,17 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                             const double ia = 1.0 / s_ap[4 * p + k];
                             for (int i = 0; i < R; ++i) norm *= ia;
                         }
-                        res = ldexp(dd_to_d(S), s_pe[b * NVAR + var]) * norm / luts[b].var[var].L;
+                        const double Sd = dd_to_d(S);
+                        res = ldexp(Sd, s_pe[b * NVAR + var]) * norm / luts[b].var[var].L;
+                        // a-posteriori bound of the split contraction:
+                        // |S^ - S| <= sum_j |c_j| bnd + 4 u^2 sum_j |c_j F_j|, sum_j |c_j| = 2^(R ns)
+                        const int ns = var ? 3 : 4;
+                        const double err = ldexp(luts[b].var[var].bnd, R * ns) + 5e-32 * sumCF;
+                        erel = err / fabs(Sd);
+                        if (!(erel <= a.split_tol)) {  // NaN-safe: recompute in double-double
+                            const int k = atomicAdd(&s_nfb, 1);
+                            s_fb[k] = (short)p;
+                        }
                     }
                     const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
                     if (a.aux) {
@@ -639,7 +685,8 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         ax[3] = w >> 8;
                         for (int k = 0; k < 4; ++k) ax[4 + k] = s_ap[4 * p + k];
                         ax[8] = 0.0;
-                        ax[9] = ax[10] = ax[11] = 0.0;
+                        ax[9] = erel;
+                        ax[10] = ax[11] = 0.0;
                     }
                     if (a.out_f32 && !a.pts)
                         ((float *)a.out)[oidx] = (float)res;
@@ -655,7 +702,44 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 }
             }
             __syncthreads();
+            // double-double fallback for the pixels whose bound exceeds
+            // TileArgs::split_tol: one warp per pixel (mesh_warp) on the base
+            // plane, read back exactly from its split limbs
+            for (int i = warp; i < s_nfb; i += FT / 32) {
+                const int p = s_fb[i];
+                const int w = s_info[p];
+                PixelScales ps;
+                ps.basis = info_basis(w);
+                ps.drop = info_var(w) - 1;
+                ps.flags = 0;
+                ps.clamped = (w >> 5) & 1;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) ps.ap[k] = s_ap[4 * p + k];
+                const int b = ps.basis;
+                const double sc = (s_vmask[b] & 1) ? ldexp(1.0, s_pe[b * NVAR]) : 0.0;
+                GView gv = {scr + s_poff[b * NVAR], s_dom[b][0], s_dom[b][1], s_dom[b][2], s_dom[b][3], sc};
+                const int x = x0 + (p % TILE), y = y0 + p / TILE;
+                int fl = 0;
+                const double res = mesh_warp<R>(gv, luts[b], ps, x, y, &fl);
+                fl = __reduce_or_sync(0xffffffffu, fl);
+                if (lane == 0) {
+                    const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
+                    if (a.out_f32 && !a.pts)
+                        ((float *)a.out)[oidx] = (float)res;
+                    else
+                        ((double *)a.out)[oidx] = res;
+                    if (a.aux) a.aux[BSF_AUX * oidx + 8] = 1.0;
+                    if (a.stats) {
+                        atomicAdd(a.stats + 5, 1ull);
+                        if (fl) atomicOr(a.stats + 4, (unsigned long long)fl);
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid == 0) s_nfb = 0;
+            __syncthreads();
             FUSED_PHASE(5);
+
         }
         }  // sub-tiles
     }

@@ -13,6 +13,54 @@ constexpr int BSF_AUX = 12;  // doubles of per-point diagnostics
 enum { FLAG_RANGE_H = 1, FLAG_INFEASIBLE_H = 2, FLAG_TWO_ZERO_H = 4, FLAG_SOLVER_H = 8 };
 constexpr int NVAR = 5;  // full kernel + one per dropped direction
 
+// Column layout of the integer tables for the FP64 MMA contraction
+// (bsf_fused.cuh).  The N dimension (monomials phi_x^i phi_y^j, degree <= deg)
+// is padded to 8 bsf_nt(deg) columns; lane l of a warp holds accumulator
+// columns 8 j + 2 (l % 4) + {0, 1}.  Each polynomial row i (the DEG - i + 1
+// monomials of x-power i) is given whole to one lane of the quad, at
+// consecutive slots k (column 8 (k / 2) + 2 lane + k % 2), highest y power
+// first, so that lane can run the row's Horner scheme in phi_y on its own
+// registers.  Partition of the row lengths 1..deg+1 over the 4 lanes:
+__host__ __device__ constexpr int bsf_nt(int deg) {
+    return deg == 1 ? 1 : deg == 2 ? 2 : deg == 4 ? 3 : deg == 6 ? 4 : deg == 7 ? 5 : deg == 10 ? 9 : deg == 14 ? 15 : -1;
+}
+__host__ __device__ constexpr int bsf_part(int deg, int lane, int k) {  // k-th row length of a lane, 0 = end
+    const int t1[4][3] = {{2, 0, 0}, {1, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    const int t2[4][3] = {{3, 1, 0}, {2, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    const int t4[4][3] = {{5, 1, 0}, {4, 2, 0}, {3, 0, 0}, {0, 0, 0}};
+    const int t6[4][3] = {{7, 1, 0}, {6, 2, 0}, {5, 3, 0}, {4, 0, 0}};
+    const int t7[4][3] = {{8, 2, 0}, {7, 3, 0}, {6, 4, 0}, {5, 1, 0}};
+    const int t10[4][5] = {{11, 7, 0, 0, 0}, {10, 8, 0, 0, 0}, {9, 6, 3, 0, 0}, {5, 4, 2, 1, 0}};
+    const int t14[4][7] = {{15, 14, 1, 0, 0, 0, 0}, {13, 12, 5, 0, 0, 0, 0}, {11, 10, 9, 0, 0, 0, 0}, {8, 7, 6, 4, 3, 2, 0}};
+    return deg == 1 ? (k < 3 ? t1[lane][k] : 0)
+         : deg == 2 ? (k < 3 ? t2[lane][k] : 0)
+         : deg == 4 ? (k < 3 ? t4[lane][k] : 0)
+         : deg == 6 ? (k < 3 ? t6[lane][k] : 0)
+         : deg == 7 ? (k < 3 ? t7[lane][k] : 0)
+         : deg == 10 ? (k < 5 ? t10[lane][k] : 0)
+         : deg == 14 ? (k < 7 ? t14[lane][k] : 0) : 0;
+}
+__host__ __device__ constexpr int bsf_row_lane(int deg, int i) {  // lane holding row i
+    for (int l = 0; l < 4; ++l)
+        for (int k = 0; bsf_part(deg, l, k); ++k)
+            if (bsf_part(deg, l, k) == deg - i + 1) return l;
+    return -1;
+}
+__host__ __device__ constexpr int bsf_row_slot(int deg, int i) {  // first slot of row i in its lane
+    const int l = bsf_row_lane(deg, i);
+    int s = 0;
+    for (int k = 0; bsf_part(deg, l, k); ++k) {
+        if (bsf_part(deg, l, k) == deg - i + 1) return s;
+        s += bsf_part(deg, l, k);
+    }
+    return -1;
+}
+// accumulator column of monomial phi_x^i phi_y^j
+__host__ __device__ constexpr int bsf_mono_col(int deg, int i, int j) {
+    return 8 * ((bsf_row_slot(deg, i) + deg - i - j) >> 1) + 2 * bsf_row_lane(deg, i) +
+           ((bsf_row_slot(deg, i) + deg - i - j) & 1);
+}
+
 // One interpolation table (basis, order, variant) in device memory.
 struct LutVar {
     int deg, nmon, nmax;
@@ -21,9 +69,10 @@ struct LutVar {
     const double2 *coef;   // [nreg][nmax][nmon] double-double (n / L)
     const double *num;     // [nreg][nslot4][nmonp] integer numerators n (exact doubles), zero padded
     const int2 *offs4;     // [nreg][nslot4] window offsets, padded with (0, 0)
-    int nmonp;             // nmon rounded up to 8 (FP64 MMA n-tiles)
+    int nmonp;             // 8 bsf_nt(deg) columns (FP64 MMA n-tiles), bsf_mono_col layout
     int nslot4;            // nmax rounded up to 4 (FP64 MMA k-steps)
     int kbits;             // |G1| <= 2^kbits keeps sum_s G1 * n exact in fp64
+    double bnd;            // bound on |F - F^| (units 2^e) of the split contraction: gamma_{n+1} 0.5 max_reg sum_s,mu |n|
     double L;              // common denominator
 };
 
@@ -77,6 +126,7 @@ struct TileArgs {
     int ntx, nty;
     unsigned long long *stats;
     unsigned long long *prof;  // optional [8] phase cycles (bsf_debug_phase_cycles)
+    double split_tol;          // relative bound above which a pixel is recomputed in double-double
 };
 constexpr int TILE = 16;
 size_t tile_capacity(int order, float max_sigma, const LutBasis *host_luts, int basis_mask, int tile);
@@ -87,7 +137,8 @@ cudaError_t launch_tile_impl(const TileArgs &a, int order, int precision, int sl
 // exact split contraction path (bsf_fused.cuh): one persistent CTA per SM,
 // NPLANE_MAX planes of `cap` points per slot
 constexpr int NPLANE_MAX = 10;
-constexpr int KBITS_MIN = 20;  // tables whose exact limb would be narrower use the double-double tile kernel
+constexpr int KBITS_MIN = 20;
+constexpr double BSF_SPLIT_TOL_DEFAULT = 5e-10;  // half the fp64 parity tolerance; see TileArgs::split_tol  // tables whose exact limb would be narrower use the double-double tile kernel
 int fused_slots();
 cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStream_t st, const LutBasis *luts_dev,
                               long long *nlaunch);

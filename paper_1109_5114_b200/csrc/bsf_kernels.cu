@@ -373,6 +373,7 @@ __device__ __forceinline__ void horner2_comp_n(const double2 *__restrict__ c, in
 struct GView {
     const double2 *g;
     int X0, Y0, NX, NY;
+    double sc;  // 0: double-double {hi, lo}; else split limbs (G1, G0) of G = sc (G1 + G0) (bsf_fused.cuh)
 };
 
 __device__ __forceinline__ double2 load_g2(const GView &v, int qx, int qy, int *flags) {
@@ -382,7 +383,10 @@ __device__ __forceinline__ double2 load_g2(const GView &v, int qx, int qy, int *
         *flags |= FLAG_RANGE;
         return make_double2(0.0, 0.0);
     }
-    return v.g[(size_t)ly * v.NX + lx];  // plain load: tile scratch is written in-kernel
+    const double2 t = v.g[(size_t)ly * v.NX + lx];  // plain load: tile scratch is written in-kernel
+    if (v.sc == 0.0) return t;
+    const dd e = two_sum(t.x * v.sc, t.y * v.sc);  // exact: power-of-two scaling of both limbs
+    return make_double2(e.hi, e.lo);
 }
 
 // G' = (1 - T_{s_drop})^R G  (exact lattice difference, R5), double-double
@@ -521,6 +525,53 @@ __device__ double mesh(const GView &gv, const LutBasis &L, const PixelScales &ps
     return S * norm;
 }
 
+// Warp-cooperative double-double mesh (the exact split path's fallback,
+// bsf_fused.cuh): the lanes share the taps of ONE pixel, each interpolates its
+// taps in double-double, and the signed sum is reduced by shuffles.  All 32
+// lanes must call it with the same arguments; every lane returns the result.
+template <int R>
+__device__ double mesh_warp(const GView &gv, const LutBasis &L, const PixelScales &ps, int x, int y, int *flags) {
+    const int lane = threadIdx.x & 31;
+    int dirs[4];
+    int ns = 0;
+    for (int k = 0; k < 4; ++k)
+        if (k != ps.drop) dirs[ns++] = k;
+    const LutVar &V = L.var[ps.drop + 1];
+    int2 sdrop = make_int2(0, 0);
+    if (ps.drop >= 0) sdrop = make_int2(c_steps[ps.basis][ps.drop][0], c_steps[ps.basis][ps.drop][1]);
+    int ntap = 1;
+    for (int q = 0; q < ns; ++q) ntap *= (R + 1);
+    dd acc = {0.0, 0.0};
+    for (int t = lane; t < ntap; t += 32) {
+        int tt = t, coef = 1;
+        double Dx = 0.0, Dy = 0.0;
+        for (int q = 0; q < ns; ++q) {
+            const int j = tt % (R + 1);
+            tt /= (R + 1);
+            coef *= binom_small(R, j) * ((j & 1) ? -1 : 1);
+            const int k = dirs[q];
+            const double m = 0.5 * R - j;
+            Dx += (m * c_steps[ps.basis][k][0]) * ps.ap[k];  // exact (R17)
+            Dy += (m * c_steps[ps.basis][k][1]) * ps.ap[k];
+        }
+        const double flx = floor(Dx), fly = floor(Dy);
+        double sumG = 0.0;
+        const dd F = interp<R, true>(gv, L, V, x + (int)flx, y + (int)fly, Dx - flx, Dy - fly, ps.drop, sdrop, flags,
+                                     &sumG);
+        acc = dd_add(acc, dd_mul_d(F, (double)coef));
+    }
+    for (int o = 16; o; o >>= 1) {
+        const dd T = {__shfl_xor_sync(0xffffffffu, acc.hi, o), __shfl_xor_sync(0xffffffffu, acc.lo, o)};
+        acc = dd_add(acc, T);
+    }
+    double norm = 1.0;
+    for (int q = 0; q < ns; ++q) {
+        const double ia = 1.0 / ps.ap[dirs[q]];
+        for (int i = 0; i < R; ++i) norm *= ia;
+    }
+    return dd_to_d(acc) * norm;
+}
+
 // BSF_PREC_AUTO: fp64 first; recompute in double-double when the estimate
 // exceeds 1e-9 (the fp64 results kept were within 1.6e-11 in calibration).
 template <int R>
@@ -575,7 +626,7 @@ __global__ void __launch_bounds__(128, BSF_GATHER_MINB) gather_kernel(GatherArgs
         res = __longlong_as_double(0x7ff8000000000000LL);
     } else {
         int slot = geo.nbases == 2 ? ps.basis : 0;
-        GView gv = {a.g + ((size_t)slot * geo.nimg + img) * geo.GH * geo.GW, -geo.P, 0, geo.GW, geo.GH};
+        GView gv = {a.g + ((size_t)slot * geo.nimg + img) * geo.GH * geo.GW, -geo.P, 0, geo.GW, geo.GH, 0.0};
         if (MODE == BSF_PREC_AUTO)
             res = mesh_auto<R>(gv, luts[ps.basis], ps, x, y, &flags, &used_dd, ratios);
         else
@@ -751,7 +802,7 @@ __global__ void __launch_bounds__(256, BSF_TILE_MINB) tile_kernel(TileArgs a, co
         double ratios[2] = {0.0, 0.0};
         if (mine && live && !s_bad) {
             TileDomain d = tile_domain(luts[ps.basis], R, x0, y0, s_ex[ps.basis], s_ey[ps.basis]);
-            GView gv = {scr + (size_t)ps.basis * a.cap, d.X0, d.Y0, d.NX, d.NY};
+            GView gv = {scr + (size_t)ps.basis * a.cap, d.X0, d.Y0, d.NX, d.NY, 0.0};
             if (MODE == BSF_PREC_AUTO) {
                 double err = 1.0;
                 res = mesh<R, false>(gv, luts[ps.basis], ps, x, y, &flags, &err, ratios);
@@ -781,7 +832,7 @@ __global__ void __launch_bounds__(256, BSF_TILE_MINB) tile_kernel(TileArgs a, co
                 PixelScales q = s_ps[src];
                 int qx = x0 + (src % TILE), qy = y0 + src / TILE, qf = 0;
                 TileDomain d = tile_domain(luts[q.basis], R, x0, y0, s_ex[q.basis], s_ey[q.basis]);
-                GView gv = {scr + (size_t)q.basis * a.cap, d.X0, d.Y0, d.NX, d.NY};
+                GView gv = {scr + (size_t)q.basis * a.cap, d.X0, d.Y0, d.NX, d.NY, 0.0};
                 s_res[src] = mesh<R, true>(gv, luts[q.basis], q, qx, qy, &qf);
                 s_flags[src] = qf;
             }
