@@ -403,7 +403,7 @@ extern "C" bsf_status bsf_filter_points_aux(bsf_plan_t p, const void *g, const v
 // for BSF_PREC_FP64, or BSF_FUSED=0 in the environment) the per-thread
 // double-double tile kernel runs.
 static bool use_fused(const bsf_plan_s *p) {
-    if (p->d.precision == BSF_PREC_FP64) return false;
+    if (p->d.precision == BSF_PREC_FP64 || p->d.order > 3) return false;
     const char *env = getenv("BSF_FUSED");
     if (env && env[0] == '0') return false;
     for (int b = 0; b < 2; ++b) {
