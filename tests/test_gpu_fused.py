@@ -1,0 +1,117 @@
+"""The fused exact-split path (bsf_fused.cuh) against the double-double tile
+kernel and against itself: its double-double fallback, its work counter and
+its dispatch.  (Parity with the oracle is in test_gpu_tile.py /
+test_gpu_orders.py, which run the fused path by default.)"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from paper_1109_5114_b200 import bsf, lut
+from gpu_util import gpu_full, make_plan, tile_points
+from test_gpu_parity import _small_smooth
+
+pytestmark = pytest.mark.gpu
+TILE = bsf.BSF_ANCHOR_TILE
+
+
+class _env:
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kw}
+        os.environ.update({k: str(v) for k, v in self.kw.items()})
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_dispatch():
+    w = synth.workload(2)
+    plan = make_plan(w, anchor=TILE)
+    pts = synth.sample_points(w, 4, seed=1)
+    tile_points(plan, synth.make_image(w)[None], synth.make_cov(w), pts)
+    assert plan.uses_fused()
+    # Theta' at r = 3: the exact limb would be 4 bits -> double-double tile kernel
+    w3 = synth.workload(1, width=40, height=40)
+    p3 = make_plan(w3, policy=1, order=3, anchor=TILE)
+    tile_points(p3, synth.make_image(w3)[None], synth.make_cov(w3), synth.sample_points(w3, 2, seed=1))
+    assert not p3.uses_fused()
+    with _env(BSF_FUSED=0):
+        p0 = make_plan(w, anchor=TILE)
+        tile_points(p0, synth.make_image(w)[None], synth.make_cov(w), pts)
+        assert not p0.uses_fused()
+
+
+@pytest.mark.parametrize("config,order,n", [(2, 2, 3000), (3, 1, 3000), (3, 2, 600)])
+def test_fused_matches_double_double_kernel(config, order, n):
+    """Split contraction vs the all-double-double tile kernel on the same
+    (full-size) workload: both are far more accurate than the 1e-9 contract,
+    so they must agree to ~1e-12."""
+    w = synth.workload(config, order=order)
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    pts = synth.sample_points(w, n, seed=5)
+    a = tile_points(make_plan(w, anchor=TILE), img[None], cov, pts)
+    with _env(BSF_FUSED=0):
+        b = tile_points(make_plan(w, anchor=TILE), img[None], cov, pts)
+    rel = (a - b).abs() / b.abs()
+    assert float(rel.max()) <= 1e-12, float(rel.max())
+
+
+@pytest.mark.parametrize("r", [1, 2])
+def test_forced_fallback_matches_split_path(r):
+    """BSF_SPLIT_TOL=0 sends every pixel to the warp-cooperative double-double
+    fallback (mesh_warp on the split planes); it must agree with the split
+    path and be counted."""
+    H, W = 45, 53
+    w, img, cov = _small_smooth(H, W, 3.0)
+    plan = make_plan(w, order=r, anchor=TILE)
+    a = gpu_full(plan, img, cov)[0]
+    st = plan.stats(reset=True)
+    assert st["double_double"] < st["pixels"] // 10
+    with _env(BSF_SPLIT_TOL=0):
+        b = gpu_full(plan, img, cov)[0]
+    st = plan.stats(reset=True)
+    assert st["double_double"] == st["pixels"] == H * W
+    rel = (a - b).abs() / b.abs()
+    assert float(rel.max()) <= 1e-12, float(rel.max())
+
+
+def test_macs_counter_is_the_algorithmic_work():
+    """bsf_stats.macs = sum over taps of (window slots of the tap's region) x
+    (monomials of the table), recomputed on the host from the per-pixel scales
+    (aux) and the tables' region classification."""
+    H, W, r = 20, 24, 2
+    w, img, cov = _small_smooth(H, W, 2.5)
+    plan = make_plan(w, order=r, anchor=TILE)
+    ys, xs = np.mgrid[0:H, 0:W]
+    pts = torch.tensor(np.stack([np.zeros(H * W), xs.ravel(), ys.ravel()], 1), dtype=torch.int32)
+    plan.stats(reset=True)
+    _, aux = tile_points(plan, img[None], cov, pts, aux=True)
+    got = plan.stats()["macs"]
+    steps = {0: [(1, 0), (1, 1), (0, 1), (-1, 1)], 1: [(2, 1), (1, 2), (-1, 2), (-2, 1)]}
+    tabs = {b: lut.load(b, r) for b in (0, 1)}
+    want = 0
+    for row in aux.numpy():
+        b, drop, ap = int(row[0]), int(row[1]), row[4:8]
+        v = tabs[b]["variants"][drop + 1]
+        dirs = [k for k in range(4) if k != drop]
+        for t in range((r + 1) ** len(dirs)):
+            tt, Dx, Dy = t, 0.0, 0.0
+            for k in dirs:
+                j = tt % (r + 1)
+                tt //= r + 1
+                m = 0.5 * r - j
+                Dx += (m * steps[b][k][0]) * ap[k]
+                Dy += (m * steps[b][k][1]) * ap[k]
+            reg = lut.region_of(tabs[b], Dx - math.floor(Dx), Dy - math.floor(Dy))
+            want += int(v["counts"][reg]) * v["nmon"]
+    assert got == want
