@@ -19,7 +19,8 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 def build(force: bool = False, verbose: bool = False) -> str:
     stale = not os.path.exists(OUT) or any(os.path.getmtime(d) > os.path.getmtime(OUT) for d in DEPS)
     if force or stale:
-        cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", OUT] + SRC
+        extra = os.environ.get("BSF_NVCC_EXTRA", "").split()  # diagnostics builds only
+        cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", OUT] + SRC
         subprocess.check_call(cmd)
     return OUT
 

@@ -66,6 +66,39 @@ __global__ void dmma16_kernel(double *out, double a) {
     if (s == 1.2345) out[threadIdx.x] = s;
 }
 
+// half the warps run DFMA chains, half DMMA: do the two FP64 paths overlap?
+__global__ void mixed_kernel(double *out, double a, double b) {
+    if ((threadIdx.x >> 5) & 1) {
+        double acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = threadIdx.x * 1e-3 + i;
+        for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] = fma(acc[i], a, b);
+        }
+        double s = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s += acc[i];
+        if (s == 1.2345) out[threadIdx.x] = s;
+    } else {
+        double A = a + threadIdx.x, B = a - threadIdx.x;
+        double c[8][2];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+        for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(c[i][0]), "+d"(c[i][1])
+                             : "d"(A), "d"(B));
+        }
+        double s = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+        if (s == 1.2345) out[threadIdx.x] = s;
+    }
+}
+
 template <class F>
 static float timeit(F launch) {
     cudaEvent_t a, b;
@@ -102,6 +135,15 @@ int main() {
         ms = timeit([&] { dmma16_kernel<<<blocks, threads>>>(out, 1.0); });
         flops = 2.0 * 16 * 8 * 16 * 4 * (double)(ITERS / 4) * blocks * (threads / 32);
         printf("{\"kernel\": \"dmma_m16n8k16\", \"warps_per_sm\": %d, \"tflops\": %.2f}\n", warps, flops / ms / 1e9);
+    }
+    {
+        // mixed: blocks of 8 warps, 4 DFMA + 4 DMMA; each half does the same work as above per warp
+        int blocks = sms * 4, threads = 256;
+        float ms = timeit([&] { mixed_kernel<<<blocks, threads>>>(out, 1.0000001, 1e-9); });
+        double dfma = 2.0 * 16 * ITERS * (double)blocks * threads / 2;
+        double dmma = 2.0 * 8 * 8 * 4 * 8 * (double)ITERS * blocks * (threads / 64);
+        printf("{\"kernel\": \"mixed dfma+dmma\", \"warps_per_sm\": 32, \"tflops_total\": %.2f, "
+               "\"dfma_share\": %.3f}\n", (dfma + dmma) / ms / 1e9, dfma / (dfma + dmma));
     }
     cudaError_t e = cudaGetLastError();
     printf("{\"status\": \"%s\"}\n", cudaGetErrorString(e));
