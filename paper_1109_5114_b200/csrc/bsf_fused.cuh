@@ -37,12 +37,16 @@ template <> struct FusedCfg<2> { static constexpr int NTAP = 81, P = 64, MT = 2;
 template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 16, MT = 1; };
 template <> struct FusedCfg<4> { static constexpr int NTAP = 625, P = 4, MT = 1; };
 
+// dynamic shared memory: the chunk buffers of phases 4-5, aliased by the
+// pre-integration ring of phase 2 (at least FUSED_SMEM_MIN bytes for it)
+constexpr size_t FUSED_SMEM_MIN = 0;
 template <int R>
 constexpr size_t fused_smem_bytes() {
     constexpr size_t ITEMS = (size_t)FusedCfg<R>::P * FusedCfg<R>::NTAP;
     constexpr size_t GS = 8 * FusedCfg<R>::MT;
-    return ITEMS * 16 + FT * 4 * 8 + ITEMS * 2 +
-           (ITEMS + GS * NKEY) * 2 + (FT / 32) * NKEY * 4 + FT * 4;
+    constexpr size_t chunk = ITEMS * 16 + FT * 4 * 8 + ITEMS * 2 + (ITEMS + GS * NKEY) * 2 + (FT / 32) * NKEY * 4 +
+                             FT * 4;
+    return chunk > FUSED_SMEM_MIN ? chunk : FUSED_SMEM_MIN;
 }
 
 // pixel info word: bit0 basis, bits1-3 variant (drop + 1), bit4 live, bit5 clamped, bits 8.. flags
@@ -251,6 +255,103 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
     }
 }
 
+// ---------------------------------------------------------------------------
+// Pre-integration of one halo plane by a wavefront row sweep (a5).
+//
+// The levels with s_y >= 1 obey v_l(x, y) = v_{l-1}(x, y) + v_l(x - s_x, y - s_y)
+// (zero state outside the domain).  At step tau level l (1-based) processes
+// row tau - l + 1: it needs its own rows y - 1, y - 2 and row y of level l - 1,
+// all written in earlier steps, so every level advances together with one
+// barrier per step, each level keeping its last three rows in a shared-memory
+// ring.  The Theta basis' horizontal levels (1, 0) are prefix sums along the
+// rows and are taken first, all R of them in one pass per row (thread per
+// row) -- on the truncated tile domain the order of the levels only changes
+// the sums by functions the mesh annihilates (R18/R20).  The plane G receives
+// the horizontal sums (Theta), then the final level of the sweep, row by row.
+// Returns false (nothing done) when the ring does not fit in `ring_bytes`.
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int Y0, int basis, const TileArgs &a,
+                            int img, double2 *ring, size_t ring_bytes) {
+    const int tid = threadIdx.x;
+    const int nh = basis == BASIS_THETA ? R : 0;  // horizontal levels, done first
+    const int L = 4 * R - nh;                    // levels in the sweep
+    if ((size_t)3 * L * NX * sizeof(double2) > ring_bytes) return false;
+    const size_t ipl = (size_t)a.H * a.W;
+    auto fval = [&](int x, int y) -> double {
+        const int X = X0 + x, Y = Y0 + y;
+        if (X < 0 || X >= a.W || Y < 0 || Y >= a.H) return 0.0;
+        const size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
+        return a.in_u8 ? (double)((const uint8_t *)a.f)[o] : (double)((const float *)a.f)[o];
+    };
+    if (nh) {
+        for (int y = tid; y < NY; y += FT) {
+            dd acc[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) acc[k] = {0.0, 0.0};
+            for (int x = 0; x < NX; ++x) {
+                acc[0] = dd_add_d(acc[0], fval(x, y));
+#pragma unroll
+                for (int k = 1; k < R; ++k) acc[k] = dd_add(acc[k], acc[k - 1]);
+                G[(size_t)y * NX + x] = make_double2(acc[R - 1].hi, acc[R - 1].lo);
+            }
+        }
+        __syncthreads();
+    }
+    // level steps of the sweep, in scan order with the horizontal levels removed
+    int lsx[4 * R], lsy[4 * R];
+    {
+        int k = 0;
+        for (int rep = 0; rep < R; ++rep)
+            for (int lv = 0; lv < 4; ++lv) {
+                const int sx = c_scan_order[basis][lv][0], sy = c_scan_order[basis][lv][1];
+                if (sy == 0) continue;
+                lsx[k] = sx;
+                lsy[k] = sy;
+                ++k;
+            }
+    }
+    // flat (level, x) work list over the CTA; (l, x) advanced incrementally
+    const int work = L * NX;
+    const int l0 = tid / NX, x0 = tid - l0 * NX, dl = FT / NX, dx = FT - dl * NX;
+    for (int tau = 0; tau < NY + L - 1; ++tau) {
+        int l = l0, x = x0;
+        for (int i = tid; i < work; i += FT) {
+            const int y = tau - l;  // level l + 1 processes row tau - l
+            if (y >= 0 && y < NY) {
+                dd below;
+                if (l == 0) {
+                    if (nh) {
+                        const double2 t = G[(size_t)y * NX + x];
+                        below = {t.x, t.y};
+                    } else {
+                        below = {fval(x, y), 0.0};
+                    }
+                } else {
+                    const double2 t = ring[((size_t)(l - 1) * 3 + y % 3) * NX + x];
+                    below = {t.x, t.y};
+                }
+                const int yp = y - lsy[l], xp = x - lsx[l];
+                if (yp >= 0 && xp >= 0 && xp < NX) {
+                    const double2 t = ring[((size_t)l * 3 + yp % 3) * NX + xp];
+                    below = dd_add(below, {t.x, t.y});
+                }
+                const double2 v = make_double2(below.hi, below.lo);
+                ring[((size_t)l * 3 + y % 3) * NX + x] = v;
+                if (l == L - 1) G[(size_t)y * NX + x] = v;
+            }
+            l += dl;
+            x += dx;
+            if (x >= NX) {
+                x -= NX;
+                ++l;
+            }
+        }
+        __syncthreads();
+    }
+    return true;
+}
+
 template <int R>
 __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
     constexpr int NTAP = FusedCfg<R>::NTAP, P = FusedCfg<R>::P, ITEMS = P * NTAP;
@@ -379,21 +480,26 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             const int X0 = s_dom[b][0], Y0 = s_dom[b][1], NX = s_dom[b][2], NY = s_dom[b][3];
             double2 *G = scr + s_poff[b * NVAR];
             const int n = NX * NY;
-            for (int i = tid; i < n; i += FT) {
-                const int X = X0 + i % NX, Y = Y0 + i / NX;
-                double v = 0.0;
-                if (X >= 0 && X < a.W && Y >= 0 && Y < a.H) {
-                    const size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
-                    v = a.in_u8 ? (double)((const uint8_t *)a.f)[o] : (double)((const float *)a.f)[o];
+            // wavefront sweep with its ring in the (idle) dynamic shared memory;
+            // level-by-level scans when the ring does not fit
+            if (!sweep_plane<R>(G, NX, NY, X0, Y0, b, a, img, reinterpret_cast<double2 *>(smem),
+                                fused_smem_bytes<R>())) {
+                for (int i = tid; i < n; i += FT) {
+                    const int X = X0 + i % NX, Y = Y0 + i / NX;
+                    double v = 0.0;
+                    if (X >= 0 && X < a.W && Y >= 0 && Y < a.H) {
+                        const size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
+                        v = a.in_u8 ? (double)((const uint8_t *)a.f)[o] : (double)((const float *)a.f)[o];
+                    }
+                    G[i] = make_double2(v, 0.0);
                 }
-                G[i] = make_double2(v, 0.0);
+                __syncthreads();
+                for (int rep = 0; rep < R; ++rep)
+                    for (int lv = 0; lv < 4; ++lv) {
+                        tile_scan_level(G, NX, NY, c_scan_order[b][lv][0], c_scan_order[b][lv][1]);
+                        __syncthreads();
+                    }
             }
-            __syncthreads();
-            for (int rep = 0; rep < R; ++rep)
-                for (int lv = 0; lv < 4; ++lv) {
-                    tile_scan_level(G, NX, NY, c_scan_order[b][lv][0], c_scan_order[b][lv][1]);
-                    __syncthreads();
-                }
             // zero-scale variants: G' = (1 - T_{s_k})^R G, exact lattice difference (R5)
             for (int v = 1; v < NVAR; ++v) {
                 if (!((s_vmask[b] >> v) & 1)) continue;
