@@ -7,9 +7,11 @@
   so each rank receives the input rows [y0 - R_s, y0) and [y1, y1 + R_s) from
   its neighbours (one NCCL send/recv pair per neighbour) and runs the
   tile-anchored kernel on its block.  Strip and halo boundaries are multiples
-  of the 16-row tile, so every kept tile sees exactly the data and domain it
-  sees in a single-GPU run: the outputs are bit-identical.  No scan carries
-  are exchanged (the tile path restarts its sums per tile).
+  of the 32-row super-tile on which the fused kernel anchors its running sums,
+  and the halo covers a super-tile's halo domain, so every kept super-tile
+  sees exactly the data and domain it sees in a single-GPU run: the outputs
+  are bit-identical (tests/test_gpu_strips.py).  No scan carries are
+  exchanged (the tile path restarts its sums per super-tile).
 
 Only plumbing lives here (partition arithmetic, halo exchange through
 torch.distributed); the compute is the C-ABI library.
@@ -21,7 +23,7 @@ from dataclasses import dataclass
 
 import torch
 
-TILE = 16
+TILE = 32  # the fused kernel's super-tile (bsf_fused.cuh STILE)
 
 
 def shard_range(n: int, rank: int, world: int):
@@ -32,8 +34,10 @@ def shard_range(n: int, rank: int, world: int):
 
 
 def halo_rows(max_sigma: float, order: int) -> int:
-    """Kernel-support half-extent bound in rows, rounded up to whole tiles."""
-    rs = int(math.ceil(max_sigma * math.sqrt(24.0 * order))) + 1
+    """Rows a super-tile's halo domain reaches beyond it (tap reach bound
+    sigma_max sqrt(24 r) plus the interpolation window, <= 6r + 2 rows),
+    rounded up to whole super-tiles."""
+    rs = int(math.ceil(max_sigma * math.sqrt(24.0 * order))) + 6 * order + 4
     return TILE * ((rs + TILE - 1) // TILE)
 
 
