@@ -125,40 +125,68 @@ struct DegCfg {
     static constexpr int NT = bsf_nt(DEG);  // 8-column n-tiles (bsf_mono_col layout)
 };
 
-// Row polynomials R_i(phi_y) owned by lane LANE of the quad (compensated
-// Horner over the accumulator slots of row i, highest y power first).
-template <int DEG, int NT, int LANE, int I>
-__device__ __forceinline__ void fused_rows(const double (&C)[2][NT][2], double fy, double (&Rh)[DEG + 1],
-                                           double (&Rl)[DEG + 1]) {
-    if constexpr (I <= DEG) {
-        if constexpr (bsf_row_lane(DEG, I) == LANE) {
-            constexpr int S0 = bsf_row_slot(DEG, I);
-            double rh = 0.0, rl = 0.0;
+// Row polynomials R_i(phi_y) of the rows this lane of the quad owns
+// (compensated Horner over its accumulator slots, highest y power first).  All
+// lanes step through the slots in lock-step; which slots start a row or belong
+// to one is a per-lane mask, applied by selects (no divergence).  The q-th row
+// of the lane ends in (Rh[q], Rl[q]).
+template <int DEG>
+struct RowCfg {
+    static constexpr int QMAX = bsf_lane_rows(DEG, 0) > bsf_lane_rows(DEG, 1)
+                                    ? (bsf_lane_rows(DEG, 0) > bsf_lane_rows(DEG, 3) ? bsf_lane_rows(DEG, 0)
+                                                                                     : bsf_lane_rows(DEG, 3))
+                                    : (bsf_lane_rows(DEG, 1) > bsf_lane_rows(DEG, 3) ? bsf_lane_rows(DEG, 1)
+                                                                                     : bsf_lane_rows(DEG, 3));
+};
+
+template <int DEG, int NT>
+__device__ __forceinline__ void fused_rows(const double (&C)[2][NT][2], double fy, int kq,
+                                           double (&Rh)[RowCfg<DEG>::QMAX], double (&Rl)[RowCfg<DEG>::QMAX]) {
+    constexpr int QMAX = RowCfg<DEG>::QMAX;
+    const unsigned smask = kq == 0 ? bsf_start_mask(DEG, 0)
+                           : kq == 1 ? bsf_start_mask(DEG, 1)
+                           : kq == 2 ? bsf_start_mask(DEG, 2) : bsf_start_mask(DEG, 3);
+    const unsigned vmask = kq == 0 ? bsf_valid_mask(DEG, 0)
+                           : kq == 1 ? bsf_valid_mask(DEG, 1)
+                           : kq == 2 ? bsf_valid_mask(DEG, 2) : bsf_valid_mask(DEG, 3);
 #pragma unroll
-            for (int k = 0; k <= DEG - I; ++k) {
-                const int sl = S0 + k;
-                const dd e = two_sum(C[0][sl >> 1][sl & 1], C[1][sl >> 1][sl & 1]);
-                if (k == 0) {
-                    rh = e.hi;
-                    rl = e.lo;
-                } else {
-                    comp_step(rh, rl, fy, e.hi, e.lo);
+    for (int q = 0; q < QMAX; ++q) Rh[q] = Rl[q] = 0.0;
+    double rh = 0.0, rl = 0.0;
+    int q = -1;
+#pragma unroll
+    for (int k = 0; k < 2 * NT; ++k) {
+        const bool start = (smask >> k) & 1, valid = (vmask >> k) & 1;
+        const dd e = two_sum(C[0][k >> 1][k & 1], C[1][k >> 1][k & 1]);
+        double nh = rh, nl = rl;
+        comp_step(nh, nl, fy, e.hi, e.lo);
+        if (start) {
+#pragma unroll
+            for (int qq = 0; qq < QMAX; ++qq)
+                if (qq == q) {
+                    Rh[qq] = rh;
+                    Rl[qq] = rl;
                 }
-            }
-            Rh[I] = rh;
-            Rl[I] = rl;
+            ++q;
         }
-        fused_rows<DEG, NT, LANE, I + 1>(C, fy, Rh, Rl);
+        rh = start ? e.hi : (valid ? nh : rh);
+        rl = start ? e.lo : (valid ? nl : rl);
     }
+#pragma unroll
+    for (int qq = 0; qq < QMAX; ++qq)
+        if (qq == q) {
+            Rh[qq] = rh;
+            Rl[qq] = rl;
+        }
 }
 
 // Horner scheme in phi_x over the rows, gathered from the quad's lanes.
 template <int DEG, int I>
-__device__ __forceinline__ void fused_xhorner(const double (&Rh)[DEG + 1], const double (&Rl)[DEG + 1], double fx,
-                                              double &ah, double &al) {
-    constexpr int SRC = bsf_row_lane(DEG, I);
+__device__ __forceinline__ void fused_xhorner(const double (&Rh)[RowCfg<DEG>::QMAX],
+                                              const double (&Rl)[RowCfg<DEG>::QMAX], double fx, double &ah,
+                                              double &al) {
+    constexpr int SRC = bsf_row_lane(DEG, I), Q = bsf_row_q(DEG, I);
     const int src = (threadIdx.x & 28) | SRC;
-    const double h = __shfl_sync(0xffffffffu, Rh[I], src), l = __shfl_sync(0xffffffffu, Rl[I], src);
+    const double h = __shfl_sync(0xffffffffu, Rh[Q], src), l = __shfl_sync(0xffffffffu, Rl[Q], src);
     if constexpr (I == DEG) {
         ah = h;
         al = l;
@@ -238,15 +266,8 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
     }
 #pragma unroll
     for (int t = 0; t < MT; ++t) {
-        double Rh[DEG + 1], Rl[DEG + 1];
-#pragma unroll
-        for (int i = 0; i <= DEG; ++i) Rh[i] = Rl[i] = 0.0;
-        switch (kq) {
-            case 0: fused_rows<DEG, NT, 0, 0>(C[t], fyt[t], Rh, Rl); break;
-            case 1: fused_rows<DEG, NT, 1, 0>(C[t], fyt[t], Rh, Rl); break;
-            case 2: fused_rows<DEG, NT, 2, 0>(C[t], fyt[t], Rh, Rl); break;
-            default: fused_rows<DEG, NT, 3, 0>(C[t], fyt[t], Rh, Rl); break;
-        }
+        double Rh[RowCfg<DEG>::QMAX], Rl[RowCfg<DEG>::QMAX];
+        fused_rows<DEG, NT>(C[t], fyt[t], kq, Rh, Rl);
         double ah, al;
         fused_xhorner<DEG, DEG>(Rh, Rl, fxt[t], ah, al);
         const dd F = fast_two_sum(ah, al);

@@ -55,6 +55,32 @@ __host__ __device__ constexpr int bsf_row_slot(int deg, int i) {  // first slot 
     }
     return -1;
 }
+__host__ __device__ constexpr int bsf_row_q(int deg, int i) {  // position of row i in its lane's list
+    const int l = bsf_row_lane(deg, i);
+    for (int k = 0; bsf_part(deg, l, k); ++k)
+        if (bsf_part(deg, l, k) == deg - i + 1) return k;
+    return -1;
+}
+__host__ __device__ constexpr int bsf_lane_rows(int deg, int lane) {
+    int k = 0;
+    while (bsf_part(deg, lane, k)) ++k;
+    return k;
+}
+// slot masks of a lane: bit k set if slot k starts a row / belongs to a row
+__host__ __device__ constexpr unsigned bsf_start_mask(int deg, int lane) {
+    unsigned m = 0;
+    int s = 0;
+    for (int k = 0; bsf_part(deg, lane, k); ++k) {
+        m |= 1u << s;
+        s += bsf_part(deg, lane, k);
+    }
+    return m;
+}
+__host__ __device__ constexpr unsigned bsf_valid_mask(int deg, int lane) {
+    int s = 0;
+    for (int k = 0; bsf_part(deg, lane, k); ++k) s += bsf_part(deg, lane, k);
+    return s >= 32 ? 0xffffffffu : ((1u << s) - 1u);
+}
 // accumulator column of monomial phi_x^i phi_y^j
 __host__ __device__ constexpr int bsf_mono_col(int deg, int i, int j) {
     return 8 * ((bsf_row_slot(deg, i) + deg - i - j) >> 1) + 2 * bsf_row_lane(deg, i) +
