@@ -196,7 +196,7 @@ class Plan:
 
     def phase_cycles(self, reset=False):
         """Per-phase SM cycles of the fused tile kernel (enables counting on first call)."""
-        buf = (ctypes.c_ulonglong * 8)()
+        buf = (ctypes.c_ulonglong * 16)()
         _check(lib().bsf_debug_phase_cycles(self.handle, buf, int(reset)))
         return list(buf)
 

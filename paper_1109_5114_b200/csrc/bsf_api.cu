@@ -555,16 +555,16 @@ extern "C" bsf_status bsf_debug_phase_cycles(bsf_plan_t p, unsigned long long *o
     if (!p) return set_err(BSF_EINVAL, "null plan");
     if (!p->prof) {
         void *q;
-        CUDA_TRY(cudaMalloc(&q, 8 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMalloc(&q, 16 * sizeof(unsigned long long)));
         p->dev_allocs.push_back(q);
         p->prof = (unsigned long long *)q;
-        CUDA_TRY(cudaMemset(q, 0, 8 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemset(q, 0, 16 * sizeof(unsigned long long)));
     }
     if (out) {
         CUDA_TRY(cudaStreamSynchronize(p->last));
-        CUDA_TRY(cudaMemcpy(out, p->prof, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(out, p->prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     }
-    if (reset) CUDA_TRY(cudaMemset(p->prof, 0, 8 * sizeof(unsigned long long)));
+    if (reset) CUDA_TRY(cudaMemset(p->prof, 0, 16 * sizeof(unsigned long long)));
     return BSF_OK;
 }
 

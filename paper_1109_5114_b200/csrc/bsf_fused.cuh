@@ -97,6 +97,44 @@ __device__ __forceinline__ TileDomain fused_domain(const LutBasis &L, int R, int
     return d;
 }
 
+// Region classifier of the unit cell (classify() in bsf_kernels.cu) with its
+// tables staged in shared memory once per CTA.
+struct ClsTables {
+    int2 normal[2][4];
+    int kmin[2][4], radix[2][4];
+    signed char table[2][81];
+};
+
+__device__ __forceinline__ int cls_key(const ClsTables &T, int b, double x, double y) {
+    int idx = 0, mul = 1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int f = (int)floor(T.normal[b][k].x * x + T.normal[b][k].y * y) - T.kmin[b][k];
+        if (f < 0 || f >= T.radix[b][k]) return -1;
+        idx += f * mul;
+        mul *= T.radix[b][k];
+    }
+    return T.table[b][idx];
+}
+
+__device__ __forceinline__ int cls_region(const ClsTables &T, int b, double x, double y) {
+    const double one_m = 1.0 - 1.1102230246251565e-16;
+    x = fmin(fmax(x, 0.0), one_m);
+    y = fmin(fmax(y, 0.0), one_m);
+    int r = cls_key(T, b, x, y);
+    if (r >= 0) return r;
+    // exactly on knot lines: any adjacent region gives the same value (the
+    // kernel is continuous), step into one -- the same nudges as classify()
+    const double e = 1e-12;
+    const double dx[4] = {e, -e, 0.7 * e, -0.3 * e};
+    const double dy[4] = {0.37 * e, 0.61 * e, -e, -0.77 * e};
+    for (int i = 0; i < 4; ++i) {
+        r = cls_key(T, b, fmin(fmax(x + dx[i], 0.0), one_m), fmin(fmax(y + dy[i], 0.0), one_m));
+        if (r >= 0) return r;
+    }
+    return 0;
+}
+
 // binomial sign weight of tap t: prod_k (-1)^{j_k} C(R, j_k)
 template <int R>
 __device__ __forceinline__ int tap_coef(int t, int drop) {
@@ -390,8 +428,21 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     __shared__ long long s_poff[NPLANE];
     __shared__ int s_pe[NPLANE];
     __shared__ unsigned long long s_pmax[NPLANE];
+    __shared__ ClsTables s_cls;
+    __shared__ unsigned long long s_stats[8];  // per-CTA statistics, flushed once per super-tile
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < 8) s_stats[tid] = 0ull;
+    if (tid < 2) {
+        const LutBasis &L = luts[tid];
+        for (int k = 0; k < 4; ++k) {
+            s_cls.normal[tid][k] = L.normal[k];
+            s_cls.kmin[tid][k] = L.kmin[k];
+            s_cls.radix[tid][k] = L.radix[k];
+        }
+        for (int i = 0; i < 81; ++i) s_cls.table[tid][i] = L.table[i];
+    }
+    __syncthreads();
     // optional phase timing (TileArgs::prof, diagnostics only): thread 0 adds
     // the SM cycles spent in each phase
     long long ph_t = clock64();
@@ -614,31 +665,37 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             for (int k = tid; k < (FT / 32) * NKEY; k += FT) s_hist[k] = 0;
             __syncthreads();
             if (!s_any) continue;  // uniform
-            // keys, per-warp histograms (warp w owns items [w*WPR, (w+1)*WPR))
+            FUSED_PHASE(8);
+            // keys of all items (independent per item: the loop is unrolled so
+            // several items' dependency chains overlap) ...
+#pragma unroll 4
+            for (int i = tid; i < ITEMS; i += FT) {
+                const int t = i / P, p = c0 + i % P;
+                const int w = s_info[p];
+                const int var = info_var(w);
+                const int ntap = var ? NTAP / (R + 1) : NTAP;
+                uint16_t key = NOKEY;
+                if (info_live(w) && (!a.pts || p == want) && t < ntap) {
+                    const int b = info_basis(w);
+                    double Dx, Dy;
+                    int cf;
+                    fused_tap<R>(s_ap + 4 * p, b, var - 1, t, Dx, Dy, cf);
+                    const int reg = cls_region(s_cls, b, Dx - floor(Dx), Dy - floor(Dy));
+                    key = (uint16_t)((b * NVAR + var) * MAX_REG + reg);
+                }
+                s_key[i] = key;
+            }
+            __syncthreads();
+            // ... then per-warp histograms (warp w owns items [w*WPR, (w+1)*WPR))
             for (int base = warp * WPR; base < min(ITEMS, (warp + 1) * WPR); base += 32) {
                 const int i = base + lane;
-                uint16_t key = NOKEY;
-                if (i < ITEMS) {
-                    const int t = i / P, p = c0 + i % P;
-                    const int w = s_info[p];
-                    const int var = info_var(w);
-                    const int ntap = var ? NTAP / (R + 1) : NTAP;
-                    if (info_live(w) && (!a.pts || p == want) && t < ntap) {
-                        const int b = info_basis(w);
-                        double Dx, Dy;
-                        int cf;
-                        fused_tap<R>(s_ap + 4 * p, b, var - 1, t, Dx, Dy, cf);
-                        const double fx = Dx - floor(Dx), fy = Dy - floor(Dy);
-                        const int reg = classify(luts[b], fx, fy);
-                        key = (uint16_t)((b * NVAR + var) * MAX_REG + reg);
-                    }
-                    s_key[i] = key;
-                }
+                const uint16_t key = i < ITEMS ? s_key[i] : NOKEY;
                 const unsigned m = __match_any_sync(0xffffffffu, key);
                 if (key != NOKEY && lane == __ffs(m) - 1) s_hist[warp * NKEY + key] += __popc(m);
                 __syncwarp();
             }
             __syncthreads();
+            FUSED_PHASE(9);
             // bucket starts (each bucket padded to a multiple of GS) and per-warp offsets
             if (warp == 0) {
                 constexpr int PER = NKEY / 32;
@@ -671,6 +728,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 if (lane == 31) s_npad = inc;
             }
             __syncthreads();
+            FUSED_PHASE(10);
             const int npad = s_npad;
             for (int i = tid; i < npad; i += FT) s_sorted[i] = NOKEY;
             __syncthreads();
@@ -729,7 +787,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     if (a.stats) {  // algorithmic work: window x monomials per real item
                         const unsigned nreal = __popc(__ballot_sync(0xffffffffu, real));
                         if (lane == 0)
-                            atomicAdd(a.stats + 6, (unsigned long long)nreal * __ldg(V.counts + reg) *
+                            atomicAdd(&s_stats[6], (unsigned long long)nreal * __ldg(V.counts + reg) *
                                                        (var == 0 ? DegCfg<4 * R - 2>::NMON : DegCfg<3 * R - 2>::NMON));
                     }
                     long long tq0 = 0;
@@ -749,7 +807,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         if (var == 0) atomicAdd(a.prof + 7, dt);
                     }
                 }
-                if (flags && a.stats) atomicOr(a.stats + 4, (unsigned long long)flags);
+                if (flags) atomicOr(&s_stats[4], (unsigned long long)flags);
             }
             __syncthreads();
             FUSED_PHASE(4);
@@ -819,12 +877,12 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         ((float *)a.out)[oidx] = (float)res;
                     else
                         ((double *)a.out)[oidx] = res;
-                    if (a.stats) {
-                        atomicAdd(a.stats + 0, 1ull);
-                        if ((w >> 5) & 1) atomicAdd(a.stats + 1, 1ull);
-                        if (var) atomicAdd(a.stats + 2, 1ull);
-                        if (b == BASIS_THETA_PRIME) atomicAdd(a.stats + 3, 1ull);
-                        if (w >> 8) atomicOr(a.stats + 4, (unsigned long long)(w >> 8));
+                    {
+                        atomicAdd(&s_stats[0], 1ull);
+                        if ((w >> 5) & 1) atomicAdd(&s_stats[1], 1ull);
+                        if (var) atomicAdd(&s_stats[2], 1ull);
+                        if (b == BASIS_THETA_PRIME) atomicAdd(&s_stats[3], 1ull);
+                        if (w >> 8) atomicOr(&s_stats[4], (unsigned long long)(w >> 8));
                     }
                 }
             }
@@ -856,9 +914,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     else
                         ((double *)a.out)[oidx] = res;
                     if (a.aux) a.aux[BSF_AUX * oidx + 8] = 1.0;
-                    if (a.stats) {
-                        atomicAdd(a.stats + 5, 1ull);
-                        if (fl) atomicOr(a.stats + 4, (unsigned long long)fl);
+                    {
+                        atomicAdd(&s_stats[5], 1ull);
+                        if (fl) atomicOr(&s_stats[4], (unsigned long long)fl);
                     }
                 }
             }
@@ -869,6 +927,14 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
 
         }
         }  // sub-tiles
+        __syncthreads();
+        if (tid < 8 && a.stats && s_stats[tid]) {
+            if (tid == 4)
+                atomicOr(a.stats + 4, s_stats[4]);
+            else
+                atomicAdd(a.stats + tid, s_stats[tid]);
+            s_stats[tid] = 0ull;
+        }
     }
 }
 

@@ -34,5 +34,7 @@ tot = sum(cyc[:6])
 print("workload", w.name, "fused", plan.uses_fused())
 for n, c in zip(PHASES, cyc):
     print("%-16s %6.1f%%  %.3e cycles" % (n, 100.0 * c / tot, c))
+print("sort sub-phases: sub-tile scales %.3e, keys %.3e, bucket scan %.3e, scatter %.3e" %
+      (cyc[8], cyc[9], cyc[10], cyc[3] - cyc[8] - cyc[9] - cyc[10]))
 print("gather groups: warp-cycles total %.3e, full-variant MMA loop %.3e (per-CTA wall equivalent /8: %.3e, %.3e)"
       % (cyc[6], cyc[7], cyc[6] / 8, cyc[7] / 8))
