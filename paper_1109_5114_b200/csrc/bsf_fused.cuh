@@ -54,6 +54,16 @@ __device__ __forceinline__ int info_basis(int w) { return w & 1; }
 __device__ __forceinline__ int info_var(int w) { return (w >> 1) & 7; }
 __device__ __forceinline__ bool info_live(int w) { return (w >> 4) & 1; }
 
+// C(R, j) for the compile-time order R (no integer division)
+template <int R>
+__device__ __forceinline__ int binomR(int j) {
+    if constexpr (R == 1) return 1;
+    if constexpr (R == 2) return j == 1 ? 2 : 1;
+    if constexpr (R == 3) return (j == 1 || j == 2) ? 3 : 1;
+    if constexpr (R == 4) return j == 2 ? 6 : ((j == 1 || j == 3) ? 4 : 1);
+    return 0;
+}
+
 // tap t of a pixel: displacement D (exact, R17) and binomial sign weight
 template <int R>
 __device__ __forceinline__ void fused_tap(const double *ap, int basis, int drop, int t, double &Dx, double &Dy,
@@ -67,7 +77,7 @@ __device__ __forceinline__ void fused_tap(const double *ap, int basis, int drop,
         if (k == drop) continue;
         int j = tt % (R + 1);
         tt /= (R + 1);
-        coef *= binom_small(R, j) * ((j & 1) ? -1 : 1);
+        coef *= binomR<R>(j) * ((j & 1) ? -1 : 1);
         double m = 0.5 * R - j;
         Dx += (m * c_steps[basis][k][0]) * ap[k];
         Dy += (m * c_steps[basis][k][1]) * ap[k];
@@ -144,7 +154,7 @@ __device__ __forceinline__ int tap_coef(int t, int drop) {
         if (k == drop) continue;
         const int j = t % (R + 1);
         t /= (R + 1);
-        c *= binom_small(R, j) * ((j & 1) ? -1 : 1);
+        c *= binomR<R>(j) * ((j & 1) ? -1 : 1);
     }
     return c;
 }
@@ -585,7 +595,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         const int yy = Y - m * sy, xx = X - m * sx;
                         if (yy < 0 || xx < 0 || xx >= NX) continue;
                         const double2 t = G[(size_t)yy * NX + xx];
-                        const int cb = binom_small(R, m) * ((m & 1) ? -1 : 1);
+                        const int cb = binomR<R>(m) * ((m & 1) ? -1 : 1);
                         acc = dd_add(acc, dd_mul_d({t.x, t.y}, (double)cb));
                     }
                     D[i] = make_double2(acc.hi, acc.lo);
@@ -820,15 +830,35 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 const int w = s_info[p];
                 const int b = info_basis(w), var = info_var(w);
                 dd S = {0.0, 0.0};
-                double sumCF = 0.0;  // sum_j |c_j F_j| (for the double-double rounding term)
+                double sumCF = 0.0;  // sum_j |c_j F_j| (for the summation rounding term)
                 if (info_live(w)) {
+                    // compensated summation (TwoProd + TwoSum on the heads, all
+                    // small terms in one fp64 accumulator), two interleaved
+                    // accumulators for instruction-level parallelism
                     const int ntap = var ? NTAP / (R + 1) : NTAP;
-                    for (int t = sub; t < ntap; t += TPP) {
-                        const double2 F = s_F[t * P + pl];
-                        const double c = (double)tap_coef<R>(t, var - 1);
-                        S = dd_add(S, dd_mul_d({F.x, F.y}, c));
-                        sumCF += fabs(c * F.x);
+                    double h0 = 0.0, e0 = 0.0, h1 = 0.0, e1 = 0.0;
+                    int t = sub;
+                    for (; t + TPP < ntap; t += 2 * TPP) {
+                        const double2 F0 = s_F[t * P + pl], F1 = s_F[(t + TPP) * P + pl];
+                        const double c0 = (double)tap_coef<R>(t, var - 1), c1 = (double)tap_coef<R>(t + TPP, var - 1);
+                        const dd p0 = two_prod(c0, F0.x), p1 = two_prod(c1, F1.x);
+                        const dd s0 = two_sum(h0, p0.hi), s1 = two_sum(h1, p1.hi);
+                        h0 = s0.hi;
+                        h1 = s1.hi;
+                        e0 += s0.lo + (p0.lo + c0 * F0.y);
+                        e1 += s1.lo + (p1.lo + c1 * F1.y);
+                        sumCF += fabs(p0.hi) + fabs(p1.hi);
                     }
+                    if (t < ntap) {
+                        const double2 F0 = s_F[t * P + pl];
+                        const double c0 = (double)tap_coef<R>(t, var - 1);
+                        const dd p0 = two_prod(c0, F0.x);
+                        const dd s0 = two_sum(h0, p0.hi);
+                        h0 = s0.hi;
+                        e0 += s0.lo + (p0.lo + c0 * F0.y);
+                        sumCF += fabs(p0.hi);
+                    }
+                    S = dd_add(two_sum(h0, e0), two_sum(h1, e1));
                 }
 #pragma unroll
                 for (int o = 1; o < TPP; o <<= 1) {
@@ -852,9 +882,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         const double Sd = dd_to_d(S);
                         res = ldexp(Sd, s_pe[b * NVAR + var]) * norm / luts[b].var[var].L;
                         // a-posteriori bound of the split contraction:
-                        // |S^ - S| <= sum_j |c_j| bnd + 4 u^2 sum_j |c_j F_j|, sum_j |c_j| = 2^(R ns)
+                        // |S^ - S| <= sum_j |c_j| bnd + (2 ntap + 8) u^2 sum_j |c_j F_j|, sum_j |c_j| = 2^(R ns)
                         const int ns = var ? 3 : 4;
-                        const double err = ldexp(luts[b].var[var].bnd, R * ns) + 5e-32 * sumCF;
+                        const double err = ldexp(luts[b].var[var].bnd, R * ns) + 2.5e-30 * (NTAP / 81.0 + 1.0) * sumCF;
                         erel = err / fabs(Sd);
                         if (!(erel <= a.split_tol)) {  // NaN-safe: recompute in double-double
                             const int k = atomicAdd(&s_nfb, 1);
