@@ -201,6 +201,41 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         while (ldexp(1.0, cm) < colmax) ++cm;
         V.kbits = 53 - cm;
         V.L = L;
+        V.nsplit = 1;
+        V.shift = 0;
+        V.num2 = V.numf = nullptr;
+        std::vector<double> num1s, num0s;
+        if (V.kbits < KBITS_MIN) {
+            // split the numerators n = n1 2^sh + n0 (|n0| <= 2^(sh-1)) so that both
+            // column sums, and with them the exact limb, stay wide
+            const int sh = (int)ceil(0.5 * log2(2.0 * colmax / V.nslot4));
+            num1s.assign(nump.size(), 0.0);
+            num0s.assign(nump.size(), 0.0);
+            double c1 = 0.0, c0 = 0.0;
+            const double scale = ldexp(1.0, sh);
+            for (size_t i = 0; i < nump.size(); ++i) {
+                const double n1 = rint(nump[i] / scale);
+                num1s[i] = n1;
+                num0s[i] = nump[i] - n1 * scale;  // exact: |n| < 2^53
+            }
+            for (uint32_t r = 0; r < nreg; ++r)
+                for (int m = 0; m < V.nmonp; ++m) {
+                    double s1 = 0.0, s0 = 0.0;
+                    for (int sl = 0; sl < V.nslot4; ++sl) {
+                        const size_t i = ((size_t)r * V.nslot4 + sl) * V.nmonp + m;
+                        s1 += fabs(num1s[i]);
+                        s0 += fabs(num0s[i]);
+                    }
+                    c1 = s1 > c1 ? s1 : c1;
+                    c0 = s0 > c0 ? s0 : c0;
+                }
+            const double cmax = c1 > c0 ? c1 : c0;
+            int cs = 0;
+            while (ldexp(1.0, cs) < cmax) ++cs;
+            V.kbits = 53 - cs;
+            V.nsplit = 2;
+            V.shift = sh;
+        }
         void *d_counts, *d_offs, *d_coef, *d_num, *d_offs4;
         CUDA_TRY(cudaMalloc(&d_offs4, offs4.size() * sizeof(int2)));
         p->dev_allocs.push_back(d_offs4);
@@ -219,6 +254,18 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         CUDA_TRY(cudaMemcpy(d_coef, coef.data(), coef.size() * sizeof(double2), cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(d_num, nump.data(), nump.size() * sizeof(double), cudaMemcpyHostToDevice));
         V.num = (const double *)d_num;
+        if (V.nsplit == 2) {
+            void *d1, *d0;
+            CUDA_TRY(cudaMalloc(&d1, num1s.size() * sizeof(double)));
+            p->dev_allocs.push_back(d1);
+            CUDA_TRY(cudaMalloc(&d0, num0s.size() * sizeof(double)));
+            p->dev_allocs.push_back(d0);
+            CUDA_TRY(cudaMemcpy(d1, num1s.data(), num1s.size() * sizeof(double), cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(d0, num0s.data(), num0s.size() * sizeof(double), cudaMemcpyHostToDevice));
+            V.numf = V.num;             // full numerators: the G0 limb
+            V.num = (const double *)d1;  // n1 with G1 (exact)
+            V.num2 = (const double *)d0; // n0 with G1 (exact)
+        }
         for (uint32_t r = 0; r < nreg; ++r)
             for (int s2 = 0; s2 < counts[r]; ++s2) {
                 double sb = 0.0;

@@ -339,6 +339,96 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
 // the horizontal sums (Theta), then the final level of the sweep, row by row.
 // Returns false (nothing done) when the ring does not fit in `ring_bytes`.
 // ---------------------------------------------------------------------------
+// Split-numerator variant (tables with n = n1 2^shift + n0): three
+// limbs per item, G1 x n1 and G1 x n0 exact, G0 x n rounded; then
+// E = (A1 2^shift + A0) + B in double-double and the same row / x Horner.
+template <int DEG, int NT>
+__device__ __forceinline__ void fused_rows3(const double (&C)[3][NT][2], double sc, double fy, int kq,
+                                            double (&Rh)[RowCfg<DEG>::QMAX], double (&Rl)[RowCfg<DEG>::QMAX]) {
+    constexpr int QMAX = RowCfg<DEG>::QMAX;
+    const unsigned smask = kq == 0 ? bsf_start_mask(DEG, 0)
+                           : kq == 1 ? bsf_start_mask(DEG, 1)
+                           : kq == 2 ? bsf_start_mask(DEG, 2) : bsf_start_mask(DEG, 3);
+    const unsigned vmask = kq == 0 ? bsf_valid_mask(DEG, 0)
+                           : kq == 1 ? bsf_valid_mask(DEG, 1)
+                           : kq == 2 ? bsf_valid_mask(DEG, 2) : bsf_valid_mask(DEG, 3);
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) Rh[q] = Rl[q] = 0.0;
+    double rh = 0.0, rl = 0.0;
+    int q = -1;
+#pragma unroll
+    for (int k = 0; k < 2 * NT; ++k) {
+        const bool start = (smask >> k) & 1, valid = (vmask >> k) & 1;
+        const dd e = dd_add_d(two_sum(C[0][k >> 1][k & 1] * sc, C[2][k >> 1][k & 1]), C[1][k >> 1][k & 1]);
+        double nh = rh, nl = rl;
+        comp_step(nh, nl, fy, e.hi, e.lo);
+        if (start) {
+#pragma unroll
+            for (int qq = 0; qq < QMAX; ++qq)
+                if (qq == q) {
+                    Rh[qq] = rh;
+                    Rl[qq] = rl;
+                }
+            ++q;
+        }
+        rh = start ? e.hi : (valid ? nh : rh);
+        rl = start ? e.lo : (valid ? nl : rl);
+    }
+#pragma unroll
+    for (int qq = 0; qq < QMAX; ++qq)
+        if (qq == q) {
+            Rh[qq] = rh;
+            Rl[qq] = rl;
+        }
+}
+
+template <int DEG, int MT>
+__device__ __forceinline__ void fused_group3(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
+                                             const int (&byt)[MT], const double (&fxt)[MT], const double (&fyt)[MT],
+                                             const int2 *__restrict__ offs, const double *__restrict__ num1,
+                                             const double *__restrict__ num0, const double *__restrict__ numf,
+                                             int nmonp, int n4, int shift, double (&Fh)[MT], double (&Fl)[MT],
+                                             int &flags) {
+    constexpr int NT = DegCfg<DEG>::NT;
+    const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
+    double C[MT][3][NT][2];
+#pragma unroll
+    for (int t = 0; t < MT; ++t)
+#pragma unroll
+        for (int L = 0; L < 3; ++L)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) C[t][L][j][0] = C[t][L][j][1] = 0.0;
+    for (int s0 = 0; s0 < n4; s0 += 4) {
+        const int s = s0 + kq;
+        const int2 d = __ldg(offs + s);
+        double2 av[MT];
+#pragma unroll
+        for (int t = 0; t < MT; ++t) av[t] = load_split(G, NX, NY, bxt[t] + d.x, byt[t] + d.y, flags);
+        const size_t o = (size_t)s * nmonp + gq;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const double b1 = __ldg(num1 + o + 8 * j), b0 = __ldg(num0 + o + 8 * j), bf = __ldg(numf + o + 8 * j);
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+                dmma(C[t][0][j], av[t].x, b1);  // exact
+                dmma(C[t][2][j], av[t].x, b0);  // exact
+                dmma(C[t][1][j], av[t].y, bf);
+            }
+        }
+    }
+    const double sc = ldexp(1.0, shift);
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+        double Rh[RowCfg<DEG>::QMAX], Rl[RowCfg<DEG>::QMAX];
+        fused_rows3<DEG, NT>(C[t], sc, fyt[t], kq, Rh, Rl);
+        double ah, al;
+        fused_xhorner<DEG, DEG>(Rh, Rl, fxt[t], ah, al);
+        const dd F = fast_two_sum(ah, al);
+        Fh[t] = F.hi;
+        Fl[t] = F.lo;
+    }
+}
+
 template <int R>
 __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int Y0, int basis, const TileArgs &a,
                             int img, double2 *ring, size_t ring_bytes) {
@@ -802,7 +892,19 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     }
                     long long tq0 = 0;
                     if (a.prof && lane == 0) tq0 = clock64();
-                    if (var == 0)
+                    bool split3 = false;
+                    if constexpr (R >= 3) split3 = V.nsplit == 2;
+                    if (split3) {
+                        if constexpr (R >= 3) {
+                            const size_t ro = (size_t)reg * V.nslot4 * V.nmonp;
+                            if (var == 0)
+                                fused_group3<4 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.num2 + ro,
+                                                            V.numf + ro, V.nmonp, n4, V.shift, Fh, Fl, flags);
+                            else
+                                fused_group3<3 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.num2 + ro,
+                                                            V.numf + ro, V.nmonp, n4, V.shift, Fh, Fl, flags);
+                        }
+                    } else if (var == 0)
                         fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.nmonp, n4, Fh, Fl, flags);
                     else
                         fused_group<3 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.nmonp, n4, Fh, Fl, flags);

@@ -97,7 +97,11 @@ struct LutVar {
     const int2 *offs4;     // [nreg][nslot4] window offsets, padded with (0, 0)
     int nmonp;             // 8 bsf_nt(deg) columns (FP64 MMA n-tiles), bsf_mono_col layout
     int nslot4;            // nmax rounded up to 4 (FP64 MMA k-steps)
-    int kbits;             // |G1| <= 2^kbits keeps sum_s G1 * n exact in fp64
+    int kbits;             // |G1| <= 2^kbits keeps sum_s G1 * n (or n1, n0) exact in fp64
+    int nsplit;            // 1: num = n; 2: numerators split n = n1 2^shift + n0 (num = n1, num2 = n0, numf = n)
+    int shift;
+    const double *num2;    // [nreg][nslot4][nmonp] n0 (nsplit 2)
+    const double *numf;    // [nreg][nslot4][nmonp] n (nsplit 2: the G0 limb's operand)
     double bnd;            // bound on |F - F^| (units 2^e) of the split contraction: gamma_{n+1} 0.5 max_reg sum_s,mu |n|
     double L;              // common denominator
 };

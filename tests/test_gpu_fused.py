@@ -40,18 +40,22 @@ def test_dispatch():
     pts = synth.sample_points(w, 4, seed=1)
     tile_points(plan, synth.make_image(w)[None], synth.make_cov(w), pts)
     assert plan.uses_fused()
-    # Theta' at r = 3: the exact limb would be 4 bits -> double-double tile kernel
+    # Theta' at r = 3: a 4-bit exact limb unsplit -> split numerators, still fused
     w3 = synth.workload(1, width=40, height=40)
     p3 = make_plan(w3, policy=1, order=3, anchor=TILE)
     tile_points(p3, synth.make_image(w3)[None], synth.make_cov(w3), synth.sample_points(w3, 2, seed=1))
-    assert not p3.uses_fused()
+    assert p3.uses_fused()
+    # order 4: double-double tile kernel
+    p4 = make_plan(w3, policy=0, order=4, anchor=TILE)
+    tile_points(p4, synth.make_image(w3)[None], synth.make_cov(w3), synth.sample_points(w3, 2, seed=1))
+    assert not p4.uses_fused()
     with _env(BSF_FUSED=0):
         p0 = make_plan(w, anchor=TILE)
         tile_points(p0, synth.make_image(w)[None], synth.make_cov(w), pts)
         assert not p0.uses_fused()
 
 
-@pytest.mark.parametrize("config,order,n", [(2, 2, 3000), (3, 1, 3000), (3, 2, 600)])
+@pytest.mark.parametrize("config,order,n", [(2, 2, 3000), (3, 1, 3000), (3, 2, 600), (4, 3, 60)])
 def test_fused_matches_double_double_kernel(config, order, n):
     """Split contraction vs the all-double-double tile kernel on the same
     (full-size) workload: both are far more accurate than the 1e-9 contract,
