@@ -109,6 +109,13 @@ def algorithmic_fma_per_px(order: int, basis_counts) -> float:
     return tot
 
 
+def workload_config(w, world, precision, anchor):
+    """The `config` object of the JSON line (shared by both arms)."""
+    return {"workload": w.name, "width": w.width, "height": w.height, "order": w.order,
+            "basis": "dual" if w.basis == 2 else str(w.basis), "in_dtype": w.in_dtype, "precision": precision,
+            "anchor": anchor, "l2": "flushed between steps (256 MB write, untimed)", "parallelism": "dp%d" % world}
+
+
 def run_reference(args, w):
     """CPU oracle arm: bounded samples of the workload per step."""
     import oracle as O
@@ -135,7 +142,8 @@ def run_reference(args, w):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": w.name, "order": w.order, "basis": "dual"},
+            "data": "synthetic",
+            "config": workload_config(w, 1, "oracle: fp64 direct sum with the exact box-spline kernel", "none"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
                              "sample": "%d stratified pixels per step of %s (direct sum, exact kernel)" % (
                                  per_step, w.name)},
@@ -348,13 +356,11 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "width": w.width, "height": w.height, "order": w.order,
-                       "basis": "dual" if w.basis == 2 else str(w.basis), "in_dtype": w.in_dtype,
-                       "precision": ("exact split contraction (2 fp64 limbs)" if tile and plan.uses_fused() else
-                                     {"dd": "double-double", "fp64": "fp64",
-                                      "auto": "fp64 + a-posteriori bound, double-double fallback"}[args.precision]),
-                       "anchor": args.anchor,
-                       "l2": "flushed between steps (256 MB write, untimed)", "parallelism": "dp%d" % world},
+            "config": workload_config(
+                w, world,
+                "exact split contraction (2 fp64 limbs)" if tile and plan.uses_fused() else
+                {"dd": "double-double", "fp64": "fp64",
+                 "auto": "fp64 + a-posteriori bound, double-double fallback"}[args.precision], args.anchor),
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
             "stats": {k: stats[k] for k in ("pixels", "clamped", "zero_scale", "theta_prime", "flags",

@@ -28,8 +28,13 @@ cov = synth.make_cov(w, device=dev).contiguous()
 out = torch.empty((1, w.height, w.width), dtype=torch.float64, device=dev)
 plan.run(img, cov, out)
 plan.phase_cycles(reset=True)
+plan.stats(reset=True)
 plan.run(img, cov, out)
 cyc = plan.phase_cycles()
+st = plan.stats(reset=True)
+print("pixels %d, double-double fallback %d (%.3f %%), macs/px %.0f" % (
+    st["pixels"], st["double_double"], 100.0 * st["double_double"] / max(st["pixels"], 1),
+    st["macs"] / max(st["pixels"], 1)))
 tot = sum(cyc[:6]) + cyc[8] + cyc[9] + cyc[10]
 print("workload", w.name, "fused", plan.uses_fused())
 for n, c in zip(PHASES, cyc):
