@@ -339,40 +339,102 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
 // the horizontal sums (Theta), then the final level of the sweep, row by row.
 // Returns false (nothing done) when the ring does not fit in `ring_bytes`.
 // ---------------------------------------------------------------------------
-// Split-numerator variant (tables with n = n1 2^shift + n0): three
-// limbs per item, G1 x n1 and G1 x n0 exact, G0 x n rounded; then
-// E = (A1 2^shift + A0) + B in double-double and the same row / x Horner.
-template <int DEG, int NT>
-__device__ __forceinline__ void fused_rows3(const double (&C)[3][NT][2], double sc, double fy, int kq,
-                                            double (&Rh)[RowCfg<DEG>::QMAX], double (&Rl)[RowCfg<DEG>::QMAX]) {
-    constexpr int QMAX = RowCfg<DEG>::QMAX;
+// Order >= 3: three G limbs split on the fly from the double-double planes,
+// G = 2^e (G1 + 2^-k G2 + 2^-k G0), G1, G2 integers below 2^k (k = kbits),
+// |G0| <= 1/2: G1 and G2 are contracted exactly, only G0 carries rounding, so
+// the contraction error is 2^-k smaller than with two limbs (the (D/a)^{4r}
+// conditioning of r = 3 needs it).  With split numerators (NSPLIT 2) the two
+// exact limbs each meet n1 and n0.  The N dimension is taken in passes of NP
+// n-tiles (bounded registers); the lock-step row Horner resumes across passes.
+template <int DEG, int NSPLIT, int NP>
+__device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, int NX, int NY, int bx, int by,
+                                               double fx, double fy, const int2 *__restrict__ offs,
+                                               const double *__restrict__ numA, const double *__restrict__ numB,
+                                               const double *__restrict__ numF, int nmonp, int n4, int shift,
+                                               double sc_e, int kbits, double &Fh, double &Fl, int &flags) {
+    constexpr int NT = DegCfg<DEG>::NT, NL = NSPLIT == 1 ? 3 : 5, QMAX = RowCfg<DEG>::QMAX;
+    const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
+    const double S = ldexp(1.0, kbits), iS = ldexp(1.0, -kbits), ssh = ldexp(1.0, shift);
     const unsigned smask = kq == 0 ? bsf_start_mask(DEG, 0)
                            : kq == 1 ? bsf_start_mask(DEG, 1)
                            : kq == 2 ? bsf_start_mask(DEG, 2) : bsf_start_mask(DEG, 3);
     const unsigned vmask = kq == 0 ? bsf_valid_mask(DEG, 0)
                            : kq == 1 ? bsf_valid_mask(DEG, 1)
                            : kq == 2 ? bsf_valid_mask(DEG, 2) : bsf_valid_mask(DEG, 3);
+    double Rh[QMAX], Rl[QMAX];
 #pragma unroll
     for (int q = 0; q < QMAX; ++q) Rh[q] = Rl[q] = 0.0;
     double rh = 0.0, rl = 0.0;
     int q = -1;
+    for (int j0 = 0; j0 < NT; j0 += NP) {
+        double C[NL][NP][2];
 #pragma unroll
-    for (int k = 0; k < 2 * NT; ++k) {
-        const bool start = (smask >> k) & 1, valid = (vmask >> k) & 1;
-        const dd e = dd_add_d(two_sum(C[0][k >> 1][k & 1] * sc, C[2][k >> 1][k & 1]), C[1][k >> 1][k & 1]);
-        double nh = rh, nl = rl;
-        comp_step(nh, nl, fy, e.hi, e.lo);
-        if (start) {
+        for (int L = 0; L < NL; ++L)
 #pragma unroll
-            for (int qq = 0; qq < QMAX; ++qq)
-                if (qq == q) {
-                    Rh[qq] = rh;
-                    Rl[qq] = rl;
+            for (int j = 0; j < NP; ++j) C[L][j][0] = C[L][j][1] = 0.0;
+        for (int s0 = 0; s0 < n4; s0 += 4) {
+            const int s = s0 + kq;
+            const int2 d = __ldg(offs + s);
+            const int lx = bx + d.x, ly = by + d.y;
+            const bool inside = lx >= 0 && lx < NX && ly >= 0 && ly < NY;
+            flags |= (ly >= 0 && !inside) ? FLAG_RANGE : 0;
+            const double2 g = G[inside ? (size_t)ly * NX + lx : 0];
+            double g1 = 0.0, g2 = 0.0, g0 = 0.0;
+            if (inside) {
+                const double h = g.x * sc_e;  // exact (power of two)
+                g1 = rint(h);
+                const double r = (h - g1) * S;  // exact: |h - g1| <= 1/2
+                g2 = rint(r);
+                g0 = (r - g2) + g.y * sc_e * S;
+            }
+            const size_t o = (size_t)s * nmonp + gq + 8 * j0;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                if (j0 + j >= NT) break;
+                const double bA = __ldg(numA + o + 8 * j);
+                dmma(C[0][j], g1, bA);  // exact
+                dmma(C[1][j], g2, bA);  // exact
+                if constexpr (NSPLIT == 1) {
+                    dmma(C[2][j], g0, bA);
+                } else {
+                    const double bB = __ldg(numB + o + 8 * j), bF = __ldg(numF + o + 8 * j);
+                    dmma(C[2][j], g0, bF);
+                    dmma(C[3][j], g1, bB);  // exact
+                    dmma(C[4][j], g2, bB);  // exact
                 }
-            ++q;
+            }
         }
-        rh = start ? e.hi : (valid ? nh : rh);
-        rl = start ? e.lo : (valid ? nl : rl);
+        // rows over this pass's slots (lock step, as fused_rows)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            if (j0 + j >= NT) break;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const int k = 2 * (j0 + j) + h2;
+                const bool start = (smask >> k) & 1, valid = (vmask >> k) & 1;
+                dd e;
+                if constexpr (NSPLIT == 1) {
+                    e = dd_add_d(two_sum(C[0][j][h2], C[1][j][h2] * iS), C[2][j][h2] * iS);
+                } else {
+                    const dd x = two_sum(C[0][j][h2] * ssh, C[3][j][h2]);
+                    const dd y = two_sum(C[1][j][h2] * ssh, C[4][j][h2]);
+                    e = dd_add_d(dd_add(x, {y.hi * iS, y.lo * iS}), C[2][j][h2] * iS);
+                }
+                double nh = rh, nl = rl;
+                comp_step(nh, nl, fy, e.hi, e.lo);
+                if (start) {
+#pragma unroll
+                    for (int qq = 0; qq < QMAX; ++qq)
+                        if (qq == q) {
+                            Rh[qq] = rh;
+                            Rl[qq] = rl;
+                        }
+                    ++q;
+                }
+                rh = start ? e.hi : (valid ? nh : rh);
+                rl = start ? e.lo : (valid ? nl : rl);
+            }
+        }
     }
 #pragma unroll
     for (int qq = 0; qq < QMAX; ++qq)
@@ -380,53 +442,11 @@ __device__ __forceinline__ void fused_rows3(const double (&C)[3][NT][2], double 
             Rh[qq] = rh;
             Rl[qq] = rl;
         }
-}
-
-template <int DEG, int MT>
-__device__ __forceinline__ void fused_group3(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
-                                             const int (&byt)[MT], const double (&fxt)[MT], const double (&fyt)[MT],
-                                             const int2 *__restrict__ offs, const double *__restrict__ num1,
-                                             const double *__restrict__ num0, const double *__restrict__ numf,
-                                             int nmonp, int n4, int shift, double (&Fh)[MT], double (&Fl)[MT],
-                                             int &flags) {
-    constexpr int NT = DegCfg<DEG>::NT;
-    const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
-    double C[MT][3][NT][2];
-#pragma unroll
-    for (int t = 0; t < MT; ++t)
-#pragma unroll
-        for (int L = 0; L < 3; ++L)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) C[t][L][j][0] = C[t][L][j][1] = 0.0;
-    for (int s0 = 0; s0 < n4; s0 += 4) {
-        const int s = s0 + kq;
-        const int2 d = __ldg(offs + s);
-        double2 av[MT];
-#pragma unroll
-        for (int t = 0; t < MT; ++t) av[t] = load_split(G, NX, NY, bxt[t] + d.x, byt[t] + d.y, flags);
-        const size_t o = (size_t)s * nmonp + gq;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-            const double b1 = __ldg(num1 + o + 8 * j), b0 = __ldg(num0 + o + 8 * j), bf = __ldg(numf + o + 8 * j);
-#pragma unroll
-            for (int t = 0; t < MT; ++t) {
-                dmma(C[t][0][j], av[t].x, b1);  // exact
-                dmma(C[t][2][j], av[t].x, b0);  // exact
-                dmma(C[t][1][j], av[t].y, bf);
-            }
-        }
-    }
-    const double sc = ldexp(1.0, shift);
-#pragma unroll
-    for (int t = 0; t < MT; ++t) {
-        double Rh[RowCfg<DEG>::QMAX], Rl[RowCfg<DEG>::QMAX];
-        fused_rows3<DEG, NT>(C[t], sc, fyt[t], kq, Rh, Rl);
-        double ah, al;
-        fused_xhorner<DEG, DEG>(Rh, Rl, fxt[t], ah, al);
-        const dd F = fast_two_sum(ah, al);
-        Fh[t] = F.hi;
-        Fl[t] = F.lo;
-    }
+    double ah, al;
+    fused_xhorner<DEG, DEG>(Rh, Rl, fx, ah, al);
+    const dd F = fast_two_sum(ah, al);
+    Fh = F.hi;
+    Fl = F.lo;
 }
 
 template <int R>
@@ -714,6 +734,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         }
         __syncthreads();
         for (int pi = 0; pi < NPLANE; ++pi) {
+            if constexpr (R >= 3) break;  // order >= 3 splits on the fly (fused_group_g3)
             const int b = pi / NVAR, v = pi % NVAR;
             if (!((s_vmask[b] >> v) & 1)) continue;
             double2 *G = scr + s_poff[pi];
@@ -892,17 +913,28 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     }
                     long long tq0 = 0;
                     if (a.prof && lane == 0) tq0 = clock64();
-                    bool split3 = false;
-                    if constexpr (R >= 3) split3 = V.nsplit == 2;
-                    if (split3) {
-                        if constexpr (R >= 3) {
-                            const size_t ro = (size_t)reg * V.nslot4 * V.nmonp;
+                    if constexpr (R >= 3) {
+                        // three G limbs from the double-double plane (MT = 1)
+                        const size_t ro = (size_t)reg * V.nslot4 * V.nmonp;
+                        const double sce = ldexp(1.0, -s_pe[b * NVAR + var]);
+                        if (V.nsplit == 2) {
                             if (var == 0)
-                                fused_group3<4 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.num2 + ro,
-                                                            V.numf + ro, V.nmonp, n4, V.shift, Fh, Fl, flags);
+                                fused_group_g3<4 * R - 2, 2, 2>(G, NX, NY, bxt[0], byt[0], fxt[0], fyt[0], offs, num,
+                                                                V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift, sce,
+                                                                V.kbits, Fh[0], Fl[0], flags);
                             else
-                                fused_group3<3 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.num2 + ro,
-                                                            V.numf + ro, V.nmonp, n4, V.shift, Fh, Fl, flags);
+                                fused_group_g3<3 * R - 2, 2, 2>(G, NX, NY, bxt[0], byt[0], fxt[0], fyt[0], offs, num,
+                                                                V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift, sce,
+                                                                V.kbits, Fh[0], Fl[0], flags);
+                        } else {
+                            if (var == 0)
+                                fused_group_g3<4 * R - 2, 1, 3>(G, NX, NY, bxt[0], byt[0], fxt[0], fyt[0], offs, num,
+                                                                nullptr, nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh[0],
+                                                                Fl[0], flags);
+                            else
+                                fused_group_g3<3 * R - 2, 1, 3>(G, NX, NY, bxt[0], byt[0], fxt[0], fyt[0], offs, num,
+                                                                nullptr, nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh[0],
+                                                                Fl[0], flags);
                         }
                     } else if (var == 0)
                         fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.nmonp, n4, Fh, Fl, flags);
@@ -986,7 +1018,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         // a-posteriori bound of the split contraction:
                         // |S^ - S| <= sum_j |c_j| bnd + (2 ntap + 8) u^2 sum_j |c_j F_j|, sum_j |c_j| = 2^(R ns)
                         const int ns = var ? 3 : 4;
-                        const double err = ldexp(luts[b].var[var].bnd, R * ns) + 2.5e-30 * (NTAP / 81.0 + 1.0) * sumCF;
+                        const double lb = R >= 3 ? ldexp(luts[b].var[var].bnd, -luts[b].var[var].kbits)
+                                                 : luts[b].var[var].bnd;  // three limbs: 2^-kbits tighter
+                        const double err = ldexp(lb, R * ns) + 2.5e-30 * (NTAP / 81.0 + 1.0) * sumCF;
                         erel = err / fabs(Sd);
                         if (!(erel <= a.split_tol)) {  // NaN-safe: recompute in double-double
                             const int k = atomicAdd(&s_nfb, 1);
@@ -1033,7 +1067,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
 #pragma unroll
                 for (int k = 0; k < 4; ++k) ps.ap[k] = s_ap[4 * p + k];
                 const int b = ps.basis;
-                const double sc = (s_vmask[b] & 1) ? ldexp(1.0, s_pe[b * NVAR]) : 0.0;
+                const double sc = (R < 3 && (s_vmask[b] & 1)) ? ldexp(1.0, s_pe[b * NVAR]) : 0.0;
                 GView gv = {scr + s_poff[b * NVAR], s_dom[b][0], s_dom[b][1], s_dom[b][2], s_dom[b][3], sc};
                 const int x = x0 + (p % TILE), y = y0 + p / TILE;
                 int fl = 0;
