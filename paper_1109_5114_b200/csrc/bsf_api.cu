@@ -132,30 +132,33 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         V.nmon = hv[2];
         V.nmax = hv[3];
         uint64_t Lden;
-        if (!take(&Lden, 8) || Lden == 0 || Lden >= (1ull << 53)) return set_err(BSF_EINVAL, "bad denominator");
-        const double L = (double)Lden;
+        if (!take(&Lden, 8) || Lden >= (1ull << 53)) return set_err(BSF_EINVAL, "bad denominator");
+        const bool exact = Lden != 0;  // 0: double-double pairs, no integer form (no fused path)
+        const double L = exact ? (double)Lden : 1.0;
         std::vector<int> counts(nreg);
         std::vector<int2> offs((size_t)nreg * V.nmax, make_int2(0, 0));
-        std::vector<double> num((size_t)nreg * V.nmax * V.nmon);
+        std::vector<double> num((size_t)nreg * V.nmax * V.nmon, 0.0);
+        std::vector<double2> coef(num.size());
         for (uint32_t r = 0; r < nreg; ++r) {
             take(&counts[r], 4);
             for (int s = 0; s < V.nmax; ++s) {
                 int o[2];
                 take(o, 8);
                 offs[(size_t)r * V.nmax + s] = make_int2(o[0], o[1]);
-                if (!take(&num[((size_t)r * V.nmax + s) * V.nmon], 8 * (size_t)V.nmon))
+                const size_t at = ((size_t)r * V.nmax + s) * V.nmon;
+                if (!(exact ? take(&num[at], 8 * (size_t)V.nmon) : take(&coef[at], 16 * (size_t)V.nmon)))
                     return set_err(BSF_EINVAL, "truncated table");
             }
         }
         // double-double coefficients n / L, correctly rounded: hi = fl(n/L);
         // n - hi*L is exact in one fma (it is a multiple of ulp(hi) below L*ulp(hi)),
         // lo = fl((n - hi*L)/L).
-        std::vector<double2> coef(num.size());
-        for (size_t i = 0; i < num.size(); ++i) {
-            double hi = num[i] / L;
-            double rem = fma(-hi, L, num[i]);
-            coef[i] = make_double2(hi, rem / L);
-        }
+        if (exact)
+            for (size_t i = 0; i < num.size(); ++i) {
+                double hi = num[i] / L;
+                double rem = fma(-hi, L, num[i]);
+                coef[i] = make_double2(hi, rem / L);
+            }
         // integer table for the exact split contraction (bsf_fused.cuh, FP64
         // tensor-core fragments): per region nslot4 = nmax rounded up to 4 window
         // slots, per slot nmonp = nmon rounded up to 8 monomials (zero padded),
@@ -199,13 +202,13 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         // sums of G1 * n stay exact while |G1| sum|n| <= 2^53
         int cm = 0;
         while (ldexp(1.0, cm) < colmax) ++cm;
-        V.kbits = 53 - cm;
+        V.kbits = exact ? 53 - cm : 0;  // no integer form: the fused path is unavailable
         V.L = L;
         V.nsplit = 1;
         V.shift = 0;
         V.num2 = V.numf = nullptr;
         std::vector<double> num1s, num0s;
-        if (V.kbits < KBITS_MIN) {
+        if (exact && V.kbits < KBITS_MIN) {
             // split the numerators n = n1 2^sh + n0 (|n0| <= 2^(sh-1)) so that both
             // column sums, and with them the exact limb, stay wide
             const int sh = (int)ceil(0.5 * log2(2.0 * colmax / V.nslot4));

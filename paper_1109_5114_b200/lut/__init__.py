@@ -62,13 +62,18 @@ def load(basis: int, r: int):
         counts = np.zeros(nreg, dtype=np.int32)
         offs = np.zeros((nreg, nmax, 2), dtype=np.int32)
         num = np.zeros((nreg, nmax, nmon))
+        coef = np.zeros((nreg, nmax, nmon, 2))
         for ri in range(nreg):
             (counts[ri],) = take("<i")
             for s in range(nmax):
                 offs[ri, s] = take("<ii")
-                num[ri, s] = np.array(take("<%dd" % nmon))
-        hi, lo = _dd_of_ratio(num, L)
-        coef = np.stack([hi, lo], axis=-1)
+                if L:
+                    num[ri, s] = np.array(take("<%dd" % nmon))
+                else:  # double-double pairs (no exact integer form)
+                    coef[ri, s] = np.array(take("<%dd" % (2 * nmon))).reshape(nmon, 2)
+        if L:
+            hi, lo = _dd_of_ratio(num, L)
+            coef = np.stack([hi, lo], axis=-1)
         variants.append(dict(drop=drop, deg=deg, nmon=nmon, nmax=nmax, counts=counts, offs=offs, coef=coef,
                              num=num, L=L))
     return dict(basis=basis, r=r, normals=normals, keys=keys, centres=np.array(centres), variants=variants)

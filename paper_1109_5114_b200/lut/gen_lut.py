@@ -423,7 +423,9 @@ def write_bin(path, basis, r, variants):
     4 knot-line normals; per region key[4] and centre[2]; per variant
     (drop, deg, nmon, nmax), L (uint64, common denominator), then per region
     count and per window slot (dx, dy) and nmon numerators n (float64, exact
-    integers |n| < 2^53): coefficient = n / L."""
+    integers |n| < 2^53): coefficient = n / L.  When L or a numerator reaches
+    2^53 (Theta' at r = 4) L is written as 0 and the slot holds nmon
+    correctly rounded double-double pairs (hi, lo) instead."""
     regs = variants[0][3]
     out = bytearray()
     out += struct.pack("<IIIII", MAGIC, VERSION, basis, r, len(variants))
@@ -439,9 +441,9 @@ def write_bin(path, basis, r, variants):
         mons = monomials(deg)
         nmax = max(len(w) for w in table)
         L = integer_table(table, len(mons))
-        assert L < 2**53
+        exact = L < 2**53 and all(abs(v * L) < 2**53 for win in table for _, poly in win for v in poly.values())
         out += struct.pack("<iiii", -1 if drop is None else drop, deg, len(mons), nmax)
-        out += struct.pack("<Q", L)
+        out += struct.pack("<Q", L if exact else 0)  # 0: coefficients stored as double-double pairs
         for win in table:
             out += struct.pack("<i", len(win))
             for slot in range(nmax):
@@ -451,9 +453,13 @@ def write_bin(path, basis, r, variants):
                     (dx, dy), poly = (0, 0), {}
                 out += struct.pack("<ii", dx, dy)
                 for (i, j) in mons:
-                    n = poly.get((i, j), Fr(0)) * L
-                    assert n.denominator == 1 and abs(n.numerator) < 2**53
-                    out += struct.pack("<d", float(n.numerator))
+                    c = poly.get((i, j), Fr(0))
+                    if exact:
+                        n = c * L
+                        assert n.denominator == 1
+                        out += struct.pack("<d", float(n.numerator))
+                    else:
+                        out += struct.pack("<dd", *to_dd(c))
     with open(path, "wb") as fh:
         fh.write(out)
 
