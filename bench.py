@@ -93,6 +93,22 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def _ncu_traffic(workload):
+    """DRAM bytes per launch of the fused kernel from the committed ncu capture
+    of the default workload (None for other workloads)."""
+    if workload != "c2_1024_f32_smooth_r2":
+        return None
+    try:
+        import csv
+        rows = list(csv.reader(open(os.path.join(ROOT, "profiles", "r01_c2_fused_raw.csv"))))
+        d = dict(zip(rows[0], rows[2]))
+        unit = dict(zip(rows[0], rows[1]))
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        return sum(float(d[k]) * scale[unit[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    except Exception:
+        return None
+
+
 def _fp64_peak():
     with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as fh:
         return json.load(fh)
@@ -330,7 +346,10 @@ def main():
         names = ["scales", "pre_integration", "exact_split", "keys_sort", "gather", "accumulate"]
         roof = {"bound": "fp64-tensor", "kernel": "fused_kernel (pre-integration + gather, DMMA m8n8k4)",
                 "achieved": achieved, "peak": fp["fp64_tensor_peak_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / fp["fp64_tensor_peak_tflops"], "traffic": None,
+                "frac": achieved / fp["fp64_tensor_peak_tflops"], "traffic": _ncu_traffic(w.name),
+                "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full "
+                                  "capture (profiles/r01_c2_fused_raw.csv); algorithmic HBM bytes %d" % (
+                                      npx * in_b + 12 * npx + 8 * npx),
                 "peak_source": "measured: tools/fp64_peak.cu DMMA m8n8k4 (profiles/r01_fp64_peak.json)",
                 "algorithmic_macs_per_px": macs_px, "executed_limbs": 2, "kernel_ms": gat,
                 "share_of_step": gat / ms if ms else None,

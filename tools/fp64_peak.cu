@@ -124,7 +124,7 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     double *out;
     cudaMalloc(&out, 1 << 20);
-    for (int warps : {8, 16, 32}) {
+    for (int warps : {4, 8, 16, 32}) {
         int blocks = sms * 4, threads = warps * 32 / 4;
         float ms = timeit([&] { dfma_kernel<<<blocks, threads>>>(out, 1.0000001, 1e-9); });
         double flops = 2.0 * 16 * ITERS * (double)blocks * threads;
