@@ -879,7 +879,7 @@ size_t tile_capacity(int order, float max_sigma, const LutBasis *L, int basis_ma
     for (int b = 0; b < 2; ++b) {
         if (!(basis_mask & (1 << b))) continue;
         size_t nx = tile + 2 * E + (L[b].wxmax - L[b].wxmin) + 4 * order + 4;
-        size_t ny = tile + 2 * E + L[b].wymax + 2;
+        size_t ny = tile + 2 * E + L[b].wymax - L[b].wymin + 2;
         cap = nx * ny > cap ? nx * ny : cap;
     }
     return cap;

@@ -67,7 +67,9 @@ def test_fused_matches_double_double_kernel(config, order, n):
     with _env(BSF_FUSED=0):
         b = tile_points(make_plan(w, anchor=TILE), img[None], cov, pts)
     rel = (a - b).abs() / b.abs()
-    assert float(rel.max()) <= 1e-12, float(rel.max())
+    # at r = 3 the double-double kernel's own error reaches ~1e-12 on the most
+    # ill-conditioned pixels (u^2 times a condition number ~1e20)
+    assert float(rel.max()) <= (1e-12 if order < 3 else 1e-11), float(rel.max())
 
 
 @pytest.mark.parametrize("r", [1, 2])
