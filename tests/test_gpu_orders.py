@@ -42,6 +42,22 @@ def test_order3_small_all_pixels(anchor, policy):
     assert plan.stats()["flags"] == 0
 
 
+@pytest.mark.parametrize("policy", [0, 1, 2])
+def test_order4_small_points(policy):
+    """Order 4 (625 taps; the double-double tile kernel, both bases' tables)
+    on a small space-variant field, sampled pixels against the oracle."""
+    _need(4)
+    H, W = 24, 28
+    w, img, cov = _small_smooth(H, W, 2.0, seed=13)
+    plan = make_plan(w, policy=policy, order=4, anchor=TILE)
+    pts = synth.sample_points(w, 24, seed=17)
+    got = tile_points(plan, img[None], cov, pts).numpy()
+    xs, ys = pts[:, 1].numpy(), pts[:, 2].numpy()
+    ref, *_ = oracle_points(img.numpy(), cov.numpy(), xs, ys, policy=policy, r=4)
+    assert max_rel(got, ref) <= TOL64
+    assert plan.stats()["flags"] == 0
+
+
 def _window_points(w, n, seed, order, frame=0):
     """Sample points and, for each, a tile-aligned window containing its halo."""
     pts = synth.sample_points(w, n, seed=seed)
