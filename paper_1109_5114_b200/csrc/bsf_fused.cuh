@@ -211,7 +211,10 @@ __device__ __forceinline__ void fused_rows(const double (&C)[2][NT][2], double f
 #pragma unroll
     for (int k = 0; k < 2 * NT; ++k) {
         const bool start = (smask >> k) & 1, valid = (vmask >> k) & 1;
-        const dd e = two_sum(C[0][k >> 1][k & 1], C[1][k >> 1][k & 1]);
+        // (A, B) = (exact integer limb, remainder limb) is already an exact,
+        // unnormalised double-double of E (|B| <= 2^-kbits |A| scale): the
+        // compensated Horner step takes it as is
+        const dd e = {C[0][k >> 1][k & 1], C[1][k >> 1][k & 1]};
         double nh = rh, nl = rl;
         comp_step(nh, nl, fy, e.hi, e.lo);
         if (start) {
