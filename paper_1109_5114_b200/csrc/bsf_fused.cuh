@@ -260,10 +260,11 @@ __device__ __forceinline__ void fused_xhorner(const double (&Rh)[RowCfg<DEG>::QM
 // the two limbs as separate accumulators; then F = sum_mu E_mu phi^mu straight
 // from the accumulator fragments (rows per lane in phi_y, then phi_x across
 // the quad), compensated.  Lane l feeds and receives item l/4 + 8t of m-tile
-// t; (bxt, byt, fxt, fyt) are that item's tap base and fractional offset.
+// t; (bxt, byt) are that item's tap base; (fxo, fyo) the fractional offset of
+// the lane's own item (shuffled to the quads for the epilogue).
 template <int DEG, int MT>
 __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
-                                            const int (&byt)[MT], const double (&fxt)[MT], const double (&fyt)[MT],
+                                            const int (&byt)[MT], double fxo, double fyo,
                                             const int2 *__restrict__ offs, const double *__restrict__ num, int nmonp,
                                             int n4, double (&Fh)[MT], double (&Fl)[MT], int &flags) {
     constexpr int NT = DegCfg<DEG>::NT;
@@ -324,10 +325,13 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
     }
 #pragma unroll
     for (int t = 0; t < MT; ++t) {
+        // fractional offset of this m-tile's item, from the lane that set it up
+        const double fxq = __shfl_sync(0xffffffffu, fxo, gq + 8 * t);
+        const double fyq = __shfl_sync(0xffffffffu, fyo, gq + 8 * t);
         double Rh[RowCfg<DEG>::QMAX], Rl[RowCfg<DEG>::QMAX];
-        fused_rows<DEG, NT>(C[t], fyt[t], kq, Rh, Rl);
+        fused_rows<DEG, NT>(C[t], fyq, kq, Rh, Rl);
         double ah, al;
-        fused_xhorner<DEG, DEG>(Rh, Rl, fxt[t], ah, al);
+        fused_xhorner<DEG, DEG>(Rh, Rl, fxq, ah, al);
         const dd F = fast_two_sum(ah, al);
         Fh[t] = F.hi;
         Fl[t] = F.lo;
@@ -358,12 +362,14 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
 // n-tiles (bounded registers); the lock-step row Horner resumes across passes.
 template <int DEG, int NSPLIT, int NP>
 __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, int NX, int NY, int bx, int by,
-                                               double fx, double fy, const int2 *__restrict__ offs,
+                                               double fxo, double fyo, const int2 *__restrict__ offs,
                                                const double *__restrict__ numA, const double *__restrict__ numB,
                                                const double *__restrict__ numF, int nmonp, int n4, int shift,
                                                double sc_e, int kbits, double &Fh, double &Fl, int &flags) {
     constexpr int NT = DegCfg<DEG>::NT, NL = NSPLIT == 1 ? 3 : 5, QMAX = RowCfg<DEG>::QMAX;
     const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
+    // this lane's item (gq) fractional offset, from the lane that set it up
+    const double fx = __shfl_sync(0xffffffffu, fxo, gq), fy = __shfl_sync(0xffffffffu, fyo, gq);
     const double S = ldexp(1.0, kbits), iS = ldexp(1.0, -kbits), ssh = ldexp(1.0, shift);
     const unsigned smask = kq == 0 ? bsf_start_mask(DEG, 0)
                            : kq == 1 ? bsf_start_mask(DEG, 1)
@@ -909,18 +915,12 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     const int bx = x0 + (p % TILE) + (int)flx - s_dom[b][0];
                     const int by = y0 + p / TILE + (int)fly - s_dom[b][1];
                     const double fx = Dx - flx, fy = Dy - fly;
-                    int bxt[MT], byt[MT], idt[MT];
-                    double fxt[MT], fyt[MT];
-                    bool realt[MT];
+                    int bxt[MT], byt[MT];
 #pragma unroll
                     for (int q = 0; q < MT; ++q) {
                         const int src = (lane >> 2) + 8 * q;
                         bxt[q] = __shfl_sync(0xffffffffu, bx, src);
                         byt[q] = __shfl_sync(0xffffffffu, by, src);
-                        fxt[q] = __shfl_sync(0xffffffffu, fx, src);
-                        fyt[q] = __shfl_sync(0xffffffffu, fy, src);
-                        idt[q] = __shfl_sync(0xffffffffu, idx, src);
-                        realt[q] = __shfl_sync(0xffffffffu, (int)real, src) != 0;
                     }
                     const double2 *G = scr + s_poff[b * NVAR + var];
                     const LutVar &V = luts[b].var[var];
@@ -943,31 +943,33 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         const double sce = ldexp(1.0, -s_pe[b * NVAR + var]);
                         if (V.nsplit == 2) {
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 2, 2>(G, NX, NY, bxt[0], byt[0], fxt[0], fyt[0], offs, num,
+                                fused_group_g3<4 * R - 2, 2, 2>(G, NX, NY, bxt[0], byt[0], fx, fy, offs, num,
                                                                 V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift, sce,
                                                                 V.kbits, Fh[0], Fl[0], flags);
                             else
-                                fused_group_g3<3 * R - 2, 2, 2>(G, NX, NY, bxt[0], byt[0], fxt[0], fyt[0], offs, num,
+                                fused_group_g3<3 * R - 2, 2, 2>(G, NX, NY, bxt[0], byt[0], fx, fy, offs, num,
                                                                 V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift, sce,
                                                                 V.kbits, Fh[0], Fl[0], flags);
                         } else {
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 1, 3>(G, NX, NY, bxt[0], byt[0], fxt[0], fyt[0], offs, num,
+                                fused_group_g3<4 * R - 2, 1, 3>(G, NX, NY, bxt[0], byt[0], fx, fy, offs, num,
                                                                 nullptr, nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh[0],
                                                                 Fl[0], flags);
                             else
-                                fused_group_g3<3 * R - 2, 1, 3>(G, NX, NY, bxt[0], byt[0], fxt[0], fyt[0], offs, num,
+                                fused_group_g3<3 * R - 2, 1, 3>(G, NX, NY, bxt[0], byt[0], fx, fy, offs, num,
                                                                 nullptr, nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh[0],
                                                                 Fl[0], flags);
                         }
                     } else if (var == 0)
-                        fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.nmonp, n4, Fh, Fl, flags);
+                        fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);
                     else
-                        fused_group<3 * R - 2, MT>(G, NX, NY, bxt, byt, fxt, fyt, offs, num, V.nmonp, n4, Fh, Fl, flags);
-                    if ((lane & 3) == 0) {
+                        fused_group<3 * R - 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);
 #pragma unroll
-                        for (int q = 0; q < MT; ++q)
-                            if (realt[q]) s_F[idt[q]] = make_double2(Fh[q], Fl[q]);
+                    for (int q = 0; q < MT; ++q) {  // item lane/4 + 8q's result, from its quad's lane 0
+                        const int src = (lane >> 2) + 8 * q;
+                        const int iq = __shfl_sync(0xffffffffu, idx, src);
+                        const bool rq = __shfl_sync(0xffffffffu, (int)real, src) != 0;
+                        if ((lane & 3) == 0 && rq) s_F[iq] = make_double2(Fh[q], Fl[q]);
                     }
                     if (a.prof && lane == 0) {
                         const unsigned long long dt = clock64() - tq0;
