@@ -30,9 +30,12 @@ constexpr int NPLANE = 2 * NVAR;              // (basis, variant)
 constexpr uint16_t NOKEY = 0xFFFF;
 
 
+#ifndef BSF_MT1
+#define BSF_MT1 4
+#endif
 template <int R> struct FusedCfg;
 // NTAP taps per pixel, P pixels per chunk, MT 8-item m-tiles per group
-template <> struct FusedCfg<1> { static constexpr int NTAP = 16, P = 256, MT = 2; };
+template <> struct FusedCfg<1> { static constexpr int NTAP = 16, P = 256, MT = BSF_MT1; };
 template <> struct FusedCfg<2> { static constexpr int NTAP = 81, P = 64, MT = 4; };
 template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 16, MT = 1; };
 template <> struct FusedCfg<4> { static constexpr int NTAP = 625, P = 4, MT = 1; };
