@@ -43,6 +43,7 @@ struct bsf_plan_s {
     int tile_nslots = 0;
     bool fused = false;
     unsigned long long *prof = nullptr;  // phase cycles of the fused kernel (diagnostics)
+    double2 *fbuf = nullptr;             // fused path: per-CTA tap values
     int *tile_counter = nullptr;
     long long nlaunch = 0;
     cudaStream_t last = nullptr;
@@ -475,6 +476,12 @@ static bsf_status ensure_tile_ws(bsf_plan_s *p) {
     if (cudaMalloc(&q, bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "tile scratch " + std::to_string(bytes));
     p->dev_allocs.push_back(q);
     p->tile_scratch = (double2 *)q;
+    if (p->fused) {
+        const size_t fb = (size_t)p->tile_nslots * fused_fbuf_items(p->d.order) * sizeof(double2);
+        if (cudaMalloc(&q, fb) != cudaSuccess) return set_err(BSF_ENOMEM, "tap buffer " + std::to_string(fb));
+        p->dev_allocs.push_back(q);
+        p->fbuf = (double2 *)q;
+    }
     if (cudaMalloc(&q, sizeof(int)) != cudaSuccess) return set_err(BSF_ENOMEM, "tile counter");
     p->dev_allocs.push_back(q);
     p->tile_counter = (int *)q;
@@ -502,6 +509,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.nty = (p->geo.H + TILE - 1) / TILE;
     a.stats = p->stats;
     a.prof = p->prof;
+    a.fbuf = p->fbuf;
     // BSF_SPLIT_TOL (environment, diagnostics): override the fallback threshold
     const char *tol = getenv("BSF_SPLIT_TOL");
     a.split_tol = tol ? atof(tol) : BSF_SPLIT_TOL_DEFAULT;

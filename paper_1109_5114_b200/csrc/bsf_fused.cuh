@@ -36,9 +36,15 @@ constexpr uint16_t NOKEY = 0xFFFF;
 template <int R> struct FusedCfg;
 // NTAP taps per pixel, P pixels per chunk, MT 8-item m-tiles per group
 template <> struct FusedCfg<1> { static constexpr int NTAP = 16, P = 256, MT = BSF_MT1; };
-template <> struct FusedCfg<2> { static constexpr int NTAP = 81, P = 64, MT = 4; };
-template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 16, MT = 1; };
-template <> struct FusedCfg<4> { static constexpr int NTAP = 625, P = 4, MT = 1; };
+template <> struct FusedCfg<2> { static constexpr int NTAP = 81, P = 256, MT = 4; };
+template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 64, MT = 1; };
+template <> struct FusedCfg<4> { static constexpr int NTAP = 625, P = 16, MT = 1; };
+
+// per-tap interpolated values F (double-double) live in a per-CTA global
+// buffer (L2-resident) of fused_fbuf_items() entries, not in shared memory,
+// so a chunk can hold a whole sub-tile (less bucket padding)
+template <int R>
+constexpr int fused_items() { return FusedCfg<R>::P * FusedCfg<R>::NTAP; }
 
 // dynamic shared memory: the chunk buffers of phases 4-5, aliased by the
 // pre-integration ring of phase 2 (at least FUSED_SMEM_MIN bytes for it)
@@ -47,7 +53,7 @@ template <int R>
 constexpr size_t fused_smem_bytes() {
     constexpr size_t ITEMS = (size_t)FusedCfg<R>::P * FusedCfg<R>::NTAP;
     constexpr size_t GS = 8 * FusedCfg<R>::MT;
-    constexpr size_t chunk = ITEMS * 16 + FT * 4 * 8 + ITEMS * 2 + (ITEMS + GS * NKEY) * 2 + (FT / 32) * NKEY * 4 +
+    constexpr size_t chunk = FT * 4 * 8 + ITEMS * 2 + (ITEMS + GS * NKEY) * 2 + (FT / 32) * NKEY * 4 +
                              FT * 4;
     return chunk > FUSED_SMEM_MIN ? chunk : FUSED_SMEM_MIN;
 }
@@ -559,8 +565,8 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     constexpr int NTAP = FusedCfg<R>::NTAP, P = FusedCfg<R>::P, ITEMS = P * NTAP;
     constexpr int MT = FusedCfg<R>::MT, GS = 8 * MT;
     extern __shared__ __align__(16) unsigned char smem[];
-    double2 *s_F = reinterpret_cast<double2 *>(smem);
-    double *s_ap = reinterpret_cast<double *>(s_F + ITEMS);
+    double2 *s_F = a.fbuf + (size_t)blockIdx.x * ITEMS;  // global, L2-resident (see fused_items)
+    double *s_ap = reinterpret_cast<double *>(smem);
     uint16_t *s_key = reinterpret_cast<uint16_t *>(s_ap + FT * 4);
     uint16_t *s_sorted = s_key + ITEMS;
     int *s_hist = reinterpret_cast<int *>(s_sorted + ITEMS + GS * NKEY);  // [warp][key]
@@ -1144,6 +1150,16 @@ static cudaError_t launch_fused_r(const TileArgs &a, int slots, cudaStream_t st,
     }
     fused_kernel<R><<<slots, FT, sm, st>>>(a, luts);
     return cudaGetLastError();
+}
+
+size_t fused_fbuf_items(int order) {
+    switch (order) {
+        case 1: return fused_items<1>();
+        case 2: return fused_items<2>();
+        case 3: return fused_items<3>();
+        case 4: return fused_items<4>();
+    }
+    return 0;
 }
 
 int fused_slots() {

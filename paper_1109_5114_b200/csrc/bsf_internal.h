@@ -157,6 +157,7 @@ struct TileArgs {
     unsigned long long *stats;
     unsigned long long *prof;  // optional [8] phase cycles (bsf_debug_phase_cycles)
     double split_tol;          // relative bound above which a pixel is recomputed in double-double
+    double2 *fbuf;             // fused path: per-CTA tap values [slots][fused_items<R>()]
 };
 constexpr int TILE = 16;
 size_t tile_capacity(int order, float max_sigma, const LutBasis *host_luts, int basis_mask, int tile);
@@ -170,6 +171,7 @@ constexpr int NPLANE_MAX = 10;
 constexpr int KBITS_MIN = 20;
 constexpr double BSF_SPLIT_TOL_DEFAULT = 5e-10;  // half the fp64 parity tolerance; see TileArgs::split_tol  // tables whose exact limb would be narrower use the double-double tile kernel
 int fused_slots();
+size_t fused_fbuf_items(int order);
 cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStream_t st, const LutBasis *luts_dev,
                               long long *nlaunch);
 
