@@ -53,7 +53,7 @@ template <int R>
 constexpr size_t fused_smem_bytes() {
     constexpr size_t ITEMS = (size_t)FusedCfg<R>::P * FusedCfg<R>::NTAP;
     constexpr size_t GS = 8 * FusedCfg<R>::MT;
-    constexpr size_t chunk = FT * 4 * 8 + ITEMS * 2 + (ITEMS + GS * NKEY) * 2 + (FT / 32) * NKEY * 4 +
+    constexpr size_t chunk = FT * 4 * 8 + FT * 5 * 16 + ITEMS * 2 + (ITEMS + GS * NKEY) * 2 + (FT / 32) * NKEY * 4 +
                              FT * 4;
     return chunk > FUSED_SMEM_MIN ? chunk : FUSED_SMEM_MIN;
 }
@@ -159,6 +159,25 @@ __device__ __forceinline__ int cls_region(const ClsTables &T, int b, double x, d
         if (r >= 0) return r;
     }
     return 0;
+}
+
+// displacement of tap t from the per-pixel geometry (see the sub-tile scales):
+// identical to fused_tap's value, with 4 FMAs per coordinate
+template <int R>
+__device__ __forceinline__ void fused_tap_v(const double2 *tv, int drop, int t, double &Dx, double &Dy) {
+    const double2 c = tv[4];
+    Dx = c.x;
+    Dy = c.y;
+    int tt = t;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k == drop) continue;
+        const double j = (double)(tt % (R + 1));
+        tt /= (R + 1);
+        const double2 v = tv[k];
+        Dx = fma(-j, v.x, Dx);  // exact (R17)
+        Dy = fma(-j, v.y, Dy);
+    }
 }
 
 // binomial sign weight of tap t: prod_k (-1)^{j_k} C(R, j_k)
@@ -567,7 +586,8 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     extern __shared__ __align__(16) unsigned char smem[];
     double2 *s_F = a.fbuf + (size_t)blockIdx.x * ITEMS;  // global, L2-resident (see fused_items)
     double *s_ap = reinterpret_cast<double *>(smem);
-    uint16_t *s_key = reinterpret_cast<uint16_t *>(s_ap + FT * 4);
+    double2 *s_tv = reinterpret_cast<double2 *>(s_ap + FT * 4);  // [pixel][5]: s_k a'_k (k < 4), centre
+    uint16_t *s_key = reinterpret_cast<uint16_t *>(s_tv + FT * 5);
     uint16_t *s_sorted = s_key + ITEMS;
     int *s_hist = reinterpret_cast<int *>(s_sorted + ITEMS + GS * NKEY);  // [warp][key]
     int *s_info = s_hist + (FT / 32) * NKEY;
@@ -811,6 +831,19 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             s_info[tid] = ps.basis | ((ps.drop + 1) << 1) | (live ? 16 : 0) | (ps.clamped ? 32 : 0) | (ps.flags << 8);
 #pragma unroll
             for (int k = 0; k < 4; ++k) s_ap[tid * 4 + k] = ps.ap[k];
+            // tap geometry: v_k = s_k a'_k and the centre sum_{k != drop} (R/2) v_k,
+            // so tap j has D = centre - sum_k j_k v_k (all exact on the 2^-41 grid, R17)
+            double cx = 0.0, cy = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double vx = c_steps[ps.basis][k][0] * ps.ap[k], vy = c_steps[ps.basis][k][1] * ps.ap[k];
+                s_tv[tid * 5 + k] = make_double2(vx, vy);
+                if (k != ps.drop) {
+                    cx += (0.5 * R) * vx;
+                    cy += (0.5 * R) * vy;
+                }
+            }
+            s_tv[tid * 5 + 4] = make_double2(cx, cy);
         }
         __syncthreads();
         // ---- 4-5. taps bucketed by key, gather, per-pixel sums -------------------
@@ -839,7 +872,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     const int b = info_basis(w);
                     double Dx, Dy;
                     int cf;
-                    fused_tap<R>(s_ap + 4 * p, b, var - 1, t, Dx, Dy, cf);
+                    fused_tap_v<R>(s_tv + 5 * p, var - 1, t, Dx, Dy);
                     const int reg = cls_region(s_cls, b, Dx - floor(Dx), Dy - floor(Dy));
                     key = (uint16_t)((b * NVAR + var) * MAX_REG + reg);
                 }
@@ -918,8 +951,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     if (!real) idx = i0;  // dummy lanes repeat the group's first item
                     const int p = c0 + idx % P, t = idx / P;
                     double Dx, Dy;
-                    int cf;
-                    fused_tap<R>(s_ap + 4 * p, b, var - 1, t, Dx, Dy, cf);
+                    fused_tap_v<R>(s_tv + 5 * p, var - 1, t, Dx, Dy);
                     const double flx = floor(Dx), fly = floor(Dy);
                     const int bx = x0 + (p % TILE) + (int)flx - s_dom[b][0];
                     const int by = y0 + p / TILE + (int)fly - s_dom[b][1];
