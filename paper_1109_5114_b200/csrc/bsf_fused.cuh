@@ -282,6 +282,31 @@ __device__ __forceinline__ void fused_xhorner(const double (&Rh)[RowCfg<DEG>::QM
     if constexpr (I > 0) fused_xhorner<DEG, I - 1>(Rh, Rl, fx, ah, al);
 }
 
+// x-Horner of m-tile kq for four m-tiles: every row is shuffled for all four
+// m-tiles and each lane keeps its own (compile-time row / slot indices)
+template <int DEG, int I>
+__device__ __forceinline__ void fused_xhorner4(const double (&Rh)[4][RowCfg<DEG>::QMAX],
+                                               const double (&Rl)[4][RowCfg<DEG>::QMAX], int kq, double fx,
+                                               double &ah, double &al) {
+    constexpr int SRC = bsf_row_lane(DEG, I), Q = bsf_row_q(DEG, I);
+    const int src = (threadIdx.x & 28) | SRC;
+    double h = 0.0, l = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const double ht = __shfl_sync(0xffffffffu, Rh[t][Q], src);
+        const double lt = __shfl_sync(0xffffffffu, Rl[t][Q], src);
+        h = kq == t ? ht : h;
+        l = kq == t ? lt : l;
+    }
+    if constexpr (I == DEG) {
+        ah = h;
+        al = l;
+    } else {
+        comp_step(ah, al, fx, h, l);
+    }
+    if constexpr (I > 0) fused_xhorner4<DEG, I - 1>(Rh, Rl, kq, fx, ah, al);
+}
+
 // Contraction of one group of GS = 8 MT items sharing a key, on the FP64
 // tensor cores: for every item (M), window slot (K) and monomial (N)
 //   E_mu = sum_s G1_s n_{s,mu}  (exact)   and   sum_s G0_s n_{s,mu},
@@ -351,18 +376,37 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
                 dmma(C[t][1][j], aB[t].y, bB[j]);
             }
     }
+    if constexpr (MT == 4) {
+        // rows of all four m-tiles on their owner lanes; then lane kq of each
+        // quad runs the x-Horner of m-tile kq only (one x-Horner per lane
+        // instead of four): the result for item gq + 8 kq stays on lane (gq, kq)
+        constexpr int QMAX = RowCfg<DEG>::QMAX;
+        double Rh[MT][QMAX], Rl[MT][QMAX];
 #pragma unroll
-    for (int t = 0; t < MT; ++t) {
-        // fractional offset of this m-tile's item, from the lane that set it up
-        const double fxq = __shfl_sync(0xffffffffu, fxo, gq + 8 * t);
-        const double fyq = __shfl_sync(0xffffffffu, fyo, gq + 8 * t);
-        double Rh[RowCfg<DEG>::QMAX], Rl[RowCfg<DEG>::QMAX];
-        fused_rows<DEG, NT>(C[t], fyq, kq, Rh, Rl);
-        double ah, al;
-        fused_xhorner<DEG, DEG>(Rh, Rl, fxq, ah, al);
+        for (int t = 0; t < MT; ++t) {
+            const double fyq = __shfl_sync(0xffffffffu, fyo, gq + 8 * t);
+            fused_rows<DEG, NT>(C[t], fyq, kq, Rh[t], Rl[t]);
+        }
+        const double fxm = __shfl_sync(0xffffffffu, fxo, gq + 8 * kq);
+        double ah = 0.0, al = 0.0;
+        fused_xhorner4<DEG, DEG>(Rh, Rl, kq, fxm, ah, al);
         const dd F = fast_two_sum(ah, al);
-        Fh[t] = F.hi;
-        Fl[t] = F.lo;
+        Fh[0] = F.hi;  // this lane's item: gq + 8 kq
+        Fl[0] = F.lo;
+    } else {
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+            // fractional offset of this m-tile's item, from the lane that set it up
+            const double fxq = __shfl_sync(0xffffffffu, fxo, gq + 8 * t);
+            const double fyq = __shfl_sync(0xffffffffu, fyo, gq + 8 * t);
+            double Rh[RowCfg<DEG>::QMAX], Rl[RowCfg<DEG>::QMAX];
+            fused_rows<DEG, NT>(C[t], fyq, kq, Rh, Rl);
+            double ah, al;
+            fused_xhorner<DEG, DEG>(Rh, Rl, fxq, ah, al);
+            const dd F = fast_two_sum(ah, al);
+            Fh[t] = F.hi;
+            Fl[t] = F.lo;
+        }
     }
 }
 
@@ -1005,12 +1049,19 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);
                     else
                         fused_group<3 * R - 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);
-#pragma unroll
-                    for (int q = 0; q < MT; ++q) {  // item lane/4 + 8q's result, from its quad's lane 0
-                        const int src = (lane >> 2) + 8 * q;
+                    if constexpr (MT == 4 && R < 3) {  // lane (g, k) holds item g + 8k's result
+                        const int src = (lane >> 2) + 8 * (lane & 3);
                         const int iq = __shfl_sync(0xffffffffu, idx, src);
                         const bool rq = __shfl_sync(0xffffffffu, (int)real, src) != 0;
-                        if ((lane & 3) == 0 && rq) s_F[iq] = make_double2(Fh[q], Fl[q]);
+                        if (rq) s_F[iq] = make_double2(Fh[0], Fl[0]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < MT; ++q) {  // item lane/4 + 8q's result, from its quad's lane 0
+                            const int src = (lane >> 2) + 8 * q;
+                            const int iq = __shfl_sync(0xffffffffu, idx, src);
+                            const bool rq = __shfl_sync(0xffffffffu, (int)real, src) != 0;
+                            if ((lane & 3) == 0 && rq) s_F[iq] = make_double2(Fh[q], Fl[q]);
+                        }
                     }
                     if (a.prof && lane == 0) {
                         const unsigned long long dt = clock64() - tq0;
