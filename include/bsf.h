@@ -174,6 +174,22 @@ bsf_status bsf_run_points(bsf_plan_t plan, const void *f_dev, const void *cov_de
  * global g).                                                                 */
 bsf_status bsf_run(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, void *stream);
 
+/* Algorithm 1 ("better accuracy"): covariance splitting
+ * C = sigma_b^2 I + Delta C (Eq. (7)).  Per covariance field b,
+ * sigma_b^2 is half the bound (9), minimised over the
+ * field's pixels (R21); then
+ *   pass 1: the isotropic box spline of covariance sigma_b^2 I (a_k =
+ *           sqrt(6) sigma_b) on f, a global O(1) convolution;
+ *   pass 2: the space-variant box spline of covariance C(p) - sigma_b^2 I on
+ *           the pass-1 image (kept in float64).
+ * Both passes use the plan's order and basis policy and the exact split path
+ * (BSF_EUNSUPPORTED for order 4).  f_dev, cov_dev, out_dev as bsf_run.
+ * sigma2_out: NULL, or host double[batch] receiving sigma_b^2 (synchronises
+ * the stream).  The plan owns a float64 [batch*channels][H][W] work image.
+ * Statistics count both passes.                                              */
+bsf_status bsf_run_alg1(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, double *sigma2_out,
+                        void *stream);
+
 /* End to end from HOST buffers (pinned for overlap): copies f and cov to the
  * device, runs bsf_run, copies out back, all on `stream`.  Returns after
  * enqueueing; synchronise the stream before reading out_host.               */

@@ -78,6 +78,8 @@ def lib():
         L.bsf_run_points.argtypes = [vp, vp, vp, vp, i, vp, vp, vp]
         L.bsf_run.restype = st
         L.bsf_run.argtypes = [vp, vp, vp, vp, vp]
+        L.bsf_run_alg1.restype = st
+        L.bsf_run_alg1.argtypes = [vp, vp, vp, vp, vp, vp]
         L.bsf_run_host.restype = st
         L.bsf_run_host.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_get_stats.restype = st
@@ -183,6 +185,14 @@ class Plan:
 
     def run(self, f, cov, out, stream=None):
         _check(lib().bsf_run(self.handle, _ptr(f), _ptr(cov), _ptr(out), _stream(stream)))
+
+    def run_alg1(self, f, cov, out, stream=None):
+        """Algorithm 1 (covariance splitting); returns sigma_b^2 per covariance field."""
+        import numpy as np
+        sig = np.zeros(self.desc.batch, dtype=np.float64)
+        _check(lib().bsf_run_alg1(self.handle, _ptr(f), _ptr(cov), _ptr(out),
+                                  sig.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
+        return sig
 
     def run_host(self, f_host, cov_host, out_host, stream=None):
         _check(lib().bsf_run_host(self.handle, _ptr(f_host), _ptr(cov_host), _ptr(out_host), _stream(stream)))

@@ -44,6 +44,8 @@ struct bsf_plan_s {
     bool fused = false;
     unsigned long long *prof = nullptr;  // phase cycles of the fused kernel (diagnostics)
     double2 *fbuf = nullptr;             // fused path: per-CTA tap values
+    double *alg1_work = nullptr;         // Algorithm 1: float64 intermediate image
+    double *alg1_sigma2 = nullptr;       // Algorithm 1: sigma_b^2 per covariance field (+ reduction bits)
     int *tile_counter = nullptr;
     long long nlaunch = 0;
     cudaStream_t last = nullptr;
@@ -560,6 +562,48 @@ extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void
     bsf_status s = bsf_preintegrate(p, f, p->g_ws, stream);
     if (s != BSF_OK) return s;
     return bsf_filter(p, p->g_ws, cov, out, stream);
+}
+
+extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov, void *out, double *sigma2_out,
+                                   void *stream) {
+    if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    bsf_status s = ensure_tile_ws(p);
+    if (s != BSF_OK) return s;
+    if (!p->fused) return set_err(BSF_EUNSUPPORTED, "Algorithm 1 runs on the exact split path (order <= 3)");
+    const Geometry &g = p->geo;
+    if (!p->alg1_work) {
+        void *q;
+        if (cudaMalloc(&q, (size_t)g.nimg * g.H * g.W * sizeof(double)) != cudaSuccess)
+            return set_err(BSF_ENOMEM, "Algorithm 1 work image");
+        p->dev_allocs.push_back(q);
+        p->alg1_work = (double *)q;
+        if (cudaMalloc(&q, 2 * (size_t)p->d.batch * sizeof(double)) != cudaSuccess)
+            return set_err(BSF_ENOMEM, "Algorithm 1 sigma");
+        p->dev_allocs.push_back(q);
+        p->alg1_sigma2 = (double *)q;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last = st;
+    CUDA_TRY(launch_alg1_sigma2((const float *)cov, p->d.batch, g.W, g.H, p->d.basis, p->d.clamp, p->alg1_sigma2, st,
+                                &p->nlaunch));
+    // pass 1: the isotropic box spline of covariance sigma_b^2 I, into the work image
+    TileArgs a1 = tile_args(p, f, cov, p->alg1_work);
+    a1.out_f32 = 0;
+    a1.cov_mode = COV_ISO;
+    a1.sigma2 = p->alg1_sigma2;
+    CUDA_TRY(launch_tile(p, a1, st));
+    // pass 2: the space-variant box spline of covariance C - sigma_b^2 I on it
+    TileArgs a2 = tile_args(p, p->alg1_work, cov, out);
+    a2.in_u8 = 0;
+    a2.in_f64 = 1;
+    a2.cov_mode = COV_SUB;
+    a2.sigma2 = p->alg1_sigma2;
+    CUDA_TRY(launch_tile(p, a2, st));
+    if (sigma2_out) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        CUDA_TRY(cudaMemcpy(sigma2_out, p->alg1_sigma2, p->d.batch * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    return BSF_OK;
 }
 
 extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void *cov_host, void *out_host,

@@ -161,6 +161,35 @@ __device__ __forceinline__ int cls_region(const ClsTables &T, int b, double x, d
     return 0;
 }
 
+// (sigma_x, sigma_y, theta) of a pixel under the covariance mode of the launch
+// (Algorithm 1): the planes, sigma_b^2 I (the global
+// isotropic pass, theta = 0), or C - sigma_b^2 I (same eigenvectors, eigenvalues
+// lowered by sigma_b^2: PAPER.md:228-231)
+__device__ __forceinline__ void load_cov(const TileArgs &a, int img, int x, int y, double &sx, double &sy,
+                                         double &th) {
+    const size_t ipl = (size_t)a.H * a.W;
+    const int b = img / a.channels;
+    if (a.cov_mode == COV_ISO) {
+        sx = sy = sqrt(a.sigma2[b]);
+        th = 0.0;
+        return;
+    }
+    const float *cv = a.cov + (size_t)b * 3 * ipl + (size_t)y * a.W + x;
+    sx = __ldg(cv);
+    sy = __ldg(cv + ipl);
+    th = __ldg(cv + 2 * ipl);
+    if (a.cov_mode == COV_SUB) {
+        const double s2 = a.sigma2[b];
+        sx = sqrt(fmax(sx * sx - s2, 0.0));
+        sy = sqrt(fmax(sy * sy - s2, 0.0));
+    }
+}
+
+__device__ __forceinline__ double load_f(const TileArgs &a, size_t o) {
+    if (a.in_f64) return ((const double *)a.f)[o];
+    return a.in_u8 ? (double)((const uint8_t *)a.f)[o] : (double)((const float *)a.f)[o];
+}
+
 // displacement of tap t from the per-pixel geometry (see the sub-tile scales):
 // identical to fused_tap's value, with 4 FMAs per coordinate
 template <int R>
@@ -553,7 +582,7 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
         const int X = X0 + x, Y = Y0 + y;
         if (X < 0 || X >= a.W || Y < 0 || Y >= a.H) return 0.0;
         const size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
-        return a.in_u8 ? (double)((const uint8_t *)a.f)[o] : (double)((const float *)a.f)[o];
+        return load_f(a, o);
     };
     if (nh) {
         for (int y = tid; y < NY; y += FT) {
@@ -701,14 +730,32 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             Y0s = (rem / nstx) * STILE;
         }
 
+        if (a.cov_mode == COV_ISO && !(a.sigma2[img / a.channels] > 0.0)) {
+            // Algorithm 1 with sigma_b = 0: the isotropic pass is the identity
+            for (int q = 0; q < 4; ++q) {
+                const int x = X0s + TILE * (q & 1) + (tid % TILE), y = Y0s + TILE * (q >> 1) + tid / TILE;
+                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H);
+                if (mine) {
+                    const double v = load_f(a, (size_t)img * ipl + (size_t)y * a.W + x);
+                    const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
+                    if (a.out_f32 && !a.pts)
+                        ((float *)a.out)[oidx] = (float)v;
+                    else
+                        ((double *)a.out)[oidx] = v;
+                }
+            }
+            __syncthreads();
+            continue;
+        }
         // ---- 1. reach of every pixel of the super-tile (a1-a4) -------------------
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {
             const int x = X0s + TILE * (q & 1) + (tid % TILE), y = Y0s + TILE * (q >> 1) + tid / TILE;
             if (x < a.W && y < a.H) {
                 PixelScales ps;
-                const float *cv = a.cov + (size_t)(img / a.channels) * 3 * ipl + (size_t)y * a.W + x;
-                pixel_scales(__ldg(cv), __ldg(cv + ipl), __ldg(cv + 2 * ipl), a.policy, a.clamp, R, ps);
+                double sx, sy, th;
+                load_cov(a, img, x, y, sx, sy, th);
+                pixel_scales(sx, sy, th, a.policy, a.clamp, R, ps);
                 if (!(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO))) {
                     double ex = 0.0, ey = 0.0;
                     for (int k = 0; k < 4; ++k) {
@@ -784,7 +831,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     double v = 0.0;
                     if (X >= 0 && X < a.W && Y >= 0 && Y < a.H) {
                         const size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
-                        v = a.in_u8 ? (double)((const uint8_t *)a.f)[o] : (double)((const float *)a.f)[o];
+                        v = load_f(a, o);
                     }
                     G[i] = make_double2(v, 0.0);
                 }
@@ -868,8 +915,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             ps.ap[0] = ps.ap[1] = ps.ap[2] = ps.ap[3] = 0.0;
             const bool valid = x < a.W && y < a.H;
             if (valid) {
-                const float *cv = a.cov + (size_t)(img / a.channels) * 3 * ipl + (size_t)y * a.W + x;
-                pixel_scales(__ldg(cv), __ldg(cv + ipl), __ldg(cv + 2 * ipl), a.policy, a.clamp, R, ps);
+                double sx, sy, th;
+                load_cov(a, img, x, y, sx, sy, th);
+                pixel_scales(sx, sy, th, a.policy, a.clamp, R, ps);
             }
             const bool live = valid && !(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
             s_info[tid] = ps.basis | ((ps.drop + 1) << 1) | (live ? 16 : 0) | (ps.clamped ? 32 : 0) | (ps.flags << 8);
@@ -1220,6 +1268,67 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             s_stats[tid] = 0ull;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Algorithm 1 step 1 (Eq. (9) at PAPER.md:276-280): per
+// covariance field b, sigma_b^2 = 1/2 min_p of the bound (9),
+//   1/2 (C11 + C22 - (1/e_B(phi)) sqrt((C11 - C22)^2 + 4 C12^2)),
+// e_B the elongation bound (as (rho-1)/(rho+1)) of the basis the pixel uses,
+// C the (clamped) covariance the pixel is filtered with (R21).
+// ---------------------------------------------------------------------------
+__global__ void alg1_bound_kernel(const float *__restrict__ cov, int W, int H, int policy, int clamp,
+                                  unsigned long long *__restrict__ minbits) {
+    const size_t ipl = (size_t)H * W;
+    const int b = blockIdx.y;
+    double m = INFINITY;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < ipl; i += (size_t)gridDim.x * blockDim.x) {
+        const float *cv = cov + (size_t)b * 3 * ipl + i;
+        double sx = cv[0], sy = cv[ipl], th = cv[2 * ipl];
+        double phi = th, maj = sx, mn = sy;
+        if (sx < sy) {
+            phi = th + M_PI / 2;
+            maj = sy;
+            mn = sx;
+        }
+        phi = fmod(phi, M_PI);
+        if (phi < 0) phi += M_PI;
+        double eT, eP;
+        bounds_e(phi, &eT, &eP);
+        int basis = policy;
+        if (policy == BASIS_DUAL) basis = (sx == sy) ? BASIS_THETA : (eP > eT ? BASIS_THETA_PRIME : BASIS_THETA);
+        const double eb = basis == BASIS_THETA ? eT : eP;
+        double l1 = maj * maj, l2 = mn * mn;
+        if (clamp && eb < 1.0 && sx != sy) {  // the clamp of pixel_scales (R9)
+            const double rb = (1.0 + eb) / (1.0 - eb), rho = l1 / l2;
+            if (rho > 0.95 * rb) {
+                const double lim = 0.95 * rb, T = l1 + l2, e = (lim - 1.0) / (lim + 1.0);
+                l1 = 0.5 * T * (1.0 + e);
+                l2 = 0.5 * T * (1.0 - e);
+            }
+        }
+        const double bound = 0.5 * (l1 + l2 - (l1 - l2) / fmin(eb, 1.0));
+        m = fmin(m, bound);
+    }
+    for (int o = 16; o; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMin(minbits + b, (unsigned long long)__double_as_longlong(fmax(m, 0.0)));
+}
+
+__global__ void alg1_finish_kernel(const unsigned long long *__restrict__ minbits, int batch, double *sigma2) {
+    const int b = threadIdx.x;
+    if (b < batch) sigma2[b] = 0.5 * __longlong_as_double((long long)minbits[b]);  // half the bound
+}
+
+cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int policy, int clamp, double *sigma2,
+                               cudaStream_t st, long long *nl) {
+    // sigma2 holds 2 * batch doubles: [0, batch) results, [batch, 2 batch) min bits
+    unsigned long long *bits = reinterpret_cast<unsigned long long *>(sigma2 + batch);
+    cudaMemsetAsync(bits, 0x7f, batch * sizeof(unsigned long long), st);  // a large positive double
+    const int blocks = (int)((size_t)H * W / 256 + 1 < 1184 ? (size_t)H * W / 256 + 1 : 1184);
+    alg1_bound_kernel<<<dim3(blocks, batch), 256, 0, st>>>(cov, W, H, policy, clamp, bits);
+    alg1_finish_kernel<<<1, 1024, 0, st>>>(bits, batch, sigma2);
+    *nl += 2;
+    return cudaGetLastError();
 }
 
 template <int R>

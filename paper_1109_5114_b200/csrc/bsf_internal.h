@@ -144,6 +144,9 @@ struct GatherArgs {
 struct TileArgs {
     int W, H, nimg, channels;
     int policy, clamp, out_f32, in_u8;
+    int in_f64;             // input image is float64 (Algorithm 1's second pass)
+    int cov_mode;           // COV_PLANES, COV_ISO (sigma_b^2 I), COV_SUB (C - sigma_b^2 I)
+    const double *sigma2;   // [batch] sigma_b^2 of Algorithm 1 (COV_ISO / COV_SUB)
     const void *f;          // [nimg][H][W]
     const float *cov;       // [batch][3][H][W]
     void *out;              // [nimg][H][W] (or float64[npts] with pts)
@@ -160,6 +163,9 @@ struct TileArgs {
     double2 *fbuf;             // fused path: per-CTA tap values [slots][fused_items<R>()]
 };
 constexpr int TILE = 16;
+enum { COV_PLANES = 0, COV_ISO = 1, COV_SUB = 2 };
+cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int policy, int clamp, double *sigma2,
+                               cudaStream_t st, long long *nlaunch);
 size_t tile_capacity(int order, float max_sigma, const LutBasis *host_luts, int basis_mask, int tile);
 int tile_slots();
 cudaError_t launch_tile_impl(const TileArgs &a, int order, int precision, int slots, cudaStream_t st,

@@ -134,9 +134,8 @@ __device__ __forceinline__ int solve_scales(int basis, double C11, double C12, d
 }
 
 // Steps a1-a4: sigma_x, sigma_y, theta -> basis, a'_k, zero-direction.
-__device__ __forceinline__ void pixel_scales(float sxf, float syf, float thf, int policy, int clamp, int order,
+__device__ __forceinline__ void pixel_scales(double sx, double sy, double th, int policy, int clamp, int order,
                                              PixelScales &ps) {
-    double sx = sxf, sy = syf, th = thf;
     ps.flags = 0;
     ps.clamped = 0;
     ps.drop = -1;

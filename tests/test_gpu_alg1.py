@@ -1,0 +1,124 @@
+"""Algorithm 1 (covariance splitting) through bsf_run_alg1
+against a two-stage oracle: the oracle's direct-sum filter applied with the
+isotropic covariance sigma_b^2 I to every pixel, then with C - sigma_b^2 I to
+that float64 image (Proposition 2: the composition is one
+space-variant filter)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from paper_1109_5114_b200 import bsf
+from gpu_util import make_plan, max_rel
+from test_gpu_parity import _small_smooth
+
+pytestmark = pytest.mark.gpu
+
+
+def _bound9(cov, policy, clamp=1):
+    """Eq. (9) per pixel with the basis each pixel uses and
+    the clamped covariance (R21); e(phi) as rho_B."""
+    sx, sy, th = (cov[i].astype(np.float64) for i in range(3))
+    swap = sx < sy
+    phi = np.where(swap, th + math.pi / 2, th) % math.pi
+    l1 = np.maximum(sx, sy) ** 2
+    l2 = np.minimum(sx, sy) ** 2
+    s2, c2 = np.abs(np.sin(2 * phi)), np.abs(np.cos(2 * phi))
+    eT = 1.0 / (s2 + c2)
+    with np.errstate(divide="ignore"):
+        eP = np.minimum(np.where(c2 > 0, 0.6 / c2, np.inf), np.where(s2 > 0, 0.8 / s2, np.inf))
+    if policy == 2:
+        theta_prime = (sx != sy) & (eP > eT)
+    else:
+        theta_prime = np.full(sx.shape, policy == 1)
+    eb = np.where(theta_prime, eP, eT)
+    rb = np.where(eb < 1, (1 + eb) / np.maximum(1 - eb, 1e-300), np.inf)
+    rho = l1 / l2
+    cl = clamp & (eb < 1) & (sx != sy) & (rho > 0.95 * rb)
+    T = l1 + l2
+    lim = 0.95 * rb
+    with np.errstate(invalid="ignore"):
+        e = np.where(cl, (lim - 1) / (lim + 1), 0.0)
+    l1 = np.where(cl, 0.5 * T * (1 + e), l1)
+    l2 = np.where(cl, 0.5 * T * (1 - e), l2)
+    return 0.5 * (l1 + l2 - (l1 - l2) / np.minimum(eb, 1.0))
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2])
+@pytest.mark.parametrize("r", [1, 2])
+def test_alg1_matches_two_stage_oracle(policy, r):
+    H, W = 34, 40
+    w, img, cov = _small_smooth(H, W, 3.5, seed=21)
+    plan = make_plan(w, policy=policy, order=r, anchor=bsf.BSF_ANCHOR_TILE)
+    out = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    sig = plan.run_alg1(img[None].cuda().contiguous(), cov.cuda().contiguous(), out)
+    torch.cuda.synchronize()
+    c = cov.numpy()
+    # sigma_b^2 = half the smallest bound (9) over the field
+    s2 = 0.5 * float(_bound9(c, policy).min())
+    assert abs(sig[0] - s2) <= 1e-12 * s2, (sig[0], s2)
+    s = math.sqrt(sig[0])
+    ys, xs = np.mgrid[0:H, 0:W]
+    xs, ys = xs.ravel(), ys.ravel()
+    g, *_ = O.filter_points(img.numpy(), xs, ys, s, s, 0.0, policy=policy, r=r)
+    g = g.reshape(H, W)
+    sx = np.sqrt(np.maximum(c[0].astype(np.float64) ** 2 - sig[0], 0.0))[ys, xs]
+    sy = np.sqrt(np.maximum(c[1].astype(np.float64) ** 2 - sig[0], 0.0))[ys, xs]
+    ref, *_ = O.filter_points(g, xs, ys, sx, sy, c[2][ys, xs].astype(np.float64), policy=policy, r=r)
+    got = out[0].cpu().numpy().ravel()
+    assert max_rel(got, ref) <= 1e-9
+    assert plan.stats()["flags"] == 0
+
+
+def test_alg1_batch_sigma_per_field():
+    """One sigma_b per covariance field of a batch (channels share it)."""
+    w = synth.workload(1, width=36, height=30, batch=2, channels=2)
+    imgs = torch.stack([synth.make_image(w, frame=b, channel=c) for b in range(2) for c in range(2)])
+    covs = torch.stack([synth.make_cov(w) for _ in range(2)])
+    covs[1, 0] *= 2.0
+    covs[1, 1] *= 1.5
+    plan = make_plan(w, anchor=bsf.BSF_ANCHOR_TILE)
+    out = torch.empty((4, 30, 36), dtype=torch.float64, device="cuda")
+    sig = plan.run_alg1(imgs.cuda().contiguous(), covs.cuda().contiguous(), out)
+    torch.cuda.synchronize()
+    for b in range(2):
+        s2 = 0.5 * float(_bound9(covs[b].numpy(), 2).min())
+        assert abs(sig[b] - s2) <= 1e-12 * s2
+    assert sig[1] > sig[0]
+    assert torch.isfinite(out).all()
+
+
+@pytest.mark.parametrize("policy", [0, 2])
+def test_alg1_closer_to_the_gaussian(policy):
+    """The paper's claim (Table 2): splitting the covariance
+    improves the Gaussian approximation.  Impulse response of the plain order-1
+    filter and of Algorithm 1 (same target covariance C, constant field) vs the
+    sampled Gaussian of covariance C: Algorithm 1 has the smaller L2 error."""
+    H = W = 49
+    w = synth.workload(2, width=W, height=H, max_sigma=6.0)
+    img = torch.zeros((H, W), dtype=torch.float32)
+    img[H // 2, W // 2] = 1.0
+    smaj, rho, th = 4.5, 2.0, math.radians(30.0)
+    cov = torch.tensor([smaj, smaj / math.sqrt(rho), th], dtype=torch.float32)[:, None, None].expand(3, H, W)
+    cov = cov.contiguous()
+    plan = make_plan(w, policy=policy, order=1, anchor=bsf.BSF_ANCHOR_TILE)
+    plain = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    plan.run(img[None].cuda(), cov.cuda(), plain)
+    alg1 = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    plan.run_alg1(img[None].cuda(), cov.cuda(), alg1)
+    torch.cuda.synchronize()
+    # sampled Gaussian of covariance C = R diag(sx^2, sy^2) R^T (impulse response)
+    sx, sy = smaj, smaj / math.sqrt(rho)
+    c, s = math.cos(th), math.sin(th)
+    C = np.array([[sx * sx * c * c + sy * sy * s * s, (sx * sx - sy * sy) * s * c],
+                  [(sx * sx - sy * sy) * s * c, sx * sx * s * s + sy * sy * c * c]])
+    Ci = np.linalg.inv(C)
+    yy, xx = np.mgrid[0:H, 0:W]
+    d = np.stack([xx - W // 2, yy - H // 2], -1).astype(np.float64)
+    gauss = np.exp(-0.5 * np.einsum("...i,ij,...j->...", d, Ci, d)) / (2 * math.pi * math.sqrt(np.linalg.det(C)))
+    err = lambda k: float(np.linalg.norm(k - gauss) / np.linalg.norm(gauss))
+    e_plain, e_alg1 = err(plain[0].cpu().numpy()), err(alg1[0].cpu().numpy())
+    assert e_alg1 < 0.75 * e_plain, (e_plain, e_alg1)
