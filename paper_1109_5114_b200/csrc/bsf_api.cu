@@ -32,8 +32,6 @@ struct bsf_plan_s {
     int bases[2];           // basis of each running-sum slot
     std::vector<void *> dev_allocs;
     LutBasis *luts_dev = nullptr;  // [2], indexed by basis id
-    void *scan_ws = nullptr;
-    size_t scan_ws_bytes = 0;
     double2 *g_ws = nullptr;       // for bsf_run
     void *f_stage = nullptr, *cov_stage = nullptr, *out_stage = nullptr;
     unsigned long long *stats = nullptr;
@@ -349,9 +347,7 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
         bsf_plan_destroy(p);
         return set_err(BSF_ENOMEM, "table upload failed");
     }
-    p->scan_ws_bytes = scan_workspace_bytes(g);
-    if (dmalloc(&p->scan_ws, p->scan_ws_bytes) != cudaSuccess ||
-        dmalloc((void **)&p->stats, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+    if (dmalloc((void **)&p->stats, 8 * sizeof(unsigned long long)) != cudaSuccess) {
         bsf_plan_destroy(p);
         return set_err(BSF_ENOMEM, "workspace allocation failed");
     }
@@ -384,11 +380,10 @@ extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, voi
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
     double2 *gd = (double2 *)g;
-    CUDA_TRY(launch_fill_dd(f, p->d.in_dtype == BSF_U8, gd, p->geo, p->geo.nbases, st, &p->nlaunch));
     size_t slot = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW;
     for (int s = 0; s < p->geo.nbases; ++s)
-        CUDA_TRY(launch_scan_dd(gd + s * slot, p->geo, p->bases[s], p->d.order, p->scan_ws, p->scan_ws_bytes, st,
-                                &p->nlaunch));
+        CUDA_TRY(launch_preint_dd(f, p->d.in_dtype == BSF_U8, gd + s * slot, p->geo, p->bases[s], p->d.order, st,
+                                  &p->nlaunch));
     return BSF_OK;
 }
 
@@ -398,11 +393,10 @@ extern "C" bsf_status bsf_preintegrate_exact(bsf_plan_t p, const void *f, void *
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
     unsigned long long *gd = (unsigned long long *)g;
-    CUDA_TRY(launch_fill_i64((const uint8_t *)f, gd, p->geo, p->geo.nbases, st, &p->nlaunch));
     size_t slot = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW;
     for (int s = 0; s < p->geo.nbases; ++s)
-        CUDA_TRY(launch_scan_i64(gd + s * slot, p->geo, p->bases[s], p->d.order, p->scan_ws, p->scan_ws_bytes, st,
-                                 &p->nlaunch));
+        CUDA_TRY(launch_preint_i64((const uint8_t *)f, gd + s * slot, p->geo, p->bases[s], p->d.order, st,
+                                   &p->nlaunch));
     return BSF_OK;
 }
 

@@ -33,11 +33,14 @@ constexpr uint16_t NOKEY = 0xFFFF;
 #ifndef BSF_MT1
 #define BSF_MT1 4
 #endif
+#ifndef BSF_MT3
+#define BSF_MT3 2
+#endif
 template <int R> struct FusedCfg;
 // NTAP taps per pixel, P pixels per chunk, MT 8-item m-tiles per group
 template <> struct FusedCfg<1> { static constexpr int NTAP = 16, P = 256, MT = BSF_MT1; };
 template <> struct FusedCfg<2> { static constexpr int NTAP = 81, P = 256, MT = 4; };
-template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 64, MT = 1; };
+template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 64, MT = BSF_MT3; };
 template <> struct FusedCfg<4> { static constexpr int NTAP = 625, P = 16, MT = 1; };
 
 // per-tap interpolated values F (double-double) live in a per-CTA global
@@ -461,16 +464,22 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
 // conditioning of r = 3 needs it).  With split numerators (NSPLIT 2) the two
 // exact limbs each meet n1 and n0.  The N dimension is taken in passes of NP
 // n-tiles (bounded registers); the lock-step row Horner resumes across passes.
-template <int DEG, int NSPLIT, int NP>
-__device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, int NX, int NY, int bx, int by,
-                                               double fxo, double fyo, const int2 *__restrict__ offs,
-                                               const double *__restrict__ numA, const double *__restrict__ numB,
-                                               const double *__restrict__ numF, int nmonp, int n4, int shift,
-                                               double sc_e, int kbits, double &Fh, double &Fl, int &flags) {
+template <int DEG, int NSPLIT, int NP, int MT>
+__device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
+                                               const int (&byt)[MT], double fxo, double fyo,
+                                               const int2 *__restrict__ offs, const double *__restrict__ numA,
+                                               const double *__restrict__ numB, const double *__restrict__ numF,
+                                               int nmonp, int n4, int shift, double sc_e, int kbits,
+                                               double (&Fh)[MT], double (&Fl)[MT], int &flags) {
     constexpr int NT = DegCfg<DEG>::NT, NL = NSPLIT == 1 ? 3 : 5, QMAX = RowCfg<DEG>::QMAX;
     const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
-    // this lane's item (gq) fractional offset, from the lane that set it up
-    const double fx = __shfl_sync(0xffffffffu, fxo, gq), fy = __shfl_sync(0xffffffffu, fyo, gq);
+    // fractional offsets of this lane's items (gq + 8t), from the lanes that set them up
+    double fxt[MT], fyt[MT];
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+        fxt[t] = __shfl_sync(0xffffffffu, fxo, gq + 8 * t);
+        fyt[t] = __shfl_sync(0xffffffffu, fyo, gq + 8 * t);
+    }
     const double S = ldexp(1.0, kbits), iS = ldexp(1.0, -kbits), ssh = ldexp(1.0, shift);
     const unsigned smask = kq == 0 ? bsf_start_mask(DEG, 0)
                            : kq == 1 ? bsf_start_mask(DEG, 1)
@@ -478,54 +487,70 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
     const unsigned vmask = kq == 0 ? bsf_valid_mask(DEG, 0)
                            : kq == 1 ? bsf_valid_mask(DEG, 1)
                            : kq == 2 ? bsf_valid_mask(DEG, 2) : bsf_valid_mask(DEG, 3);
-    double Rh[QMAX], Rl[QMAX];
+    double Rh[MT][QMAX], Rl[MT][QMAX], rh[MT], rl[MT];
+    int q = -1;  // the row counter is the same for every m-tile (same lane, same slots)
 #pragma unroll
-    for (int q = 0; q < QMAX; ++q) Rh[q] = Rl[q] = 0.0;
-    double rh = 0.0, rl = 0.0;
-    int q = -1;
+    for (int t = 0; t < MT; ++t) {
+        rh[t] = rl[t] = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < QMAX; ++qq) Rh[t][qq] = Rl[t][qq] = 0.0;
+    }
     for (int j0 = 0; j0 < NT; j0 += NP) {
-        double C[NL][NP][2];
+        double C[MT][NL][NP][2];
 #pragma unroll
-        for (int L = 0; L < NL; ++L)
+        for (int t = 0; t < MT; ++t)
 #pragma unroll
-            for (int j = 0; j < NP; ++j) C[L][j][0] = C[L][j][1] = 0.0;
+            for (int L = 0; L < NL; ++L)
+#pragma unroll
+                for (int j = 0; j < NP; ++j) C[t][L][j][0] = C[t][L][j][1] = 0.0;
         for (int s0 = 0; s0 < n4; s0 += 4) {
             const int s = s0 + kq;
             const int2 d = __ldg(offs + s);
-            const int lx = bx + d.x, ly = by + d.y;
+            double g1[MT], g2[MT], g0[MT];
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+                const int lx = bxt[t] + d.x, ly = byt[t] + d.y;
 #ifdef BSF_CHECK_RANGE
-            const bool inside = lx >= 0 && lx < NX && ly >= 0 && ly < NY;
-            flags |= (ly >= 0 && !inside) ? FLAG_RANGE : 0;
+                const bool inside = lx >= 0 && lx < NX && ly >= 0 && ly < NY;
+                flags |= (ly >= 0 && !inside) ? FLAG_RANGE : 0;
 #else
-            const bool inside = true;  // fused_domain covers every window read
+                const bool inside = true;  // fused_domain covers every window read
 #endif
-            const double2 g = G[inside ? (size_t)ly * NX + lx : 0];
-            double g1 = 0.0, g2 = 0.0, g0 = 0.0;
-            if (inside) {
-                const double h = g.x * sc_e;  // exact (power of two)
-                g1 = rint(h);
-                const double r = (h - g1) * S;  // exact: |h - g1| <= 1/2
-                g2 = rint(r);
-                g0 = (r - g2) + g.y * sc_e * S;
+                const double2 g = G[inside ? (size_t)ly * NX + lx : 0];
+                g1[t] = g2[t] = g0[t] = 0.0;
+                if (inside) {
+                    const double h = g.x * sc_e;  // exact (power of two)
+                    g1[t] = rint(h);
+                    const double r = (h - g1[t]) * S;  // exact: |h - g1| <= 1/2
+                    g2[t] = rint(r);
+                    g0[t] = (r - g2[t]) + g.y * sc_e * S;
+                }
             }
             const size_t o = (size_t)s * nmonp + gq + 8 * j0;
 #pragma unroll
             for (int j = 0; j < NP; ++j) {
                 if (j0 + j >= NT) break;
                 const double bA = __ldg(numA + o + 8 * j);
-                dmma(C[0][j], g1, bA);  // exact
-                dmma(C[1][j], g2, bA);  // exact
-                if constexpr (NSPLIT == 1) {
-                    dmma(C[2][j], g0, bA);
-                } else {
-                    const double bB = __ldg(numB + o + 8 * j), bF = __ldg(numF + o + 8 * j);
-                    dmma(C[2][j], g0, bF);
-                    dmma(C[3][j], g1, bB);  // exact
-                    dmma(C[4][j], g2, bB);  // exact
+                double bB = 0.0, bF = 0.0;
+                if constexpr (NSPLIT == 2) {
+                    bB = __ldg(numB + o + 8 * j);
+                    bF = __ldg(numF + o + 8 * j);
+                }
+#pragma unroll
+                for (int t = 0; t < MT; ++t) {
+                    dmma(C[t][0][j], g1[t], bA);  // exact
+                    dmma(C[t][1][j], g2[t], bA);  // exact
+                    if constexpr (NSPLIT == 1) {
+                        dmma(C[t][2][j], g0[t], bA);
+                    } else {
+                        dmma(C[t][2][j], g0[t], bF);
+                        dmma(C[t][3][j], g1[t], bB);  // exact
+                        dmma(C[t][4][j], g2[t], bB);  // exact
+                    }
                 }
             }
         }
-        // rows over this pass's slots (lock step, as fused_rows)
+        // rows over this pass's slots (lock step, as fused_rows), every m-tile
 #pragma unroll
         for (int j = 0; j < NP; ++j) {
             if (j0 + j >= NT) break;
@@ -533,41 +558,47 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
             for (int h2 = 0; h2 < 2; ++h2) {
                 const int k = 2 * (j0 + j) + h2;
                 const bool start = (smask >> k) & 1, valid = (vmask >> k) & 1;
-                dd e;
-                if constexpr (NSPLIT == 1) {
-                    e = dd_add_d(two_sum(C[0][j][h2], C[1][j][h2] * iS), C[2][j][h2] * iS);
-                } else {
-                    const dd x = two_sum(C[0][j][h2] * ssh, C[3][j][h2]);
-                    const dd y = two_sum(C[1][j][h2] * ssh, C[4][j][h2]);
-                    e = dd_add_d(dd_add(x, {y.hi * iS, y.lo * iS}), C[2][j][h2] * iS);
-                }
-                double nh = rh, nl = rl;
-                comp_step(nh, nl, fy, e.hi, e.lo);
-                if (start) {
 #pragma unroll
-                    for (int qq = 0; qq < QMAX; ++qq)
-                        if (qq == q) {
-                            Rh[qq] = rh;
-                            Rl[qq] = rl;
-                        }
-                    ++q;
+                for (int t = 0; t < MT; ++t) {
+                    dd e;
+                    if constexpr (NSPLIT == 1) {
+                        e = dd_add_d(two_sum(C[t][0][j][h2], C[t][1][j][h2] * iS), C[t][2][j][h2] * iS);
+                    } else {
+                        const dd x = two_sum(C[t][0][j][h2] * ssh, C[t][3][j][h2]);
+                        const dd y = two_sum(C[t][1][j][h2] * ssh, C[t][4][j][h2]);
+                        e = dd_add_d(dd_add(x, {y.hi * iS, y.lo * iS}), C[t][2][j][h2] * iS);
+                    }
+                    double nh = rh[t], nl = rl[t];
+                    comp_step(nh, nl, fyt[t], e.hi, e.lo);
+                    if (start) {
+#pragma unroll
+                        for (int qq = 0; qq < QMAX; ++qq)
+                            if (qq == q) {
+                                Rh[t][qq] = rh[t];
+                                Rl[t][qq] = rl[t];
+                            }
+                    }
+                    rh[t] = start ? e.hi : (valid ? nh : rh[t]);
+                    rl[t] = start ? e.lo : (valid ? nl : rl[t]);
                 }
-                rh = start ? e.hi : (valid ? nh : rh);
-                rl = start ? e.lo : (valid ? nl : rl);
+                if (start) ++q;
             }
         }
     }
 #pragma unroll
-    for (int qq = 0; qq < QMAX; ++qq)
-        if (qq == q) {
-            Rh[qq] = rh;
-            Rl[qq] = rl;
-        }
-    double ah, al;
-    fused_xhorner<DEG, DEG>(Rh, Rl, fx, ah, al);
-    const dd F = fast_two_sum(ah, al);
-    Fh = F.hi;
-    Fl = F.lo;
+    for (int t = 0; t < MT; ++t) {
+#pragma unroll
+        for (int qq = 0; qq < QMAX; ++qq)
+            if (qq == q) {
+                Rh[t][qq] = rh[t];
+                Rl[t][qq] = rl[t];
+            }
+        double ah, al;
+        fused_xhorner<DEG, DEG>(Rh[t], Rl[t], fxt[t], ah, al);
+        const dd F = fast_two_sum(ah, al);
+        Fh[t] = F.hi;
+        Fl[t] = F.lo;
+    }
 }
 
 template <int R>
@@ -1076,22 +1107,22 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         const double sce = ldexp(1.0, -s_pe[b * NVAR + var]);
                         if (V.nsplit == 2) {
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 2, 2>(G, NX, NY, bxt[0], byt[0], fx, fy, offs, num,
-                                                                V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift, sce,
-                                                                V.kbits, Fh[0], Fl[0], flags);
+                                fused_group_g3<4 * R - 2, 2, 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num,
+                                                                    V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift,
+                                                                    sce, V.kbits, Fh, Fl, flags);
                             else
-                                fused_group_g3<3 * R - 2, 2, 2>(G, NX, NY, bxt[0], byt[0], fx, fy, offs, num,
-                                                                V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift, sce,
-                                                                V.kbits, Fh[0], Fl[0], flags);
+                                fused_group_g3<3 * R - 2, 2, 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num,
+                                                                    V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift,
+                                                                    sce, V.kbits, Fh, Fl, flags);
                         } else {
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 1, 3>(G, NX, NY, bxt[0], byt[0], fx, fy, offs, num,
-                                                                nullptr, nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh[0],
-                                                                Fl[0], flags);
+                                fused_group_g3<4 * R - 2, 1, 3, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, nullptr,
+                                                                    nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
+                                                                    flags);
                             else
-                                fused_group_g3<3 * R - 2, 1, 3>(G, NX, NY, bxt[0], byt[0], fx, fy, offs, num,
-                                                                nullptr, nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh[0],
-                                                                Fl[0], flags);
+                                fused_group_g3<3 * R - 2, 1, 3, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, nullptr,
+                                                                    nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
+                                                                    flags);
                         }
                     } else if (var == 0)
                         fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);

@@ -182,15 +182,11 @@ cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStrea
                               long long *nlaunch);
 
 // launchers (bsf_kernels.cu)
-cudaError_t launch_fill_dd(const void *f, int u8, double2 *g, const Geometry &geo, int nbasis_copy,
-                           cudaStream_t st, long long *nlaunch);
-cudaError_t launch_fill_i64(const uint8_t *f, unsigned long long *g, const Geometry &geo, int nbasis_copy,
-                            cudaStream_t st, long long *nlaunch);
-cudaError_t launch_scan_dd(double2 *g, const Geometry &geo, int basis, int order, void *ws, size_t ws_bytes,
-                           cudaStream_t st, long long *nlaunch);
-cudaError_t launch_scan_i64(unsigned long long *g, const Geometry &geo, int basis, int order, void *ws,
-                            size_t ws_bytes, cudaStream_t st, long long *nlaunch);
-size_t scan_workspace_bytes(const Geometry &geo);
+// global pre-integration: one single-pass kernel per level (bsf_scan.cuh)
+cudaError_t launch_preint_dd(const void *f, int u8, double2 *g, const Geometry &geo, int basis, int order,
+                             cudaStream_t st, long long *nlaunch);
+cudaError_t launch_preint_i64(const uint8_t *f, unsigned long long *g, const Geometry &geo, int basis, int order,
+                              cudaStream_t st, long long *nlaunch);
 cudaError_t launch_gather_impl(const GatherArgs &a, int order, int precision, cudaStream_t st,
                                const LutBasis *luts_dev, long long *nlaunch);
 

@@ -10,6 +10,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "bsf_dd.cuh"
 #include "bsf_internal.h"
 #include "bsf_pixel.cuh"
@@ -37,219 +39,103 @@ struct OpDD {
     __device__ static T shfl_up(T v, int d) {
         return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
     }
+    __device__ static T shfl_idx(T v, int l) {
+        return make_double2(__shfl_sync(0xffffffffu, v.x, l), __shfl_sync(0xffffffffu, v.y, l));
+    }
+    __device__ static T shfl_xor(T v, int l) {
+        return make_double2(__shfl_xor_sync(0xffffffffu, v.x, l), __shfl_xor_sync(0xffffffffu, v.y, l));
+    }
 };
 struct OpU64 {
     typedef unsigned long long T;
     __device__ static T zero() { return 0ull; }
     __device__ static T add(T a, T b) { return a + b; }  // wraps mod 2^64
     __device__ static T shfl_up(T v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+    __device__ static T shfl_idx(T v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+    __device__ static T shfl_xor(T v, int l) { return __shfl_xor_sync(0xffffffffu, v, l); }
 };
 
+#include "bsf_scan.cuh"
+
 // ---------------------------------------------------------------------------
-// fill: g = 0 on the domain, g[y][x+P] = f[y][x] on the image
+// launchers of the global pre-integration (one kernel per level)
 // ---------------------------------------------------------------------------
+// per level: rows (sy = 0) or strips of 32 u-columns walked in blocks of 32
+// rows, ND row blocks in flight (64 KB of shared memory per block)
+// block shapes (measured on config 3, tools/time_preint.py): int64 8 warps x 16
+// rows, 2 blocks in flight (64 KB); double-double 8 warps x 8 rows, 3 blocks (96 KB)
+#ifndef BSF_SCAN_NW_I64
+#define BSF_SCAN_NW_I64 8
+#define BSF_SCAN_RPW_I64 16
+#define BSF_SCAN_ND_I64 2
+#endif
+#ifndef BSF_SCAN_NW_DD
+#define BSF_SCAN_NW_DD 8
+#define BSF_SCAN_RPW_DD 8
+#define BSF_SCAN_ND_DD 3
+#endif
+template <class Op, class In, int SX, int SY>
+static cudaError_t scan_strips(const In *in, typename Op::T *g, const Geometry &geo, cudaStream_t st) {
+    constexpr bool DD = sizeof(typename Op::T) == 16;
+    constexpr int NW = DD ? BSF_SCAN_NW_DD : BSF_SCAN_NW_I64, RPW = DD ? BSF_SCAN_RPW_DD : BSF_SCAN_RPW_I64,
+                  ND = DD ? BSF_SCAN_ND_DD : BSF_SCAN_ND_I64;
+    constexpr int SMEM = ND * NW * RPW * 32 * (int)sizeof(typename Op::T);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(scan_strip_kernel<Op, In, SX, SY, NW, RPW, ND>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int span = abs(SX) * ((geo.GH - 1) / SY);
+    const int U0 = SX > 0 ? -span : 0, NS = (geo.GW + span + 31) / 32;
+    scan_strip_kernel<Op, In, SX, SY, NW, RPW, ND>
+        <<<(unsigned)((long long)geo.nimg * NS), 32 * NW, SMEM, st>>>(in, g, geo, U0, NS);
+    return cudaGetLastError();
+}
+
 template <class Op, class In>
-__global__ void fill_kernel(const In *__restrict__ f, typename Op::T *__restrict__ g, Geometry geo, int ncopy) {
-    long long n = (long long)geo.GH * geo.GW;
-    int img = blockIdx.y;
-    const In *fi = f + (size_t)img * geo.H * geo.W;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        int y = (int)(i / geo.GW), xg = (int)(i % geo.GW);
-        int x = xg - geo.P;
-        typename Op::T v = Op::zero();
-        if (y < geo.H && x >= 0 && x < geo.W) {
-            if constexpr (sizeof(typename Op::T) == 16)
-                v = make_double2((double)fi[(size_t)y * geo.W + x], 0.0);
-            else
-                v = (typename Op::T)fi[(size_t)y * geo.W + x];
-        }
-        for (int b = 0; b < ncopy; ++b) g[((size_t)b * geo.nimg + img) * n + i] = v;
+static cudaError_t scan_level(const In *in, typename Op::T *g, const Geometry &geo, int sx, int sy, cudaStream_t st) {
+    if (sy == 0) {
+        constexpr int EPL = sizeof(typename Op::T) == 16 ? 4 : 8, WPC = 8;
+        const long long rows = (long long)geo.nimg * geo.GH;
+        scan_row_kernel<Op, In, EPL, WPC><<<(unsigned)((rows + WPC - 1) / WPC), 32 * WPC, 0, st>>>(in, g, geo);
+        return cudaGetLastError();
     }
+    // the seven lattice steps of the two bases (c_scan_order)
+    if (sy == 1 && sx == 1) return scan_strips<Op, In, 1, 1>(in, g, geo, st);
+    if (sy == 1 && sx == 0) return scan_strips<Op, In, 0, 1>(in, g, geo, st);
+    if (sy == 1 && sx == -1) return scan_strips<Op, In, -1, 1>(in, g, geo, st);
+    if (sy == 2 && sx == 1) return scan_strips<Op, In, 1, 2>(in, g, geo, st);
+    if (sy == 1 && sx == 2) return scan_strips<Op, In, 2, 1>(in, g, geo, st);
+    if (sy == 2 && sx == -1) return scan_strips<Op, In, -1, 2>(in, g, geo, st);
+    if (sy == 1 && sx == -2) return scan_strips<Op, In, -2, 1>(in, g, geo, st);
+    return cudaErrorInvalidValue;
 }
 
-// ---------------------------------------------------------------------------
-// Horizontal level s = (1, 0): one CTA per (row, image); tiles of 256 with a
-// warp-shuffle block scan and a running carry.
-// ---------------------------------------------------------------------------
-template <class Op>
-__global__ void __launch_bounds__(256) scan_rows_kernel(typename Op::T *__restrict__ g, int GW, size_t img_stride) {
-    typedef typename Op::T T;
-    __shared__ T warp_tot[8];
-    __shared__ T carry_s;
-    T *row = g + blockIdx.y * img_stride + (size_t)blockIdx.x * GW;
-    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    T carry = Op::zero();
-    for (int base = 0; base < GW; base += 256) {
-        int x = base + threadIdx.x;
-        T v = x < GW ? row[x] : Op::zero();
-        // inclusive warp scan
-        for (int d = 1; d < 32; d <<= 1) {
-            T o = Op::shfl_up(v, d);
-            if (lane >= d) v = Op::add(v, o);
-        }
-        if (lane == 31) warp_tot[wid] = v;
-        __syncthreads();
-        T pre = carry;
-        for (int w = 0; w < wid; ++w) pre = Op::add(pre, warp_tot[w]);
-        v = Op::add(pre, v);
-        if (x < GW) row[x] = v;
-        if (threadIdx.x == 255) carry_s = v;
-        __syncthreads();
-        carry = carry_s;
-        __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Levels with s_y >= 1: lines q0 + j s.  Rows are cut into chunks of RC rows;
-// a line meets chunk c in one segment.  Three passes:
-//   partial: per (chunk, phase, line) segment sum          (reads level input)
-//   carry:   per line, exclusive scan over chunks          (tiny)
-//   apply:   per segment, inclusive scan + carry, in place (reads + writes)
-// Lines are indexed at the chunk's first row of their phase by i = x + Xpad,
-// i in [0, NL); a line moves by delta = sx*RC/sy columns per chunk.
-// Points outside the domain are zero state (truncated domain, R3).
-// ---------------------------------------------------------------------------
-constexpr int RC = 32;
-
-struct ScanShape {
-    int sx, sy, Xpad, NL, NC, delta;
-};
-
-static ScanShape scan_shape(const Geometry &geo, int sx, int sy) {
-    ScanShape s;
-    s.sx = sx;
-    s.sy = sy;
-    s.Xpad = abs(sx) * ((RC + sy - 1) / sy);
-    s.NL = geo.GW + 2 * s.Xpad;
-    s.NC = (geo.GH + RC - 1) / RC;
-    s.delta = sx * (RC / sy);
-    return s;
-}
-
-template <class Op>
-__global__ void scan_partial_kernel(const typename Op::T *__restrict__ g, Geometry geo, ScanShape sh,
-                                    typename Op::T *__restrict__ partial) {
-    typedef typename Op::T T;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= sh.NL) return;
-    int c = blockIdx.y / sh.sy, ph = blockIdx.y % sh.sy, img = blockIdx.z;
-    const T *gi = g + (size_t)img * geo.GH * geo.GW;
-    int y = c * RC + ph, x = i - sh.Xpad;
-    int yend = min((c + 1) * RC, geo.GH);
-    T acc = Op::zero();
-    for (; y < yend; y += sh.sy, x += sh.sx)
-        if (x >= 0 && x < geo.GW) acc = Op::add(acc, gi[(size_t)y * geo.GW + x]);
-    partial[(((size_t)img * sh.NC + c) * sh.sy + ph) * sh.NL + i] = acc;
-}
-
-template <class Op>
-__global__ void scan_carry_kernel(const typename Op::T *__restrict__ partial, typename Op::T *__restrict__ carry,
-                                  ScanShape sh, int i0lo, int nlines) {
-    typedef typename Op::T T;
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nlines * sh.sy) return;
-    int img = blockIdx.y;
-    int ph = t % sh.sy, i0 = i0lo + t / sh.sy;
-    size_t base = (size_t)img * sh.NC * sh.sy * sh.NL;
-    T run = Op::zero();
-    for (int c = 0; c < sh.NC; ++c) {
-        int ic = i0 + c * sh.delta;
-        if (ic >= 0 && ic < sh.NL) {
-            size_t o = base + ((size_t)c * sh.sy + ph) * sh.NL + ic;
-            carry[o] = run;
-            run = Op::add(run, partial[o]);
-        }
-    }
-}
-
-template <class Op>
-__global__ void scan_apply_kernel(typename Op::T *__restrict__ g, Geometry geo, ScanShape sh,
-                                  const typename Op::T *__restrict__ carry) {
-    typedef typename Op::T T;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= sh.NL) return;
-    int c = blockIdx.y / sh.sy, ph = blockIdx.y % sh.sy, img = blockIdx.z;
-    T *gi = g + (size_t)img * geo.GH * geo.GW;
-    int y = c * RC + ph, x = i - sh.Xpad;
-    int yend = min((c + 1) * RC, geo.GH);
-    T acc = carry[(((size_t)img * sh.NC + c) * sh.sy + ph) * sh.NL + i];
-    for (; y < yend; y += sh.sy, x += sh.sx)
-        if (x >= 0 && x < geo.GW) {
-            size_t o = (size_t)y * geo.GW + x;
-            acc = Op::add(acc, gi[o]);
-            gi[o] = acc;
-        }
-}
-
-size_t scan_workspace_bytes(const Geometry &geo) {
-    ScanShape s = scan_shape(geo, 2, 1);  // widest NL, most chunks per phase
-    size_t per = (size_t)s.NC * 2 * (geo.GW + 4 * RC);
-    return 2 * per * 16 * (size_t)geo.nimg;
-}
-
-template <class Op>
-static cudaError_t scan_levels(typename Op::T *g, const Geometry &geo, int basis, int order, void *ws,
-                               size_t ws_bytes, cudaStream_t st, long long *nl) {
-    typedef typename Op::T T;
-    if (ws_bytes < scan_workspace_bytes(geo)) return cudaErrorInvalidValue;
-    size_t half = ws_bytes / 2;
-    T *partial = (T *)ws;
-    T *carry = (T *)((char *)ws + half);
-    size_t img_stride = (size_t)geo.GH * geo.GW;
-    for (int rep = 0; rep < order; ++rep) {
+template <class Op, class In>
+static cudaError_t scan_basis(const In *f, typename Op::T *g, const Geometry &geo, int basis, int order,
+                              cudaStream_t st, long long *nl) {
+    for (int rep = 0; rep < order; ++rep)
         for (int lv = 0; lv < 4; ++lv) {
-            int sx = h_scan_order[basis][lv][0], sy = h_scan_order[basis][lv][1];
-            if (sy == 0) {
-                scan_rows_kernel<Op><<<dim3(geo.GH, geo.nimg), 256, 0, st>>>(g, geo.GW, img_stride);
-                ++*nl;
-                continue;
-            }
-            ScanShape sh = scan_shape(geo, sx, sy);
-            dim3 grid((sh.NL + 127) / 128, sh.NC * sh.sy, geo.nimg);
-            scan_partial_kernel<Op><<<grid, 128, 0, st>>>(g, geo, sh, partial);
-            int span = (sh.NC - 1) * abs(sh.delta);
-            int i0lo = sh.delta > 0 ? -span : 0;
-            int nlines = sh.NL + span;
-            scan_carry_kernel<Op><<<dim3((nlines * sh.sy + 127) / 128, geo.nimg), 128, 0, st>>>(partial, carry, sh,
-                                                                                                  i0lo, nlines);
-            scan_apply_kernel<Op><<<grid, 128, 0, st>>>(g, geo, sh, carry);
-            *nl += 3;
+            const int sx = h_scan_order[basis][lv][0], sy = h_scan_order[basis][lv][1];
+            cudaError_t e = (rep == 0 && lv == 0) ? scan_level<Op, In>(f, g, geo, sx, sy, st)
+                                                  : scan_level<Op, typename Op::T>(g, g, geo, sx, sy, st);
+            ++*nl;
+            if (e != cudaSuccess) return e;
         }
-    }
-    return cudaGetLastError();
+    return cudaSuccess;
 }
 
-cudaError_t launch_fill_dd(const void *f, int u8, double2 *g, const Geometry &geo, int ncopy, cudaStream_t st,
-                           long long *nl) {
-    long long n = (long long)geo.GH * geo.GW;
-    int blocks = (int)min((n + 255) / 256, 148LL * 8);
-    dim3 grid(blocks, geo.nimg);
-    if (u8)
-        fill_kernel<OpDD, uint8_t><<<grid, 256, 0, st>>>((const uint8_t *)f, g, geo, ncopy);
-    else
-        fill_kernel<OpDD, float><<<grid, 256, 0, st>>>((const float *)f, g, geo, ncopy);
-    ++*nl;
-    return cudaGetLastError();
+cudaError_t launch_preint_dd(const void *f, int u8, double2 *g, const Geometry &geo, int basis, int order,
+                             cudaStream_t st, long long *nl) {
+    if (u8) return scan_basis<OpDD, uint8_t>((const uint8_t *)f, g, geo, basis, order, st, nl);
+    return scan_basis<OpDD, float>((const float *)f, g, geo, basis, order, st, nl);
 }
 
-cudaError_t launch_fill_i64(const uint8_t *f, unsigned long long *g, const Geometry &geo, int ncopy,
-                            cudaStream_t st, long long *nl) {
-    long long n = (long long)geo.GH * geo.GW;
-    int blocks = (int)min((n + 255) / 256, 148LL * 8);
-    fill_kernel<OpU64, uint8_t><<<dim3(blocks, geo.nimg), 256, 0, st>>>(f, g, geo, ncopy);
-    ++*nl;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_scan_dd(double2 *g, const Geometry &geo, int basis, int order, void *ws, size_t ws_bytes,
-                           cudaStream_t st, long long *nl) {
-    return scan_levels<OpDD>(g, geo, basis, order, ws, ws_bytes, st, nl);
-}
-
-cudaError_t launch_scan_i64(unsigned long long *g, const Geometry &geo, int basis, int order, void *ws,
-                            size_t ws_bytes, cudaStream_t st, long long *nl) {
-    return scan_levels<OpU64>(g, geo, basis, order, ws, ws_bytes, st, nl);
+cudaError_t launch_preint_i64(const uint8_t *f, unsigned long long *g, const Geometry &geo, int basis, int order,
+                              cudaStream_t st, long long *nl) {
+    return scan_basis<OpU64, uint8_t>(f, g, geo, basis, order, st, nl);
 }
 
 // ---------------------------------------------------------------------------

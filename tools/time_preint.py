@@ -14,7 +14,7 @@ from paper_1109_5114_b200 import bsf  # noqa: E402
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json"))).get("hbm_gbs", 6542.4) if os.path.exists(
     "MEASURED_PEAKS.json") else 6542.4
-for cfg, r in ((2, 2), (3, 1), (3, 2)):
+for cfg, r in ((2, 2), (3, 1), (3, 2), (3, 4)):
     w = synth.workload(cfg, order=r)
     plan = bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" else bsf.BSF_F32, order=r,
                     basis=w.basis, max_sigma=w.max_sigma)
