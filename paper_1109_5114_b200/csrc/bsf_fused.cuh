@@ -34,7 +34,7 @@ constexpr uint16_t NOKEY = 0xFFFF;
 #define BSF_MT1 4
 #endif
 #ifndef BSF_MT3
-#define BSF_MT3 2
+#define BSF_MT3 1
 #endif
 template <int R> struct FusedCfg;
 // NTAP taps per pixel, P pixels per chunk, MT 8-item m-tiles per group
