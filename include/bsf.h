@@ -84,7 +84,9 @@ typedef struct {
     bsf_basis basis;
     float max_sigma;     /* upper bound of sigma_x, sigma_y over the covariance field         */
     int margin_x;        /* P: domain columns [-P, W+P); 0 = derive from max_sigma            */
-    int margin_y;        /* Pb: domain rows [0, H+Pb); 0 = derive from max_sigma              */
+    int margin_y;        /* Pb: domain rows [0, H+Pb); 0 = derive from max_sigma; -1 = none:
+                          * the plan is a row strip of a larger domain (multi-GPU GLOBAL
+                          * mode, bsf_scan_level), only pre-integration calls are valid   */
     int clamp;           /* 1: rho <- min(rho, 0.95 rho_B(phi)) at fixed trace/orientation    */
                          /* 0: infeasible pixels give NaN and raise BSF_EINFEASIBLE            */
     bsf_precision precision;
@@ -138,6 +140,24 @@ bsf_status bsf_preintegrate(bsf_plan_t plan, const void *f_dev, void *g_dev, voi
  *          (1,0),(1,1),(0,1),(-1,1); Theta' (1,2),(2,1),(-1,2),(-2,1)
  *          (Alg. 3 (a)-(d)); repeated r times.  BSF_EINVAL for f32 input.   */
 bsf_status bsf_preintegrate_exact(bsf_plan_t plan, const void *f_dev, void *g_dev, void *stream);
+
+/* One running-sum level of the global pre-integration (PAPER.md:106-110,
+ * Alg. 3 step 2), for row strips of one domain sharded over ranks (SURVEY.md
+ * 8(e) GLOBAL mode: the scan carries travel down the rank chain).
+ *   slot:  running-sum slot (0; 1 = Theta' under BSF_DUAL); level in [0, 4r):
+ *          the step is bsf_scan_step(slot, level), levels run in order.
+ *   exact: 1 = int64 wrapping (u8 input, bit-exact), 0 = double-double.
+ *   f_dev: the strip's image rows (read by level 0 only); g_dev: as for
+ *          bsf_preintegrate[_exact] (all slots), updated in place.
+ *   carry_dev: [batch*channels][sy][g_width] elements of g's type = this
+ *          level's running sums on the sy domain rows just above the strip
+ *          (the previous rank's last sy rows after this level), or NULL for
+ *          the first strip (zero state).  Strip boundaries must be even rows.
+ * Running every level with the carries of the strip above reproduces the
+ * single-plan bsf_preintegrate_exact bit for bit.                            */
+bsf_status bsf_scan_step(bsf_plan_t plan, int slot, int level, int *sx, int *sy);
+bsf_status bsf_scan_level(bsf_plan_t plan, int slot, int level, int exact, const void *f_dev, void *g_dev,
+                          const void *carry_dev, void *stream);
 
 /* Local finite difference for every pixel (Alg. 3 step 3, PAPER.md:400-403,
  * generalised to order r and to Algorithm 2's basis choice).

@@ -68,6 +68,10 @@ def lib():
         for name in ("bsf_preintegrate", "bsf_preintegrate_exact"):
             getattr(L, name).restype = st
             getattr(L, name).argtypes = [vp, vp, vp, vp]
+        L.bsf_scan_step.restype = st
+        L.bsf_scan_step.argtypes = [vp, i, i, ctypes.POINTER(i), ctypes.POINTER(i)]
+        L.bsf_scan_level.restype = st
+        L.bsf_scan_level.argtypes = [vp, i, i, i, vp, vp, vp, vp]
         L.bsf_filter.restype = st
         L.bsf_filter.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_filter_points.restype = st
@@ -165,6 +169,18 @@ class Plan:
 
     def preintegrate_exact(self, f, g, stream=None):
         _check(lib().bsf_preintegrate_exact(self.handle, _ptr(f), _ptr(g), _stream(stream)))
+
+    def scan_step(self, slot, level):
+        """(sx, sy) of running-sum level `level` of slot `slot`."""
+        sx, sy = ctypes.c_int(), ctypes.c_int()
+        _check(lib().bsf_scan_step(self.handle, slot, level, ctypes.byref(sx), ctypes.byref(sy)))
+        return sx.value, sy.value
+
+    def scan_level(self, slot, level, f, g, carry=None, exact=True, stream=None):
+        """One pre-integration level in place on g (level 0 reads f); carry = the
+        level's sums on the sy domain rows above this row strip, or None."""
+        _check(lib().bsf_scan_level(self.handle, slot, level, 1 if exact else 0, _ptr(f), _ptr(g),
+                                    _ptr(carry) if carry is not None else None, _stream(stream)))
 
     def filter(self, g, cov, out, stream=None):
         _check(lib().bsf_filter(self.handle, _ptr(g), _ptr(cov), _ptr(out), _stream(stream)))

@@ -304,11 +304,11 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     if (!(d.max_sigma > 0) || !isfinite(d.max_sigma)) return set_err(BSF_EINVAL, "max_sigma must be > 0");
     if (d.precision != BSF_PREC_FP64 && d.precision != BSF_PREC_DD && d.precision != BSF_PREC_AUTO)
         return set_err(BSF_EINVAL, "bad precision");
-    if (d.margin_x < 0 || d.margin_y < 0) return set_err(BSF_EINVAL, "negative margin");
+    if (d.margin_x < 0 || d.margin_y < -1) return set_err(BSF_EINVAL, "negative margin");
     if (d.anchor != BSF_ANCHOR_GLOBAL && d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EINVAL, "bad anchor");
     int disp = required_disp(d.max_sigma, d.order);
     int needP = disp + 3 * d.order + 2, needPb = disp + 2;
-    if ((d.margin_x && d.margin_x < needP) || (d.margin_y && d.margin_y < needPb))
+    if ((d.margin_x && d.margin_x < needP) || (d.margin_y > 0 && d.margin_y < needPb))
         return set_err(BSF_ERANGE, "margins smaller than the kernel reach (need P >= " + std::to_string(needP) +
                                        ", Pb >= " + std::to_string(needPb) + ")");
     CUDA_TRY(cudaSetDevice(d.device));
@@ -318,7 +318,7 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     g.W = d.width;
     g.H = d.height;
     g.P = d.margin_x ? d.margin_x : needP;
-    g.Pb = d.margin_y ? d.margin_y : needPb;
+    g.Pb = d.margin_y > 0 ? d.margin_y : (d.margin_y == 0 ? needPb : 0);  // -1: row strip, no bottom margin
     g.GW = g.W + 2 * g.P;
     g.GH = g.H + g.Pb;
     g.nimg = d.batch * d.channels;
@@ -400,6 +400,29 @@ extern "C" bsf_status bsf_preintegrate_exact(bsf_plan_t p, const void *f, void *
     return BSF_OK;
 }
 
+extern "C" bsf_status bsf_scan_step(bsf_plan_t p, int slot, int level, int *sx, int *sy) {
+    if (!p || !sx || !sy) return set_err(BSF_EINVAL, "null argument");
+    if (slot < 0 || slot >= p->geo.nbases || level < 0 || level >= 4 * p->d.order)
+        return set_err(BSF_EINVAL, "slot or level out of range");
+    scan_step(p->bases[slot], level, sx, sy);
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_scan_level(bsf_plan_t p, int slot, int level, int exact, const void *f, void *g,
+                                     const void *carry, void *stream) {
+    if (!p || !g || (level == 0 && !f)) return set_err(BSF_EINVAL, "null argument");
+    if (slot < 0 || slot >= p->geo.nbases || level < 0 || level >= 4 * p->d.order)
+        return set_err(BSF_EINVAL, "slot or level out of range");
+    if (exact && p->d.in_dtype != BSF_U8) return set_err(BSF_EINVAL, "exact pre-integration needs u8 input");
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last = st;
+    const size_t slot_bytes = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW * (exact ? 8 : 16);
+    CUDA_TRY(launch_scan_level(f, p->d.in_dtype == BSF_U8, (char *)g + slot * slot_bytes, exact, p->geo,
+                               p->bases[slot], level, carry, st));
+    ++p->nlaunch;
+    return BSF_OK;
+}
+
 static GatherArgs gather_args(bsf_plan_s *p, const void *g, const void *cov, void *out) {
     GatherArgs a;
     memset(&a, 0, sizeof a);
@@ -417,6 +440,7 @@ static GatherArgs gather_args(bsf_plan_s *p, const void *g, const void *cov, voi
 
 extern "C" bsf_status bsf_filter(bsf_plan_t p, const void *g, const void *cov, void *out, void *stream) {
     if (!p || !g || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
     GatherArgs a = gather_args(p, g, cov, out);
@@ -432,6 +456,7 @@ extern "C" bsf_status bsf_filter_points(bsf_plan_t p, const void *g, const void 
 extern "C" bsf_status bsf_filter_points_aux(bsf_plan_t p, const void *g, const void *cov, const int *pts, int npts,
                                             double *out, double *aux, void *stream) {
     if (!p || !g || !cov || !out || (!pts && npts)) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (npts < 0) return set_err(BSF_EINVAL, "npts < 0");
     if (npts == 0) return BSF_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -520,6 +545,7 @@ static cudaError_t launch_tile(bsf_plan_s *p, const TileArgs &a, cudaStream_t st
 extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *cov, const int *pts, int npts,
                                      double *out, double *aux, void *stream) {
     if (!p || !f || !cov || !out || (!pts && npts)) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (npts < 0) return set_err(BSF_EINVAL, "npts < 0");
     if (npts == 0) return BSF_OK;
     bsf_status s = ensure_tile_ws(p);
@@ -561,6 +587,7 @@ extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void
 extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov, void *out, double *sigma2_out,
                                    void *stream) {
     if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     bsf_status s = ensure_tile_ws(p);
     if (s != BSF_OK) return s;
     if (!p->fused) return set_err(BSF_EUNSUPPORTED, "Algorithm 1 runs on the exact split path (order <= 3)");
@@ -603,6 +630,7 @@ extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov,
 extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void *cov_host, void *out_host,
                                    void *stream) {
     if (!p || !f_host || !cov_host || !out_host) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     const Geometry &g = p->geo;
     size_t fb = (size_t)g.nimg * g.H * g.W * (p->d.in_dtype == BSF_U8 ? 1 : 4);
     size_t cb = (size_t)p->d.batch * 3 * g.H * g.W * 4;

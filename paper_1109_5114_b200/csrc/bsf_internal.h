@@ -187,6 +187,11 @@ cudaError_t launch_preint_dd(const void *f, int u8, double2 *g, const Geometry &
                              cudaStream_t st, long long *nlaunch);
 cudaError_t launch_preint_i64(const uint8_t *f, unsigned long long *g, const Geometry &geo, int basis, int order,
                               cudaStream_t st, long long *nlaunch);
+// one level (level 0 reads f) of one basis, optionally continuing the running
+// sums from the sy domain rows above (carry, [nimg][sy][GW]; null = zero state)
+cudaError_t launch_scan_level(const void *f, int u8, void *g, int exact, const Geometry &geo, int basis, int level,
+                              const void *carry, cudaStream_t st);
+void scan_step(int basis, int level, int *sx, int *sy);
 cudaError_t launch_gather_impl(const GatherArgs &a, int order, int precision, cudaStream_t st,
                                const LutBasis *luts_dev, long long *nlaunch);
 

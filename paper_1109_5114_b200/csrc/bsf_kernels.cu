@@ -75,7 +75,8 @@ struct OpU64 {
 #define BSF_SCAN_ND_DD 3
 #endif
 template <class Op, class In, int SX, int SY>
-static cudaError_t scan_strips(const In *in, typename Op::T *g, const Geometry &geo, cudaStream_t st) {
+static cudaError_t scan_strips(const In *in, typename Op::T *g, const Geometry &geo, const typename Op::T *carry,
+                               cudaStream_t st) {
     constexpr bool DD = sizeof(typename Op::T) == 16;
     constexpr int NW = DD ? BSF_SCAN_NW_DD : BSF_SCAN_NW_I64, RPW = DD ? BSF_SCAN_RPW_DD : BSF_SCAN_RPW_I64,
                   ND = DD ? BSF_SCAN_ND_DD : BSF_SCAN_ND_I64;
@@ -90,12 +91,13 @@ static cudaError_t scan_strips(const In *in, typename Op::T *g, const Geometry &
     const int span = abs(SX) * ((geo.GH - 1) / SY);
     const int U0 = SX > 0 ? -span : 0, NS = (geo.GW + span + 31) / 32;
     scan_strip_kernel<Op, In, SX, SY, NW, RPW, ND>
-        <<<(unsigned)((long long)geo.nimg * NS), 32 * NW, SMEM, st>>>(in, g, geo, U0, NS);
+        <<<(unsigned)((long long)geo.nimg * NS), 32 * NW, SMEM, st>>>(in, g, geo, U0, NS, carry);
     return cudaGetLastError();
 }
 
 template <class Op, class In>
-static cudaError_t scan_level(const In *in, typename Op::T *g, const Geometry &geo, int sx, int sy, cudaStream_t st) {
+static cudaError_t scan_level(const In *in, typename Op::T *g, const Geometry &geo, int sx, int sy,
+                              const typename Op::T *carry, cudaStream_t st) {
     if (sy == 0) {
         constexpr int EPL = sizeof(typename Op::T) == 16 ? 4 : 8, WPC = 8;
         const long long rows = (long long)geo.nimg * geo.GH;
@@ -103,13 +105,13 @@ static cudaError_t scan_level(const In *in, typename Op::T *g, const Geometry &g
         return cudaGetLastError();
     }
     // the seven lattice steps of the two bases (c_scan_order)
-    if (sy == 1 && sx == 1) return scan_strips<Op, In, 1, 1>(in, g, geo, st);
-    if (sy == 1 && sx == 0) return scan_strips<Op, In, 0, 1>(in, g, geo, st);
-    if (sy == 1 && sx == -1) return scan_strips<Op, In, -1, 1>(in, g, geo, st);
-    if (sy == 2 && sx == 1) return scan_strips<Op, In, 1, 2>(in, g, geo, st);
-    if (sy == 1 && sx == 2) return scan_strips<Op, In, 2, 1>(in, g, geo, st);
-    if (sy == 2 && sx == -1) return scan_strips<Op, In, -1, 2>(in, g, geo, st);
-    if (sy == 1 && sx == -2) return scan_strips<Op, In, -2, 1>(in, g, geo, st);
+    if (sy == 1 && sx == 1) return scan_strips<Op, In, 1, 1>(in, g, geo, carry, st);
+    if (sy == 1 && sx == 0) return scan_strips<Op, In, 0, 1>(in, g, geo, carry, st);
+    if (sy == 1 && sx == -1) return scan_strips<Op, In, -1, 1>(in, g, geo, carry, st);
+    if (sy == 2 && sx == 1) return scan_strips<Op, In, 1, 2>(in, g, geo, carry, st);
+    if (sy == 1 && sx == 2) return scan_strips<Op, In, 2, 1>(in, g, geo, carry, st);
+    if (sy == 2 && sx == -1) return scan_strips<Op, In, -1, 2>(in, g, geo, carry, st);
+    if (sy == 1 && sx == -2) return scan_strips<Op, In, -2, 1>(in, g, geo, carry, st);
     return cudaErrorInvalidValue;
 }
 
@@ -119,8 +121,8 @@ static cudaError_t scan_basis(const In *f, typename Op::T *g, const Geometry &ge
     for (int rep = 0; rep < order; ++rep)
         for (int lv = 0; lv < 4; ++lv) {
             const int sx = h_scan_order[basis][lv][0], sy = h_scan_order[basis][lv][1];
-            cudaError_t e = (rep == 0 && lv == 0) ? scan_level<Op, In>(f, g, geo, sx, sy, st)
-                                                  : scan_level<Op, typename Op::T>(g, g, geo, sx, sy, st);
+            cudaError_t e = (rep == 0 && lv == 0) ? scan_level<Op, In>(f, g, geo, sx, sy, nullptr, st)
+                                                  : scan_level<Op, typename Op::T>(g, g, geo, sx, sy, nullptr, st);
             ++*nl;
             if (e != cudaSuccess) return e;
         }
@@ -136,6 +138,27 @@ cudaError_t launch_preint_dd(const void *f, int u8, double2 *g, const Geometry &
 cudaError_t launch_preint_i64(const uint8_t *f, unsigned long long *g, const Geometry &geo, int basis, int order,
                               cudaStream_t st, long long *nl) {
     return scan_basis<OpU64, uint8_t>(f, g, geo, basis, order, st, nl);
+}
+
+void scan_step(int basis, int level, int *sx, int *sy) {
+    *sx = h_scan_order[basis][level % 4][0];
+    *sy = h_scan_order[basis][level % 4][1];
+}
+
+cudaError_t launch_scan_level(const void *f, int u8, void *g, int exact, const Geometry &geo, int basis, int level,
+                              const void *carry, cudaStream_t st) {
+    int sx, sy;
+    scan_step(basis, level, &sx, &sy);
+    if (exact) {
+        typedef unsigned long long T;
+        if (level == 0) return scan_level<OpU64, uint8_t>((const uint8_t *)f, (T *)g, geo, sx, sy, (const T *)carry, st);
+        return scan_level<OpU64, T>((const T *)g, (T *)g, geo, sx, sy, (const T *)carry, st);
+    }
+    if (level == 0) {
+        if (u8) return scan_level<OpDD, uint8_t>((const uint8_t *)f, (double2 *)g, geo, sx, sy, (const double2 *)carry, st);
+        return scan_level<OpDD, float>((const float *)f, (double2 *)g, geo, sx, sy, (const double2 *)carry, st);
+    }
+    return scan_level<OpDD, double2>((const double2 *)g, (double2 *)g, geo, sx, sy, (const double2 *)carry, st);
 }
 
 // ---------------------------------------------------------------------------

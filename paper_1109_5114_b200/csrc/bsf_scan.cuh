@@ -107,7 +107,7 @@ __device__ __forceinline__ typename Op::T strip_value(const unsigned char *slot,
 // registers.  The rows stream through a cp.async ring of ND row blocks.
 template <class Op, class In, int SX, int SY, int NW, int RPW, int ND>
 __global__ void __launch_bounds__(32 * NW) scan_strip_kernel(const In *in, typename Op::T *out, Geometry geo, int U0,
-                                                              int NS) {
+                                                              int NS, const typename Op::T *carry_in) {
     typedef typename Op::T T;
     static_assert(RPW % 2 == 0, "phases of SY = 2 lines need an even row count per warp");
     constexpr int SLOT = sizeof(T);  // >= 4: also holds a u8 word or an f32
@@ -147,7 +147,14 @@ __global__ void __launch_bounds__(32 * NW) scan_strip_kernel(const In *in, typen
     for (int j = 0; j < ND - 1; ++j) issue(j);
     T carry[SY];  // strip carry of the lines y even / odd (odd only for SY = 2)
 #pragma unroll
-    for (int ph = 0; ph < SY; ++ph) carry[ph] = Op::zero();
+    for (int ph = 0; ph < SY; ++ph) {
+        // a row strip of a larger domain (multi-GPU GLOBAL mode): the line through
+        // (u, ph) continues the level's running sum at (u - SX, ph - SY), which is
+        // row ph of carry_in ([nimg][SY][GW], the SY domain rows above the strip)
+        carry[ph] = Op::zero();
+        if (carry_in && ph < geo.GH && u >= 0 && u < geo.GW && u - SX >= 0 && u - SX < geo.GW)
+            carry[ph] = carry_in[((size_t)img * SY + ph) * geo.GW + u - SX];
+    }
     T *o = out + (size_t)img * geo.GH * geo.GW;
     for (int j = 0; j < nblk; ++j) {
         issue(j + ND - 1);

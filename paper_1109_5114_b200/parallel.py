@@ -127,3 +127,77 @@ def filter_strip(plan_factory, f_own: torch.Tensor, cov_own: torch.Tensor, strip
     out = torch.empty((1, strip.rows, f_own.shape[-1]), dtype=torch.float64, device=f_own.device)
     plan.run(f_blk.contiguous(), cov_blk.contiguous(), out, stream)
     return out[0, strip.out_slice, :]
+
+
+# ---------------------------------------------------------------------------
+# GLOBAL mode: the paper's single global pre-integration of
+# one image sharded by row strips, with the scan carries passed down the rank
+# chain.  Rank k owns domain rows [Y0, Y1) of the global g; after every
+# running-sum level with a vertical step (sy >= 1) it sends its last sy rows
+# of that level to rank k + 1, which starts the level's lines from them
+# (bsf_scan_level's carry).  Horizontal levels need nothing.  The result is
+# the single-GPU bsf_preintegrate_exact g, bit for bit.
+# ---------------------------------------------------------------------------
+@dataclass
+class GlobalStrip:
+    rank: int
+    world: int
+    Y0: int        # first global domain row of this rank
+    Y1: int        # one past the last
+    height: int    # image rows in the strip (plan height)
+    margin_y: int  # plan margin_y: -1 (no bottom margin) except on the last rank
+
+
+def global_strip(H: int, Pb: int, rank: int, world: int, unit: int = TILE) -> GlobalStrip:
+    """Split the H image rows in multiples of `unit` (even: the Theta' steps
+    have sy = 2); the last rank also owns the Pb margin rows of the domain."""
+    n = (H + unit - 1) // unit
+    t0, t1 = shard_range(n, rank, world)
+    Y0, y1 = t0 * unit, min(H, t1 * unit)
+    last = rank == world - 1
+    return GlobalStrip(rank, world, Y0, y1 + (Pb if last else 0), y1 - Y0, Pb if last else -1)
+
+
+def preintegrate_strip(plan, f, g, *, recv_carry, send_carry, exact=True, stream=None):
+    """Run every level of every slot on this strip.
+
+    plan: a bsf.Plan for the strip (height = image rows of the strip,
+    margin_y as global_strip says); f the strip's image rows; g its running-sum
+    buffer (int64 [nbases][nimg][rows][GW], or the float64 double-double
+    buffer).  recv_carry(slot, level, sy) -> tensor [nimg][sy][GW](x2) or None
+    (first rank); send_carry(slot, level, rows) is called with this strip's last
+    sy rows of the level (skipped by the last rank)."""
+    geo = plan.geometry
+    nimg = plan.desc.batch * plan.desc.channels
+    k = 1 if exact else 2
+    gv = g.view(geo.nbases, nimg, geo.g_height, geo.g_width * k)
+    for slot in range(geo.nbases):
+        for level in range(4 * plan.desc.order):
+            sx, sy = plan.scan_step(slot, level)
+            carry = recv_carry(slot, level, sy) if sy > 0 else None
+            plan.scan_level(slot, level, f, g, carry, exact=exact, stream=stream)
+            if sy > 0:
+                send_carry(slot, level, gv[slot, :, geo.g_height - sy:, :].clone())  # a copy: g is updated in place
+
+
+def preintegrate_global_strips(plan, f, g, strip: GlobalStrip, *, exact=True, group=None, stream=None):
+    """Multi-process GLOBAL-mode pre-integration: one rank per strip, carries
+    by point-to-point send/recv (NCCL over NVLink for CUDA tensors, gloo on
+    CPU).  Ranks form a chain, so there is no cycle and no deadlock."""
+    import torch.distributed as dist
+    geo = plan.geometry
+    nimg = plan.desc.batch * plan.desc.channels
+    k = 1 if exact else 2
+
+    def recv_carry(slot, level, sy):
+        if strip.rank == 0:
+            return None
+        buf = torch.empty((nimg, sy, geo.g_width * k), dtype=g.dtype, device=g.device)
+        dist.recv(buf, strip.rank - 1, group=group)
+        return buf
+
+    def send_carry(slot, level, rows):
+        if strip.rank < strip.world - 1:
+            dist.send(rows, strip.rank + 1, group=group)
+
+    preintegrate_strip(plan, f, g, recv_carry=recv_carry, send_carry=send_carry, exact=exact, stream=stream)

@@ -52,3 +52,83 @@ def test_strips_bitwise_equal_single_gpu(world, order, policy):
         got = out[0, st.out_slice]
         ref = full[0, st.y0:st.y1]
         assert torch.equal(got, ref), (rank, float((got - ref).abs().max()))
+
+
+def _global_strips_sequential(make_plan, img, H, Pb, world, exact):
+    """Run parallel.preintegrate_strip for every rank of a `world` chain in one
+    process, the carries passed through a dict (what the NCCL send/recv of
+    preintegrate_global_strips carries)."""
+    carries, parts = {}, []
+    for rank in range(world):
+        st = PL.global_strip(H, Pb, rank, world)
+        plan = make_plan(st.height, st.margin_y)
+        assert plan.geometry.g_height == st.Y1 - st.Y0
+        g = plan.empty_g_exact() if exact else plan.empty_g()
+        f = img[:, st.Y0:st.Y0 + st.height].contiguous()
+
+        def recv(slot, level, sy, rank=rank):
+            return carries.pop((rank, slot, level)) if rank > 0 else None
+
+        def send(slot, level, rows, rank=rank):
+            if rank < world - 1:
+                carries[(rank + 1, slot, level)] = rows
+
+        PL.preintegrate_strip(plan, f, g, recv_carry=recv, send_carry=send, exact=exact)
+        geo = plan.geometry
+        parts.append(g.view(geo.nbases, img.shape[0], geo.g_height, -1))
+    assert not carries
+    return torch.cat(parts, dim=2)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("order,policy", [(1, bsf.BSF_DUAL), (2, bsf.BSF_DUAL), (3, bsf.BSF_THETA_PRIME)])
+def test_global_mode_strips_bit_exact(world, order, policy):
+    """SURVEY 8(e) GLOBAL mode: row strips + scan carries down the rank chain
+    reproduce the single-plan int64 pre-integration bit for bit (u8 input,
+    batch of 2 images, ragged last strip)."""
+    H, W, smax = 150, 90, 3.0
+    gen = torch.Generator().manual_seed(7)
+    img = torch.randint(0, 256, (2, H, W), generator=gen, dtype=torch.uint8).cuda()
+
+    def make_plan(height, margin_y):
+        return bsf.Plan(W, height, batch=2, in_dtype=bsf.BSF_U8, order=order, basis=policy, max_sigma=smax,
+                        margin_y=margin_y)
+
+    full_plan = make_plan(H, 0)
+    Pb = full_plan.geometry.margin_y
+    g_full = full_plan.empty_g_exact()
+    full_plan.preintegrate_exact(img, g_full)
+    g_str = _global_strips_sequential(make_plan, img, H, Pb, world, exact=True)
+    torch.cuda.synchronize()
+    assert torch.equal(g_str, g_full), "GLOBAL-mode strips differ from the single-plan pre-integration"
+
+
+def test_global_mode_strips_double_double():
+    """Same chain on the double-double running sums (f32 input): equal to the
+    single plan up to double-double rounding order."""
+    H, W, smax, order = 130, 70, 2.5, 2
+    gen = torch.Generator().manual_seed(8)
+    img = torch.rand((1, H, W), generator=gen).cuda()
+
+    def make_plan(height, margin_y):
+        return bsf.Plan(W, height, in_dtype=bsf.BSF_F32, order=order, basis=bsf.BSF_DUAL, max_sigma=smax,
+                        margin_y=margin_y)
+
+    full_plan = make_plan(H, 0)
+    geo = full_plan.geometry
+    g_full = full_plan.empty_g()
+    full_plan.preintegrate(img, g_full)
+    g_str = _global_strips_sequential(make_plan, img, H, geo.margin_y, 3, exact=False)
+    a = g_full.view(geo.nbases, 1, geo.g_height, geo.g_width, 2).sum(-1)
+    b = g_str.reshape(geo.nbases, 1, geo.g_height, geo.g_width, 2).sum(-1)
+    assert torch.allclose(a, b, rtol=1e-15, atol=0.0)
+
+
+def test_row_strip_plan_rejects_filtering():
+    plan = bsf.Plan(64, 32, in_dtype=bsf.BSF_U8, order=1, max_sigma=2.0, margin_y=-1)
+    assert plan.geometry.margin_y == 0
+    g = plan.empty_g()
+    cov = torch.ones((1, 3, 32, 64), dtype=torch.float32, device="cuda")
+    out = torch.empty((1, 32, 64), dtype=torch.float64, device="cuda")
+    with pytest.raises(RuntimeError):
+        plan.filter(g, cov, out)

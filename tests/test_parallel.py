@@ -100,3 +100,86 @@ def test_row_strips_reproduce_full_image(world):
     for rank, ok_blk, y0, y1, res in got:
         assert ok_blk, rank
         assert torch.equal(res, ref[0, y0:y1]), rank
+
+
+class _ScanStandIn:
+    """Stand-in for a bsf.Plan in GLOBAL-mode pre-integration: the running-sum
+    levels computed by plain loops on CPU int64 tensors (the definition
+    G(x, y) = V(x, y) + G(x - sx, y - sy), zero state outside the strip's
+    domain unless a carry row supplies it)."""
+
+    STEPS = [(1, 2), (2, 1), (-1, 2), (-2, 1)]  # Theta' order
+
+    class _Geo:
+        pass
+
+    def __init__(self, W, P, rows, order):
+        self.geometry = self._Geo()
+        self.geometry.nbases, self.geometry.g_height, self.geometry.g_width = 1, rows, W + 2 * P
+        self.P = P
+
+        class _D:
+            pass
+        self.desc = _D()
+        self.desc.batch, self.desc.channels, self.desc.order = 1, 1, order
+
+    def scan_step(self, slot, level):
+        return self.STEPS[level % 4]
+
+    def scan_level(self, slot, level, f, g, carry=None, exact=True, stream=None):
+        sx, sy = self.STEPS[level % 4]
+        GH, GW = self.geometry.g_height, self.geometry.g_width
+        gv = g.view(GH, GW)
+        if level == 0:
+            gv.zero_()
+            gv[:f.shape[-2], self.P:self.P + f.shape[-1]] = f.reshape(f.shape[-2], f.shape[-1]).to(torch.int64)
+        for y in range(GH):
+            for x in range(GW):
+                px, py = x - sx, y - sy
+                if 0 <= px < GW:
+                    if py >= 0:
+                        gv[y, x] += gv[py, px]
+                    elif carry is not None:
+                        gv[y, x] += carry.view(sy, GW)[py + sy, px]
+
+
+def _global_worker(rank, world, port, H, W, P, Pb, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gen = torch.Generator().manual_seed(3)
+        img = torch.randint(0, 256, (H, W), generator=gen, dtype=torch.uint8)
+        st = PL.global_strip(H, Pb, rank, world, unit=4)
+        plan = _ScanStandIn(W, P, st.Y1 - st.Y0, order=1)
+        g = torch.zeros((st.Y1 - st.Y0) * (W + 2 * P), dtype=torch.int64)
+        PL.preintegrate_global_strips(plan, img[st.Y0:st.Y0 + st.height], g, st)
+        q.put((rank, st.Y0, st.Y1, g.view(st.Y1 - st.Y0, W + 2 * P)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_global_mode_carry_chain_gloo():
+    """SURVEY 8(e) GLOBAL mode over a gloo rank chain (world 3): the strips'
+    running sums, with the scan carries sent down the chain, equal the
+    one-strip computation exactly."""
+    H, W, P, Pb, world = 22, 9, 3, 5, 3
+    gen = torch.Generator().manual_seed(3)
+    img = torch.randint(0, 256, (H, W), generator=gen, dtype=torch.uint8)
+    ref_plan = _ScanStandIn(W, P, H + Pb, order=1)
+    ref = torch.zeros((H + Pb) * (W + 2 * P), dtype=torch.int64)
+    PL.preintegrate_strip(ref_plan, img, ref, recv_carry=lambda *a: None, send_carry=lambda *a: None)
+    ref = ref.view(H + Pb, W + 2 * P)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_global_worker, args=(r, world, port, H, W, P, Pb, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == 0 and res[-1][2] == H + Pb
+    for rank, Y0, Y1, g in res:
+        assert torch.equal(g, ref[Y0:Y1]), "rank %d rows [%d, %d) differ" % (rank, Y0, Y1)
