@@ -100,6 +100,9 @@ typedef struct {
     int nbases;              /* running-sum sets per image: 2 for BSF_DUAL, else 1             */
     size_t g_bytes;          /* bytes of the pre-integrated buffer bsf_preintegrate writes    */
     size_t g_exact_bytes;    /* bytes of the bit-exact int64 buffer (u8 input only, else 0)   */
+    int super_tile;          /* BSF_ANCHOR_TILE: side of the super-tiles the running sums are
+                              * anchored on (32 or 64, larger for large max_sigma); row strips
+                              * that must reproduce a one-GPU run align to it                */
 } bsf_geometry;
 
 typedef struct {

@@ -39,7 +39,7 @@ class bsf_plan_desc(ctypes.Structure):
 class bsf_geometry(ctypes.Structure):
     _fields_ = [("margin_x", ctypes.c_int), ("margin_y", ctypes.c_int), ("g_width", ctypes.c_int),
                 ("g_height", ctypes.c_int), ("nbases", ctypes.c_int), ("g_bytes", ctypes.c_size_t),
-                ("g_exact_bytes", ctypes.c_size_t)]
+                ("g_exact_bytes", ctypes.c_size_t), ("super_tile", ctypes.c_int)]
 
 
 class bsf_stats(ctypes.Structure):

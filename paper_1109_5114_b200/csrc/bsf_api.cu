@@ -39,6 +39,7 @@ struct bsf_plan_s {
     double2 *tile_scratch = nullptr;
     size_t tile_cap = 0;
     int tile_nslots = 0;
+    int stile = 32;                // fused path: super-tile side
     bool fused = false;
     unsigned long long *prof = nullptr;  // phase cycles of the fused kernel (diagnostics)
     double2 *fbuf = nullptr;             // fused path: per-CTA tap values
@@ -322,6 +323,17 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     g.GW = g.W + 2 * g.P;
     g.GH = g.H + g.Pb;
     g.nimg = d.batch * d.channels;
+    // super-tile of the fused path: the halo domain per super-tile grows with
+    // the reach E = max_sigma sqrt(24 r); at order 1, 64 x 64 super-tiles
+    // amortise it over 4x the pixels once E is large (config 3: +33 %); at
+    // r >= 2 the larger domains push pixels to the double-double fallback
+    // (BSF_STILE = 32 / 64 overrides, diagnostics)
+    {
+        const double E = (double)d.max_sigma * sqrt(24.0 * d.order);
+        p->stile = (d.order == 1 && E > BSF_STILE64_REACH) ? 64 : 32;  // r >= 2: larger domains cost precision
+        const char *env = getenv("BSF_STILE");
+        if (env && (atoi(env) == 32 || atoi(env) == 64)) p->stile = atoi(env);
+    }
     g.nbases = d.basis == BSF_DUAL ? 2 : 1;
     p->bases[0] = d.basis == BSF_DUAL ? BSF_THETA : d.basis;
     p->bases[1] = BSF_THETA_PRIME;
@@ -372,6 +384,7 @@ extern "C" bsf_status bsf_plan_geometry(bsf_plan_t p, bsf_geometry *geom) {
     geom->nbases = p->geo.nbases;
     geom->g_bytes = g_bytes(p);
     geom->g_exact_bytes = p->d.in_dtype == BSF_U8 ? g_bytes(p) / 2 : 0;
+    geom->super_tile = p->stile;
     return BSF_OK;
 }
 
@@ -490,7 +503,7 @@ static bsf_status ensure_tile_ws(bsf_plan_s *p) {
     if (p->tile_scratch) return BSF_OK;
     int mask = p->d.basis == BSF_DUAL ? 3 : (1 << p->d.basis);
     p->fused = use_fused(p);
-    p->tile_cap = tile_capacity(p->d.order, p->d.max_sigma, p->host_luts, mask, p->fused ? 2 * TILE : TILE);
+    p->tile_cap = tile_capacity(p->d.order, p->d.max_sigma, p->host_luts, mask, p->fused ? p->stile : TILE);
     p->tile_nslots = p->fused ? fused_slots() : tile_slots();
     void *q;
     size_t bytes = (size_t)p->tile_nslots * (p->fused ? NPLANE_MAX : 2) * p->tile_cap * sizeof(double2);
@@ -531,6 +544,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.stats = p->stats;
     a.prof = p->prof;
     a.fbuf = p->fbuf;
+    a.stile = p->stile;
     // BSF_SPLIT_TOL (environment, diagnostics): override the fallback threshold
     const char *tol = getenv("BSF_SPLIT_TOL");
     a.split_tol = tol ? atof(tol) : BSF_SPLIT_TOL_DEFAULT;

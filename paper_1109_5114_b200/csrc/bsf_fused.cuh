@@ -114,13 +114,14 @@ __device__ __forceinline__ double2 load_split(const double2 *__restrict__ G, int
     return inside ? v : make_double2(0.0, 0.0);
 }
 
-// Halo domain of a super-tile (as tile_domain, for STILE x STILE outputs).
-__device__ __forceinline__ TileDomain fused_domain(const LutBasis &L, int R, int x0, int y0, int EX, int EY) {
+// Halo domain of a super-tile (as tile_domain, for ST x ST outputs).
+__device__ __forceinline__ TileDomain fused_domain(const LutBasis &L, int R, int x0, int y0, int EX, int EY,
+                                                   int ST) {
     TileDomain d;
     d.X0 = x0 - EX + L.wxmin - 2 * R - 1;  // zero-scale lattice difference reaches back R|s_x| <= 2R
-    const int X1 = x0 + STILE - 1 + EX + L.wxmax + 2 * R + 1;
+    const int X1 = x0 + ST - 1 + EX + L.wxmax + 2 * R + 1;
     d.Y0 = y0 - EY;  // no kernel support above: zero state (reads above hit the zero pad rows)
-    const int Y1 = y0 + STILE - 1 + EY + L.wymax + 1;
+    const int Y1 = y0 + ST - 1 + EY + L.wymax + 1;
     d.NX = X1 - d.X0 + 1;
     d.NY = Y1 - d.Y0 + 1;
     return d;
@@ -726,7 +727,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         ph_t = t_;                                            \
     }
     double2 *scr = a.scratch + (size_t)blockIdx.x * NPLANE * a.cap;
-    const int nstx = (a.W + STILE - 1) / STILE, nsty = (a.H + STILE - 1) / STILE;
+    // super-tile of ST x ST pixels = SQ x SQ sub-tiles of TILE x TILE (ST = 32 or 64, per plan)
+    const int ST = a.stile, SQ = ST / TILE, NQ = SQ * SQ;
+    const int nstx = (a.W + ST - 1) / ST, nsty = (a.H + ST - 1) / ST;
     const int stiles_per_img = nstx * nsty;
     const int nitems = a.pts ? a.npts : stiles_per_img * a.nimg;
     const size_t ipl = (size_t)a.H * a.W;
@@ -750,21 +753,21 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (a.pts) {
             img = a.pts[3 * item];
             const int px = a.pts[3 * item + 1], py = a.pts[3 * item + 2];
-            X0s = px & ~(STILE - 1);
-            Y0s = py & ~(STILE - 1);
-            qwant = ((px - X0s) >= TILE ? 1 : 0) + ((py - Y0s) >= TILE ? 2 : 0);
+            X0s = px & ~(ST - 1);
+            Y0s = py & ~(ST - 1);
+            qwant = (px - X0s) / TILE + SQ * ((py - Y0s) / TILE);
             want = (px & (TILE - 1)) + TILE * (py & (TILE - 1));
         } else {
             img = item / stiles_per_img;
             const int rem = item % stiles_per_img;
-            X0s = (rem % nstx) * STILE;
-            Y0s = (rem / nstx) * STILE;
+            X0s = (rem % nstx) * ST;
+            Y0s = (rem / nstx) * ST;
         }
 
         if (a.cov_mode == COV_ISO && !(a.sigma2[img / a.channels] > 0.0)) {
             // Algorithm 1 with sigma_b = 0: the isotropic pass is the identity
-            for (int q = 0; q < 4; ++q) {
-                const int x = X0s + TILE * (q & 1) + (tid % TILE), y = Y0s + TILE * (q >> 1) + tid / TILE;
+            for (int q = 0; q < NQ; ++q) {
+                const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
                 const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H);
                 if (mine) {
                     const double v = load_f(a, (size_t)img * ipl + (size_t)y * a.W + x);
@@ -780,8 +783,8 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         }
         // ---- 1. reach of every pixel of the super-tile (a1-a4) -------------------
 #pragma unroll 1
-        for (int q = 0; q < 4; ++q) {
-            const int x = X0s + TILE * (q & 1) + (tid % TILE), y = Y0s + TILE * (q >> 1) + tid / TILE;
+        for (int q = 0; q < NQ; ++q) {
+            const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
             if (x < a.W && y < a.H) {
                 PixelScales ps;
                 double sx, sy, th;
@@ -806,7 +809,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (tid == 0) {
             int np = 0;
             for (int b = 0; b < 2; ++b) {
-                TileDomain d = fused_domain(luts[b], R, X0s, Y0s, s_ex[b], s_ey[b]);
+                TileDomain d = fused_domain(luts[b], R, X0s, Y0s, s_ex[b], s_ey[b], ST);
                 s_dom[b][0] = d.X0;
                 s_dom[b][1] = d.Y0;
                 s_dom[b][2] = d.NX;
@@ -826,8 +829,8 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (s_bad) {
             // domain exceeds the plan's capacity: NaN for every pixel (cannot
             // happen when max_sigma bounds the covariance field)
-            for (int q = 0; q < 4; ++q) {
-                const int x = X0s + TILE * (q & 1) + (tid % TILE), y = Y0s + TILE * (q >> 1) + tid / TILE;
+            for (int q = 0; q < NQ; ++q) {
+                const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
                 const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H);
                 if (mine) {
                     const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
@@ -933,9 +936,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
 
         // ---- sub-tiles: per-pixel scales, then 4-5 ------------------------------
 #pragma unroll 1
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < NQ; ++q) {
         if (a.pts && q != qwant) continue;
-        const int x0 = X0s + TILE * (q & 1), y0 = Y0s + TILE * (q >> 1);
+        const int x0 = X0s + TILE * (q % SQ), y0 = Y0s + TILE * (q / SQ);
         {
             const int x = x0 + (tid % TILE), y = y0 + tid / TILE;
             PixelScales ps;

@@ -161,6 +161,7 @@ struct TileArgs {
     unsigned long long *prof;  // optional [8] phase cycles (bsf_debug_phase_cycles)
     double split_tol;          // relative bound above which a pixel is recomputed in double-double
     double2 *fbuf;             // fused path: per-CTA tap values [slots][fused_items<R>()]
+    int stile;                 // fused path: super-tile side (32 or 64)
 };
 constexpr int TILE = 16;
 enum { COV_PLANES = 0, COV_ISO = 1, COV_SUB = 2 };
@@ -175,7 +176,10 @@ cudaError_t launch_tile_impl(const TileArgs &a, int order, int precision, int sl
 // NPLANE_MAX planes of `cap` points per slot
 constexpr int NPLANE_MAX = 10;
 constexpr int KBITS_MIN = 20;
-constexpr double BSF_SPLIT_TOL_DEFAULT = 5e-10;  // half the fp64 parity tolerance; see TileArgs::split_tol  // tables whose exact limb would be narrower use the double-double tile kernel
+constexpr double BSF_SPLIT_TOL_DEFAULT = 5e-10;  // half the fp64 parity tolerance; see TileArgs::split_tol
+#ifndef BSF_STILE64_REACH
+#define BSF_STILE64_REACH 64.0  // reach above which the order-1 fused path uses 64 x 64 super-tiles
+#endif
 int fused_slots();
 size_t fused_fbuf_items(int order);
 cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStream_t st, const LutBasis *luts_dev,

@@ -7,7 +7,8 @@
   so each rank receives the input rows [y0 - R_s, y0) and [y1, y1 + R_s) from
   its neighbours (one NCCL send/recv pair per neighbour) and runs the
   tile-anchored kernel on its block.  Strip and halo boundaries are multiples
-  of the 32-row super-tile on which the fused kernel anchors its running sums,
+  of the super-tile (plan.geometry.super_tile rows: 32, or 64 at order 1 with a
+  large reach) on which the fused kernel anchors its running sums,
   and the halo covers a super-tile's halo domain, so every kept super-tile
   sees exactly the data and domain it sees in a single-GPU run: the outputs
   are bit-identical (tests/test_gpu_strips.py).  No scan carries are
@@ -23,7 +24,7 @@ from dataclasses import dataclass
 
 import torch
 
-TILE = 32  # the fused kernel's super-tile (bsf_fused.cuh STILE)
+TILE = 32  # the fused kernel's default super-tile (plan.geometry.super_tile: 32, or 64 at order 1 / large sigma)
 
 
 def shard_range(n: int, rank: int, world: int):
@@ -33,12 +34,12 @@ def shard_range(n: int, rank: int, world: int):
     return start, start + base + (1 if rank < extra else 0)
 
 
-def halo_rows(max_sigma: float, order: int) -> int:
+def halo_rows(max_sigma: float, order: int, tile: int = TILE) -> int:
     """Rows a super-tile's halo domain reaches beyond it (tap reach bound
     sigma_max sqrt(24 r) plus the interpolation window, <= 6r + 2 rows),
-    rounded up to whole super-tiles."""
+    rounded up to whole super-tiles of side `tile`."""
     rs = int(math.ceil(max_sigma * math.sqrt(24.0 * order))) + 6 * order + 4
-    return TILE * ((rs + TILE - 1) // TILE)
+    return tile * ((rs + tile - 1) // tile)
 
 
 @dataclass
@@ -50,6 +51,7 @@ class Strip:
     b0: int      # first row of the local block (input incl. halo)
     b1: int      # one past the last row of the local block
     halo: int
+    tile: int = TILE  # super-tile side the strips align to
 
     @property
     def rows(self):
@@ -61,13 +63,13 @@ class Strip:
         return slice(self.y0 - self.b0, self.y1 - self.b0)
 
 
-def strip_plan(H: int, rank: int, world: int, halo: int) -> Strip:
-    """Row strips aligned to the tile grid (every strip but the last has a
-    multiple of 16 rows)."""
-    ntiles = (H + TILE - 1) // TILE
+def strip_plan(H: int, rank: int, world: int, halo: int, tile: int = TILE) -> Strip:
+    """Row strips aligned to the super-tile grid (side `tile` = the plan's
+    geometry.super_tile; every strip but the last has a multiple of it)."""
+    ntiles = (H + tile - 1) // tile
     t0, t1 = shard_range(ntiles, rank, world)
-    y0, y1 = t0 * TILE, min(H, t1 * TILE)
-    return Strip(rank, world, y0, y1, max(0, y0 - halo), min(H, y1 + halo), halo)
+    y0, y1 = t0 * tile, min(H, t1 * tile)
+    return Strip(rank, world, y0, y1, max(0, y0 - halo), min(H, y1 + halo), halo, tile)
 
 
 def exchange_halos(own: torch.Tensor, strip: Strip, H: int, group=None) -> torch.Tensor:
@@ -86,13 +88,13 @@ def exchange_halos(own: torch.Tensor, strip: Strip, H: int, group=None) -> torch
     top = strip.y0 - strip.b0          # rows needed from rank - 1
     bot = strip.b1 - strip.y1          # rows needed from rank + 1
     if r > 0:
-        prev = strip_plan(H, r - 1, n, strip.halo)
+        prev = strip_plan(H, r - 1, n, strip.halo, strip.tile)
         send_up = prev.b1 - prev.y1    # rows rank-1 needs from me
         ops.append(dist.P2POp(dist.isend, own[..., :send_up, :].contiguous(), r - 1, group))
         recv_top = block.new_empty(lead + (top, W))
         ops.append(dist.P2POp(dist.irecv, recv_top, r - 1, group))
     if r < n - 1:
-        nxt = strip_plan(H, r + 1, n, strip.halo)
+        nxt = strip_plan(H, r + 1, n, strip.halo, strip.tile)
         send_dn = nxt.y0 - nxt.b0      # rows rank+1 needs from me
         ops.append(dist.P2POp(dist.isend, own[..., own.shape[-2] - send_dn:, :].contiguous(), r + 1, group))
         recv_bot = block.new_empty(lead + (bot, W))

@@ -121,3 +121,29 @@ def test_macs_counter_is_the_algorithmic_work():
             reg = lut.region_of(tabs[b], Dx - math.floor(Dx), Dy - math.floor(Dy))
             want += int(v["counts"][reg]) * v["nmon"]
     assert got == want
+
+
+def test_super_tile_64_matches_32():
+    """Order 1 with a large reach anchors the running sums on 64 x 64
+    super-tiles (plan geometry); the whole image (ragged in both directions,
+    batch of 2) must agree with the 32 x 32 anchoring to ~1e-12, and with the
+    oracle at sampled pixels to the 1e-9 contract."""
+    w = synth.workload(3, order=1, width=300, height=170)
+    img = torch.stack([synth.make_image(w), synth.make_image(w, frame=1)])
+    cov = synth.make_cov(w)[None].expand(2, -1, -1, -1).contiguous()
+    p64 = make_plan(w, anchor=TILE, batch=2)
+    assert p64.geometry.super_tile == 64
+    a = gpu_full(p64, img, cov)
+    with _env(BSF_STILE=32):
+        p32 = make_plan(w, anchor=TILE, batch=2)
+        assert p32.geometry.super_tile == 32
+        b = gpu_full(p32, img, cov)
+    rel = ((a - b).abs() / b.abs()).max()
+    assert float(rel) <= 1e-12, float(rel)
+    from gpu_util import oracle_points
+    pts = synth.sample_points(w, 40, seed=9)
+    xs, ys = pts[:, 1].numpy(), pts[:, 2].numpy()
+    ref = oracle_points(img[0].numpy(), cov[0].numpy(), xs, ys, policy=w.basis, r=1)[0]
+    got = a[0].cpu().numpy()[ys, xs]
+    err = np.max(np.abs(got - ref) / np.abs(ref))
+    assert err <= 1e-9, err

@@ -26,9 +26,11 @@ def _field(H, W, smax):
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-@pytest.mark.parametrize("order,policy", [(2, bsf.BSF_DUAL), (3, bsf.BSF_THETA)])
-def test_strips_bitwise_equal_single_gpu(world, order, policy):
-    H, W, smax = 352, 200, 5.0
+@pytest.mark.parametrize("order,policy,smax", [(2, bsf.BSF_DUAL, 5.0), (3, bsf.BSF_THETA, 5.0),
+                                               (1, bsf.BSF_DUAL, 16.0)])
+def test_strips_bitwise_equal_single_gpu(world, order, policy, smax):
+    """(order 1, sigma 16: the plan anchors on 64 x 64 super-tiles)"""
+    H, W = 352, 200
     w = synth.workload(5, width=W, height=H, max_sigma=smax, order=order)
     img = synth.make_image(w).cuda()
     cov = _field(H, W, smax).cuda()
@@ -38,11 +40,14 @@ def test_strips_bitwise_equal_single_gpu(world, order, policy):
                         anchor=bsf.BSF_ANCHOR_TILE)
 
     full = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
-    plan(H).run(img[None].contiguous(), cov.contiguous(), full)
-    halo = PL.halo_rows(smax, order)
+    p_full = plan(H)
+    tile = p_full.geometry.super_tile
+    assert tile == (64 if order == 1 else 32)
+    p_full.run(img[None].contiguous(), cov.contiguous(), full)
+    halo = PL.halo_rows(smax, order, tile)
     for rank in range(world):
-        st = PL.strip_plan(H, rank, world, halo)
-        assert st.y0 % PL.TILE == 0 and st.b0 % PL.TILE == 0
+        st = PL.strip_plan(H, rank, world, halo, tile)
+        assert st.y0 % tile == 0 and st.b0 % tile == 0
         f_blk = img[st.b0:st.b1]                     # = exchange_halos(own rows)
         cov_blk = torch.ones((3, st.rows, W), dtype=torch.float32, device="cuda")
         cov_blk[:, st.out_slice] = cov[:, st.y0:st.y1]  # halo outputs are discarded
