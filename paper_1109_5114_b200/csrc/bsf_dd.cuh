@@ -44,6 +44,15 @@ __device__ __forceinline__ dd dd_add(dd a, dd b) {
     return fast_two_sum(s.hi, s.lo);
 }
 
+// addition for operands of the same sign (no cancellation): 11 flops instead
+// of 20, relative error <= 3u^2 (QD's "sloppy" add is accurate in this case).
+// Used by the running sums of non-negative images.
+__device__ __forceinline__ dd dd_add_same_sign(dd a, dd b) {
+    dd s = two_sum(a.hi, b.hi);
+    s.lo = __dadd_rn(s.lo, __dadd_rn(a.lo, b.lo));
+    return fast_two_sum(s.hi, s.lo);
+}
+
 __device__ __forceinline__ dd dd_neg(dd a) { return {-a.hi, -a.lo}; }
 __device__ __forceinline__ dd dd_sub(dd a, dd b) { return dd_add(a, dd_neg(b)); }
 

@@ -608,7 +608,10 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
     const int tid = threadIdx.x;
     const int nh = basis == BASIS_THETA ? R : 0;  // horizontal levels, done first
     const int L = 4 * R - nh;                    // levels in the sweep
-    if ((size_t)3 * L * NX * sizeof(double2) > ring_bytes) return false;
+    // levels per pass: as many as the ring holds (large halo domains take
+    // several passes, each reading the previous pass' last level from G)
+    const int LC = min(L, (int)(ring_bytes / ((size_t)3 * NX * sizeof(double2))));
+    if (LC < 1) return false;
     const size_t ipl = (size_t)a.H * a.W;
     auto fval = [&](int x, int y) -> double {
         const int X = X0 + x, Y = Y0 + y;
@@ -616,15 +619,50 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
         const size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
         return load_f(a, o);
     };
+    // a non-negative image makes every running sum non-negative: the cheaper
+    // same-sign double-double addition is then exact to 3u^2 (u8 input always;
+    // float input checked over the domain)
+    bool same_sign = a.in_u8 != 0;
+    if (!same_sign) {
+        int neg = 0;
+        const int xa = max(X0, 0), xb = min(X0 + NX, a.W), ya = max(Y0, 0), yb = min(Y0 + NY, a.H);
+        for (int Y = ya; Y < yb; ++Y)
+            for (int X = xa + tid; X < xb; X += FT) neg |= load_f(a, (size_t)img * ipl + (size_t)Y * a.W + X) < 0.0;
+        same_sign = !__syncthreads_or(neg);
+    }
+    auto add = [&](dd u, dd v) -> dd { return same_sign ? dd_add_same_sign(u, v) : dd_add(u, v); };
+    // u8 input: the running sums are integers, and a level whose values stay
+    // below 2^53 (255 x the product of the line lengths so far) is exact in
+    // plain fp64 -- one DADD instead of a double-double addition.  Bit k of
+    // exact_h / exact_v: horizontal level k / sweep level k is exact.
+    unsigned exact_h = 0u, exact_v = 0u;
+    if (a.in_u8) {
+        double bound = 255.0;
+        int k = 0;
+        for (int j = 0; j < nh; ++j, ++k) {
+            bound *= NX;
+            if (bound < 0x1p53) exact_h |= 1u << j;
+        }
+        k = 0;
+        for (int rep = 0; rep < R; ++rep)
+            for (int lv = 0; lv < 4; ++lv) {
+                const int sy = c_scan_order[basis][lv][1];
+                if (sy == 0) continue;
+                bound *= (double)(NY / sy + 1);
+                if (bound < 0x1p53) exact_v |= 1u << k;
+                ++k;
+            }
+    }
     if (nh) {
         for (int y = tid; y < NY; y += FT) {
             dd acc[R];
 #pragma unroll
             for (int k = 0; k < R; ++k) acc[k] = {0.0, 0.0};
             for (int x = 0; x < NX; ++x) {
-                acc[0] = dd_add_d(acc[0], fval(x, y));
+                acc[0] = (exact_h & 1u) ? dd{acc[0].hi + fval(x, y), 0.0} : dd_add_d(acc[0], fval(x, y));
 #pragma unroll
-                for (int k = 1; k < R; ++k) acc[k] = dd_add(acc[k], acc[k - 1]);
+                for (int k = 1; k < R; ++k)
+                    acc[k] = ((exact_h >> k) & 1u) ? dd{acc[k].hi + acc[k - 1].hi, 0.0} : add(acc[k], acc[k - 1]);
                 G[(size_t)y * NX + x] = make_double2(acc[R - 1].hi, acc[R - 1].lo);
             }
         }
@@ -643,43 +681,46 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
                 ++k;
             }
     }
-    // flat (level, x) work list over the CTA; (l, x) advanced incrementally
-    const int work = L * NX;
-    const int l0 = tid / NX, x0 = tid - l0 * NX, dl = FT / NX, dx = FT - dl * NX;
-    for (int tau = 0; tau < NY + L - 1; ++tau) {
-        int l = l0, x = x0;
-        for (int i = tid; i < work; i += FT) {
-            const int y = tau - l;  // level l + 1 processes row tau - l
-            if (y >= 0 && y < NY) {
-                dd below;
-                if (l == 0) {
-                    if (nh) {
-                        const double2 t = G[(size_t)y * NX + x];
-                        below = {t.x, t.y};
+    for (int lb = 0; lb < L; lb += LC) {
+        const int Lp = min(LC, L - lb);  // levels lb .. lb + Lp - 1 in this pass
+        // flat (level, x) work list over the CTA; (l, x) advanced incrementally
+        const int work = Lp * NX;
+        const int l0 = tid / NX, x0 = tid - l0 * NX, dl = FT / NX, dx = FT - dl * NX;
+        for (int tau = 0; tau < NY + Lp - 1; ++tau) {
+            int l = l0, x = x0;
+            for (int i = tid; i < work; i += FT) {
+                const int y = tau - l;  // level lb + l processes row tau - l
+                if (y >= 0 && y < NY) {
+                    dd below;
+                    if (l == 0) {
+                        if (nh || lb > 0) {  // horizontal sums, or the previous pass' last level
+                            const double2 t = G[(size_t)y * NX + x];
+                            below = {t.x, t.y};
+                        } else {
+                            below = {fval(x, y), 0.0};
+                        }
                     } else {
-                        below = {fval(x, y), 0.0};
+                        const double2 t = ring[((size_t)(l - 1) * 3 + y % 3) * NX + x];
+                        below = {t.x, t.y};
                     }
-                } else {
-                    const double2 t = ring[((size_t)(l - 1) * 3 + y % 3) * NX + x];
-                    below = {t.x, t.y};
+                    const int yp = y - lsy[lb + l], xp = x - lsx[lb + l];
+                    if (yp >= 0 && xp >= 0 && xp < NX) {
+                        const double2 t = ring[((size_t)l * 3 + yp % 3) * NX + xp];
+                        below = ((exact_v >> (lb + l)) & 1u) ? dd{below.hi + t.x, 0.0} : add(below, {t.x, t.y});
+                    }
+                    const double2 v = make_double2(below.hi, below.lo);
+                    ring[((size_t)l * 3 + y % 3) * NX + x] = v;
+                    if (l == Lp - 1) G[(size_t)y * NX + x] = v;
                 }
-                const int yp = y - lsy[l], xp = x - lsx[l];
-                if (yp >= 0 && xp >= 0 && xp < NX) {
-                    const double2 t = ring[((size_t)l * 3 + yp % 3) * NX + xp];
-                    below = dd_add(below, {t.x, t.y});
+                l += dl;
+                x += dx;
+                if (x >= NX) {
+                    x -= NX;
+                    ++l;
                 }
-                const double2 v = make_double2(below.hi, below.lo);
-                ring[((size_t)l * 3 + y % 3) * NX + x] = v;
-                if (l == L - 1) G[(size_t)y * NX + x] = v;
             }
-            l += dl;
-            x += dx;
-            if (x >= NX) {
-                x -= NX;
-                ++l;
-            }
+            __syncthreads();
         }
-        __syncthreads();
     }
     return true;
 }
