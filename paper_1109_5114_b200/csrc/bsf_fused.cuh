@@ -619,17 +619,10 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
         const size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
         return load_f(a, o);
     };
-    // a non-negative image makes every running sum non-negative: the cheaper
-    // same-sign double-double addition is then exact to 3u^2 (u8 input always;
-    // float input checked over the domain)
-    bool same_sign = a.in_u8 != 0;
-    if (!same_sign) {
-        int neg = 0;
-        const int xa = max(X0, 0), xb = min(X0 + NX, a.W), ya = max(Y0, 0), yb = min(Y0 + NY, a.H);
-        for (int Y = ya; Y < yb; ++Y)
-            for (int X = xa + tid; X < xb; X += FT) neg |= load_f(a, (size_t)img * ipl + (size_t)Y * a.W + X) < 0.0;
-        same_sign = !__syncthreads_or(neg);
-    }
+    // a u8 image makes every running sum non-negative: the cheaper same-sign
+    // double-double addition is then exact to 3u^2 (float input may be signed;
+    // scanning the domain for signs cost more than it saved on config 2)
+    const bool same_sign = a.in_u8 != 0;
     auto add = [&](dd u, dd v) -> dd { return same_sign ? dd_add_same_sign(u, v) : dd_add(u, v); };
     // u8 input: the running sums are integers, and a level whose values stay
     // below 2^53 (255 x the product of the line lengths so far) is exact in
