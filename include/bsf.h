@@ -213,6 +213,20 @@ bsf_status bsf_run(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void
 bsf_status bsf_run_alg1(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, double *sigma2_out,
                         void *stream);
 
+/* Generalised covariance splitting (the repeated
+ * filtering of PAPER.md:161-166 made space-variant through Algorithm 1's
+ * split, composed by Proposition 2):
+ * `passes` = n >= 2 passes of the plan's order,
+ *   passes 1 .. n-1: the isotropic box spline of covariance (B_b / n) I,
+ *   pass n:          the space-variant box spline of C(p) - ((n-1) B_b / n) I,
+ * with B_b = 2 sigma_b^2 the smallest bound (9) of covariance field b
+ * (R22).  n = 2 is bsf_run_alg1 exactly; for a constant isotropic
+ * field every pass has covariance C / n (the order-n kernel up to the
+ * intermediate sampling).  Arguments and errors as bsf_run_alg1 (BSF_EINVAL
+ * for n outside 2..16); a second float64 work image is allocated for n > 2. */
+bsf_status bsf_run_split(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, int passes,
+                         double *sigma2_out, void *stream);
+
 /* End to end from HOST buffers (pinned for overlap): copies f and cov to the
  * device, runs bsf_run, copies out back, all on `stream`.  Returns after
  * enqueueing; synchronise the stream before reading out_host.               */

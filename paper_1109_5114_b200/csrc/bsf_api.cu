@@ -44,6 +44,7 @@ struct bsf_plan_s {
     unsigned long long *prof = nullptr;  // phase cycles of the fused kernel (diagnostics)
     double2 *fbuf = nullptr;             // fused path: per-CTA tap values
     double *alg1_work = nullptr;         // Algorithm 1: float64 intermediate image
+    double *alg1_work2 = nullptr;        // generalised splitting: second intermediate (ping-pong)
     double *alg1_sigma2 = nullptr;       // Algorithm 1: sigma_b^2 per covariance field (+ reduction bits)
     int *tile_counter = nullptr;
     long long nlaunch = 0;
@@ -545,6 +546,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.prof = p->prof;
     a.fbuf = p->fbuf;
     a.stile = p->stile;
+    a.sigma2_scale = 1.0;
     // BSF_SPLIT_TOL (environment, diagnostics): override the fallback threshold
     const char *tol = getenv("BSF_SPLIT_TOL");
     a.split_tol = tol ? atof(tol) : BSF_SPLIT_TOL_DEFAULT;
@@ -598,18 +600,12 @@ extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void
     return bsf_filter(p, p->g_ws, cov, out, stream);
 }
 
-extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov, void *out, double *sigma2_out,
-                                   void *stream) {
-    if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
-    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
-    bsf_status s = ensure_tile_ws(p);
-    if (s != BSF_OK) return s;
-    if (!p->fused) return set_err(BSF_EUNSUPPORTED, "Algorithm 1 runs on the exact split path (order <= 3)");
+static bsf_status ensure_alg1_ws(bsf_plan_s *p, bool two) {
     const Geometry &g = p->geo;
+    const size_t img_bytes = (size_t)g.nimg * g.H * g.W * sizeof(double);
+    void *q;
     if (!p->alg1_work) {
-        void *q;
-        if (cudaMalloc(&q, (size_t)g.nimg * g.H * g.W * sizeof(double)) != cudaSuccess)
-            return set_err(BSF_ENOMEM, "Algorithm 1 work image");
+        if (cudaMalloc(&q, img_bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "Algorithm 1 work image");
         p->dev_allocs.push_back(q);
         p->alg1_work = (double *)q;
         if (cudaMalloc(&q, 2 * (size_t)p->d.batch * sizeof(double)) != cudaSuccess)
@@ -617,28 +613,68 @@ extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov,
         p->dev_allocs.push_back(q);
         p->alg1_sigma2 = (double *)q;
     }
+    if (two && !p->alg1_work2) {
+        if (cudaMalloc(&q, img_bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "splitting work image");
+        p->dev_allocs.push_back(q);
+        p->alg1_work2 = (double *)q;
+    }
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov, void *out, int passes,
+                                    double *sigma2_out, void *stream) {
+    if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
+    if (passes < 2 || passes > 16) return set_err(BSF_EINVAL, "passes must be 2..16");
+    bsf_status s = ensure_tile_ws(p);
+    if (s != BSF_OK) return s;
+    if (!p->fused) return set_err(BSF_EUNSUPPORTED, "covariance splitting runs on the exact split path (order <= 3)");
+    s = ensure_alg1_ws(p, passes > 2);
+    if (s != BSF_OK) return s;
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
-    CUDA_TRY(launch_alg1_sigma2((const float *)cov, p->d.batch, g.W, g.H, p->d.basis, p->d.clamp, p->alg1_sigma2, st,
-                                &p->nlaunch));
-    // pass 1: the isotropic box spline of covariance sigma_b^2 I, into the work image
-    TileArgs a1 = tile_args(p, f, cov, p->alg1_work);
-    a1.out_f32 = 0;
-    a1.cov_mode = COV_ISO;
-    a1.sigma2 = p->alg1_sigma2;
-    CUDA_TRY(launch_tile(p, a1, st));
-    // pass 2: the space-variant box spline of covariance C - sigma_b^2 I on it
-    TileArgs a2 = tile_args(p, p->alg1_work, cov, out);
-    a2.in_u8 = 0;
-    a2.in_f64 = 1;
-    a2.cov_mode = COV_SUB;
-    a2.sigma2 = p->alg1_sigma2;
-    CUDA_TRY(launch_tile(p, a2, st));
+    // sigma_b^2 = half the smallest bound (9) of the field (R21): the bound is 2 sigma_b^2
+    CUDA_TRY(launch_alg1_sigma2((const float *)cov, p->d.batch, p->geo.W, p->geo.H, p->d.basis, p->d.clamp,
+                                p->alg1_sigma2, st, &p->nlaunch));
+    // passes - 1 isotropic passes of (2 sigma_b^2 / n) I each, ping-ponging
+    // through float64 work images, then the space-variant residual
+    // C - (n - 1)(2 sigma_b^2 / n) I (R22; n = 2 is Algorithm 1)
+    const double n = passes;
+    const void *src = f;
+    bool src_f64 = false;
+    double *bufs[2] = {p->alg1_work, p->alg1_work2};
+    for (int i = 0; i < passes - 1; ++i) {
+        double *dst = bufs[i & 1];
+        TileArgs a = tile_args(p, src, cov, dst);
+        a.out_f32 = 0;
+        if (src_f64) {
+            a.in_u8 = 0;
+            a.in_f64 = 1;
+        }
+        a.cov_mode = COV_ISO;
+        a.sigma2 = p->alg1_sigma2;
+        a.sigma2_scale = 2.0 / n;
+        CUDA_TRY(launch_tile(p, a, st));
+        src = dst;
+        src_f64 = true;
+    }
+    TileArgs a = tile_args(p, src, cov, out);
+    a.in_u8 = 0;
+    a.in_f64 = 1;
+    a.cov_mode = COV_SUB;
+    a.sigma2 = p->alg1_sigma2;
+    a.sigma2_scale = 2.0 * (n - 1.0) / n;
+    CUDA_TRY(launch_tile(p, a, st));
     if (sigma2_out) {
         CUDA_TRY(cudaStreamSynchronize(st));
         CUDA_TRY(cudaMemcpy(sigma2_out, p->alg1_sigma2, p->d.batch * sizeof(double), cudaMemcpyDeviceToHost));
     }
     return BSF_OK;
+}
+
+extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov, void *out, double *sigma2_out,
+                                   void *stream) {
+    return bsf_run_split(p, f, cov, out, 2, sigma2_out, stream);
 }
 
 extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void *cov_host, void *out_host,

@@ -166,15 +166,16 @@ __device__ __forceinline__ int cls_region(const ClsTables &T, int b, double x, d
 }
 
 // (sigma_x, sigma_y, theta) of a pixel under the covariance mode of the launch
-// (Algorithm 1): the planes, sigma_b^2 I (the global
-// isotropic pass, theta = 0), or C - sigma_b^2 I (same eigenvectors, eigenvalues
-// lowered by sigma_b^2: PAPER.md:228-231)
+// (Algorithm 1): the planes, s sigma_b^2 I (the global
+// isotropic pass, theta = 0), or C - s sigma_b^2 I (same eigenvectors,
+// eigenvalues lowered: PAPER.md:228-231); s = sigma2_scale (1 for Algorithm 1,
+// the generalised splitting's shares otherwise, R22)
 __device__ __forceinline__ void load_cov(const TileArgs &a, int img, int x, int y, double &sx, double &sy,
                                          double &th) {
     const size_t ipl = (size_t)a.H * a.W;
     const int b = img / a.channels;
     if (a.cov_mode == COV_ISO) {
-        sx = sy = sqrt(a.sigma2[b]);
+        sx = sy = sqrt(a.sigma2[b] * a.sigma2_scale);
         th = 0.0;
         return;
     }
@@ -183,7 +184,7 @@ __device__ __forceinline__ void load_cov(const TileArgs &a, int img, int x, int 
     sy = __ldg(cv + ipl);
     th = __ldg(cv + 2 * ipl);
     if (a.cov_mode == COV_SUB) {
-        const double s2 = a.sigma2[b];
+        const double s2 = a.sigma2[b] * a.sigma2_scale;
         sx = sqrt(fmax(sx * sx - s2, 0.0));
         sy = sqrt(fmax(sy * sy - s2, 0.0));
     }

@@ -147,6 +147,7 @@ struct TileArgs {
     int in_f64;             // input image is float64 (Algorithm 1's second pass)
     int cov_mode;           // COV_PLANES, COV_ISO (sigma_b^2 I), COV_SUB (C - sigma_b^2 I)
     const double *sigma2;   // [batch] sigma_b^2 of Algorithm 1 (COV_ISO / COV_SUB)
+    double sigma2_scale;    // multiplies sigma2 (1 for Algorithm 1; the split shares of bsf_run_split)
     const void *f;          // [nimg][H][W]
     const float *cov;       // [batch][3][H][W]
     void *out;              // [nimg][H][W] (or float64[npts] with pts)

@@ -122,3 +122,46 @@ def test_alg1_closer_to_the_gaussian(policy):
     err = lambda k: float(np.linalg.norm(k - gauss) / np.linalg.norm(gauss))
     e_plain, e_alg1 = err(plain[0].cpu().numpy()), err(alg1[0].cpu().numpy())
     assert e_alg1 < 0.75 * e_plain, (e_plain, e_alg1)
+
+
+def test_split_two_passes_is_algorithm1():
+    """bsf_run_split with n = 2 is Algorithm 1, bit for bit."""
+    H, W = 34, 40
+    w, img, cov = _small_smooth(H, W, 3.5, seed=22)
+    plan = make_plan(w, policy=2, order=1, anchor=bsf.BSF_ANCHOR_TILE)
+    a = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    s1 = plan.run_alg1(img[None].cuda().contiguous(), cov.cuda().contiguous(), a)
+    s2 = plan.run_split(img[None].cuda().contiguous(), cov.cuda().contiguous(), b, 2)
+    torch.cuda.synchronize()
+    assert s1[0] == s2[0] and torch.equal(a, b)
+
+
+@pytest.mark.parametrize("policy,r,n", [(0, 1, 3), (2, 1, 4), (2, 2, 3)])
+def test_split_matches_multi_stage_oracle(policy, r, n):
+    """n - 1 isotropic passes of (B/n) I then C - ((n-1) B/n) I (R22),
+    against the oracle applied stage by stage to every pixel (float64
+    intermediates; Proposition 2 composes them)."""
+    H, W = 30, 34
+    w, img, cov = _small_smooth(H, W, 3.5, seed=23)
+    plan = make_plan(w, policy=policy, order=r, anchor=bsf.BSF_ANCHOR_TILE)
+    out = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    sig = plan.run_split(img[None].cuda().contiguous(), cov.cuda().contiguous(), out, n)
+    torch.cuda.synchronize()
+    c = cov.numpy()
+    bound = float(_bound9(c, policy).min())
+    assert abs(2.0 * sig[0] - bound) <= 1e-12 * bound
+    ys, xs = np.mgrid[0:H, 0:W]
+    xs, ys = xs.ravel(), ys.ravel()
+    g = img.numpy()
+    s = math.sqrt(2.0 * sig[0] / n)
+    for _ in range(n - 1):
+        g, *_ = O.filter_points(g, xs, ys, s, s, 0.0, policy=policy, r=r)
+        g = g.reshape(H, W)
+    t = 2.0 * sig[0] * (n - 1) / n
+    sx = np.sqrt(np.maximum(c[0].astype(np.float64) ** 2 - t, 0.0))[ys, xs]
+    sy = np.sqrt(np.maximum(c[1].astype(np.float64) ** 2 - t, 0.0))[ys, xs]
+    ref, *_ = O.filter_points(g, xs, ys, sx, sy, c[2][ys, xs].astype(np.float64), policy=policy, r=r)
+    got = out[0].cpu().numpy().ravel()
+    assert max_rel(got, ref) <= 1e-9
+    assert plan.stats()["flags"] == 0

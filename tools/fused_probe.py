@@ -17,6 +17,7 @@ ap.add_argument("--order", type=int, default=0)
 ap.add_argument("--width", type=int, default=512)
 ap.add_argument("--height", type=int, default=512)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--split", type=int, default=0, help="bsf_run_split with this many passes (order from --order)")
 args = ap.parse_args()
 kw = {"width": args.width, "height": args.height}
 if args.order:
@@ -28,17 +29,18 @@ plan = bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" els
 img = synth.make_image(w, device=dev).contiguous()
 cov = synth.make_cov(w, device=dev).contiguous()
 out = torch.empty((1, w.height, w.width), dtype=torch.float64, device=dev)
-plan.run(img, cov, out)
+run = (lambda: plan.run_split(img, cov, out, args.split)) if args.split else (lambda: plan.run(img, cov, out))
+run()
 torch.cuda.synchronize()
 plan.stats(reset=True)
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record()
 for _ in range(args.reps):
-    plan.run(img, cov, out)
+    run()
 b.record()
 torch.cuda.synchronize()
 ms = a.elapsed_time(b) / args.reps
 st = plan.stats(reset=True)
 npx = w.width * w.height
-print("%s %dx%d r=%d: %.3f ms, %.3f Mpx/s, macs/px %.0f, dd fallback %d" % (
-    w.name, w.width, w.height, w.order, ms, npx / ms / 1e3, st["macs"] / max(st["pixels"], 1), st["double_double"]))
+print("%s %dx%d r=%d%s: %.3f ms, %.3f Mpx/s, macs/px %.0f, dd fallback %d" % (
+    w.name, w.width, w.height, w.order, " split n=%d" % args.split if args.split else "", ms, npx / ms / 1e3, st["macs"] / max(st["pixels"], 1), st["double_double"]))
