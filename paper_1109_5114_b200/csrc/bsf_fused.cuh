@@ -662,55 +662,66 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
         }
         __syncthreads();
     }
-    // level steps of the sweep, in scan order with the horizontal levels removed
-    int lsx[4 * R], lsy[4 * R];
+    // level steps of the sweep, in scan order with the horizontal levels removed,
+    // packed 4 bits per level in one register word (sx + 2 in bits 0-2, sy - 1
+    // in bit 3): no local-memory array in the inner loop
+    unsigned long long steps = 0ull;
     {
         int k = 0;
         for (int rep = 0; rep < R; ++rep)
             for (int lv = 0; lv < 4; ++lv) {
                 const int sx = c_scan_order[basis][lv][0], sy = c_scan_order[basis][lv][1];
                 if (sy == 0) continue;
-                lsx[k] = sx;
-                lsy[k] = sy;
+                steps |= (unsigned long long)((sx + 2) | ((sy - 1) << 3)) << (4 * k);
                 ++k;
             }
     }
     for (int lb = 0; lb < L; lb += LC) {
         const int Lp = min(LC, L - lb);  // levels lb .. lb + Lp - 1 in this pass
-        // flat (level, x) work list over the CTA; (l, x) advanced incrementally
+        const unsigned long long pst = steps >> (4 * lb);
+        // flat (level, x) work list over the CTA; (l, x) advanced incrementally;
+        // ring rows rotate mod 3: row y of level l lives in slot (l, y mod 3)
         const int work = Lp * NX;
         const int l0 = tid / NX, x0 = tid - l0 * NX, dl = FT / NX, dx = FT - dl * NX;
         for (int tau = 0; tau < NY + Lp - 1; ++tau) {
             int l = l0, x = x0;
+            int ym = (tau - l0) % 3;  // y mod 3 for y = tau - l (>= 0 when used)
+            if (ym < 0) ym += 3;
             for (int i = tid; i < work; i += FT) {
                 const int y = tau - l;  // level lb + l processes row tau - l
                 if (y >= 0 && y < NY) {
+                    const unsigned st4 = (unsigned)(pst >> (4 * l)) & 15u;
+                    const int sx = (int)(st4 & 7u) - 2, sy = (int)(st4 >> 3) + 1;
                     dd below;
                     if (l == 0) {
                         if (nh || lb > 0) {  // horizontal sums, or the previous pass' last level
-                            const double2 t = G[(size_t)y * NX + x];
+                            const double2 t = G[y * NX + x];
                             below = {t.x, t.y};
                         } else {
                             below = {fval(x, y), 0.0};
                         }
                     } else {
-                        const double2 t = ring[((size_t)(l - 1) * 3 + y % 3) * NX + x];
+                        const double2 t = ring[((l - 1) * 3 + ym) * NX + x];
                         below = {t.x, t.y};
                     }
-                    const int yp = y - lsy[lb + l], xp = x - lsx[lb + l];
+                    const int yp = y - sy, xp = x - sx;
                     if (yp >= 0 && xp >= 0 && xp < NX) {
-                        const double2 t = ring[((size_t)l * 3 + yp % 3) * NX + xp];
+                        const int ypm = ym >= sy ? ym - sy : ym - sy + 3;
+                        const double2 t = ring[(l * 3 + ypm) * NX + xp];
                         below = ((exact_v >> (lb + l)) & 1u) ? dd{below.hi + t.x, 0.0} : add(below, {t.x, t.y});
                     }
                     const double2 v = make_double2(below.hi, below.lo);
-                    ring[((size_t)l * 3 + y % 3) * NX + x] = v;
-                    if (l == Lp - 1) G[(size_t)y * NX + x] = v;
+                    ring[(l * 3 + ym) * NX + x] = v;
+                    if (l == Lp - 1) G[y * NX + x] = v;
                 }
                 l += dl;
+                ym -= dl % 3;
+                if (ym < 0) ym += 3;
                 x += dx;
                 if (x >= NX) {
                     x -= NX;
                     ++l;
+                    ym = ym == 0 ? 2 : ym - 1;
                 }
             }
             __syncthreads();
