@@ -344,9 +344,14 @@ def main():
         cyc = plan.phase_cycles()
         tot = float(sum(cyc[:6])) or 1.0
         names = ["scales", "pre_integration", "exact_split", "keys_sort", "gather", "accumulate"]
-        roof = {"bound": "fp64-tensor", "kernel": "fused_kernel (pre-integration + gather, DMMA m8n8k4)",
+        alg_bytes = npx * in_b + 12 * npx + 8 * npx  # read f + cov once, write out once
+        hbm_gbs = alg_bytes / (gat * 1e-3) / 1e9
+        roof = {"bound": "tensor", "pipe": "FP64 tensor (DMMA m8n8k4; tcgen05 has no f64 kind)",
+                "kernel": "fused_kernel (pre-integration + gather, DMMA m8n8k4)",
                 "achieved": achieved, "peak": fp["fp64_tensor_peak_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / fp["fp64_tensor_peak_tflops"], "traffic": _ncu_traffic(w.name),
+                "hbm": {"algorithmic_bytes": alg_bytes, "achieved_gbs": hbm_gbs, "peak_gbs": peaks.get("hbm_gbs"),
+                        "frac": hbm_gbs / peaks.get("hbm_gbs", 6650.0), "peak_source": src},
                 "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full "
                                   "capture (profiles/r01_c2_fused_raw.csv); algorithmic HBM bytes %d" % (
                                       npx * in_b + 12 * npx + 8 * npx),
