@@ -349,7 +349,22 @@ __device__ __forceinline__ void fused_xhorner4(const double (&Rh)[4][RowCfg<DEG>
 // the quad), compensated.  Lane l feeds and receives item l/4 + 8t of m-tile
 // t; (bxt, byt) are that item's tap base; (fxo, fyo) the fractional offset of
 // the lane's own item (shuffled to the quads for the epilogue).
-template <int DEG, int MT>
+// u8 input: every running-sum level is an integer below 255 x the product of
+// the line lengths so far (a line of step (sx, sy) has at most NY/sy + 1
+// points, a row NX); a zero-scale variant plane (1 - T_s)^R G at most 2^R
+// times that.  When this stays below 2^kbits the planes are their own exact
+// split (G1 = G, G0 = 0): no scaling pass, and a single MMA limb.
+__device__ __forceinline__ double u8_plane_bound(int basis, int R, int NX, int NY) {
+    double bound = 255.0;
+    for (int rep = 0; rep < R; ++rep)
+        for (int lv = 0; lv < 4; ++lv) {
+            const int sy = c_scan_order[basis][lv][1];
+            bound *= sy == 0 ? (double)NX : (double)(NY / sy + 1);
+        }
+    return bound;
+}
+
+template <int DEG, int MT, int LIMBS = 2>
 __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
                                             const int (&byt)[MT], double fxo, double fyo,
                                             const int2 *__restrict__ offs, const double *__restrict__ num, int nmonp,
@@ -392,7 +407,7 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
 #pragma unroll
             for (int t = 0; t < MT; ++t) {
                 dmma(C[t][0][j], aA[t].x, bA[j]);  // exact: integers below 2^53
-                dmma(C[t][1][j], aA[t].y, bA[j]);
+                if constexpr (LIMBS == 2) dmma(C[t][1][j], aA[t].y, bA[j]);  // LIMBS 1: the G0 limb is zero
             }
         if (st + 1 >= nsteps) break;
         if (st + 2 < nsteps) {
@@ -407,7 +422,7 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
 #pragma unroll
             for (int t = 0; t < MT; ++t) {
                 dmma(C[t][0][j], aB[t].x, bB[j]);
-                dmma(C[t][1][j], aB[t].y, bB[j]);
+                if constexpr (LIMBS == 2) dmma(C[t][1][j], aB[t].y, bB[j]);
             }
     }
     if constexpr (MT == 4) {
@@ -743,6 +758,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     int *s_hist = reinterpret_cast<int *>(s_sorted + ITEMS + GS * NKEY);  // [warp][key]
     int *s_info = s_hist + (FT / 32) * NKEY;
     __shared__ int s_item, s_ex[2], s_ey[2], s_vmask[2], s_bad, s_npad, s_any, s_nfb;
+    __shared__ int s_one[NPLANE];  // plane is its own exact split (u8, order 1): single-limb MMA
     __shared__ short s_fb[FT];
     __shared__ int s_dom[2][4];
     __shared__ long long s_poff[NPLANE];
@@ -946,9 +962,19 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         FUSED_PHASE(1);
 
         // ---- 3. exact split G = 2^e (G1 + G0) of every plane that is read --------
+        if (tid < NPLANE) {
+            const int b = tid / NVAR, v = tid % NVAR;
+            bool one = false;
+            if constexpr (R == 1) {
+                const double bnd = u8_plane_bound(b, R, s_dom[b][2], s_dom[b][3]) * (v ? (double)(1 << R) : 1.0);
+                one = a.in_u8 && bnd < ldexp(1.0, min(53, luts[b].var[v].kbits));
+            }
+            s_one[tid] = one;
+        }
+        __syncthreads();
         for (int pi = 0; pi < NPLANE; ++pi) {
             const int b = pi / NVAR, v = pi % NVAR;
-            if (!((s_vmask[b] >> v) & 1)) continue;
+            if (!((s_vmask[b] >> v) & 1) || s_one[pi]) continue;
             const double2 *G = scr + s_poff[pi];
             const int n = s_dom[b][2] * s_dom[b][3];
             double m = 0.0;
@@ -960,13 +986,13 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (tid < NPLANE) {
             const double m = __longlong_as_double((long long)s_pmax[tid]);
             const int b = tid / NVAR, v = tid % NVAR;
-            s_pe[tid] = m > 0.0 ? ilogb(m) + 1 - luts[b].var[v].kbits : 0;
+            s_pe[tid] = (m > 0.0 && !s_one[tid]) ? ilogb(m) + 1 - luts[b].var[v].kbits : 0;
         }
         __syncthreads();
         for (int pi = 0; pi < NPLANE; ++pi) {
             if constexpr (R >= 3) break;  // order >= 3 splits on the fly (fused_group_g3)
             const int b = pi / NVAR, v = pi % NVAR;
-            if (!((s_vmask[b] >> v) & 1)) continue;
+            if (!((s_vmask[b] >> v) & 1) || s_one[pi]) continue;  // s_one: already (G, 0)
             double2 *G = scr + s_poff[pi];
             const int n = s_dom[b][2] * s_dom[b][3];
             const double sc = ldexp(1.0, -s_pe[pi]);
@@ -1173,6 +1199,13 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                                                                     nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
                                                                     flags);
                         }
+                    } else if (R == 1 && s_one[b * NVAR + var]) {
+                        if (var == 0)
+                            fused_group<4 * R - 2, MT, 1>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl,
+                                                          flags);
+                        else
+                            fused_group<3 * R - 2, MT, 1>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl,
+                                                          flags);
                     } else if (var == 0)
                         fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);
                     else
