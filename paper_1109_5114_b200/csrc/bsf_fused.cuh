@@ -662,7 +662,32 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
                 ++k;
             }
     }
-    if (nh) {
+    if (nh && exact_h == (1u << nh) - 1u) {
+        // every horizontal level exact in fp64: one warp per row, 32-column
+        // chunks, a warp-shuffle inclusive scan per level and chunk
+        const int lane = tid & 31, wid = tid >> 5;
+        for (int y = wid; y < NY; y += FT / 32) {
+            double carry[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) carry[k] = 0.0;
+            for (int x0 = 0; x0 < NX; x0 += 32) {
+                const int x = x0 + lane;
+                double v = x < NX ? fval(x, y) : 0.0;
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double t = __shfl_up_sync(0xffffffffu, v, o);
+                        if (lane >= o) v += t;
+                    }
+                    v += carry[k];  // exact: integers below 2^53
+                    carry[k] = __shfl_sync(0xffffffffu, v, 31);
+                }
+                if (x < NX) G[(size_t)y * NX + x] = make_double2(v, 0.0);
+            }
+        }
+        __syncthreads();
+    } else if (nh) {
         for (int y = tid; y < NY; y += FT) {
             dd acc[R];
 #pragma unroll
@@ -690,6 +715,54 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
                 steps |= (unsigned long long)((sx + 2) | ((sy - 1) << 3)) << (4 * k);
                 ++k;
             }
+    }
+    if (a.in_u8 && exact_v == (1u << L) - 1u) {
+        // every level exact in fp64 (u8 input, moderate domain): the same sweep
+        // on a ring of plain doubles -- half the shared-memory traffic, no
+        // double-double arithmetic; G receives (value, 0)
+        double *rd = reinterpret_cast<double *>(ring);
+        const int LD = min(L, (int)(ring_bytes / ((size_t)3 * NX * sizeof(double))));
+        for (int lb = 0; lb < L; lb += LD) {
+            const int Lp = min(LD, L - lb);
+            const unsigned long long pst = steps >> (4 * lb);
+            const int work = Lp * NX;
+            const int l0 = tid / NX, x0 = tid - l0 * NX, dl = FT / NX, dx = FT - dl * NX;
+            for (int tau = 0; tau < NY + Lp - 1; ++tau) {
+                int l = l0, x = x0;
+                int ym = (tau - l0) % 3;
+                if (ym < 0) ym += 3;
+                for (int i = tid; i < work; i += FT) {
+                    const int y = tau - l;
+                    if (y >= 0 && y < NY) {
+                        const unsigned st4 = (unsigned)(pst >> (4 * l)) & 15u;
+                        const int sx = (int)(st4 & 7u) - 2, sy = (int)(st4 >> 3) + 1;
+                        double below;
+                        if (l == 0)
+                            below = (nh || lb > 0) ? G[y * NX + x].x : fval(x, y);
+                        else
+                            below = rd[((l - 1) * 3 + ym) * NX + x];
+                        const int yp = y - sy, xp = x - sx;
+                        if (yp >= 0 && xp >= 0 && xp < NX) {
+                            const int ypm = ym >= sy ? ym - sy : ym - sy + 3;
+                            below += rd[(l * 3 + ypm) * NX + xp];  // exact: integers below 2^53
+                        }
+                        rd[(l * 3 + ym) * NX + x] = below;
+                        if (l == Lp - 1) G[y * NX + x] = make_double2(below, 0.0);
+                    }
+                    l += dl;
+                    ym -= dl % 3;
+                    if (ym < 0) ym += 3;
+                    x += dx;
+                    if (x >= NX) {
+                        x -= NX;
+                        ++l;
+                        ym = ym == 0 ? 2 : ym - 1;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        return true;
     }
     for (int lb = 0; lb < L; lb += LC) {
         const int Lp = min(LC, L - lb);  // levels lb .. lb + Lp - 1 in this pass
@@ -938,11 +1011,30 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         __syncthreads();
                     }
             }
-            // zero-scale variants: G' = (1 - T_{s_k})^R G, exact lattice difference (R5)
+            __syncthreads();
+            FUSED_PHASE(11);  // diagnostics: sweep of basis b
+            // zero-scale variants: G' = (1 - T_{s_k})^R G, exact lattice difference (R5);
+            // integer planes below 2^53 (u8 input) take plain fp64 arithmetic
+            const bool exact_plane =
+                a.in_u8 && u8_plane_bound(b, R, NX, NY) * (double)(1 << R) < 0x1p53;
             for (int v = 1; v < NVAR; ++v) {
                 if (!((s_vmask[b] >> v) & 1)) continue;
                 const int sx = c_steps[b][v - 1][0], sy = c_steps[b][v - 1][1];
                 double2 *D = scr + s_poff[b * NVAR + v];
+                if (exact_plane) {
+                    for (int Y = 0; Y < NY; ++Y)
+                        for (int X = tid; X < NX; X += FT) {
+                            double acc = 0.0;
+#pragma unroll
+                            for (int m = 0; m <= R; ++m) {
+                                const int yy = Y - m * sy, xx = X - m * sx;
+                                if (yy < 0 || xx < 0 || xx >= NX) continue;
+                                acc += (double)(binomR<R>(m) * ((m & 1) ? -1 : 1)) * G[yy * NX + xx].x;
+                            }
+                            D[Y * NX + X] = make_double2(acc, 0.0);
+                        }
+                    continue;
+                }
                 for (int i = tid; i < n; i += FT) {
                     const int X = i % NX, Y = i / NX;
                     dd acc = {0.0, 0.0};
@@ -959,7 +1051,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             }
         }
         __syncthreads();
-        FUSED_PHASE(1);
+        FUSED_PHASE(12);  // diagnostics: zero-scale variant planes (remainder of phase 1)
 
         // ---- 3. exact split G = 2^e (G1 + G0) of every plane that is read --------
         if (tid < NPLANE) {

@@ -13,7 +13,7 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_1109_5114_b200 import bsf  # noqa: E402
 
-PHASES = ["scales", "pre-integration", "exact split", "scatter", "gather", "accumulate"]
+PHASES = ["scales", "preint: zero pads", "exact split", "scatter", "gather", "accumulate"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
@@ -35,11 +35,12 @@ st = plan.stats(reset=True)
 print("pixels %d, double-double fallback %d (%.3f %%), macs/px %.0f" % (
     st["pixels"], st["double_double"], 100.0 * st["double_double"] / max(st["pixels"], 1),
     st["macs"] / max(st["pixels"], 1)))
-tot = sum(cyc[:6]) + cyc[8] + cyc[9] + cyc[10]
+tot = sum(cyc[:6]) + cyc[8] + cyc[9] + cyc[10] + cyc[11] + cyc[12]
 print("workload", w.name, "fused", plan.uses_fused())
 for n, c in zip(PHASES, cyc):
     print("%-16s %6.1f%%  %.3e cycles" % (n, 100.0 * c / tot, c))
-for n, c in (("sub-tile scales", cyc[8]), ("keys", cyc[9]), ("bucket scan", cyc[10])):
+for n, c in (("sub-tile scales", cyc[8]), ("keys", cyc[9]), ("bucket scan", cyc[10]),
+             ("  preint: sweeps", cyc[11]), ("  preint: variants", cyc[12])):
     print("%-16s %6.1f%%  %.3e cycles" % (n, 100.0 * c / tot, c))
 print("gather groups: warp-cycles total %.3e, full-variant MMA loop %.3e (per-CTA wall equivalent /8: %.3e, %.3e)"
       % (cyc[6], cyc[7], cyc[6] / 8, cyc[7] / 8))
