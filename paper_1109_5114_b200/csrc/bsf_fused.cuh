@@ -36,6 +36,12 @@ constexpr uint16_t NOKEY = 0xFFFF;
 #ifndef BSF_MT3
 #define BSF_MT3 1
 #endif
+#ifndef BSF_G3_NP1
+#define BSF_G3_NP1 9  // order >= 3, unsplit numerators: n-tiles per pass (9 = all at degree 10: one pass)
+#endif
+#ifndef BSF_G3_NP2
+#define BSF_G3_NP2 3  // order >= 3, split numerators (five limb products per tile): 9 = 3 x 3 at degree 10
+#endif
 template <int R> struct FusedCfg;
 // NTAP taps per pixel, P pixels per chunk, MT 8-item m-tiles per group
 template <> struct FusedCfg<1> { static constexpr int NTAP = 16, P = 256, MT = BSF_MT1; };
@@ -1274,20 +1280,20 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         const double sce = ldexp(1.0, -s_pe[b * NVAR + var]);
                         if (V.nsplit == 2) {
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 2, 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num,
+                                fused_group_g3<4 * R - 2, 2, BSF_G3_NP2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num,
                                                                     V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift,
                                                                     sce, V.kbits, Fh, Fl, flags);
                             else
-                                fused_group_g3<3 * R - 2, 2, 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num,
+                                fused_group_g3<3 * R - 2, 2, BSF_G3_NP2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num,
                                                                     V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift,
                                                                     sce, V.kbits, Fh, Fl, flags);
                         } else {
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 1, 3, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, nullptr,
+                                fused_group_g3<4 * R - 2, 1, BSF_G3_NP1, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, nullptr,
                                                                     nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
                                                                     flags);
                             else
-                                fused_group_g3<3 * R - 2, 1, 3, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, nullptr,
+                                fused_group_g3<3 * R - 2, 1, BSF_G3_NP1, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, nullptr,
                                                                     nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
                                                                     flags);
                         }
