@@ -216,16 +216,19 @@ bsf_status bsf_run_alg1(bsf_plan_t plan, const void *f_dev, const void *cov_dev,
 /* Generalised covariance splitting (the repeated
  * filtering of PAPER.md:161-166 made space-variant through Algorithm 1's
  * split, composed by Proposition 2):
- * `passes` = n >= 2 passes of the plan's order,
- *   passes 1 .. n-1: the isotropic box spline of covariance (B_b / n) I,
- *   pass n:          the space-variant box spline of C(p) - ((n-1) B_b / n) I,
- * with B_b = 2 sigma_b^2 the smallest bound (9) of covariance field b
- * (R22).  n = 2 is bsf_run_alg1 exactly; for a constant isotropic
- * field every pass has covariance C / n (the order-n kernel up to the
- * intermediate sampling).  Arguments and errors as bsf_run_alg1 (BSF_EINVAL
- * for n outside 2..16); a second float64 work image is allocated for n > 2. */
+ * `passes` = n >= 2 passes of the plan's order, with an isotropic part
+ * T = fraction * B_b (B_b = 2 sigma_b^2 the smallest bound (9) of covariance
+ * field b, R21/R22):
+ *   passes 1 .. n-1: the isotropic box spline of covariance (T / (n-1)) I,
+ *   pass n:          the space-variant box spline of C(p) - T I.
+ * fraction in (0, 1); 0 selects the default (n-1)/n, for which a constant
+ * isotropic field gets covariance C / n in every pass (the order-n kernel up
+ * to the intermediate sampling).  n = 2 with fraction 1/2 is bsf_run_alg1
+ * exactly (Table 3, sweeps this fraction).  Arguments and
+ * errors as bsf_run_alg1 (BSF_EINVAL for n outside 2..16 or fraction outside
+ * [0, 1)); a second float64 work image is allocated for n > 2.              */
 bsf_status bsf_run_split(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, int passes,
-                         double *sigma2_out, void *stream);
+                         double fraction, double *sigma2_out, void *stream);
 
 /* End to end from HOST buffers (pinned for overlap): copies f and cov to the
  * device, runs bsf_run, copies out back, all on `stream`.  Returns after

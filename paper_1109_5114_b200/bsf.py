@@ -85,7 +85,7 @@ def lib():
         L.bsf_run_alg1.restype = st
         L.bsf_run_alg1.argtypes = [vp, vp, vp, vp, vp, vp]
         L.bsf_run_split.restype = st
-        L.bsf_run_split.argtypes = [vp, vp, vp, vp, i, vp, vp]
+        L.bsf_run_split.argtypes = [vp, vp, vp, vp, i, ctypes.c_double, vp, vp]
         L.bsf_run_host.restype = st
         L.bsf_run_host.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_get_stats.restype = st
@@ -212,12 +212,13 @@ class Plan:
                                   sig.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
         return sig
 
-    def run_split(self, f, cov, out, passes, stream=None):
-        """Generalised covariance splitting with `passes` passes; returns sigma_b^2
-        per covariance field (the bound (9) is 2 sigma_b^2)."""
+    def run_split(self, f, cov, out, passes, fraction=0.0, stream=None):
+        """Generalised covariance splitting with `passes` passes and isotropic
+        share `fraction` of the bound (0: (n-1)/n); returns sigma_b^2 per
+        covariance field (the bound (9) is 2 sigma_b^2)."""
         import numpy as np
         sig = np.zeros(self.desc.batch, dtype=np.float64)
-        _check(lib().bsf_run_split(self.handle, _ptr(f), _ptr(cov), _ptr(out), int(passes),
+        _check(lib().bsf_run_split(self.handle, _ptr(f), _ptr(cov), _ptr(out), int(passes), float(fraction),
                                    sig.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
         return sig
 

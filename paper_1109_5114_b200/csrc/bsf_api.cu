@@ -622,10 +622,12 @@ static bsf_status ensure_alg1_ws(bsf_plan_s *p, bool two) {
 }
 
 extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov, void *out, int passes,
-                                    double *sigma2_out, void *stream) {
+                                    double fraction, double *sigma2_out, void *stream) {
     if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (passes < 2 || passes > 16) return set_err(BSF_EINVAL, "passes must be 2..16");
+    if (!(fraction < 1.0) || fraction < 0.0 || fraction != fraction)
+        return set_err(BSF_EINVAL, "fraction must be in [0, 1) (0: the default (n - 1) / n)");
     bsf_status s = ensure_tile_ws(p);
     if (s != BSF_OK) return s;
     if (!p->fused) return set_err(BSF_EUNSUPPORTED, "covariance splitting runs on the exact split path (order <= 3)");
@@ -636,10 +638,12 @@ extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov
     // sigma_b^2 = half the smallest bound (9) of the field (R21): the bound is 2 sigma_b^2
     CUDA_TRY(launch_alg1_sigma2((const float *)cov, p->d.batch, p->geo.W, p->geo.H, p->d.basis, p->d.clamp,
                                 p->alg1_sigma2, st, &p->nlaunch));
-    // passes - 1 isotropic passes of (2 sigma_b^2 / n) I each, ping-ponging
-    // through float64 work images, then the space-variant residual
-    // C - (n - 1)(2 sigma_b^2 / n) I (R22; n = 2 is Algorithm 1)
+    // the isotropic part T = phi B (B = 2 sigma_b^2 the bound, phi = fraction,
+    // default (n - 1) / n): passes - 1 isotropic passes of T / (n - 1) each,
+    // ping-ponging through float64 work images, then the space-variant
+    // residual C - T I (R22; n = 2, phi = 1/2 is Algorithm 1)
     const double n = passes;
+    const double phi = fraction > 0.0 ? fraction : (n - 1.0) / n;
     const void *src = f;
     bool src_f64 = false;
     double *bufs[2] = {p->alg1_work, p->alg1_work2};
@@ -653,7 +657,7 @@ extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov
         }
         a.cov_mode = COV_ISO;
         a.sigma2 = p->alg1_sigma2;
-        a.sigma2_scale = 2.0 / n;
+        a.sigma2_scale = 2.0 * phi / (n - 1.0);
         CUDA_TRY(launch_tile(p, a, st));
         src = dst;
         src_f64 = true;
@@ -663,7 +667,7 @@ extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov
     a.in_f64 = 1;
     a.cov_mode = COV_SUB;
     a.sigma2 = p->alg1_sigma2;
-    a.sigma2_scale = 2.0 * (n - 1.0) / n;
+    a.sigma2_scale = 2.0 * phi;
     CUDA_TRY(launch_tile(p, a, st));
     if (sigma2_out) {
         CUDA_TRY(cudaStreamSynchronize(st));
@@ -674,7 +678,7 @@ extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov
 
 extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov, void *out, double *sigma2_out,
                                    void *stream) {
-    return bsf_run_split(p, f, cov, out, 2, sigma2_out, stream);
+    return bsf_run_split(p, f, cov, out, 2, 0.5, sigma2_out, stream);
 }
 
 extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void *cov_host, void *out_host,

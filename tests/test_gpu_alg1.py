@@ -165,3 +165,52 @@ def test_split_matches_multi_stage_oracle(policy, r, n):
     got = out[0].cpu().numpy().ravel()
     assert max_rel(got, ref) <= 1e-9
     assert plan.stats()["flags"] == 0
+
+
+def _impulse_errors(fracs, smaj=5.0, rho=3.0, theta=math.pi / 4, policy=2):
+    """L2 error (relative) of impulse responses against the sampled Gaussian of
+    the same covariance: the plain order-1 filter, then the two-pass split with
+    isotropic share `frac` of the bound (9) for each frac."""
+    H = W = 61
+    w = synth.workload(2, width=W, height=H, max_sigma=smaj + 1.0)
+    img = torch.zeros((H, W), dtype=torch.float32)
+    img[H // 2, W // 2] = 1.0
+    cov = torch.tensor([smaj, smaj / math.sqrt(rho), theta], dtype=torch.float32)[:, None, None].expand(3, H, W)
+    cov = cov.contiguous().cuda()
+    plan = make_plan(w, policy=policy, order=1, anchor=bsf.BSF_ANCHOR_TILE)
+    sx, sy = smaj, smaj / math.sqrt(rho)
+    c, s = math.cos(theta), math.sin(theta)
+    C = np.array([[sx * sx * c * c + sy * sy * s * s, (sx * sx - sy * sy) * s * c],
+                  [(sx * sx - sy * sy) * s * c, sx * sx * s * s + sy * sy * c * c]])
+    Ci = np.linalg.inv(C)
+    yy, xx = np.mgrid[0:H, 0:W]
+    d = np.stack([xx - W // 2, yy - H // 2], -1).astype(np.float64)
+    gauss = np.exp(-0.5 * np.einsum("...i,ij,...j->...", d, Ci, d)) / (2 * math.pi * math.sqrt(np.linalg.det(C)))
+    err = lambda k: float(np.linalg.norm(k - gauss) / np.linalg.norm(gauss))
+    out = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    plan.run(img[None].cuda(), cov, out)
+    torch.cuda.synchronize()
+    e0 = err(out[0].cpu().numpy())
+    es = []
+    for fr in fracs:
+        plan.run_split(img[None].cuda(), cov, out, 2, fr)
+        torch.cuda.synchronize()
+        es.append(err(out[0].cpu().numpy()))
+    return e0, es
+
+
+def test_table3_fraction_sweep_trend():
+    """Table 3: the improvement of Algorithm 1 over the
+    plain filter for the Gaussian (s = 5, rho = 3, theta = pi/4) as the
+    isotropic share of the bound (9) sweeps 10..80 %.  The paper's values come
+    from a continuous-domain protocol (not reproduced); on the
+    sampled impulse response the trend it reports holds: small shares help
+    little, the improvement rises to ~50 % and stays within a few points of
+    its maximum beyond."""
+    fracs = [0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8]
+    e0, es = _impulse_errors(fracs)
+    imp = [1.0 - e / e0 for e in es]
+    print("table 3 (sampled):", " ".join("%d%%:%.1f" % (100 * f, 100 * i) for f, i in zip(fracs, imp)))
+    assert imp[0] < imp[4], imp
+    assert all(imp[k] <= imp[k + 1] + 1e-3 for k in range(4)), imp  # rising up to 50 %
+    assert imp[4] >= max(imp) - 0.05, imp  # 50 % within 5 points of the best
