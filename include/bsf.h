@@ -230,6 +230,16 @@ bsf_status bsf_run_alg1(bsf_plan_t plan, const void *f_dev, const void *cov_dev,
 bsf_status bsf_run_split(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, int passes,
                          double fraction, double *sigma2_out, void *stream);
 
+/* DC-renormalised output (not in the paper, whose
+ * filter is not renormalised, R12): out(p) = filter(f)(p) /
+ * sum_{q in image} beta_{a(p)}(p - q), the denominator being the same filter
+ * applied to the image indicator, so a constant image is reproduced exactly
+ * up to rounding, edges included.  Runs the fused path twice plus one
+ * division kernel (BSF_EUNSUPPORTED unless anchor = BSF_ANCHOR_TILE); the
+ * plan owns the indicator image and a float64 denominator.  Arguments as
+ * bsf_run.                                                                  */
+bsf_status bsf_run_normalized(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, void *stream);
+
 /* End to end from HOST buffers (pinned for overlap): copies f and cov to the
  * device, runs bsf_run, copies out back, all on `stream`.  Returns after
  * enqueueing; synchronise the stream before reading out_host.               */

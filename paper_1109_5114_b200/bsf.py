@@ -82,6 +82,8 @@ def lib():
         L.bsf_run_points.argtypes = [vp, vp, vp, vp, i, vp, vp, vp]
         L.bsf_run.restype = st
         L.bsf_run.argtypes = [vp, vp, vp, vp, vp]
+        L.bsf_run_normalized.restype = st
+        L.bsf_run_normalized.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_run_alg1.restype = st
         L.bsf_run_alg1.argtypes = [vp, vp, vp, vp, vp, vp]
         L.bsf_run_split.restype = st
@@ -203,6 +205,10 @@ class Plan:
 
     def run(self, f, cov, out, stream=None):
         _check(lib().bsf_run(self.handle, _ptr(f), _ptr(cov), _ptr(out), _stream(stream)))
+
+    def run_normalized(self, f, cov, out, stream=None):
+        """DC-renormalised filter: out / filter(image indicator)."""
+        _check(lib().bsf_run_normalized(self.handle, _ptr(f), _ptr(cov), _ptr(out), _stream(stream)))
 
     def run_alg1(self, f, cov, out, stream=None):
         """Algorithm 1 (covariance splitting); returns sigma_b^2 per covariance field."""

@@ -45,6 +45,8 @@ struct bsf_plan_s {
     double2 *fbuf = nullptr;             // fused path: per-CTA tap values
     double *alg1_work = nullptr;         // Algorithm 1: float64 intermediate image
     double *alg1_work2 = nullptr;        // generalised splitting: second intermediate (ping-pong)
+    void *ones = nullptr;                // DC renormalisation: image indicator (input type)
+    double *norm_den = nullptr;          // DC renormalisation: filtered indicator
     double *alg1_sigma2 = nullptr;       // Algorithm 1: sigma_b^2 per covariance field (+ reduction bits)
     int *tile_counter = nullptr;
     long long nlaunch = 0;
@@ -598,6 +600,36 @@ extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void
     bsf_status s = bsf_preintegrate(p, f, p->g_ws, stream);
     if (s != BSF_OK) return s;
     return bsf_filter(p, p->g_ws, cov, out, stream);
+}
+
+extern "C" bsf_status bsf_run_normalized(bsf_plan_t p, const void *f, const void *cov, void *out, void *stream) {
+    if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
+    if (p->d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EUNSUPPORTED, "DC renormalisation runs with BSF_ANCHOR_TILE");
+    bsf_status s = ensure_tile_ws(p);
+    if (s != BSF_OK) return s;
+    const Geometry &g = p->geo;
+    const size_t n = (size_t)g.nimg * g.H * g.W;
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last = st;
+    if (!p->ones) {
+        void *q;
+        if (cudaMalloc(&q, n * (p->d.in_dtype == BSF_U8 ? 1 : 4)) != cudaSuccess)
+            return set_err(BSF_ENOMEM, "indicator image");
+        p->dev_allocs.push_back(q);
+        p->ones = q;
+        if (cudaMalloc(&q, n * sizeof(double)) != cudaSuccess) return set_err(BSF_ENOMEM, "normaliser");
+        p->dev_allocs.push_back(q);
+        p->norm_den = (double *)q;
+        CUDA_TRY(launch_fill_ones(p->ones, p->d.in_dtype == BSF_U8, n, st, &p->nlaunch));
+    }
+    TileArgs a = tile_args(p, f, cov, out);
+    CUDA_TRY(launch_tile(p, a, st));
+    TileArgs b = tile_args(p, p->ones, cov, p->norm_den);  // sum_q beta(p - q) over the image
+    b.out_f32 = 0;
+    CUDA_TRY(launch_tile(p, b, st));
+    CUDA_TRY(launch_normalize(out, p->d.out_dtype == BSF_F32, p->norm_den, n, st, &p->nlaunch));
+    return BSF_OK;
 }
 
 static bsf_status ensure_alg1_ws(bsf_plan_s *p, bool two) {

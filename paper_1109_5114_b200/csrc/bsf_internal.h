@@ -197,6 +197,9 @@ cudaError_t launch_preint_i64(const uint8_t *f, unsigned long long *g, const Geo
 cudaError_t launch_scan_level(const void *f, int u8, void *g, int exact, const Geometry &geo, int basis, int level,
                               const void *carry, cudaStream_t st);
 void scan_step(int basis, int level, int *sx, int *sy);
+cudaError_t launch_fill_ones(void *f, int u8, size_t n, cudaStream_t st, long long *nlaunch);
+cudaError_t launch_normalize(void *out, int out_f32, const double *den, size_t n, cudaStream_t st,
+                             long long *nlaunch);
 cudaError_t launch_gather_impl(const GatherArgs &a, int order, int precision, cudaStream_t st,
                                const LutBasis *luts_dev, long long *nlaunch);
 

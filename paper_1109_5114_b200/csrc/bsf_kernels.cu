@@ -162,6 +162,40 @@ cudaError_t launch_scan_level(const void *f, int u8, void *g, int exact, const G
 }
 
 // ---------------------------------------------------------------------------
+// DC renormalisation (R12): out / (filter of the
+// image indicator), the indicator being an image of ones in the input type
+// ---------------------------------------------------------------------------
+__global__ void fill_ones_kernel(void *f, int u8, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        if (u8)
+            ((uint8_t *)f)[i] = 1;
+        else
+            ((float *)f)[i] = 1.0f;
+    }
+}
+
+__global__ void normalize_kernel(void *out, int out_f32, const double *__restrict__ den, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        if (out_f32)
+            ((float *)out)[i] = (float)((double)((float *)out)[i] / den[i]);
+        else
+            ((double *)out)[i] /= den[i];
+    }
+}
+
+cudaError_t launch_fill_ones(void *f, int u8, size_t n, cudaStream_t st, long long *nl) {
+    fill_ones_kernel<<<148 * 8, 256, 0, st>>>(f, u8, n);
+    ++*nl;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_normalize(void *out, int out_f32, const double *den, size_t n, cudaStream_t st, long long *nl) {
+    normalize_kernel<<<148 * 8, 256, 0, st>>>(out, out_f32, den, n);
+    ++*nl;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Gather
 // ---------------------------------------------------------------------------
 
