@@ -73,6 +73,12 @@ typedef enum {
     BSF_ANCHOR_TILE = 1    /* fused: sums restarted per 16x16 output tile on its halo (R18) */
 } bsf_anchor;
 
+typedef enum {
+    BSF_BOUNDARY_ZERO = 0,     /* f = 0 outside the image (the paper's running sums, R1)  */
+    BSF_BOUNDARY_REPLICATE = 1 /* f(q) = f(nearest image pixel) outside;    */
+                               /* fused path only (BSF_ANCHOR_TILE, order <= 3)                   */
+} bsf_boundary;
+
 typedef struct {
     int width, height;   /* image size W, H (pixels)                                          */
     int batch;           /* number of covariance fields (independent images / frames)         */
@@ -92,6 +98,7 @@ typedef struct {
     bsf_precision precision;
     int device;          /* CUDA device ordinal                                               */
     bsf_anchor anchor;   /* how bsf_run anchors the running sums                              */
+    bsf_boundary boundary; /* image extension outside [0, W) x [0, H)                         */
 } bsf_plan_desc;
 
 typedef struct {

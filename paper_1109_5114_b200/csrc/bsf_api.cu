@@ -310,6 +310,8 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
         return set_err(BSF_EINVAL, "bad precision");
     if (d.margin_x < 0 || d.margin_y < -1) return set_err(BSF_EINVAL, "negative margin");
     if (d.anchor != BSF_ANCHOR_GLOBAL && d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EINVAL, "bad anchor");
+    if (d.boundary != BSF_BOUNDARY_ZERO && d.boundary != BSF_BOUNDARY_REPLICATE)
+        return set_err(BSF_EINVAL, "bad boundary");
     int disp = required_disp(d.max_sigma, d.order);
     int needP = disp + 3 * d.order + 2, needPb = disp + 2;
     if ((d.margin_x && d.margin_x < needP) || (d.margin_y > 0 && d.margin_y < needPb))
@@ -393,6 +395,7 @@ extern "C" bsf_status bsf_plan_geometry(bsf_plan_t p, bsf_geometry *geom) {
 
 extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, void *stream) {
     if (!p || !f || !g) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.boundary != BSF_BOUNDARY_ZERO) return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only");
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
     double2 *gd = (double2 *)g;
@@ -405,6 +408,7 @@ extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, voi
 
 extern "C" bsf_status bsf_preintegrate_exact(bsf_plan_t p, const void *f, void *g, void *stream) {
     if (!p || !f || !g) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.boundary != BSF_BOUNDARY_ZERO) return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only");
     if (p->d.in_dtype != BSF_U8) return set_err(BSF_EINVAL, "exact pre-integration needs u8 input");
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
@@ -427,6 +431,7 @@ extern "C" bsf_status bsf_scan_step(bsf_plan_t p, int slot, int level, int *sx, 
 extern "C" bsf_status bsf_scan_level(bsf_plan_t p, int slot, int level, int exact, const void *f, void *g,
                                      const void *carry, void *stream) {
     if (!p || !g || (level == 0 && !f)) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.boundary != BSF_BOUNDARY_ZERO) return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only");
     if (slot < 0 || slot >= p->geo.nbases || level < 0 || level >= 4 * p->d.order)
         return set_err(BSF_EINVAL, "slot or level out of range");
     if (exact && p->d.in_dtype != BSF_U8) return set_err(BSF_EINVAL, "exact pre-integration needs u8 input");
@@ -548,6 +553,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.prof = p->prof;
     a.fbuf = p->fbuf;
     a.stile = p->stile;
+    a.replicate = p->d.boundary == BSF_BOUNDARY_REPLICATE;
     a.sigma2_scale = 1.0;
     // BSF_SPLIT_TOL (environment, diagnostics): override the fallback threshold
     const char *tol = getenv("BSF_SPLIT_TOL");
@@ -557,6 +563,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
 
 static cudaError_t launch_tile(bsf_plan_s *p, const TileArgs &a, cudaStream_t st) {
     if (p->fused) return launch_fused_impl(a, p->d.order, p->tile_nslots, st, p->luts_dev, &p->nlaunch);
+    if (a.replicate) return cudaErrorNotSupported;  // the double-double tile kernel is zero-extension only
     return launch_tile_impl(a, p->d.order, p->d.precision, p->tile_nslots, st, p->luts_dev, &p->nlaunch);
 }
 
@@ -568,6 +575,8 @@ extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *co
     if (npts == 0) return BSF_OK;
     bsf_status s = ensure_tile_ws(p);
     if (s != BSF_OK) return s;
+    if (p->d.boundary != BSF_BOUNDARY_ZERO && !p->fused)
+        return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only (order <= 3)");
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
     TileArgs a = tile_args(p, f, cov, out);
@@ -585,6 +594,8 @@ extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void
         if (!f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
         bsf_status s = ensure_tile_ws(p);
         if (s != BSF_OK) return s;
+        if (p->d.boundary != BSF_BOUNDARY_ZERO && !p->fused)
+            return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only (order <= 3)");
         cudaStream_t st = (cudaStream_t)stream;
         p->last = st;
         TileArgs a = tile_args(p, f, cov, out);
@@ -608,6 +619,8 @@ extern "C" bsf_status bsf_run_normalized(bsf_plan_t p, const void *f, const void
     if (p->d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EUNSUPPORTED, "DC renormalisation runs with BSF_ANCHOR_TILE");
     bsf_status s = ensure_tile_ws(p);
     if (s != BSF_OK) return s;
+    if (p->d.boundary != BSF_BOUNDARY_ZERO && !p->fused)
+        return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only (order <= 3)");
     const Geometry &g = p->geo;
     const size_t n = (size_t)g.nimg * g.H * g.W;
     cudaStream_t st = (cudaStream_t)stream;

@@ -636,8 +636,13 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
     if (LC < 1) return false;
     const size_t ipl = (size_t)a.H * a.W;
     auto fval = [&](int x, int y) -> double {
-        const int X = X0 + x, Y = Y0 + y;
-        if (X < 0 || X >= a.W || Y < 0 || Y >= a.H) return 0.0;
+        int X = X0 + x, Y = Y0 + y;
+        if (a.replicate) {  // BSF_BOUNDARY_REPLICATE: the nearest image pixel
+            X = min(max(X, 0), a.W - 1);
+            Y = min(max(Y, 0), a.H - 1);
+        } else if (X < 0 || X >= a.W || Y < 0 || Y >= a.H) {
+            return 0.0;
+        }
         const size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
         return load_f(a, o);
     };
@@ -1002,8 +1007,12 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             if (!sweep_plane<R>(G, NX, NY, X0, Y0, b, a, img, reinterpret_cast<double2 *>(smem),
                                 fused_smem_bytes<R>())) {
                 for (int i = tid; i < n; i += FT) {
-                    const int X = X0 + i % NX, Y = Y0 + i / NX;
+                    int X = X0 + i % NX, Y = Y0 + i / NX;
                     double v = 0.0;
+                    if (a.replicate) {
+                        X = min(max(X, 0), a.W - 1);
+                        Y = min(max(Y, 0), a.H - 1);
+                    }
                     if (X >= 0 && X < a.W && Y >= 0 && Y < a.H) {
                         const size_t o = (size_t)img * ipl + (size_t)Y * a.W + X;
                         v = load_f(a, o);

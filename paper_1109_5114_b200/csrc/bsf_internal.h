@@ -163,6 +163,7 @@ struct TileArgs {
     double split_tol;          // relative bound above which a pixel is recomputed in double-double
     double2 *fbuf;             // fused path: per-CTA tap values [slots][fused_items<R>()]
     int stile;                 // fused path: super-tile side (32 or 64)
+    int replicate;             // fused path: f outside the image = nearest image pixel
 };
 constexpr int TILE = 16;
 enum { COV_PLANES = 0, COV_ISO = 1, COV_SUB = 2 };

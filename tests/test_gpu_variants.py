@@ -54,3 +54,40 @@ def test_normalized_needs_tile_anchor():
     out = torch.empty((1, 32, 32), dtype=torch.float64, device="cuda")
     with pytest.raises(bsf.BsfError):
         plan.run_normalized(img, cov, out)
+
+
+@pytest.mark.parametrize("r,policy", [(1, 2), (2, 2), (2, 1), (3, 0)])
+def test_replicate_boundary_matches_padded_oracle(r, policy):
+    """BSF_BOUNDARY_REPLICATE: f outside the image is its nearest pixel.  The
+    oracle is unchanged: filtering the edge-padded image with zero extension
+    (pad >= the kernel reach) at the shifted pixels is the same sum."""
+    H, W = 38, 42
+    w, img, cov = _small_smooth(H, W, 3.0, seed=33)
+    plan = bsf.Plan(W, H, in_dtype=bsf.BSF_F32, order=r, basis=policy, max_sigma=3.0, anchor=bsf.BSF_ANCHOR_TILE,
+                    boundary=bsf.BSF_BOUNDARY_REPLICATE)
+    out = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    plan.run(img[None].cuda().contiguous(), cov.cuda().contiguous(), out)
+    torch.cuda.synchronize()
+    pad = int(np.ceil(3.0 * np.sqrt(24.0 * r))) + 6 * r + 4
+    big = np.pad(img.numpy(), pad, mode="edge")
+    ys, xs = np.mgrid[0:H, 0:W]
+    xs, ys = xs.ravel(), ys.ravel()
+    c = cov.numpy()
+    ref, *_ = O.filter_points(big, xs + pad, ys + pad, c[0][ys, xs].astype(np.float64), c[1][ys, xs].astype(np.float64),
+                              c[2][ys, xs].astype(np.float64), policy=policy, r=r)
+    got = out[0].cpu().numpy().ravel()
+    assert max_rel(got, ref) <= 1e-9
+    # interior pixels far from the edges do not see the extension
+    plan0 = bsf.Plan(W, H, in_dtype=bsf.BSF_F32, order=r, basis=policy, max_sigma=3.0, anchor=bsf.BSF_ANCHOR_TILE)
+    out0 = torch.empty_like(out)
+    plan0.run(img[None].cuda().contiguous(), cov.cuda().contiguous(), out0)
+    torch.cuda.synchronize()
+    assert not torch.equal(out, out0)
+
+
+def test_replicate_boundary_unsupported_paths():
+    w = synth.workload(1, width=32, height=32)
+    g_plan = bsf.Plan(32, 32, in_dtype=bsf.BSF_U8, order=1, max_sigma=3.0, boundary=bsf.BSF_BOUNDARY_REPLICATE)
+    img = synth.make_image(w)[None].cuda()
+    with pytest.raises(bsf.BsfError):
+        g_plan.preintegrate(img, g_plan.empty_g())
