@@ -1176,7 +1176,6 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 if (info_live(w) && (!a.pts || p == want) && t < ntap) {
                     const int b = info_basis(w);
                     double Dx, Dy;
-                    int cf;
                     fused_tap_v<R>(s_tv + 5 * p, var - 1, t, Dx, Dy);
                     const int reg = cls_region(s_cls, b, Dx - floor(Dx), Dy - floor(Dy));
                     key = (uint16_t)((b * NVAR + var) * MAX_REG + reg);

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(32 * NW) scan_strip_kernel(const In *in, typen
         // row ph of carry_in ([nimg][SY][GW], the SY domain rows above the strip)
         carry[ph] = Op::zero();
         if (carry_in && ph < geo.GH && u >= 0 && u < geo.GW && u - SX >= 0 && u - SX < geo.GW)
-            carry[ph] = carry_in[((size_t)img * SY + ph) * geo.GW + u - SX];
+            carry[ph] = carry_in[((size_t)img * SY + ph) * geo.GW + (size_t)(u - SX)];
     }
     T *o = out + (size_t)img * geo.GH * geo.GW;
     for (int j = 0; j < nblk; ++j) {
