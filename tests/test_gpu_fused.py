@@ -147,3 +147,19 @@ def test_super_tile_64_matches_32():
     got = a[0].cpu().numpy()[ys, xs]
     err = np.max(np.abs(got - ref) / np.abs(ref))
     assert err <= 1e-9, err
+
+
+@pytest.mark.parametrize("r", [1, 2, 3])
+def test_fused_tiny_and_thin_images(r):
+    """Degenerate shapes through the fused product path (a super-tile larger
+    than the image, single rows/columns, one pixel) against the oracle."""
+    for H, W in ((1, 1), (1, 37), (29, 1), (3, 2), (33, 65)):
+        w = synth.workload(1, width=W, height=H)
+        img, cov = synth.make_image(w), synth.make_cov(w)
+        plan = make_plan(w, order=r, anchor=TILE)
+        out = gpu_full(plan, img[None], cov)[0].cpu().numpy()
+        assert plan.uses_fused()
+        ys, xs = np.mgrid[0:H, 0:W]
+        from gpu_util import oracle_points, max_rel
+        ref, *_ = oracle_points(img.numpy(), cov.numpy(), xs.ravel(), ys.ravel(), policy=2, r=r)
+        assert max_rel(out.ravel(), ref) <= 1e-9, (H, W)
