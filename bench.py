@@ -341,8 +341,9 @@ def main():
         plan.run(img, cov, out, stream)
         plan.phase_cycles(reset=True)
         plan.run(img, cov, out, stream)
-        cyc = plan.phase_cycles()
-        tot = float(sum(cyc[:6])) or 1.0
+        c = plan.phase_cycles()  # counters of bsf_debug_phase_cycles (include/bsf.h)
+        cyc = [c[0] + c[8], c[1] + c[11] + c[12], c[2], c[3] + c[9] + c[10], c[4], c[5]]
+        tot = float(sum(cyc)) or 1.0
         names = ["scales", "pre_integration", "exact_split", "keys_sort", "gather", "accumulate"]
         alg_bytes = npx * in_b + 12 * npx + 8 * npx  # read f + cov once, write out once
         hbm_gbs = alg_bytes / (gat * 1e-3) / 1e9

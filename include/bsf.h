@@ -260,10 +260,11 @@ long long bsf_launch_count(bsf_plan_t plan);
 
 /* Diagnostics.  bsf_debug_phase_cycles: the first call enables per-phase
  * cycle counters in the tile path (adds one clock read per phase per tile);
- * later calls copy the 16 counters (SM cycles summed over tiles: 0 scales,
- * 1 pre-integration, 2 exact split, 3 sort, 4 gather, 5 accumulation, 6-7
- * warp-cycles of the MMA groups, 8 sub-tile scales, 9 keys, 10 bucket scan;
- * 3 = 8 + 9 + 10 + scatter) to host `out`
+ * later calls copy the 16 counters (SM cycles summed over tiles, each phase
+ * measured from the previous mark: 0 reach pass, 1 zero pad rows, 11 the
+ * running-sum sweeps, 12 the zero-scale variant planes, 2 exact split,
+ * 8 sub-tile scales, 9 keys, 10 bucket scan, 3 scatter, 4 gather,
+ * 5 accumulation; 6-7 warp-cycles of the MMA groups) to host `out`
  * (may be NULL) after synchronising the plan's last stream, and zero them when
  * `reset`.  bsf_uses_fused: 1 when the tile path runs the exact split
  * contraction kernel (known after the first tile-path call), else 0.        */

@@ -13,7 +13,7 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_1109_5114_b200 import bsf  # noqa: E402
 
-PHASES = ["scales", "preint: zero pads", "exact split", "scatter", "gather", "accumulate"]
+PHASES = ["scales (reach)", "preint: zero pads", "exact split", "scatter", "gather", "accumulate"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
