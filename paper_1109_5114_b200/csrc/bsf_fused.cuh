@@ -1553,12 +1553,9 @@ cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int po
 template <int R>
 static cudaError_t launch_fused_r(const TileArgs &a, int slots, cudaStream_t st, const LutBasis *luts) {
     constexpr size_t sm = fused_smem_bytes<R>();
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(fused_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0ull};
+    cudaError_t e = set_smem_attr(fused_kernel<R>, (int)sm, attr);
+    if (e != cudaSuccess) return e;
     fused_kernel<R><<<slots, FT, sm, st>>>(a, luts);
     return cudaGetLastError();
 }

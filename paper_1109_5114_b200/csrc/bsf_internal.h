@@ -1,5 +1,6 @@
 // Internal declarations shared by bsf_api.cu and bsf_kernels.cu.
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -165,6 +166,21 @@ struct TileArgs {
     int stile;                 // fused path: super-tile side (32 or 64)
     int replicate;             // fused path: f outside the image = nearest image pixel
 };
+// Opt a kernel into more than 48 KB of dynamic shared memory, once per device
+// (the attribute belongs to the device's context; plans may live on several
+// devices of one process).  `done` is the caller's per-kernel flag array.
+template <class K>
+inline cudaError_t set_smem_attr(K kernel, int bytes, std::atomic<unsigned long long> &done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+
 constexpr int TILE = 16;
 enum { COV_PLANES = 0, COV_ISO = 1, COV_SUB = 2 };
 cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int policy, int clamp, double *sigma2,

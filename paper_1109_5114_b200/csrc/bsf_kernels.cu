@@ -81,13 +81,9 @@ static cudaError_t scan_strips(const In *in, typename Op::T *g, const Geometry &
     constexpr int NW = DD ? BSF_SCAN_NW_DD : BSF_SCAN_NW_I64, RPW = DD ? BSF_SCAN_RPW_DD : BSF_SCAN_RPW_I64,
                   ND = DD ? BSF_SCAN_ND_DD : BSF_SCAN_ND_I64;
     constexpr int SMEM = ND * NW * RPW * 32 * (int)sizeof(typename Op::T);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(scan_strip_kernel<Op, In, SX, SY, NW, RPW, ND>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0ull};
+    cudaError_t e = set_smem_attr(scan_strip_kernel<Op, In, SX, SY, NW, RPW, ND>, SMEM, attr);
+    if (e != cudaSuccess) return e;
     const int span = abs(SX) * ((geo.GH - 1) / SY);
     const int U0 = SX > 0 ? -span : 0, NS = (geo.GW + span + 31) / 32;
     scan_strip_kernel<Op, In, SX, SY, NW, RPW, ND>
