@@ -163,3 +163,18 @@ def test_fused_tiny_and_thin_images(r):
         from gpu_util import oracle_points, max_rel
         ref, *_ = oracle_points(img.numpy(), cov.numpy(), xs.ravel(), ys.ravel(), policy=2, r=r)
         assert max_rel(out.ravel(), ref) <= 1e-9, (H, W)
+
+
+def test_run_host_matches_device_run():
+    """bsf_run_host (the e2e path of bench.py: pinned host buffers, copies on
+    the stream) gives the device run's output bit for bit."""
+    w, img, cov = _small_smooth(80, 96, 6.0, seed=12)
+    plan = make_plan(w, anchor=TILE)
+    dev = gpu_full(plan, img[None], cov).cpu()
+    assert torch.isfinite(dev).all()
+    f_h = img[None].contiguous().pin_memory()
+    c_h = cov.contiguous().pin_memory()
+    o_h = torch.empty((1, 80, 96), dtype=torch.float64).pin_memory()
+    plan.run_host(f_h, c_h, o_h)
+    torch.cuda.synchronize()
+    assert torch.equal(o_h, dev)
