@@ -624,7 +624,7 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
     }
 }
 
-template <int R>
+template <int R, bool SAME_SIGN>
 __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int Y0, int basis, const TileArgs &a,
                             int img, double2 *ring, size_t ring_bytes) {
     const int tid = threadIdx.x;
@@ -649,8 +649,12 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
     // a u8 image makes every running sum non-negative: the cheaper same-sign
     // double-double addition is then exact to 3u^2 (float input may be signed;
     // scanning the domain for signs cost more than it saved on config 2)
-    const bool same_sign = a.in_u8 != 0;
-    auto add = [&](dd u, dd v) -> dd { return same_sign ? dd_add_same_sign(u, v) : dd_add(u, v); };
+    auto add = [&](dd u, dd v) -> dd {
+        if constexpr (SAME_SIGN)
+            return dd_add_same_sign(u, v);
+        else
+            return dd_add(u, v);
+    };
     // u8 input: the running sums are integers, and a level whose values stay
     // below 2^53 (255 x the product of the line lengths so far) is exact in
     // plain fp64 -- one DADD instead of a double-double addition.  Bit k of
@@ -1004,8 +1008,11 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             const int n = NX * NY;
             // wavefront sweep with its ring in the (idle) dynamic shared memory;
             // level-by-level scans when the ring does not fit
-            if (!sweep_plane<R>(G, NX, NY, X0, Y0, b, a, img, reinterpret_cast<double2 *>(smem),
-                                fused_smem_bytes<R>())) {
+            const bool swept = a.in_u8 ? sweep_plane<R, true>(G, NX, NY, X0, Y0, b, a, img,
+                                                                reinterpret_cast<double2 *>(smem), fused_smem_bytes<R>())
+                                       : sweep_plane<R, false>(G, NX, NY, X0, Y0, b, a, img,
+                                                                 reinterpret_cast<double2 *>(smem), fused_smem_bytes<R>());
+            if (!swept) {
                 for (int i = tid; i < n; i += FT) {
                     int X = X0 + i % NX, Y = Y0 + i / NX;
                     double v = 0.0;
