@@ -557,7 +557,7 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
                 double bB = 0.0, bF = 0.0;
                 if constexpr (NSPLIT == 2) {
                     bB = __ldg(numB + o + 8 * j);
-                    bF = __ldg(numF + o + 8 * j);
+                    bF = fma(bA, ssh, bB);  // the full numerator n = n1 2^sh + n0, exact (|n| < 2^53)
                 }
 #pragma unroll
                 for (int t = 0; t < MT; ++t) {
