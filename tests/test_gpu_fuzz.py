@@ -1,0 +1,70 @@
+"""Seeded random cases through the fused product path against the oracle:
+sizes (ragged, smaller and larger than a super-tile), orders 1-3, the three
+basis policies, u8 / f32 input, f64 / f32 output, batch and channels, random
+smooth covariance fields with random sigma ranges, elongations and angles."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from paper_1109_5114_b200 import bsf
+from gpu_util import max_rel, oracle_points
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    H, W = int(rng.integers(5, 90)), int(rng.integers(5, 90))
+    r = int(rng.integers(1, 4))
+    policy = int(rng.integers(0, 3))
+    u8 = bool(rng.integers(0, 2))
+    batch, channels = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+    smax = float(rng.uniform(0.7, 5.0 if r < 3 else 3.0))
+    ph = rng.uniform(0, 2 * math.pi, 4)
+    X = np.arange(W)[None, :] / max(W - 1, 1)
+    Y = np.arange(H)[:, None] / max(H - 1, 1)
+    covs, imgs = [], []
+    for b in range(batch):
+        smaj = 0.6 + (smax - 0.6) * (0.5 + 0.5 * np.sin(3 * X + ph[0] + b) * np.cos(2 * Y + ph[1]))
+        ratio = 1.0 + rng.uniform(0, 5.5) * (0.5 + 0.5 * np.cos(2 * X - 3 * Y + ph[2]))
+        th = np.mod(ph[3] + 2.0 * X - 1.5 * Y + b, math.pi)
+        covs.append(np.stack([smaj, smaj / np.sqrt(ratio), th + 0 * X]).astype(np.float32))
+        for c in range(channels):
+            if u8:
+                imgs.append(rng.integers(0, 256, (H, W)).astype(np.uint8))
+            else:
+                imgs.append(rng.uniform(-0.5, 1.0, (H, W)).astype(np.float32))
+    return dict(H=H, W=W, r=r, policy=policy, u8=u8, batch=batch, channels=channels, smax=smax,
+                cov=np.stack(covs), img=np.stack(imgs), out_f32=bool(rng.integers(0, 2)), rng=rng)
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_fuzz_fused_vs_oracle(seed):
+    c = _case(seed)
+    H, W = c["H"], c["W"]
+    plan = bsf.Plan(W, H, batch=c["batch"], channels=c["channels"],
+                    in_dtype=bsf.BSF_U8 if c["u8"] else bsf.BSF_F32,
+                    out_dtype=bsf.BSF_F32 if c["out_f32"] else bsf.BSF_F64, order=c["r"], basis=c["policy"],
+                    max_sigma=c["smax"], anchor=bsf.BSF_ANCHOR_TILE)
+    nimg = c["batch"] * c["channels"]
+    out = torch.empty((nimg, H, W), dtype=torch.float32 if c["out_f32"] else torch.float64, device="cuda")
+    plan.run(torch.from_numpy(c["img"]).cuda(), torch.from_numpy(c["cov"]).cuda(), out)
+    torch.cuda.synchronize()
+    assert plan.uses_fused()
+    got = out.cpu().numpy().astype(np.float64)
+    rng = c["rng"]
+    n = min(H * W, 24)
+    for i in range(nimg):
+        b = i // c["channels"]
+        idx = rng.choice(H * W, n, replace=False)
+        ys, xs = idx // W, idx % W
+        ref = oracle_points(c["img"][i], c["cov"][b], xs, ys, policy=c["policy"], r=c["r"])[0]
+        tol = 1e-6 if c["out_f32"] else 1e-9
+        # signed float images: relative error against the larger of |ref| and the
+        # output scale (outputs can pass through zero)
+        scale = np.maximum(np.abs(ref), 1e-3 * np.max(np.abs(ref)))
+        err = float(np.max(np.abs(got[i][ys, xs] - ref) / scale))
+        assert err <= tol, (seed, i, err, {k: c[k] for k in ("H", "W", "r", "policy", "u8", "smax")})
