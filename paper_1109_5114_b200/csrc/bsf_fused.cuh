@@ -539,7 +539,10 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
 #else
                 const bool inside = true;  // fused_domain covers every window read
 #endif
-                const double2 g = G[inside ? (size_t)ly * NX + lx : 0];
+                // the order-3 halo planes are too large for L1 and are read from L2 anyway:
+                // bypass L1 so that it keeps the region's coefficient table
+                // (an L1 prefetch of the next step's sums evicted the table: +32 %)
+                const double2 g = __ldcg(G + (inside ? (size_t)ly * NX + lx : 0));
                 g1[t] = g2[t] = g0[t] = 0.0;
                 if (inside) {
                     const double h = g.x * sc_e;  // exact (power of two)
