@@ -46,7 +46,10 @@ template <int R> struct FusedCfg;
 // NTAP taps per pixel, P pixels per chunk, MT 8-item m-tiles per group
 template <> struct FusedCfg<1> { static constexpr int NTAP = 16, P = 256, MT = BSF_MT1; };
 template <> struct FusedCfg<2> { static constexpr int NTAP = 81, P = 256, MT = 4; };
-template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = 64, MT = BSF_MT3; };
+#ifndef BSF_P3
+#define BSF_P3 64
+#endif
+template <> struct FusedCfg<3> { static constexpr int NTAP = 256, P = BSF_P3, MT = BSF_MT3; };
 template <> struct FusedCfg<4> { static constexpr int NTAP = 625, P = 16, MT = 1; };
 
 // per-tap interpolated values F (double-double) live in a per-CTA global
