@@ -274,6 +274,33 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
             V.num = (const double *)d1;  // n1 with G1 (exact)
             V.num2 = (const double *)d0; // n0 with G1 (exact)
         }
+        // order >= 3: the B operand tables in fp32 when every value is exact there
+        // (|n| <= 2^24 integers; all order-3 tables qualify)
+        V.num32 = nullptr;
+        if (exact && p->d.order >= 3) {
+            std::vector<float> c32;
+            bool ok = true;
+            auto put = [&](double v) {
+                const float f = (float)v;
+                ok = ok && (double)f == v;
+                c32.push_back(f);
+            };
+            if (V.nsplit == 1) {
+                for (double v : nump) put(v);
+            } else {
+                for (size_t i = 0; i < num1s.size(); ++i) {
+                    put(num1s[i]);
+                    put(num0s[i]);
+                }
+            }
+            if (ok) {
+                void *d32;
+                CUDA_TRY(cudaMalloc(&d32, c32.size() * sizeof(float)));
+                p->dev_allocs.push_back(d32);
+                CUDA_TRY(cudaMemcpy(d32, c32.data(), c32.size() * sizeof(float), cudaMemcpyHostToDevice));
+                V.num32 = (const float *)d32;
+            }
+        }
         for (uint32_t r = 0; r < nreg; ++r)
             for (int s2 = 0; s2 < counts[r]; ++s2) {
                 double sb = 0.0;
@@ -501,8 +528,10 @@ static bool use_fused(const bsf_plan_s *p) {
     if (env && env[0] == '0') return false;
     for (int b = 0; b < 2; ++b) {
         if (!(p->d.basis == BSF_DUAL || p->d.basis == b)) continue;
-        for (int v = 0; v < NVAR; ++v)
+        for (int v = 0; v < NVAR; ++v) {
             if (p->host_luts[b].var[v].kbits < KBITS_MIN) return false;
+            if (p->d.order >= 3 && !p->host_luts[b].var[v].num32) return false;  // fp32-exact B tables
+        }
     }
     return true;
 }

@@ -493,8 +493,7 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
 template <int DEG, int NSPLIT, int NP, int MT>
 __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
                                                const int (&byt)[MT], double fxo, double fyo,
-                                               const int2 *__restrict__ offs, const double *__restrict__ numA,
-                                               const double *__restrict__ numB, const double *__restrict__ numF,
+                                               const int2 *__restrict__ offs, const float *__restrict__ numc,
                                                int nmonp, int n4, int shift, double sc_e, int kbits,
                                                double (&Fh)[MT], double (&Fl)[MT], int &flags) {
     constexpr int NT = DegCfg<DEG>::NT, NL = NSPLIT == 1 ? 3 : 5, QMAX = RowCfg<DEG>::QMAX;
@@ -559,10 +558,15 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
 #pragma unroll
             for (int j = 0; j < NP; ++j) {
                 if (j0 + j >= NT) break;
-                const double bA = __ldg(numA + o + 8 * j);
-                double bB = 0.0, bF = 0.0;
-                if constexpr (NSPLIT == 2) {
-                    bB = __ldg(numB + o + 8 * j);
+                // fp32 numerator tables (exact: all order-3 numerators are integers
+                // below 2^24): half the bytes of the B loads, which L1 must hold
+                double bA, bB = 0.0, bF = 0.0;
+                if constexpr (NSPLIT == 1) {
+                    bA = (double)__ldg(numc + o + 8 * j);
+                } else {
+                    const float2 v = __ldg(reinterpret_cast<const float2 *>(numc) + o + 8 * j);  // (n1, n0)
+                    bA = (double)v.x;
+                    bB = (double)v.y;
                     bF = fma(bA, ssh, bB);  // the full numerator n = n1 2^sh + n0, exact (|n| < 2^53)
                 }
 #pragma unroll
@@ -1300,23 +1304,25 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         const size_t ro = (size_t)reg * V.nslot4 * V.nmonp;
                         const double sce = ldexp(1.0, -s_pe[b * NVAR + var]);
                         if (V.nsplit == 2) {
+                            const float *nc = V.num32 + 2 * ro;  // (n1, n0) pairs
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 2, BSF_G3_NP2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num,
-                                                                    V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift,
-                                                                    sce, V.kbits, Fh, Fl, flags);
+                                fused_group_g3<4 * R - 2, 2, BSF_G3_NP2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, V.shift, sce, V.kbits, Fh,
+                                                                             Fl, flags);
                             else
-                                fused_group_g3<3 * R - 2, 2, BSF_G3_NP2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num,
-                                                                    V.num2 + ro, V.numf + ro, V.nmonp, n4, V.shift,
-                                                                    sce, V.kbits, Fh, Fl, flags);
+                                fused_group_g3<3 * R - 2, 2, BSF_G3_NP2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, V.shift, sce, V.kbits, Fh,
+                                                                             Fl, flags);
                         } else {
+                            const float *nc = V.num32 + ro;
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 1, BSF_G3_NP1, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, nullptr,
-                                                                    nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
-                                                                    flags);
+                                fused_group_g3<4 * R - 2, 1, BSF_G3_NP1, MT>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
+                                                                             flags);
                             else
-                                fused_group_g3<3 * R - 2, 1, BSF_G3_NP1, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, nullptr,
-                                                                    nullptr, V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
-                                                                    flags);
+                                fused_group_g3<3 * R - 2, 1, BSF_G3_NP1, MT>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
+                                                                             flags);
                         }
                     } else if (R == 1 && s_one[b * NVAR + var]) {
                         if (var == 0)

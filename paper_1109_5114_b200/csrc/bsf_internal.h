@@ -103,6 +103,8 @@ struct LutVar {
     int shift;
     const double *num2;    // [nreg][nslot4][nmonp] n0 (nsplit 2)
     const double *numf;    // [nreg][nslot4][nmonp] n (nsplit 2: the G0 limb's operand)
+    const float *num32;    // order >= 3, when exact in fp32: [nreg][nslot4][nmonp] n (nsplit 1) or
+                           // interleaved (n1, n0) pairs (nsplit 2) -- half the bytes of the MMA's B loads
     double bnd;            // bound on |F - F^| (units 2^e) of the split contraction: gamma_{n+1} 0.5 max_reg sum_s,mu |n|
     double L;              // common denominator
 };
