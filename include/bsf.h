@@ -99,6 +99,10 @@ typedef struct {
     int device;          /* CUDA device ordinal                                               */
     bsf_anchor anchor;   /* how bsf_run anchors the running sums                              */
     bsf_boundary boundary; /* image extension outside [0, W) x [0, H)                         */
+    int super_tile;      /* BSF_ANCHOR_TILE anchoring unit: 0 = automatic (16 for images of
+                          * fewer than 148 32x32 tiles, 64 at order 1 with a large reach, else
+                          * 32), or 16 / 32 / 64.  Row strips that must reproduce a one-GPU
+                          * run bit for bit pass the full image's geometry.super_tile      */
 } bsf_plan_desc;
 
 typedef struct {
@@ -108,8 +112,8 @@ typedef struct {
     size_t g_bytes;          /* bytes of the pre-integrated buffer bsf_preintegrate writes    */
     size_t g_exact_bytes;    /* bytes of the bit-exact int64 buffer (u8 input only, else 0)   */
     int super_tile;          /* BSF_ANCHOR_TILE: side of the super-tiles the running sums are
-                              * anchored on (32 or 64, larger for large max_sigma); row strips
-                              * that must reproduce a one-GPU run align to it                */
+                              * anchored on (16, 32 or 64); row strips that must reproduce a
+                              * one-GPU run align to it and use it in their plans           */
 } bsf_geometry;
 
 typedef struct {

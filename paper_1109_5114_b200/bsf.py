@@ -37,7 +37,7 @@ class bsf_plan_desc(ctypes.Structure):
                 ("order", ctypes.c_int), ("basis", ctypes.c_int), ("max_sigma", ctypes.c_float),
                 ("margin_x", ctypes.c_int), ("margin_y", ctypes.c_int), ("clamp", ctypes.c_int),
                 ("precision", ctypes.c_int), ("device", ctypes.c_int), ("anchor", ctypes.c_int),
-                ("boundary", ctypes.c_int)]
+                ("boundary", ctypes.c_int), ("super_tile", ctypes.c_int)]
 
 
 class bsf_geometry(ctypes.Structure):
@@ -138,9 +138,10 @@ class Plan:
 
     def __init__(self, width, height, *, batch=1, channels=1, in_dtype=BSF_F32, out_dtype=BSF_F64, order=1,
                  basis=BSF_DUAL, max_sigma=1.0, margin_x=0, margin_y=0, clamp=1, precision=BSF_PREC_DD,
-                 device=0, anchor=BSF_ANCHOR_GLOBAL, boundary=0, lut_dir=LUT_DIR):
+                 device=0, anchor=BSF_ANCHOR_GLOBAL, boundary=0, super_tile=0, lut_dir=LUT_DIR):
         self.desc = bsf_plan_desc(width, height, batch, channels, in_dtype, out_dtype, order, basis,
-                                  float(max_sigma), margin_x, margin_y, clamp, precision, device, anchor, boundary)
+                                  float(max_sigma), margin_x, margin_y, clamp, precision, device, anchor, boundary,
+                                  super_tile)
         h = ctypes.c_void_p()
         _check(lib().bsf_plan_create(ctypes.byref(self.desc), lut_dir.encode(), ctypes.byref(h)))
         self.handle = h

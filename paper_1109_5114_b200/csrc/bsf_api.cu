@@ -339,6 +339,8 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     if (d.anchor != BSF_ANCHOR_GLOBAL && d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EINVAL, "bad anchor");
     if (d.boundary != BSF_BOUNDARY_ZERO && d.boundary != BSF_BOUNDARY_REPLICATE)
         return set_err(BSF_EINVAL, "bad boundary");
+    if (d.super_tile != 0 && d.super_tile != 16 && d.super_tile != 32 && d.super_tile != 64)
+        return set_err(BSF_EINVAL, "super_tile must be 0, 16, 32 or 64");
     int disp = required_disp(d.max_sigma, d.order);
     int needP = disp + 3 * d.order + 2, needPb = disp + 2;
     if ((d.margin_x && d.margin_x < needP) || (d.margin_y > 0 && d.margin_y < needPb))
@@ -363,8 +365,13 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     {
         const double E = (double)d.max_sigma * sqrt(24.0 * d.order);
         p->stile = (d.order == 1 && E > BSF_STILE64_REACH) ? 64 : 32;  // r >= 2: larger domains cost precision
+        // small images: 16 x 16 super-tiles when 32 x 32 ones would leave most
+        // SMs idle (config 1: 16 super-tiles for 148 SMs)
+        const long long n32 = (long long)((d.width + 31) / 32) * ((d.height + 31) / 32) * d.batch * d.channels;
+        if (p->stile == 32 && n32 < 148) p->stile = 16;
+        if (d.super_tile) p->stile = d.super_tile;
         const char *env = getenv("BSF_STILE");
-        if (env && (atoi(env) == 32 || atoi(env) == 64)) p->stile = atoi(env);
+        if (env && (atoi(env) == 16 || atoi(env) == 32 || atoi(env) == 64)) p->stile = atoi(env);
     }
     g.nbases = d.basis == BSF_DUAL ? 2 : 1;
     p->bases[0] = d.basis == BSF_DUAL ? BSF_THETA : d.basis;

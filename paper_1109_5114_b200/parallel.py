@@ -7,8 +7,10 @@
   so each rank receives the input rows [y0 - R_s, y0) and [y1, y1 + R_s) from
   its neighbours (one NCCL send/recv pair per neighbour) and runs the
   tile-anchored kernel on its block.  Strip and halo boundaries are multiples
-  of the super-tile (plan.geometry.super_tile rows: 32, or 64 at order 1 with a
-  large reach) on which the fused kernel anchors its running sums,
+  of the super-tile (plan.geometry.super_tile rows) on which the fused kernel
+  anchors its running sums -- every rank's plan is created with the full
+  image's super_tile (bsf_plan_desc.super_tile), since the automatic choice
+  depends on the image size --
   and the halo covers a super-tile's halo domain, so every kept super-tile
   sees exactly the data and domain it sees in a single-GPU run: the outputs
   are bit-identical (tests/test_gpu_strips.py).  No scan carries are
@@ -24,7 +26,7 @@ from dataclasses import dataclass
 
 import torch
 
-TILE = 32  # the fused kernel's default super-tile (plan.geometry.super_tile: 32, or 64 at order 1 / large sigma)
+TILE = 32  # the fused kernel's usual super-tile (plan.geometry.super_tile: 16, 32 or 64)
 
 
 def shard_range(n: int, rank: int, world: int):
@@ -114,7 +116,8 @@ def filter_strip(plan_factory, f_own: torch.Tensor, cov_own: torch.Tensor, strip
     """Filter this rank's strip of one image: exchange input halos, run the
     tile-anchored library path on the block, keep the own rows.
 
-    plan_factory(height) -> a bsf.Plan for a W x height block (anchor TILE)
+    plan_factory(height) -> a bsf.Plan for a W x height block (anchor TILE,
+    super_tile = strip.tile: the anchoring unit of the full image)
     f_own (y1 - y0, W); cov_own (3, y1 - y0, W) -- this rank's rows only.
     The covariance of halo rows is never used (their outputs are discarded),
     so it is not exchanged."""

@@ -35,12 +35,12 @@ def test_strips_bitwise_equal_single_gpu(world, order, policy, smax):
     img = synth.make_image(w).cuda()
     cov = _field(H, W, smax).cuda()
 
-    def plan(height):
+    def plan(height, super_tile=0):
         return bsf.Plan(W, height, in_dtype=bsf.BSF_F32, order=order, basis=policy, max_sigma=smax,
-                        anchor=bsf.BSF_ANCHOR_TILE)
+                        anchor=bsf.BSF_ANCHOR_TILE, super_tile=super_tile)
 
     full = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
-    p_full = plan(H)
+    p_full = plan(H, 64 if order == 1 else 32)  # the strips reuse the full plan's anchoring unit
     tile = p_full.geometry.super_tile
     assert tile == (64 if order == 1 else 32)
     p_full.run(img[None].contiguous(), cov.contiguous(), full)
@@ -52,7 +52,7 @@ def test_strips_bitwise_equal_single_gpu(world, order, policy, smax):
         cov_blk = torch.ones((3, st.rows, W), dtype=torch.float32, device="cuda")
         cov_blk[:, st.out_slice] = cov[:, st.y0:st.y1]  # halo outputs are discarded
         out = torch.empty((1, st.rows, W), dtype=torch.float64, device="cuda")
-        plan(st.rows).run(f_blk[None].contiguous(), cov_blk.contiguous(), out)
+        plan(st.rows, tile).run(f_blk[None].contiguous(), cov_blk.contiguous(), out)
         torch.cuda.synchronize()
         got = out[0, st.out_slice]
         ref = full[0, st.y0:st.y1]

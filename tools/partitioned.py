@@ -73,7 +73,7 @@ else:
 
     def factory(height):
         p = bsf.Plan(w.width, height, in_dtype=bsf.BSF_F32, order=w.order, basis=w.basis,
-                     max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_TILE, device=local)
+                     max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_TILE, device=local, super_tile=tile)
         assert p.geometry.super_tile == tile
         return p
 
