@@ -1181,23 +1181,35 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             __syncthreads();
             if (!s_any) continue;  // uniform
             FUSED_PHASE(8);
-            // keys of all items (independent per item: the loop is unrolled so
-            // several items' dependency chains overlap) ...
-#pragma unroll 4
-            for (int i = tid; i < ITEMS; i += FT) {
-                const int t = i / P, p = c0 + i % P;
-                const int w = s_info[p];
-                const int var = info_var(w);
-                const int ntap = var ? NTAP / (R + 1) : NTAP;
-                uint16_t key = NOKEY;
-                if (info_live(w) && (!a.pts || p == want) && t < ntap) {
+            // keys of all items (item i = t P + pixel): each thread keeps one
+            // pixel's geometry in registers and walks its taps (t0, t0 + FT/P,
+            // ...); the tap loop is unrolled so several chains overlap ...
+            {
+                static_assert(FT % P == 0 || P % FT == 0, "chunk and block sizes must nest");
+                constexpr int TSTEP = FT >= P ? FT / P : 1;
+#pragma unroll 1
+                for (int pl = tid % P; pl < P; pl += (FT >= P ? P : FT)) {
+                    const int p = c0 + pl;
+                    const int w = s_info[p];
+                    const int var = info_var(w);
+                    const int ntap = var ? NTAP / (R + 1) : NTAP;
+                    const bool live = info_live(w) && (!a.pts || p == want);
                     const int b = info_basis(w);
-                    double Dx, Dy;
-                    fused_tap_v<R>(s_tv + 5 * p, var - 1, t, Dx, Dy);
-                    const int reg = cls_region(s_cls, b, Dx - floor(Dx), Dy - floor(Dy));
-                    key = (uint16_t)((b * NVAR + var) * MAX_REG + reg);
+                    double2 tv[5];
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) tv[k] = s_tv[5 * p + k];
+#pragma unroll 4
+                    for (int t = (FT >= P ? tid / P : 0); t < NTAP; t += TSTEP) {
+                        uint16_t key = NOKEY;
+                        if (live && t < ntap) {
+                            double Dx, Dy;
+                            fused_tap_v<R>(tv, var - 1, t, Dx, Dy);
+                            const int reg = cls_region(s_cls, b, Dx - floor(Dx), Dy - floor(Dy));
+                            key = (uint16_t)((b * NVAR + var) * MAX_REG + reg);
+                        }
+                        s_key[t * P + pl] = key;
+                    }
                 }
-                s_key[i] = key;
             }
             __syncthreads();
             // ... then per-warp histograms (warp w owns items [w*WPR, (w+1)*WPR))
