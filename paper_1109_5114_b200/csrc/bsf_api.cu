@@ -43,6 +43,7 @@ struct bsf_plan_s {
     bool fused = false;
     unsigned long long *prof = nullptr;  // phase cycles of the fused kernel (diagnostics)
     double2 *fbuf = nullptr;             // fused path: per-CTA tap values
+    double *sbuf = nullptr;              // fused path: per-CTA per-pixel scales
     double *alg1_work = nullptr;         // Algorithm 1: float64 intermediate image
     double *alg1_work2 = nullptr;        // generalised splitting: second intermediate (ping-pong)
     void *ones = nullptr;                // DC renormalisation: image indicator (input type)
@@ -559,6 +560,10 @@ static bsf_status ensure_tile_ws(bsf_plan_s *p) {
         if (cudaMalloc(&q, fb) != cudaSuccess) return set_err(BSF_ENOMEM, "tap buffer " + std::to_string(fb));
         p->dev_allocs.push_back(q);
         p->fbuf = (double2 *)q;
+        const size_t sb = (size_t)p->tile_nslots * FUSED_NQ_MAX * 256 * 5 * sizeof(double);
+        if (cudaMalloc(&q, sb) != cudaSuccess) return set_err(BSF_ENOMEM, "scale buffer " + std::to_string(sb));
+        p->dev_allocs.push_back(q);
+        p->sbuf = (double *)q;
     }
     if (cudaMalloc(&q, sizeof(int)) != cudaSuccess) return set_err(BSF_ENOMEM, "tile counter");
     p->dev_allocs.push_back(q);
@@ -588,6 +593,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.stats = p->stats;
     a.prof = p->prof;
     a.fbuf = p->fbuf;
+    a.sbuf = p->sbuf;
     a.stile = p->stile;
     a.replicate = p->d.boundary == BSF_BOUNDARY_REPLICATE;
     a.sigma2_scale = 1.0;

@@ -849,6 +849,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     constexpr int MT = FusedCfg<R>::MT, GS = 8 * MT;
     extern __shared__ __align__(16) unsigned char smem[];
     double2 *s_F = a.fbuf + (size_t)blockIdx.x * ITEMS;  // global, L2-resident (see fused_items)
+    double *s_scl = a.sbuf + (size_t)blockIdx.x * FUSED_NQ_MAX * FT * 5;  // per-pixel scales of the super-tile
     double *s_ap = reinterpret_cast<double *>(smem);
     double2 *s_tv = reinterpret_cast<double2 *>(s_ap + FT * 4);  // [pixel][5]: s_k a'_k (k < 4), centre
     uint16_t *s_key = reinterpret_cast<uint16_t *>(s_tv + FT * 5);
@@ -945,11 +946,15 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
 #pragma unroll 1
         for (int q = 0; q < NQ; ++q) {
             const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
+            double *sb = s_scl + ((size_t)q * FT + tid) * 5;  // this pixel's scales, reused by its sub-tile
             if (x < a.W && y < a.H) {
                 PixelScales ps;
                 double sx, sy, th;
                 load_cov(a, img, x, y, sx, sy, th);
                 pixel_scales(sx, sy, th, a.policy, a.clamp, R, ps);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sb[k] = ps.ap[k];
+                sb[4] = (double)(ps.basis | ((ps.drop + 1) << 1) | (ps.clamped ? 32 : 0) | (ps.flags << 8));
                 if (!(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO))) {
                     double ex = 0.0, ey = 0.0;
                     for (int k = 0; k < 4; ++k) {
@@ -1144,10 +1149,15 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             ps.clamped = 0;
             ps.ap[0] = ps.ap[1] = ps.ap[2] = ps.ap[3] = 0.0;
             const bool valid = x < a.W && y < a.H;
-            if (valid) {
-                double sx, sy, th;
-                load_cov(a, img, x, y, sx, sy, th);
-                pixel_scales(sx, sy, th, a.policy, a.clamp, R, ps);
+            if (valid) {  // the scales solved in the reach pass (same thread, same pixel)
+                const double *sb = s_scl + ((size_t)q * FT + tid) * 5;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) ps.ap[k] = sb[k];
+                const int w = (int)sb[4];
+                ps.basis = w & 1;
+                ps.drop = ((w >> 1) & 7) - 1;
+                ps.clamped = (w >> 5) & 1;
+                ps.flags = w >> 8;
             }
             const bool live = valid && !(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
             s_info[tid] = ps.basis | ((ps.drop + 1) << 1) | (live ? 16 : 0) | (ps.clamped ? 32 : 0) | (ps.flags << 8);

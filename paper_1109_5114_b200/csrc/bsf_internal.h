@@ -167,6 +167,7 @@ struct TileArgs {
     double2 *fbuf;             // fused path: per-CTA tap values [slots][fused_items<R>()]
     int stile;                 // fused path: super-tile side (32 or 64)
     int replicate;             // fused path: f outside the image = nearest image pixel
+    double *sbuf;              // fused path: per-CTA per-pixel scales [slots][FUSED_NQ_MAX][FT][5]
 };
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per device
 // (the attribute belongs to the device's context; plans may live on several
@@ -184,6 +185,7 @@ inline cudaError_t set_smem_attr(K kernel, int bytes, std::atomic<unsigned long 
 }
 
 constexpr int TILE = 16;
+constexpr int FUSED_NQ_MAX = 16;  // sub-tiles per super-tile (64 x 64)
 enum { COV_PLANES = 0, COV_ISO = 1, COV_SUB = 2 };
 cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int policy, int clamp, double *sigma2,
                                cudaStream_t st, long long *nlaunch);
