@@ -28,7 +28,10 @@
  *    errors are returned synchronously; device-side conditions (margin
  *    violation, infeasible covariance with clamp = 0) raise flags read by
  *    bsf_get_stats(), which synchronises the stream.
- *  - Thread safety: a plan may be used by one host thread at a time.
+ *  - Thread safety: a plan may be used by one host thread at a time, and its
+ *    calls must be ordered (one stream, or streams the caller serialises):
+ *    the plan's workspace (halo planes, tap and scale buffers, work counter)
+ *    is shared by its launches.  Use one plan per concurrent stream.
  */
 #ifndef BSF_H
 #define BSF_H
