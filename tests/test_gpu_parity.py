@@ -193,3 +193,33 @@ def test_config3_full_size_sampled(r):
     xs, ys = pts[:, 1].numpy(), pts[:, 2].numpy()
     ref, *_ = oracle_points(img.numpy(), cov.numpy(), xs, ys, policy=2, r=r)
     assert max_rel(got, ref) <= TOL64
+
+
+@pytest.mark.parametrize("r", [3, 4])
+def test_exact_preintegration_high_orders(r):
+    """Orders 3 and 4 (config 3 sweeps r = 1..4), both bases, wrapping mod 2^64."""
+    w = synth.workload(3, width=150, height=97)
+    img = synth.make_image(w)
+    plan = make_plan(w, policy=bsf.BSF_DUAL, order=r)
+    P, Pb = plan.geometry.margin_x, plan.geometry.margin_y
+    g = plan.empty_g_exact()
+    plan.preintegrate_exact(img.cuda(), g)
+    torch.cuda.synchronize()
+    for slot in (0, 1):
+        ref = O.preintegrate_u8(img.numpy(), slot, r, P, Pb)
+        assert np.array_equal(g[slot, 0].cpu().numpy().view(np.uint64), ref), slot
+
+
+@pytest.mark.parametrize("H,W", [(1, 1), (1, 41), (29, 1), (2, 3)])
+def test_exact_preintegration_degenerate_shapes(H, W):
+    w = synth.workload(1, width=W, height=H)
+    img = synth.make_image(w)
+    for r in (1, 2):
+        plan = make_plan(w, policy=bsf.BSF_DUAL, order=r)
+        P, Pb = plan.geometry.margin_x, plan.geometry.margin_y
+        g = plan.empty_g_exact()
+        plan.preintegrate_exact(img.cuda(), g)
+        torch.cuda.synchronize()
+        for slot in (0, 1):
+            ref = O.preintegrate_u8(img.numpy(), slot, r, P, Pb)
+            assert np.array_equal(g[slot, 0].cpu().numpy().view(np.uint64), ref), (r, slot)
