@@ -72,3 +72,13 @@ def test_table2_column_5_4_0_reproduced():
     e0, e1, basis = _errors(5.0, 4.0, 0.0)
     assert basis == O.THETA
     assert abs(e0 - 18.7) < 0.3 and abs(e1 - 14.6) < 0.3, (e0, e1)
+
+
+@pytest.mark.parametrize("s", [1.0, 5.0])
+def test_table2_isotropic_columns_algorithm1(s):
+    """(s, 1, 0) columns: 10.8 % -> 4.9 % (PAPER.md:465-467), here with
+    Algorithm 1 composed explicitly (isotropic pass at half the bound, then the
+    residual) rather than through the order-2 equivalence of R11."""
+    h, L = (0.02, 6.0) if s < 2 else (0.1, 22.0)
+    e0, e1, _ = _errors(s, 1.0, 0.0, h=h, L=L)
+    assert round(e0, 1) == 10.8 and round(e1, 1) == 4.9, (e0, e1)
