@@ -44,6 +44,7 @@ struct bsf_plan_s {
     unsigned long long *prof = nullptr;  // phase cycles of the fused kernel (diagnostics)
     double2 *fbuf = nullptr;             // fused path: per-CTA tap values
     double *sbuf = nullptr;              // fused path: per-CTA per-pixel scales
+    double *scratch0 = nullptr;          // fused path, order >= 3: rounded limb planes
     double *alg1_work = nullptr;         // Algorithm 1: float64 intermediate image
     double *alg1_work2 = nullptr;        // generalised splitting: second intermediate (ping-pong)
     void *ones = nullptr;                // DC renormalisation: image indicator (input type)
@@ -564,6 +565,12 @@ static bsf_status ensure_tile_ws(bsf_plan_s *p) {
         if (cudaMalloc(&q, sb) != cudaSuccess) return set_err(BSF_ENOMEM, "scale buffer " + std::to_string(sb));
         p->dev_allocs.push_back(q);
         p->sbuf = (double *)q;
+        if (p->d.order >= 3) {
+            const size_t b0 = (size_t)p->tile_nslots * NPLANE_MAX * p->tile_cap * sizeof(double);
+            if (cudaMalloc(&q, b0) != cudaSuccess) return set_err(BSF_ENOMEM, "limb scratch " + std::to_string(b0));
+            p->dev_allocs.push_back(q);
+            p->scratch0 = (double *)q;
+        }
     }
     if (cudaMalloc(&q, sizeof(int)) != cudaSuccess) return set_err(BSF_ENOMEM, "tile counter");
     p->dev_allocs.push_back(q);
@@ -594,6 +601,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.prof = p->prof;
     a.fbuf = p->fbuf;
     a.sbuf = p->sbuf;
+    a.scratch0 = p->scratch0;
     a.stile = p->stile;
     a.replicate = p->d.boundary == BSF_BOUNDARY_REPLICATE;
     a.sigma2_scale = 1.0;

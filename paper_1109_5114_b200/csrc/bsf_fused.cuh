@@ -39,6 +39,12 @@ constexpr uint16_t NOKEY = 0xFFFF;
 #ifndef BSF_G3_NP1
 #define BSF_G3_NP1 9  // order >= 3, unsplit numerators: n-tiles per pass (9 = all at degree 10: one pass)
 #endif
+#ifndef G3_PRESPLIT_MAX
+// order 3: halo planes up to this many points are split into their three limbs
+// once (the groups then load them); larger ones (config 5's sigma <= 64) are
+// split on the fly, where the pass over the whole domain would cost more
+#define G3_PRESPLIT_MAX 250000
+#endif
 #ifndef BSF_G3_NP2
 #define BSF_G3_NP2 3  // order >= 3, split numerators (five limb products per tile): 9 = 3 x 3 at degree 10
 #endif
@@ -490,12 +496,13 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
 // conditioning of r = 3 needs it).  With split numerators (NSPLIT 2) the two
 // exact limbs each meet n1 and n0.  The N dimension is taken in passes of NP
 // n-tiles (bounded registers); the lock-step row Horner resumes across passes.
-template <int DEG, int NSPLIT, int NP, int MT>
+template <int DEG, int NSPLIT, int NP, int MT, bool PRE>
 __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
                                                const int (&byt)[MT], double fxo, double fyo,
                                                const int2 *__restrict__ offs, const float *__restrict__ numc,
-                                               int nmonp, int n4, int shift, double sc_e, int kbits,
-                                               double (&Fh)[MT], double (&Fl)[MT], int &flags) {
+                                               int nmonp, int n4, int shift, const double *__restrict__ G0,
+                                               double sc_e, int kbits, double (&Fh)[MT], double (&Fl)[MT],
+                                               int &flags) {
     constexpr int NT = DegCfg<DEG>::NT, NL = NSPLIT == 1 ? 3 : 5, QMAX = RowCfg<DEG>::QMAX;
     const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
     // fractional offsets of this lane's items (gq + 8t), from the lanes that set them up
@@ -544,14 +551,22 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
                 // the order-3 halo planes are too large for L1 and are read from L2 anyway:
                 // bypass L1 so that it keeps the region's coefficient table
                 // (an L1 prefetch of the next step's sums evicted the table: +32 %)
-                const double2 g = __ldcg(G + (inside ? (size_t)ly * NX + lx : 0));
-                g1[t] = g2[t] = g0[t] = 0.0;
-                if (inside) {
-                    const double h = g.x * sc_e;  // exact (power of two)
-                    g1[t] = rint(h);
-                    const double r = (h - g1[t]) * S;  // exact: |h - g1| <= 1/2
-                    g2[t] = rint(r);
-                    g0[t] = (r - g2[t]) + g.y * sc_e * S;
+                const size_t gi = inside ? (size_t)ly * NX + lx : 0;
+                const double2 g = __ldcg(G + gi);
+                if constexpr (PRE) {  // (G1, G2) and G0 split once per plane
+                    const double gz = __ldcg(G0 + gi);
+                    g1[t] = inside ? g.x : 0.0;
+                    g2[t] = inside ? g.y : 0.0;
+                    g0[t] = inside ? gz : 0.0;
+                } else {  // double-double plane, split on the fly (large domains)
+                    g1[t] = g2[t] = g0[t] = 0.0;
+                    if (inside) {
+                        const double h = g.x * sc_e;  // exact (power of two)
+                        g1[t] = rint(h);
+                        const double r = (h - g1[t]) * S;  // exact: |h - g1| <= 1/2
+                        g2[t] = rint(r);
+                        g0[t] = (r - g2[t]) + g.y * sc_e * S;
+                    }
                 }
             }
             const size_t o = (size_t)s * nmonp + gq + 8 * j0;
@@ -888,6 +903,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         ph_t = t_;                                            \
     }
     double2 *scr = a.scratch + (size_t)blockIdx.x * NPLANE * a.cap;
+    double *scr0 = R >= 3 ? a.scratch0 + (size_t)blockIdx.x * NPLANE * a.cap : nullptr;  // G0 planes (order 3)
     // super-tile of ST x ST pixels = SQ x SQ sub-tiles of TILE x TILE (ST = 32 or 64, per plan)
     const int ST = a.stile, SQ = ST / TILE, NQ = SQ * SQ;
     const int nstx = (a.W + ST - 1) / ST, nsty = (a.H + ST - 1) / ST;
@@ -1015,6 +1031,10 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             const int n = -luts[b].wymin * s_dom[b][2];
             double2 *P0 = scr + s_poff[pi] - n;
             for (int i = tid; i < n; i += FT) P0[i] = make_double2(0.0, 0.0);
+            if constexpr (R >= 3) {
+                double *Q0 = scr0 + s_poff[pi] - n;
+                for (int i = tid; i < n; i += FT) Q0[i] = 0.0;
+            }
         }
         for (int b = 0; b < 2; ++b) {
             if (!s_vmask[b]) continue;
@@ -1118,8 +1138,30 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             s_pe[tid] = (m > 0.0 && !s_one[tid]) ? ilogb(m) + 1 - luts[b].var[v].kbits : 0;
         }
         __syncthreads();
+        if constexpr (R >= 3) {
+            // three limbs G = 2^e (G1 + 2^-k G2 + 2^-k G0) (fused_group_g3): (G1, G2)
+            // in place of the double-double value, G0 in its own plane
+            for (int pi = 0; pi < NPLANE; ++pi) {
+                const int b = pi / NVAR, v = pi % NVAR;
+                if (!((s_vmask[b] >> v) & 1)) continue;
+                const int n = s_dom[b][2] * s_dom[b][3];
+                if (n > G3_PRESPLIT_MAX) continue;  // large domain: split on the fly
+                double2 *G = scr + s_poff[pi];
+                double *G0p = scr0 + s_poff[pi];
+                const double sc = ldexp(1.0, -s_pe[pi]), S = ldexp(1.0, luts[b].var[v].kbits);
+                for (int i = tid; i < n; i += FT) {
+                    const double2 g = G[i];
+                    const double h = g.x * sc;  // exact (power of two)
+                    const double g1 = rint(h);
+                    const double r = (h - g1) * S;  // exact: |h - g1| <= 1/2
+                    const double g2 = rint(r);
+                    G[i] = make_double2(g1, g2);
+                    G0p[i] = (r - g2) + g.y * sc * S;
+                }
+            }
+        }
         for (int pi = 0; pi < NPLANE; ++pi) {
-            if constexpr (R >= 3) break;  // order >= 3 splits on the fly (fused_group_g3)
+            if constexpr (R >= 3) break;  // order >= 3: above
             const int b = pi / NVAR, v = pi % NVAR;
             if (!((s_vmask[b] >> v) & 1) || s_one[pi]) continue;  // s_one: already (G, 0)
             double2 *G = scr + s_poff[pi];
@@ -1324,27 +1366,37 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     if constexpr (R >= 3) {
                         // three G limbs from the double-double plane (MT = 1)
                         const size_t ro = (size_t)reg * V.nslot4 * V.nmonp;
+                        const double *G0 = scr0 + s_poff[b * NVAR + var];
                         const double sce = ldexp(1.0, -s_pe[b * NVAR + var]);
+                        const bool pre = NX * NY <= G3_PRESPLIT_MAX;
                         if (V.nsplit == 2) {
                             const float *nc = V.num32 + 2 * ro;  // (n1, n0) pairs
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 2, BSF_G3_NP2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
-                                                                             V.nmonp, n4, V.shift, sce, V.kbits, Fh,
-                                                                             Fl, flags);
+                                (pre ? (fused_group_g3<4 * R - 2, 2, BSF_G3_NP2, MT, true>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, V.shift, G0, sce, V.kbits, Fh,
+                                                                             Fl, flags)) : (fused_group_g3<4 * R - 2, 2, BSF_G3_NP2, MT, false>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, V.shift, G0, sce, V.kbits, Fh,
+                                                                             Fl, flags)));
                             else
-                                fused_group_g3<3 * R - 2, 2, BSF_G3_NP2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
-                                                                             V.nmonp, n4, V.shift, sce, V.kbits, Fh,
-                                                                             Fl, flags);
+                                (pre ? (fused_group_g3<3 * R - 2, 2, BSF_G3_NP2, MT, true>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, V.shift, G0, sce, V.kbits, Fh,
+                                                                             Fl, flags)) : (fused_group_g3<3 * R - 2, 2, BSF_G3_NP2, MT, false>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, V.shift, G0, sce, V.kbits, Fh,
+                                                                             Fl, flags)));
                         } else {
                             const float *nc = V.num32 + ro;
                             if (var == 0)
-                                fused_group_g3<4 * R - 2, 1, BSF_G3_NP1, MT>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
-                                                                             V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
-                                                                             flags);
+                                (pre ? (fused_group_g3<4 * R - 2, 1, BSF_G3_NP1, MT, true>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, 0, G0, sce, V.kbits, Fh, Fl,
+                                                                             flags)) : (fused_group_g3<4 * R - 2, 1, BSF_G3_NP1, MT, false>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, 0, G0, sce, V.kbits, Fh, Fl,
+                                                                             flags)));
                             else
-                                fused_group_g3<3 * R - 2, 1, BSF_G3_NP1, MT>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
-                                                                             V.nmonp, n4, 0, sce, V.kbits, Fh, Fl,
-                                                                             flags);
+                                (pre ? (fused_group_g3<3 * R - 2, 1, BSF_G3_NP1, MT, true>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, 0, G0, sce, V.kbits, Fh, Fl,
+                                                                             flags)) : (fused_group_g3<3 * R - 2, 1, BSF_G3_NP1, MT, false>(G, NX, NY, bxt, byt, fx, fy, offs, nc,
+                                                                             V.nmonp, n4, 0, G0, sce, V.kbits, Fh, Fl,
+                                                                             flags)));
                         }
                     } else if (R == 1 && s_one[b * NVAR + var]) {
                         if (var == 0)
@@ -1493,8 +1545,16 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
 #pragma unroll
                 for (int k = 0; k < 4; ++k) ps.ap[k] = s_ap[4 * p + k];
                 const int b = ps.basis;
-                const double sc = (R < 3 && (s_vmask[b] & 1)) ? ldexp(1.0, s_pe[b * NVAR]) : 0.0;
+                // the base plane as left by phase 3: split limbs (G1, G0) for r <= 2;
+                // at order 3 (G1, G2) plus the G0 plane when it was pre-split, else
+                // still the double-double running sums
+                const bool pre3 = R >= 3 && s_dom[b][2] * s_dom[b][3] <= G3_PRESPLIT_MAX;
+                const double sc = ((R < 3 || pre3) && (s_vmask[b] & 1)) ? ldexp(1.0, s_pe[b * NVAR]) : 0.0;
                 GView gv = {scr + s_poff[b * NVAR], s_dom[b][0], s_dom[b][1], s_dom[b][2], s_dom[b][3], sc};
+                if (pre3) {
+                    gv.g0 = scr0 + s_poff[b * NVAR];
+                    gv.sk = ldexp(1.0, -luts[b].var[0].kbits);
+                }
                 const int x = x0 + (p % TILE), y = y0 + p / TILE;
                 int fl = 0;
                 const double res = mesh_warp<R>(gv, luts[b], ps, x, y, &fl);

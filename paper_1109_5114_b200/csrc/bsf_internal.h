@@ -168,6 +168,7 @@ struct TileArgs {
     int stile;                 // fused path: super-tile side (32 or 64)
     int replicate;             // fused path: f outside the image = nearest image pixel
     double *sbuf;              // fused path: per-CTA per-pixel scales [slots][FUSED_NQ_MAX][FT][5]
+    double *scratch0;          // fused path, order >= 3: the rounded limb G0 of every plane, [slots][NPLANE][cap]
 };
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per device
 // (the attribute belongs to the device's context; plans may live on several

@@ -313,6 +313,8 @@ struct GView {
     const double2 *g;
     int X0, Y0, NX, NY;
     double sc;  // 0: double-double {hi, lo}; else split limbs (G1, G0) of G = sc (G1 + G0) (bsf_fused.cuh)
+    const double *g0 = nullptr;  // order 3: g holds (G1, G2) and g0 the third limb, G = sc (G1 + sk (G2 + G0))
+    double sk = 0.0;
 };
 
 __device__ __forceinline__ double2 load_g2(const GView &v, int qx, int qy, int *flags) {
@@ -322,8 +324,13 @@ __device__ __forceinline__ double2 load_g2(const GView &v, int qx, int qy, int *
         *flags |= FLAG_RANGE;
         return make_double2(0.0, 0.0);
     }
-    const double2 t = v.g[(size_t)ly * v.NX + lx];  // plain load: tile scratch is written in-kernel
+    const size_t i = (size_t)ly * v.NX + lx;
+    const double2 t = v.g[i];  // plain load: tile scratch is written in-kernel
     if (v.sc == 0.0) return t;
+    if (v.g0) {  // three limbs: every product below is an exact power-of-two scaling
+        const dd e = dd_add_d(two_sum(t.x * v.sc, t.y * v.sc * v.sk), v.g0[i] * v.sc * v.sk);
+        return make_double2(e.hi, e.lo);
+    }
     const dd e = two_sum(t.x * v.sc, t.y * v.sc);  // exact: power-of-two scaling of both limbs
     return make_double2(e.hi, e.lo);
 }

@@ -72,7 +72,7 @@ def test_fused_matches_double_double_kernel(config, order, n):
     assert float(rel.max()) <= (1e-12 if order < 3 else 1e-11), float(rel.max())
 
 
-@pytest.mark.parametrize("r", [1, 2])
+@pytest.mark.parametrize("r", [1, 2, 3])
 def test_forced_fallback_matches_split_path(r):
     """BSF_SPLIT_TOL=0 sends every pixel to the warp-cooperative double-double
     fallback (mesh_warp on the split planes); it must agree with the split
@@ -88,7 +88,7 @@ def test_forced_fallback_matches_split_path(r):
     st = plan.stats(reset=True)
     assert st["double_double"] == st["pixels"] == H * W
     rel = (a - b).abs() / b.abs()
-    assert float(rel.max()) <= 1e-12, float(rel.max())
+    assert float(rel.max()) <= (1e-12 if r < 3 else 1e-11), float(rel.max())
 
 
 def test_macs_counter_is_the_algorithmic_work():
