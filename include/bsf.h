@@ -276,6 +276,17 @@ long long bsf_launch_count(bsf_plan_t plan);
  * `reset`.  bsf_uses_fused: 1 when the tile path runs the exact split
  * contraction kernel (known after the first tile-path call), else 0.        */
 bsf_status bsf_debug_phase_cycles(bsf_plan_t plan, unsigned long long *out, int reset);
+/* bsf_debug_item_cycles (after bsf_debug_phase_cycles enabled the counters):
+ * host `items[i]` = SM cycles of fused-path work item i (super-tile, in the
+ * order the atomic counter hands them out; i < min(nitems, 8192)) in the last
+ * run; host `work[4i .. 4i+3]` (may be NULL) = its interpolation MACs, its
+ * double-double fallback pixels, the halo domain points of the bases it
+ * pre-integrates and its number of planes; host `ctas[c]` = busy cycles of CTA
+ * c summed since the last reset (c < min(nctas, 1024)).  `items` may be NULL
+ * with nitems 0, `ctas` with nctas 0.  BSF_EINVAL when the counters are not
+ * enabled.                                                                  */
+bsf_status bsf_debug_item_cycles(bsf_plan_t plan, unsigned long long *items, unsigned long long *work, int nitems,
+                                 unsigned long long *ctas, int nctas);
 int bsf_uses_fused(bsf_plan_t plan);
 
 const char *bsf_status_str(bsf_status s);

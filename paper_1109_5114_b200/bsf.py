@@ -100,6 +100,8 @@ def lib():
         L.bsf_launch_count.argtypes = [vp]
         L.bsf_debug_phase_cycles.restype = st
         L.bsf_debug_phase_cycles.argtypes = [vp, vp, i]
+        L.bsf_debug_item_cycles.restype = st
+        L.bsf_debug_item_cycles.argtypes = [vp, vp, vp, i, vp, i]
         L.bsf_uses_fused.restype = i
         L.bsf_uses_fused.argtypes = [vp]
         L.bsf_status_str.restype = ctypes.c_char_p
@@ -248,6 +250,17 @@ class Plan:
         buf = (ctypes.c_ulonglong * 16)()
         _check(lib().bsf_debug_phase_cycles(self.handle, buf, int(reset)))
         return list(buf)
+
+    def item_cycles(self, nitems, nctas=0):
+        """(per-item cycles of the last run, per-item (MACs, fallback pixels,
+        halo points, planes), per-CTA busy cycles since the last reset) of the
+        fused tile kernel; phase_cycles() must have enabled the counters."""
+        it = (ctypes.c_ulonglong * max(nitems, 1))()
+        wk = (ctypes.c_ulonglong * max(4 * nitems, 1))()
+        ct = (ctypes.c_ulonglong * max(nctas, 1))()
+        _check(lib().bsf_debug_item_cycles(self.handle, it, wk, int(nitems), ct, int(nctas)))
+        wl = list(wk)
+        return list(it)[:nitems], [tuple(wl[4 * i:4 * i + 4]) for i in range(nitems)], list(ct)[:nctas]
 
     def uses_fused(self):
         return bool(lib().bsf_uses_fused(self.handle))

@@ -3,6 +3,7 @@
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <algorithm>
 #include <string.h>
 
 #include <string>
@@ -51,6 +52,10 @@ struct bsf_plan_s {
     double *norm_den = nullptr;          // DC renormalisation: filtered indicator
     double *alg1_sigma2 = nullptr;       // Algorithm 1: sigma_b^2 per covariance field (+ reduction bits)
     int *tile_counter = nullptr;
+    int *sched_order = nullptr;          // fused path: work order of the super-tiles (largest first)
+    unsigned char *sched_bin = nullptr;
+    unsigned *sched_hist = nullptr;
+    long long sched_cap = 0;
     long long nlaunch = 0;
     cudaStream_t last = nullptr;
 };
@@ -146,8 +151,10 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         std::vector<int2> offs((size_t)nreg * V.nmax, make_int2(0, 0));
         std::vector<double> num((size_t)nreg * V.nmax * V.nmon, 0.0);
         std::vector<double2> coef(num.size());
+        double csum = 0.0;
         for (uint32_t r = 0; r < nreg; ++r) {
             take(&counts[r], 4);
+            csum += counts[r];
             for (int s = 0; s < V.nmax; ++s) {
                 int o[2];
                 take(o, 8);
@@ -211,6 +218,7 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         while (ldexp(1.0, cm) < colmax) ++cm;
         V.kbits = exact ? 53 - cm : 0;  // no integer form: the fused path is unavailable
         V.L = L;
+        V.mean_count = nreg ? (float)(csum / nreg) : 0.f;
         V.nsplit = 1;
         V.shift = 0;
         V.num2 = V.numf = nullptr;
@@ -575,6 +583,18 @@ static bsf_status ensure_tile_ws(bsf_plan_s *p) {
     if (cudaMalloc(&q, sizeof(int)) != cudaSuccess) return set_err(BSF_ENOMEM, "tile counter");
     p->dev_allocs.push_back(q);
     p->tile_counter = (int *)q;
+    if (p->fused) {
+        // largest-first work order of the super-tiles (launch_fused_impl)
+        const long long n = (long long)((p->geo.W + p->stile - 1) / p->stile) * ((p->geo.H + p->stile - 1) / p->stile) *
+                            p->geo.nimg;
+        const size_t ob = (size_t)n * (sizeof(int) + 1) + 2 * SCHED_NBIN * sizeof(unsigned) + 16;
+        if (cudaMalloc(&q, ob) != cudaSuccess) return set_err(BSF_ENOMEM, "work order " + std::to_string(ob));
+        p->dev_allocs.push_back(q);
+        p->sched_hist = (unsigned *)q;
+        p->sched_order = (int *)((char *)q + 2 * SCHED_NBIN * sizeof(unsigned));
+        p->sched_bin = (unsigned char *)(p->sched_order + n);
+        p->sched_cap = n;
+    }
     return BSF_OK;
 }
 
@@ -605,6 +625,14 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.stile = p->stile;
     a.replicate = p->d.boundary == BSF_BOUNDARY_REPLICATE;
     a.sigma2_scale = 1.0;
+    // BSF_ORDER=0 (environment, diagnostics): hand the super-tiles out in raster order
+    const char *ord = getenv("BSF_ORDER");
+    if (!(ord && ord[0] == '0')) {
+        a.order = p->sched_order;
+        a.order_bin = p->sched_bin;
+        a.order_hist = p->sched_hist;
+        a.order_cap = p->sched_cap;
+    }
     // BSF_SPLIT_TOL (environment, diagnostics): override the fallback threshold
     const char *tol = getenv("BSF_SPLIT_TOL");
     a.split_tol = tol ? atof(tol) : BSF_SPLIT_TOL_DEFAULT;
@@ -828,16 +856,37 @@ extern "C" bsf_status bsf_debug_phase_cycles(bsf_plan_t p, unsigned long long *o
     if (!p) return set_err(BSF_EINVAL, "null plan");
     if (!p->prof) {
         void *q;
-        CUDA_TRY(cudaMalloc(&q, 16 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMalloc(&q, BSF_PROF_WORDS * sizeof(unsigned long long)));
         p->dev_allocs.push_back(q);
         p->prof = (unsigned long long *)q;
-        CUDA_TRY(cudaMemset(q, 0, 16 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemset(q, 0, BSF_PROF_WORDS * sizeof(unsigned long long)));
     }
     if (out) {
         CUDA_TRY(cudaStreamSynchronize(p->last));
         CUDA_TRY(cudaMemcpy(out, p->prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     }
-    if (reset) CUDA_TRY(cudaMemset(p->prof, 0, 16 * sizeof(unsigned long long)));
+    if (reset) CUDA_TRY(cudaMemset(p->prof, 0, BSF_PROF_WORDS * sizeof(unsigned long long)));
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_debug_item_cycles(bsf_plan_t p, unsigned long long *items, unsigned long long *work,
+                                            int nitems, unsigned long long *ctas, int nctas) {
+    if (!p) return set_err(BSF_EINVAL, "null plan");
+    if (!p->prof) return set_err(BSF_EINVAL, "enable the counters with bsf_debug_phase_cycles first");
+    if (nitems < 0 || nctas < 0 || (nitems && !items) || (nctas && !ctas))
+        return set_err(BSF_EINVAL, "bad output buffers");
+    CUDA_TRY(cudaStreamSynchronize(p->last));
+    if (nitems)
+        CUDA_TRY(cudaMemcpy(items, p->prof + 16, (size_t)std::min(nitems, BSF_PROF_ITEMS) * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost));
+    if (nitems && work)
+        CUDA_TRY(cudaMemcpy(work, p->prof + BSF_PROF_WORK,
+                            4 * (size_t)std::min(nitems, BSF_PROF_ITEMS) * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost));
+    if (nctas)
+        CUDA_TRY(cudaMemcpy(ctas, p->prof + 16 + BSF_PROF_ITEMS,
+                            (size_t)std::min(nctas, BSF_PROF_CTAS) * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost));
     return BSF_OK;
 }
 

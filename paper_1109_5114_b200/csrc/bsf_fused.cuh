@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     __syncthreads();
     // optional phase timing (TileArgs::prof, diagnostics only): thread 0 adds
     // the SM cycles spent in each phase
-    long long ph_t = clock64();
+    long long ph_t = clock64(), t_item = ph_t;
 #define FUSED_PHASE(k)                                        \
     if (a.prof && tid == 0) {                                 \
         const long long t_ = clock64();                       \
@@ -921,9 +921,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (tid < NPLANE) s_pmax[tid] = 0ull;
         if (tid == 0) s_nfb = 0;
         __syncthreads();
-        const int item = s_item;
-        if (item >= nitems) break;
-        if (a.prof && tid == 0) ph_t = clock64();
+        if (s_item >= nitems) break;
+        const int item = a.order && !a.pts ? a.order[s_item] : s_item;
+        if (a.prof && tid == 0) ph_t = t_item = clock64();
         // super-tile origin (X0s, Y0s): the running sums are anchored on its
         // halo domain; its four TILE x TILE sub-tiles are gathered in turn
         int img, X0s, Y0s, want = -1, qwant = -1;
@@ -1580,12 +1580,30 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         }
         }  // sub-tiles
         __syncthreads();
+        if (a.prof && tid == 0 && item < BSF_PROF_ITEMS) {
+            // per-item work (bsf_debug_item_cycles): interpolation MACs, fallback pixels,
+            // halo domain points of the bases in use, planes
+            unsigned long long halo = 0, planes = 0;
+            for (int b = 0; b < 2; ++b)
+                if (s_vmask[b]) halo += (unsigned long long)s_dom[b][2] * s_dom[b][3];
+            for (int pi = 0; pi < NPLANE; ++pi) planes += s_poff[pi] >= 0;
+            a.prof[BSF_PROF_WORK + 4 * item] = s_stats[6];
+            a.prof[BSF_PROF_WORK + 4 * item + 1] = s_stats[5];
+            a.prof[BSF_PROF_WORK + 4 * item + 2] = halo;
+            a.prof[BSF_PROF_WORK + 4 * item + 3] = planes;
+        }
         if (tid < 8 && a.stats && s_stats[tid]) {
             if (tid == 4)
                 atomicOr(a.stats + 4, s_stats[4]);
             else
                 atomicAdd(a.stats + tid, s_stats[tid]);
             s_stats[tid] = 0ull;
+        }
+        if (a.prof && tid == 0) {
+            // per-item and per-CTA busy cycles (bsf_debug_item_cycles)
+            const unsigned long long dt = (unsigned long long)(clock64() - t_item);
+            if (item < BSF_PROF_ITEMS) a.prof[16 + item] = dt;
+            if (blockIdx.x < BSF_PROF_CTAS) atomicAdd(a.prof + 16 + BSF_PROF_ITEMS + blockIdx.x, dt);
         }
     }
 }
@@ -1651,6 +1669,113 @@ cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int po
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Work order of the persistent kernel: the super-tiles' interpolation work
+// varies several-fold (variants and bases per pixel; profiles/README.md v13),
+// so a raster hand-out leaves the CTAs that draw the last heavy tiles running
+// alone.  fused_cost_kernel estimates each super-tile's work from 64 sampled
+// pixels (their scales as in the reach pass): the interpolation MACs (taps x
+// mean window slots x monomials of the table each pixel uses) plus the
+// pre-integration (halo points x planes, weighted), and bins it on a log
+// scale (four bins per octave); fused_order_kernel lists the super-tiles heaviest bin
+// first (within a bin in any order).  The order changes nothing but which CTA
+// computes a super-tile and when: each super-tile's arithmetic is the same.
+// ---------------------------------------------------------------------------
+// MAC-equivalents of one halo-plane point of the pre-integration (sweep and
+// split), fitted on the measured per-super-tile cycles (tools/item_balance.py:
+// cycles ~ a MACs + b halo-points x planes; b/a ~ 10 at r = 1, 140-180 at r = 2;
+// at r = 3 the MACs alone explain 98 %)
+template <int R>
+__device__ __forceinline__ float sched_halo_weight() {
+    return R == 1 ? 10.f : R == 2 ? 160.f : 0.f;  // (order 1 keeps raster order, launch_fused_impl)
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) fused_cost_kernel(TileArgs a, const LutBasis *__restrict__ luts, int nitems) {
+    constexpr int NTAP = FusedCfg<R>::NTAP;
+    const int lane = threadIdx.x & 31, item = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (item >= nitems) return;
+    const int ST = a.stile, nstx = (a.W + ST - 1) / ST, spi = nstx * ((a.H + ST - 1) / ST);
+    const int img = item / spi, rem = item % spi, X0s = (rem % nstx) * ST, Y0s = (rem / nstx) * ST;
+    const int step = ST / 8;
+    float acc = 0.f;
+    int ex[2] = {0, 0}, ey[2] = {0, 0}, vm[2] = {0, 0};
+    if (!(a.cov_mode == COV_ISO && !(a.sigma2[img / a.channels] > 0.0))) {
+        for (int s = lane; s < 64; s += 32) {
+            const int x = X0s + (s & 7) * step + step / 2, y = Y0s + (s >> 3) * step + step / 2;
+            if (x < a.W && y < a.H) {
+                double sx, sy, th;
+                load_cov(a, img, x, y, sx, sy, th);
+                PixelScales ps;
+                pixel_scales(sx, sy, th, a.policy, a.clamp, R, ps);
+                if (!(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO))) {
+                    const LutVar &V = luts[ps.basis].var[ps.drop + 1];
+                    acc += (float)(ps.drop >= 0 ? NTAP / (R + 1) : NTAP) * V.mean_count * (float)V.nmon;
+                    double rx = 0.0, ry = 0.0;  // the reach, as in the kernel's reach pass
+                    for (int k = 0; k < 4; ++k) {
+                        rx += ps.ap[k] * abs(c_steps[ps.basis][k][0]);
+                        ry += ps.ap[k] * c_steps[ps.basis][k][1];
+                    }
+                    ex[ps.basis] = max(ex[ps.basis], (int)ceil(0.5 * R * rx));
+                    ey[ps.basis] = max(ey[ps.basis], (int)ceil(0.5 * R * ry));
+                    vm[ps.basis] |= 1 << (ps.drop + 1);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            ex[b] = max(ex[b], __shfl_xor_sync(0xffffffffu, ex[b], o));
+            ey[b] = max(ey[b], __shfl_xor_sync(0xffffffffu, ey[b], o));
+            vm[b] |= __shfl_xor_sync(0xffffffffu, vm[b], o);
+        }
+    }
+    if (lane == 0) {
+        float cost = acc * (float)(ST * ST) / 64.f;  // sampled MACs scaled to the super-tile
+        for (int b = 0; b < 2; ++b)
+            if (vm[b]) {
+                const TileDomain d = fused_domain(luts[b], R, X0s, Y0s, ex[b], ey[b], ST);
+                cost += sched_halo_weight<R>() * (float)d.NX * (float)d.NY * (float)__popc(vm[b] | 1);
+            }
+        const int b = cost >= 1.f ? min(SCHED_NBIN - 1, 1 + (int)(4.f * __log2f(cost))) : 0;
+        a.order_bin[item] = (unsigned char)b;
+        atomicAdd(a.order_hist + b, 1u);
+    }
+}
+
+__global__ void __launch_bounds__(256) fused_order_kernel(TileArgs a, int nitems) {
+    static_assert(SCHED_NBIN == 128, "four bins per lane");
+    __shared__ unsigned base[SCHED_NBIN];
+    if (threadIdx.x < 32) {
+        // exclusive scan over the bins in descending order: lane l owns bins
+        // 127 - 4l ... 124 - 4l
+        const int lane = threadIdx.x;
+        unsigned h[4], t = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) t += (h[k] = a.order_hist[SCHED_NBIN - 1 - 4 * lane - k]);
+        unsigned inc = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        unsigned run = inc - t;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            base[SCHED_NBIN - 1 - 4 * lane - k] = run;
+            run += h[k];
+        }
+    }
+    __syncthreads();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
+        const int b = a.order_bin[i];
+        a.order[base[b] + atomicAdd(a.order_hist + SCHED_NBIN + b, 1u)] = i;
+    }
+}
+
 template <int R>
 static cudaError_t launch_fused_r(const TileArgs &a, int slots, cudaStream_t st, const LutBasis *luts) {
     constexpr size_t sm = fused_smem_bytes<R>();
@@ -1682,11 +1807,33 @@ cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStrea
                               long long *nl) {
     cudaMemsetAsync(a.counter, 0, sizeof(int), st);
     cudaError_t e;
+    TileArgs b = a;
+    const long long nitems = (long long)((a.W + a.stile - 1) / a.stile) * ((a.H + a.stile - 1) / a.stile) * a.nimg;
+    if (a.order && !a.pts && order >= 2 && nitems >= 2 * (long long)slots && nitems <= a.order_cap) {
+        // largest-first work order (see fused_cost_kernel); at order 1 the
+        // balance it gains (3.7 -> 1.2 % on config 3) is lost to the halo reads
+        // of raster neighbours no longer sharing L2, so raster order stays
+        cudaMemsetAsync(a.order_hist, 0, 2 * SCHED_NBIN * sizeof(unsigned), st);
+        const int nb = (int)((nitems + 7) / 8);
+        switch (order) {
+            case 1: fused_cost_kernel<1><<<nb, 256, 0, st>>>(a, luts, (int)nitems); break;
+            case 2: fused_cost_kernel<2><<<nb, 256, 0, st>>>(a, luts, (int)nitems); break;
+            case 3: fused_cost_kernel<3><<<nb, 256, 0, st>>>(a, luts, (int)nitems); break;
+            case 4: fused_cost_kernel<4><<<nb, 256, 0, st>>>(a, luts, (int)nitems); break;
+            default: return cudaErrorInvalidValue;
+        }
+        fused_order_kernel<<<(int)std::min<long long>((nitems + 255) / 256, 4 * (long long)slots), 256, 0, st>>>(
+            a, (int)nitems);
+        *nl += 2;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    } else {
+        b.order = nullptr;
+    }
     switch (order) {
-        case 1: e = launch_fused_r<1>(a, slots, st, luts); break;
-        case 2: e = launch_fused_r<2>(a, slots, st, luts); break;
-        case 3: e = launch_fused_r<3>(a, slots, st, luts); break;
-        case 4: e = launch_fused_r<4>(a, slots, st, luts); break;
+        case 1: e = launch_fused_r<1>(b, slots, st, luts); break;
+        case 2: e = launch_fused_r<2>(b, slots, st, luts); break;
+        case 3: e = launch_fused_r<3>(b, slots, st, luts); break;
+        case 4: e = launch_fused_r<4>(b, slots, st, luts); break;
         default: return cudaErrorInvalidValue;
     }
     ++*nl;

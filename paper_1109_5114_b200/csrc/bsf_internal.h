@@ -105,6 +105,7 @@ struct LutVar {
     const double *numf;    // [nreg][nslot4][nmonp] n (nsplit 2: the G0 limb's operand)
     const float *num32;    // order >= 3, when exact in fp32: [nreg][nslot4][nmonp] n (nsplit 1) or
                            // interleaved (n1, n0) pairs (nsplit 2) -- half the bytes of the MMA's B loads
+    float mean_count;      // window slots averaged over the regions (work-item cost estimate)
     double bnd;            // bound on |F - F^| (units 2^e) of the split contraction: gamma_{n+1} 0.5 max_reg sum_s,mu |n|
     double L;              // common denominator
 };
@@ -169,7 +170,14 @@ struct TileArgs {
     int replicate;             // fused path: f outside the image = nearest image pixel
     double *sbuf;              // fused path: per-CTA per-pixel scales [slots][FUSED_NQ_MAX][FT][5]
     double *scratch0;          // fused path, order >= 3: the rounded limb G0 of every plane, [slots][NPLANE][cap]
+    // fused path work order (optional): order[i] = super-tile handed out i-th,
+    // largest estimated work first (fused_cost_kernel / fused_order_kernel)
+    int *order;
+    unsigned char *order_bin;  // [items] cost bin of each super-tile
+    unsigned *order_hist;      // [2][SCHED_NBIN] bin counts, scatter cursors
+    long long order_cap;       // items the order buffers hold
 };
+constexpr int SCHED_NBIN = 128;
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per device
 // (the attribute belongs to the device's context; plans may live on several
 // devices of one process).  `done` is the caller's per-kernel flag array.
@@ -187,6 +195,11 @@ inline cudaError_t set_smem_attr(K kernel, int bytes, std::atomic<unsigned long 
 
 constexpr int TILE = 16;
 constexpr int FUSED_NQ_MAX = 16;  // sub-tiles per super-tile (64 x 64)
+// diagnostics buffer (TileArgs::prof): 16 phase counters, then the busy cycles
+// of the first BSF_PROF_ITEMS work items, then those of the first BSF_PROF_CTAS CTAs
+constexpr int BSF_PROF_ITEMS = 8192, BSF_PROF_CTAS = 1024;
+constexpr int BSF_PROF_WORK = 16 + BSF_PROF_ITEMS + BSF_PROF_CTAS;  // then 4 work figures per item
+constexpr int BSF_PROF_WORDS = BSF_PROF_WORK + 4 * BSF_PROF_ITEMS;
 enum { COV_PLANES = 0, COV_ISO = 1, COV_SUB = 2 };
 cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int policy, int clamp, double *sigma2,
                                cudaStream_t st, long long *nlaunch);

@@ -178,3 +178,29 @@ def test_run_host_matches_device_run():
     plan.run_host(f_h, c_h, o_h)
     torch.cuda.synchronize()
     assert torch.equal(o_h, dev)
+
+
+@pytest.mark.parametrize("r", [2, 3])
+def test_work_order_changes_nothing_but_the_schedule(r):
+    """The largest-first hand-out of super-tiles (fused_cost_kernel /
+    fused_order_kernel) only changes which CTA computes a super-tile and when:
+    the output is bit-identical to the raster hand-out, and the two scheduling
+    launches are counted."""
+    if r == 2:
+        w = synth.workload(2, width=640, height=480)  # 300 super-tiles
+        img = synth.make_image(w)[None]
+    else:
+        w = synth.workload(4, width=608, height=512)  # 3 channels x 304 super-tiles
+        img = torch.stack([synth.make_image(w, channel=c) for c in range(w.channels)])
+    cov = synth.make_cov(w)
+    runs = {}
+    for o in ("0", "1"):
+        with _env(BSF_ORDER=o):
+            plan = make_plan(w, anchor=TILE, batch=1)
+            n0 = plan.launch_count()
+            out = gpu_full(plan, img, cov)
+            runs[o] = (out, plan.launch_count() - n0, plan.stats())
+    assert torch.equal(runs["0"][0], runs["1"][0])
+    assert runs["1"][1] == runs["0"][1] + 2
+    for k in ("pixels", "macs", "double_double"):
+        assert runs["0"][2][k] == runs["1"][2][k], k
