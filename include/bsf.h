@@ -271,7 +271,8 @@ long long bsf_launch_count(bsf_plan_t plan);
  * measured from the previous mark: 0 reach pass, 1 zero pad rows, 11 the
  * running-sum sweeps, 12 the zero-scale variant planes, 2 exact split,
  * 8 sub-tile scales, 9 keys, 10 bucket scan, 3 scatter, 4 gather,
- * 5 accumulation; 6-7 warp-cycles of the MMA groups) to host `out`
+ * 5 accumulation; 6-7 warp-cycles of the MMA groups; 13 executed MMA
+ * multiply-adds per limb incl. padding, 14 real items, 15 group slots) to host `out`
  * (may be NULL) after synchronising the plan's last stream, and zero them when
  * `reset`.  bsf_uses_fused: 1 when the tile path runs the exact split
  * contraction kernel (known after the first tile-path call), else 0.        */

@@ -1361,6 +1361,14 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                             atomicAdd(&s_stats[6], (unsigned long long)nreal * __ldg(V.counts + reg) *
                                                        (var == 0 ? DegCfg<4 * R - 2>::NMON : DegCfg<3 * R - 2>::NMON));
                     }
+                    if (a.prof) {  // diagnostics: group fill, executed (padded) MMA MACs per limb
+                        const unsigned nreal = __popc(__ballot_sync(0xffffffffu, real));
+                        if (lane == 0) {
+                            atomicAdd(a.prof + 13, (unsigned long long)GS * n4 * V.nmonp);
+                            atomicAdd(a.prof + 14, (unsigned long long)nreal);
+                            atomicAdd(a.prof + 15, (unsigned long long)GS);
+                        }
+                    }
                     long long tq0 = 0;
                     if (a.prof && lane == 0) tq0 = clock64();
                     if constexpr (R >= 3) {

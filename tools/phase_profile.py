@@ -44,3 +44,7 @@ for n, c in (("sub-tile scales", cyc[8]), ("keys", cyc[9]), ("bucket scan", cyc[
     print("%-16s %6.1f%%  %.3e cycles" % (n, 100.0 * c / tot, c))
 print("gather groups: warp-cycles total %.3e, full-variant MMA loop %.3e (per-CTA wall equivalent /8: %.3e, %.3e)"
       % (cyc[6], cyc[7], cyc[6] / 8, cyc[7] / 8))
+if cyc[15]:
+    # executed MMA work per limb (incl. item, window-slot and column padding) vs the algorithmic MACs
+    print("MMA padding: item fill %.3f (%d real / %d group slots), executed/algorithmic MACs per limb %.3f"
+          % (cyc[14] / cyc[15], cyc[14], cyc[15], cyc[13] / max(st["macs"], 1)))
