@@ -368,13 +368,17 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     g.GH = g.H + g.Pb;
     g.nimg = d.batch * d.channels;
     // super-tile of the fused path: the halo domain per super-tile grows with
-    // the reach E = max_sigma sqrt(24 r); at order 1, 64 x 64 super-tiles
-    // amortise it over 4x the pixels once E is large (config 3: +33 %); at
-    // r >= 2 the larger domains push pixels to the double-double fallback
-    // (BSF_STILE = 32 / 64 overrides, diagnostics)
+    // the reach E = max_sigma sqrt(24 r); 64 x 64 super-tiles amortise it over
+    // 4x the pixels once E is large: order 1 (config 3: +33 %) and order 2
+    // with u8 input (config 3: +20 %, 0.03 % of the pixels to the fallback).
+    // Otherwise the larger domains push pixels to the double-double fallback
+    // (config 2, f32, r = 2: 85k pixels, 16x slower; u8 r = 3: 3x slower);
+    // the passes of bsf_run_split run 32 x 32 at order 2 for that reason.
+    // (BSF_STILE = 16 / 32 / 64 overrides, diagnostics)
     {
         const double E = (double)d.max_sigma * sqrt(24.0 * d.order);
-        p->stile = (d.order == 1 && E > BSF_STILE64_REACH) ? 64 : 32;  // r >= 2: larger domains cost precision
+        const bool big = d.order == 1 || (d.order == 2 && d.in_dtype == BSF_U8);
+        p->stile = (big && E > BSF_STILE64_REACH) ? 64 : 32;
         // small images: 16 x 16 super-tiles when 32 x 32 ones would leave most
         // SMs idle (config 1: 16 super-tiles for 148 SMs)
         const long long n32 = (long long)((d.width + 31) / 32) * ((d.height + 31) / 32) * d.batch * d.channels;
@@ -585,8 +589,8 @@ static bsf_status ensure_tile_ws(bsf_plan_s *p) {
     p->tile_counter = (int *)q;
     if (p->fused) {
         // largest-first work order of the super-tiles (launch_fused_impl)
-        const long long n = (long long)((p->geo.W + p->stile - 1) / p->stile) * ((p->geo.H + p->stile - 1) / p->stile) *
-                            p->geo.nimg;
+        const int ts = p->stile == 64 && p->d.order >= 2 ? 32 : p->stile;  // bsf_run_split's float64 passes
+        const long long n = (long long)((p->geo.W + ts - 1) / ts) * ((p->geo.H + ts - 1) / ts) * p->geo.nimg;
         const size_t ob = (size_t)n * (sizeof(int) + 1) + 2 * SCHED_NBIN * sizeof(unsigned) + 16;
         if (cudaMalloc(&q, ob) != cudaSuccess) return set_err(BSF_ENOMEM, "work order " + std::to_string(ob));
         p->dev_allocs.push_back(q);
@@ -778,6 +782,10 @@ extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov
             a.in_u8 = 0;
             a.in_f64 = 1;
         }
+        // 64 x 64 anchoring at order 2 only for the plain u8 run: the small
+        // isotropic scales of these passes (and float64 input) send every pixel
+        // of a 64 x 64 domain to the fallback (config 3: 16.8M of 16.8M)
+        if (p->d.order >= 2) a.stile = std::min(a.stile, 32);
         a.cov_mode = COV_ISO;
         a.sigma2 = p->alg1_sigma2;
         a.sigma2_scale = 2.0 * phi / (n - 1.0);
@@ -788,6 +796,7 @@ extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov
     TileArgs a = tile_args(p, src, cov, out);
     a.in_u8 = 0;
     a.in_f64 = 1;
+    if (p->d.order >= 2) a.stile = std::min(a.stile, 32);
     a.cov_mode = COV_SUB;
     a.sigma2 = p->alg1_sigma2;
     a.sigma2_scale = 2.0 * phi;

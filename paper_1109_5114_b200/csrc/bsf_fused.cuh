@@ -440,6 +440,22 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
                 if constexpr (LIMBS == 2) dmma(C[t][1][j], aB[t].y, bB[j]);
             }
     }
+#ifdef BSF_DBG_NO_EPI
+    // diagnostics build only (timing of the MMA loop without the polynomial
+    // epilogue; results are wrong): keep every accumulator live
+    {
+        double s0 = fxo + fyo;
+#pragma unroll
+        for (int t = 0; t < MT; ++t)
+#pragma unroll
+            for (int L = 0; L < 2; ++L)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) s0 += C[t][L][j][0] + C[t][L][j][1];
+#pragma unroll
+        for (int t = 0; t < MT; ++t) Fh[t] = Fl[t] = s0;
+        return;
+    }
+#endif
     if constexpr (MT == 4) {
         // rows of all four m-tiles on their owner lanes; then lane kq of each
         // quad runs the x-Horner of m-tile kq only (one x-Horner per lane

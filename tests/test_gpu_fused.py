@@ -204,3 +204,36 @@ def test_work_order_changes_nothing_but_the_schedule(r):
     assert runs["1"][1] == runs["0"][1] + 2
     for k in ("pixels", "macs", "double_double"):
         assert runs["0"][2][k] == runs["1"][2][k], k
+
+
+def test_order2_u8_super_tile_64():
+    """u8 input at order 2 with a large reach anchors on 64 x 64 super-tiles
+    (its exact low levels keep the larger domains accurate); the output agrees
+    with the 32 x 32 anchoring and with the oracle to the 1e-9 contract, and
+    bsf_run_split's float64 passes (which run 32 x 32) agree too."""
+    w = synth.workload(3, order=2, width=330, height=200)
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    dev = torch.device("cuda:0")
+    p64 = make_plan(w, anchor=TILE)
+    assert p64.geometry.super_tile == 64
+    a = gpu_full(p64, img[None], cov)
+    with _env(BSF_STILE=32):
+        p32 = make_plan(w, anchor=TILE)
+        assert p32.geometry.super_tile == 32
+        b = gpu_full(p32, img[None], cov)
+    rel = ((a - b).abs() / b.abs()).max()
+    assert float(rel) <= 2e-9, float(rel)
+    from gpu_util import oracle_points
+    pts = synth.sample_points(w, 24, seed=11)
+    xs, ys = pts[:, 1].numpy(), pts[:, 2].numpy()
+    ref = oracle_points(img.numpy(), cov.numpy(), xs, ys, policy=w.basis, r=2)[0]
+    err = np.max(np.abs(a[0].numpy()[ys, xs] - ref) / np.abs(ref))
+    assert err <= 1e-9, err
+    outs = []
+    for p in (p64, p32):
+        o = torch.empty((1, w.height, w.width), dtype=torch.float64, device=dev)
+        p.run_alg1(img[None].to(dev).contiguous(), cov.to(dev).contiguous(), o)
+        torch.cuda.synchronize()
+        outs.append(o.cpu())
+    rel = ((outs[0] - outs[1]).abs() / outs[1].abs()).max()
+    assert float(rel) <= 2e-9, float(rel)
