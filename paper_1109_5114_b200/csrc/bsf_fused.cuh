@@ -1685,7 +1685,8 @@ cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int po
                                cudaStream_t st, long long *nl) {
     // sigma2 holds 2 * batch doubles: [0, batch) results, [batch, 2 batch) min bits
     unsigned long long *bits = reinterpret_cast<unsigned long long *>(sigma2 + batch);
-    cudaMemsetAsync(bits, 0x7f, batch * sizeof(unsigned long long), st);  // a large positive double
+    cudaError_t e = cudaMemsetAsync(bits, 0x7f, batch * sizeof(unsigned long long), st);  // a large positive double
+    if (e != cudaSuccess) return e;
     const int blocks = (int)((size_t)H * W / 256 + 1 < 1184 ? (size_t)H * W / 256 + 1 : 1184);
     alg1_bound_kernel<<<dim3(blocks, batch), 256, 0, st>>>(cov, W, H, policy, clamp, bits);
     alg1_finish_kernel<<<1, 1024, 0, st>>>(bits, batch, sigma2);
@@ -1829,15 +1830,15 @@ int fused_slots() {
 
 cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStream_t st, const LutBasis *luts,
                               long long *nl) {
-    cudaMemsetAsync(a.counter, 0, sizeof(int), st);
-    cudaError_t e;
+    cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
     TileArgs b = a;
     const long long nitems = (long long)((a.W + a.stile - 1) / a.stile) * ((a.H + a.stile - 1) / a.stile) * a.nimg;
     if (a.order && !a.pts && order >= 2 && nitems >= 2 * (long long)slots && nitems <= a.order_cap) {
         // largest-first work order (see fused_cost_kernel); at order 1 the
         // balance it gains (3.7 -> 1.2 % on config 3) is lost to the halo reads
         // of raster neighbours no longer sharing L2, so raster order stays
-        cudaMemsetAsync(a.order_hist, 0, 2 * SCHED_NBIN * sizeof(unsigned), st);
+        if ((e = cudaMemsetAsync(a.order_hist, 0, 2 * SCHED_NBIN * sizeof(unsigned), st)) != cudaSuccess) return e;
         const int nb = (int)((nitems + 7) / 8);
         switch (order) {
             case 1: fused_cost_kernel<1><<<nb, 256, 0, st>>>(a, luts, (int)nitems); break;

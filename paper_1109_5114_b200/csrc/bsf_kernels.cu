@@ -850,7 +850,8 @@ static void launch_tile_r(const TileArgs &a, int prec, int slots, cudaStream_t s
 
 cudaError_t launch_tile_impl(const TileArgs &a, int order, int prec, int slots, cudaStream_t st,
                              const LutBasis *luts, long long *nl) {
-    cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+    const cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
     switch (order) {
         case 1: launch_tile_r<1>(a, prec, slots, st, luts); break;
         case 2: launch_tile_r<2>(a, prec, slots, st, luts); break;
