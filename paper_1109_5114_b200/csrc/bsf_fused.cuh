@@ -283,10 +283,13 @@ __device__ __forceinline__ void fused_rows(const double (&C)[2][NT][2], double f
                            : kq == 2 ? bsf_valid_mask(DEG, 2) : bsf_valid_mask(DEG, 3);
 #pragma unroll
     for (int q = 0; q < QMAX; ++q) Rh[q] = Rl[q] = 0.0;
-    double rh = 0.0, rl = 0.0;
-    int q = -1;
+    // slot 0 starts a row on every lane that has rows (bsf_start_mask): no
+    // Horner step, the row value is the slot itself
+    const bool any = vmask & 1u;
+    double rh = any ? C[0][0][0] : 0.0, rl = any ? C[1][0][0] : 0.0;
+    int q = any ? 0 : -1;
 #pragma unroll
-    for (int k = 0; k < 2 * NT; ++k) {
+    for (int k = 1; k < 2 * NT; ++k) {
         const bool start = (smask >> k) & 1, valid = (vmask >> k) & 1;
         // (A, B) = (exact integer limb, remainder limb) is already an exact,
         // unnormalised double-double of E (|B| <= 2^-kbits |A| scale): the
