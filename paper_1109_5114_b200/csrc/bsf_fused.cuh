@@ -1255,9 +1255,88 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             // keys of all items (item i = t P + pixel): each thread keeps one
             // pixel's geometry in registers and walks its taps (t0, t0 + FT/P,
             // ...); the tap loop is unrolled so several chains overlap ...
-            {
-                static_assert(FT % P == 0 || P % FT == 0, "chunk and block sizes must nest");
-                constexpr int TSTEP = FT >= P ? FT / P : 1;
+            static_assert(FT % P == 0 || P % FT == 0, "chunk and block sizes must nest");
+            constexpr int TSTEP = FT >= P ? FT / P : 1;
+            if constexpr (TSTEP == 1 && R <= 2) {
+                // one pixel per thread, its taps in order: the tap positions
+                // D_t = centre - sum_k j_k v_k and the knot-line coordinates
+                // U_m = n_m . D_t are walked incrementally (odometer over the
+                // digits j_k, fully unrolled: every step is known at compile
+                // time); all values are exact (R17: the 2^-41 grid, |n_m| small),
+                // so floor(n_m . phi) = floor(U_m) - n_m . floor(D) equals the
+                // direct classification of cls_region bit for bit
+#pragma unroll 1
+                for (int pl = tid % P; pl < P; pl += FT) {
+                    const int p = c0 + pl;
+                    const int w = s_info[p];
+                    const int var = info_var(w);
+                    const int ntap = var ? NTAP / (R + 1) : NTAP;
+                    const bool live = info_live(w) && (!a.pts || p == want);
+                    const int b = info_basis(w);
+                    const int drop = var - 1;
+                    // digit i's direction: the i-th non-dropped k
+                    double2 dv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int k = (drop >= 0 && i >= drop) ? min(i + 1, 3) : i;
+                        dv[i] = s_tv[5 * p + k];
+                    }
+                    const double2 cen = s_tv[5 * p + 4];
+                    int nx[4], ny[4], km[4], rx[4];
+                    double U[4], cu[4][4];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        nx[m] = s_cls.normal[b][m].x;
+                        ny[m] = s_cls.normal[b][m].y;
+                        km[m] = s_cls.kmin[b][m];
+                        rx[m] = s_cls.radix[b][m];
+                        U[m] = nx[m] * cen.x + ny[m] * cen.y;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) cu[i][m] = nx[m] * dv[i].x + ny[m] * dv[i].y;
+                    }
+                    double Dx = cen.x, Dy = cen.y;
+#pragma unroll
+                    for (int t = 0; t < NTAP; ++t) {
+                        uint16_t key = NOKEY;
+                        if (live && t < ntap) {
+                            const double flx = floor(Dx), fly = floor(Dy);
+                            const int ix = (int)flx, iy = (int)fly;
+                            int idx = 0, mul = 1;
+                            bool in = true;
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const int f = (int)floor(U[m]) - (nx[m] * ix + ny[m] * iy) - km[m];
+                                in = in && f >= 0 && f < rx[m];
+                                idx += f * mul;
+                                mul *= rx[m];
+                            }
+                            int reg = in ? s_cls.table[b][idx] : -1;
+                            if (reg < 0) reg = cls_region(s_cls, b, Dx - flx, Dy - fly);  // knot lines
+                            key = (uint16_t)((b * NVAR + var) * MAX_REG + reg);
+                        }
+                        s_key[t * P + pl] = key;
+                        if (t + 1 < NTAP) {
+                            // odometer step t -> t + 1: digits at R wrap to 0, the next one increments
+                            int tt = t;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                if (tt % (R + 1) < R) {
+                                    Dx -= dv[i].x;
+                                    Dy -= dv[i].y;
+#pragma unroll
+                                    for (int m = 0; m < 4; ++m) U[m] -= cu[i][m];
+                                    break;
+                                }
+                                Dx += R * dv[i].x;
+                                Dy += R * dv[i].y;
+#pragma unroll
+                                for (int m = 0; m < 4; ++m) U[m] += R * cu[i][m];
+                                tt /= (R + 1);
+                            }
+                        }
+                    }
+                }
+            } else {
 #pragma unroll 1
                 for (int pl = tid % P; pl < P; pl += (FT >= P ? P : FT)) {
                     const int p = c0 + pl;
