@@ -237,3 +237,25 @@ def test_order2_u8_super_tile_64():
         outs.append(o.cpu())
     rel = ((outs[0] - outs[1]).abs() / outs[1].abs()).max()
     assert float(rel) <= 2e-9, float(rel)
+
+
+def test_item_diagnostics_are_consistent():
+    """bsf_debug_item_cycles: the per-super-tile MACs add up to bsf_stats.macs,
+    the fallback counts to bsf_stats.double_double, every super-tile reports
+    cycles and a halo, and the CTAs' busy cycles add up to the items' cycles."""
+    w = synth.workload(2, width=640, height=480)
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    plan = make_plan(w, anchor=TILE)
+    with pytest.raises(RuntimeError):
+        plan.item_cycles(4)  # counters not enabled yet
+    plan.phase_cycles(reset=True)
+    plan.stats(reset=True)
+    gpu_full(plan, img[None], cov)
+    st = plan.stats(reset=True)
+    n = 20 * 15
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    items, work, ctas = plan.item_cycles(n, nsm)
+    assert sum(x[0] for x in work) == st["macs"]
+    assert sum(x[1] for x in work) == st["double_double"]
+    assert all(c > 0 for c in items) and all(x[2] > 0 and x[3] > 0 for x in work)
+    assert sum(ctas) == sum(items)
