@@ -68,3 +68,49 @@ def test_fuzz_fused_vs_oracle(seed):
         scale = np.maximum(np.abs(ref), 1e-3 * np.max(np.abs(ref)))
         err = float(np.max(np.abs(got[i][ys, xs] - ref) / scale))
         assert err <= tol, (seed, i, err, {k: c[k] for k in ("H", "W", "r", "policy", "u8", "smax")})
+
+
+def _case_large(seed):
+    """Image sizes that give the persistent kernel several super-tiles per SM
+    (the largest-first work order runs) and, for u8 at order 2 with a large
+    reach, 64 x 64 super-tiles."""
+    rng = np.random.default_rng(5000 + seed)
+    H, W = int(rng.integers(480, 720)), int(rng.integers(640, 900))
+    r = int(rng.integers(1, 4))
+    u8 = bool(rng.integers(0, 2)) if r != 2 else seed % 2 == 0
+    smax = float(rng.uniform(3.0, 14.0 if r < 3 else 3.0))
+    ph = rng.uniform(0, 2 * math.pi, 4)
+    X = np.arange(W)[None, :] / (W - 1)
+    Y = np.arange(H)[:, None] / (H - 1)
+    smaj = 0.6 + (smax - 0.6) * (0.5 + 0.5 * np.sin(3 * X + ph[0]) * np.cos(2 * Y + ph[1]))
+    ratio = 1.0 + rng.uniform(0, 5.5) * (0.5 + 0.5 * np.cos(2 * X - 3 * Y + ph[2]))
+    th = np.mod(ph[3] + 2.0 * X - 1.5 * Y, math.pi)
+    cov = np.stack([smaj, smaj / np.sqrt(ratio), th + 0 * X]).astype(np.float32)
+    img = rng.integers(0, 256, (H, W)).astype(np.uint8) if u8 else rng.uniform(-0.5, 1.0, (H, W)).astype(np.float32)
+    return dict(H=H, W=W, r=r, policy=int(rng.integers(0, 3)), u8=u8, smax=smax, cov=cov, img=img, rng=rng)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuzz_large_images_vs_oracle(seed):
+    c = _case_large(seed)
+    H, W = c["H"], c["W"]
+    plan = bsf.Plan(W, H, in_dtype=bsf.BSF_U8 if c["u8"] else bsf.BSF_F32, order=c["r"], basis=c["policy"],
+                    max_sigma=c["smax"], anchor=bsf.BSF_ANCHOR_TILE)
+    n0 = plan.launch_count()
+    out = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
+    plan.run(torch.from_numpy(c["img"]).cuda()[None], torch.from_numpy(c["cov"]).cuda(), out)
+    torch.cuda.synchronize()
+    assert plan.uses_fused()
+    st = plan.geometry.super_tile
+    items = ((W + st - 1) // st) * ((H + st - 1) // st)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    ordered = c["r"] >= 2 and items >= 2 * nsm
+    assert plan.launch_count() - n0 == (3 if ordered else 1)
+    got = out[0].cpu().numpy()
+    rng = c["rng"]
+    idx = rng.choice(H * W, 24, replace=False)
+    ys, xs = idx // W, idx % W
+    ref = oracle_points(c["img"], c["cov"], xs, ys, policy=c["policy"], r=c["r"])[0]
+    scale = np.maximum(np.abs(ref), 1e-3 * np.max(np.abs(ref)))
+    err = float(np.max(np.abs(got[ys, xs] - ref) / scale))
+    assert err <= 1e-9, (seed, err, st, {k: c[k] for k in ("H", "W", "r", "policy", "u8", "smax")})
