@@ -589,13 +589,17 @@ static bsf_status ensure_tile_ws(bsf_plan_s *p) {
     p->tile_counter = (int *)q;
     if (p->fused) {
         // largest-first work order of the super-tiles (launch_fused_impl)
-        const int ts = p->stile == 64 && p->d.order >= 2 ? 32 : p->stile;  // bsf_run_split's float64 passes
-        const long long n = (long long)((p->geo.W + ts - 1) / ts) * ((p->geo.H + ts - 1) / ts) * p->geo.nimg;
-        const size_t ob = (size_t)n * (sizeof(int) + 1) + 2 * SCHED_NBIN * sizeof(unsigned) + 16;
+        // units: super-tiles, or at 64 x 64 and order >= 2 up to four 32 x 32
+        // quadrants each (split mode; also covers bsf_run_split's 32 x 32 passes)
+        const int ts = p->stile;
+        long long n = (long long)((p->geo.W + ts - 1) / ts) * ((p->geo.H + ts - 1) / ts) * p->geo.nimg;
+        if (ts == 64 && p->d.order >= 2) n *= 4;
+        const size_t hw = 2 * SCHED_NBIN + 4;  // bin counts, cursors, unit count (+ pad)
+        const size_t ob = (size_t)n * (sizeof(int) + 1) + hw * sizeof(unsigned) + 16;
         if (cudaMalloc(&q, ob) != cudaSuccess) return set_err(BSF_ENOMEM, "work order " + std::to_string(ob));
         p->dev_allocs.push_back(q);
         p->sched_hist = (unsigned *)q;
-        p->sched_order = (int *)((char *)q + 2 * SCHED_NBIN * sizeof(unsigned));
+        p->sched_order = (int *)((char *)q + hw * sizeof(unsigned));
         p->sched_bin = (unsigned char *)(p->sched_order + n);
         p->sched_cap = n;
     }

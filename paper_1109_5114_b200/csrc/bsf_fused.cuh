@@ -877,7 +877,7 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
     return true;
 }
 
-template <int R>
+template <int R, bool SPLIT>
 __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
     constexpr int NTAP = FusedCfg<R>::NTAP, P = FusedCfg<R>::P, ITEMS = P * NTAP;
     constexpr int MT = FusedCfg<R>::MT, GS = 8 * MT;
@@ -890,7 +890,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     uint16_t *s_sorted = s_key + ITEMS;
     int *s_hist = reinterpret_cast<int *>(s_sorted + ITEMS + GS * NKEY);  // [warp][key]
     int *s_info = s_hist + (FT / 32) * NKEY;
-    __shared__ int s_item, s_ex[2], s_ey[2], s_vmask[2], s_bad, s_npad, s_any, s_nfb;
+    __shared__ int s_item, s_ex[2], s_ey[2], s_vmask[2], s_bad, s_npad, s_any, s_nfb, s_quad;
     __shared__ int s_one[NPLANE];  // plane is its own exact split (u8, order 1): single-limb MMA
     __shared__ short s_fb[FT];
     __shared__ int s_dom[2][4];
@@ -927,12 +927,17 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     const int ST = a.stile, SQ = ST / TILE, NQ = SQ * SQ;
     const int nstx = (a.W + ST - 1) / ST, nsty = (a.H + ST - 1) / ST;
     const int stiles_per_img = nstx * nsty;
-    const int nitems = a.pts ? a.npts : stiles_per_img * a.nimg;
+    // work units: points, super-tiles, or in split mode the unit count the
+    // order kernel wrote (quadrant units included)
+    int nitems = a.pts ? a.npts : stiles_per_img * a.nimg;
+    if constexpr (SPLIT) nitems = (int)__ldcg(a.order_hist + 2 * SCHED_NBIN);
     const size_t ipl = (size_t)a.H * a.W;
 
     for (;;) {
         if (tid == 0) {
             s_item = atomicAdd(a.counter, 1);
+            // split mode: >= 0 when the unit is only this quadrant of the super-tile
+            if constexpr (SPLIT) s_quad = s_item < nitems ? (__ldcg(a.order + s_item) & 7) - 1 : -1;
             s_ex[0] = s_ex[1] = s_ey[0] = s_ey[1] = 0;
             s_vmask[0] = s_vmask[1] = 0;
             s_bad = 0;
@@ -941,7 +946,14 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (tid == 0) s_nfb = 0;
         __syncthreads();
         if (s_item >= nitems) break;
-        const int item = a.order && !a.pts ? a.order[s_item] : s_item;
+        int item = a.order && !a.pts ? a.order[s_item] : s_item;
+        if constexpr (SPLIT) item >>= 3;  // unit code: super-tile << 3 | quadrant
+        // sub-tile q of the super-tile belongs to this unit (always, unless split mode)
+        auto qin = [&](int q) {
+            if constexpr (!SPLIT) return true;
+            const int qd = s_quad;
+            return qd < 0 || ((2 * (q % SQ) >= SQ) == (qd & 1) && (2 * (q / SQ) >= SQ) == (qd >> 1));
+        };
         if (a.prof && tid == 0) ph_t = t_item = clock64();
         // super-tile origin (X0s, Y0s): the running sums are anchored on its
         // halo domain; its four TILE x TILE sub-tiles are gathered in turn
@@ -964,7 +976,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             // Algorithm 1 with sigma_b = 0: the isotropic pass is the identity
             for (int q = 0; q < NQ; ++q) {
                 const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
-                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H);
+                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H && qin(q));
                 if (mine) {
                     const double v = load_f(a, (size_t)img * ipl + (size_t)y * a.W + x);
                     const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
@@ -982,7 +994,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         for (int q = 0; q < NQ; ++q) {
             const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
             double *sb = s_scl + ((size_t)q * FT + tid) * 5;  // this pixel's scales, reused by its sub-tile
-            if (x < a.W && y < a.H) {
+            if (x < a.W && y < a.H && qin(q)) {
                 PixelScales ps;
                 double sx, sy, th;
                 load_cov(a, img, x, y, sx, sy, th);
@@ -1009,7 +1021,14 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (tid == 0) {
             int np = 0;
             for (int b = 0; b < 2; ++b) {
-                TileDomain d = fused_domain(luts[b], R, X0s, Y0s, s_ex[b], s_ey[b], ST);
+                TileDomain d;
+                if constexpr (SPLIT) {  // a quadrant unit: its own 32 x 32 anchoring
+                    const int qd = s_quad, hs = qd < 0 ? 0 : ST / 2;
+                    d = fused_domain(luts[b], R, X0s + hs * (qd & 1), Y0s + hs * (qd >> 1), s_ex[b], s_ey[b],
+                                     qd < 0 ? ST : hs);
+                } else {
+                    d = fused_domain(luts[b], R, X0s, Y0s, s_ex[b], s_ey[b], ST);
+                }
                 s_dom[b][0] = d.X0;
                 s_dom[b][1] = d.Y0;
                 s_dom[b][2] = d.NX;
@@ -1031,7 +1050,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             // happen when max_sigma bounds the covariance field)
             for (int q = 0; q < NQ; ++q) {
                 const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
-                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H);
+                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H && qin(q));
                 if (mine) {
                     const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
                     if (a.out_f32 && !a.pts)
@@ -1199,7 +1218,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         // ---- sub-tiles: per-pixel scales, then 4-5 ------------------------------
 #pragma unroll 1
         for (int q = 0; q < NQ; ++q) {
-        if (a.pts && q != qwant) continue;
+        if ((a.pts && q != qwant) || !qin(q)) continue;
         const int x0 = X0s + TILE * (q % SQ), y0 = Y0s + TILE * (q / SQ);
         {
             const int x = x0 + (tid % TILE), y = y0 + tid / TILE;
@@ -1797,15 +1816,26 @@ __device__ __forceinline__ float sched_halo_weight() {
     return R == 1 ? 10.f : R == 2 ? 160.f : 0.f;  // (order 1 keeps raster order, launch_fused_impl)
 }
 
+// Split mode (64 x 64 super-tiles at order 2, u8 plans): a super-tile whose
+// conditioning proxy (64 + 2E) / sigma_min exceeds SCHED_SPLIT_COND -- small
+// scales next to a large reach, where the 64 x 64 anchoring sends pixels to the
+// double-double fallback (profiles/README.md, tools/stile_risk.py: hundreds to
+// thousands per super-tile once sigma_min < 1) -- is handed out as its four
+// 32 x 32 quadrants, each anchored on its own halo.  Units are written to the
+// bin array with stride S = 4: slot 4i + q = quadrant q of super-tile i (bin |
+// 128), or slot 4i = the whole super-tile; unused slots hold 255.
+constexpr float SCHED_SPLIT_COND = 160.f;
+
 template <int R>
-__global__ void __launch_bounds__(256) fused_cost_kernel(TileArgs a, const LutBasis *__restrict__ luts, int nitems) {
+__global__ void __launch_bounds__(256) fused_cost_kernel(TileArgs a, const LutBasis *__restrict__ luts, int nitems,
+                                                         int S) {
     constexpr int NTAP = FusedCfg<R>::NTAP;
     const int lane = threadIdx.x & 31, item = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (item >= nitems) return;
     const int ST = a.stile, nstx = (a.W + ST - 1) / ST, spi = nstx * ((a.H + ST - 1) / ST);
     const int img = item / spi, rem = item % spi, X0s = (rem % nstx) * ST, Y0s = (rem / nstx) * ST;
     const int step = ST / 8;
-    float acc = 0.f;
+    float acc = 0.f, smin = 3.0e38f;
     int ex[2] = {0, 0}, ey[2] = {0, 0}, vm[2] = {0, 0};
     if (!(a.cov_mode == COV_ISO && !(a.sigma2[img / a.channels] > 0.0))) {
         for (int s = lane; s < 64; s += 32) {
@@ -1813,6 +1843,7 @@ __global__ void __launch_bounds__(256) fused_cost_kernel(TileArgs a, const LutBa
             if (x < a.W && y < a.H) {
                 double sx, sy, th;
                 load_cov(a, img, x, y, sx, sy, th);
+                smin = fminf(smin, (float)fmin(sx, sy));
                 PixelScales ps;
                 pixel_scales(sx, sy, th, a.policy, a.clamp, R, ps);
                 if (!(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO))) {
@@ -1833,6 +1864,7 @@ __global__ void __launch_bounds__(256) fused_cost_kernel(TileArgs a, const LutBa
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        smin = fminf(smin, __shfl_xor_sync(0xffffffffu, smin, o));
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
             ex[b] = max(ex[b], __shfl_xor_sync(0xffffffffu, ex[b], o));
@@ -1847,13 +1879,26 @@ __global__ void __launch_bounds__(256) fused_cost_kernel(TileArgs a, const LutBa
                 const TileDomain d = fused_domain(luts[b], R, X0s, Y0s, ex[b], ey[b], ST);
                 cost += sched_halo_weight<R>() * (float)d.NX * (float)d.NY * (float)__popc(vm[b] | 1);
             }
-        const int b = cost >= 1.f ? min(SCHED_NBIN - 1, 1 + (int)(4.f * __log2f(cost))) : 0;
-        a.order_bin[item] = (unsigned char)b;
-        atomicAdd(a.order_hist + b, 1u);
+        const int E = max(max(ex[0], ex[1]), max(ey[0], ey[1]));
+        const bool split = S == 4 && (float)(ST + 2 * E) > SCHED_SPLIT_COND * smin;
+        if (!split) {
+            const int b = cost >= 1.f ? min(SCHED_NBIN - 1, 1 + (int)(4.f * __log2f(cost))) : 0;
+            a.order_bin[(size_t)S * item] = (unsigned char)b;
+            atomicAdd(a.order_hist + b, 1u);
+            for (int q = 1; q < S; ++q) a.order_bin[(size_t)S * item + q] = 255;
+        } else {
+            const float c4 = 0.25f * cost;
+            const int b = c4 >= 1.f ? min(SCHED_NBIN - 1, 1 + (int)(4.f * __log2f(c4))) : 0;
+            for (int q = 0; q < 4; ++q) {
+                const bool in = X0s + (ST / 2) * (q & 1) < a.W && Y0s + (ST / 2) * (q >> 1) < a.H;
+                a.order_bin[(size_t)4 * item + q] = in ? (unsigned char)(b | 128) : 255;
+                if (in) atomicAdd(a.order_hist + b, 1u);
+            }
+        }
     }
 }
 
-__global__ void __launch_bounds__(256) fused_order_kernel(TileArgs a, int nitems) {
+__global__ void __launch_bounds__(256) fused_order_kernel(TileArgs a, int nslots, int S) {
     static_assert(SCHED_NBIN == 128, "four bins per lane");
     __shared__ unsigned base[SCHED_NBIN];
     if (threadIdx.x < 32) {
@@ -1875,21 +1920,28 @@ __global__ void __launch_bounds__(256) fused_order_kernel(TileArgs a, int nitems
             base[SCHED_NBIN - 1 - 4 * lane - k] = run;
             run += h[k];
         }
+        // the number of units, for the fused kernel's loop bound
+        if (blockIdx.x == 0 && lane == 31) a.order_hist[2 * SCHED_NBIN] = inc;
     }
     __syncthreads();
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nitems; i += gridDim.x * blockDim.x) {
-        const int b = a.order_bin[i];
-        a.order[base[b] + atomicAdd(a.order_hist + SCHED_NBIN + b, 1u)] = i;
+    // unit code: the super-tile (S = 1), or super-tile << 3 | (0 whole, 1 + q
+    // quadrant q) in split mode
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nslots; i += gridDim.x * blockDim.x) {
+        const int v = a.order_bin[i];
+        if (v == 255) continue;
+        const int b = v & 127;
+        const int code = S == 1 ? i : ((i / S) << 3) | ((v & 128) ? 1 + i % S : 0);
+        a.order[base[b] + atomicAdd(a.order_hist + SCHED_NBIN + b, 1u)] = code;
     }
 }
 
-template <int R>
+template <int R, bool SPLIT = false>
 static cudaError_t launch_fused_r(const TileArgs &a, int slots, cudaStream_t st, const LutBasis *luts) {
     constexpr size_t sm = fused_smem_bytes<R>();
     static std::atomic<unsigned long long> attr{0ull};
-    cudaError_t e = set_smem_attr(fused_kernel<R>, (int)sm, attr);
+    cudaError_t e = set_smem_attr(fused_kernel<R, SPLIT>, (int)sm, attr);
     if (e != cudaSuccess) return e;
-    fused_kernel<R><<<slots, FT, sm, st>>>(a, luts);
+    fused_kernel<R, SPLIT><<<slots, FT, sm, st>>>(a, luts);
     return cudaGetLastError();
 }
 
@@ -1916,21 +1968,26 @@ cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStrea
     if (e != cudaSuccess) return e;
     TileArgs b = a;
     const long long nitems = (long long)((a.W + a.stile - 1) / a.stile) * ((a.H + a.stile - 1) / a.stile) * a.nimg;
-    if (a.order && !a.pts && order >= 2 && nitems >= 2 * (long long)slots && nitems <= a.order_cap) {
+    // split mode (see fused_cost_kernel): 64 x 64 super-tiles at order 2 run the
+    // scheduling kernels at any item count
+    const int S = (a.stile == 64 && order == 2) ? 4 : 1;
+    if (a.order && !a.pts && order >= 2 && (S == 4 || nitems >= 2 * (long long)slots) &&
+        nitems * S <= a.order_cap) {
         // largest-first work order (see fused_cost_kernel); at order 1 the
         // balance it gains (3.7 -> 1.2 % on config 3) is lost to the halo reads
         // of raster neighbours no longer sharing L2, so raster order stays
-        if ((e = cudaMemsetAsync(a.order_hist, 0, 2 * SCHED_NBIN * sizeof(unsigned), st)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(a.order_hist, 0, (2 * SCHED_NBIN + 1) * sizeof(unsigned), st)) != cudaSuccess)
+            return e;
         const int nb = (int)((nitems + 7) / 8);
         switch (order) {
-            case 1: fused_cost_kernel<1><<<nb, 256, 0, st>>>(a, luts, (int)nitems); break;
-            case 2: fused_cost_kernel<2><<<nb, 256, 0, st>>>(a, luts, (int)nitems); break;
-            case 3: fused_cost_kernel<3><<<nb, 256, 0, st>>>(a, luts, (int)nitems); break;
-            case 4: fused_cost_kernel<4><<<nb, 256, 0, st>>>(a, luts, (int)nitems); break;
+            case 1: fused_cost_kernel<1><<<nb, 256, 0, st>>>(a, luts, (int)nitems, S); break;
+            case 2: fused_cost_kernel<2><<<nb, 256, 0, st>>>(a, luts, (int)nitems, S); break;
+            case 3: fused_cost_kernel<3><<<nb, 256, 0, st>>>(a, luts, (int)nitems, S); break;
+            case 4: fused_cost_kernel<4><<<nb, 256, 0, st>>>(a, luts, (int)nitems, S); break;
             default: return cudaErrorInvalidValue;
         }
-        fused_order_kernel<<<(int)std::min<long long>((nitems + 255) / 256, 4 * (long long)slots), 256, 0, st>>>(
-            a, (int)nitems);
+        fused_order_kernel<<<(int)std::min<long long>((nitems * S + 255) / 256, 4 * (long long)slots), 256, 0, st>>>(
+            a, (int)(nitems * S), S);
         *nl += 2;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     } else {
@@ -1938,7 +1995,9 @@ cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStrea
     }
     switch (order) {
         case 1: e = launch_fused_r<1>(b, slots, st, luts); break;
-        case 2: e = launch_fused_r<2>(b, slots, st, luts); break;
+        case 2:  // split mode only in its own instantiation (register allocation of the other plans untouched)
+            e = b.order && S == 4 ? launch_fused_r<2, true>(b, slots, st, luts) : launch_fused_r<2>(b, slots, st, luts);
+            break;
         case 3: e = launch_fused_r<3>(b, slots, st, luts); break;
         case 4: e = launch_fused_r<4>(b, slots, st, luts); break;
         default: return cudaErrorInvalidValue;

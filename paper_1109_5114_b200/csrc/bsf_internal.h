@@ -174,8 +174,8 @@ struct TileArgs {
     // largest estimated work first (fused_cost_kernel / fused_order_kernel)
     int *order;
     unsigned char *order_bin;  // [items] cost bin of each super-tile
-    unsigned *order_hist;      // [2][SCHED_NBIN] bin counts, scatter cursors
-    long long order_cap;       // items the order buffers hold
+    unsigned *order_hist;      // [2][SCHED_NBIN] bin counts, scatter cursors, then the unit count
+    long long order_cap;       // units (bin slots) the order buffers hold
 };
 constexpr int SCHED_NBIN = 128;
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per device

@@ -259,3 +259,37 @@ def test_item_diagnostics_are_consistent():
     assert sum(x[1] for x in work) == st["double_double"]
     assert all(c > 0 for c in items) and all(x[2] > 0 and x[3] > 0 for x in work)
     assert sum(ctas) == sum(items)
+
+
+def test_split_mode_quadrants_small_scales():
+    """u8 at order 2 with a large reach (64 x 64 super-tiles) and a region of
+    tiny scales: the work order hands the ill-conditioned super-tiles out as
+    32 x 32 quadrants (split mode), which keeps their pixels off the
+    double-double fallback; the output matches the oracle everywhere sampled,
+    the small-scale region included."""
+    W, H = 448, 320
+    w = synth.workload(3, order=2, width=W, height=H)
+    img = synth.make_image(w)
+    X = torch.arange(W, dtype=torch.float64)[None, :].expand(H, W)
+    Y = torch.arange(H, dtype=torch.float64)[:, None].expand(H, W)
+    smaj = 0.45 + 13.5 * (X / (W - 1)) ** 2
+    th = torch.remainder(0.7 + 0.004 * X + 0.003 * Y, math.pi)
+    cov = torch.stack([smaj, smaj / 1.6, th]).to(torch.float32)
+    res = {}
+    for o in ("0", "1"):
+        with _env(BSF_ORDER=o):
+            plan = make_plan(w, anchor=TILE, batch=1)
+            assert plan.geometry.super_tile == 64
+            n0 = plan.launch_count()
+            out = gpu_full(plan, img[None], cov)
+            res[o] = (out, plan.stats()["double_double"], plan.launch_count() - n0)
+    assert res["1"][2] == 3 and res["0"][2] == 1
+    assert res["1"][1] < res["0"][1], (res["1"][1], res["0"][1])
+    from gpu_util import oracle_points
+    rng = np.random.default_rng(5)
+    xs = np.concatenate([rng.integers(0, 64, 16), rng.integers(0, W, 16)])
+    ys = rng.integers(0, H, 32)
+    ref = oracle_points(img.numpy(), cov.numpy(), xs, ys, policy=w.basis, r=2)[0]
+    for o in ("0", "1"):
+        err = np.max(np.abs(res[o][0][0].numpy()[ys, xs] - ref) / np.abs(ref))
+        assert err <= 1e-9, (o, err)
