@@ -415,3 +415,168 @@ def test_preintegration_impulse_single_level_ray():
     # semantics through a constant image instead: g on the first row with
     # W = 5 counts lattice points of the cone.
     assert g[1, 12 + 2] >= 7 and g[0].sum() == 0
+
+
+# ----------------------------------------------------------------------------
+# Anisotropic minimum-kurtosis scales with C12 != 0, solved independently here
+# (hand-derived families, the paper's kurtosis matrices, numpy polynomial roots)
+# ----------------------------------------------------------------------------
+
+def _family_theta(C):
+    """Theta, Eq. (4) inverted by hand.  24 C11 = 2u1 + u2 + u4,
+    24 C12 = u2 - u4, 24 C22 = 2u3 + u2 + u4: the null direction of u -> C is
+    (-1, 1, -1, 1)/2, so u(t) = (A1 - t/2, B + t/2, A3 - t/2, t/2 - B) with
+    A1 = 12 C11, A3 = 12 C22, B = 12 C12; u >= 0 gives t in [2|B|, 2 min(A1, A3)]."""
+    A1, A3, B = 12 * float(C[0]), 12 * float(C[2]), 12 * float(C[1])
+    T = np.poly1d([1.0, 0.0])
+    u = [A1 - T / 2, B + T / 2, A3 - T / 2, T / 2 - B]
+    return u, 2 * abs(B), 2 * min(A1, A3)
+
+
+def _family_theta_prime(C):
+    """Theta', PAPER.md:413-416 inverted by hand.  60 C11 = 4u1 + u2 + u3 + 4u4,
+    60 C22 = u1 + 4u2 + 4u3 + u4, 60 C12 = 2(u1 + u2 - u3 - u4).  Adding and
+    subtracting the diagonal equations: u1 + u4 = P = 16 C11 - 4 C22 and
+    u2 + u3 = Q = 16 C22 - 4 C11; then u1 - u4 + u2 - u3 = D = 30 C12.  Null
+    direction (1, -1, 1, -1): u(t) = ((P + t)/2, (Q + D - t)/2, (Q - D + t)/2,
+    (P - t)/2)."""
+    C = [float(c) for c in C]
+    P = 16 * C[0] - 4 * C[2]
+    Q = 16 * C[2] - 4 * C[0]
+    D = 30 * C[1]
+    T = np.poly1d([1.0, 0.0])
+    u = [(P + T) / 2, (Q + D - T) / 2, (Q - D + T) / 2, (P - T) / 2]
+    lo = max(-P, D - Q)
+    hi = min(P, D + Q)
+    return u, lo, hi
+
+
+def _kurt_J(basis, u):
+    """||K||_F^2 with K the kurtosis matrix: PAPER.md:428-429 for Theta' (kappa/5
+    dropped), sum_k a_k^4 u_k u_k^T for Theta (R6); the off-diagonal
+    entry appears twice in the Frobenius norm."""
+    q = [p * p for p in u]
+    if basis == O.THETA_PRIME:
+        K11 = (4 * q[0] + q[1] + q[2] + 4 * q[3]) / 5
+        K12 = 2 * (q[0] + q[1] - q[2] - q[3]) / 5
+        K22 = (q[0] + 4 * q[1] + 4 * q[2] + q[3]) / 5
+    else:
+        # unit vectors (1,0), (1,1)/sqrt2, (0,1), (-1,1)/sqrt2: the diagonal ones
+        # contribute q/2 to every entry, with sign -1 off-diagonal for (-1, 1)
+        K11 = q[0] + q[1] / 2 + q[3] / 2
+        K12 = q[1] / 2 - q[3] / 2
+        K22 = q[2] + q[1] / 2 + q[3] / 2
+    return K11 * K11 + 2 * K12 * K12 + K22 * K22
+
+
+def _min_kurtosis_t(basis, C):
+    u, lo, hi = (_family_theta if basis == O.THETA else _family_theta_prime)(C)
+    J = _kurt_J(basis, u)
+    cands = [lo, hi] + [float(z.real) for z in J.deriv().r if abs(z.imag) < 1e-9 and lo < z.real < hi]
+    t = min(cands, key=lambda x: J(x))
+    return t, np.array([max(p(t), 0.0) for p in u]), J
+
+
+def test_solver_theta_45deg_closed_form():
+    """Theta at phi = 45 deg (C11 = C22, C12 != 0), the VERDICT's closed form:
+    u = (A - t/2, B + t/2, A - t/2, t/2 - B), K11 = K22 = (A - t/2)^2 + B^2 + t^2/4,
+    K12 = B t, so J' = 4 [(t - A) K11 + B^2 t]; the optimum is the root of that
+    cubic on [2|B|, 2A]."""
+    for C11, C12 in ((1.0, 0.3), (2.5, -0.9), (7.0, 2.0)):
+        A, B = 12 * C11, 12 * C12
+        t = np.poly1d([1.0, 0.0])
+        K11 = (A - t / 2) ** 2 + B * B + t * t / 4
+        cubic = (t - A) * K11 + B * B * t
+        roots = [z.real for z in cubic.r if abs(z.imag) < 1e-9 and 2 * abs(B) <= z.real <= 2 * A]
+        assert len(roots) == 1
+        ts = roots[0]
+        u = np.array([A - ts / 2, B + ts / 2, A - ts / 2, ts / 2 - B])
+        a, to = O.solve_scales(O.THETA, [C11, C12, C11])
+        np.testing.assert_allclose(a, np.sqrt(u), rtol=1e-10)
+
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+def test_solver_anisotropic_offdiagonal_pins(basis):
+    """Random feasible covariances with C12 != 0 (both bases): the oracle's
+    scales (Gauss-Jordan family + bisection on its chain-rule J') equal the
+    minimiser of the hand-derived quartic J(t) found by numpy's polynomial
+    roots.  A wrong weight of the off-diagonal kurtosis term changes t."""
+    rng = np.random.default_rng(31 + basis)
+    n = interior = 0
+    while n < 40:
+        smaj = rng.uniform(1, 12)
+        rho = rng.uniform(1.05, 5.5)
+        th = rng.uniform(0, math.pi)
+        sx, sy = smaj, smaj / math.sqrt(rho)
+        phi, rho2 = O.orient(sx, sy, th)
+        if rho2 > 0.95 * O.bound_rho(basis, phi):
+            continue
+        C = O.decode(sx, sy, th)
+        if abs(C[1]) < 0.05 * C[0]:
+            continue
+        n += 1
+        ts, u, J = _min_kurtosis_t(basis, C)
+        _, lo, hi = (_family_theta if basis == O.THETA else _family_theta_prime)(C)
+        interior += lo + 1e-9 * abs(hi) < ts < hi - 1e-9 * abs(hi)
+        a, _ = O.solve_scales(basis, C)
+        np.testing.assert_allclose(a * a, u, rtol=1e-8, atol=1e-8 * u.max())
+    assert interior >= 10  # the off-diagonal term decides the interior optima
+
+
+@pytest.mark.parametrize("basis", [O.THETA, O.THETA_PRIME])
+def test_decode_orientation_matches_eq5(basis):
+    """Covariance decode + scale solve, read back through the paper's shape
+    formulas: Eq. (5) (PAPER.md:144-147) for Theta, PAPER.md:417-421 for
+    Theta'.  The orientation of the solved box spline must be the input theta
+    (mod pi), its elongation (sx/sy)^2 and its size sx^2 + sy^2: this pins the
+    sign convention of C12 in the decode."""
+    rng = np.random.default_rng(41 + basis)
+    n = 0
+    while n < 40:
+        smaj = rng.uniform(1, 10)
+        rho = rng.uniform(1.3, 5.0)
+        th = rng.uniform(0.02, math.pi - 0.02)
+        sx, sy = smaj, smaj / math.sqrt(rho)
+        phi, rho2 = O.orient(sx, sy, th)
+        if rho2 > 0.95 * O.bound_rho(basis, phi):
+            continue
+        n += 1
+        a, _ = O.solve_scales(basis, O.decode(sx, sy, th))
+        u = a * a
+        if basis == O.THETA:
+            Dd = (u[0] - u[2]) ** 2 + (u[1] - u[3]) ** 2
+            size = u.sum() / 12.0
+            elong = (u.sum() + math.sqrt(Dd)) / (u.sum() - math.sqrt(Dd))
+            num, den = u[2] - u[0] + math.sqrt(Dd), u[1] - u[3]
+        else:
+            p = 3 * (u[0] - u[1] - u[2] + u[3])
+            q = 4 * (u[0] + u[1] - u[2] - u[3])
+            rr = 5 * u.sum()
+            size = rr / 60.0
+            elong = (rr + math.hypot(p, q)) / (rr - math.hypot(p, q))
+            num, den = -p + math.hypot(p, q), q
+        tha = math.atan2(num, den) % math.pi  # tan(theta_a) = num / den
+        d = (tha - th) % math.pi
+        assert min(d, math.pi - d) < 1e-7, (th, tha)
+        assert elong == pytest.approx(rho, rel=1e-8)
+        assert size == pytest.approx(sx * sx + sy * sy, rel=1e-10)
+
+
+def test_order2_filter_has_target_covariance():
+    """Prop. 1 through the whole filter: at order r the
+    r-fold kernel is built from the scales of C/r, so the impulse response has
+    mass ~1 and second moments C = R(theta) diag(sx^2, sy^2) R(theta)^T (the
+    lattice sums of a C^1 piecewise polynomial match its moments closely)."""
+    H = W = 27
+    img = np.zeros((H, W))
+    img[13, 13] = 1.0
+    sx, sy, th = 2.0, 1.25, 0.5
+    ys, xs = np.mgrid[0:H, 0:W]
+    out = O.filter_points(img, xs.ravel(), ys.ravel(), sx, sy, th, policy=O.THETA, r=2)[0].reshape(H, W)
+    dx, dy = (xs - 13).astype(float), (ys - 13).astype(float)
+    m = out.sum()
+    C = np.array([(out * dx * dx).sum(), (out * dx * dy).sum(), (out * dy * dy).sum()]) / m
+    c, s = math.cos(th), math.sin(th)
+    ref = np.array([sx * sx * c * c + sy * sy * s * s, (sx * sx - sy * sy) * s * c, sx * sx * s * s + sy * sy * c * c])
+    assert abs(m - 1) < 1e-3
+    np.testing.assert_allclose(C, ref, atol=2e-3 * ref.max())

@@ -1,0 +1,78 @@
+"""Mutation check of the oracle pins (test infrastructure, CPU only).
+
+Applies plausible single-point mistakes to a copy of oracle/bsf_oracle.c in a
+temporary directory, rebuilds it there and runs the `-m "not gpu"` oracle pins
+against it; every mutation must make at least one pin fail.  Usage:
+    python tools/oracle_mutations.py
+"""
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# (name, original text, mutated text) -- each original must occur exactly once
+MUTATIONS = [
+    ("kurtosis off-diagonal weight 2 -> 0.5",
+     "return K[0] * K[0] + 2 * K[1] * K[1] + K[2] * K[2];",
+     "return K[0] * K[0] + 0.5 * K[1] * K[1] + K[2] * K[2];"),
+    ("decode: sign of C12",
+     "C[1] = (vx - vy) * s * c;",
+     "C[1] = -(vx - vy) * s * c;"),
+    ("Theta covariance: C12 = (u2 + u4)/24",
+     "C[1] = (u2 - u4) / 24.0;",
+     "C[1] = (u2 + u4) / 24.0;"),
+    ("Theta' covariance: dropped 4 u4 in C11",
+     "C[0] = (4 * u1 + u2 + u3 + 4 * u4) / 60.0;",
+     "C[0] = (4 * u1 + u2 + u3) / 60.0;"),
+    ("Theta' kurtosis: K22 weight of q2 4 -> 1",
+     "K[2] = (q1 + 4 * q2 + 4 * q3 + q4) / 5.0;",
+     "K[2] = (q1 + q2 + 4 * q3 + q4) / 5.0;"),
+    ("Theta' bound: 3/5 -> 4/5",
+     "double b1 = c2 > 0 ? 0.6 / c2 : INFINITY;",
+     "double b1 = c2 > 0 ? 0.8 / c2 : INFINITY;"),
+    ("clamp factor 0.95 -> 0.9",
+     "double lim = 0.95 * rb;",
+     "double lim = 0.9 * rb;"),
+    ("B-spline: centring r/2 -> r",
+     "double xx = s / a + 0.5 * r;",
+     "double xx = s / a + 1.0 * r;"),
+    ("order: C/r -> C",
+     "double Cr[3] = {C[0] / r, C[1] / r, C[2] / r};",
+     "double Cr[3] = {C[0], C[1], C[2]};"),
+    ("support: transposed pixel offset",
+     "or_beta(basis, r, a, (double)(px - qx), (double)(py - qy));",
+     "or_beta(basis, r, a, (double)(py - qy), (double)(px - qx));"),
+    ("pre-integration: step sign",
+     "int py = y - sy, pxi = xi - sx;",
+     "int py = y - sy, pxi = xi + sx;"),
+]
+
+
+def main() -> int:
+    src = open(os.path.join(ROOT, "oracle", "bsf_oracle.c")).read()
+    bad = 0
+    with tempfile.TemporaryDirectory() as tmp:
+        shutil.copytree(os.path.join(ROOT, "oracle"), os.path.join(tmp, "oracle"))
+        shutil.copytree(os.path.join(ROOT, "tests"), os.path.join(tmp, "tests"))
+        shutil.copy(os.path.join(ROOT, "pytest.ini"), tmp)
+        for name, old, new in MUTATIONS:
+            assert src.count(old) == 1, name
+            with open(os.path.join(tmp, "oracle", "bsf_oracle.c"), "w") as fh:
+                fh.write(src.replace(old, new))
+            so = os.path.join(tmp, "oracle", "libbsf_oracle.so")
+            if os.path.exists(so):
+                os.remove(so)
+            r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                                "tests/test_oracle_pins.py", "tests/test_accuracy.py"], cwd=tmp,
+                               capture_output=True, text=True)
+            caught = r.returncode != 0
+            bad += not caught
+            print("%-45s %s" % (name, "caught" if caught else "NOT CAUGHT"))
+    return 1 if bad else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
