@@ -72,8 +72,17 @@ typedef enum {
 } bsf_precision;
 
 typedef enum {
-    BSF_ANCHOR_GLOBAL = 0, /* one pre-integration of the whole image (bsf_preintegrate + bsf_filter) */
-    BSF_ANCHOR_TILE = 1    /* fused: sums restarted per 16x16 output tile on its halo (R18) */
+    BSF_ANCHOR_GLOBAL = 0, /* the paper's single pre-integration of the whole image.
+                            * u8 input at order 1 with every running sum below 2^62 ("global mode",
+                            * bsf_geometry.global_mode = 1): exact int64 sums (bsf_preintegrate_exact)
+                            * gathered by the fused kernel with an exact contraction.
+                            * Otherwise double-double sums (bsf_preintegrate) + the per-pixel
+                            * double-double gather (bsf_filter), whose rounding grows with the image
+                            * size                                                      */
+    BSF_ANCHOR_TILE = 1,   /* fused: running sums restarted per 32x32 (16x16 on small images, 64x64
+                            * at order 1-2 with a large reach) output super-tile on its halo domain
+                            * (R18, R20)                                                     */
+    BSF_ANCHOR_AUTO = 2    /* global mode when the plan qualifies, else BSF_ANCHOR_TILE              */
 } bsf_anchor;
 
 typedef enum {
@@ -117,6 +126,8 @@ typedef struct {
     int super_tile;          /* BSF_ANCHOR_TILE: side of the super-tiles the running sums are
                               * anchored on (16, 32 or 64); row strips that must reproduce a
                               * one-GPU run align to it and use it in their plans           */
+    int global_mode;         /* 1: bsf_run gathers from exact int64 global sums (BSF_ANCHOR_GLOBAL /
+                              * BSF_ANCHOR_AUTO, u8 input, order 1, sums below 2^62)        */
 } bsf_geometry;
 
 typedef struct {
@@ -278,8 +289,9 @@ long long bsf_launch_count(bsf_plan_t plan);
  * contraction kernel (known after the first tile-path call), else 0.        */
 bsf_status bsf_debug_phase_cycles(bsf_plan_t plan, unsigned long long *out, int reset);
 /* bsf_debug_item_cycles (after bsf_debug_phase_cycles enabled the counters):
- * host `items[i]` = SM cycles of fused-path work item i (super-tile, in the
- * order the atomic counter hands them out; i < min(nitems, 8192)) in the last
+ * host `items[i]` = SM cycles of fused-path work unit i (a super-tile, or in
+ * split mode a 32x32 quadrant unit; i is the hand-out index of the atomic
+ * counter; i < min(nitems, 8192)) in the last
  * run; host `work[4i .. 4i+3]` (may be NULL) = its interpolation MACs, its
  * double-double fallback pixels, the halo domain points of the bases it
  * pre-integrates and its number of planes; host `ctas[c]` = busy cycles of CTA
@@ -289,6 +301,16 @@ bsf_status bsf_debug_phase_cycles(bsf_plan_t plan, unsigned long long *out, int 
 bsf_status bsf_debug_item_cycles(bsf_plan_t plan, unsigned long long *items, unsigned long long *work, int nitems,
                                  unsigned long long *ctas, int nctas);
 int bsf_uses_fused(bsf_plan_t plan);
+/* bsf_debug_option (diagnostics and tests only; the defaults are the product
+ * path): "fused" 0/1 -- 0 runs the per-thread double-double tile kernel instead
+ * of the exact split path (set before the first run); "work_order" 0/1 -- 0
+ * hands the fused path's super-tiles out in raster order; "split_tol" -- the
+ * relative a-posteriori bound above which a pixel is recomputed in
+ * double-double (default 5e-10; 0 sends every pixel to the fallback, inf
+ * none, which voids the 1e-9 contract); "global_kernel" 0/1 -- global mode
+ * gathers with the order-1 integer kernel (1, default) or the fused kernel's
+ * DMMA groups (0).  BSF_EINVAL for an unknown name.                          */
+bsf_status bsf_debug_option(bsf_plan_t plan, const char *name, double value);
 
 const char *bsf_status_str(bsf_status s);
 const char *bsf_last_error(void);

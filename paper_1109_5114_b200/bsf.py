@@ -16,7 +16,7 @@ LUT_DIR = os.path.join(HERE, "lut")
 BSF_U8, BSF_F32, BSF_F64, BSF_I64, BSF_DD = 0, 1, 2, 3, 4
 BSF_THETA, BSF_THETA_PRIME, BSF_DUAL = 0, 1, 2
 BSF_PREC_FP64, BSF_PREC_DD, BSF_PREC_AUTO = 0, 1, 2
-BSF_ANCHOR_GLOBAL, BSF_ANCHOR_TILE = 0, 1
+BSF_ANCHOR_GLOBAL, BSF_ANCHOR_TILE, BSF_ANCHOR_AUTO = 0, 1, 2
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "out of memory", 3: "CUDA error", 4: "infeasible covariance",
           5: "kernel reach exceeds plan margins", 6: "communication error", 7: "unsupported"}
@@ -43,7 +43,8 @@ class bsf_plan_desc(ctypes.Structure):
 class bsf_geometry(ctypes.Structure):
     _fields_ = [("margin_x", ctypes.c_int), ("margin_y", ctypes.c_int), ("g_width", ctypes.c_int),
                 ("g_height", ctypes.c_int), ("nbases", ctypes.c_int), ("g_bytes", ctypes.c_size_t),
-                ("g_exact_bytes", ctypes.c_size_t), ("super_tile", ctypes.c_int)]
+                ("g_exact_bytes", ctypes.c_size_t), ("super_tile", ctypes.c_int),
+                ("global_mode", ctypes.c_int)]
 
 
 class bsf_stats(ctypes.Structure):
@@ -102,6 +103,8 @@ def lib():
         L.bsf_debug_phase_cycles.argtypes = [vp, vp, i]
         L.bsf_debug_item_cycles.restype = st
         L.bsf_debug_item_cycles.argtypes = [vp, vp, vp, i, vp, i]
+        L.bsf_debug_option.restype = st
+        L.bsf_debug_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_double]
         L.bsf_uses_fused.restype = i
         L.bsf_uses_fused.argtypes = [vp]
         L.bsf_status_str.restype = ctypes.c_char_p
@@ -133,6 +136,30 @@ def _ptr(t):
     if isinstance(t, int):
         return ctypes.c_void_p(t)
     return ctypes.c_void_p(t.data_ptr())
+
+
+_IN_TORCH = {BSF_U8: "uint8", BSF_F32: "float32"}
+_OUT_TORCH = {BSF_F64: "float64", BSF_F32: "float32"}
+
+
+def _want(t, name, dtypes, numel, device=None):
+    """Validate a tensor handed to the C ABI (which cannot check it): dtype,
+    contiguity, element count and device (an int ordinal, or "cpu").  Raw
+    integer pointers are passed through unchecked."""
+    if t is None or isinstance(t, int):
+        return
+    dt = str(t.dtype).replace("torch.", "")
+    if dt not in dtypes:
+        raise BsfError(1, "%s: dtype %s, expected %s" % (name, dt, "/".join(dtypes)))
+    if not t.is_contiguous():
+        raise BsfError(1, "%s: not contiguous" % name)
+    if t.numel() < numel:
+        raise BsfError(1, "%s: %d elements, need %d" % (name, t.numel(), numel))
+    if device == "cpu":
+        if t.device.type != "cpu":
+            raise BsfError(1, "%s: expected a host tensor" % name)
+    elif device is not None and (t.device.type != "cuda" or t.device.index != device):
+        raise BsfError(1, "%s: on %s, plan is on cuda:%d" % (name, t.device, device))
 
 
 class Plan:
@@ -174,11 +201,32 @@ class Plan:
         return torch.empty(n, dtype=torch.int64, device="cuda:%d" % self.desc.device).view(
             g.nbases, self.desc.batch * self.desc.channels, g.g_height, g.g_width)
 
+    # --- argument checks (the C ABI takes raw pointers) ------------------------
+    def _npix(self):
+        d = self.desc
+        return d.batch * d.channels * d.height * d.width
+
+    def _check_f(self, f, device=None):
+        _want(f, "f", [_IN_TORCH[self.desc.in_dtype]], self._npix(),
+              self.desc.device if device is None else device)
+
+    def _check_cov(self, cov, device=None):
+        d = self.desc
+        _want(cov, "cov", ["float32"], d.batch * 3 * d.height * d.width, d.device if device is None else device)
+
+    def _check_out(self, out, device=None):
+        _want(out, "out", [_OUT_TORCH[self.desc.out_dtype]], self._npix(),
+              self.desc.device if device is None else device)
+
     # --- C-ABI calls ------------------------------------------------------------
     def preintegrate(self, f, g, stream=None):
+        self._check_f(f)
+        _want(g, "g", ["float64"], self.geometry.g_bytes // 8, self.desc.device)
         _check(lib().bsf_preintegrate(self.handle, _ptr(f), _ptr(g), _stream(stream)))
 
     def preintegrate_exact(self, f, g, stream=None):
+        self._check_f(f)
+        _want(g, "g", ["int64"], self.geometry.g_exact_bytes // 8, self.desc.device)
         _check(lib().bsf_preintegrate_exact(self.handle, _ptr(f), _ptr(g), _stream(stream)))
 
     def scan_step(self, slot, level):
@@ -194,32 +242,58 @@ class Plan:
                                     _ptr(carry) if carry is not None else None, _stream(stream)))
 
     def filter(self, g, cov, out, stream=None):
+        _want(g, "g", ["float64"], self.geometry.g_bytes // 8, self.desc.device)
+        self._check_cov(cov)
+        self._check_out(out)
         _check(lib().bsf_filter(self.handle, _ptr(g), _ptr(cov), _ptr(out), _stream(stream)))
 
-    def filter_points(self, g, cov, pts, out, stream=None):
+    def _check_pts(self, pts, out, aux=None):
         n = pts.numel() // 3
+        _want(pts, "pts", ["int32"], 3 * n, self.desc.device)
+        _want(out, "out", ["float64"], n, self.desc.device)
+        _want(aux, "aux", ["float64"], 12 * n, self.desc.device)
+        return n
+
+    def filter_points(self, g, cov, pts, out, stream=None):
+        n = self._check_pts(pts, out)
+        _want(cov, "cov", ["float32"], 3 * self.desc.height * self.desc.width, self.desc.device)
         _check(lib().bsf_filter_points(self.handle, _ptr(g), _ptr(cov), _ptr(pts), n, _ptr(out), _stream(stream)))
 
     def filter_points_aux(self, g, cov, pts, out, aux, stream=None):
-        n = pts.numel() // 3
+        n = self._check_pts(pts, out, aux)
+        _want(cov, "cov", ["float32"], 3 * self.desc.height * self.desc.width, self.desc.device)
         _check(lib().bsf_filter_points_aux(self.handle, _ptr(g), _ptr(cov), _ptr(pts), n, _ptr(out), _ptr(aux),
                                            _stream(stream)))
 
     def run_points(self, f, cov, pts, out, aux=None, stream=None):
-        n = pts.numel() // 3
+        # points name their image: f and cov must hold every image the points
+        # use (at least one; the caller guarantees the indices)
+        n = self._check_pts(pts, out, aux)
+        d = self.desc
+        _want(f, "f", [_IN_TORCH[d.in_dtype]], d.height * d.width, d.device)
+        _want(cov, "cov", ["float32"], 3 * d.height * d.width, d.device)
         _check(lib().bsf_run_points(self.handle, _ptr(f), _ptr(cov), _ptr(pts), n, _ptr(out), _ptr(aux),
                                     _stream(stream)))
 
     def run(self, f, cov, out, stream=None):
+        self._check_f(f)
+        self._check_cov(cov)
+        self._check_out(out)
         _check(lib().bsf_run(self.handle, _ptr(f), _ptr(cov), _ptr(out), _stream(stream)))
 
     def run_normalized(self, f, cov, out, stream=None):
         """DC-renormalised filter: out / filter(image indicator)."""
+        self._check_f(f)
+        self._check_cov(cov)
+        self._check_out(out)
         _check(lib().bsf_run_normalized(self.handle, _ptr(f), _ptr(cov), _ptr(out), _stream(stream)))
 
     def run_alg1(self, f, cov, out, stream=None):
         """Algorithm 1 (covariance splitting); returns sigma_b^2 per covariance field."""
         import numpy as np
+        self._check_f(f)
+        self._check_cov(cov)
+        self._check_out(out)
         sig = np.zeros(self.desc.batch, dtype=np.float64)
         _check(lib().bsf_run_alg1(self.handle, _ptr(f), _ptr(cov), _ptr(out),
                                   sig.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
@@ -230,12 +304,18 @@ class Plan:
         share `fraction` of the bound (0: (n-1)/n); returns sigma_b^2 per
         covariance field (the bound (9) is 2 sigma_b^2)."""
         import numpy as np
+        self._check_f(f)
+        self._check_cov(cov)
+        self._check_out(out)
         sig = np.zeros(self.desc.batch, dtype=np.float64)
         _check(lib().bsf_run_split(self.handle, _ptr(f), _ptr(cov), _ptr(out), int(passes), float(fraction),
                                    sig.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
         return sig
 
     def run_host(self, f_host, cov_host, out_host, stream=None):
+        self._check_f(f_host, "cpu")
+        self._check_cov(cov_host, "cpu")
+        self._check_out(out_host, "cpu")
         _check(lib().bsf_run_host(self.handle, _ptr(f_host), _ptr(cov_host), _ptr(out_host), _stream(stream)))
 
     def stats(self, reset=False):
@@ -261,6 +341,10 @@ class Plan:
         _check(lib().bsf_debug_item_cycles(self.handle, it, wk, int(nitems), ct, int(nctas)))
         wl = list(wk)
         return list(it)[:nitems], [tuple(wl[4 * i:4 * i + 4]) for i in range(nitems)], list(ct)[:nctas]
+
+    def debug_option(self, name, value):
+        """Diagnostics options of bsf_debug_option (include/bsf.h)."""
+        _check(lib().bsf_debug_option(self.handle, name.encode(), float(value)))
 
     def uses_fused(self):
         return bool(lib().bsf_uses_fused(self.handle))

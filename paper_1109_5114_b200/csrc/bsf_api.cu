@@ -58,8 +58,35 @@ struct bsf_plan_s {
     long long sched_cap = 0;
     long long nlaunch = 0;
     cudaStream_t last = nullptr;
+    bool fused_ready = false;            // fused-path buffers (fbuf, sbuf, counter, order) allocated
+    bool scratch_ready = false;          // tile-anchored halo scratch allocated
+    // global mode (order 1, u8 input): the exact int64 running
+    // sums of the whole image, read by the fused kernel's taps
+    bool global_ok = false;              // every sum of every basis stays below 2^62
+    int gshift[2] = {0, 0};              // limb split G = 2^k G1 + G0 per basis
+    int stile_global = 32;
+    long long *gx_ws = nullptr;          // [nbases][nimg][GH][GW] int64
+    // diagnostics options (bsf_debug_option); the defaults are the product path
+    bool opt_fused = true;
+    bool opt_order = true;
+    int opt_global_kernel = 1;  // global mode: 1 the order-1 integer gather (bsf_gx1.cuh), 0 the fused kernel
+    double opt_split_tol = BSF_SPLIT_TOL_DEFAULT;
 };
 
+// Select the plan's device for the duration of a call and restore the
+// caller's current device afterwards (plans may live on any device).
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+static bool global_exact(const bsf_plan_s *p);
 static size_t g_bytes(const bsf_plan_s *p) {
     return (size_t)p->geo.nbases * p->geo.nimg * p->geo.GH * p->geo.GW * sizeof(double2);
 }
@@ -284,6 +311,26 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
             V.num = (const double *)d1;  // n1 with G1 (exact)
             V.num2 = (const double *)d0; // n0 with G1 (exact)
         }
+        // order 1: int8 numerators for the global-mode gather (bsf_gx1.cuh)
+        V.n8 = nullptr;
+        if (exact && p->d.order == 1 && V.nmon <= 8) {
+            std::vector<signed char> n8((size_t)nreg * V.nmax * 8, 0);
+            bool fits = true;
+            for (size_t i = 0; i < (size_t)nreg * V.nmax; ++i)
+                for (int m = 0; m < V.nmon; ++m) {
+                    const double v = num[i * V.nmon + m];
+                    // int8, and the gather's int32 limb sums: 2^21 |n| nmax < 2^31
+                    fits = fits && fabs(v) <= 127.0 && ldexp(fabs(v) * V.nmax, 21) < 0x1p31;
+                    n8[i * 8 + m] = (signed char)v;
+                }
+            if (fits) {
+                void *d8;
+                CUDA_TRY(cudaMalloc(&d8, n8.size()));
+                p->dev_allocs.push_back(d8);
+                CUDA_TRY(cudaMemcpy(d8, n8.data(), n8.size(), cudaMemcpyHostToDevice));
+                V.n8 = (const signed char *)d8;
+            }
+        }
         // order >= 3: the B operand tables in fp32 when every value is exact there
         // (|n| <= 2^24 integers; all order-3 tables qualify)
         V.num32 = nullptr;
@@ -346,7 +393,8 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     if (d.precision != BSF_PREC_FP64 && d.precision != BSF_PREC_DD && d.precision != BSF_PREC_AUTO)
         return set_err(BSF_EINVAL, "bad precision");
     if (d.margin_x < 0 || d.margin_y < -1) return set_err(BSF_EINVAL, "negative margin");
-    if (d.anchor != BSF_ANCHOR_GLOBAL && d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EINVAL, "bad anchor");
+    if (d.anchor != BSF_ANCHOR_GLOBAL && d.anchor != BSF_ANCHOR_TILE && d.anchor != BSF_ANCHOR_AUTO)
+        return set_err(BSF_EINVAL, "bad anchor");
     if (d.boundary != BSF_BOUNDARY_ZERO && d.boundary != BSF_BOUNDARY_REPLICATE)
         return set_err(BSF_EINVAL, "bad boundary");
     if (d.super_tile != 0 && d.super_tile != 16 && d.super_tile != 32 && d.super_tile != 64)
@@ -356,7 +404,10 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     if ((d.margin_x && d.margin_x < needP) || (d.margin_y > 0 && d.margin_y < needPb))
         return set_err(BSF_ERANGE, "margins smaller than the kernel reach (need P >= " + std::to_string(needP) +
                                        ", Pb >= " + std::to_string(needPb) + ")");
-    CUDA_TRY(cudaSetDevice(d.device));
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (d.device < 0 || d.device >= ndev) return set_err(BSF_EINVAL, "device ordinal out of range");
+    DevGuard guard(d.device);
     bsf_plan_s *p = new bsf_plan_s();
     p->d = d;
     Geometry &g = p->geo;
@@ -374,7 +425,6 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
     // Otherwise the larger domains push pixels to the double-double fallback
     // (config 2, f32, r = 2: 85k pixels, 16x slower; u8 r = 3: 3x slower);
     // the passes of bsf_run_split run 32 x 32 at order 2 for that reason.
-    // (BSF_STILE = 16 / 32 / 64 overrides, diagnostics)
     {
         const double E = (double)d.max_sigma * sqrt(24.0 * d.order);
         const bool big = d.order == 1 || (d.order == 2 && d.in_dtype == BSF_U8);
@@ -384,12 +434,14 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
         const long long n32 = (long long)((d.width + 31) / 32) * ((d.height + 31) / 32) * d.batch * d.channels;
         if (p->stile == 32 && n32 < 148) p->stile = 16;
         if (d.super_tile) p->stile = d.super_tile;
-        const char *env = getenv("BSF_STILE");
-        if (env && (atoi(env) == 16 || atoi(env) == 32 || atoi(env) == 64)) p->stile = atoi(env);
     }
     g.nbases = d.basis == BSF_DUAL ? 2 : 1;
     p->bases[0] = d.basis == BSF_DUAL ? BSF_THETA : d.basis;
     p->bases[1] = BSF_THETA_PRIME;
+    {
+        const long long n32 = (long long)((d.width + 31) / 32) * ((d.height + 31) / 32) * d.batch * d.channels;
+        p->stile_global = n32 < 148 ? 16 : 32;
+    }
     LutBasis host[2];
     memset(host, 0, sizeof host);
     for (int b = 0; b < 2; ++b) {
@@ -417,12 +469,47 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
         return set_err(BSF_ENOMEM, "workspace allocation failed");
     }
     cudaMemset(p->stats, 0, 8 * sizeof(unsigned long long));
+    // global mode eligibility (u8, order 1, zero extension, full-domain plan):
+    // every running sum is an integer of at most 255 x the product of the line
+    // lengths of its levels (a row holds GW points, a line of step (sx, sy)
+    // at most GH/sy + 1), a zero-scale variant difference at most twice that;
+    // it must stay below 2^62 (int64, no wrap), and the limb split
+    // G = 2^k G1 + G0 keeps |G1|, G0 below 2^kbits of every table in use
+    if (d.in_dtype == BSF_U8 && d.order == 1 && d.boundary == BSF_BOUNDARY_ZERO && d.margin_y != -1) {
+        bool ok = true;
+        for (int b = 0; b < 2; ++b) {
+            if (!(d.basis == BSF_DUAL || d.basis == b)) continue;
+            static const int sy_order[2][4] = {{0, 1, 1, 1}, {2, 1, 2, 1}};
+            double bound = 255.0 * 2.0;
+            for (int lv = 0; lv < 4; ++lv)
+                bound *= sy_order[b][lv] == 0 ? (double)g.GW : (double)(g.GH / sy_order[b][lv] + 1);
+            int bits = 0;
+            while (ldexp(1.0, bits) <= bound) ++bits;
+            int kb = 64;
+            for (int v = 0; v < NVAR; ++v) kb = std::min(kb, host[b].var[v].kbits);
+            const int k = std::max(1, bits - kb);
+            if (bits > 62 || k > kb) ok = false;
+            p->gshift[b] = k;
+        }
+        // the order-1 gather stages every table in use in shared memory
+        int slots = 0;
+        for (int b = 0; b < 2; ++b) {
+            if (!(d.basis == BSF_DUAL || d.basis == b)) continue;
+            if (host[b].nreg > GX1_MAXREG_H) ok = false;
+            for (int v = 0; v < NVAR; ++v) {
+                slots += host[b].nreg * ((host[b].var[v].nmax + 3) & ~3);
+                if (!host[b].var[v].n8) ok = false;
+            }
+        }
+        p->global_ok = ok && slots <= GX1_SLOTS_H;
+    }
     *out = p;
     return BSF_OK;
 }
 
 extern "C" bsf_status bsf_plan_destroy(bsf_plan_t p) {
     if (!p) return BSF_OK;
+    DevGuard guard(p->d.device);
     for (void *q : p->dev_allocs) cudaFree(q);
     delete p;
     return BSF_OK;
@@ -438,11 +525,13 @@ extern "C" bsf_status bsf_plan_geometry(bsf_plan_t p, bsf_geometry *geom) {
     geom->g_bytes = g_bytes(p);
     geom->g_exact_bytes = p->d.in_dtype == BSF_U8 ? g_bytes(p) / 2 : 0;
     geom->super_tile = p->stile;
+    geom->global_mode = global_exact(p) ? 1 : 0;
     return BSF_OK;
 }
 
 extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, void *stream) {
     if (!p || !f || !g) return set_err(BSF_EINVAL, "null argument");
+    DevGuard guard(p->d.device);
     if (p->d.boundary != BSF_BOUNDARY_ZERO) return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only");
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
@@ -456,6 +545,7 @@ extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, voi
 
 extern "C" bsf_status bsf_preintegrate_exact(bsf_plan_t p, const void *f, void *g, void *stream) {
     if (!p || !f || !g) return set_err(BSF_EINVAL, "null argument");
+    DevGuard guard(p->d.device);
     if (p->d.boundary != BSF_BOUNDARY_ZERO) return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only");
     if (p->d.in_dtype != BSF_U8) return set_err(BSF_EINVAL, "exact pre-integration needs u8 input");
     cudaStream_t st = (cudaStream_t)stream;
@@ -479,6 +569,7 @@ extern "C" bsf_status bsf_scan_step(bsf_plan_t p, int slot, int level, int *sx, 
 extern "C" bsf_status bsf_scan_level(bsf_plan_t p, int slot, int level, int exact, const void *f, void *g,
                                      const void *carry, void *stream) {
     if (!p || !g || (level == 0 && !f)) return set_err(BSF_EINVAL, "null argument");
+    DevGuard guard(p->d.device);
     if (p->d.boundary != BSF_BOUNDARY_ZERO) return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only");
     if (slot < 0 || slot >= p->geo.nbases || level < 0 || level >= 4 * p->d.order)
         return set_err(BSF_EINVAL, "slot or level out of range");
@@ -509,6 +600,7 @@ static GatherArgs gather_args(bsf_plan_s *p, const void *g, const void *cov, voi
 
 extern "C" bsf_status bsf_filter(bsf_plan_t p, const void *g, const void *cov, void *out, void *stream) {
     if (!p || !g || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    DevGuard guard(p->d.device);
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
@@ -525,6 +617,7 @@ extern "C" bsf_status bsf_filter_points(bsf_plan_t p, const void *g, const void 
 extern "C" bsf_status bsf_filter_points_aux(bsf_plan_t p, const void *g, const void *cov, const int *pts, int npts,
                                             double *out, double *aux, void *stream) {
     if (!p || !g || !cov || !out || (!pts && npts)) return set_err(BSF_EINVAL, "null argument");
+    DevGuard guard(p->d.device);
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (npts < 0) return set_err(BSF_EINVAL, "npts < 0");
     if (npts == 0) return BSF_OK;
@@ -541,12 +634,11 @@ extern "C" bsf_status bsf_filter_points_aux(bsf_plan_t p, const void *g, const v
 
 // The exact split contraction (bsf_fused.cuh) serves the tile path whenever
 // every table in use keeps an exact limb of >= KBITS_MIN bits; otherwise (and
-// for BSF_PREC_FP64, or BSF_FUSED=0 in the environment) the per-thread
+// for BSF_PREC_FP64, or the diagnostics option "fused" = 0) the per-thread
 // double-double tile kernel runs.
 static bool use_fused(const bsf_plan_s *p) {
     if (p->d.precision == BSF_PREC_FP64 || p->d.order > 3) return false;
-    const char *env = getenv("BSF_FUSED");
-    if (env && env[0] == '0') return false;
+    if (!p->opt_fused) return false;
     for (int b = 0; b < 2; ++b) {
         if (!(p->d.basis == BSF_DUAL || p->d.basis == b)) continue;
         for (int v = 0; v < NVAR; ++v) {
@@ -557,17 +649,31 @@ static bool use_fused(const bsf_plan_s *p) {
     return true;
 }
 
-static bsf_status ensure_tile_ws(bsf_plan_s *p) {
-    if (p->tile_scratch) return BSF_OK;
+// Workspace of the tile path (fused or double-double tile kernel).  The halo
+// scratch (`scratch`) is only needed by tile-anchored runs; global-mode runs
+// use the fused buffers alone.  Each group is marked ready only once all of its
+// allocations succeeded, so a failed call can be retried.
+static bsf_status ensure_tile_ws(bsf_plan_s *p, bool scratch = true) {
+    if (p->fused_ready && (p->scratch_ready || !scratch)) return BSF_OK;
     int mask = p->d.basis == BSF_DUAL ? 3 : (1 << p->d.basis);
     p->fused = use_fused(p);
     p->tile_cap = tile_capacity(p->d.order, p->d.max_sigma, p->host_luts, mask, p->fused ? p->stile : TILE);
     p->tile_nslots = p->fused ? fused_slots() : tile_slots();
     void *q;
-    size_t bytes = (size_t)p->tile_nslots * (p->fused ? NPLANE_MAX : 2) * p->tile_cap * sizeof(double2);
-    if (cudaMalloc(&q, bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "tile scratch " + std::to_string(bytes));
-    p->dev_allocs.push_back(q);
-    p->tile_scratch = (double2 *)q;
+    if (scratch && !p->scratch_ready) {
+        size_t bytes = (size_t)p->tile_nslots * (p->fused ? NPLANE_MAX : 2) * p->tile_cap * sizeof(double2);
+        if (cudaMalloc(&q, bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "tile scratch " + std::to_string(bytes));
+        p->dev_allocs.push_back(q);
+        p->tile_scratch = (double2 *)q;
+        if (p->fused && p->d.order >= 3) {
+            const size_t b0 = (size_t)p->tile_nslots * NPLANE_MAX * p->tile_cap * sizeof(double);
+            if (cudaMalloc(&q, b0) != cudaSuccess) return set_err(BSF_ENOMEM, "limb scratch " + std::to_string(b0));
+            p->dev_allocs.push_back(q);
+            p->scratch0 = (double *)q;
+        }
+        p->scratch_ready = true;
+    }
+    if (p->fused_ready) return BSF_OK;
     if (p->fused) {
         const size_t fb = (size_t)p->tile_nslots * fused_fbuf_items(p->d.order) * sizeof(double2);
         if (cudaMalloc(&q, fb) != cudaSuccess) return set_err(BSF_ENOMEM, "tap buffer " + std::to_string(fb));
@@ -577,12 +683,6 @@ static bsf_status ensure_tile_ws(bsf_plan_s *p) {
         if (cudaMalloc(&q, sb) != cudaSuccess) return set_err(BSF_ENOMEM, "scale buffer " + std::to_string(sb));
         p->dev_allocs.push_back(q);
         p->sbuf = (double *)q;
-        if (p->d.order >= 3) {
-            const size_t b0 = (size_t)p->tile_nslots * NPLANE_MAX * p->tile_cap * sizeof(double);
-            if (cudaMalloc(&q, b0) != cudaSuccess) return set_err(BSF_ENOMEM, "limb scratch " + std::to_string(b0));
-            p->dev_allocs.push_back(q);
-            p->scratch0 = (double *)q;
-        }
     }
     if (cudaMalloc(&q, sizeof(int)) != cudaSuccess) return set_err(BSF_ENOMEM, "tile counter");
     p->dev_allocs.push_back(q);
@@ -603,6 +703,7 @@ static bsf_status ensure_tile_ws(bsf_plan_s *p) {
         p->sched_bin = (unsigned char *)(p->sched_order + n);
         p->sched_cap = n;
     }
+    p->fused_ready = true;
     return BSF_OK;
 }
 
@@ -633,17 +734,14 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
     a.stile = p->stile;
     a.replicate = p->d.boundary == BSF_BOUNDARY_REPLICATE;
     a.sigma2_scale = 1.0;
-    // BSF_ORDER=0 (environment, diagnostics): hand the super-tiles out in raster order
-    const char *ord = getenv("BSF_ORDER");
-    if (!(ord && ord[0] == '0')) {
+    // diagnostics option "work_order" = 0: hand the super-tiles out in raster order
+    if (p->opt_order) {
         a.order = p->sched_order;
         a.order_bin = p->sched_bin;
         a.order_hist = p->sched_hist;
         a.order_cap = p->sched_cap;
     }
-    // BSF_SPLIT_TOL (environment, diagnostics): override the fallback threshold
-    const char *tol = getenv("BSF_SPLIT_TOL");
-    a.split_tol = tol ? atof(tol) : BSF_SPLIT_TOL_DEFAULT;
+    a.split_tol = p->opt_split_tol;  // BSF_SPLIT_TOL_DEFAULT unless a diagnostics option changed it
     return a;
 }
 
@@ -653,12 +751,74 @@ static cudaError_t launch_tile(bsf_plan_s *p, const TileArgs &a, cudaStream_t st
     return launch_tile_impl(a, p->d.order, p->d.precision, p->tile_nslots, st, p->luts_dev, &p->nlaunch);
 }
 
+// Global mode: the paper's single global pre-integration as
+// exact int64 running sums, gathered by the fused kernel with both limbs of
+// the contraction exact.  Used by BSF_ANCHOR_GLOBAL and BSF_ANCHOR_AUTO when
+// the plan qualifies (u8 input, order 1, sums below 2^62).
+static bool global_exact(const bsf_plan_s *p) {
+    return p->global_ok && p->d.anchor != BSF_ANCHOR_TILE && p->opt_fused && p->d.precision != BSF_PREC_FP64;
+}
+
+static bsf_status run_global(bsf_plan_s *p, const void *f, const void *cov, void *out, const int *pts, int npts,
+                             double *aux, cudaStream_t st) {
+    bsf_status s = ensure_tile_ws(p, false);
+    if (s != BSF_OK) return s;
+    if (!p->fused) return set_err(BSF_EUNSUPPORTED, "global mode needs the exact split path");
+    // per basis and image: PadT zero rows (the zero state above the domain,
+    // read by taps near the top edge without a bounds check), then the GH x GW
+    // domain of bsf_preintegrate_exact
+    const Geometry &geo = p->geo;
+    const int padT = required_disp(p->d.max_sigma, p->d.order) + 8;
+    const size_t img_elems = (size_t)(padT + geo.GH) * geo.GW, slot = (size_t)geo.nimg * img_elems;
+    if (!p->gx_ws) {
+        void *q;
+        const size_t bytes = (size_t)geo.nbases * slot * sizeof(long long);
+        if (cudaMalloc(&q, bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "global int64 sums " + std::to_string(bytes));
+        p->dev_allocs.push_back(q);
+        p->gx_ws = (long long *)q;
+        CUDA_TRY(cudaMemsetAsync(q, 0, bytes, st));  // the pad rows stay zero (the scans write the domain only)
+    }
+    p->last = st;
+    Geometry g1 = geo;
+    g1.nimg = 1;
+    const size_t plane = (size_t)geo.H * geo.W;
+    for (int b = 0; b < geo.nbases; ++b)
+        for (int i = 0; i < geo.nimg; ++i)
+            CUDA_TRY(launch_preint_i64((const uint8_t *)f + i * plane,
+                                       (unsigned long long *)p->gx_ws + b * slot + i * img_elems + (size_t)padT * geo.GW,
+                                       g1, p->bases[b], p->d.order, st, &p->nlaunch));
+    TileArgs a = tile_args(p, f, cov, out);
+    a.gPadT = padT;
+    a.stile = p->stile_global;
+    a.order = nullptr;  // order 1: raster hand-out
+    a.gP = p->geo.P;
+    a.gGW = p->geo.GW;
+    a.gGH = p->geo.GH;
+    for (int sl = 0; sl < p->geo.nbases; ++sl) {  // slot sl of the int64 buffer holds basis bases[sl]
+        a.gglob[p->bases[sl]] = p->gx_ws + sl * slot + (size_t)padT * geo.GW;
+        a.gshift[p->bases[sl]] = p->gshift[p->bases[sl]];
+    }
+    if (pts) {
+        a.pts = pts;
+        a.npts = npts;
+        a.aux = aux;
+        a.out_f32 = 0;
+    }
+    if (p->opt_global_kernel == 1)
+        CUDA_TRY(launch_gx1(a, st, p->luts_dev, &p->nlaunch));
+    else  // diagnostics: the fused kernel's global mode (keys, bucket sort, DMMA groups)
+        CUDA_TRY(launch_fused_impl(a, p->d.order, p->tile_nslots, st, p->luts_dev, &p->nlaunch));
+    return BSF_OK;
+}
+
 extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *cov, const int *pts, int npts,
                                      double *out, double *aux, void *stream) {
     if (!p || !f || !cov || !out || (!pts && npts)) return set_err(BSF_EINVAL, "null argument");
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (npts < 0) return set_err(BSF_EINVAL, "npts < 0");
     if (npts == 0) return BSF_OK;
+    DevGuard guard(p->d.device);
+    if (global_exact(p)) return run_global(p, f, cov, out, pts, npts, aux, (cudaStream_t)stream);
     bsf_status s = ensure_tile_ws(p);
     if (s != BSF_OK) return s;
     if (p->d.boundary != BSF_BOUNDARY_ZERO && !p->fused)
@@ -676,7 +836,13 @@ extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *co
 
 extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void *out, void *stream) {
     if (!p) return set_err(BSF_EINVAL, "null plan");
-    if (p->d.anchor == BSF_ANCHOR_TILE) {
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
+    DevGuard guard(p->d.device);
+    if (global_exact(p)) {
+        if (!f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+        return run_global(p, f, cov, out, nullptr, 0, nullptr, (cudaStream_t)stream);
+    }
+    if (p->d.anchor != BSF_ANCHOR_GLOBAL) {  // BSF_ANCHOR_TILE, or AUTO without global mode
         if (!f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
         bsf_status s = ensure_tile_ws(p);
         if (s != BSF_OK) return s;
@@ -701,6 +867,7 @@ extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void
 
 extern "C" bsf_status bsf_run_normalized(bsf_plan_t p, const void *f, const void *cov, void *out, void *stream) {
     if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    DevGuard guard(p->d.device);
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (p->d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EUNSUPPORTED, "DC renormalisation runs with BSF_ANCHOR_TILE");
     bsf_status s = ensure_tile_ws(p);
@@ -755,6 +922,7 @@ static bsf_status ensure_alg1_ws(bsf_plan_s *p, bool two) {
 extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov, void *out, int passes,
                                     double fraction, double *sigma2_out, void *stream) {
     if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    DevGuard guard(p->d.device);
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (passes < 2 || passes > 16) return set_err(BSF_EINVAL, "passes must be 2..16");
     if (!(fraction < 1.0) || fraction < 0.0 || fraction != fraction)
@@ -820,6 +988,7 @@ extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov,
 extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void *cov_host, void *out_host,
                                    void *stream) {
     if (!p || !f_host || !cov_host || !out_host) return set_err(BSF_EINVAL, "null argument");
+    DevGuard guard(p->d.device);
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     const Geometry &g = p->geo;
     size_t fb = (size_t)g.nimg * g.H * g.W * (p->d.in_dtype == BSF_U8 ? 1 : 4);
@@ -847,6 +1016,7 @@ extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void 
 
 extern "C" bsf_status bsf_get_stats(bsf_plan_t p, bsf_stats *s, int reset) {
     if (!p || !s) return set_err(BSF_EINVAL, "null argument");
+    DevGuard guard(p->d.device);
     CUDA_TRY(cudaStreamSynchronize(p->last));
     unsigned long long h[8];
     CUDA_TRY(cudaMemcpy(h, p->stats, sizeof h, cudaMemcpyDeviceToHost));
@@ -867,6 +1037,7 @@ extern "C" long long bsf_launch_count(bsf_plan_t p) { return p ? p->nlaunch : 0;
 
 extern "C" bsf_status bsf_debug_phase_cycles(bsf_plan_t p, unsigned long long *out, int reset) {
     if (!p) return set_err(BSF_EINVAL, "null plan");
+    DevGuard guard(p->d.device);
     if (!p->prof) {
         void *q;
         CUDA_TRY(cudaMalloc(&q, BSF_PROF_WORDS * sizeof(unsigned long long)));
@@ -885,6 +1056,7 @@ extern "C" bsf_status bsf_debug_phase_cycles(bsf_plan_t p, unsigned long long *o
 extern "C" bsf_status bsf_debug_item_cycles(bsf_plan_t p, unsigned long long *items, unsigned long long *work,
                                             int nitems, unsigned long long *ctas, int nctas) {
     if (!p) return set_err(BSF_EINVAL, "null plan");
+    DevGuard guard(p->d.device);
     if (!p->prof) return set_err(BSF_EINVAL, "enable the counters with bsf_debug_phase_cycles first");
     if (nitems < 0 || nctas < 0 || (nitems && !items) || (nctas && !ctas))
         return set_err(BSF_EINVAL, "bad output buffers");
@@ -904,6 +1076,25 @@ extern "C" bsf_status bsf_debug_item_cycles(bsf_plan_t p, unsigned long long *it
 }
 
 extern "C" int bsf_uses_fused(bsf_plan_t p) { return p && p->fused ? 1 : 0; }
+
+extern "C" bsf_status bsf_debug_option(bsf_plan_t p, const char *name, double value) {
+    if (!p || !name) return set_err(BSF_EINVAL, "null argument");
+    const std::string n(name);
+    if (n == "fused") {
+        if (p->fused_ready || p->scratch_ready) return set_err(BSF_EINVAL, "option 'fused' must be set before the first run");
+        p->opt_fused = value != 0.0;
+    } else if (n == "work_order") {
+        p->opt_order = value != 0.0;
+    } else if (n == "global_kernel") {
+        p->opt_global_kernel = value != 0.0 ? 1 : 0;
+    } else if (n == "split_tol") {
+        if (!(value >= 0.0)) return set_err(BSF_EINVAL, "split_tol must be >= 0");
+        p->opt_split_tol = value;
+    } else {
+        return set_err(BSF_EINVAL, "unknown option " + n);
+    }
+    return BSF_OK;
+}
 
 extern "C" const char *bsf_status_str(bsf_status s) {
     switch (s) {

@@ -271,9 +271,13 @@ struct RowCfg {
                                                                                      : bsf_lane_rows(DEG, 3));
 };
 
-template <int DEG, int NT>
+// NORM (global int64 sums, both limbs exact): the accumulators hold E1 and E0
+// of E = 2^k E1 + E0; e = TwoSum(E1, E0 2^-k) is E / 2^k as an exact,
+// normalised double-double.  Otherwise (A, B) is taken as it is (below).
+template <int DEG, int NT, bool NORM = false>
 __device__ __forceinline__ void fused_rows(const double (&C)[2][NT][2], double fy, int kq,
-                                           double (&Rh)[RowCfg<DEG>::QMAX], double (&Rl)[RowCfg<DEG>::QMAX]) {
+                                           double (&Rh)[RowCfg<DEG>::QMAX], double (&Rl)[RowCfg<DEG>::QMAX],
+                                           double isc = 0.0) {
     constexpr int QMAX = RowCfg<DEG>::QMAX;
     const unsigned smask = kq == 0 ? bsf_start_mask(DEG, 0)
                            : kq == 1 ? bsf_start_mask(DEG, 1)
@@ -287,6 +291,11 @@ __device__ __forceinline__ void fused_rows(const double (&C)[2][NT][2], double f
     // Horner step, the row value is the slot itself
     const bool any = vmask & 1u;
     double rh = any ? C[0][0][0] : 0.0, rl = any ? C[1][0][0] : 0.0;
+    if constexpr (NORM) {
+        const dd e0 = two_sum(rh, rl * isc);
+        rh = e0.hi;
+        rl = e0.lo;
+    }
     int q = any ? 0 : -1;
 #pragma unroll
     for (int k = 1; k < 2 * NT; ++k) {
@@ -294,7 +303,8 @@ __device__ __forceinline__ void fused_rows(const double (&C)[2][NT][2], double f
         // (A, B) = (exact integer limb, remainder limb) is already an exact,
         // unnormalised double-double of E (|B| <= 2^-kbits |A| scale): the
         // compensated Horner step takes it as is
-        const dd e = {C[0][k >> 1][k & 1], C[1][k >> 1][k & 1]};
+        const dd e = NORM ? two_sum(C[0][k >> 1][k & 1], C[1][k >> 1][k & 1] * isc)
+                          : dd{C[0][k >> 1][k & 1], C[1][k >> 1][k & 1]};
         double nh = rh, nl = rl;
         comp_step(nh, nl, fy, e.hi, e.lo);
         if (start) {
@@ -382,11 +392,47 @@ __device__ __forceinline__ double u8_plane_bound(int basis, int R, int NX, int N
     return bound;
 }
 
-template <int DEG, int MT, int LIMBS = 2>
-__device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
+// Operand sources of fused_group: the A operand (two limbs) at a window point.
+// PlaneSrc: a super-tile halo plane already split into (G1, G0) (phase 3).
+struct PlaneSrc {
+    static constexpr bool NORM = false;
+    const double2 *__restrict__ G;
+    int NX, NY;
+    __device__ __forceinline__ double2 operator()(int lx, int ly, int &flags) const {
+        return load_split(G, NX, NY, lx, ly, flags);
+    }
+};
+// GlobSrc: the global int64 running sums of bsf_preintegrate_exact (u8 input;
+// the plan checked that no sum reaches 2^62), read at domain point (lx, ly):
+// zero above the domain (no image there), a zero-scale variant by its exact
+// lattice difference G(q) - G(q - s) (order 1, R5), split exactly
+// into G1 = v >> k and G0 = v & (2^k - 1): both limbs are integers below
+// 2^kbits, so both contractions are exact (global mode).
+struct GlobSrc {
+    static constexpr bool NORM = true;
+    const long long *__restrict__ G;
+    int GW, GH, k;
+    int sdx, sdy;  // lattice step of the dropped direction (variant planes), else (0, 0)
+    bool var;
+    __device__ __forceinline__ long long at(int lx, int ly, int &flags) const {
+        const bool inside = lx >= 0 && lx < GW && ly >= 0 && ly < GH;
+        flags |= (ly >= 0 && !inside) ? FLAG_RANGE : 0;
+        const long long v = __ldg(G + (inside ? (size_t)ly * GW + lx : 0));
+        return inside ? v : 0ll;
+    }
+    __device__ __forceinline__ double2 operator()(int lx, int ly, int &flags) const {
+        long long v = at(lx, ly, flags);
+        if (var) v -= at(lx - sdx, ly - sdy, flags);
+        return make_double2((double)(v >> k), (double)(v & ((1ll << k) - 1)));
+    }
+};
+
+template <int DEG, int MT, int LIMBS = 2, class Src = PlaneSrc>
+__device__ __forceinline__ void fused_group(const Src &src, const int (&bxt)[MT],
                                             const int (&byt)[MT], double fxo, double fyo,
                                             const int2 *__restrict__ offs, const double *__restrict__ num, int nmonp,
-                                            int n4, double (&Fh)[MT], double (&Fl)[MT], int &flags) {
+                                            int n4, double (&Fh)[MT], double (&Fl)[MT], int &flags,
+                                            double isc = 0.0) {
     constexpr int NT = DegCfg<DEG>::NT;
     const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
     double C[MT][2][NT][2];
@@ -408,14 +454,14 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
     double bA[NT], bB[NT];
     int2 dA = __ldg(offs + kq), dB = make_int2(0, 0);
 #pragma unroll
-    for (int t = 0; t < MT; ++t) aA[t] = load_split(G, NX, NY, bxt[t] + dA.x, byt[t] + dA.y, flags);
+    for (int t = 0; t < MT; ++t) aA[t] = src(bxt[t] + dA.x, byt[t] + dA.y, flags);
 #pragma unroll
     for (int j = 0; j < NT; ++j) bA[j] = __ldg(cs + 8 * j);
     if (nsteps > 1) dB = __ldg(offs + 4 + kq);
     for (int st = 0; st < nsteps; st += 2) {
         if (st + 1 < nsteps) {
 #pragma unroll
-            for (int t = 0; t < MT; ++t) aB[t] = load_split(G, NX, NY, bxt[t] + dB.x, byt[t] + dB.y, flags);
+            for (int t = 0; t < MT; ++t) aB[t] = src(bxt[t] + dB.x, byt[t] + dB.y, flags);
 #pragma unroll
             for (int j = 0; j < NT; ++j) bB[j] = __ldg(cs + (size_t)(st + 1) * cstep + 8 * j);
         }
@@ -430,7 +476,7 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
         if (st + 1 >= nsteps) break;
         if (st + 2 < nsteps) {
 #pragma unroll
-            for (int t = 0; t < MT; ++t) aA[t] = load_split(G, NX, NY, bxt[t] + dA.x, byt[t] + dA.y, flags);
+            for (int t = 0; t < MT; ++t) aA[t] = src(bxt[t] + dA.x, byt[t] + dA.y, flags);
 #pragma unroll
             for (int j = 0; j < NT; ++j) bA[j] = __ldg(cs + (size_t)(st + 2) * cstep + 8 * j);
         }
@@ -468,7 +514,7 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
             const double fyq = __shfl_sync(0xffffffffu, fyo, gq + 8 * t);
-            fused_rows<DEG, NT>(C[t], fyq, kq, Rh[t], Rl[t]);
+            fused_rows<DEG, NT, Src::NORM>(C[t], fyq, kq, Rh[t], Rl[t], isc);
         }
         const double fxm = __shfl_sync(0xffffffffu, fxo, gq + 8 * kq);
         double ah = 0.0, al = 0.0;
@@ -483,7 +529,7 @@ __device__ __forceinline__ void fused_group(const double2 *__restrict__ G, int N
             const double fxq = __shfl_sync(0xffffffffu, fxo, gq + 8 * t);
             const double fyq = __shfl_sync(0xffffffffu, fyo, gq + 8 * t);
             double Rh[RowCfg<DEG>::QMAX], Rl[RowCfg<DEG>::QMAX];
-            fused_rows<DEG, NT>(C[t], fyq, kq, Rh, Rl);
+            fused_rows<DEG, NT, Src::NORM>(C[t], fyq, kq, Rh, Rl, isc);
             double ah, al;
             fused_xhorner<DEG, DEG>(Rh, Rl, fxq, ah, al);
             const dd F = fast_two_sum(ah, al);
@@ -877,7 +923,11 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
     return true;
 }
 
-template <int R, bool SPLIT>
+// GLOBAL (order 1, u8 input): no per-super-tile pre-integration -- the taps
+// read the paper's single global pre-integration (Alg. 3
+// step 2), the exact int64 running sums of bsf_preintegrate_exact, through
+// GlobSrc; phases 2-3 are skipped and both contraction limbs are exact.
+template <int R, bool SPLIT, bool GLOBAL = false>
 __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
     constexpr int NTAP = FusedCfg<R>::NTAP, P = FusedCfg<R>::P, ITEMS = P * NTAP;
     constexpr int MT = FusedCfg<R>::MT, GS = 8 * MT;
@@ -946,6 +996,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (tid == 0) s_nfb = 0;
         __syncthreads();
         if (s_item >= nitems) break;
+        const int unit = s_item;  // hand-out index (diagnostics are keyed by it: unique in split mode too)
         int item = a.order && !a.pts ? a.order[s_item] : s_item;
         if constexpr (SPLIT) item >>= 3;  // unit code: super-tile << 3 | quadrant
         // sub-tile q of the super-tile belongs to this unit (always, unless split mode)
@@ -1017,6 +1068,23 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         __syncthreads();
         FUSED_PHASE(0);
 
+        if constexpr (GLOBAL) {
+            // the global running sums: domain x in [-P, W+P), y in [0, H+Pb)
+            if (tid < 2) {
+                s_dom[tid][0] = -a.gP;
+                s_dom[tid][1] = 0;
+                s_dom[tid][2] = a.gGW;
+                s_dom[tid][3] = a.gGH;
+            }
+            if (tid < NPLANE) {
+                const int b = tid / NVAR, v = tid % NVAR;
+                s_pe[tid] = a.gshift[b];
+                s_one[tid] = 0;
+                s_poff[tid] = ((s_vmask[b] >> v) & 1) ? 0 : -1;
+            }
+            __syncthreads();
+            FUSED_PHASE(2);
+        } else {
         // ---- 2. pre-integration planes ------------------------------------------
         if (tid == 0) {
             int np = 0;
@@ -1214,6 +1282,8 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         }
         __syncthreads();
         FUSED_PHASE(2);
+
+        }  // !GLOBAL
 
         // ---- sub-tiles: per-pixel scales, then 4-5 ------------------------------
 #pragma unroll 1
@@ -1523,17 +1593,30 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                                                                              V.nmonp, n4, 0, G0, sce, V.kbits, Fh, Fl,
                                                                              flags)));
                         }
-                    } else if (R == 1 && s_one[b * NVAR + var]) {
+                    } else if (GLOBAL) {
+                        const int k = s_pe[b * NVAR + var];
+                        const GlobSrc gs{a.gglob[b] + (size_t)img * (a.gGH + a.gPadT) * a.gGW, a.gGW, a.gGH, k,
+                                         var ? c_steps[b][var - 1][0] : 0, var ? c_steps[b][var - 1][1] : 0, var != 0};
+                        const double isc = ldexp(1.0, -k);
                         if (var == 0)
-                            fused_group<4 * R - 2, MT, 1>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl,
-                                                          flags);
+                            fused_group<4 * R - 2, MT, 2, GlobSrc>(gs, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl,
+                                                                   flags, isc);
                         else
-                            fused_group<3 * R - 2, MT, 1>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl,
-                                                          flags);
-                    } else if (var == 0)
-                        fused_group<4 * R - 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);
-                    else
-                        fused_group<3 * R - 2, MT>(G, NX, NY, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);
+                            fused_group<3 * R - 2, MT, 2, GlobSrc>(gs, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl,
+                                                                   flags, isc);
+                    } else if (R == 1 && s_one[b * NVAR + var]) {
+                        const PlaneSrc ps{G, NX, NY};
+                        if (var == 0)
+                            fused_group<4 * R - 2, MT, 1>(ps, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);
+                        else
+                            fused_group<3 * R - 2, MT, 1>(ps, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh, Fl, flags);
+                    } else if (var == 0) {
+                        fused_group<4 * R - 2, MT>(PlaneSrc{G, NX, NY}, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh,
+                                                   Fl, flags);
+                    } else {
+                        fused_group<3 * R - 2, MT>(PlaneSrc{G, NX, NY}, bxt, byt, fx, fy, offs, num, V.nmonp, n4, Fh,
+                                                   Fl, flags);
+                    }
                     if constexpr (MT == 4 && R < 3) {  // lane (g, k) holds item g + 8k's result
                         const int src = (lane >> 2) + 8 * (lane & 3);
                         const int iq = __shfl_sync(0xffffffffu, idx, src);
@@ -1621,8 +1704,10 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         // a-posteriori bound of the split contraction:
                         // |S^ - S| <= sum_j |c_j| bnd + (2 ntap + 8) u^2 sum_j |c_j F_j|, sum_j |c_j| = 2^(R ns)
                         const int ns = var ? 3 : 4;
-                        const double lb = R >= 3 ? ldexp(luts[b].var[var].bnd, -luts[b].var[var].kbits)
-                                                 : luts[b].var[var].bnd;  // three limbs: 2^-kbits tighter
+                        // (three limbs: 2^-kbits tighter; global int64 sums: both limbs exact)
+                        const double lb = GLOBAL ? 0.0
+                                          : R >= 3 ? ldexp(luts[b].var[var].bnd, -luts[b].var[var].kbits)
+                                                   : luts[b].var[var].bnd;
                         const double err = ldexp(lb, R * ns) + 2.5e-30 * (NTAP / 81.0 + 1.0) * sumCF;
                         erel = err / fabs(Sd);
                         if (!(erel <= a.split_tol)) {  // NaN-safe: recompute in double-double
@@ -1676,6 +1761,11 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 const bool pre3 = R >= 3 && s_dom[b][2] * s_dom[b][3] <= G3_PRESPLIT_MAX;
                 const double sc = ((R < 3 || pre3) && (s_vmask[b] & 1)) ? ldexp(1.0, s_pe[b * NVAR]) : 0.0;
                 GView gv = {scr + s_poff[b * NVAR], s_dom[b][0], s_dom[b][1], s_dom[b][2], s_dom[b][3], sc};
+                if constexpr (GLOBAL) {  // exact int64 global sums
+                    gv.g = nullptr;
+                    gv.sc = 0.0;
+                    gv.gi = a.gglob[b] + (size_t)img * (a.gGH + a.gPadT) * a.gGW;
+                }
                 if (pre3) {
                     gv.g0 = scr0 + s_poff[b * NVAR];
                     gv.sk = ldexp(1.0, -luts[b].var[0].kbits);
@@ -1705,17 +1795,17 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         }
         }  // sub-tiles
         __syncthreads();
-        if (a.prof && tid == 0 && item < BSF_PROF_ITEMS) {
+        if (a.prof && tid == 0 && unit < BSF_PROF_ITEMS) {
             // per-item work (bsf_debug_item_cycles): interpolation MACs, fallback pixels,
             // halo domain points of the bases in use, planes
             unsigned long long halo = 0, planes = 0;
             for (int b = 0; b < 2; ++b)
                 if (s_vmask[b]) halo += (unsigned long long)s_dom[b][2] * s_dom[b][3];
             for (int pi = 0; pi < NPLANE; ++pi) planes += s_poff[pi] >= 0;
-            a.prof[BSF_PROF_WORK + 4 * item] = s_stats[6];
-            a.prof[BSF_PROF_WORK + 4 * item + 1] = s_stats[5];
-            a.prof[BSF_PROF_WORK + 4 * item + 2] = halo;
-            a.prof[BSF_PROF_WORK + 4 * item + 3] = planes;
+            a.prof[BSF_PROF_WORK + 4 * unit] = s_stats[6];
+            a.prof[BSF_PROF_WORK + 4 * unit + 1] = s_stats[5];
+            a.prof[BSF_PROF_WORK + 4 * unit + 2] = halo;
+            a.prof[BSF_PROF_WORK + 4 * unit + 3] = planes;
         }
         if (tid < 8 && a.stats && s_stats[tid]) {
             if (tid == 4)
@@ -1727,7 +1817,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         if (a.prof && tid == 0) {
             // per-item and per-CTA busy cycles (bsf_debug_item_cycles)
             const unsigned long long dt = (unsigned long long)(clock64() - t_item);
-            if (item < BSF_PROF_ITEMS) a.prof[16 + item] = dt;
+            if (unit < BSF_PROF_ITEMS) a.prof[16 + unit] = dt;
             if (blockIdx.x < BSF_PROF_CTAS) atomicAdd(a.prof + 16 + BSF_PROF_ITEMS + blockIdx.x, dt);
         }
     }
@@ -1882,13 +1972,15 @@ __global__ void __launch_bounds__(256) fused_cost_kernel(TileArgs a, const LutBa
         const int E = max(max(ex[0], ex[1]), max(ey[0], ey[1]));
         const bool split = S == 4 && (float)(ST + 2 * E) > SCHED_SPLIT_COND * smin;
         if (!split) {
-            const int b = cost >= 1.f ? min(SCHED_NBIN - 1, 1 + (int)(4.f * __log2f(cost))) : 0;
+            // bins stop at SCHED_NBIN - 2: a split unit is stored as bin | 128,
+            // which must never equal the unused-slot sentinel 255
+            const int b = cost >= 1.f ? min(SCHED_NBIN - 2, 1 + (int)(4.f * __log2f(cost))) : 0;
             a.order_bin[(size_t)S * item] = (unsigned char)b;
             atomicAdd(a.order_hist + b, 1u);
             for (int q = 1; q < S; ++q) a.order_bin[(size_t)S * item + q] = 255;
         } else {
             const float c4 = 0.25f * cost;
-            const int b = c4 >= 1.f ? min(SCHED_NBIN - 1, 1 + (int)(4.f * __log2f(c4))) : 0;
+            const int b = c4 >= 1.f ? min(SCHED_NBIN - 2, 1 + (int)(4.f * __log2f(c4))) : 0;
             for (int q = 0; q < 4; ++q) {
                 const bool in = X0s + (ST / 2) * (q & 1) < a.W && Y0s + (ST / 2) * (q >> 1) < a.H;
                 a.order_bin[(size_t)4 * item + q] = in ? (unsigned char)(b | 128) : 255;
@@ -1935,13 +2027,13 @@ __global__ void __launch_bounds__(256) fused_order_kernel(TileArgs a, int nslots
     }
 }
 
-template <int R, bool SPLIT = false>
+template <int R, bool SPLIT = false, bool GLOBAL = false>
 static cudaError_t launch_fused_r(const TileArgs &a, int slots, cudaStream_t st, const LutBasis *luts) {
     constexpr size_t sm = fused_smem_bytes<R>();
     static std::atomic<unsigned long long> attr{0ull};
-    cudaError_t e = set_smem_attr(fused_kernel<R, SPLIT>, (int)sm, attr);
+    cudaError_t e = set_smem_attr(fused_kernel<R, SPLIT, GLOBAL>, (int)sm, attr);
     if (e != cudaSuccess) return e;
-    fused_kernel<R, SPLIT><<<slots, FT, sm, st>>>(a, luts);
+    fused_kernel<R, SPLIT, GLOBAL><<<slots, FT, sm, st>>>(a, luts);
     return cudaGetLastError();
 }
 
@@ -1971,6 +2063,7 @@ cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStrea
     // split mode (see fused_cost_kernel): 64 x 64 super-tiles at order 2 run the
     // scheduling kernels at any item count
     const int S = (a.stile == 64 && order == 2) ? 4 : 1;
+    if ((a.gglob[0] || a.gglob[1]) && order != 1) return cudaErrorInvalidValue;  // global mode: order 1 only
     if (a.order && !a.pts && order >= 2 && (S == 4 || nitems >= 2 * (long long)slots) &&
         nitems * S <= a.order_cap) {
         // largest-first work order (see fused_cost_kernel); at order 1 the
@@ -1994,7 +2087,7 @@ cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStrea
         b.order = nullptr;
     }
     switch (order) {
-        case 1: e = launch_fused_r<1>(b, slots, st, luts); break;
+        case 1: e = (b.gglob[0] || b.gglob[1]) ? launch_fused_r<1, false, true>(b, slots, st, luts) : launch_fused_r<1>(b, slots, st, luts); break;
         case 2:  // split mode only in its own instantiation (register allocation of the other plans untouched)
             e = b.order && S == 4 ? launch_fused_r<2, true>(b, slots, st, luts) : launch_fused_r<2>(b, slots, st, luts);
             break;

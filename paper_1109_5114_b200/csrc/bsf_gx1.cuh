@@ -1,0 +1,344 @@
+// Global-mode gather at order 1: the paper's Algorithm 3 step
+// 3 read from the single global pre-integration
+// held as exact int64 running sums
+// (bsf_preintegrate_exact), one thread per pixel, with an EXACT integer
+// contraction of Eq. (11):
+//
+//   E_mu = sum_s G'(b + o_s) n_{s,mu}        (integers; G' = G or its zero-
+//                                             scale lattice difference, R5)
+//   F    = (1/L) sum_mu E_mu phi_x^i phi_y^j (double-double Horner)
+//   out  = prod_k a'_k^{-1} sum_j c_j F_j    (double-double signed sum)
+//
+// At order 1 every table numerator n is a small integer (|n| < 2^5, L <= 2^6,
+// lut/gen_lut.py) and every sum |G'| < 2^62 (the plan checks it), so the
+// running sum is split into three 21-bit limbs G' = 2^42 v2 + 2^21 v1 + v0 and
+// each limb is contracted in int32 (|v| n summed over <= 24 window slots stays
+// below 2^31): one IMAD per limb and coefficient, no rounding at all before
+// the polynomial in phi.  The only rounding is in the double-double Horner and
+// signed sum (relative ~u^2 x the cancellation), bounded a posteriori; pixels
+// over the bound are recomputed by the double-double per-pixel mesh (never
+// observed).
+//
+// Included by bsf_kernels.cu after bsf_fused.cuh (uses pixel_scales,
+// ClsTables / cls_region, comp_step, mesh<>, warp_count).
+
+constexpr int GX1_BLOCK = 256;           // threads per block = pixels per tile (32 x 8)
+constexpr int GX1_TW = 32, GX1_TH = 8;
+constexpr int GX1_MAXREG = 32;
+constexpr int GX1_SLOTS = 2048;          // window slots of all order-1 tables, padded to 4 (Theta 96, Theta' 1800)
+
+// order-1 tables of one (basis, variant) in shared memory
+struct Gx1Var {
+    int nmax4, base;  // slots per region (padded to 4), first slot of region 0 in the flat arrays
+    double invL;
+};
+
+struct Gx1Smem {
+    ClsTables cls;
+    Gx1Var var[2][NVAR];
+    unsigned char cnt[2][NVAR][GX1_MAXREG];   // window slots of the region
+    int4 ext[2];                              // window offset extents (wxmin, wxmax, wymin, wymax) per basis
+    // per (basis, variant, region, slot), flat: the window offset as a linear
+    // index dy GW + dx into the running sums, and the numerators n_mu
+    // (monomials in gen_lut order, int8, padded to 8 bytes); padding slots
+    // have offset 0 and zero numerators
+    int off[GX1_SLOTS];
+    uint2 num[GX1_SLOTS];
+};
+
+__device__ __forceinline__ int gx1_byte(unsigned w, int k) {  // signed byte k of w
+    return (int)((signed char)(unsigned char)(w >> (8 * k)));
+}
+
+// One tap: F(b + phi) for the region's window, exact integer contraction then
+// double-double Horner.  NMON = 6 (degree 2, full kernel) or 3 (degree 1,
+// zero-scale variant: G' = G(q) - G(q - s_drop), exact).  Gt points at the
+// running sum of the tap's lattice base; the pixel's reach was checked against
+// the domain (and the buffer has zero rows above it), so no read is bounds
+// checked.  Slots go in groups of four with all loads of a group issued before
+// its multiply-adds.
+template <int NMON>
+__device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restrict__ Gt, int b, int v, int reg,
+                                      double fx, double fy, int sdl) {
+    int acc[3][NMON];
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int m = 0; m < NMON; ++m) acc[l][m] = 0;
+    const int n4 = (S.cnt[b][v][reg] + 3) & ~3;
+    const int row = S.var[b][v].base + reg * S.var[b][v].nmax4;
+    const int *off = S.off + row;
+    const uint2 *num = S.num + row;
+    for (int s0 = 0; s0 < n4; s0 += 4) {
+        long long g[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int o = off[s0 + i];
+            g[i] = __ldg(Gt + o);
+            if (NMON == 3) g[i] -= __ldg(Gt + (o - sdl));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint2 nw = num[s0 + i];
+            const int v0 = (int)(g[i] & 0x1FFFFF), v1 = (int)((g[i] >> 21) & 0x1FFFFF), v2 = (int)(g[i] >> 42);
+#pragma unroll
+            for (int m = 0; m < NMON; ++m) {
+                const int c = gx1_byte(m < 4 ? nw.x : nw.y, m & 3);
+                acc[0][m] += v0 * c;
+                acc[1][m] += v1 * c;
+                acc[2][m] += v2 * c;
+            }
+        }
+    }
+    // E_mu = 2^42 acc2 + 2^21 acc1 + acc0 as a normalised double-double
+    // (each term exact in fp64; the first TwoSum is exact, the second rounds
+    // only below 2^-104 |E|)
+    dd E[NMON];
+#pragma unroll
+    for (int m = 0; m < NMON; ++m) {
+        const dd t = two_sum((double)acc[2][m] * 0x1p42, (double)acc[1][m] * 0x1p21);
+        E[m] = dd_add_d(t, (double)acc[0][m]);
+    }
+    // Horner: rows i (x power) in phi_y, then phi_x; monomial order (i, j):
+    // i = deg..0, j = deg - i..0 (lut/gen_lut.py)
+    double h, l;
+    if constexpr (NMON == 6) {  // (2,0) | (1,1) (1,0) | (0,2) (0,1) (0,0)
+        double r1h = E[1].hi, r1l = E[1].lo;
+        comp_step(r1h, r1l, fy, E[2].hi, E[2].lo);
+        double r0h = E[3].hi, r0l = E[3].lo;
+        comp_step(r0h, r0l, fy, E[4].hi, E[4].lo);
+        comp_step(r0h, r0l, fy, E[5].hi, E[5].lo);
+        h = E[0].hi;
+        l = E[0].lo;
+        comp_step(h, l, fx, r1h, r1l);
+        comp_step(h, l, fx, r0h, r0l);
+    } else {  // (1,0) | (0,1) (0,0)
+        double r0h = E[1].hi, r0l = E[1].lo;
+        comp_step(r0h, r0l, fy, E[2].hi, E[2].lo);
+        h = E[0].hi;
+        l = E[0].lo;
+        comp_step(h, l, fx, r0h, r0l);
+    }
+    return fast_two_sum(h, l);
+}
+
+// The pixel's (r+1)^ns = 2^ns taps (Table 1, generalised to
+// both bases; shift of Eq. (10) absorbed in the uncentred interpolant, DESIGN.md
+// R3): D_j = sum_k (1/2 - j_k) a'_k s_k, sign (-1)^{sum j}.
+template <int NMON>
+__device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__restrict__ G, int GW, int P,
+                                           const PixelScales &ps, int x, int y, double &erel,
+                                           unsigned long long &macs) {
+    const int b = ps.basis, v = ps.drop + 1;
+    int dirs[4];
+    int ns = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (k != ps.drop) dirs[ns++] = k;
+    // v_k = s_k a'_k and the centre sum_k v_k / 2 (exact on the 2^-41 grid, R17)
+    double vx[4], vy[4], cx = 0.0, cy = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int k = q < ns ? dirs[q] : 0;
+        vx[q] = c_steps[b][k][0] * ps.ap[k];
+        vy[q] = c_steps[b][k][1] * ps.ap[k];
+        if (q < ns) {
+            cx += 0.5 * vx[q];
+            cy += 0.5 * vy[q];
+        }
+    }
+    const int sdl = v ? c_steps[b][v - 1][1] * GW + c_steps[b][v - 1][0] : 0;
+    const int ntap = 1 << ns;
+    double h0 = 0.0, e0 = 0.0, sumF = 0.0;
+    for (int t = 0; t < ntap; ++t) {
+        double Dx = cx, Dy = cy;
+        int sgn = 1;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q < ns && ((t >> q) & 1)) {
+                Dx -= vx[q];  // exact (R17)
+                Dy -= vy[q];
+                sgn = -sgn;
+            }
+        const double flx = floor(Dx), fly = floor(Dy);
+        const double fx = Dx - flx, fy = Dy - fly;  // exact
+        const int reg = cls_region(S.cls, b, fx, fy);
+        const long long *Gt = G + ((ptrdiff_t)(y + (int)fly) * GW + (x + (int)flx + P));
+        const dd F = gx1_tap<NMON>(S, Gt, b, v, reg, fx, fy, sdl);
+        macs += (unsigned long long)S.cnt[b][v][reg] * NMON;  // algorithmic: window x monomials
+        // compensated signed sum: TwoSum on the heads, small terms in e0
+        const double fh = sgn > 0 ? F.hi : -F.hi, fl = sgn > 0 ? F.lo : -F.lo;
+        const dd s = two_sum(h0, fh);
+        h0 = s.hi;
+        e0 += s.lo + fl;
+        sumF += fabs(F.hi);
+    }
+    const dd Ssum = fast_two_sum(h0, e0);
+    double norm = S.var[b][v].invL;  // 1 / L
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (q < ns) norm /= ps.ap[dirs[q]];
+    const double Sd = dd_to_d(Ssum);
+    // rounding of the Horner steps and of the sum: (2 ntap + 8) u^2 sum_j |F_j|
+    erel = 2.5e-30 * (double)(2 * ntap + 8) * sumF / fabs(Sd);
+    return Sd * norm;
+}
+
+// the double-double fallback, out of line (rarely taken: keeps the main
+// path's register allocation small)
+__device__ __noinline__ double gx1_fallback(const long long *G, int P, int GW, int GH, const LutBasis &L,
+                                            const PixelScales &ps, int x, int y, int *flags) {
+    GView gv = {nullptr, -P, 0, GW, GH, 0.0};
+    gv.gi = G;
+    return mesh<1, true>(gv, L, ps, x, y, flags);
+}
+
+#ifndef GX1_MINB
+#define GX1_MINB 2
+#endif
+__global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
+    __shared__ Gx1Smem S;
+    const int tid = threadIdx.x;
+    // stage the classifier and the order-1 integer tables of both bases
+    if (tid < 2) {
+        const LutBasis &L = luts[tid];
+        for (int k = 0; k < 4; ++k) {
+            S.cls.normal[tid][k] = L.normal[k];
+            S.cls.kmin[tid][k] = L.kmin[k];
+            S.cls.radix[tid][k] = L.radix[k];
+        }
+        for (int i = 0; i < 81; ++i) S.cls.table[tid][i] = L.table[i];
+    }
+    int base = 0;  // the host checked that the tables in use fit GX1_SLOTS / GX1_MAXREG
+    for (int bv = 0; bv < 2 * NVAR; ++bv) {
+        const int b = bv / NVAR, v = bv % NVAR;
+        if (!a.gglob[b]) continue;  // basis not in the plan
+        const LutVar &V = luts[b].var[v];
+        const int nreg = luts[b].nreg;
+        const int nmax4 = (V.nmax + 3) & ~3;
+        if (tid == 0) S.var[b][v] = Gx1Var{nmax4, base, 1.0 / V.L};
+        if (tid == 0 && v == 0) S.ext[b] = make_int4(luts[b].wxmin, luts[b].wxmax, luts[b].wymin, luts[b].wymax);
+        for (int i = tid; i < nreg; i += GX1_BLOCK) S.cnt[b][v][i] = (unsigned char)__ldg(V.counts + i);
+        for (int i = tid; i < nreg * nmax4; i += GX1_BLOCK) {
+            const int r = i / nmax4, sl = i % nmax4;
+            const bool real = sl < __ldg(V.counts + r);
+            const int2 o = real ? __ldg(V.offs + r * V.nmax + sl) : make_int2(0, 0);
+            S.off[base + i] = o.y * a.gGW + o.x;
+            S.num[base + i] = real ? __ldg(reinterpret_cast<const uint2 *>(V.n8) + r * V.nmax + sl) : make_uint2(0u, 0u);
+        }
+        base += nreg * nmax4;
+    }
+    __syncthreads();
+    const size_t ipl = (size_t)a.H * a.W;
+    const int ntx = (a.W + GX1_TW - 1) / GX1_TW, nty = (a.H + GX1_TH - 1) / GX1_TH;
+    const long long nunits = a.pts ? ((long long)a.npts + GX1_BLOCK - 1) / GX1_BLOCK : (long long)ntx * nty * a.nimg;
+    unsigned long long macs = 0;
+    // static grid-stride over 32 x 8 pixel tiles in raster order: the blocks of
+    // a wave read neighbouring rows of the running sums (L2 reuse of the taps)
+    for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
+        int img, x, y;
+        long long oidx;
+        bool valid;
+        if (a.pts) {
+            const long long i = u * GX1_BLOCK + tid;
+            valid = i < a.npts;
+            img = valid ? a.pts[3 * i] : 0;
+            x = valid ? a.pts[3 * i + 1] : 0;
+            y = valid ? a.pts[3 * i + 2] : 0;
+            oidx = i;
+        } else {
+            img = (int)(u / ((long long)ntx * nty));
+            const int rem = (int)(u % ((long long)ntx * nty));
+            x = (rem % ntx) * GX1_TW + tid % GX1_TW;
+            y = (rem / ntx) * GX1_TH + tid / GX1_TW;
+            valid = x < a.W && y < a.H;
+            oidx = (long long)img * ipl + (size_t)y * a.W + x;
+        }
+        PixelScales ps;
+        ps.flags = 0;
+        ps.basis = 0;
+        ps.drop = -1;
+        ps.clamped = 0;
+        if (valid) {
+            double sx, sy, th;
+            load_cov(a, img, x, y, sx, sy, th);
+            pixel_scales(sx, sy, th, a.policy, a.clamp, 1, ps);
+        }
+        int flags = ps.flags;
+        const bool live = valid && !(flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
+        double res = __longlong_as_double(0x7ff8000000000000LL), erel = 0.0;
+        bool used_dd = false;
+        if (live) {
+            // every read stays inside the domain (plus the zero rows above it)
+            // when the pixel's reach is within the plan's margins; else NaN and
+            // BSF_ERANGE (a covariance above the plan's max_sigma)
+            double rx = 0.0, ry = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                rx += ps.ap[k] * abs(c_steps[ps.basis][k][0]);
+                ry += ps.ap[k] * c_steps[ps.basis][k][1];
+            }
+            const int ex = (int)ceil(0.5 * rx) + 1, ey = (int)ceil(0.5 * ry) + 1;
+            const int4 E = S.ext[ps.basis];
+            const bool in = x + a.gP - ex + E.x - 2 >= 0 && x + a.gP + ex + E.y + 2 < a.gGW &&
+                            y - ey + E.z - 2 >= -a.gPadT && y + ey + E.w < a.gGH;
+            if (!in) {
+                flags |= FLAG_RANGE;
+            } else {
+                const long long *G = a.gglob[ps.basis] + (size_t)img * (a.gGH + a.gPadT) * a.gGW;
+                res = ps.drop < 0 ? gx1_mesh<6>(S, G, a.gGW, a.gP, ps, x, y, erel, macs)
+                                  : gx1_mesh<3>(S, G, a.gGW, a.gP, ps, x, y, erel, macs);
+                if (!(erel <= a.split_tol)) {  // NaN-safe: the double-double mesh on the same sums
+                    res = gx1_fallback(G, a.gP, a.gGW, a.gGH, luts[ps.basis], ps, x, y, &flags);
+                    used_dd = true;
+                }
+            }
+        }
+        if (valid) {
+            if (a.aux) {
+                double *ax = a.aux + BSF_AUX * oidx;
+                ax[0] = ps.basis;
+                ax[1] = ps.drop;
+                ax[2] = ps.clamped;
+                ax[3] = flags;
+                for (int k = 0; k < 4; ++k) ax[4 + k] = ps.ap[k];
+                ax[8] = used_dd;
+                ax[9] = erel;
+                ax[10] = ax[11] = 0.0;
+            }
+            if (a.out_f32 && !a.pts)
+                ((float *)a.out)[oidx] = (float)res;
+            else
+                ((double *)a.out)[oidx] = res;
+        }
+        if (a.stats) {
+            warp_count(a.stats + 0, valid);
+            warp_count(a.stats + 1, valid && ps.clamped);
+            warp_count(a.stats + 2, valid && ps.drop >= 0);
+            warp_count(a.stats + 3, valid && ps.basis == BASIS_THETA_PRIME);
+            warp_count(a.stats + 5, used_dd);
+            if (valid && flags) atomicOr(a.stats + 4, (unsigned long long)flags);
+        }
+    }
+    if (a.stats) {
+        for (int o = 16; o; o >>= 1) macs += __shfl_xor_sync(0xffffffffu, macs, o);
+        if ((tid & 31) == 0 && macs) atomicAdd(a.stats + 6, macs);
+    }
+}
+
+int gx1_slots() {
+    int dev = 0, sms = 148, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gx1_kernel, GX1_BLOCK, 0) != cudaSuccess || per < 1)
+        per = 1;
+    return sms * per;
+}
+
+cudaError_t launch_gx1(const TileArgs &a, cudaStream_t st, const LutBasis *luts, long long *nl) {
+    static int slots = 0;
+    if (!slots) slots = gx1_slots();
+    gx1_kernel<<<slots, GX1_BLOCK, 0, st>>>(a, luts);
+    ++*nl;
+    return cudaGetLastError();
+}

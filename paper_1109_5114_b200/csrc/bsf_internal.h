@@ -105,6 +105,8 @@ struct LutVar {
     const double *numf;    // [nreg][nslot4][nmonp] n (nsplit 2: the G0 limb's operand)
     const float *num32;    // order >= 3, when exact in fp32: [nreg][nslot4][nmonp] n (nsplit 1) or
                            // interleaved (n1, n0) pairs (nsplit 2) -- half the bytes of the MMA's B loads
+    const signed char *n8; // order 1 (global-mode gather, bsf_gx1.cuh): [nreg][nmax][8] numerators n as int8
+                           // (monomials in gen_lut order, zero padded); null when some |n| > 127
     float mean_count;      // window slots averaged over the regions (work-item cost estimate)
     double bnd;            // bound on |F - F^| (units 2^e) of the split contraction: gamma_{n+1} 0.5 max_reg sum_s,mu |n|
     double L;              // common denominator
@@ -176,6 +178,13 @@ struct TileArgs {
     unsigned char *order_bin;  // [items] cost bin of each super-tile
     unsigned *order_hist;      // [2][SCHED_NBIN] bin counts, scatter cursors, then the unit count
     long long order_cap;       // units (bin slots) the order buffers hold
+    // global mode (order 1, u8): taps read the exact int64 global running sums
+    // [nbases][nimg][gGH][gGW] (bsf_preintegrate_exact layout), limb shift per basis
+    const long long *gglob[2];  // per basis id (null: basis not in the plan / not global mode): row 0 of
+                                // image 0's domain; images are (gPadT + gGH) rows apart, the first gPadT
+                                // rows of each being zeros (the zero state above the domain)
+    int gP, gGW, gGH, gPadT;
+    int gshift[2];
 };
 constexpr int SCHED_NBIN = 128;
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per device
@@ -220,6 +229,9 @@ int fused_slots();
 size_t fused_fbuf_items(int order);
 cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStream_t st, const LutBasis *luts_dev,
                               long long *nlaunch);
+// global-mode gather at order 1 (bsf_gx1.cuh): one thread per pixel, exact int32-limb contraction
+constexpr int GX1_SLOTS_H = 2048, GX1_MAXREG_H = 32;
+cudaError_t launch_gx1(const TileArgs &a, cudaStream_t st, const LutBasis *luts_dev, long long *nlaunch);
 
 // launchers (bsf_kernels.cu)
 // global pre-integration: one single-pass kernel per level (bsf_scan.cuh)

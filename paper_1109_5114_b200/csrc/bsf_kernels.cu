@@ -315,6 +315,7 @@ struct GView {
     double sc;  // 0: double-double {hi, lo}; else split limbs (G1, G0) of G = sc (G1 + G0) (bsf_fused.cuh)
     const double *g0 = nullptr;  // order 3: g holds (G1, G2) and g0 the third limb, G = sc (G1 + sk (G2 + G0))
     double sk = 0.0;
+    const long long *gi = nullptr;  // exact int64 global sums (fused global mode): read as exact double-doubles
 };
 
 __device__ __forceinline__ double2 load_g2(const GView &v, int qx, int qy, int *flags) {
@@ -325,6 +326,11 @@ __device__ __forceinline__ double2 load_g2(const GView &v, int qx, int qy, int *
         return make_double2(0.0, 0.0);
     }
     const size_t i = (size_t)ly * v.NX + lx;
+    if (v.gi) {  // |value| < 2^62: hi = fl(value), the remainder is exact
+        const long long q = __ldg(v.gi + i);
+        const double hi = (double)q;
+        return make_double2(hi, (double)(q - (long long)hi));
+    }
     const double2 t = v.g[i];  // plain load: tile scratch is written in-kernel
     if (v.sc == 0.0) return t;
     if (v.g0) {  // three limbs: every product below is an exact power-of-two scaling
@@ -879,6 +885,7 @@ static void launch_r(const GatherArgs &a, int prec, cudaStream_t st, const LutBa
 }
 
 #include "bsf_fused.cuh"
+#include "bsf_gx1.cuh"
 
 #ifdef BSF_TAP_DUMP
 extern "C" void bsf_debug_set_dump(double *p) { cudaMemcpyToSymbol(g_tap_dump, &p, sizeof p); }

@@ -211,3 +211,74 @@ def sample_points(w: Workload, n: int, seed: int = 0, frames: int = 1):
         pts.append((img, int(ux[i] * W), int(uy[i] * H)))
         i += 1
     return torch.tensor(pts[:n], dtype=torch.int32)
+
+
+def _upsample_pts(grid: torch.Tensor, n: int, ys: torch.Tensor, xs: torch.Tensor) -> torch.Tensor:
+    """_upsample at scattered pixels (ys[i], xs[i]): the same arithmetic per
+    element, so the values are bit-identical to the gridded version."""
+    g = grid.shape[0]
+    fy = ys.to(torch.float64) * (g - 1) / (n - 1)
+    fx = xs.to(torch.float64) * (g - 1) / (n - 1)
+    iy = torch.clamp(fy.floor().long(), max=g - 2)
+    ix = torch.clamp(fx.floor().long(), max=g - 2)
+    ty = fy - iy
+    tx = fx - ix
+    a = grid[iy, ix]
+    b = grid[iy, ix + 1]
+    c = grid[iy + 1, ix]
+    d = grid[iy + 1, ix + 1]
+    return (a * (1 - ty) * (1 - tx) + b * (1 - ty) * tx + c * ty * (1 - tx) + d * ty * tx)
+
+
+def cov_at(w: Workload, xs, ys, frame: int = 0) -> torch.Tensor:
+    """make_cov's float32 (sigma_x, sigma_y, theta) at scattered pixels:
+    returns (3, n), bit-identical to make_cov(w)[:, ys, xs] without building
+    the whole field (config 5 is 32768^2)."""
+    xs = torch.as_tensor(xs, dtype=torch.int64)
+    ys = torch.as_tensor(ys, dtype=torch.int64)
+    cfg = int(w.name[1])
+    H, W = w.height, w.width
+    if cfg == 1 or w.extra.get("isotropic"):
+        s = w.extra.get("sigma", 3.0)
+        smaj = torch.full(xs.shape, s, dtype=torch.float64)
+        ratio = torch.ones_like(smaj)
+        th = torch.zeros_like(smaj)
+    elif cfg in (2, 4):
+        scale = 1.0
+        if cfg == 4:
+            scale = 0.5 + 1.5 * float(uniform(torch.tensor([frame]), w.seed, 700)[0])
+        X = xs.to(torch.float64)
+        Y = ys.to(torch.float64)
+        smaj = (1.0 + 15.0 * X / (W - 1)) * scale + 0 * Y
+        ratio = 1.0 + 3.0 * Y / (H - 1) + 0 * X
+        th = torch.remainder(torch.atan2(Y - H / 2, X - W / 2), math.pi)
+    else:
+        n = 32 if cfg == 3 else 256
+        smax = 40.0 if cfg == 3 else 64.0
+        gi = torch.arange(n * n, dtype=torch.int64)
+        gs = (2.0 + (smax - 2.0) * uniform(gi, w.seed, 800)).view(n, n)
+        gr = (1.0 + 5.0 * uniform(gi, w.seed, 801)).view(n, n)
+        gt = (math.pi * uniform(gi, w.seed, 802)).view(n, n)
+        span = w.extra.get("grid_span", max(H, W))
+        smaj = _upsample_pts(gs, span, ys, xs)
+        ratio = _upsample_pts(gr, span, ys, xs)
+        th = _upsample_pts(gt, span, ys, xs)
+    smin = smaj / torch.sqrt(ratio)
+    return torch.stack([smaj, smin, th]).to(torch.float32)
+
+
+def image_at(w: Workload, xs, ys, frame: int = 0, channel: int = 0) -> torch.Tensor:
+    """make_image's values at scattered pixels (configs 1, 3, 4, 5: per-pixel
+    hashes; config 2's rectangles are painted by make_image only)."""
+    xs = torch.as_tensor(xs, dtype=torch.int64)
+    ys = torch.as_tensor(ys, dtype=torch.int64)
+    idx = ys * w.width + xs
+    stream = 10 + 97 * frame + channel
+    cfg = int(w.name[1])
+    if w.in_dtype == "u8":
+        return uniform_u8(idx, w.seed, stream)
+    if cfg == 4:
+        return (0.5 + 0.15 * normal(idx, w.seed, stream)).clamp(0.0, 1.0).to(torch.float32)
+    if cfg == 2:
+        raise ValueError("config 2: use make_image")
+    return uniform(idx, w.seed, stream, torch.float32)

@@ -12,11 +12,11 @@ DT = {"u8": bsf.BSF_U8, "f32": bsf.BSF_F32}
 
 
 def make_plan(w: synth.Workload, *, policy=None, order=None, precision=bsf.BSF_PREC_DD, clamp=1, out_f32=False,
-              margin_x=0, margin_y=0, batch=None, anchor=bsf.BSF_ANCHOR_GLOBAL):
+              margin_x=0, margin_y=0, batch=None, anchor=bsf.BSF_ANCHOR_GLOBAL, super_tile=0):
     return bsf.Plan(w.width, w.height, batch=batch or w.batch, channels=w.channels, in_dtype=DT[w.in_dtype],
                     out_dtype=bsf.BSF_F32 if out_f32 else bsf.BSF_F64, order=order or w.order,
                     basis=w.basis if policy is None else policy, max_sigma=w.max_sigma, margin_x=margin_x,
-                    margin_y=margin_y, clamp=clamp, precision=precision, anchor=anchor)
+                    margin_y=margin_y, clamp=clamp, precision=precision, anchor=anchor, super_tile=super_tile)
 
 
 def gpu_full(plan: bsf.Plan, img: torch.Tensor, cov: torch.Tensor, out_dtype=torch.float64) -> torch.Tensor:

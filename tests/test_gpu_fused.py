@@ -3,7 +3,6 @@ kernel and against itself: its double-double fallback, its work counter and
 its dispatch.  (Parity with the oracle is in test_gpu_tile.py /
 test_gpu_orders.py, which run the fused path by default.)"""
 import math
-import os
 
 import numpy as np
 import pytest
@@ -16,22 +15,6 @@ from test_gpu_parity import _small_smooth
 
 pytestmark = pytest.mark.gpu
 TILE = bsf.BSF_ANCHOR_TILE
-
-
-class _env:
-    def __init__(self, **kw):
-        self.kw = kw
-
-    def __enter__(self):
-        self.old = {k: os.environ.get(k) for k in self.kw}
-        os.environ.update({k: str(v) for k, v in self.kw.items()})
-
-    def __exit__(self, *a):
-        for k, v in self.old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
 
 
 def test_dispatch():
@@ -49,10 +32,10 @@ def test_dispatch():
     p4 = make_plan(w3, policy=0, order=4, anchor=TILE)
     tile_points(p4, synth.make_image(w3)[None], synth.make_cov(w3), synth.sample_points(w3, 2, seed=1))
     assert not p4.uses_fused()
-    with _env(BSF_FUSED=0):
-        p0 = make_plan(w, anchor=TILE)
-        tile_points(p0, synth.make_image(w)[None], synth.make_cov(w), pts)
-        assert not p0.uses_fused()
+    p0 = make_plan(w, anchor=TILE)
+    p0.debug_option("fused", 0)
+    tile_points(p0, synth.make_image(w)[None], synth.make_cov(w), pts)
+    assert not p0.uses_fused()
 
 
 @pytest.mark.parametrize("config,order,n", [(2, 2, 3000), (3, 1, 3000), (3, 2, 600), (4, 3, 60)])
@@ -64,8 +47,9 @@ def test_fused_matches_double_double_kernel(config, order, n):
     img, cov = synth.make_image(w), synth.make_cov(w)
     pts = synth.sample_points(w, n, seed=5)
     a = tile_points(make_plan(w, anchor=TILE), img[None], cov, pts)
-    with _env(BSF_FUSED=0):
-        b = tile_points(make_plan(w, anchor=TILE), img[None], cov, pts)
+    pb = make_plan(w, anchor=TILE)
+    pb.debug_option("fused", 0)
+    b = tile_points(pb, img[None], cov, pts)
     rel = (a - b).abs() / b.abs()
     # at r = 3 the double-double kernel's own error reaches ~1e-12 on the most
     # ill-conditioned pixels (u^2 times a condition number ~1e20)
@@ -74,7 +58,7 @@ def test_fused_matches_double_double_kernel(config, order, n):
 
 @pytest.mark.parametrize("r", [1, 2, 3])
 def test_forced_fallback_matches_split_path(r):
-    """BSF_SPLIT_TOL=0 sends every pixel to the warp-cooperative double-double
+    """split_tol = 0 sends every pixel to the warp-cooperative double-double
     fallback (mesh_warp on the split planes); it must agree with the split
     path and be counted."""
     H, W = 45, 53
@@ -83,8 +67,8 @@ def test_forced_fallback_matches_split_path(r):
     a = gpu_full(plan, img, cov)[0]
     st = plan.stats(reset=True)
     assert st["double_double"] < st["pixels"] // 10
-    with _env(BSF_SPLIT_TOL=0):
-        b = gpu_full(plan, img, cov)[0]
+    plan.debug_option("split_tol", 0.0)
+    b = gpu_full(plan, img, cov)[0]
     st = plan.stats(reset=True)
     assert st["double_double"] == st["pixels"] == H * W
     rel = (a - b).abs() / b.abs()
@@ -134,10 +118,9 @@ def test_super_tile_64_matches_32():
     p64 = make_plan(w, anchor=TILE, batch=2)
     assert p64.geometry.super_tile == 64
     a = gpu_full(p64, img, cov)
-    with _env(BSF_STILE=32):
-        p32 = make_plan(w, anchor=TILE, batch=2)
-        assert p32.geometry.super_tile == 32
-        b = gpu_full(p32, img, cov)
+    p32 = make_plan(w, anchor=TILE, batch=2, super_tile=32)
+    assert p32.geometry.super_tile == 32
+    b = gpu_full(p32, img, cov)
     rel = ((a - b).abs() / b.abs()).max()
     assert float(rel) <= 1e-12, float(rel)
     from gpu_util import oracle_points
@@ -195,11 +178,11 @@ def test_work_order_changes_nothing_but_the_schedule(r):
     cov = synth.make_cov(w)
     runs = {}
     for o in ("0", "1"):
-        with _env(BSF_ORDER=o):
-            plan = make_plan(w, anchor=TILE, batch=1)
-            n0 = plan.launch_count()
-            out = gpu_full(plan, img, cov)
-            runs[o] = (out, plan.launch_count() - n0, plan.stats())
+        plan = make_plan(w, anchor=TILE, batch=1)
+        plan.debug_option("work_order", int(o))
+        n0 = plan.launch_count()
+        out = gpu_full(plan, img, cov)
+        runs[o] = (out, plan.launch_count() - n0, plan.stats())
     assert torch.equal(runs["0"][0], runs["1"][0])
     assert runs["1"][1] == runs["0"][1] + 2
     for k in ("pixels", "macs", "double_double"):
@@ -217,10 +200,9 @@ def test_order2_u8_super_tile_64():
     p64 = make_plan(w, anchor=TILE)
     assert p64.geometry.super_tile == 64
     a = gpu_full(p64, img[None], cov)
-    with _env(BSF_STILE=32):
-        p32 = make_plan(w, anchor=TILE)
-        assert p32.geometry.super_tile == 32
-        b = gpu_full(p32, img[None], cov)
+    p32 = make_plan(w, anchor=TILE, super_tile=32)
+    assert p32.geometry.super_tile == 32
+    b = gpu_full(p32, img[None], cov)
     rel = ((a - b).abs() / b.abs()).max()
     assert float(rel) <= 2e-9, float(rel)
     from gpu_util import oracle_points
@@ -277,12 +259,12 @@ def test_split_mode_quadrants_small_scales():
     cov = torch.stack([smaj, smaj / 1.6, th]).to(torch.float32)
     res = {}
     for o in ("0", "1"):
-        with _env(BSF_ORDER=o):
-            plan = make_plan(w, anchor=TILE, batch=1)
-            assert plan.geometry.super_tile == 64
-            n0 = plan.launch_count()
-            out = gpu_full(plan, img[None], cov)
-            res[o] = (out, plan.stats()["double_double"], plan.launch_count() - n0)
+        plan = make_plan(w, anchor=TILE, batch=1)
+        plan.debug_option("work_order", int(o))
+        assert plan.geometry.super_tile == 64
+        n0 = plan.launch_count()
+        out = gpu_full(plan, img[None], cov)
+        res[o] = (out, plan.stats()["double_double"], plan.launch_count() - n0)
     assert res["1"][2] == 3 and res["0"][2] == 1
     assert res["1"][1] < res["0"][1], (res["1"][1], res["0"][1])
     from gpu_util import oracle_points
@@ -293,3 +275,26 @@ def test_split_mode_quadrants_small_scales():
     for o in ("0", "1"):
         err = np.max(np.abs(res[o][0][0].numpy()[ys, xs] - ref) / np.abs(ref))
         assert err <= 1e-9, (o, err)
+
+
+def test_split_mode_cost_bin_saturation():
+    """A covariance far above the plan's max_sigma in one 64 x 64 super-tile
+    of an order-2 u8 plan: its cost estimate saturates the largest bin and it
+    is handed out as quadrant units (tiny sigma_min).  Every unit must still
+    be scheduled: NaN and BSF_ERANGE there (the documented behaviour), finite
+    results elsewhere, no out-of-bounds writes."""
+    W, H = 256, 192
+    w = synth.workload(3, order=2, width=W, height=H, max_sigma=20.0)
+    img = synth.make_image(w)
+    cov = torch.stack([torch.full((H, W), 3.0), torch.full((H, W), 2.0), torch.full((H, W), 0.3)])
+    cov[0, 64:128, 64:128] = 800.0
+    cov[1, 64:128, 64:128] = 0.3
+    plan = make_plan(w, anchor=TILE)
+    assert plan.geometry.super_tile == 64
+    out = gpu_full(plan, img[None], cov.to(torch.float32))[0]
+    st = plan.stats(reset=True)
+    assert st["status"] == 5  # BSF_ERANGE
+    assert torch.isnan(out[64:128, 64:128]).all()
+    mask = torch.ones(H, W, dtype=torch.bool)
+    mask[64:128, 64:128] = False
+    assert torch.isfinite(out[mask]).all()

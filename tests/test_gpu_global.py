@@ -1,0 +1,92 @@
+"""Global mode: the paper's single global pre-integration
+(Alg. 3 step 2) as exact int64 running
+sums, gathered by the fused kernel with an exact two-limb contraction.  Parity
+with the oracle at 1e-9 through the full-image launch (bsf_run), at config
+scale on stratified pixels."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from paper_1109_5114_b200 import bsf
+from gpu_util import gpu_full, make_plan, oracle_points
+from strata import stratified_points
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(w, img, cov, pts, out, r=1, policy=None):
+    policy = w.basis if policy is None else policy
+    xs, ys = pts[:, 1].numpy(), pts[:, 2].numpy()
+    ref, *_ = oracle_points(img.numpy(), cov.numpy(), xs, ys, policy=policy, r=r)
+    got = out[0].numpy()[ys, xs]
+    rel = np.abs(got - ref) / np.abs(ref)
+    return float(rel.max()), rel
+
+
+def test_global_mode_config1_every_pixel():
+    w = synth.workload(1)
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    for anchor in (bsf.BSF_ANCHOR_GLOBAL, bsf.BSF_ANCHOR_AUTO):
+        plan = make_plan(w, anchor=anchor)
+        assert plan.geometry.global_mode == 1
+        out = gpu_full(plan, img[None], cov)
+        ys, xs = np.mgrid[0:w.height, 0:w.width]
+        pts = torch.tensor(np.stack([0 * xs.ravel(), xs.ravel(), ys.ravel()], 1), dtype=torch.int32)
+        err, _ = _check(w, img, cov, pts, out)
+        assert err <= 1e-9, err
+        st = plan.stats(reset=True)
+        assert st["status"] == 0 and st["pixels"] == w.width * w.height and st["double_double"] == 0
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2])
+def test_global_mode_space_variant_small(policy):
+    """Every pixel of a ragged 150 x 97 u8 image, config-3 field (large
+    sigma relative to the image, zero-scale variants, both bases)."""
+    w = synth.workload(3, width=150, height=97, max_sigma=40.0, extra={"grid_span": 300})
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    plan = make_plan(w, policy=policy, anchor=bsf.BSF_ANCHOR_GLOBAL)
+    assert plan.geometry.global_mode == 1
+    out = gpu_full(plan, img[None], cov)
+    ys, xs = np.mgrid[0:w.height:3, 0:w.width:3]
+    pts = torch.tensor(np.stack([0 * xs.ravel(), xs.ravel(), ys.ravel()], 1), dtype=torch.int32)
+    err, _ = _check(w, img, cov, pts, out, policy=policy)
+    assert err <= 1e-9, err
+    st = plan.stats(reset=True)
+    assert st["status"] == 0 and st["zero_scale"] > 0
+
+
+def test_global_mode_config3_full_size_stratified():
+    """Config 3 at full size (4096^2 u8, order 1) through bsf_run: >= 300
+    stratified pixels against the oracle, no tolerance floor."""
+    w = synth.workload(3)
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    plan = make_plan(w, anchor=bsf.BSF_ANCHOR_AUTO)
+    assert plan.geometry.global_mode == 1
+    out = gpu_full(plan, img[None], cov)
+    pts, labels = stratified_points(w, 320, seed=3, r=1)
+    err, rel = _check(w, img, cov, pts, out)
+    worst = {k: float(rel[v].max()) for k, v in labels.items() if v}
+    assert err <= 1e-9, worst
+    st = plan.stats()
+    assert st["status"] == 0 and st["double_double"] == 0 and st["pixels"] == w.width * w.height
+
+
+def test_global_mode_matches_tile_path():
+    """The global (paper-literal) and the tile-anchored paths compute the same
+    filter: agreement far inside the 1e-9 contract on a 512^2 crop."""
+    w = synth.workload(3, width=512, height=512, extra={"grid_span": 4096})
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    a = gpu_full(make_plan(w, anchor=bsf.BSF_ANCHOR_GLOBAL), img[None], cov)
+    b = gpu_full(make_plan(w, anchor=bsf.BSF_ANCHOR_TILE), img[None], cov)
+    rel = ((a - b).abs() / b.abs()).max()
+    assert float(rel) <= 1e-11, float(rel)
+
+
+def test_global_mode_not_taken_when_sums_could_overflow():
+    """Order 2 at config-3 size: the int64 sums would wrap, so AUTO anchors
+    per super-tile and GLOBAL keeps the double-double global path."""
+    w = synth.workload(3, order=2)
+    assert make_plan(w, anchor=bsf.BSF_ANCHOR_AUTO).geometry.global_mode == 0
+    w2 = synth.workload(2)  # float input: never global mode
+    assert make_plan(w2, anchor=bsf.BSF_ANCHOR_AUTO).geometry.global_mode == 0

@@ -18,6 +18,8 @@ ap.add_argument("--width", type=int, default=512)
 ap.add_argument("--height", type=int, default=512)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--split", type=int, default=0, help="bsf_run_split with this many passes (order from --order)")
+ap.add_argument("--anchor", default="tile", choices=["tile", "global", "auto"])
+ap.add_argument("--opt", action="append", default=[], help="bsf_debug_option name=value (diagnostics)")
 args = ap.parse_args()
 kw = {"width": args.width, "height": args.height}
 if args.order:
@@ -25,7 +27,11 @@ if args.order:
 w = synth.workload(args.config, **kw)
 dev = torch.device("cuda:0")
 plan = bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" else bsf.BSF_F32, order=w.order,
-                basis=w.basis, max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_TILE)
+                basis=w.basis, max_sigma=w.max_sigma,
+                anchor={"tile": bsf.BSF_ANCHOR_TILE, "global": bsf.BSF_ANCHOR_GLOBAL, "auto": bsf.BSF_ANCHOR_AUTO}[args.anchor])
+for o in args.opt:
+    k, v = o.split("=")
+    plan.debug_option(k, float(v))
 img = synth.make_image(w, device=dev).contiguous()
 cov = synth.make_cov(w, device=dev).contiguous()
 out = torch.empty((1, w.height, w.width), dtype=torch.float64, device=dev)
@@ -42,5 +48,6 @@ torch.cuda.synchronize()
 ms = a.elapsed_time(b) / args.reps
 st = plan.stats(reset=True)
 npx = w.width * w.height
-print("%s %dx%d r=%d%s: %.3f ms, %.3f Mpx/s, macs/px %.0f, dd fallback %d" % (
-    w.name, w.width, w.height, w.order, " split n=%d" % args.split if args.split else "", ms, npx / ms / 1e3, st["macs"] / max(st["pixels"], 1), st["double_double"]))
+print("%s %dx%d r=%d%s %s(global_mode=%d): %.3f ms, %.3f Mpx/s, macs/px %.0f, dd fallback %d" % (
+    w.name, w.width, w.height, w.order, " split n=%d" % args.split if args.split else "", args.anchor,
+    plan.geometry.global_mode, ms, npx / ms / 1e3, st["macs"] / max(st["pixels"], 1), st["double_double"]))

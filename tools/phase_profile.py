@@ -13,16 +13,18 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_1109_5114_b200 import bsf  # noqa: E402
 
-PHASES = ["scales (reach)", "preint: zero pads", "exact split", "scatter", "gather", "accumulate"]
+PHASES = ["scales (reach)", "preint: zero pads", "exact split (global: setup)", "scatter", "gather", "accumulate"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--order", type=int, default=0)
+ap.add_argument("--anchor", default="tile", choices=["tile", "global", "auto"])
 args = ap.parse_args()
 w = synth.workload(args.config, order=args.order) if args.order else synth.workload(args.config)
 dev = torch.device("cuda:0")
 plan = bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" else bsf.BSF_F32, order=w.order,
-                basis=w.basis, max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_TILE)
+                basis=w.basis, max_sigma=w.max_sigma,
+                anchor={"tile": bsf.BSF_ANCHOR_TILE, "global": bsf.BSF_ANCHOR_GLOBAL, "auto": bsf.BSF_ANCHOR_AUTO}[args.anchor])
 img = synth.make_image(w, device=dev).contiguous()
 cov = synth.make_cov(w, device=dev).contiguous()
 out = torch.empty((1, w.height, w.width), dtype=torch.float64, device=dev)
