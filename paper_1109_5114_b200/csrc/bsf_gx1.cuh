@@ -90,14 +90,14 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
             }
         }
     }
-    // E_mu = 2^42 acc2 + 2^21 acc1 + acc0 as a normalised double-double
-    // (each term exact in fp64; the first TwoSum is exact, the second rounds
-    // only below 2^-104 |E|)
+    // E_mu = 2^21 (2^21 acc2 + acc1) + acc0 as an exact double-double: the
+    // bracket is an integer below 2^53 (exact in fp64, times 2^21 exact), and
+    // TwoSum is error-free
     dd E[NMON];
 #pragma unroll
     for (int m = 0; m < NMON; ++m) {
-        const dd t = two_sum((double)acc[2][m] * 0x1p42, (double)acc[1][m] * 0x1p21);
-        E[m] = dd_add_d(t, (double)acc[0][m]);
+        const long long hi = ((long long)acc[2][m] << 21) + acc[1][m];
+        E[m] = two_sum((double)hi * 0x1p21, (double)acc[0][m]);
     }
     // Horner: rows i (x power) in phi_y, then phi_x; monomial order (i, j):
     // i = deg..0, j = deg - i..0 (lut/gen_lut.py)
@@ -233,92 +233,156 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
     const int ntx = (a.W + GX1_TW - 1) / GX1_TW, nty = (a.H + GX1_TH - 1) / GX1_TH;
     const long long nunits = a.pts ? ((long long)a.npts + GX1_BLOCK - 1) / GX1_BLOCK : (long long)ntx * nty * a.nimg;
     unsigned long long macs = 0;
+    // per tile: phase A solves every pixel's scales (a1-a4); the pixels are
+    // then ordered by class (basis, zero-scale variant; dead pixels last) with
+    // a counting sort, so that in phase B a warp mostly runs ONE tap program
+    // (same tap count, same tables) -- lanes of mixed classes would execute
+    // both programs one after the other
+    constexpr int NCLS = 2 * NVAR + 1;
+    __shared__ double s_ap[GX1_BLOCK][4];
+    __shared__ int s_info[GX1_BLOCK];  // basis | (drop + 1) << 1 | clamped << 4 | valid << 5 | flags << 8
+    __shared__ short s_order[GX1_BLOCK];
+    __shared__ int s_wcnt[GX1_BLOCK / 32][NCLS];
+    const int lane = tid & 31, warp = tid >> 5;
     // static grid-stride over 32 x 8 pixel tiles in raster order: the blocks of
     // a wave read neighbouring rows of the running sums (L2 reuse of the taps)
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
-        int img, x, y;
-        long long oidx;
-        bool valid;
-        if (a.pts) {
-            const long long i = u * GX1_BLOCK + tid;
-            valid = i < a.npts;
-            img = valid ? a.pts[3 * i] : 0;
-            x = valid ? a.pts[3 * i + 1] : 0;
-            y = valid ? a.pts[3 * i + 2] : 0;
-            oidx = i;
-        } else {
-            img = (int)(u / ((long long)ntx * nty));
-            const int rem = (int)(u % ((long long)ntx * nty));
-            x = (rem % ntx) * GX1_TW + tid % GX1_TW;
-            y = (rem / ntx) * GX1_TH + tid / GX1_TW;
-            valid = x < a.W && y < a.H;
-            oidx = (long long)img * ipl + (size_t)y * a.W + x;
-        }
-        PixelScales ps;
-        ps.flags = 0;
-        ps.basis = 0;
-        ps.drop = -1;
-        ps.clamped = 0;
-        if (valid) {
-            double sx, sy, th;
-            load_cov(a, img, x, y, sx, sy, th);
-            pixel_scales(sx, sy, th, a.policy, a.clamp, 1, ps);
-        }
-        int flags = ps.flags;
-        const bool live = valid && !(flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
-        double res = __longlong_as_double(0x7ff8000000000000LL), erel = 0.0;
-        bool used_dd = false;
-        if (live) {
-            // every read stays inside the domain (plus the zero rows above it)
-            // when the pixel's reach is within the plan's margins; else NaN and
-            // BSF_ERANGE (a covariance above the plan's max_sigma)
-            double rx = 0.0, ry = 0.0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                rx += ps.ap[k] * abs(c_steps[ps.basis][k][0]);
-                ry += ps.ap[k] * c_steps[ps.basis][k][1];
-            }
-            const int ex = (int)ceil(0.5 * rx) + 1, ey = (int)ceil(0.5 * ry) + 1;
-            const int4 E = S.ext[ps.basis];
-            const bool in = x + a.gP - ex + E.x - 2 >= 0 && x + a.gP + ex + E.y + 2 < a.gGW &&
-                            y - ey + E.z - 2 >= -a.gPadT && y + ey + E.w < a.gGH;
-            if (!in) {
-                flags |= FLAG_RANGE;
+        const int img_t = a.pts ? 0 : (int)(u / ((long long)ntx * nty));
+        const int rem_t = a.pts ? 0 : (int)(u % ((long long)ntx * nty));
+        const int x0 = (rem_t % ntx) * GX1_TW, y0 = (rem_t / ntx) * GX1_TH;
+        // ---- phase A: this thread's pixel of the tile
+        int cls;
+        {
+            int img, x, y;
+            bool valid;
+            if (a.pts) {
+                const long long i = u * GX1_BLOCK + tid;
+                valid = i < a.npts;
+                img = valid ? a.pts[3 * i] : 0;
+                x = valid ? a.pts[3 * i + 1] : 0;
+                y = valid ? a.pts[3 * i + 2] : 0;
             } else {
-                const long long *G = a.gglob[ps.basis] + (size_t)img * (a.gGH + a.gPadT) * a.gGW;
-                res = ps.drop < 0 ? gx1_mesh<6>(S, G, a.gGW, a.gP, ps, x, y, erel, macs)
-                                  : gx1_mesh<3>(S, G, a.gGW, a.gP, ps, x, y, erel, macs);
-                if (!(erel <= a.split_tol)) {  // NaN-safe: the double-double mesh on the same sums
-                    res = gx1_fallback(G, a.gP, a.gGW, a.gGH, luts[ps.basis], ps, x, y, &flags);
-                    used_dd = true;
+                img = img_t;
+                x = x0 + tid % GX1_TW;
+                y = y0 + tid / GX1_TW;
+                valid = x < a.W && y < a.H;
+            }
+            PixelScales ps;
+            ps.flags = 0;
+            ps.basis = 0;
+            ps.drop = -1;
+            ps.clamped = 0;
+            ps.ap[0] = ps.ap[1] = ps.ap[2] = ps.ap[3] = 0.0;
+            if (valid) {
+                double sx, sy, th;
+                load_cov(a, img, x, y, sx, sy, th);
+                pixel_scales(sx, sy, th, a.policy, a.clamp, 1, ps);
+            }
+            const bool live = valid && !(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s_ap[tid][k] = ps.ap[k];
+            s_info[tid] = ps.basis | ((ps.drop + 1) << 1) | (ps.clamped << 4) | (valid ? 32 : 0) | (ps.flags << 8);
+            cls = live ? ps.basis * NVAR + ps.drop + 1 : NCLS - 1;
+        }
+        // counting sort by class: per-warp class counts, then every thread
+        // computes its slot from the counts of the classes before its own and
+        // of the same class in earlier warps (stable)
+        const unsigned m = __match_any_sync(0xffffffffu, cls);
+        if (lane < NCLS) s_wcnt[warp][lane] = 0;
+        __syncwarp();
+        if (lane == __ffs(m) - 1) s_wcnt[warp][cls] = __popc(m);
+        __syncthreads();
+        {
+            int pos = __popc(m & ((1u << lane) - 1u));
+            for (int w = 0; w < GX1_BLOCK / 32; ++w)
+                for (int c = 0; c < NCLS; ++c)
+                    pos += (c < cls || (c == cls && w < warp)) ? s_wcnt[w][c] : 0;
+            s_order[pos] = (short)tid;
+        }
+        __syncthreads();
+        // ---- phase B: pixel p = s_order[tid] (class-sorted)
+        {
+            const int p = s_order[tid];
+            const int w = s_info[p];
+            const bool valid = (w >> 5) & 1;
+            PixelScales ps;
+            ps.basis = w & 1;
+            ps.drop = ((w >> 1) & 7) - 1;
+            ps.clamped = (w >> 4) & 1;
+            ps.flags = w >> 8;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ps.ap[k] = s_ap[p][k];
+            int img, x, y;
+            long long oidx;
+            if (a.pts) {
+                const long long i = u * GX1_BLOCK + p;
+                img = valid ? a.pts[3 * i] : 0;
+                x = valid ? a.pts[3 * i + 1] : 0;
+                y = valid ? a.pts[3 * i + 2] : 0;
+                oidx = i;
+            } else {
+                img = img_t;
+                x = x0 + p % GX1_TW;
+                y = y0 + p / GX1_TW;
+                oidx = (long long)img * ipl + (size_t)y * a.W + x;
+            }
+            int flags = ps.flags;
+            const bool live = valid && !(flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
+            double res = __longlong_as_double(0x7ff8000000000000LL), erel = 0.0;
+            bool used_dd = false;
+            if (live) {
+                // every read stays inside the domain (plus the zero rows above
+                // it) when the pixel's reach is within the plan's margins; else
+                // NaN and BSF_ERANGE (a covariance above the plan's max_sigma)
+                double rx = 0.0, ry = 0.0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    rx += ps.ap[k] * abs(c_steps[ps.basis][k][0]);
+                    ry += ps.ap[k] * c_steps[ps.basis][k][1];
+                }
+                const int ex = (int)ceil(0.5 * rx) + 1, ey = (int)ceil(0.5 * ry) + 1;
+                const int4 E = S.ext[ps.basis];
+                const bool in = x + a.gP - ex + E.x - 2 >= 0 && x + a.gP + ex + E.y + 2 < a.gGW &&
+                                y - ey + E.z - 2 >= -a.gPadT && y + ey + E.w < a.gGH;
+                if (!in) {
+                    flags |= FLAG_RANGE;
+                } else {
+                    const long long *G = a.gglob[ps.basis] + (size_t)img * (a.gGH + a.gPadT) * a.gGW;
+                    res = ps.drop < 0 ? gx1_mesh<6>(S, G, a.gGW, a.gP, ps, x, y, erel, macs)
+                                      : gx1_mesh<3>(S, G, a.gGW, a.gP, ps, x, y, erel, macs);
+                    if (!(erel <= a.split_tol)) {  // NaN-safe: the double-double mesh on the same sums
+                        res = gx1_fallback(G, a.gP, a.gGW, a.gGH, luts[ps.basis], ps, x, y, &flags);
+                        used_dd = true;
+                    }
                 }
             }
-        }
-        if (valid) {
-            if (a.aux) {
-                double *ax = a.aux + BSF_AUX * oidx;
-                ax[0] = ps.basis;
-                ax[1] = ps.drop;
-                ax[2] = ps.clamped;
-                ax[3] = flags;
-                for (int k = 0; k < 4; ++k) ax[4 + k] = ps.ap[k];
-                ax[8] = used_dd;
-                ax[9] = erel;
-                ax[10] = ax[11] = 0.0;
+            if (valid) {
+                if (a.aux) {
+                    double *ax = a.aux + BSF_AUX * oidx;
+                    ax[0] = ps.basis;
+                    ax[1] = ps.drop;
+                    ax[2] = ps.clamped;
+                    ax[3] = flags;
+                    for (int k = 0; k < 4; ++k) ax[4 + k] = ps.ap[k];
+                    ax[8] = used_dd;
+                    ax[9] = erel;
+                    ax[10] = ax[11] = 0.0;
+                }
+                if (a.out_f32 && !a.pts)
+                    ((float *)a.out)[oidx] = (float)res;
+                else
+                    ((double *)a.out)[oidx] = res;
             }
-            if (a.out_f32 && !a.pts)
-                ((float *)a.out)[oidx] = (float)res;
-            else
-                ((double *)a.out)[oidx] = res;
+            if (a.stats) {
+                warp_count(a.stats + 0, valid);
+                warp_count(a.stats + 1, valid && ps.clamped);
+                warp_count(a.stats + 2, valid && ps.drop >= 0);
+                warp_count(a.stats + 3, valid && ps.basis == BASIS_THETA_PRIME);
+                warp_count(a.stats + 5, used_dd);
+                if (valid && flags) atomicOr(a.stats + 4, (unsigned long long)flags);
+            }
         }
-        if (a.stats) {
-            warp_count(a.stats + 0, valid);
-            warp_count(a.stats + 1, valid && ps.clamped);
-            warp_count(a.stats + 2, valid && ps.drop >= 0);
-            warp_count(a.stats + 3, valid && ps.basis == BASIS_THETA_PRIME);
-            warp_count(a.stats + 5, used_dd);
-            if (valid && flags) atomicOr(a.stats + 4, (unsigned long long)flags);
-        }
+        __syncthreads();  // s_ap / s_info / s_order are rewritten by the next tile
     }
     if (a.stats) {
         for (int o = 16; o; o >>= 1) macs += __shfl_xor_sync(0xffffffffu, macs, o);
