@@ -91,8 +91,15 @@ typedef enum {
                                /* fused path only (BSF_ANCHOR_TILE, order <= 3)                   */
 } bsf_boundary;
 
+typedef enum {
+    BSF_COV_SIGMA_THETA = 0, /* planes (sigma_x, sigma_y, theta): C = R(theta) diag(sx^2, sy^2) R(theta)^T,
+                              * theta the angle of the sigma_x axis from the x axis (R14) */
+    BSF_COV_C11_C12_C22 = 1  /* planes (C11, C12, C22) of the target covariance;
+                              * decoded in fp64 to the same (sigma_x >= sigma_y, theta) form     */
+} bsf_cov_layout;
+
 typedef struct {
-    int width, height;   /* image size W, H (pixels)                                          */
+    int width, height;   /* image size W, H (pixels); with nranks > 1 the WHOLE image's size   */
     int batch;           /* number of covariance fields (independent images / frames)         */
     int channels;        /* images per covariance field (e.g. 3 for RGB); image b*C+c uses    */
                          /* covariance field b                                                */
@@ -115,6 +122,30 @@ typedef struct {
                           * fewer than 148 32x32 tiles, 64 at order 1 with a large reach, else
                           * 32), or 16 / 32 / 64.  Row strips that must reproduce a one-GPU
                           * run bit for bit pass the full image's geometry.super_tile      */
+    bsf_cov_layout cov_layout; /* meaning of the three covariance planes                      */
+    /* Multi-GPU: one image sharded by row strips over nranks
+     * processes, one GPU each.  nranks = 1: single GPU (rank, nccl_id unused).
+     * nranks > 1: the plan covers this rank's strip (bsf_strip_rows; rows given
+     * by geometry.row0 / row_count), and
+     *  - bsf_run (tile path) filters the strip: it needs the input rows within
+     *    geometry.halo of the strip, which the library exchanges with the
+     *    neighbouring ranks (ncclSend / ncclRecv on the call's stream) when the
+     *    plan has a communicator (nccl_id != NULL); f_dev then holds the
+     *    strip's own rows [row0, row0 + row_count).  Without a communicator
+     *    (nccl_id == NULL: the caller assembles the halo, e.g. through
+     *    torch.distributed) f_dev holds the block rows [block_row0,
+     *    block_row0 + block_rows).  cov_dev and out_dev always hold the strip's
+     *    own rows.  Only the own rows are computed; the result is bit-identical
+     *    to a one-GPU run (same anchoring super-tiles).
+     *  - bsf_preintegrate_exact computes the strip's rows of the paper's single
+     *    global pre-integration (GLOBAL mode): domain rows [g_row0, g_row0 +
+     *    g_rows) (the last rank also holds the bottom margin), scan carries
+     *    passed down the rank chain after every level with a vertical step
+     *    (needs the communicator); bit-identical to the one-GPU sums.
+     * Plans with nranks > 1 are created collectively (ncclCommInitRank). */
+    int rank, nranks;
+    const void *nccl_id; /* 128-byte unique id from bsf_get_unique_id on rank 0, the same bytes on
+                          * every rank (broadcast by the caller); NULL: no communicator      */
 } bsf_plan_desc;
 
 typedef struct {
@@ -128,7 +159,27 @@ typedef struct {
                               * one-GPU run align to it and use it in their plans           */
     int global_mode;         /* 1: bsf_run gathers from exact int64 global sums (BSF_ANCHOR_GLOBAL /
                               * BSF_ANCHOR_AUTO, u8 input, order 1, sums below 2^62)        */
+    int tile_unit;           /* side of the tiles bsf_run_tiles indexes (the anchoring unit of the tile
+                              * path: super_tile, or 16 for the double-double tile kernel); 0 in
+                              * global mode                                                 */
+    /* row strips (nranks > 1; else the whole image): */
+    int row0, row_count;     /* the image rows this rank filters                              */
+    int block_row0, block_rows; /* the input rows the filter reads (own rows + halo)          */
+    int halo;                /* halo rows (a multiple of super_tile)                          */
+    int g_row0, g_rows;      /* GLOBAL mode: this rank's domain rows of the global sums       */
 } bsf_geometry;
+
+/* Partition of H image rows into nranks row strips aligned to `unit` rows
+ * (super-tiles; the strips hold whole units, balanced, in rank order) and the
+ * block of input rows a strip's filter reads, [b0, b1) = [max(0, y0 - halo),
+ * min(H, y1 + halo)).  Pure host arithmetic (no device needed).  BSF_EINVAL
+ * for a bad argument or a strip shorter than the halo (the halo would then
+ * span two neighbours).                                                      */
+bsf_status bsf_strip_rows(int height, int unit, int halo, int rank, int nranks, int *y0, int *y1, int *b0, int *b1);
+
+/* NCCL unique id for a multi-GPU plan (call on rank 0, broadcast the 128
+ * bytes to every rank).  BSF_ENCCL when NCCL cannot be loaded.               */
+bsf_status bsf_get_unique_id(void *id_out128);
 
 typedef struct {
     long long pixels;        /* pixels filtered since the last reset                          */
@@ -195,6 +246,15 @@ bsf_status bsf_scan_level(bsf_plan_t plan, int slot, int level, int exact, const
  *   out_dev: [batch*channels][H][W] of out_dtype.                            */
 bsf_status bsf_filter(bsf_plan_t plan, const void *g_dev, const void *cov_dev, void *out_dev, void *stream);
 
+/* Global mode (geometry.global_mode = 1): the local finite difference read
+ * from the exact int64 sums of bsf_preintegrate_exact (the paper's Alg. 3
+ * step 3 on its single global pre-integration), with an
+ * exact integer contraction of Eq. (11).  g_dev as written
+ * by bsf_preintegrate_exact; cov_dev, out_dev as bsf_filter.
+ * bsf_preintegrate_exact + bsf_filter_exact = bsf_run of a global-mode plan.
+ * BSF_EUNSUPPORTED when the plan is not in global mode.                     */
+bsf_status bsf_filter_exact(bsf_plan_t plan, const void *g_dev, const void *cov_dev, void *out_dev, void *stream);
+
 /* Same computation for an explicit pixel list (parity at full size):
  *   pts_dev: int32 triples (image, x, y) * npts;  out_dev: float64[npts].    */
 bsf_status bsf_filter_points(bsf_plan_t plan, const void *g_dev, const void *cov_dev, const int *pts_dev,
@@ -221,6 +281,16 @@ bsf_status bsf_run_points(bsf_plan_t plan, const void *f_dev, const void *cov_de
  * the plan's own g workspace; BSF_ANCHOR_TILE = the fused tile kernel (no
  * global g).                                                                 */
 bsf_status bsf_run(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, void *stream);
+
+/* The tile path on a subset of the image: only the listed anchoring tiles
+ * (side geometry.tile_unit; index (image * ty_count + ty) * tx_count + tx,
+ * tx_count = ceil(W / tile_unit), ty_count = ceil(H / tile_unit)) are
+ * filtered, every one exactly as bsf_run computes it (same kernel, same
+ * anchoring); other outputs are left untouched (region-of-interest
+ * filtering; the bench times order 4 this way).  tiles_dev: int32[ntiles].
+ * BSF_EUNSUPPORTED for global-mode plans.                                    */
+bsf_status bsf_run_tiles(bsf_plan_t plan, const void *f_dev, const void *cov_dev, void *out_dev, const int *tiles_dev,
+                         int ntiles, void *stream);
 
 /* Algorithm 1 ("better accuracy"): covariance splitting
  * C = sigma_b^2 I + Delta C (Eq. (7)).  Per covariance field b,

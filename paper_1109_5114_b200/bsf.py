@@ -29,6 +29,7 @@ class BsfError(RuntimeError):
 
 
 BSF_BOUNDARY_ZERO, BSF_BOUNDARY_REPLICATE = 0, 1
+BSF_COV_SIGMA_THETA, BSF_COV_C11_C12_C22 = 0, 1
 
 
 class bsf_plan_desc(ctypes.Structure):
@@ -37,14 +38,17 @@ class bsf_plan_desc(ctypes.Structure):
                 ("order", ctypes.c_int), ("basis", ctypes.c_int), ("max_sigma", ctypes.c_float),
                 ("margin_x", ctypes.c_int), ("margin_y", ctypes.c_int), ("clamp", ctypes.c_int),
                 ("precision", ctypes.c_int), ("device", ctypes.c_int), ("anchor", ctypes.c_int),
-                ("boundary", ctypes.c_int), ("super_tile", ctypes.c_int)]
+                ("boundary", ctypes.c_int), ("super_tile", ctypes.c_int), ("cov_layout", ctypes.c_int),
+                ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p)]
 
 
 class bsf_geometry(ctypes.Structure):
     _fields_ = [("margin_x", ctypes.c_int), ("margin_y", ctypes.c_int), ("g_width", ctypes.c_int),
                 ("g_height", ctypes.c_int), ("nbases", ctypes.c_int), ("g_bytes", ctypes.c_size_t),
                 ("g_exact_bytes", ctypes.c_size_t), ("super_tile", ctypes.c_int),
-                ("global_mode", ctypes.c_int)]
+                ("global_mode", ctypes.c_int), ("tile_unit", ctypes.c_int), ("row0", ctypes.c_int),
+                ("row_count", ctypes.c_int), ("block_row0", ctypes.c_int), ("block_rows", ctypes.c_int),
+                ("halo", ctypes.c_int), ("g_row0", ctypes.c_int), ("g_rows", ctypes.c_int)]
 
 
 class bsf_stats(ctypes.Structure):
@@ -77,6 +81,8 @@ def lib():
         L.bsf_scan_step.argtypes = [vp, i, i, ctypes.POINTER(i), ctypes.POINTER(i)]
         L.bsf_scan_level.restype = st
         L.bsf_scan_level.argtypes = [vp, i, i, i, vp, vp, vp, vp]
+        L.bsf_filter_exact.restype = st
+        L.bsf_filter_exact.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_filter.restype = st
         L.bsf_filter.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_filter_points.restype = st
@@ -85,6 +91,8 @@ def lib():
         L.bsf_filter_points_aux.argtypes = [vp, vp, vp, vp, i, vp, vp, vp]
         L.bsf_run_points.restype = st
         L.bsf_run_points.argtypes = [vp, vp, vp, vp, i, vp, vp, vp]
+        L.bsf_run_tiles.restype = st
+        L.bsf_run_tiles.argtypes = [vp, vp, vp, vp, vp, i, vp]
         L.bsf_run.restype = st
         L.bsf_run.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_run_normalized.restype = st
@@ -112,6 +120,10 @@ def lib():
         L.bsf_last_error.restype = ctypes.c_char_p
         L.bsf_last_error.argtypes = []
         L.bsf_version.restype = i
+        L.bsf_strip_rows.restype = st
+        L.bsf_strip_rows.argtypes = [i, i, i, i, i] + [ctypes.POINTER(i)] * 4
+        L.bsf_get_unique_id.restype = st
+        L.bsf_get_unique_id.argtypes = [vp]
         _lib = L
     return _lib
 
@@ -167,10 +179,13 @@ class Plan:
 
     def __init__(self, width, height, *, batch=1, channels=1, in_dtype=BSF_F32, out_dtype=BSF_F64, order=1,
                  basis=BSF_DUAL, max_sigma=1.0, margin_x=0, margin_y=0, clamp=1, precision=BSF_PREC_DD,
-                 device=0, anchor=BSF_ANCHOR_GLOBAL, boundary=0, super_tile=0, lut_dir=LUT_DIR):
+                 device=0, anchor=BSF_ANCHOR_GLOBAL, boundary=0, super_tile=0, cov_layout=BSF_COV_SIGMA_THETA,
+                 rank=0, nranks=1, nccl_id=None, lut_dir=LUT_DIR):
+        self._id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         self.desc = bsf_plan_desc(width, height, batch, channels, in_dtype, out_dtype, order, basis,
                                   float(max_sigma), margin_x, margin_y, clamp, precision, device, anchor, boundary,
-                                  super_tile)
+                                  super_tile, cov_layout, rank, nranks,
+                                  ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None)
         h = ctypes.c_void_p()
         _check(lib().bsf_plan_create(ctypes.byref(self.desc), lut_dir.encode(), ctypes.byref(h)))
         self.handle = h
@@ -202,17 +217,24 @@ class Plan:
             g.nbases, self.desc.batch * self.desc.channels, g.g_height, g.g_width)
 
     # --- argument checks (the C ABI takes raw pointers) ------------------------
+    def _rows(self):  # rows of cov / out (a row strip's own rows for multi-GPU plans)
+        return self.geometry.row_count if self.desc.nranks > 1 else self.desc.height
+
     def _npix(self):
         d = self.desc
-        return d.batch * d.channels * d.height * d.width
+        return d.batch * d.channels * self._rows() * d.width
 
     def _check_f(self, f, device=None):
-        _want(f, "f", [_IN_TORCH[self.desc.in_dtype]], self._npix(),
-              self.desc.device if device is None else device)
+        d = self.desc
+        rows = self._rows()
+        if d.nranks > 1 and not d.nccl_id:
+            rows = self.geometry.block_rows  # the caller assembled the block (own rows + halo)
+        _want(f, "f", [_IN_TORCH[d.in_dtype]], d.batch * d.channels * rows * d.width,
+              d.device if device is None else device)
 
     def _check_cov(self, cov, device=None):
         d = self.desc
-        _want(cov, "cov", ["float32"], d.batch * 3 * d.height * d.width, d.device if device is None else device)
+        _want(cov, "cov", ["float32"], d.batch * 3 * self._rows() * d.width, d.device if device is None else device)
 
     def _check_out(self, out, device=None):
         _want(out, "out", [_OUT_TORCH[self.desc.out_dtype]], self._npix(),
@@ -247,6 +269,13 @@ class Plan:
         self._check_out(out)
         _check(lib().bsf_filter(self.handle, _ptr(g), _ptr(cov), _ptr(out), _stream(stream)))
 
+    def filter_exact(self, g, cov, out, stream=None):
+        """bsf_filter_exact: global-mode gather from bsf_preintegrate_exact's sums."""
+        _want(g, "g", ["int64"], self.geometry.g_exact_bytes // 8, self.desc.device)
+        self._check_cov(cov)
+        self._check_out(out)
+        _check(lib().bsf_filter_exact(self.handle, _ptr(g), _ptr(cov), _ptr(out), _stream(stream)))
+
     def _check_pts(self, pts, out, aux=None):
         n = pts.numel() // 3
         _want(pts, "pts", ["int32"], 3 * n, self.desc.device)
@@ -280,6 +309,15 @@ class Plan:
         self._check_cov(cov)
         self._check_out(out)
         _check(lib().bsf_run(self.handle, _ptr(f), _ptr(cov), _ptr(out), _stream(stream)))
+
+    def run_tiles(self, f, cov, out, tiles, stream=None):
+        """bsf_run_tiles: filter only the listed anchoring tiles (int32 indices)."""
+        self._check_f(f)
+        self._check_cov(cov)
+        self._check_out(out)
+        _want(tiles, "tiles", ["int32"], tiles.numel(), self.desc.device)
+        _check(lib().bsf_run_tiles(self.handle, _ptr(f), _ptr(cov), _ptr(out), _ptr(tiles), int(tiles.numel()),
+                                   _stream(stream)))
 
     def run_normalized(self, f, cov, out, stream=None):
         """DC-renormalised filter: out / filter(image indicator)."""
@@ -351,6 +389,20 @@ class Plan:
 
     def launch_count(self):
         return lib().bsf_launch_count(self.handle)
+
+
+def strip_rows(height, unit, halo, rank, nranks):
+    """bsf_strip_rows: (y0, y1, b0, b1) of a row strip (pure host arithmetic)."""
+    v = [ctypes.c_int() for _ in range(4)]
+    _check(lib().bsf_strip_rows(int(height), int(unit), int(halo), int(rank), int(nranks), *[ctypes.byref(x) for x in v]))
+    return tuple(x.value for x in v)
+
+
+def get_unique_id() -> bytes:
+    """bsf_get_unique_id: the 128-byte NCCL id (rank 0), to broadcast to all ranks."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().bsf_get_unique_id(buf))
+    return buf.raw
 
 
 # C-ABI names, re-exported (the binding keeps the library's vocabulary)

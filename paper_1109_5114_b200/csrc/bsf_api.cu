@@ -9,9 +9,53 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is loaded at run time (dlopen), no link dependency
+
+#include <mutex>
+
 #include "bsf_internal.h"
 
 using namespace bsf;
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded on first use: the process' libnccl.so.2 (the one PyTorch
+// already loaded when present, else the system's).  Used for the row-strip
+// halo exchange and the GLOBAL-mode scan carries of multi-GPU plans.
+// ---------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+    bool ok = false;
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclGetErrorString) errStr = nullptr;
+};
+NcclApi &nccl_api() {
+    static NcclApi n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        n.getUniqueId = (decltype(n.getUniqueId))dlsym(h, "ncclGetUniqueId");
+        n.commInitRank = (decltype(n.commInitRank))dlsym(h, "ncclCommInitRank");
+        n.commDestroy = (decltype(n.commDestroy))dlsym(h, "ncclCommDestroy");
+        n.send = (decltype(n.send))dlsym(h, "ncclSend");
+        n.recv = (decltype(n.recv))dlsym(h, "ncclRecv");
+        n.groupStart = (decltype(n.groupStart))dlsym(h, "ncclGroupStart");
+        n.groupEnd = (decltype(n.groupEnd))dlsym(h, "ncclGroupEnd");
+        n.errStr = (decltype(n.errStr))dlsym(h, "ncclGetErrorString");
+        n.ok = n.getUniqueId && n.commInitRank && n.commDestroy && n.send && n.recv && n.groupStart && n.groupEnd &&
+               n.errStr;
+    });
+    return n;
+}
+}  // namespace
 
 static thread_local std::string g_last_error;
 
@@ -19,6 +63,13 @@ static bsf_status set_err(bsf_status s, const std::string &msg) {
     g_last_error = msg;
     return s;
 }
+
+#define NCCL_TRY(expr)                                                                        \
+    do {                                                                                      \
+        ncclResult_t r_ = (expr);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return set_err(BSF_ENCCL, std::string(#expr ": ") + nccl_api().errStr(r_));      \
+    } while (0)
 
 #define CUDA_TRY(expr)                                                                        \
     do {                                                                                      \
@@ -66,6 +117,12 @@ struct bsf_plan_s {
     int gshift[2] = {0, 0};              // limb split G = 2^k G1 + G0 per basis
     int stile_global = 32;
     long long *gx_ws = nullptr;          // [nbases][nimg][GH][GW] int64
+    // row strips (nranks > 1): own rows [y0, y1), block [b0, b1), halo; GLOBAL-mode
+    // strip: image rows [gy0, gy1), domain rows [gy0, gy0 + g_rows)
+    int y0 = 0, y1 = 0, b0 = 0, b1 = 0, halo = 0, gy0 = 0, gy1 = 0, g_rows = 0;
+    ncclComm_t comm = nullptr;
+    void *f_blk = nullptr;                // block image (library halo exchange)
+    unsigned long long *carry = nullptr;  // scan carries [nimg][2][GW]
     // diagnostics options (bsf_debug_option); the defaults are the product path
     bool opt_fused = true;
     bool opt_order = true;
@@ -87,6 +144,7 @@ struct DevGuard {
 };
 
 static bool global_exact(const bsf_plan_s *p);
+static bool use_fused(const bsf_plan_s *p);
 static size_t g_bytes(const bsf_plan_s *p) {
     return (size_t)p->geo.nbases * p->geo.nimg * p->geo.GH * p->geo.GW * sizeof(double2);
 }
@@ -399,6 +457,9 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
         return set_err(BSF_EINVAL, "bad boundary");
     if (d.super_tile != 0 && d.super_tile != 16 && d.super_tile != 32 && d.super_tile != 64)
         return set_err(BSF_EINVAL, "super_tile must be 0, 16, 32 or 64");
+    if (d.cov_layout != BSF_COV_SIGMA_THETA && d.cov_layout != BSF_COV_C11_C12_C22)
+        return set_err(BSF_EINVAL, "bad cov_layout");
+    if (d.nranks < 1 || d.rank < 0 || d.rank >= d.nranks) return set_err(BSF_EINVAL, "bad rank / nranks");
     int disp = required_disp(d.max_sigma, d.order);
     int needP = disp + 3 * d.order + 2, needPb = disp + 2;
     if ((d.margin_x && d.margin_x < needP) || (d.margin_y > 0 && d.margin_y < needPb))
@@ -503,13 +564,84 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
         }
         p->global_ok = ok && slots <= GX1_SLOTS_H;
     }
+    // row strips: own rows aligned to the super-tile, a halo
+    // covering a super-tile's halo domain (tap reach + interpolation window),
+    // and the GLOBAL-mode strip aligned to 32 rows (even: Theta' steps sy = 2)
+    if (d.nranks > 1) {
+        p->global_ok = false;  // global mode needs the whole image's sums on one GPU
+        const int disp = required_disp(d.max_sigma, d.order);
+        p->halo = p->stile * ((disp + 6 * d.order + 4 + p->stile - 1) / p->stile);
+        bsf_status s = bsf_strip_rows(d.height, p->stile, p->halo, d.rank, d.nranks, &p->y0, &p->y1, &p->b0, &p->b1);
+        if (s != BSF_OK) {
+            bsf_plan_destroy(p);
+            return s;
+        }
+        int gb0, gb1;
+        s = bsf_strip_rows(d.height, 32, 0, d.rank, d.nranks, &p->gy0, &p->gy1, &gb0, &gb1);
+        if (s != BSF_OK) {
+            bsf_plan_destroy(p);
+            return s;
+        }
+        p->g_rows = (p->gy1 - p->gy0) + (d.rank == d.nranks - 1 ? g.Pb : 0);
+        if (d.nccl_id) {
+            NcclApi &nc = nccl_api();
+            if (!nc.ok) {
+                bsf_plan_destroy(p);
+                return set_err(BSF_ENCCL, "libnccl.so.2 could not be loaded");
+            }
+            ncclUniqueId id;
+            memcpy(&id, d.nccl_id, sizeof id);
+            const ncclResult_t r = nc.commInitRank(&p->comm, d.nranks, id, d.rank);
+            if (r != ncclSuccess) {
+                p->comm = nullptr;
+                bsf_plan_destroy(p);
+                return set_err(BSF_ENCCL, std::string("ncclCommInitRank: ") + nc.errStr(r));
+            }
+        }
+    } else {
+        p->y0 = p->gy0 = 0;
+        p->y1 = p->gy1 = p->b1 = d.height;
+        p->g_rows = g.GH;
+    }
     *out = p;
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_strip_rows(int H, int unit, int halo, int rank, int nranks, int *y0, int *y1, int *b0,
+                                     int *b1) {
+    if (!y0 || !y1 || !b0 || !b1) return set_err(BSF_EINVAL, "null argument");
+    if (H < 1 || unit < 1 || halo < 0 || nranks < 1 || rank < 0 || rank >= nranks)
+        return set_err(BSF_EINVAL, "bad strip arguments");
+    const long long n = (H + unit - 1) / unit, base = n / nranks, extra = n % nranks;
+    const long long t0 = rank * base + std::min<long long>(rank, extra);
+    const long long t1 = t0 + base + (rank < extra ? 1 : 0);
+    *y0 = (int)std::min<long long>(H, t0 * unit);
+    *y1 = (int)std::min<long long>(H, t1 * unit);
+    *b0 = std::max(0, *y0 - halo);
+    *b1 = std::min(H, *y1 + halo);
+    if (*y1 <= *y0) return set_err(BSF_EINVAL, "empty row strip (more ranks than row units)");
+    // the neighbours' halos must come from this strip alone
+    // (rank - 1's bottom halo is my first rows, rank + 1's top halo my last rows)
+    if ((rank > 0 && *y1 - *y0 < std::min(halo, H - *y0)) || (rank < nranks - 1 && *y1 - *y0 < std::min(halo, *y1)))
+        return set_err(BSF_EINVAL, "row strip shorter than the halo (" + std::to_string(*y1 - *y0) + " < " +
+                                       std::to_string(halo) + " rows): use fewer ranks");
+    return BSF_OK;
+}
+
+extern "C" bsf_status bsf_get_unique_id(void *id_out) {
+    if (!id_out) return set_err(BSF_EINVAL, "null argument");
+    NcclApi &nc = nccl_api();
+    if (!nc.ok) return set_err(BSF_ENCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    NCCL_TRY(nc.getUniqueId(&id));
+    memcpy(id_out, &id, sizeof id);
     return BSF_OK;
 }
 
 extern "C" bsf_status bsf_plan_destroy(bsf_plan_t p) {
     if (!p) return BSF_OK;
     DevGuard guard(p->d.device);
+    if (p->comm) nccl_api().commDestroy(p->comm);
     for (void *q : p->dev_allocs) cudaFree(q);
     delete p;
     return BSF_OK;
@@ -526,12 +658,26 @@ extern "C" bsf_status bsf_plan_geometry(bsf_plan_t p, bsf_geometry *geom) {
     geom->g_exact_bytes = p->d.in_dtype == BSF_U8 ? g_bytes(p) / 2 : 0;
     geom->super_tile = p->stile;
     geom->global_mode = global_exact(p) ? 1 : 0;
+    geom->tile_unit = global_exact(p) ? 0 : (use_fused(p) ? p->stile : TILE);
+    geom->row0 = p->y0;
+    geom->row_count = p->y1 - p->y0;
+    geom->block_row0 = p->b0;
+    geom->block_rows = p->b1 - p->b0;
+    geom->halo = p->halo;
+    geom->g_row0 = p->gy0;
+    geom->g_rows = p->g_rows;
+    if (p->d.nranks > 1) {  // the strip's share of the GLOBAL-mode sums
+        geom->g_height = p->g_rows;
+        geom->g_bytes = (size_t)geom->nbases * p->geo.nimg * p->g_rows * p->geo.GW * sizeof(double2);
+        geom->g_exact_bytes = p->d.in_dtype == BSF_U8 ? geom->g_bytes / 2 : 0;
+    }
     return BSF_OK;
 }
 
 extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, void *stream) {
     if (!p || !f || !g) return set_err(BSF_EINVAL, "null argument");
     DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
     if (p->d.boundary != BSF_BOUNDARY_ZERO) return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only");
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
@@ -543,6 +689,55 @@ extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, voi
     return BSF_OK;
 }
 
+// GLOBAL mode over row strips (Alg. 3 step 2):
+// this rank holds image rows [gy0, gy1) and domain rows [gy0, gy0 + g_rows) of
+// the single global pre-integration.  Before every level with a vertical step
+// it receives the level's sums on the sy domain rows just above the strip
+// (the scan carry) from rank - 1, runs the level from them, and sends its own
+// last sy rows of the level to rank + 1.  The ranks form a chain (no cycle);
+// the result is the one-GPU bsf_preintegrate_exact, bit for bit.
+static bsf_status preintegrate_exact_strip(bsf_plan_s *p, const uint8_t *f, unsigned long long *g, cudaStream_t st) {
+    if (!p->comm) return set_err(BSF_EINVAL, "multi-GPU GLOBAL-mode pre-integration needs the plan's communicator");
+    NcclApi &nc = nccl_api();
+    Geometry gs = p->geo;
+    gs.H = p->gy1 - p->gy0;
+    gs.Pb = p->d.rank == p->d.nranks - 1 ? p->geo.Pb : 0;
+    gs.GH = gs.H + gs.Pb;
+    const size_t GW = gs.GW, nimg = gs.nimg, slot = nimg * gs.GH * GW;
+    if (!p->carry) {
+        void *q;
+        if (cudaMalloc(&q, nimg * 2 * GW * sizeof(unsigned long long)) != cudaSuccess)
+            return set_err(BSF_ENOMEM, "scan carry buffer");
+        p->dev_allocs.push_back(q);
+        p->carry = (unsigned long long *)q;
+    }
+    const bool first = p->d.rank == 0, last = p->d.rank == p->d.nranks - 1;
+    for (int sl = 0; sl < gs.nbases; ++sl) {
+        unsigned long long *gsl = g + sl * slot;
+        for (int lv = 0; lv < 4 * p->d.order; ++lv) {
+            int sx, sy;
+            scan_step(p->bases[sl], lv, &sx, &sy);
+            if (sy > 0 && !first) {
+                NCCL_TRY(nc.groupStart());
+                for (size_t i = 0; i < nimg; ++i)
+                    NCCL_TRY(nc.recv(p->carry + i * sy * GW, sy * GW, ncclUint64, p->d.rank - 1, p->comm, st));
+                NCCL_TRY(nc.groupEnd());
+            }
+            CUDA_TRY(launch_scan_level(f, 1, gsl, 1, gs, p->bases[sl], lv, (sy > 0 && !first) ? p->carry : nullptr,
+                                       st));
+            ++p->nlaunch;
+            if (sy > 0 && !last) {
+                NCCL_TRY(nc.groupStart());
+                for (size_t i = 0; i < nimg; ++i)
+                    NCCL_TRY(nc.send(gsl + (i * gs.GH + gs.GH - sy) * GW, sy * GW, ncclUint64, p->d.rank + 1, p->comm,
+                                     st));
+                NCCL_TRY(nc.groupEnd());
+            }
+        }
+    }
+    return BSF_OK;
+}
+
 extern "C" bsf_status bsf_preintegrate_exact(bsf_plan_t p, const void *f, void *g, void *stream) {
     if (!p || !f || !g) return set_err(BSF_EINVAL, "null argument");
     DevGuard guard(p->d.device);
@@ -551,6 +746,7 @@ extern "C" bsf_status bsf_preintegrate_exact(bsf_plan_t p, const void *f, void *
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
     unsigned long long *gd = (unsigned long long *)g;
+    if (p->d.nranks > 1) return preintegrate_exact_strip(p, (const uint8_t *)f, gd, st);
     size_t slot = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW;
     for (int s = 0; s < p->geo.nbases; ++s)
         CUDA_TRY(launch_preint_i64((const uint8_t *)f, gd + s * slot, p->geo, p->bases[s], p->d.order, st,
@@ -570,6 +766,7 @@ extern "C" bsf_status bsf_scan_level(bsf_plan_t p, int slot, int level, int exac
                                      const void *carry, void *stream) {
     if (!p || !g || (level == 0 && !f)) return set_err(BSF_EINVAL, "null argument");
     DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
     if (p->d.boundary != BSF_BOUNDARY_ZERO) return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only");
     if (slot < 0 || slot >= p->geo.nbases || level < 0 || level >= 4 * p->d.order)
         return set_err(BSF_EINVAL, "slot or level out of range");
@@ -595,12 +792,14 @@ static GatherArgs gather_args(bsf_plan_s *p, const void *g, const void *cov, voi
     a.cov = (const float *)cov;
     a.out = out;
     a.stats = p->stats;
+    a.cov_layout = p->d.cov_layout;
     return a;
 }
 
 extern "C" bsf_status bsf_filter(bsf_plan_t p, const void *g, const void *cov, void *out, void *stream) {
     if (!p || !g || !cov || !out) return set_err(BSF_EINVAL, "null argument");
     DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     cudaStream_t st = (cudaStream_t)stream;
     p->last = st;
@@ -618,6 +817,7 @@ extern "C" bsf_status bsf_filter_points_aux(bsf_plan_t p, const void *g, const v
                                             double *out, double *aux, void *stream) {
     if (!p || !g || !cov || !out || (!pts && npts)) return set_err(BSF_EINVAL, "null argument");
     DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (npts < 0) return set_err(BSF_EINVAL, "npts < 0");
     if (npts == 0) return BSF_OK;
@@ -742,6 +942,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
         a.order_cap = p->sched_cap;
     }
     a.split_tol = p->opt_split_tol;  // BSF_SPLIT_TOL_DEFAULT unless a diagnostics option changed it
+    a.cov_layout = p->d.cov_layout;
     return a;
 }
 
@@ -759,43 +960,25 @@ static bool global_exact(const bsf_plan_s *p) {
     return p->global_ok && p->d.anchor != BSF_ANCHOR_TILE && p->opt_fused && p->d.precision != BSF_PREC_FP64;
 }
 
-static bsf_status run_global(bsf_plan_s *p, const void *f, const void *cov, void *out, const int *pts, int npts,
-                             double *aux, cudaStream_t st) {
+// gather of global mode from exact int64 sums g ([nbases][nimg][GH][GW], the
+// bsf_preintegrate_exact layout): the order-1 integer kernel (bsf_gx1.cuh),
+// or (diagnostics option global_kernel = 0) the fused kernel's global mode
+static bsf_status filter_global(bsf_plan_s *p, const void *g, const void *cov, void *out, const int *pts, int npts,
+                                double *aux, cudaStream_t st) {
     bsf_status s = ensure_tile_ws(p, false);
     if (s != BSF_OK) return s;
     if (!p->fused) return set_err(BSF_EUNSUPPORTED, "global mode needs the exact split path");
-    // per basis and image: PadT zero rows (the zero state above the domain,
-    // read by taps near the top edge without a bounds check), then the GH x GW
-    // domain of bsf_preintegrate_exact
-    const Geometry &geo = p->geo;
-    const int padT = required_disp(p->d.max_sigma, p->d.order) + 8;
-    const size_t img_elems = (size_t)(padT + geo.GH) * geo.GW, slot = (size_t)geo.nimg * img_elems;
-    if (!p->gx_ws) {
-        void *q;
-        const size_t bytes = (size_t)geo.nbases * slot * sizeof(long long);
-        if (cudaMalloc(&q, bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "global int64 sums " + std::to_string(bytes));
-        p->dev_allocs.push_back(q);
-        p->gx_ws = (long long *)q;
-        CUDA_TRY(cudaMemsetAsync(q, 0, bytes, st));  // the pad rows stay zero (the scans write the domain only)
-    }
     p->last = st;
-    Geometry g1 = geo;
-    g1.nimg = 1;
-    const size_t plane = (size_t)geo.H * geo.W;
-    for (int b = 0; b < geo.nbases; ++b)
-        for (int i = 0; i < geo.nimg; ++i)
-            CUDA_TRY(launch_preint_i64((const uint8_t *)f + i * plane,
-                                       (unsigned long long *)p->gx_ws + b * slot + i * img_elems + (size_t)padT * geo.GW,
-                                       g1, p->bases[b], p->d.order, st, &p->nlaunch));
-    TileArgs a = tile_args(p, f, cov, out);
-    a.gPadT = padT;
+    const Geometry &geo = p->geo;
+    const size_t slot = (size_t)geo.nimg * geo.GH * geo.GW;
+    TileArgs a = tile_args(p, nullptr, cov, out);
     a.stile = p->stile_global;
     a.order = nullptr;  // order 1: raster hand-out
-    a.gP = p->geo.P;
-    a.gGW = p->geo.GW;
-    a.gGH = p->geo.GH;
-    for (int sl = 0; sl < p->geo.nbases; ++sl) {  // slot sl of the int64 buffer holds basis bases[sl]
-        a.gglob[p->bases[sl]] = p->gx_ws + sl * slot + (size_t)padT * geo.GW;
+    a.gP = geo.P;
+    a.gGW = geo.GW;
+    a.gGH = geo.GH;
+    for (int sl = 0; sl < geo.nbases; ++sl) {  // slot sl of the int64 buffer holds basis bases[sl]
+        a.gglob[p->bases[sl]] = (const long long *)g + sl * slot;
         a.gshift[p->bases[sl]] = p->gshift[p->bases[sl]];
     }
     if (pts) {
@@ -806,9 +989,35 @@ static bsf_status run_global(bsf_plan_s *p, const void *f, const void *cov, void
     }
     if (p->opt_global_kernel == 1)
         CUDA_TRY(launch_gx1(a, st, p->luts_dev, &p->nlaunch));
-    else  // diagnostics: the fused kernel's global mode (keys, bucket sort, DMMA groups)
+    else
         CUDA_TRY(launch_fused_impl(a, p->d.order, p->tile_nslots, st, p->luts_dev, &p->nlaunch));
     return BSF_OK;
+}
+
+static bsf_status run_global(bsf_plan_s *p, const void *f, const void *cov, void *out, const int *pts, int npts,
+                             double *aux, cudaStream_t st) {
+    if (!p->gx_ws) {
+        void *q;
+        const size_t bytes = g_bytes(p) / 2;  // int64 elements
+        if (cudaMalloc(&q, bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "global int64 sums " + std::to_string(bytes));
+        p->dev_allocs.push_back(q);
+        p->gx_ws = (long long *)q;
+    }
+    p->last = st;
+    const size_t slot = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW;
+    for (int b = 0; b < p->geo.nbases; ++b)
+        CUDA_TRY(launch_preint_i64((const uint8_t *)f, (unsigned long long *)p->gx_ws + b * slot, p->geo, p->bases[b],
+                                   p->d.order, st, &p->nlaunch));
+    return filter_global(p, p->gx_ws, cov, out, pts, npts, aux, st);
+}
+
+extern "C" bsf_status bsf_filter_exact(bsf_plan_t p, const void *g, const void *cov, void *out, void *stream) {
+    if (!p || !g || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
+    DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
+    if (!global_exact(p)) return set_err(BSF_EUNSUPPORTED, "bsf_filter_exact: the plan is not in global mode");
+    return filter_global(p, g, cov, out, nullptr, 0, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *cov, const int *pts, int npts,
@@ -818,6 +1027,7 @@ extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *co
     if (npts < 0) return set_err(BSF_EINVAL, "npts < 0");
     if (npts == 0) return BSF_OK;
     DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
     if (global_exact(p)) return run_global(p, f, cov, out, pts, npts, aux, (cudaStream_t)stream);
     bsf_status s = ensure_tile_ws(p);
     if (s != BSF_OK) return s;
@@ -834,6 +1044,86 @@ extern "C" bsf_status bsf_run_points(bsf_plan_t p, const void *f, const void *co
     return BSF_OK;
 }
 
+extern "C" bsf_status bsf_run_tiles(bsf_plan_t p, const void *f, const void *cov, void *out, const int *tiles,
+                                    int ntiles, void *stream) {
+    if (!p || !f || !cov || !out || (!tiles && ntiles)) return set_err(BSF_EINVAL, "null argument");
+    if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
+    if (ntiles < 0) return set_err(BSF_EINVAL, "ntiles < 0");
+    DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
+    if (global_exact(p)) return set_err(BSF_EUNSUPPORTED, "bsf_run_tiles: global-mode plans have no anchoring tiles");
+    if (ntiles == 0) return BSF_OK;
+    bsf_status s = ensure_tile_ws(p);
+    if (s != BSF_OK) return s;
+    if (p->d.boundary != BSF_BOUNDARY_ZERO && !p->fused)
+        return set_err(BSF_EUNSUPPORTED, "replicate boundary: fused path only (order <= 3)");
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last = st;
+    TileArgs a = tile_args(p, f, cov, out);
+    a.tiles = tiles;
+    a.ntiles = ntiles;
+    CUDA_TRY(launch_tile(p, a, st));
+    return BSF_OK;
+}
+
+// Row strip of a multi-GPU plan (include/bsf.h, bsf_plan_desc): the block of
+// input rows [b0, b1) is assembled from this rank's rows and the neighbours'
+// halo rows (ncclSend / ncclRecv, one group per call) unless the caller passed
+// the block itself (no communicator); then the fused kernel filters the own
+// rows [y0, y1) only, anchored on the full image's super-tiles.
+static bsf_status run_strip(bsf_plan_s *p, const void *f, const void *cov, void *out, cudaStream_t st) {
+    if (p->d.anchor == BSF_ANCHOR_GLOBAL) return set_err(BSF_EUNSUPPORTED, "row strips run the tile path");
+    bsf_status s = ensure_tile_ws(p);
+    if (s != BSF_OK) return s;
+    if (!p->fused) return set_err(BSF_EUNSUPPORTED, "row strips need the exact split path (order <= 3)");
+    p->last = st;
+    const int W = p->geo.W, nimg = p->geo.nimg;
+    const int own = p->y1 - p->y0, blk = p->b1 - p->b0, top = p->y0 - p->b0, bot = p->b1 - p->y1;
+    const size_t es = p->d.in_dtype == BSF_U8 ? 1 : 4;
+    const void *fb = f;
+    if (p->comm) {
+        if (!p->f_blk) {
+            void *q;
+            if (cudaMalloc(&q, (size_t)nimg * blk * W * es) != cudaSuccess) return set_err(BSF_ENOMEM, "strip block");
+            p->dev_allocs.push_back(q);
+            p->f_blk = q;
+        }
+        char *B = (char *)p->f_blk;
+        const char *F = (const char *)f;
+        const size_t row = (size_t)W * es;
+        for (int i = 0; i < nimg; ++i)
+            CUDA_TRY(cudaMemcpyAsync(B + ((size_t)i * blk + top) * row, F + (size_t)i * own * row, (size_t)own * row,
+                                     cudaMemcpyDeviceToDevice, st));
+        NcclApi &nc = nccl_api();
+        const ncclDataType_t dt = p->d.in_dtype == BSF_U8 ? ncclUint8 : ncclFloat32;
+        NCCL_TRY(nc.groupStart());
+        for (int i = 0; i < nimg; ++i) {
+            const char *Fi = F + (size_t)i * own * row;
+            char *Bi = B + (size_t)i * blk * row;
+            if (p->d.rank > 0) {  // rows [b0, y0) from rank - 1; it needs my first rows
+                const int up = std::min(p->halo, p->geo.H - p->y0) - 0;
+                const int need_up = std::min(up, own);  // rank - 1's bottom halo (<= own, checked at plan time)
+                NCCL_TRY(nc.send(Fi, (size_t)need_up * W, dt, p->d.rank - 1, p->comm, st));
+                NCCL_TRY(nc.recv(Bi, (size_t)top * W, dt, p->d.rank - 1, p->comm, st));
+            }
+            if (p->d.rank < p->d.nranks - 1) {  // rows [y1, b1) from rank + 1; it needs my last rows
+                const int need_dn = std::min(std::min(p->halo, p->y1), own);
+                NCCL_TRY(nc.send(Fi + (size_t)(own - need_dn) * row, (size_t)need_dn * W, dt, p->d.rank + 1, p->comm,
+                                 st));
+                NCCL_TRY(nc.recv(Bi + (size_t)(top + own) * row, (size_t)bot * W, dt, p->d.rank + 1, p->comm, st));
+            }
+        }
+        NCCL_TRY(nc.groupEnd());
+        fb = p->f_blk;
+    }
+    TileArgs a = tile_args(p, fb, cov, out);
+    a.H = blk;
+    a.oy0 = top;
+    a.oH = own;
+    CUDA_TRY(launch_tile(p, a, st));
+    return BSF_OK;
+}
+
 extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void *out, void *stream) {
     if (!p) return set_err(BSF_EINVAL, "null plan");
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
@@ -841,6 +1131,10 @@ extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void
     if (global_exact(p)) {
         if (!f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
         return run_global(p, f, cov, out, nullptr, 0, nullptr, (cudaStream_t)stream);
+    }
+    if (p->d.nranks > 1) {
+        if (!f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
+        return run_strip(p, f, cov, out, (cudaStream_t)stream);
     }
     if (p->d.anchor != BSF_ANCHOR_GLOBAL) {  // BSF_ANCHOR_TILE, or AUTO without global mode
         if (!f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
@@ -868,6 +1162,7 @@ extern "C" bsf_status bsf_run(bsf_plan_t p, const void *f, const void *cov, void
 extern "C" bsf_status bsf_run_normalized(bsf_plan_t p, const void *f, const void *cov, void *out, void *stream) {
     if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
     DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (p->d.anchor != BSF_ANCHOR_TILE) return set_err(BSF_EUNSUPPORTED, "DC renormalisation runs with BSF_ANCHOR_TILE");
     bsf_status s = ensure_tile_ws(p);
@@ -923,6 +1218,7 @@ extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov
                                     double fraction, double *sigma2_out, void *stream) {
     if (!p || !f || !cov || !out) return set_err(BSF_EINVAL, "null argument");
     DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     if (passes < 2 || passes > 16) return set_err(BSF_EINVAL, "passes must be 2..16");
     if (!(fraction < 1.0) || fraction < 0.0 || fraction != fraction)
@@ -936,7 +1232,7 @@ extern "C" bsf_status bsf_run_split(bsf_plan_t p, const void *f, const void *cov
     p->last = st;
     // sigma_b^2 = half the smallest bound (9) of the field (R21): the bound is 2 sigma_b^2
     CUDA_TRY(launch_alg1_sigma2((const float *)cov, p->d.batch, p->geo.W, p->geo.H, p->d.basis, p->d.clamp,
-                                p->alg1_sigma2, st, &p->nlaunch));
+                                p->d.cov_layout, p->alg1_sigma2, st, &p->nlaunch));
     // the isotropic part T = phi B (B = 2 sigma_b^2 the bound, phi = fraction,
     // default (n - 1) / n): passes - 1 isotropic passes of T / (n - 1) each,
     // ping-ponging through float64 work images, then the space-variant
@@ -989,6 +1285,7 @@ extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void 
                                    void *stream) {
     if (!p || !f_host || !cov_host || !out_host) return set_err(BSF_EINVAL, "null argument");
     DevGuard guard(p->d.device);
+    if (p->d.nranks > 1) return set_err(BSF_EUNSUPPORTED, "multi-GPU plans: bsf_run and bsf_preintegrate_exact only");
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     const Geometry &g = p->geo;
     size_t fb = (size_t)g.nimg * g.H * g.W * (p->d.in_dtype == BSF_U8 ? 1 : 4);

@@ -185,19 +185,29 @@ __device__ __forceinline__ int cls_region(const ClsTables &T, int b, double x, d
 // isotropic pass, theta = 0), or C - s sigma_b^2 I (same eigenvectors,
 // eigenvalues lowered: PAPER.md:228-231); s = sigma2_scale (1 for Algorithm 1,
 // the generalised splitting's shares otherwise, R22)
+// output row window (row strips): rows of cov / out, and membership
+__device__ __forceinline__ int out_rows(const TileArgs &a) { return a.oH ? a.oH : a.H; }
+__device__ __forceinline__ bool out_row(const TileArgs &a, int y) {
+    return y >= a.oy0 && y < a.oy0 + out_rows(a) && y < a.H;
+}
+__device__ __forceinline__ long long out_index(const TileArgs &a, int img, int x, int y) {
+    return ((long long)img * out_rows(a) + (y - a.oy0)) * a.W + x;
+}
+
 __device__ __forceinline__ void load_cov(const TileArgs &a, int img, int x, int y, double &sx, double &sy,
                                          double &th) {
-    const size_t ipl = (size_t)a.H * a.W;
+    const size_t ipl = (size_t)out_rows(a) * a.W;
     const int b = img / a.channels;
     if (a.cov_mode == COV_ISO) {
         sx = sy = sqrt(a.sigma2[b] * a.sigma2_scale);
         th = 0.0;
         return;
     }
-    const float *cv = a.cov + (size_t)b * 3 * ipl + (size_t)y * a.W + x;
+    const float *cv = a.cov + (size_t)b * 3 * ipl + (size_t)(y - a.oy0) * a.W + x;
     sx = __ldg(cv);
     sy = __ldg(cv + ipl);
     th = __ldg(cv + 2 * ipl);
+    if (a.cov_layout == BSF_COV_C11_C12_C22) cov_from_c(sx, sy, th, sx, sy, th);
     if (a.cov_mode == COV_SUB) {
         const double s2 = a.sigma2[b] * a.sigma2_scale;
         sx = sqrt(fmax(sx * sx - s2, 0.0));
@@ -975,11 +985,13 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
     double *scr0 = R >= 3 ? a.scratch0 + (size_t)blockIdx.x * NPLANE * a.cap : nullptr;  // G0 planes (order 3)
     // super-tile of ST x ST pixels = SQ x SQ sub-tiles of TILE x TILE (ST = 32 or 64, per plan)
     const int ST = a.stile, SQ = ST / TILE, NQ = SQ * SQ;
-    const int nstx = (a.W + ST - 1) / ST, nsty = (a.H + ST - 1) / ST;
+    // super-tile rows of the output window (all rows unless a row strip)
+    const int sty0 = a.oy0 / ST;
+    const int nstx = (a.W + ST - 1) / ST, nsty = (min(a.H, a.oy0 + out_rows(a)) + ST - 1) / ST - sty0;
     const int stiles_per_img = nstx * nsty;
     // work units: points, super-tiles, or in split mode the unit count the
     // order kernel wrote (quadrant units included)
-    int nitems = a.pts ? a.npts : stiles_per_img * a.nimg;
+    int nitems = a.pts ? a.npts : a.tiles ? a.ntiles : stiles_per_img * a.nimg;
     if constexpr (SPLIT) nitems = (int)__ldcg(a.order_hist + 2 * SCHED_NBIN);
     const size_t ipl = (size_t)a.H * a.W;
 
@@ -997,7 +1009,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         __syncthreads();
         if (s_item >= nitems) break;
         const int unit = s_item;  // hand-out index (diagnostics are keyed by it: unique in split mode too)
-        int item = a.order && !a.pts ? a.order[s_item] : s_item;
+        int item = a.tiles ? a.tiles[s_item] : (a.order && !a.pts ? a.order[s_item] : s_item);
         if constexpr (SPLIT) item >>= 3;  // unit code: super-tile << 3 | quadrant
         // sub-tile q of the super-tile belongs to this unit (always, unless split mode)
         auto qin = [&](int q) {
@@ -1020,17 +1032,17 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             img = item / stiles_per_img;
             const int rem = item % stiles_per_img;
             X0s = (rem % nstx) * ST;
-            Y0s = (rem / nstx) * ST;
+            Y0s = (sty0 + rem / nstx) * ST;
         }
 
         if (a.cov_mode == COV_ISO && !(a.sigma2[img / a.channels] > 0.0)) {
             // Algorithm 1 with sigma_b = 0: the isotropic pass is the identity
             for (int q = 0; q < NQ; ++q) {
                 const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
-                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H && qin(q));
+                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && out_row(a, y) && qin(q));
                 if (mine) {
                     const double v = load_f(a, (size_t)img * ipl + (size_t)y * a.W + x);
-                    const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
+                    const long long oidx = a.pts ? item : out_index(a, img, x, y);
                     if (a.out_f32 && !a.pts)
                         ((float *)a.out)[oidx] = (float)v;
                     else
@@ -1045,7 +1057,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         for (int q = 0; q < NQ; ++q) {
             const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
             double *sb = s_scl + ((size_t)q * FT + tid) * 5;  // this pixel's scales, reused by its sub-tile
-            if (x < a.W && y < a.H && qin(q)) {
+            if (x < a.W && out_row(a, y) && qin(q)) {
                 PixelScales ps;
                 double sx, sy, th;
                 load_cov(a, img, x, y, sx, sy, th);
@@ -1118,9 +1130,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             // happen when max_sigma bounds the covariance field)
             for (int q = 0; q < NQ; ++q) {
                 const int x = X0s + TILE * (q % SQ) + (tid % TILE), y = Y0s + TILE * (q / SQ) + tid / TILE;
-                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && y < a.H && qin(q));
+                const bool mine = a.pts ? (q == qwant && tid == want) : (x < a.W && out_row(a, y) && qin(q));
                 if (mine) {
-                    const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
+                    const long long oidx = a.pts ? item : out_index(a, img, x, y);
                     if (a.out_f32 && !a.pts)
                         ((float *)a.out)[oidx] = __int_as_float(0x7fc00000);
                     else
@@ -1298,7 +1310,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             ps.drop = -1;
             ps.clamped = 0;
             ps.ap[0] = ps.ap[1] = ps.ap[2] = ps.ap[3] = 0.0;
-            const bool valid = x < a.W && y < a.H;
+            const bool valid = x < a.W && out_row(a, y);
             if (valid) {  // the scales solved in the reach pass (same thread, same pixel)
                 const double *sb = s_scl + ((size_t)q * FT + tid) * 5;
 #pragma unroll
@@ -1595,7 +1607,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                         }
                     } else if (GLOBAL) {
                         const int k = s_pe[b * NVAR + var];
-                        const GlobSrc gs{a.gglob[b] + (size_t)img * (a.gGH + a.gPadT) * a.gGW, a.gGW, a.gGH, k,
+                        const GlobSrc gs{a.gglob[b] + (size_t)img * a.gGH * a.gGW, a.gGW, a.gGH, k,
                                          var ? c_steps[b][var - 1][0] : 0, var ? c_steps[b][var - 1][1] : 0, var != 0};
                         const double isc = ldexp(1.0, -k);
                         if (var == 0)
@@ -1687,7 +1699,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                     sumCF += __shfl_xor_sync(0xffffffffu, sumCF, o);
                 }
                 const int x = x0 + (p % TILE), y = y0 + p / TILE;
-                const bool valid = x < a.W && y < a.H;
+                const bool valid = x < a.W && out_row(a, y);
                 const bool mine = sub == 0 && (a.pts ? (p == want) : valid);
                 if (mine) {
                     double res = __longlong_as_double(0x7ff8000000000000LL);
@@ -1715,7 +1727,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                             s_fb[k] = (short)p;
                         }
                     }
-                    const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
+                    const long long oidx = a.pts ? item : out_index(a, img, x, y);
                     if (a.aux) {
                         double *ax = a.aux + BSF_AUX * oidx;
                         ax[0] = b;
@@ -1764,7 +1776,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 if constexpr (GLOBAL) {  // exact int64 global sums
                     gv.g = nullptr;
                     gv.sc = 0.0;
-                    gv.gi = a.gglob[b] + (size_t)img * (a.gGH + a.gPadT) * a.gGW;
+                    gv.gi = a.gglob[b] + (size_t)img * a.gGH * a.gGW;
                 }
                 if (pre3) {
                     gv.g0 = scr0 + s_poff[b * NVAR];
@@ -1775,7 +1787,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
                 const double res = mesh_warp<R>(gv, luts[b], ps, x, y, &fl);
                 fl = __reduce_or_sync(0xffffffffu, fl);
                 if (lane == 0) {
-                    const long long oidx = a.pts ? item : (long long)img * ipl + (size_t)y * a.W + x;
+                    const long long oidx = a.pts ? item : out_index(a, img, x, y);
                     if (a.out_f32 && !a.pts)
                         ((float *)a.out)[oidx] = (float)res;
                     else
@@ -1830,7 +1842,7 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
 // e_B the elongation bound (as (rho-1)/(rho+1)) of the basis the pixel uses,
 // C the (clamped) covariance the pixel is filtered with (R21).
 // ---------------------------------------------------------------------------
-__global__ void alg1_bound_kernel(const float *__restrict__ cov, int W, int H, int policy, int clamp,
+__global__ void alg1_bound_kernel(const float *__restrict__ cov, int W, int H, int policy, int clamp, int layout,
                                   unsigned long long *__restrict__ minbits) {
     const size_t ipl = (size_t)H * W;
     const int b = blockIdx.y;
@@ -1838,6 +1850,7 @@ __global__ void alg1_bound_kernel(const float *__restrict__ cov, int W, int H, i
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < ipl; i += (size_t)gridDim.x * blockDim.x) {
         const float *cv = cov + (size_t)b * 3 * ipl + i;
         double sx = cv[0], sy = cv[ipl], th = cv[2 * ipl];
+        if (layout == BSF_COV_C11_C12_C22) cov_from_c(sx, sy, th, sx, sy, th);
         double phi = th, maj = sx, mn = sy;
         if (sx < sy) {
             phi = th + M_PI / 2;
@@ -1872,14 +1885,14 @@ __global__ void alg1_finish_kernel(const unsigned long long *__restrict__ minbit
     if (b < batch) sigma2[b] = 0.5 * __longlong_as_double((long long)minbits[b]);  // half the bound
 }
 
-cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int policy, int clamp, double *sigma2,
-                               cudaStream_t st, long long *nl) {
+cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int policy, int clamp, int layout,
+                               double *sigma2, cudaStream_t st, long long *nl) {
     // sigma2 holds 2 * batch doubles: [0, batch) results, [batch, 2 batch) min bits
     unsigned long long *bits = reinterpret_cast<unsigned long long *>(sigma2 + batch);
     cudaError_t e = cudaMemsetAsync(bits, 0x7f, batch * sizeof(unsigned long long), st);  // a large positive double
     if (e != cudaSuccess) return e;
     const int blocks = (int)((size_t)H * W / 256 + 1 < 1184 ? (size_t)H * W / 256 + 1 : 1184);
-    alg1_bound_kernel<<<dim3(blocks, batch), 256, 0, st>>>(cov, W, H, policy, clamp, bits);
+    alg1_bound_kernel<<<dim3(blocks, batch), 256, 0, st>>>(cov, W, H, policy, clamp, layout, bits);
     alg1_finish_kernel<<<1, 1024, 0, st>>>(bits, batch, sigma2);
     *nl += 2;
     return cudaGetLastError();
@@ -1922,15 +1935,16 @@ __global__ void __launch_bounds__(256) fused_cost_kernel(TileArgs a, const LutBa
     constexpr int NTAP = FusedCfg<R>::NTAP;
     const int lane = threadIdx.x & 31, item = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (item >= nitems) return;
-    const int ST = a.stile, nstx = (a.W + ST - 1) / ST, spi = nstx * ((a.H + ST - 1) / ST);
-    const int img = item / spi, rem = item % spi, X0s = (rem % nstx) * ST, Y0s = (rem / nstx) * ST;
+    const int ST = a.stile, nstx = (a.W + ST - 1) / ST, sty0 = a.oy0 / ST;
+    const int spi = nstx * ((min(a.H, a.oy0 + out_rows(a)) + ST - 1) / ST - sty0);
+    const int img = item / spi, rem = item % spi, X0s = (rem % nstx) * ST, Y0s = (sty0 + rem / nstx) * ST;
     const int step = ST / 8;
     float acc = 0.f, smin = 3.0e38f;
     int ex[2] = {0, 0}, ey[2] = {0, 0}, vm[2] = {0, 0};
     if (!(a.cov_mode == COV_ISO && !(a.sigma2[img / a.channels] > 0.0))) {
         for (int s = lane; s < 64; s += 32) {
             const int x = X0s + (s & 7) * step + step / 2, y = Y0s + (s >> 3) * step + step / 2;
-            if (x < a.W && y < a.H) {
+            if (x < a.W && out_row(a, y)) {
                 double sx, sy, th;
                 load_cov(a, img, x, y, sx, sy, th);
                 smin = fminf(smin, (float)fmin(sx, sy));
@@ -2059,12 +2073,14 @@ cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStrea
     cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
     TileArgs b = a;
-    const long long nitems = (long long)((a.W + a.stile - 1) / a.stile) * ((a.H + a.stile - 1) / a.stile) * a.nimg;
+    const int oh = a.oH ? a.oH : a.H, sty0 = a.oy0 / a.stile;
+    const long long nitems = (long long)((a.W + a.stile - 1) / a.stile) *
+                             ((std::min(a.H, a.oy0 + oh) + a.stile - 1) / a.stile - sty0) * a.nimg;
     // split mode (see fused_cost_kernel): 64 x 64 super-tiles at order 2 run the
     // scheduling kernels at any item count
     const int S = (a.stile == 64 && order == 2) ? 4 : 1;
     if ((a.gglob[0] || a.gglob[1]) && order != 1) return cudaErrorInvalidValue;  // global mode: order 1 only
-    if (a.order && !a.pts && order >= 2 && (S == 4 || nitems >= 2 * (long long)slots) &&
+    if (a.order && !a.pts && !a.tiles && order >= 2 && (S == 4 || nitems >= 2 * (long long)slots) &&
         nitems * S <= a.order_cap) {
         // largest-first work order (see fused_cost_kernel); at order 1 the
         // balance it gains (3.7 -> 1.2 % on config 3) is lost to the halo reads

@@ -57,9 +57,9 @@ __device__ __forceinline__ int gx1_byte(unsigned w, int k) {  // signed byte k o
 // the domain (and the buffer has zero rows above it), so no read is bounds
 // checked.  Slots go in groups of four with all loads of a group issued before
 // its multiply-adds.
-template <int NMON>
+template <int NMON, bool TOP>
 __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restrict__ Gt, int b, int v, int reg,
-                                      double fx, double fy, int sdl) {
+                                      double fx, double fy, int sdl, int row0, int GW) {
     int acc[3][NMON];
 #pragma unroll
     for (int l = 0; l < 3; ++l)
@@ -74,8 +74,17 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int o = off[s0 + i];
-            g[i] = __ldg(Gt + o);
-            if (NMON == 3) g[i] -= __ldg(Gt + (o - sdl));
+            if constexpr (TOP) {
+                // the tap's window reaches above the domain: zero state there
+                // (row of a read = row0 + floor((o + GW/2) / GW), GW > 2 |dx|)
+                const int ry = row0 + (o + (GW >> 1) + 16 * GW) / GW - 16;
+                const int ryv = ry - (sdl + (GW >> 1) + 16 * GW) / GW + 16;
+                g[i] = ry >= 0 ? __ldg(Gt + o) : 0ll;
+                if (NMON == 3) g[i] -= ryv >= 0 ? __ldg(Gt + (o - sdl)) : 0ll;
+            } else {
+                g[i] = __ldg(Gt + o);
+                if (NMON == 3) g[i] -= __ldg(Gt + (o - sdl));
+            }
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -148,6 +157,7 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
         }
     }
     const int sdl = v ? c_steps[b][v - 1][1] * GW + c_steps[b][v - 1][0] : 0;
+    const int wymin = S.ext[b].z;
     const int ntap = 1 << ns;
     double h0 = 0.0, e0 = 0.0, sumF = 0.0;
     for (int t = 0; t < ntap; ++t) {
@@ -163,8 +173,12 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
         const double flx = floor(Dx), fly = floor(Dy);
         const double fx = Dx - flx, fy = Dy - fly;  // exact
         const int reg = cls_region(S.cls, b, fx, fy);
-        const long long *Gt = G + ((ptrdiff_t)(y + (int)fly) * GW + (x + (int)flx + P));
-        const dd F = gx1_tap<NMON>(S, Gt, b, v, reg, fx, fy, sdl);
+        const int by = y + (int)fly;
+        const long long *Gt = G + ((ptrdiff_t)by * GW + (x + (int)flx + P));
+        // windows that reach above row 0 read the zero state there (checked
+        // loads); all other reads are inside the domain (reach checked)
+        const dd F = by + wymin - 2 >= 0 ? gx1_tap<NMON, false>(S, Gt, b, v, reg, fx, fy, sdl, by, GW)
+                                         : gx1_tap<NMON, true>(S, Gt, b, v, reg, fx, fy, sdl, by, GW);
         macs += (unsigned long long)S.cnt[b][v][reg] * NMON;  // algorithmic: window x monomials
         // compensated signed sum: TwoSum on the heads, small terms in e0
         const double fh = sgn > 0 ? F.hi : -F.hi, fl = sgn > 0 ? F.lo : -F.lo;
@@ -229,7 +243,6 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
         base += nreg * nmax4;
     }
     __syncthreads();
-    const size_t ipl = (size_t)a.H * a.W;
     const int ntx = (a.W + GX1_TW - 1) / GX1_TW, nty = (a.H + GX1_TH - 1) / GX1_TH;
     const long long nunits = a.pts ? ((long long)a.npts + GX1_BLOCK - 1) / GX1_BLOCK : (long long)ntx * nty * a.nimg;
     unsigned long long macs = 0;
@@ -265,7 +278,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
                 img = img_t;
                 x = x0 + tid % GX1_TW;
                 y = y0 + tid / GX1_TW;
-                valid = x < a.W && y < a.H;
+                valid = x < a.W && out_row(a, y);
             }
             PixelScales ps;
             ps.flags = 0;
@@ -324,7 +337,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
                 img = img_t;
                 x = x0 + p % GX1_TW;
                 y = y0 + p / GX1_TW;
-                oidx = (long long)img * ipl + (size_t)y * a.W + x;
+                oidx = out_index(a, img, x, y);
             }
             int flags = ps.flags;
             const bool live = valid && !(flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
@@ -343,11 +356,11 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
                 const int ex = (int)ceil(0.5 * rx) + 1, ey = (int)ceil(0.5 * ry) + 1;
                 const int4 E = S.ext[ps.basis];
                 const bool in = x + a.gP - ex + E.x - 2 >= 0 && x + a.gP + ex + E.y + 2 < a.gGW &&
-                                y - ey + E.z - 2 >= -a.gPadT && y + ey + E.w < a.gGH;
+                                y + ey + E.w < a.gGH;
                 if (!in) {
                     flags |= FLAG_RANGE;
                 } else {
-                    const long long *G = a.gglob[ps.basis] + (size_t)img * (a.gGH + a.gPadT) * a.gGW;
+                    const long long *G = a.gglob[ps.basis] + (size_t)img * a.gGH * a.gGW;
                     res = ps.drop < 0 ? gx1_mesh<6>(S, G, a.gGW, a.gP, ps, x, y, erel, macs)
                                       : gx1_mesh<3>(S, G, a.gGW, a.gP, ps, x, y, erel, macs);
                     if (!(erel <= a.split_tol)) {  // NaN-safe: the double-double mesh on the same sums

@@ -143,6 +143,7 @@ struct GatherArgs {
     int npts;
     double *aux;            // optional per-point diagnostics [8 * npts]
     unsigned long long *stats;  // [6]: pixels, clamped, zero, theta', flags(or), double-double
+    int cov_layout;             // BSF_COV_SIGMA_THETA / BSF_COV_C11_C12_C22
 };
 
 // Tile-anchored fused path: per 16x16 output tile, local running sums on the
@@ -180,10 +181,16 @@ struct TileArgs {
     long long order_cap;       // units (bin slots) the order buffers hold
     // global mode (order 1, u8): taps read the exact int64 global running sums
     // [nbases][nimg][gGH][gGW] (bsf_preintegrate_exact layout), limb shift per basis
-    const long long *gglob[2];  // per basis id (null: basis not in the plan / not global mode): row 0 of
-                                // image 0's domain; images are (gPadT + gGH) rows apart, the first gPadT
-                                // rows of each being zeros (the zero state above the domain)
-    int gP, gGW, gGH, gPadT;
+    // output row window (row strips, bsf_plan_desc.nranks > 1): only image rows
+    // [oy0, oy0 + oH) of the f block are filtered (oy0 a multiple of the
+    // super-tile side); cov and out hold those rows only.  oH = 0: all rows.
+    int oy0, oH;
+    int cov_layout;             // BSF_COV_SIGMA_THETA / BSF_COV_C11_C12_C22
+    const int *tiles;           // optional list of anchoring-tile indices to compute (bsf_run_tiles);
+    int ntiles;                 // index = (img * tiles_y + ty) * tiles_x + tx in units of the plan's tile side
+    const long long *gglob[2];  // per basis id (null: basis not in the plan / not global mode): the
+                                // bsf_preintegrate_exact sums [nimg][gGH][gGW] of that basis
+    int gP, gGW, gGH;
     int gshift[2];
 };
 constexpr int SCHED_NBIN = 128;
@@ -210,8 +217,8 @@ constexpr int BSF_PROF_ITEMS = 8192, BSF_PROF_CTAS = 1024;
 constexpr int BSF_PROF_WORK = 16 + BSF_PROF_ITEMS + BSF_PROF_CTAS;  // then 4 work figures per item
 constexpr int BSF_PROF_WORDS = BSF_PROF_WORK + 4 * BSF_PROF_ITEMS;
 enum { COV_PLANES = 0, COV_ISO = 1, COV_SUB = 2 };
-cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int policy, int clamp, double *sigma2,
-                               cudaStream_t st, long long *nlaunch);
+cudaError_t launch_alg1_sigma2(const float *cov, int batch, int W, int H, int policy, int clamp, int layout,
+                               double *sigma2, cudaStream_t st, long long *nlaunch);
 size_t tile_capacity(int order, float max_sigma, const LutBasis *host_luts, int basis_mask, int tile);
 int tile_slots();
 cudaError_t launch_tile_impl(const TileArgs &a, int order, int precision, int slots, cudaStream_t st,

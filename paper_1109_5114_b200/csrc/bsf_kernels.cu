@@ -569,7 +569,9 @@ __global__ void __launch_bounds__(128, BSF_GATHER_MINB) gather_kernel(GatherArgs
     int bc = img / a.channels;
     const float *cv = a.cov + (size_t)bc * 3 * plane + (size_t)y * geo.W + x;
     PixelScales ps;
-    pixel_scales(__ldg(cv), __ldg(cv + plane), __ldg(cv + 2 * plane), a.policy, a.clamp, R, ps);
+    double sx = __ldg(cv), sy = __ldg(cv + plane), th = __ldg(cv + 2 * plane);
+    if (a.cov_layout == BSF_COV_C11_C12_C22) cov_from_c(sx, sy, th, sx, sy, th);
+    pixel_scales(sx, sy, th, a.policy, a.clamp, R, ps);
     double res;
     int flags = ps.flags;
     int used_dd = MODE == BSF_PREC_DD;
@@ -671,7 +673,7 @@ __global__ void __launch_bounds__(256, BSF_TILE_MINB) tile_kernel(TileArgs a, co
     const int tid = threadIdx.x;
     double2 *scr = a.scratch + (size_t)blockIdx.x * 2 * a.cap;
     const int tiles_per_img = a.ntx * a.nty;
-    const int nitems = a.pts ? a.npts : tiles_per_img * a.nimg;
+    const int nitems = a.pts ? a.npts : a.tiles ? a.ntiles : tiles_per_img * a.nimg;
     for (;;) {
         if (tid == 0) {
             s_item = atomicAdd(a.counter, 1);
@@ -680,8 +682,8 @@ __global__ void __launch_bounds__(256, BSF_TILE_MINB) tile_kernel(TileArgs a, co
             s_bad = 0;
         }
         __syncthreads();
-        const int item = s_item;
-        if (item >= nitems) break;
+        if (s_item >= nitems) break;
+        const int item = a.tiles ? a.tiles[s_item] : s_item;
         int img, x0, y0, want = -1;
         if (a.pts) {
             img = a.pts[3 * item];
@@ -705,7 +707,9 @@ __global__ void __launch_bounds__(256, BSF_TILE_MINB) tile_kernel(TileArgs a, co
         if (valid) {
             size_t plane = (size_t)a.H * a.W;
             const float *cv = a.cov + (size_t)(img / a.channels) * 3 * plane + (size_t)y * a.W + x;
-            pixel_scales(__ldg(cv), __ldg(cv + plane), __ldg(cv + 2 * plane), a.policy, a.clamp, R, ps);
+            double sx = __ldg(cv), sy = __ldg(cv + plane), th = __ldg(cv + 2 * plane);
+            if (a.cov_layout == BSF_COV_C11_C12_C22) cov_from_c(sx, sy, th, sx, sy, th);
+            pixel_scales(sx, sy, th, a.policy, a.clamp, R, ps);
         }
         const bool live = valid && !(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
         if (live) {

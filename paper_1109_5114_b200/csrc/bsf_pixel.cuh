@@ -133,6 +133,18 @@ __device__ __forceinline__ int solve_scales(int basis, double C11, double C12, d
     return flags;
 }
 
+// BSF_COV_C11_C12_C22: the covariance planes decoded in fp64 to the
+// (sigma_x >= sigma_y, theta) form of the sigma/theta layout: eigenvalues of
+// [[C11, C12], [C12, C22]] and the angle of the top eigenvector,
+// theta = atan2(2 C12, C11 - C22) / 2
+__device__ __forceinline__ void cov_from_c(double c11, double c12, double c22, double &sx, double &sy, double &th) {
+    const double m = 0.5 * (c11 + c22), d = hypot(0.5 * (c11 - c22), c12);
+    sx = sqrt(fmax(m + d, 0.0));
+    sy = sqrt(fmax(m - d, 0.0));
+    th = 0.5 * atan2(2.0 * c12, c11 - c22);
+    if (th < 0.0) th += M_PI;
+}
+
 // Steps a1-a4: sigma_x, sigma_y, theta -> basis, a'_k, zero-direction.
 __device__ __forceinline__ void pixel_scales(double sx, double sy, double th, int policy, int clamp, int order,
                                              PixelScales &ps) {

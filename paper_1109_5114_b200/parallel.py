@@ -6,7 +6,10 @@
   on f inside p's kernel support (half-extent <= R_s = sigma_max sqrt(24 r)),
   so each rank receives the input rows [y0 - R_s, y0) and [y1, y1 + R_s) from
   its neighbours (one NCCL send/recv pair per neighbour) and runs the
-  tile-anchored kernel on its block.  Strip and halo boundaries are multiples
+  tile-anchored kernel on its block, computing its own rows only.  The
+  exchange runs inside the library when the plan has a communicator
+  (bsf_plan_desc.nccl_id, include/bsf.h), or here through torch.distributed
+  (filter_strip).  Strip and halo boundaries are multiples
   of the super-tile (plan.geometry.super_tile rows) on which the fused kernel
   anchors its running sums -- every rank's plan is created with the full
   image's super_tile (bsf_plan_desc.super_tile), since the automatic choice
@@ -38,9 +41,10 @@ def shard_range(n: int, rank: int, world: int):
 
 def halo_rows(max_sigma: float, order: int, tile: int = TILE) -> int:
     """Rows a super-tile's halo domain reaches beyond it (tap reach bound
-    sigma_max sqrt(24 r) plus the interpolation window, <= 6r + 2 rows),
-    rounded up to whole super-tiles of side `tile`."""
-    rs = int(math.ceil(max_sigma * math.sqrt(24.0 * order))) + 6 * order + 4
+    ceil(sigma_max sqrt(24 r)) + 1 plus the interpolation window, <= 6r + 2
+    rows), rounded up to whole super-tiles of side `tile`: the value the
+    library uses for multi-GPU plans (bsf_geometry.halo)."""
+    rs = int(math.ceil(max_sigma * math.sqrt(24.0 * order))) + 1 + 6 * order + 4
     return tile * ((rs + tile - 1) // tile)
 
 
@@ -67,11 +71,11 @@ class Strip:
 
 def strip_plan(H: int, rank: int, world: int, halo: int, tile: int = TILE) -> Strip:
     """Row strips aligned to the super-tile grid (side `tile` = the plan's
-    geometry.super_tile; every strip but the last has a multiple of it)."""
-    ntiles = (H + tile - 1) // tile
-    t0, t1 = shard_range(ntiles, rank, world)
-    y0, y1 = t0 * tile, min(H, t1 * tile)
-    return Strip(rank, world, y0, y1, max(0, y0 - halo), min(H, y1 + halo), halo, tile)
+    geometry.super_tile; every strip but the last has a multiple of it): the
+    library's own partition (bsf_strip_rows, host arithmetic, no GPU)."""
+    from . import bsf
+    y0, y1, b0, b1 = bsf.strip_rows(H, tile, halo, rank, world)
+    return Strip(rank, world, y0, y1, b0, b1, halo, tile)
 
 
 def exchange_halos(own: torch.Tensor, strip: Strip, H: int, group=None) -> torch.Tensor:
@@ -111,27 +115,29 @@ def exchange_halos(own: torch.Tensor, strip: Strip, H: int, group=None) -> torch
     return block
 
 
-def filter_strip(plan_factory, f_own: torch.Tensor, cov_own: torch.Tensor, strip: Strip, H: int, group=None,
+def filter_strip(plan, f_own: torch.Tensor, cov_own: torch.Tensor, strip: Strip, H: int, group=None,
                  stream=None) -> torch.Tensor:
-    """Filter this rank's strip of one image: exchange input halos, run the
-    tile-anchored library path on the block, keep the own rows.
-
-    plan_factory(height) -> a bsf.Plan for a W x height block (anchor TILE,
-    super_tile = strip.tile: the anchoring unit of the full image)
-    f_own (y1 - y0, W); cov_own (3, y1 - y0, W) -- this rank's rows only.
-    The covariance of halo rows is never used (their outputs are discarded),
-    so it is not exchanged."""
+    """Filter this rank's strip of one image with the halo exchanged through
+    torch.distributed (NCCL over NVLink for CUDA tensors, gloo on CPU), then
+    the library on the block: `plan` is this rank's multi-GPU plan without a
+    communicator (bsf.Plan(..., height=H, rank=, nranks=): its geometry is the
+    strip), whose bsf_run takes the block of input rows and computes only the
+    strip's own rows.  f_own (C, y1 - y0, W); cov_own (3, y1 - y0, W): this
+    rank's rows only.  Returns (C, y1 - y0, W) float64.  (A plan WITH a
+    communicator, nccl_id=bsf.get_unique_id() broadcast from rank 0, does the
+    same exchange inside the library: plan.run(f_own, cov_own, out).)"""
     f_blk = exchange_halos(f_own, strip, H, group)
-    cov_blk = cov_own.new_zeros((3, strip.rows, cov_own.shape[-1]))
-    cov_blk[:, strip.out_slice, :] = cov_own
-    if strip.y0 > strip.b0:
-        cov_blk[:, :strip.y0 - strip.b0, :] = 1.0  # placeholder sigma for discarded halo outputs
-    if strip.b1 > strip.y1:
-        cov_blk[:, strip.rows - (strip.b1 - strip.y1):, :] = 1.0
-    plan = plan_factory(strip.rows)
-    out = torch.empty((1, strip.rows, f_own.shape[-1]), dtype=torch.float64, device=f_own.device)
-    plan.run(f_blk.contiguous(), cov_blk.contiguous(), out, stream)
-    return out[0, strip.out_slice, :]
+    out = torch.empty((f_own.shape[0] if f_own.dim() == 3 else 1, strip.y1 - strip.y0, f_own.shape[-1]),
+                      dtype=torch.float64, device=f_own.device)
+    plan.run(f_blk.contiguous(), cov_own.contiguous(), out, stream)
+    return out
+
+
+def strip_plan_of(plan) -> Strip:
+    """The Strip of a multi-GPU bsf.Plan (its geometry)."""
+    g, d = plan.geometry, plan.desc
+    return Strip(d.rank, d.nranks, g.row0, g.row0 + g.row_count, g.block_row0, g.block_row0 + g.block_rows, g.halo,
+                 g.super_tile)
 
 
 # ---------------------------------------------------------------------------

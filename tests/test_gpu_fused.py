@@ -298,3 +298,41 @@ def test_split_mode_cost_bin_saturation():
     mask = torch.ones(H, W, dtype=torch.bool)
     mask[64:128, 64:128] = False
     assert torch.isfinite(out[mask]).all()
+
+
+@pytest.mark.parametrize("r", [2, 4])
+def test_run_tiles_equals_run_on_listed_tiles(r):
+    """bsf_run_tiles computes exactly bsf_run's values on the listed anchoring
+    tiles (same kernel, same anchoring) and leaves the other outputs alone."""
+    w = synth.workload(3, order=r, width=160 if r == 4 else 300, height=96 if r == 4 else 200,
+                       max_sigma=4.0 if r == 4 else 40.0, extra={"grid_span": 800})
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    if r == 4:
+        cov[0] = cov[0].clamp(max=3.0)
+        cov[1] = torch.minimum(cov[1], cov[0])
+    plan = make_plan(w, anchor=TILE)
+    u = plan.geometry.tile_unit
+    assert u in (16, 32, 64)
+    ntx, nty = (w.width + u - 1) // u, (w.height + u - 1) // u
+    ids = torch.tensor(sorted({0, ntx - 1, ntx * nty - 1, ntx + 1}), dtype=torch.int32)
+    dev = torch.device("cuda:0")
+    sub = torch.full((1, w.height, w.width), float("nan"), dtype=torch.float64, device=dev)
+    plan.run_tiles(img[None].to(dev).contiguous(), cov.to(dev).contiguous(), sub, ids.to(dev))
+    torch.cuda.synchronize()
+    sub = sub.cpu()[0]
+    if r == 4:  # order 4: compare with the oracle on the listed tiles (a full run is slow)
+        from gpu_util import oracle_points
+        for t in ids.tolist()[:2]:
+            ty, tx = divmod(t, ntx)
+            ys, xs = np.mgrid[ty * u:min(w.height, ty * u + u):5, tx * u:min(w.width, tx * u + u):5]
+            ref = oracle_points(img.numpy(), cov.numpy(), xs.ravel(), ys.ravel(), policy=w.basis, r=4)[0]
+            got = sub.numpy()[ys.ravel(), xs.ravel()]
+            assert np.max(np.abs(got - ref) / np.abs(ref)) <= 1e-9
+    else:
+        full = gpu_full(plan, img[None], cov)[0]
+        mask = torch.zeros(w.height, w.width, dtype=torch.bool)
+        for t in ids.tolist():
+            ty, tx = divmod(t, ntx)
+            mask[ty * u:(ty + 1) * u, tx * u:(tx + 1) * u] = True
+        assert torch.equal(sub[mask], full[mask])
+        assert torch.isnan(sub[~mask]).all()

@@ -90,3 +90,22 @@ def test_global_mode_not_taken_when_sums_could_overflow():
     assert make_plan(w, anchor=bsf.BSF_ANCHOR_AUTO).geometry.global_mode == 0
     w2 = synth.workload(2)  # float input: never global mode
     assert make_plan(w2, anchor=bsf.BSF_ANCHOR_AUTO).geometry.global_mode == 0
+
+
+def test_filter_exact_is_run_split_in_two_calls():
+    """bsf_preintegrate_exact + bsf_filter_exact (the two-call form bench.py
+    times) give bsf_run's output bit for bit; non-global plans refuse it."""
+    w = synth.workload(3, width=256, height=200, extra={"grid_span": 4096})
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    plan = make_plan(w, anchor=bsf.BSF_ANCHOR_AUTO)
+    a = gpu_full(plan, img[None], cov)
+    dev = torch.device("cuda:0")
+    g = plan.empty_g_exact()
+    out = torch.empty((1, w.height, w.width), dtype=torch.float64, device=dev)
+    plan.preintegrate_exact(img[None].to(dev).contiguous(), g)
+    plan.filter_exact(g, cov.to(dev).contiguous(), out)
+    torch.cuda.synchronize()
+    assert torch.equal(a, out.cpu())
+    tp = make_plan(w, anchor=bsf.BSF_ANCHOR_TILE)
+    with pytest.raises(bsf.BsfError):
+        tp.filter_exact(g, cov.to(dev).contiguous(), out)

@@ -29,34 +29,56 @@ def _field(H, W, smax):
 @pytest.mark.parametrize("order,policy,smax", [(2, bsf.BSF_DUAL, 5.0), (3, bsf.BSF_THETA, 5.0),
                                                (1, bsf.BSF_DUAL, 16.0)])
 def test_strips_bitwise_equal_single_gpu(world, order, policy, smax):
-    """(order 1, sigma 16: the plan anchors on 64 x 64 super-tiles)"""
-    H, W = 352, 200
+    """Multi-GPU plans (bsf_plan_desc rank / nranks, no communicator: the
+    caller assembles the halo, what parallel.exchange_halos does): each rank's
+    bsf_run takes its block of input rows and computes its own rows only; they
+    equal the one-GPU run bit for bit.  (order 1, sigma 16: 64 x 64 super-tiles
+    and a 128-row halo, so a taller image: every strip holds its neighbours'
+    halos)"""
+    H, W = (640 if order == 1 else 352), 200
     w = synth.workload(5, width=W, height=H, max_sigma=smax, order=order)
     img = synth.make_image(w).cuda()
     cov = _field(H, W, smax).cuda()
 
-    def plan(height, super_tile=0):
-        return bsf.Plan(W, height, in_dtype=bsf.BSF_F32, order=order, basis=policy, max_sigma=smax,
-                        anchor=bsf.BSF_ANCHOR_TILE, super_tile=super_tile)
+    def plan(rank=0, nranks=1):
+        return bsf.Plan(W, H, in_dtype=bsf.BSF_F32, order=order, basis=policy, max_sigma=smax,
+                        anchor=bsf.BSF_ANCHOR_TILE, rank=rank, nranks=nranks, super_tile=64 if order == 1 else 32)
 
     full = torch.empty((1, H, W), dtype=torch.float64, device="cuda")
-    p_full = plan(H, 64 if order == 1 else 32)  # the strips reuse the full plan's anchoring unit
+    p_full = plan()
     tile = p_full.geometry.super_tile
     assert tile == (64 if order == 1 else 32)
     p_full.run(img[None].contiguous(), cov.contiguous(), full)
-    halo = PL.halo_rows(smax, order, tile)
+    rows = 0
     for rank in range(world):
-        st = PL.strip_plan(H, rank, world, halo, tile)
+        p = plan(rank, world)
+        st = PL.strip_plan_of(p)
+        assert st.tile == tile and st.halo == PL.halo_rows(smax, order, tile)
+        assert (st.y0, st.y1, st.b0, st.b1) == bsf.strip_rows(H, tile, st.halo, rank, world)
         assert st.y0 % tile == 0 and st.b0 % tile == 0
         f_blk = img[st.b0:st.b1]                     # = exchange_halos(own rows)
-        cov_blk = torch.ones((3, st.rows, W), dtype=torch.float32, device="cuda")
-        cov_blk[:, st.out_slice] = cov[:, st.y0:st.y1]  # halo outputs are discarded
-        out = torch.empty((1, st.rows, W), dtype=torch.float64, device="cuda")
-        plan(st.rows, tile).run(f_blk[None].contiguous(), cov_blk.contiguous(), out)
+        out = torch.empty((1, st.y1 - st.y0, W), dtype=torch.float64, device="cuda")
+        p.run(f_blk[None].contiguous(), cov[:, st.y0:st.y1].contiguous(), out)
         torch.cuda.synchronize()
-        got = out[0, st.out_slice]
         ref = full[0, st.y0:st.y1]
-        assert torch.equal(got, ref), (rank, float((got - ref).abs().max()))
+        assert torch.equal(out[0], ref), (rank, float((out[0] - ref).abs().max()))
+        assert p.stats()["pixels"] == (st.y1 - st.y0) * W  # own rows only
+        rows += st.y1 - st.y0
+    assert rows == H
+
+
+def test_multi_gpu_plan_refuses_other_entry_points_and_nccl_id():
+    w = synth.workload(5, width=64, height=256, max_sigma=2.0, order=1)
+    p = bsf.Plan(64, 256, in_dtype=bsf.BSF_F32, order=1, basis=2, max_sigma=2.0, anchor=bsf.BSF_ANCHOR_TILE,
+                 rank=0, nranks=2)
+    g = p.geometry
+    assert g.row0 == 0 and g.row_count == 128 and g.block_rows == 128 + g.halo
+    img = synth.make_image(w).cuda()
+    out = torch.empty((1, 256, 64), dtype=torch.float64, device="cuda")
+    with pytest.raises(bsf.BsfError):
+        p.run_tiles(img[None].contiguous(), torch.ones(3, 256, 64, device="cuda"), out,
+                    torch.zeros(1, dtype=torch.int32, device="cuda"))
+    assert len(bsf.get_unique_id()) == 128  # NCCL loads in-process (the id a rank-0 caller broadcasts)
 
 
 def _global_strips_sequential(make_plan, img, H, Pb, world, exact):

@@ -91,3 +91,23 @@ def test_replicate_boundary_unsupported_paths():
     img = synth.make_image(w)[None].cuda()
     with pytest.raises(bsf.BsfError):
         g_plan.preintegrate(img, g_plan.empty_g())
+
+
+@pytest.mark.parametrize("anchor", [bsf.BSF_ANCHOR_TILE, bsf.BSF_ANCHOR_AUTO])
+def test_covariance_planes_layout(anchor):
+    """BSF_COV_C11_C12_C22: the covariance given as (C11, C12, C22) planes
+     filters like the same covariance in the (sigma_x,
+    sigma_y, theta) layout, to the rounding of the eigen-decomposition."""
+    from gpu_util import gpu_full
+    w = synth.workload(3, order=1, width=200, height=150, extra={"grid_span": 1200})
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    sx, sy, th = cov.double()
+    c, s = torch.cos(th), torch.sin(th)
+    C = torch.stack([sx * sx * c * c + sy * sy * s * s, (sx * sx - sy * sy) * s * c,
+                     sx * sx * s * s + sy * sy * c * c]).float()
+    a = gpu_full(bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8, order=1, basis=2, max_sigma=w.max_sigma,
+                          anchor=anchor), img[None], cov)
+    b = gpu_full(bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8, order=1, basis=2, max_sigma=w.max_sigma,
+                          anchor=anchor, cov_layout=bsf.BSF_COV_C11_C12_C22), img[None], C)
+    rel = ((a - b).abs() / a.abs()).max()
+    assert float(rel) < 1e-5, float(rel)  # float32 planes: the two layouts round differently

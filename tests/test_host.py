@@ -104,3 +104,16 @@ def test_plan_rejects_bad_descriptors():
     with pytest.raises(bsf.BsfError) as e:
         bsf.Plan(10, 10, max_sigma=10.0, margin_x=5)
     assert e.value.status == 5
+
+
+def test_binding_validates_tensors_before_the_c_abi():
+    """The C ABI takes raw pointers and cannot check them: the binding does
+    (dtype, contiguity, element count, device)."""
+    import torch
+    from paper_1109_5114_b200 import bsf
+    t = torch.zeros(10, dtype=torch.float32)
+    bsf._want(t, "x", ["float32"], 10, "cpu")
+    for args in ((t, "x", ["float64"], 10, "cpu"), (t, "x", ["float32"], 11, "cpu"),
+                 (t.view(2, 5).t(), "x", ["float32"], 10, "cpu"), (t, "x", ["float32"], 10, 0)):
+        with pytest.raises(bsf.BsfError):
+            bsf._want(*args)

@@ -29,6 +29,11 @@ def test_strip_plan_alignment_and_cover():
     H = 1000
     halo = PL.halo_rows(8.0, 3)
     assert halo % PL.TILE == 0 and halo >= 8.0 * (72 ** 0.5)
+    # the library's partition arithmetic (bsf_strip_rows, no GPU needed)
+    from paper_1109_5114_b200 import bsf
+    assert bsf.strip_rows(100, 32, 32, 1, 2) == (64, 100, 32, 100)
+    with pytest.raises(bsf.BsfError):
+        bsf.strip_rows(100, 32, 64, 1, 3)  # a 32-row strip cannot feed its neighbours' 64-row halos
     for world in (1, 2, 4, 8):
         strips = [PL.strip_plan(H, r, world, halo) for r in range(world)]
         assert strips[0].y0 == 0 and strips[-1].y1 == H
@@ -39,18 +44,21 @@ def test_strip_plan_alignment_and_cover():
 
 
 class _StandIn:
-    """Stand-in for a bsf.Plan: 2R+1 box mean with zero extension (reach R)."""
+    """Stand-in for a multi-GPU bsf.Plan without communicator: bsf_run takes
+    the strip's block and writes its own rows only; the filter is a 2R+1 box
+    mean with zero extension (reach R)."""
 
     R = 3
 
-    def __init__(self, height):
-        self.height = height
+    def __init__(self, strip=None):
+        self.strip = strip
 
     def run(self, f, cov, out, stream=None):
         k = 2 * self.R + 1
-        x = f.to(torch.float64)[None, None]
+        x = f.to(torch.float64).reshape(1, 1, f.shape[-2], f.shape[-1])
         w = torch.ones(1, 1, k, k, dtype=torch.float64) / (k * k)
-        out[0] = torch.nn.functional.conv2d(x, w, padding=self.R)[0, 0]
+        y = torch.nn.functional.conv2d(x, w, padding=self.R)[0, 0]
+        out[0] = y[self.strip.out_slice] if self.strip is not None else y
 
 
 def _worker(rank, world, port, H, W, q):
@@ -66,7 +74,7 @@ def _worker(rank, world, port, H, W, q):
         blk = PL.exchange_halos(own, st, H)
         ok_blk = torch.equal(blk, full[st.b0:st.b1])
         cov = torch.ones(3, st.y1 - st.y0, W)
-        res = PL.filter_strip(_StandIn, own, cov, st, H)
+        res = PL.filter_strip(_StandIn(st), own[None], cov, st, H)[0]
         q.put((rank, ok_blk, st.y0, st.y1, res))
     finally:
         dist.destroy_process_group()
@@ -96,7 +104,7 @@ def test_row_strips_reproduce_full_image(world):
     g = torch.Generator().manual_seed(1)
     full = torch.rand(H, W, generator=g, dtype=torch.float64).float()
     ref = torch.empty(1, H, W, dtype=torch.float64)
-    _StandIn(H).run(full, None, ref)
+    _StandIn().run(full, None, ref)
     for rank, ok_blk, y0, y1, res in got:
         assert ok_blk, rank
         assert torch.equal(res, ref[0, y0:y1]), rank
