@@ -41,20 +41,22 @@ def _classify(c, policy, r):
 
 
 def stratified_points(w: synth.Workload, n: int, *, seed: int = 0, frames: int = 1, strip_rows=(), r=None,
-                      policy=None, pool: int = 20000, per_stratum: int = 0):
+                      policy=None, pool: int = 20000, per_stratum: int = 0, rows=None):
     """int32 (m, 3) (image, x, y) with m >= n points and a dict stratum ->
     indices.  `strip_rows`: row-strip boundaries (rows y0 - 1 and y0 are
-    sampled); frames > 1: frame-edge pixels of the first and last frames."""
+    sampled); frames > 1: frame-edge pixels of the first and last frames;
+    rows = (ya, yb): every point in those image rows (a row strip)."""
     r = r or w.order
     policy = w.basis if policy is None else policy
-    H, W = w.height, w.width
+    ya, yb = rows if rows is not None else (0, w.height)
+    H, W = yb - ya, w.width
     rng = np.random.default_rng(1000 + seed)
     k = per_stratum or max(4, n // 10)
     pts, labels = [], {}
 
-    def add(name, img, xs, ys):
+    def add(name, img, xs, ys):  # ys relative to the first row ya
         idx = list(range(len(pts), len(pts) + len(xs)))
-        pts.extend((int(img), int(x), int(y)) for x, y in zip(xs, ys))
+        pts.extend((int(img), int(x), int(y) + ya) for x, y in zip(xs, ys))
         labels.setdefault(name, []).extend(idx)
 
     cx = [0, W - 1, 0, W - 1, W // 2, 0, W - 1, W // 2, W // 2]
@@ -73,7 +75,7 @@ def stratified_points(w: synth.Workload, n: int, *, seed: int = 0, frames: int =
     # method-dependent strata from a uniform candidate pool, classified by the oracle
     px = rng.integers(0, W, pool)
     py = rng.integers(0, H, pool)
-    c = synth.cov_at(w, px, py).numpy().astype(np.float64)
+    c = synth.cov_at(w, px, py + ya).numpy().astype(np.float64)
     clamped, zero, switch = _classify(c, policy, r)
     smaj = np.maximum(c[0], c[1])
     order = np.argsort(smaj)
@@ -85,6 +87,6 @@ def stratified_points(w: synth.Workload, n: int, *, seed: int = 0, frames: int =
     nu = max(0, n - len(pts))
     ui = rng.integers(0, frames, nu) if frames > 1 else np.zeros(nu, int)
     base = len(pts)
-    pts.extend((int(i), int(x), int(y)) for i, x, y in zip(ui, rng.integers(0, W, nu), rng.integers(0, H, nu)))
+    pts.extend((int(i), int(x), int(y) + ya) for i, x, y in zip(ui, rng.integers(0, W, nu), rng.integers(0, H, nu)))
     labels["uniform"] = list(range(base, len(pts)))
     return torch.tensor(pts, dtype=torch.int32), labels
