@@ -22,8 +22,11 @@
 // Included by bsf_kernels.cu after bsf_fused.cuh (uses pixel_scales,
 // ClsTables / cls_region, comp_step, mesh<>, warp_count).
 
-constexpr int GX1_BLOCK = 256;           // threads per block = pixels per tile (32 x 8)
-constexpr int GX1_TW = 32, GX1_TH = 8;
+constexpr int GX1_BLOCK = 256;           // threads per block
+constexpr int GX1_TW = 32, GX1_TH = 32;  // pixel tile
+constexpr int GX1_TILE = GX1_TW * GX1_TH, GX1_PPT = GX1_TILE / GX1_BLOCK;
+constexpr size_t GX1_DYN_SMEM = (size_t)GX1_TILE * (4 * sizeof(double) + sizeof(int) + sizeof(short));
+extern __shared__ __align__(16) unsigned char gx1_dyn[];
 constexpr int GX1_MAXREG = 32;
 constexpr int GX1_SLOTS = 2048;          // window slots of all order-1 tables, padded to 4 (Theta 96, Theta' 1800)
 
@@ -244,40 +247,47 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
     }
     __syncthreads();
     const int ntx = (a.W + GX1_TW - 1) / GX1_TW, nty = (a.H + GX1_TH - 1) / GX1_TH;
-    const long long nunits = a.pts ? ((long long)a.npts + GX1_BLOCK - 1) / GX1_BLOCK : (long long)ntx * nty * a.nimg;
+    const long long nunits = a.pts ? ((long long)a.npts + GX1_TILE - 1) / GX1_TILE : (long long)ntx * nty * a.nimg;
     unsigned long long macs = 0;
-    // per tile: phase A solves every pixel's scales (a1-a4); the pixels are
-    // then ordered by class (basis, zero-scale variant; dead pixels last) with
-    // a counting sort, so that in phase B a warp mostly runs ONE tap program
-    // (same tap count, same tables) -- lanes of mixed classes would execute
-    // both programs one after the other
-    constexpr int NCLS = 2 * NVAR + 1;
-    __shared__ double s_ap[GX1_BLOCK][4];
-    __shared__ int s_info[GX1_BLOCK];  // basis | (drop + 1) << 1 | clamped << 4 | valid << 5 | flags << 8
-    __shared__ short s_order[GX1_BLOCK];
-    __shared__ int s_wcnt[GX1_BLOCK / 32][NCLS];
+    // per tile of GX1_TILE pixels: phase A solves every pixel's scales
+    // (a1-a4, GX1_PPT pixels per thread); a counting sort orders the pixels
+    // by class (basis, zero-scale variant), most expensive class first, dead
+    // pixels last; in phase B the warps take groups of 32 consecutive sorted
+    // pixels from a block counter, so a warp mostly runs ONE tap program (same
+    // tap count, same tables: lanes of mixed classes would run both programs
+    // one after the other) and the expensive groups are handed out first
+    // (the block's warps finish together at the tile barrier)
+    constexpr int NCLS = 2 * NVAR + 1, NPAIR = GX1_PPT * (GX1_BLOCK / 32);
+    static_assert(NPAIR == 32, "one lane per (round, warp) pair in the class scan");
+    double(*s_ap)[4] = reinterpret_cast<double(*)[4]>(gx1_dyn);
+    int *s_info = reinterpret_cast<int *>(s_ap + GX1_TILE);  // basis | (drop+1) << 1 | clamped << 4 | valid << 5 | flags << 8
+    short *s_order = reinterpret_cast<short *>(s_info + GX1_TILE);
+    __shared__ int s_pcnt[NPAIR][NCLS];  // class counts per (round, warp), then exclusive offsets
+    __shared__ int s_next;
     const int lane = tid & 31, warp = tid >> 5;
-    // static grid-stride over 32 x 8 pixel tiles in raster order: the blocks of
+    // static grid-stride over 32 x 32 pixel tiles in raster order: the blocks of
     // a wave read neighbouring rows of the running sums (L2 reuse of the taps)
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int img_t = a.pts ? 0 : (int)(u / ((long long)ntx * nty));
         const int rem_t = a.pts ? 0 : (int)(u % ((long long)ntx * nty));
         const int x0 = (rem_t % ntx) * GX1_TW, y0 = (rem_t / ntx) * GX1_TH;
-        // ---- phase A: this thread's pixel of the tile
-        int cls;
-        {
+        if (tid == 0) s_next = 0;
+        // ---- phase A: pixels tid + GX1_BLOCK k of the tile
+#pragma unroll 1
+        for (int k = 0; k < GX1_PPT; ++k) {
+            const int e = tid + GX1_BLOCK * k;
             int img, x, y;
             bool valid;
             if (a.pts) {
-                const long long i = u * GX1_BLOCK + tid;
+                const long long i = u * GX1_TILE + e;
                 valid = i < a.npts;
                 img = valid ? a.pts[3 * i] : 0;
                 x = valid ? a.pts[3 * i + 1] : 0;
                 y = valid ? a.pts[3 * i + 2] : 0;
             } else {
                 img = img_t;
-                x = x0 + tid % GX1_TW;
-                y = y0 + tid / GX1_TW;
+                x = x0 + e % GX1_TW;
+                y = y0 + e / GX1_TW;
                 valid = x < a.W && out_row(a, y);
             }
             PixelScales ps;
@@ -293,29 +303,56 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
             }
             const bool live = valid && !(ps.flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
 #pragma unroll
-            for (int k = 0; k < 4; ++k) s_ap[tid][k] = ps.ap[k];
-            s_info[tid] = ps.basis | ((ps.drop + 1) << 1) | (ps.clamped << 4) | (valid ? 32 : 0) | (ps.flags << 8);
-            cls = live ? ps.basis * NVAR + ps.drop + 1 : NCLS - 1;
-        }
-        // counting sort by class: per-warp class counts, then every thread
-        // computes its slot from the counts of the classes before its own and
-        // of the same class in earlier warps (stable)
-        const unsigned m = __match_any_sync(0xffffffffu, cls);
-        if (lane < NCLS) s_wcnt[warp][lane] = 0;
-        __syncwarp();
-        if (lane == __ffs(m) - 1) s_wcnt[warp][cls] = __popc(m);
-        __syncthreads();
-        {
-            int pos = __popc(m & ((1u << lane) - 1u));
-            for (int w = 0; w < GX1_BLOCK / 32; ++w)
-                for (int c = 0; c < NCLS; ++c)
-                    pos += (c < cls || (c == cls && w < warp)) ? s_wcnt[w][c] : 0;
-            s_order[pos] = (short)tid;
+            for (int q = 0; q < 4; ++q) s_ap[e][q] = ps.ap[q];
+            s_info[e] = ps.basis | ((ps.drop + 1) << 1) | (ps.clamped << 4) | (valid ? 32 : 0) | (ps.flags << 8);
+            // class rank, most expensive first: Theta' full, Theta full,
+            // Theta' variants, Theta variants, dead
+            const int cls = !live ? NCLS - 1
+                                  : ps.drop < 0 ? (ps.basis == BASIS_THETA_PRIME ? 0 : 1)
+                                                : 2 + (ps.basis == BASIS_THETA_PRIME ? 0 : 4) + ps.drop;
+            const unsigned m = __match_any_sync(0xffffffffu, cls);
+            const int pair = k * (GX1_BLOCK / 32) + warp;
+            if (lane < NCLS) s_pcnt[pair][lane] = 0;
+            __syncwarp();
+            if (lane == __ffs(m) - 1) s_pcnt[pair][cls] = __popc(m);
+            s_order[e] = (short)(cls | (__popc(m & ((1u << lane) - 1u)) << 4));  // class, rank in the warp
         }
         __syncthreads();
-        // ---- phase B: pixel p = s_order[tid] (class-sorted)
-        {
-            const int p = s_order[tid];
+        // exclusive offsets: class bases (in class-rank order) + earlier pairs
+        if (warp == 0) {
+            int run = 0;
+#pragma unroll 1
+            for (int c = 0; c < NCLS; ++c) {
+                const int v = s_pcnt[lane][c];
+                int inc = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += t;
+                }
+                s_pcnt[lane][c] = run + inc - v;
+                run += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+        __syncthreads();
+        short slot[GX1_PPT];
+#pragma unroll
+        for (int k = 0; k < GX1_PPT; ++k) {
+            const int e = tid + GX1_BLOCK * k;
+            const int w = s_order[e];
+            slot[k] = (short)(s_pcnt[k * (GX1_BLOCK / 32) + warp][w & 15] + (w >> 4));
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < GX1_PPT; ++k) s_order[slot[k]] = (short)(tid + GX1_BLOCK * k);
+        __syncthreads();
+        // ---- phase B: groups of 32 sorted pixels from the block counter
+        for (;;) {
+            int grp = 0;
+            if (lane == 0) grp = atomicAdd(&s_next, 1);
+            grp = __shfl_sync(0xffffffffu, grp, 0);
+            if (grp >= GX1_TILE / 32) break;
+            const int p = s_order[32 * grp + lane];
             const int w = s_info[p];
             const bool valid = (w >> 5) & 1;
             PixelScales ps;
@@ -324,11 +361,11 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
             ps.clamped = (w >> 4) & 1;
             ps.flags = w >> 8;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) ps.ap[k] = s_ap[p][k];
+            for (int q = 0; q < 4; ++q) ps.ap[q] = s_ap[p][q];
             int img, x, y;
             long long oidx;
             if (a.pts) {
-                const long long i = u * GX1_BLOCK + p;
+                const long long i = u * GX1_TILE + p;
                 img = valid ? a.pts[3 * i] : 0;
                 x = valid ? a.pts[3 * i + 1] : 0;
                 y = valid ? a.pts[3 * i + 2] : 0;
@@ -344,9 +381,9 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
             double res = __longlong_as_double(0x7ff8000000000000LL), erel = 0.0;
             bool used_dd = false;
             if (live) {
-                // every read stays inside the domain (plus the zero rows above
-                // it) when the pixel's reach is within the plan's margins; else
-                // NaN and BSF_ERANGE (a covariance above the plan's max_sigma)
+                // every read stays inside the domain when the pixel's reach is
+                // within the plan's margins; else NaN and BSF_ERANGE (a
+                // covariance above the plan's max_sigma)
                 double rx = 0.0, ry = 0.0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -395,7 +432,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
                 if (valid && flags) atomicOr(a.stats + 4, (unsigned long long)flags);
             }
         }
-        __syncthreads();  // s_ap / s_info / s_order are rewritten by the next tile
+        __syncthreads();  // s_ap / s_info / s_order / s_next are rewritten by the next tile
     }
     if (a.stats) {
         for (int o = 16; o; o >>= 1) macs += __shfl_xor_sync(0xffffffffu, macs, o);
@@ -407,15 +444,19 @@ int gx1_slots() {
     int dev = 0, sms = 148, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gx1_kernel, GX1_BLOCK, 0) != cudaSuccess || per < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gx1_kernel, GX1_BLOCK, GX1_DYN_SMEM) != cudaSuccess ||
+        per < 1)
         per = 1;
     return sms * per;
 }
 
 cudaError_t launch_gx1(const TileArgs &a, cudaStream_t st, const LutBasis *luts, long long *nl) {
+    static std::atomic<unsigned long long> attr{0ull};
+    cudaError_t e = set_smem_attr(gx1_kernel, (int)GX1_DYN_SMEM, attr);
+    if (e != cudaSuccess) return e;
     static int slots = 0;
     if (!slots) slots = gx1_slots();
-    gx1_kernel<<<slots, GX1_BLOCK, 0, st>>>(a, luts);
+    gx1_kernel<<<slots, GX1_BLOCK, GX1_DYN_SMEM, st>>>(a, luts);
     ++*nl;
     return cudaGetLastError();
 }
