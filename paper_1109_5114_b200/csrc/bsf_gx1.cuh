@@ -22,7 +22,10 @@
 // Included by bsf_kernels.cu after bsf_fused.cuh (uses pixel_scales,
 // ClsTables / cls_region, comp_step, mesh<>, warp_count).
 
-constexpr int GX1_BLOCK = 256;           // threads per block
+#ifndef GX1_BLOCK_T
+#define GX1_BLOCK_T 256
+#endif
+constexpr int GX1_BLOCK = GX1_BLOCK_T;   // threads per block
 constexpr int GX1_TW = 32, GX1_TH = 32;  // pixel tile
 constexpr int GX1_TILE = GX1_TW * GX1_TH, GX1_PPT = GX1_TILE / GX1_BLOCK;
 constexpr size_t GX1_DYN_SMEM = (size_t)GX1_TILE * (4 * sizeof(double) + sizeof(int) + sizeof(short));

@@ -82,3 +82,107 @@ def test_table2_isotropic_columns_algorithm1(s):
     h, L = (0.02, 6.0) if s < 2 else (0.1, 22.0)
     e0, e1, _ = _errors(s, 1.0, 0.0, h=h, L=L)
     assert round(e0, 1) == 10.8 and round(e1, 1) == 4.9, (e0, e1)
+
+
+# ----------------------------------------------------------------------------
+# Tables 3 and 4 and the remaining Table 2 columns,
+# recomputed with the oracle in the continuous protocol (tools/accuracy_tables.py
+# wrote tests/golden/accuracy_tables_recomputed.json calling only oracle/)
+# ----------------------------------------------------------------------------
+import json  # noqa: E402
+import os  # noqa: E402
+import sys  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+
+
+def _golden_rows(name):
+    rows = []
+    for line in open(os.path.join(GOLD, name)):
+        line = line.strip()
+        if line and not line.startswith("#"):
+            rows.append(line.split())
+    return rows
+
+
+def _recomputed():
+    return json.load(open(os.path.join(GOLD, "accuracy_tables_recomputed.json")))
+
+
+def test_table3_sigma_fraction_sweep():
+    """Table 3 in the continuous protocol, reading sigma^2 =
+    fraction x bound (9) (R21): Algorithm 1 improves at every fraction, the
+    improvement rises to a maximum in the 50-70 % range and decreases after it,
+    with the 50 % value within one point of the maximum -- the paper's claim
+    "the best results are obtained when sigma^2 is roughly 50 % of the bound"
+    (PAPER.md:483-487).  The paper's values are lower at small fractions
+    (3.5 vs ~16 % at 10 %): its protocol is not stated beyond "numerical
+    integration" (its Table 2 columns (1,4,0) and (5,4,0) differ although the
+    continuous error is scale-invariant), so the values are not pinned; the
+    recomputation is (regression against the stored oracle run)."""
+    import accuracy_tables as T
+    e0, e1, basis = T.errors(5.0, 3.0, math.pi / 4, fracs=T.TABLE3_FRACS)
+    imp = [100 * (e0 - e) / e0 for e in e1]
+    paper = [float(v) for _, v in _golden_rows("table3_sigma_fraction.txt")]
+    print("Table 3 improvement %:", ["%.1f" % v for v in imp], "paper:", paper)
+    assert all(v > 0 for v in imp)
+    k = int(np.argmax(imp))
+    assert 0.5 <= T.TABLE3_FRACS[k] <= 0.7
+    assert all(imp[i] < imp[i + 1] for i in range(k))
+    assert all(imp[i] > imp[i + 1] for i in range(k, len(imp) - 1))
+    assert imp[4] >= imp[k] - 1.0
+    assert max(paper) == paper[4]  # the paper's maximum is at 50 %
+    stored = _recomputed()["table3"]["improvement"]
+    np.testing.assert_allclose(imp, stored, atol=0.06)
+
+
+def test_table4_new_bound_row():
+    """Table 4's new-bound row recomputed exactly (R7): the dual
+    bound max(rho_Theta, rho_Theta') at each orientation.  It agrees where the
+    Theta bound wins (0, 5, 40, 45 deg: inf, 13.6, 13.6, inf), is unbounded on
+    Theta''s axis (atan 1/2 = 26.565 deg), and at 25 deg (29.05 vs 30.1); the
+    paper's empirical values at 13.3-22.5 deg and 30 deg are not those of the
+    P:413-416 covariance (B.4: 6.85 / 8.23 / 12.20 / 25.23 vs 8.2 / 9.5 / 10.8 /
+    28.8), and its minimum is 6.171 at 16.85 deg (pinned in
+    test_oracle_pins.test_dual_sector_switch_angles), not 8.2 at 13.3 deg."""
+    paper = {float(d): (math.inf if v == "inf" else float(v)) for d, v in _golden_rows("table4_new_bound.txt")}
+    ours = {}
+    for d in paper:
+        phi = math.radians(26.565051177 if d == 26.6 else d)
+        ours[d] = max(O.bound_rho(O.THETA, phi), O.bound_rho(O.THETA_PRIME, phi))
+    print("Table 4 new bound:", {d: "%.2f / %s" % (ours[d], paper[d]) for d in paper})
+    for d in (0.0, 45.0, 26.6):
+        assert ours[d] > 1e6 and math.isinf(paper[d])
+    for d in (5.0, 40.0):
+        assert round(ours[d], 1) == paper[d]
+    assert abs(ours[25.0] - paper[25.0]) / paper[25.0] < 0.05
+    for d in (20.0, 22.5, 25.0, 30.0):  # Theta' lifts the Theta bound there, as the paper says
+        assert ours[d] > O.bound_rho(O.THETA, math.radians(d)) + 2
+    stored = {r["deg"]: r["dual"] for r in _recomputed()["table4_new_bound"]}
+    for d, v in stored.items():
+        if v is not None and d != 26.6:
+            assert round(ours[d], 2) == v
+
+
+def test_table2_all_columns_recomputed():
+    """Every column of Table 2 under the stated readings
+    (s = sigma_major, rho = eigenvalue ratio, Algorithm 2's basis): Algorithm 1
+    improves every column, the isotropic ones by 54.8 % (10.8 -> 4.9, pinned in
+    test_oracle_pins), (5,4,0) matches the paper (pinned above); (1,4,0) equals
+    (5,4,0) (the continuous error is scale-invariant; the paper's 19.1 -> 15.3
+    differs from its own 18.7 -> 14.6 by its discretisation); the other three
+    anisotropic columns are not reproduced under any reading tried (basis Theta
+    or dual, rho as sigma or eigenvalue ratio: DESIGN.md R23) -- their stored
+    oracle values are a regression pin only."""
+    rec = _recomputed()["table2"]
+    for r in rec:
+        assert r["alg1"] < r["plain"], r
+    iso = [r for r in rec if r["rho"] == 1]
+    assert all(round(r["plain"], 1) == 10.8 and round(r["alg1"], 1) == 4.9 for r in iso)
+    by = {(r["s"], r["rho"]): r for r in rec if r["theta"] == 0.0}
+    assert abs(by[(1, 4)]["plain"] - by[(5, 4)]["plain"]) < 0.05 and abs(by[(1, 4)]["alg1"] - by[(5, 4)]["alg1"]) < 0.1
+    # spot-recompute one anisotropic column from the oracle
+    e0, e1, b = _errors(5.0, 5.0, math.pi / 2)
+    r = [x for x in rec if x["rho"] == 5][0]
+    assert abs(e0 - r["plain"]) < 0.01 and abs(e1 - r["alg1"]) < 0.01
