@@ -6,12 +6,17 @@
  *
  *   out(p) = sum_q f(q) beta^{(r)}_{a(p)}(p - q)
  *
- * computed the paper's way: one global pre-integration of the image (running
- * sums along the four grid directions of the box spline, each repeated r
- * times; Alg. 3 step 2 PAPER.md:395-399) followed
- * by a per-pixel local finite difference (the (r+1)^4-tap mesh of Table 1,
- * PAPER.md:355-373, shifts of Eq. (10)) whose taps are read
- * from the running sum with the interpolation of Eq. (11).
+ * computed by pre-integration (running sums along the four grid directions of
+ * the box spline, each repeated r times; Alg. 3
+ * step 2 PAPER.md:395-399) followed by a per-pixel local finite difference
+ * (the (r+1)^4-tap mesh of Table 1, shifts of Eq. (10),
+ * PAPER.md:339-342) whose taps are read from the running sums with the
+ * interpolation of Eq. (11).  Where the running sums start
+ * is the plan's anchoring (bsf_anchor): the paper's ONE global
+ * pre-integration of the image (exact int64 at order 1 on u8 images, the
+ * "global mode"; double-double otherwise), or sums restarted per output
+ * super-tile on its halo (the same filter up to rounding, R18) at
+ * orders where exact global sums would overflow.
  * The per-pixel scales a(p) come from the pixel's covariance (sigma_x,
  * sigma_y, theta) by the minimum-kurtosis rule on
  * C(p)/r (Prop. 1); basis Theta, Theta' or the per-pixel

@@ -1,3 +1,4 @@
-for v in "" tools/libbsf_b.so tools/libbsf_e.so tools/libbsf_f.so; do
+BSF_LIB=tools/libbsf_pair.so timeout 900 python -m pytest tests/test_gpu_global.py -q -x 2>&1 | tail -2
+for v in "" tools/libbsf_pair.so; do
   echo "lib=$v"; BSF_LIB=$v timeout 300 python tools/fused_probe.py --config 3 --width 4096 --height 4096 --order 1 --reps 10 --anchor global
 done
