@@ -26,7 +26,10 @@
 #define GX1_BLOCK_T 256
 #endif
 constexpr int GX1_BLOCK = GX1_BLOCK_T;   // threads per block
-constexpr int GX1_TW = 32, GX1_TH = 32;  // pixel tile
+#ifndef GX1_TH_T
+#define GX1_TH_T 32
+#endif
+constexpr int GX1_TW = 32, GX1_TH = GX1_TH_T;  // pixel tile
 constexpr int GX1_TILE = GX1_TW * GX1_TH, GX1_PPT = GX1_TILE / GX1_BLOCK;
 constexpr size_t GX1_DYN_SMEM = (size_t)GX1_TILE * (4 * sizeof(double) + sizeof(int) + sizeof(short));
 extern __shared__ __align__(16) unsigned char gx1_dyn[];
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
     // one after the other) and the expensive groups are handed out first
     // (the block's warps finish together at the tile barrier)
     constexpr int NCLS = 2 * NVAR + 1, NPAIR = GX1_PPT * (GX1_BLOCK / 32);
-    static_assert(NPAIR == 32, "one lane per (round, warp) pair in the class scan");
+    static_assert(NPAIR <= 32, "one lane per (round, warp) pair in the class scan");
     double(*s_ap)[4] = reinterpret_cast<double(*)[4]>(gx1_dyn);
     int *s_info = reinterpret_cast<int *>(s_ap + GX1_TILE);  // basis | (drop+1) << 1 | clamped << 4 | valid << 5 | flags << 8
     short *s_order = reinterpret_cast<short *>(s_info + GX1_TILE);
@@ -326,14 +329,14 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
             int run = 0;
 #pragma unroll 1
             for (int c = 0; c < NCLS; ++c) {
-                const int v = s_pcnt[lane][c];
+                const int v = lane < NPAIR ? s_pcnt[lane][c] : 0;
                 int inc = v;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int t = __shfl_up_sync(0xffffffffu, inc, o);
                     if (lane >= o) inc += t;
                 }
-                s_pcnt[lane][c] = run + inc - v;
+                if (lane < NPAIR) s_pcnt[lane][c] = run + inc - v;
                 run += __shfl_sync(0xffffffffu, inc, 31);
             }
         }

@@ -1,4 +1,4 @@
-BSF_LIB=tools/libbsf_pair.so timeout 900 python -m pytest tests/test_gpu_global.py -q -x 2>&1 | tail -2
-for v in "" tools/libbsf_pair.so; do
+BSF_LIB=tools/libbsf_tha.so timeout 900 python -m pytest tests/test_gpu_global.py -q -x 2>&1 | tail -2
+for v in tools/libbsf_tha.so tools/libbsf_thb.so; do
   echo "lib=$v"; BSF_LIB=$v timeout 300 python tools/fused_probe.py --config 3 --width 4096 --height 4096 --order 1 --reps 10 --anchor global
 done
