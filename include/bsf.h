@@ -182,6 +182,14 @@ typedef struct {
  * span two neighbours).                                                      */
 bsf_status bsf_strip_rows(int height, int unit, int halo, int rank, int nranks, int *y0, int *y1, int *b0, int *b1);
 
+/* The halo exchange of a row strip (what bsf_run sends and receives per image
+ * on a multi-GPU plan), pure host arithmetic: x[0], x[1] = first own row and
+ * row count sent to rank - 1; x[2] = rows received from it into block rows
+ * [0, x[2]); x[3], x[4] = first own row and row count sent to rank + 1;
+ * x[5], x[6] = first block row and row count received from it; x[7] = the
+ * block row of the first own row.  Zeros where there is no neighbour.       */
+bsf_status bsf_strip_exchange(int height, int unit, int halo, int rank, int nranks, int *x8);
+
 /* NCCL unique id for a multi-GPU plan (call on rank 0, broadcast the 128
  * bytes to every rank).  BSF_ENCCL when NCCL cannot be loaded.               */
 bsf_status bsf_get_unique_id(void *id_out128);

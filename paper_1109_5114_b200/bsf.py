@@ -122,6 +122,8 @@ def lib():
         L.bsf_version.restype = i
         L.bsf_strip_rows.restype = st
         L.bsf_strip_rows.argtypes = [i, i, i, i, i] + [ctypes.POINTER(i)] * 4
+        L.bsf_strip_exchange.restype = st
+        L.bsf_strip_exchange.argtypes = [i, i, i, i, i, ctypes.POINTER(i)]
         L.bsf_get_unique_id.restype = st
         L.bsf_get_unique_id.argtypes = [vp]
         _lib = L
@@ -396,6 +398,13 @@ def strip_rows(height, unit, halo, rank, nranks):
     v = [ctypes.c_int() for _ in range(4)]
     _check(lib().bsf_strip_rows(int(height), int(unit), int(halo), int(rank), int(nranks), *[ctypes.byref(x) for x in v]))
     return tuple(x.value for x in v)
+
+
+def strip_exchange(height, unit, halo, rank, nranks):
+    """bsf_strip_exchange: the 8 row counts / offsets of a strip's halo exchange."""
+    x = (ctypes.c_int * 8)()
+    _check(lib().bsf_strip_exchange(int(height), int(unit), int(halo), int(rank), int(nranks), x))
+    return list(x)
 
 
 def get_unique_id() -> bytes:

@@ -628,6 +628,29 @@ extern "C" bsf_status bsf_strip_rows(int H, int unit, int halo, int rank, int nr
     return BSF_OK;
 }
 
+extern "C" bsf_status bsf_strip_exchange(int H, int unit, int halo, int rank, int nranks, int *x) {
+    if (!x) return set_err(BSF_EINVAL, "null argument");
+    int y0, y1, b0, b1;
+    bsf_status s = bsf_strip_rows(H, unit, halo, rank, nranks, &y0, &y1, &b0, &b1);
+    if (s != BSF_OK) return s;
+    const int own = y1 - y0, top = y0 - b0, bot = b1 - y1;
+    for (int i = 0; i < 8; ++i) x[i] = 0;
+    if (rank > 0) {
+        x[0] = 0;                                // rank - 1's bottom halo = my first rows
+        x[1] = std::min(std::min(halo, H - y0), own);
+        x[2] = top;                              // my block rows [0, top) = rank - 1's last rows
+    }
+    if (rank < nranks - 1) {
+        const int dn = std::min(std::min(halo, y1), own);  // rank + 1's top halo = my last rows
+        x[3] = own - dn;
+        x[4] = dn;
+        x[5] = top + own;                        // my block rows [top + own, top + own + bot)
+        x[6] = bot;
+    }
+    x[7] = top;                                  // block row of my first own row
+    return BSF_OK;
+}
+
 extern "C" bsf_status bsf_get_unique_id(void *id_out) {
     if (!id_out) return set_err(BSF_EINVAL, "null argument");
     NcclApi &nc = nccl_api();
@@ -1094,23 +1117,22 @@ static bsf_status run_strip(bsf_plan_s *p, const void *f, const void *cov, void 
         for (int i = 0; i < nimg; ++i)
             CUDA_TRY(cudaMemcpyAsync(B + ((size_t)i * blk + top) * row, F + (size_t)i * own * row, (size_t)own * row,
                                      cudaMemcpyDeviceToDevice, st));
+        int x[8];
+        bsf_status xs = bsf_strip_exchange(p->geo.H, p->stile, p->halo, p->d.rank, p->d.nranks, x);
+        if (xs != BSF_OK) return xs;
         NcclApi &nc = nccl_api();
         const ncclDataType_t dt = p->d.in_dtype == BSF_U8 ? ncclUint8 : ncclFloat32;
         NCCL_TRY(nc.groupStart());
         for (int i = 0; i < nimg; ++i) {
             const char *Fi = F + (size_t)i * own * row;
             char *Bi = B + (size_t)i * blk * row;
-            if (p->d.rank > 0) {  // rows [b0, y0) from rank - 1; it needs my first rows
-                const int up = std::min(p->halo, p->geo.H - p->y0) - 0;
-                const int need_up = std::min(up, own);  // rank - 1's bottom halo (<= own, checked at plan time)
-                NCCL_TRY(nc.send(Fi, (size_t)need_up * W, dt, p->d.rank - 1, p->comm, st));
-                NCCL_TRY(nc.recv(Bi, (size_t)top * W, dt, p->d.rank - 1, p->comm, st));
+            if (p->d.rank > 0) {  // my first rows to rank - 1, block rows [0, top) from it
+                NCCL_TRY(nc.send(Fi + (size_t)x[0] * row, (size_t)x[1] * W, dt, p->d.rank - 1, p->comm, st));
+                NCCL_TRY(nc.recv(Bi, (size_t)x[2] * W, dt, p->d.rank - 1, p->comm, st));
             }
-            if (p->d.rank < p->d.nranks - 1) {  // rows [y1, b1) from rank + 1; it needs my last rows
-                const int need_dn = std::min(std::min(p->halo, p->y1), own);
-                NCCL_TRY(nc.send(Fi + (size_t)(own - need_dn) * row, (size_t)need_dn * W, dt, p->d.rank + 1, p->comm,
-                                 st));
-                NCCL_TRY(nc.recv(Bi + (size_t)(top + own) * row, (size_t)bot * W, dt, p->d.rank + 1, p->comm, st));
+            if (p->d.rank < p->d.nranks - 1) {  // my last rows to rank + 1, block rows [top + own, blk) from it
+                NCCL_TRY(nc.send(Fi + (size_t)x[3] * row, (size_t)x[4] * W, dt, p->d.rank + 1, p->comm, st));
+                NCCL_TRY(nc.recv(Bi + (size_t)x[5] * row, (size_t)x[6] * W, dt, p->d.rank + 1, p->comm, st));
             }
         }
         NCCL_TRY(nc.groupEnd());

@@ -191,3 +191,36 @@ def test_global_mode_carry_chain_gloo():
     assert res[0][1] == 0 and res[-1][2] == H + Pb
     for rank, Y0, Y1, g in res:
         assert torch.equal(g, ref[Y0:Y1]), "rank %d rows [%d, %d) differ" % (rank, Y0, Y1)
+
+
+@pytest.mark.parametrize("H,unit,halo", [(1000, 32, 96), (4096, 64, 128), (352, 32, 32), (777, 16, 48)])
+@pytest.mark.parametrize("world", [2, 3, 4, 5, 8])
+def test_library_halo_exchange_plan_assembles_every_block(H, unit, halo, world):
+    """The row counts bsf_run sends and receives over NCCL (bsf_strip_exchange,
+    the library's own arithmetic, no GPU needed) are consistent between
+    neighbours and, replayed on a host image, assemble every rank's block
+    rows [b0, b1) exactly."""
+    import numpy as np
+    from paper_1109_5114_b200 import bsf
+    try:
+        strips = [bsf.strip_rows(H, unit, halo, r, world) for r in range(world)]
+    except bsf.BsfError:
+        pytest.skip("strips thinner than the halo: the library refuses this partition")
+    img = np.arange(H)[:, None] * 1000 + np.arange(7)[None, :]
+    xs = [bsf.strip_exchange(H, unit, halo, r, world) for r in range(world)]
+    for r, ((y0, y1, b0, b1), x) in enumerate(zip(strips, xs)):
+        own = img[y0:y1]
+        blk = np.full((b1 - b0, 7), -1)
+        blk[x[7]:x[7] + (y1 - y0)] = own
+        if r > 0:
+            yp0, yp1, _, _ = strips[r - 1]
+            xp = xs[r - 1]
+            assert xp[6] == x[1] and xp[4] == x[2]  # what each side sends is what the other receives
+            prev_own = img[yp0:yp1]
+            blk[0:x[2]] = prev_own[xp[3]:xp[3] + xp[4]]
+        if r < world - 1:
+            yn0, yn1, _, _ = strips[r + 1]
+            xn = xs[r + 1]
+            nxt_own = img[yn0:yn1]
+            blk[x[5]:x[5] + x[6]] = nxt_own[xn[0]:xn[0] + xn[1]]
+        assert np.array_equal(blk, img[b0:b1]), r
