@@ -78,6 +78,8 @@ static bsf_status set_err(bsf_status s, const std::string &msg) {
             return set_err(BSF_ECUDA, std::string(#expr ": ") + cudaGetErrorString(e_));      \
     } while (0)
 
+constexpr int BSF_HOST_BANDS = 8;  // bsf_run_host (global mode): row bands of the copy / compute pipeline
+
 struct bsf_plan_s {
     bsf_plan_desc d;
     Geometry geo;
@@ -110,6 +112,9 @@ struct bsf_plan_s {
     long long nlaunch = 0;
     cudaStream_t last = nullptr;
     bool fused_ready = false;            // fused-path buffers (fbuf, sbuf, counter, order) allocated
+    cudaStream_t s_in = nullptr, s_out = nullptr;  // bsf_run_host pipeline (global mode): copy streams
+    cudaStream_t s_c2 = nullptr;                   // second compute stream (odd bands fill the even bands' tails)
+    cudaEvent_t ev[2 * BSF_HOST_BANDS + 5] = {};
     bool scratch_ready = false;          // tile-anchored halo scratch allocated
     // global mode (order 1, u8 input): the exact int64 running
     // sums of the whole image, read by the fused kernel's taps
@@ -665,6 +670,16 @@ extern "C" bsf_status bsf_plan_destroy(bsf_plan_t p) {
     if (!p) return BSF_OK;
     DevGuard guard(p->d.device);
     if (p->comm) nccl_api().commDestroy(p->comm);
+    if (p->s_in) {
+        cudaStreamSynchronize(p->s_in);
+        cudaStreamSynchronize(p->s_out);
+        cudaStreamSynchronize(p->s_c2);
+        cudaStreamDestroy(p->s_in);
+        cudaStreamDestroy(p->s_out);
+        cudaStreamDestroy(p->s_c2);
+        for (cudaEvent_t e : p->ev)
+            if (e) cudaEventDestroy(e);
+    }
     for (void *q : p->dev_allocs) cudaFree(q);
     delete p;
     return BSF_OK;
@@ -1017,6 +1032,29 @@ static bsf_status filter_global(bsf_plan_s *p, const void *g, const void *cov, v
     return BSF_OK;
 }
 
+// the order-1 gather on output rows [y0, y0 + h) only (cov and out hold those
+// rows: [batch][3][h][W] and [nimg][h][W]); y0 a multiple of 32
+static bsf_status filter_global_window(bsf_plan_s *p, const void *g, const void *cov, void *out, int y0, int h,
+                                       cudaStream_t st) {
+    bsf_status s = ensure_tile_ws(p, false);
+    if (s != BSF_OK) return s;
+    const Geometry &geo = p->geo;
+    const size_t slot = (size_t)geo.nimg * geo.GH * geo.GW;
+    TileArgs a = tile_args(p, nullptr, cov, out);
+    a.order = nullptr;
+    a.gP = geo.P;
+    a.gGW = geo.GW;
+    a.gGH = geo.GH;
+    a.oy0 = y0;
+    a.oH = h;
+    for (int sl = 0; sl < geo.nbases; ++sl) {
+        a.gglob[p->bases[sl]] = (const long long *)g + sl * slot;
+        a.gshift[p->bases[sl]] = p->gshift[p->bases[sl]];
+    }
+    CUDA_TRY(launch_gx1(a, st, p->luts_dev, &p->nlaunch));
+    return BSF_OK;
+}
+
 static bsf_status run_global(bsf_plan_s *p, const void *f, const void *cov, void *out, const int *pts, int npts,
                              double *aux, cudaStream_t st) {
     if (!p->gx_ws) {
@@ -1101,7 +1139,7 @@ static bsf_status run_strip(bsf_plan_s *p, const void *f, const void *cov, void 
     if (!p->fused) return set_err(BSF_EUNSUPPORTED, "row strips need the exact split path (order <= 3)");
     p->last = st;
     const int W = p->geo.W, nimg = p->geo.nimg;
-    const int own = p->y1 - p->y0, blk = p->b1 - p->b0, top = p->y0 - p->b0, bot = p->b1 - p->y1;
+    const int own = p->y1 - p->y0, blk = p->b1 - p->b0, top = p->y0 - p->b0;
     const size_t es = p->d.in_dtype == BSF_U8 ? 1 : 4;
     const void *fb = f;
     if (p->comm) {
@@ -1303,6 +1341,85 @@ extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov,
     return bsf_run_split(p, f, cov, out, 2, 0.5, sigma2_out, stream);
 }
 
+// Global mode from host buffers: the copies overlap the compute.  The image
+// goes first (the pre-integration needs all of it), then the covariance in
+// row bands on a copy-in stream while the scans run; the gather runs band by
+// band as each band's covariance lands (its output row window), and each
+// finished band of the output goes back on a copy-out stream (the H2D and
+// D2H engines work in parallel).  The caller's stream waits for the last copy.
+static bsf_status run_host_global(bsf_plan_s *p, const void *f_host, const void *cov_host, void *out_host,
+                                  cudaStream_t st) {
+    const Geometry &g = p->geo;
+    const int nb = BSF_HOST_BANDS;
+    if (!p->s_in) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&p->s_c2, cudaStreamNonBlocking));
+        for (int i = 0; i < 2 * BSF_HOST_BANDS + 5; ++i)
+            CUDA_TRY(cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming));
+    }
+    cudaEvent_t ev_start = p->ev[0], ev_f = p->ev[1], ev_end = p->ev[2], ev_pre = p->ev[3], ev_c2 = p->ev[4];
+    cudaEvent_t *ev_cov = p->ev + 5, *ev_band = p->ev + 5 + BSF_HOST_BANDS;
+    p->last = st;
+    const size_t plane = (size_t)g.H * g.W, fes = p->d.in_dtype == BSF_U8 ? 1 : 4,
+                 oes = p->d.out_dtype == BSF_F32 ? 4 : 8;
+    // bands of whole gather tiles (rows multiple of 32)
+    const int rows = ((g.H + nb - 1) / nb + 31) / 32 * 32;
+    CUDA_TRY(cudaEventRecord(ev_start, st));  // earlier work on the caller's stream comes first
+    CUDA_TRY(cudaStreamWaitEvent(p->s_in, ev_start, 0));
+    CUDA_TRY(cudaMemcpyAsync(p->f_stage, f_host, (size_t)g.nimg * plane * fes, cudaMemcpyHostToDevice, p->s_in));
+    CUDA_TRY(cudaEventRecord(ev_f, p->s_in));
+    int nband = 0;
+    for (int y0 = 0; y0 < g.H; y0 += rows, ++nband) {
+        const int h = std::min(rows, g.H - y0);
+        // the band's covariance as planes [batch][3][h][W], stored contiguously at
+        // float offset batch 3 y0 W of cov_stage (the bands tile the buffer)
+        float *cb = (float *)p->cov_stage + (size_t)p->d.batch * 3 * (size_t)y0 * g.W;
+        for (int b = 0; b < p->d.batch; ++b)
+            for (int c = 0; c < 3; ++c)
+                CUDA_TRY(cudaMemcpyAsync(cb + ((size_t)b * 3 + c) * (size_t)h * g.W,
+                                         (const float *)cov_host + ((size_t)b * 3 + c) * plane + (size_t)y0 * g.W,
+                                         (size_t)h * g.W * sizeof(float), cudaMemcpyHostToDevice, p->s_in));
+        CUDA_TRY(cudaEventRecord(ev_cov[nband], p->s_in));
+    }
+    // pre-integration on the caller's stream once the image is in
+    CUDA_TRY(cudaStreamWaitEvent(st, ev_f, 0));
+    const size_t slot = (size_t)g.nimg * g.GH * g.GW;
+    if (!p->gx_ws) {
+        void *q;
+        const size_t bytes = g_bytes(p) / 2;
+        if (cudaMalloc(&q, bytes) != cudaSuccess) return set_err(BSF_ENOMEM, "global int64 sums " + std::to_string(bytes));
+        p->dev_allocs.push_back(q);
+        p->gx_ws = (long long *)q;
+    }
+    for (int b = 0; b < g.nbases; ++b)
+        CUDA_TRY(launch_preint_i64((const uint8_t *)p->f_stage, (unsigned long long *)p->gx_ws + b * slot, g,
+                                   p->bases[b], p->d.order, st, &p->nlaunch));
+    CUDA_TRY(cudaEventRecord(ev_pre, st));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_c2, ev_pre, 0));
+    int band = 0;
+    for (int y0 = 0; y0 < g.H; y0 += rows, ++band) {
+        const int h = std::min(rows, g.H - y0);
+        cudaStream_t sc = (band & 1) ? p->s_c2 : st;  // alternate: a band's blocks fill the previous band's tail
+        CUDA_TRY(cudaStreamWaitEvent(sc, ev_cov[band], 0));
+        const size_t obase = (size_t)g.nimg * (size_t)y0 * g.W;  // band output: [nimg][h][W] at nimg y0 W
+        bsf_status s = filter_global_window(p, p->gx_ws, (const float *)p->cov_stage + (size_t)p->d.batch * 3 * y0 * g.W,
+                                            (char *)p->out_stage + obase * oes, y0, h, sc);
+        if (s != BSF_OK) return s;
+        CUDA_TRY(cudaEventRecord(ev_band[band], sc));
+        CUDA_TRY(cudaStreamWaitEvent(p->s_out, ev_band[band], 0));
+        for (int i = 0; i < g.nimg; ++i)
+            CUDA_TRY(cudaMemcpyAsync((char *)out_host + ((size_t)i * plane + (size_t)y0 * g.W) * oes,
+                                     (char *)p->out_stage + (obase + (size_t)i * h * g.W) * oes, (size_t)h * g.W * oes,
+                                     cudaMemcpyDeviceToHost, p->s_out));
+    }
+    CUDA_TRY(cudaEventRecord(ev_c2, p->s_c2));
+    CUDA_TRY(cudaStreamWaitEvent(st, ev_c2, 0));
+    CUDA_TRY(cudaEventRecord(ev_end, p->s_out));
+    CUDA_TRY(cudaStreamWaitEvent(st, ev_end, 0));
+    return BSF_OK;
+}
+
 extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void *cov_host, void *out_host,
                                    void *stream) {
     if (!p || !f_host || !cov_host || !out_host) return set_err(BSF_EINVAL, "null argument");
@@ -1325,6 +1442,7 @@ extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void 
         p->out_stage = c;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    if (global_exact(p)) return run_host_global(p, f_host, cov_host, out_host, st);
     CUDA_TRY(cudaMemcpyAsync(p->f_stage, f_host, fb, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(p->cov_stage, cov_host, cb, cudaMemcpyHostToDevice, st));
     bsf_status s = bsf_run(p, p->f_stage, p->cov_stage, p->out_stage, stream);

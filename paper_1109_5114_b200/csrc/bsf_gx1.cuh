@@ -252,7 +252,10 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
         base += nreg * nmax4;
     }
     __syncthreads();
-    const int ntx = (a.W + GX1_TW - 1) / GX1_TW, nty = (a.H + GX1_TH - 1) / GX1_TH;
+    // tiles of the output row window (a band of rows, bsf_run_host's pipeline;
+    // all rows when oH = 0); the window starts on a multiple of GX1_TH
+    const int ty0 = a.oy0 / GX1_TH;
+    const int ntx = (a.W + GX1_TW - 1) / GX1_TW, nty = (min(a.H, a.oy0 + out_rows(a)) + GX1_TH - 1) / GX1_TH - ty0;
     const long long nunits = a.pts ? ((long long)a.npts + GX1_TILE - 1) / GX1_TILE : (long long)ntx * nty * a.nimg;
     unsigned long long macs = 0;
     // per tile of GX1_TILE pixels: phase A solves every pixel's scales
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
     for (long long u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int img_t = a.pts ? 0 : (int)(u / ((long long)ntx * nty));
         const int rem_t = a.pts ? 0 : (int)(u % ((long long)ntx * nty));
-        const int x0 = (rem_t % ntx) * GX1_TW, y0 = (rem_t / ntx) * GX1_TH;
+        const int x0 = (rem_t % ntx) * GX1_TW, y0 = (ty0 + rem_t / ntx) * GX1_TH;
         if (tid == 0) s_next = 0;
         // ---- phase A: pixels tid + GX1_BLOCK k of the tile
 #pragma unroll 1

@@ -109,3 +109,30 @@ def test_filter_exact_is_run_split_in_two_calls():
     tp = make_plan(w, anchor=bsf.BSF_ANCHOR_TILE)
     with pytest.raises(bsf.BsfError):
         tp.filter_exact(g, cov.to(dev).contiguous(), out)
+
+
+@pytest.mark.parametrize("out_f32", [False, True])
+def test_run_host_pipeline_global_mode(out_f32):
+    """bsf_run_host in global mode overlaps the copies with the compute (image,
+    then covariance row bands on a copy-in stream; the gather band by band;
+    output bands back on a copy-out stream): bit-identical to the device run,
+    with 2 covariance fields x 2 channels and uneven bands (H = 301)."""
+    W, H = 230, 301
+    w = synth.workload(3, width=W, height=H, extra={"grid_span": 1500})
+    img = torch.stack([synth.make_image(w, frame=f, channel=c) for f in range(2) for c in range(2)])
+    cov = torch.stack([synth.make_cov(w), synth.make_cov(w, window=(0, H, 1, W + 1))]).contiguous()
+    plan = bsf.Plan(W, H, batch=2, channels=2, in_dtype=bsf.BSF_U8, out_dtype=bsf.BSF_F32 if out_f32 else bsf.BSF_F64,
+                    order=1, basis=2, max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_AUTO)
+    assert plan.geometry.global_mode == 1
+    dt = torch.float32 if out_f32 else torch.float64
+    dev = gpu_full(plan, img, cov, out_dtype=dt)
+    f_h = img.contiguous().pin_memory()
+    c_h = cov.contiguous().pin_memory()
+    o_h = torch.full((4, H, W), float("nan"), dtype=dt).pin_memory()
+    plan.run_host(f_h, c_h, o_h)
+    torch.cuda.synchronize()
+    assert torch.equal(o_h, dev)
+    for _ in range(2):  # repeated calls reuse the streams and events
+        plan.run_host(f_h, c_h, o_h)
+    torch.cuda.synchronize()
+    assert torch.equal(o_h, dev)
