@@ -169,21 +169,60 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
     const int wymin = S.ext[b].z;
     const int ntap = 1 << ns;
     double h0 = 0.0, e0 = 0.0, sumF = 0.0;
-    for (int t = 0; t < ntap; ++t) {
-        double Dx = cx, Dy = cy;
-        int sgn = 1;
+    // taps in Gray-code order: consecutive taps differ in one digit j_q, so
+    // the displacement D and the knot-line coordinates U_m = n_m . D move by
+    // one exact step (R17: every value on the 2^-41 grid, |n_m| <= 2); the
+    // region key floor(n_m . phi) = floor(U_m) - n_m . floor(D) is then the
+    // same integer as cls_region's (the fused kernel's key pass does the same)
+    int nx[4], ny[4], km[4], rx[4];
+    double U[4], cu[4][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (q < ns && ((t >> q) & 1)) {
-                Dx -= vx[q];  // exact (R17)
-                Dy -= vy[q];
-                sgn = -sgn;
-            }
+    for (int m = 0; m < 4; ++m) {
+        nx[m] = S.cls.normal[b][m].x;
+        ny[m] = S.cls.normal[b][m].y;
+        km[m] = S.cls.kmin[b][m];
+        rx[m] = S.cls.radix[b][m];
+        U[m] = nx[m] * cx + ny[m] * cy;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cu[q][m] = nx[m] * vx[q] + ny[m] * vy[q];
+    }
+    double Dx = cx, Dy = cy;
+    int sgn = 1;
+    for (int t = 0; t < ntap; ++t) {
+        if (t > 0) {  // Gray step: digit q = ctz(t) flips to (gray(t) >> q) & 1
+            const int q = __ffs(t) - 1;
+            const bool on = ((t ^ (t >> 1)) >> q) & 1;
+            double dx = 0.0, dy = 0.0, du[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq)
+                if (qq == q) {
+                    dx = vx[qq];
+                    dy = vy[qq];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) du[m] = cu[qq][m];
+                }
+            Dx = on ? Dx - dx : Dx + dx;  // exact
+            Dy = on ? Dy - dy : Dy + dy;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) U[m] = on ? U[m] - du[m] : U[m] + du[m];
+            sgn = -sgn;
+        }
         const double flx = floor(Dx), fly = floor(Dy);
         const double fx = Dx - flx, fy = Dy - fly;  // exact
-        const int reg = cls_region(S.cls, b, fx, fy);
-        const int by = y + (int)fly;
-        const long long *Gt = G + ((ptrdiff_t)by * GW + (x + (int)flx + P));
+        const int ix = (int)flx, iy = (int)fly;
+        int idx = 0, mul = 1;
+        bool in = true;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int f = (int)floor(U[m]) - (nx[m] * ix + ny[m] * iy) - km[m];
+            in = in && f >= 0 && f < rx[m];
+            idx += f * mul;
+            mul *= rx[m];
+        }
+        int reg = in ? S.cls.table[b][idx] : -1;
+        if (reg < 0) reg = cls_region(S.cls, b, fx, fy);  // exactly on a knot line
+        const int by = y + iy;
+        const long long *Gt = G + ((ptrdiff_t)by * GW + (x + ix + P));
         // windows that reach above row 0 read the zero state there (checked
         // loads); all other reads are inside the domain (reach checked)
         const dd F = by + wymin - 2 >= 0 ? gx1_tap<NMON, false>(S, Gt, b, v, reg, fx, fy, sdl, by, GW)
