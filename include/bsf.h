@@ -392,7 +392,9 @@ int bsf_uses_fused(bsf_plan_t plan);
  * double-double (default 5e-10; 0 sends every pixel to the fallback, inf
  * none, which voids the 1e-9 contract); "global_kernel" 0/1 -- global mode
  * gathers with the order-1 integer kernel (1, default) or the fused kernel's
- * DMMA groups (0).  BSF_EINVAL for an unknown name.                          */
+ * DMMA groups (0); "scan_tma" 0/1 (process-wide) -- the running-sum strip
+ * kernels stream their rows by TMA (1, default when the row pitch allows) or
+ * by cp.async (0).  BSF_EINVAL for an unknown name.                          */
 bsf_status bsf_debug_option(bsf_plan_t plan, const char *name, double value);
 
 const char *bsf_status_str(bsf_status s);

@@ -1522,6 +1522,8 @@ extern "C" bsf_status bsf_debug_option(bsf_plan_t p, const char *name, double va
         p->opt_fused = value != 0.0;
     } else if (n == "work_order") {
         p->opt_order = value != 0.0;
+    } else if (n == "scan_tma") {  // process-wide: the scans' row streaming (TMA or cp.async)
+        set_scan_tma(value != 0.0);
     } else if (n == "global_kernel") {
         p->opt_global_kernel = value != 0.0 ? 1 : 0;
     } else if (n == "split_tol") {

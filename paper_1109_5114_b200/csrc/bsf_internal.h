@@ -251,6 +251,7 @@ cudaError_t launch_preint_i64(const uint8_t *f, unsigned long long *g, const Geo
 cudaError_t launch_scan_level(const void *f, int u8, void *g, int exact, const Geometry &geo, int basis, int level,
                               const void *carry, cudaStream_t st);
 void scan_step(int basis, int level, int *sx, int *sy);
+void set_scan_tma(int on);  // diagnostics: 0 = the cp.async strip kernel instead of the TMA-fed one
 cudaError_t launch_fill_ones(void *f, int u8, size_t n, cudaStream_t st, long long *nlaunch);
 cudaError_t launch_normalize(void *out, int out_f32, const double *den, size_t n, cudaStream_t st,
                              long long *nlaunch);

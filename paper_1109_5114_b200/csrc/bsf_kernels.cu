@@ -10,6 +10,9 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cuda.h>  // CUtensorMap (types only; cuTensorMapEncodeTiled through cudaGetDriverEntryPoint)
+
+#include <mutex>
 #include <type_traits>
 
 #include "bsf_dd.cuh"
@@ -74,20 +77,73 @@ struct OpU64 {
 #define BSF_SCAN_RPW_DD 8
 #define BSF_SCAN_ND_DD 3
 #endif
+// TMA tensor map of a level input (3-D: x, y, image), box {TmaRow::BX, 1, 1};
+// false when TMA's rules (16-byte aligned base and row pitch) do not hold
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    });
+    return fn;
+}
+
+template <class In, class T>
+static bool scan_tensor_map(CUtensorMap *map, const In *in, const Geometry &geo) {
+    constexpr bool IMG = !std::is_same<In, T>::value;
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn || ((uintptr_t)in & 15)) return false;
+    const int xs = TmaRow<In>::XS;  // double-double: pairs of fp64
+    const size_t es = TmaRow<In>::ES;
+    const cuuint64_t X = (cuuint64_t)(IMG ? geo.W : geo.GW) * xs, Y = IMG ? geo.H : geo.GH;
+    const cuuint64_t dims[3] = {X, Y, (cuuint64_t)geo.nimg};
+    const cuuint64_t strides[2] = {X * es, X * es * Y};
+    if (strides[0] % 16 || strides[0] >= (1ull << 40) || strides[1] >= (1ull << 40)) return false;
+    const cuuint32_t box[3] = {(cuuint32_t)TmaRow<In>::BX, 1u, 1u}, estr[3] = {1u, 1u, 1u};
+    const CUtensorMapDataType dt = std::is_same<In, uint8_t>::value   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : std::is_same<In, float>::value   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                   : sizeof(In) == 8                  ? CU_TENSOR_MAP_DATA_TYPE_INT64
+                                                                      : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+    return fn(map, dt, 3, (void *)in, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
+static std::atomic<int> g_scan_tma{1};
+static int scan_use_tma() { return g_scan_tma.load(std::memory_order_relaxed); }
+void set_scan_tma(int on) { g_scan_tma.store(on ? 1 : 0, std::memory_order_relaxed); }
+
 template <class Op, class In, int SX, int SY>
 static cudaError_t scan_strips(const In *in, typename Op::T *g, const Geometry &geo, const typename Op::T *carry,
                                cudaStream_t st) {
     constexpr bool DD = sizeof(typename Op::T) == 16;
     constexpr int NW = DD ? BSF_SCAN_NW_DD : BSF_SCAN_NW_I64, RPW = DD ? BSF_SCAN_RPW_DD : BSF_SCAN_RPW_I64,
                   ND = DD ? BSF_SCAN_ND_DD : BSF_SCAN_ND_I64;
+    const int span = abs(SX) * ((geo.GH - 1) / SY);
+    const int U0 = SX > 0 ? -span : 0, NS = (geo.GW + span + 31) / 32;
+    const unsigned grid = (unsigned)((long long)geo.nimg * NS);
+    CUtensorMap map;
+    if (scan_use_tma() && scan_tensor_map<In, typename Op::T>(&map, in, geo)) {
+        // rows streamed by TMA (bulk tensor copies completing on mbarriers)
+        constexpr int SMEM = ND * NW * RPW * tma_row_bytes<In>() + 128;  // + alignment slack
+        static std::atomic<unsigned long long> attr{0ull};
+        cudaError_t e = set_smem_attr(scan_strip_tma_kernel<Op, In, SX, SY, NW, RPW, ND>, SMEM, attr);
+        if (e != cudaSuccess) return e;
+        scan_strip_tma_kernel<Op, In, SX, SY, NW, RPW, ND><<<grid, 32 * NW, SMEM, st>>>(map, g, geo, U0, NS, carry);
+        return cudaGetLastError();
+    }
     constexpr int SMEM = ND * NW * RPW * 32 * (int)sizeof(typename Op::T);
     static std::atomic<unsigned long long> attr{0ull};
     cudaError_t e = set_smem_attr(scan_strip_kernel<Op, In, SX, SY, NW, RPW, ND>, SMEM, attr);
     if (e != cudaSuccess) return e;
-    const int span = abs(SX) * ((geo.GH - 1) / SY);
-    const int U0 = SX > 0 ? -span : 0, NS = (geo.GW + span + 31) / 32;
-    scan_strip_kernel<Op, In, SX, SY, NW, RPW, ND>
-        <<<(unsigned)((long long)geo.nimg * NS), 32 * NW, SMEM, st>>>(in, g, geo, U0, NS, carry);
+    scan_strip_kernel<Op, In, SX, SY, NW, RPW, ND><<<grid, 32 * NW, SMEM, st>>>(in, g, geo, U0, NS, carry);
     return cudaGetLastError();
 }
 

@@ -235,3 +235,174 @@ __global__ void __launch_bounds__(32 * WPC) scan_row_kernel(const In *in, typena
         for (int j = 0; j < EPL; ++j) cur[j] = nxt[j];
     }
 }
+
+// ---------------------------------------------------------------------------
+// The same strip scan with its rows streamed by TMA (cp.async.bulk.tensor):
+// each warp owns RPW rows per block of rows and fetches each of them with ONE
+// 3-D tensor copy (box {BX, 1, 1}) into a 128-byte aligned shared-memory row,
+// completing on the warp's mbarrier of that ring stage (arrive.expect_tx by
+// lane 0, then the lanes issue one row each).  A box's first x coordinate
+// must sit on a 16-byte boundary of the row (measured: an unaligned start is
+// an illegal instruction on sm_100a), so the box starts at the aligned
+// coordinate below the warp's 32 elements and is A - 1 elements wider; each
+// lane reads its element at the row's offset.  The tensor map's bounds give
+// the zero state outside the domain (levels >= 1) or outside the image
+// (level 0: the u8 / f32 image itself, zero-extended) for free: no
+// per-element predicates in the copy.  Used when the base address and row
+// pitch meet TMA's 16-byte rules (scan_strips checks), else the cp.async
+// kernel above runs.  The scan arithmetic is identical (bit-exact int64, same
+// double-double order).
+// ---------------------------------------------------------------------------
+template <class In>
+struct TmaRow {
+    static constexpr int XS = sizeof(In) == 16 ? 2 : 1;     // double-double rows are fp64 pairs in the map
+    static constexpr int ES = (int)sizeof(In) / XS;          // map element size
+    static constexpr int A = 16 / ES;                        // map elements per 16-byte boundary
+    static constexpr int BX = (32 * XS + (A > XS ? A - XS : 0) + A - 1) / A * A;  // box width (map elements)
+    static constexpr unsigned BYTES = (unsigned)(BX * ES);   // bytes one row copy delivers
+    static constexpr int PITCH = (int)((BYTES + 127) / 128 * 128);
+};
+template <class In>
+constexpr int tma_row_bytes() {
+    return TmaRow<In>::PITCH;
+}
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_row(unsigned dst, const CUtensorMap *map, int x, int y, int z, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
+        : "memory");
+}
+
+template <class Op, class In, int SX, int SY, int NW, int RPW, int ND>
+__global__ void __launch_bounds__(32 * NW) scan_strip_tma_kernel(const __grid_constant__ CUtensorMap map,
+                                                                  typename Op::T *out, Geometry geo, int U0, int NS,
+                                                                  const typename Op::T *carry_in) {
+    typedef typename Op::T T;
+    static_assert(RPW % 2 == 0 && RPW <= 32, "phases of SY = 2 lines need an even row count per warp");
+    constexpr int BR = NW * RPW;
+    typedef TmaRow<In> TR;
+    constexpr int PITCH = TR::PITCH;
+    extern __shared__ __align__(128) unsigned char scan_tma_smem[];
+    __shared__ T tot[2][NW][SY][32];
+    __shared__ __align__(8) unsigned long long bars[ND][NW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int img = blockIdx.x / NS, ua = U0 + 32 * (blockIdx.x % NS), u = ua + lane;
+    int qlo = 0, qhi = (geo.GH - 1) / SY;
+    if (SX > 0) {
+        qlo = max(qlo, ceildiv(-ua - 31, SX));
+        qhi = min(qhi, floordiv(geo.GW - 1 - ua, SX));
+    } else if (SX < 0) {
+        qlo = max(qlo, ceildiv(ua - geo.GW + 1, -SX));
+        qhi = min(qhi, floordiv(ua + 31, -SX));
+    } else if (ua + 31 < 0 || ua >= geo.GW) {
+        return;
+    }
+    if (qlo > qhi) return;
+    const int ylo = qlo * SY, yhi = min(geo.GH - 1, qhi * SY + SY - 1);
+    const int nblk = (yhi - ylo + BR) / BR;
+    // 128-byte aligned TMA destinations (the launch adds 128 bytes of slack)
+    const unsigned ring = ((unsigned)__cvta_generic_to_shared(scan_tma_smem) + 127u) & ~127u;
+    const unsigned char *ring_g = scan_tma_smem + (ring - (unsigned)__cvta_generic_to_shared(scan_tma_smem));
+    const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&bars[0][0]);
+    if (lane == 0)
+        for (int s = 0; s < ND; ++s) mbar_init(bar0 + 8u * (s * NW + warp), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    // level 0 reads the image (coordinates x - P, y, img: zero outside it);
+    // later levels read the domain (x, y, img: zero outside [0, GW))
+    constexpr bool IMG = !std::is_same<In, T>::value;
+    auto issue = [&](int j) {
+        if (j >= nblk) return;
+        const int s = j % ND;
+        const unsigned bar = bar0 + 8u * (s * NW + warp);
+        const int yb = ylo + j * BR + RPW * warp;
+        const int nrow = max(0, min(RPW, yhi - yb + 1));
+        if (nrow == 0) return;
+        if (lane == 0) mbar_expect_tx(bar, TR::BYTES * (unsigned)nrow);
+        __syncwarp();
+        if (lane < nrow) {
+            const int y = yb + lane, x = ua + SX * (y / SY);
+            const unsigned dst = ring + (unsigned)(((s * NW + warp) * RPW + lane) * PITCH);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the row was read through the generic proxy
+            const int xc = TR::XS * (IMG ? x - geo.P : x);
+            tma_load_row(dst, &map, xc - (int)((unsigned)xc % TR::A), y, img, bar);  // 16-byte aligned box start
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < ND - 1; ++j) issue(j);
+    T carry[SY];
+#pragma unroll
+    for (int ph = 0; ph < SY; ++ph) {
+        carry[ph] = Op::zero();
+        if (carry_in && ph < geo.GH && u >= 0 && u < geo.GW && u - SX >= 0 && u - SX < geo.GW)
+            carry[ph] = carry_in[((size_t)img * SY + ph) * geo.GW + (size_t)(u - SX)];
+    }
+    T *o = out + (size_t)img * geo.GH * geo.GW;
+    for (int j = 0; j < nblk; ++j) {
+        issue(j + ND - 1);
+        const int s = j % ND;
+        const int yb = ylo + j * BR + RPW * warp;
+        const int nrow = max(0, min(RPW, yhi - yb + 1));
+        if (nrow) mbar_wait(bar0 + 8u * (s * NW + warp), (unsigned)((j / ND) & 1));
+        const unsigned char *rows = ring_g + (size_t)((s * NW + warp) * RPW) * PITCH;
+        T v[RPW];
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int y = yb + k, x = u + SX * (y / SY);
+            const bool ok = k < nrow && x >= 0 && x < geo.GW;
+            T t = Op::zero();
+            if (ok) {
+                const int xc = TR::XS * (IMG ? ua + SX * (y / SY) - geo.P : ua + SX * (y / SY));
+                const int off = (int)((unsigned)xc % TR::A) / TR::XS;  // the warp's first element in the box
+                const In e = reinterpret_cast<const In *>(rows + k * PITCH)[off + lane];
+                if constexpr (sizeof(T) == 16 && !std::is_same<In, T>::value)
+                    t = make_double2((double)e, 0.0);
+                else if constexpr (std::is_same<In, T>::value)
+                    t = e;
+                else
+                    t = (T)e;
+            }
+            v[k] = t;
+        }
+        __syncwarp();  // every lane read the stage before lane < nrow refills it (issue above, next iterations)
+#pragma unroll
+        for (int k = SY; k < RPW; ++k) v[k] = Op::add(v[k - SY], v[k]);
+        T(*tb)[SY][32] = tot[j & 1];
+#pragma unroll
+        for (int ph = 0; ph < SY; ++ph) tb[warp][ph][lane] = v[RPW - SY + ph];
+        __syncthreads();
+        T ex[SY];
+#pragma unroll
+        for (int ph = 0; ph < SY; ++ph) {
+            T acc = carry[ph];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                if (w == warp) ex[ph] = acc;
+                acc = Op::add(acc, tb[w][ph][lane]);
+            }
+            carry[ph] = acc;
+        }
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+            const int y = yb + k, x = u + SX * (y / SY);
+            if (y <= yhi && x >= 0 && x < geo.GW) o[(size_t)y * geo.GW + x] = Op::add(ex[k % SY], v[k]);
+        }
+    }
+}
