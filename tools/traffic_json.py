@@ -1,0 +1,53 @@
+"""Write profiles/r02_traffic.json (DRAM bytes per launch, keyed by the hash of
+the CUDA sources the captures were taken on) from ncu --set full raw CSV
+exports: dram__bytes_read.sum + dram__bytes_write.sum per kernel family.
+
+python tools/traffic_json.py  (after tools/gpu/r02_final.sh copied the
+r02_r1_full_raw.csv / r02_r2_fused_raw.csv exports into profiles/)."""
+import csv
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from bench import _src_hash  # noqa: E402
+
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def per_kernel(path):
+    rows = list(csv.reader(open(os.path.join(ROOT, path))))
+    h, units = rows[0], rows[1]
+    ik, ir, iw = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+    out = []
+    for r in rows[2:]:
+        b = float(r[ir]) * UNIT[units[ir]] + float(r[iw]) * UNIT[units[iw]]
+        out.append((r[ik], b))
+    return out
+
+
+def main():
+    sh = _src_hash()
+    caps = {}
+    r1 = per_kernel("profiles/r02_r1_full_raw.csv")
+    scans = [b for k, b in r1 if "scan_" in k]
+    gx = [b for k, b in r1 if "gx1_kernel" in k]
+    caps["c3_4096_u8_grid32/r1/scan"] = {"dram_bytes": sum(scans), "src_hash": sh, "launches": len(scans),
+                                         "file": "profiles/r02_r1_full_raw.csv"}
+    caps["c3_4096_u8_grid32/r1/gx1_kernel"] = {"dram_bytes": gx[0], "src_hash": sh,
+                                               "file": "profiles/r02_r1_full_raw.csv"}
+    r2 = per_kernel("profiles/r02_r2_fused_raw.csv")
+    caps["c3_4096_u8_grid32/r2/fused_kernel"] = {"dram_bytes": r2[0][1], "src_hash": sh,
+                                                 "file": "profiles/r02_r2_fused_raw.csv"}
+    doc = {"what": "dram__bytes_read.sum + dram__bytes_write.sum per launch (per step for the 8 scan launches of "
+                   "order 1), one ncu --set full --clock-control none capture of tools/step_probe.py on config 3 "
+                   "(tools/gpu/r02_final.sh); bench.py reports them only while src_hash matches the CUDA sources",
+           "src_hash": sh, "captures": caps}
+    with open(os.path.join(ROOT, "profiles", "r02_traffic.json"), "w") as fh:
+        json.dump(doc, fh, indent=1)
+    print(json.dumps(doc, indent=1))
+
+
+if __name__ == "__main__":
+    main()
