@@ -1,7 +1,8 @@
 """Calibrate the exact split contraction's a-posteriori bound (GPU).
 
 For sampled pixels of a config, runs the fused path with the fallback
-disabled (BSF_SPLIT_TOL=inf) and the double-double tile kernel (BSF_FUSED=0),
+disabled (bsf_debug_option split_tol = inf) and the double-double tile kernel
+(bsf_debug_option fused = 0),
 and prints the true relative error of the split path against its bound
 (aux[9]).  python tools/calib_split.py --config 2 [--order R] [--n 20000]"""
 import argparse
@@ -18,6 +19,7 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--order", type=int, default=0)
 ap.add_argument("--n", type=int, default=20000)
 ap.add_argument("--child", default="")
+ap.add_argument("--opt", action="append", default=[], help="bsf_debug_option name=value")
 args = ap.parse_args()
 
 if args.child:
@@ -29,6 +31,9 @@ if args.child:
     dev = torch.device("cuda:0")
     plan = bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" else bsf.BSF_F32,
                     order=w.order, basis=w.basis, max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_TILE)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        plan.debug_option(k, float(v))
     img = synth.make_image(w, device=dev).contiguous()
     cov = synth.make_cov(w, device=dev).contiguous()
     pts = synth.sample_points(w, args.n, seed=21).to(dev).contiguous()
@@ -43,8 +48,8 @@ import numpy as np  # noqa: E402
 tag = "c%d_r%d" % (args.config, args.order)
 f1, f2 = "/tmp/split_%s.npz" % tag, "/tmp/dd_%s.npz" % tag
 base = [sys.executable, __file__, "--config", str(args.config), "--order", str(args.order), "--n", str(args.n)]
-subprocess.check_call(base + ["--child", f1], env=dict(os.environ, BSF_SPLIT_TOL="inf"))
-subprocess.check_call(base + ["--child", f2], env=dict(os.environ, BSF_FUSED="0"))
+subprocess.check_call(base + ["--child", f1, "--opt", "split_tol=inf"])
+subprocess.check_call(base + ["--child", f2, "--opt", "fused=0"])
 a, b = np.load(f1), np.load(f2)
 assert bool(a["fused"]) and not bool(b["fused"])
 err = np.abs(a["out"] - b["out"]) / np.abs(b["out"])

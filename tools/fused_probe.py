@@ -20,6 +20,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--split", type=int, default=0, help="bsf_run_split with this many passes (order from --order)")
 ap.add_argument("--anchor", default="tile", choices=["tile", "global", "auto"])
 ap.add_argument("--opt", action="append", default=[], help="bsf_debug_option name=value (diagnostics)")
+ap.add_argument("--super-tile", type=int, default=0, help="bsf_plan_desc.super_tile (0: the plan's choice)")
 args = ap.parse_args()
 kw = {"width": args.width, "height": args.height}
 if args.order:
@@ -27,7 +28,7 @@ if args.order:
 w = synth.workload(args.config, **kw)
 dev = torch.device("cuda:0")
 plan = bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" else bsf.BSF_F32, order=w.order,
-                basis=w.basis, max_sigma=w.max_sigma,
+                basis=w.basis, max_sigma=w.max_sigma, super_tile=args.super_tile,
                 anchor={"tile": bsf.BSF_ANCHOR_TILE, "global": bsf.BSF_ANCHOR_GLOBAL, "auto": bsf.BSF_ANCHOR_AUTO}[args.anchor])
 for o in args.opt:
     k, v = o.split("=")

@@ -1,6 +1,6 @@
 """Fallback pixels per 64 x 64 super-tile against its scales (diagnostics).
 
-Runs a workload with BSF_STILE=64 and relates each super-tile's double-double
+Runs a workload with 64 x 64 super-tiles (raster work order) and relates each super-tile's double-double
 fallback count (bsf_debug_item_cycles) to the conditioning proxy
 (64 + 2 E) / sigma_min, E = sqrt(24 r) max sigma_major over the tile,
 sigma_min the smallest minor standard deviation in the tile."""
@@ -9,8 +9,6 @@ import math
 import os
 import sys
 
-os.environ["BSF_STILE"] = "64"
-os.environ["BSF_ORDER"] = "0"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -32,7 +30,8 @@ if args.order:
 w = synth.workload(args.config, **kw)
 dev = torch.device("cuda:0")
 plan = bsf.Plan(w.width, w.height, in_dtype=bsf.BSF_U8 if w.in_dtype == "u8" else bsf.BSF_F32, order=w.order,
-                basis=w.basis, max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_TILE)
+                basis=w.basis, max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_TILE, super_tile=64)
+plan.debug_option("work_order", 0)
 img = synth.make_image(w, device=dev).contiguous()
 cov = synth.make_cov(w, device=dev).contiguous()
 out = torch.empty((1, w.height, w.width), dtype=torch.float64, device=dev)
