@@ -63,9 +63,10 @@ def test_fuzz_fused_vs_oracle(seed):
         ys, xs = idx // W, idx % W
         ref = oracle_points(c["img"][i], c["cov"][b], xs, ys, policy=c["policy"], r=c["r"])[0]
         tol = 1e-6 if c["out_f32"] else 1e-9
-        # signed float images: relative error against the larger of |ref| and the
-        # output scale (outputs can pass through zero)
-        scale = np.maximum(np.abs(ref), 1e-3 * np.max(np.abs(ref)))
+        # u8 images: plain relative error (outputs are positive); signed float
+        # images only: against the larger of |ref| and 1e-3 of the output scale
+        # (outputs pass through zero, where a relative error is undefined)
+        scale = np.abs(ref) if c["u8"] else np.maximum(np.abs(ref), 1e-3 * np.max(np.abs(ref)))
         err = float(np.max(np.abs(got[i][ys, xs] - ref) / scale))
         assert err <= tol, (seed, i, err, {k: c[k] for k in ("H", "W", "r", "policy", "u8", "smax")})
 
@@ -111,6 +112,59 @@ def test_fuzz_large_images_vs_oracle(seed):
     idx = rng.choice(H * W, 24, replace=False)
     ys, xs = idx // W, idx % W
     ref = oracle_points(c["img"], c["cov"], xs, ys, policy=c["policy"], r=c["r"])[0]
-    scale = np.maximum(np.abs(ref), 1e-3 * np.max(np.abs(ref)))
+    scale = np.abs(ref) if c["u8"] else np.maximum(np.abs(ref), 1e-3 * np.max(np.abs(ref)))  # as above
     err = float(np.max(np.abs(got[ys, xs] - ref) / scale))
     assert err <= 1e-9, (seed, err, st, {k: c[k] for k in ("H", "W", "r", "policy", "u8", "smax")})
+
+
+def _case_global(seed):
+    """u8 images at order 1 through global mode (exact int64 sums + the
+    integer gather): ragged and thin sizes across the 32 x 32 gather tiles,
+    batch and channels, sigma ranges with zero-scale and clamped pixels."""
+    rng = np.random.default_rng(9000 + seed)
+    H, W = int(rng.integers(1, 200)), int(rng.integers(1, 260))
+    batch, channels = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+    smax = float(rng.uniform(0.6, 12.0))
+    ph = rng.uniform(0, 2 * math.pi, 4)
+    X = np.arange(W)[None, :] / max(W - 1, 1)
+    Y = np.arange(H)[:, None] / max(H - 1, 1)
+    covs, imgs = [], []
+    for b in range(batch):
+        smaj = 0.5 + (smax - 0.5) * (0.5 + 0.5 * np.sin(4 * X + ph[0] + b) * np.cos(3 * Y + ph[1]))
+        ratio = 1.0 + rng.uniform(0, 12.0) * (0.5 + 0.5 * np.cos(2 * X - 3 * Y + ph[2]))
+        th = np.mod(ph[3] + 2.5 * X - 1.5 * Y + b, math.pi)
+        covs.append(np.stack([smaj, smaj / np.sqrt(ratio), th + 0 * X]).astype(np.float32))
+        for c in range(channels):
+            imgs.append(rng.integers(0, 256, (H, W)).astype(np.uint8))
+    return dict(H=H, W=W, policy=int(rng.integers(0, 3)), batch=batch, channels=channels, smax=smax,
+                cov=np.stack(covs), img=np.stack(imgs), out_f32=bool(rng.integers(0, 2)), rng=rng)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_global_mode_vs_oracle(seed):
+    """Relative error against the oracle with no floor (u8 outputs are
+    positive): 1e-9 for f64 output, 1e-6 for f32 output."""
+    c = _case_global(seed)
+    H, W = c["H"], c["W"]
+    plan = bsf.Plan(W, H, batch=c["batch"], channels=c["channels"], in_dtype=bsf.BSF_U8,
+                    out_dtype=bsf.BSF_F32 if c["out_f32"] else bsf.BSF_F64, order=1, basis=c["policy"],
+                    max_sigma=c["smax"], anchor=bsf.BSF_ANCHOR_GLOBAL)
+    assert plan.geometry.global_mode == 1
+    nimg = c["batch"] * c["channels"]
+    out = torch.empty((nimg, H, W), dtype=torch.float32 if c["out_f32"] else torch.float64, device="cuda")
+    plan.run(torch.from_numpy(c["img"]).cuda(), torch.from_numpy(c["cov"]).cuda(), out)
+    torch.cuda.synchronize()
+    st = plan.stats(reset=True)
+    assert st["status"] == 0 and st["pixels"] == nimg * H * W
+    got = out.cpu().numpy().astype(np.float64)
+    rng = c["rng"]
+    n = min(H * W, 20)
+    for i in range(nimg):
+        b = i // c["channels"]
+        idx = rng.choice(H * W, n, replace=False)
+        ys, xs = idx // W, idx % W
+        ref = oracle_points(c["img"][i], c["cov"][b], xs, ys, policy=c["policy"], r=1)[0]
+        ok = ref != 0  # an all-zero neighbourhood: both sides exactly 0
+        assert np.all(got[i][ys, xs][~ok] == 0.0)
+        err = float(np.max(np.abs(got[i][ys, xs][ok] - ref[ok]) / np.abs(ref[ok]), initial=0.0))
+        assert err <= (1e-6 if c["out_f32"] else 1e-9), (seed, i, err, {k: c[k] for k in ("H", "W", "policy", "smax")})
