@@ -13,4 +13,9 @@ for s in range(32, 160):
         T.test_fuzz_fused_vs_oracle(s)
     except AssertionError as e:
         bad += 1; print("FAIL small", s, e)
+for s in range(24, 224):
+    try:
+        T.test_fuzz_global_mode_vs_oracle(s)
+    except AssertionError as e:
+        bad += 1; print("FAIL global", s, e)
 print("failures", bad)
