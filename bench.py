@@ -256,7 +256,7 @@ def time_order(args, w, r, dev, rank, world, stream, flush, pg):
     npx = w.width * w.height
     mode = "global" if geo.global_mode else ("tile" if r <= 3 else "tiles_sample")
     K = args.steps if r <= 2 else (min(args.steps, 2) if r == 3 else 1)
-    Wm = args.warmup if r <= 2 else 1
+    Wm = max(3, args.warmup)  # W >= 3 at every order (orders 3 / 4: ~5 s per step)
     g = plan.empty_g_exact() if mode == "global" else None
     tiles = None
     if mode == "tiles_sample":
@@ -487,7 +487,7 @@ def run_partitioned(args, rank, world, local):
                "halo_rows": g.halo, "super_tile": g.super_tile,
                "parallelism": "row strips over %d ranks, halo exchange by ncclSend/ncclRecv in the library" % world}
         scaling = "strong"
-    for _ in range(args.warmup if args.config == 4 else 1):
+    for _ in range(args.warmup):  # W >= 3 (config 5: minutes per step on few GPUs)
         step()
     torch.cuda.synchronize()
     if dist:
@@ -543,7 +543,6 @@ def main():
             if rank == 0:
                 run_reference(args, synth.workload(args.config), [synth.workload(args.config).order])
             return
-        args.warmup = 1 if args.steps <= 1 else args.warmup
         run_partitioned(args, rank, world, local)
         return
     w = synth.workload(args.config)
