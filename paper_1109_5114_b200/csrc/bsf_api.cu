@@ -115,6 +115,10 @@ struct bsf_plan_s {
     cudaStream_t s_in = nullptr, s_out = nullptr;  // bsf_run_host pipeline (global mode): copy streams
     cudaStream_t s_c2 = nullptr;                   // second compute stream (odd bands fill the even bands' tails)
     cudaEvent_t ev[2 * BSF_HOST_BANDS + 5] = {};
+    // the two bases' running sums are independent: basis 1 runs on a side
+    // stream forked from (and joined back into) the caller's stream
+    cudaStream_t s_side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool scratch_ready = false;          // tile-anchored halo scratch allocated
     // global mode (order 1, u8 input): the exact int64 running
     // sums of the whole image, read by the fused kernel's taps
@@ -680,6 +684,12 @@ extern "C" bsf_status bsf_plan_destroy(bsf_plan_t p) {
         for (cudaEvent_t e : p->ev)
             if (e) cudaEventDestroy(e);
     }
+    if (p->s_side) {
+        cudaStreamSynchronize(p->s_side);
+        cudaStreamDestroy(p->s_side);
+        cudaEventDestroy(p->ev_fork);
+        cudaEventDestroy(p->ev_join);
+    }
     for (void *q : p->dev_allocs) cudaFree(q);
     delete p;
     return BSF_OK;
@@ -712,6 +722,34 @@ extern "C" bsf_status bsf_plan_geometry(bsf_plan_t p, bsf_geometry *geom) {
     return BSF_OK;
 }
 
+// The pre-integration of every basis of the plan (launch(slot, stream) runs
+// one basis' 4r levels): with two bases, basis 1 runs concurrently on the
+// plan's side stream (its levels' grids are ~1 CTA per SM each: two bases in
+// flight fill the GPU), forked from and joined back into `st` by events, so
+// the caller sees one stream (CUDA-graph capture included).
+template <class F>
+static bsf_status preint_bases(bsf_plan_s *p, cudaStream_t st, F launch) {
+    if (p->geo.nbases == 2 && !p->s_side) {
+        if (cudaStreamCreateWithFlags(&p->s_side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+            p->s_side = nullptr;
+            return set_err(BSF_ECUDA, "side stream for the second basis");
+        }
+    }
+    if (p->geo.nbases == 2) {
+        CUDA_TRY(cudaEventRecord(p->ev_fork, st));
+        CUDA_TRY(cudaStreamWaitEvent(p->s_side, p->ev_fork, 0));
+        CUDA_TRY(launch(1, p->s_side));
+        CUDA_TRY(launch(0, st));
+        CUDA_TRY(cudaEventRecord(p->ev_join, p->s_side));
+        CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
+        return BSF_OK;
+    }
+    for (int s = 0; s < p->geo.nbases; ++s) CUDA_TRY(launch(s, st));
+    return BSF_OK;
+}
+
 extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, void *stream) {
     if (!p || !f || !g) return set_err(BSF_EINVAL, "null argument");
     DevGuard guard(p->d.device);
@@ -721,10 +759,10 @@ extern "C" bsf_status bsf_preintegrate(bsf_plan_t p, const void *f, void *g, voi
     p->last = st;
     double2 *gd = (double2 *)g;
     size_t slot = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW;
-    for (int s = 0; s < p->geo.nbases; ++s)
-        CUDA_TRY(launch_preint_dd(f, p->d.in_dtype == BSF_U8, gd + s * slot, p->geo, p->bases[s], p->d.order, st,
-                                  &p->nlaunch));
-    return BSF_OK;
+    return preint_bases(p, st, [&](int s, cudaStream_t ss) {
+        return launch_preint_dd(f, p->d.in_dtype == BSF_U8, gd + s * slot, p->geo, p->bases[s], p->d.order, ss,
+                                &p->nlaunch);
+    });
 }
 
 // GLOBAL mode over row strips (Alg. 3 step 2):
@@ -786,10 +824,9 @@ extern "C" bsf_status bsf_preintegrate_exact(bsf_plan_t p, const void *f, void *
     unsigned long long *gd = (unsigned long long *)g;
     if (p->d.nranks > 1) return preintegrate_exact_strip(p, (const uint8_t *)f, gd, st);
     size_t slot = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW;
-    for (int s = 0; s < p->geo.nbases; ++s)
-        CUDA_TRY(launch_preint_i64((const uint8_t *)f, gd + s * slot, p->geo, p->bases[s], p->d.order, st,
-                                   &p->nlaunch));
-    return BSF_OK;
+    return preint_bases(p, st, [&](int s, cudaStream_t ss) {
+        return launch_preint_i64((const uint8_t *)f, gd + s * slot, p->geo, p->bases[s], p->d.order, ss, &p->nlaunch);
+    });
 }
 
 extern "C" bsf_status bsf_scan_step(bsf_plan_t p, int slot, int level, int *sx, int *sy) {
@@ -1066,9 +1103,11 @@ static bsf_status run_global(bsf_plan_s *p, const void *f, const void *cov, void
     }
     p->last = st;
     const size_t slot = (size_t)p->geo.nimg * p->geo.GH * p->geo.GW;
-    for (int b = 0; b < p->geo.nbases; ++b)
-        CUDA_TRY(launch_preint_i64((const uint8_t *)f, (unsigned long long *)p->gx_ws + b * slot, p->geo, p->bases[b],
-                                   p->d.order, st, &p->nlaunch));
+    const bsf_status e = preint_bases(p, st, [&](int b, cudaStream_t ss) {
+        return launch_preint_i64((const uint8_t *)f, (unsigned long long *)p->gx_ws + b * slot, p->geo, p->bases[b],
+                                 p->d.order, ss, &p->nlaunch);
+    });
+    if (e != BSF_OK) return e;
     return filter_global(p, p->gx_ws, cov, out, pts, npts, aux, st);
 }
 
@@ -1392,9 +1431,13 @@ static bsf_status run_host_global(bsf_plan_s *p, const void *f_host, const void 
         p->dev_allocs.push_back(q);
         p->gx_ws = (long long *)q;
     }
-    for (int b = 0; b < g.nbases; ++b)
-        CUDA_TRY(launch_preint_i64((const uint8_t *)p->f_stage, (unsigned long long *)p->gx_ws + b * slot, g,
-                                   p->bases[b], p->d.order, st, &p->nlaunch));
+    {
+        const bsf_status e = preint_bases(p, st, [&](int b, cudaStream_t ss) {
+            return launch_preint_i64((const uint8_t *)p->f_stage, (unsigned long long *)p->gx_ws + b * slot, g,
+                                     p->bases[b], p->d.order, ss, &p->nlaunch);
+        });
+        if (e != BSF_OK) return e;
+    }
     CUDA_TRY(cudaEventRecord(ev_pre, st));
     CUDA_TRY(cudaStreamWaitEvent(p->s_c2, ev_pre, 0));
     int band = 0;
