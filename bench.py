@@ -201,6 +201,13 @@ def run_reference(args, w, orders):
     nthreads = os.cpu_count() or 1
     r = orders[0]
     per_step = args.ref_points
+    if per_step <= 0:  # auto: ~0.5 s of oracle work per step (calibrated on a separate stratified sample)
+        cx, cy = _sample_pixels(w, 2 * nthreads, 13)
+        _oracle_chunk(w, r, cx[:1], cy[:1], 1)  # image generation outside the calibration
+        t0 = time.perf_counter()
+        _oracle_chunk(w, r, cx, cy, nthreads)
+        per_px = (time.perf_counter() - t0) / len(cx)
+        per_step = int(min(4000, max(nthreads, 0.5 / max(per_px, 1e-9))))
     xs, ys = _sample_pixels(w, per_step * (args.steps + args.warmup), 11)
 
     def step(i):
@@ -523,7 +530,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--orders", default="", help="comma list; default: the config's orders (config 3: 1,2,3,4)")
     ap.add_argument("--impl", default="bsf")
-    ap.add_argument("--ref-points", type=int, default=8)
+    ap.add_argument("--ref-points", type=int, default=0, help="oracle pixels per reference step (0: ~0.5 s of work)")
     ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds of oracle time per order")
     ap.add_argument("--r4-tiles", type=int, default=148)
     ap.add_argument("--no-cpu-baseline", action="store_true")
