@@ -145,24 +145,21 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
 // R3): D_j = sum_k (1/2 - j_k) a'_k s_k, sign (-1)^{sum j}.
 template <int NMON>
 __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__restrict__ G, int GW, int P,
-                                           const PixelScales &ps, int x, int y, double &erel,
-                                           unsigned long long &macs) {
-    const int b = ps.basis, v = ps.drop + 1;
-    int dirs[4];
-    int ns = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        if (k != ps.drop) dirs[ns++] = k;
+                                           int b, int drop, const double *apm, int x, int y, double &erel,
+                                           unsigned int &macs) {
+    // apm: the pixel's scales a'_k in shared memory (read at each step, not
+    // held in registers across the tap loop)
+    const int v = drop + 1;
+    const int ns = drop < 0 ? 4 : 3;
+    auto dir = [&](int q) { return q + (drop >= 0 && q >= drop ? 1 : 0); };  // q-th direction in use
     // v_k = s_k a'_k and the centre sum_k v_k / 2 (exact on the 2^-41 grid, R17)
-    double vx[4], vy[4], cx = 0.0, cy = 0.0;
+    double cx = 0.0, cy = 0.0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const int k = q < ns ? dirs[q] : 0;
-        vx[q] = c_steps[b][k][0] * ps.ap[k];
-        vy[q] = c_steps[b][k][1] * ps.ap[k];
         if (q < ns) {
-            cx += 0.5 * vx[q];
-            cy += 0.5 * vy[q];
+            const int k = dir(q);
+            cx += 0.5 * (c_steps[b][k][0] * apm[k]);
+            cy += 0.5 * (c_steps[b][k][1] * apm[k]);
         }
     }
     const int sdl = v ? c_steps[b][v - 1][1] * GW + c_steps[b][v - 1][0] : 0;
@@ -174,33 +171,23 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
     // one exact step (R17: every value on the 2^-41 grid, |n_m| <= 2); the
     // region key floor(n_m . phi) = floor(U_m) - n_m . floor(D) is then the
     // same integer as cls_region's (the fused kernel's key pass does the same)
-    int nx[4], ny[4], km[4], rx[4];
-    double U[4], cu[4][4];
+    // the knot-line normals stay in shared memory and the per-step increments
+    // n_m . v_q are formed at the step (exact: |n_m| <= 2, R17)
+    double U[4];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        nx[m] = S.cls.normal[b][m].x;
-        ny[m] = S.cls.normal[b][m].y;
-        km[m] = S.cls.kmin[b][m];
-        rx[m] = S.cls.radix[b][m];
-        U[m] = nx[m] * cx + ny[m] * cy;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) cu[q][m] = nx[m] * vx[q] + ny[m] * vy[q];
-    }
+    for (int m = 0; m < 4; ++m) U[m] = S.cls.normal[b][m].x * cx + S.cls.normal[b][m].y * cy;
     double Dx = cx, Dy = cy;
     int sgn = 1;
     for (int t = 0; t < ntap; ++t) {
         if (t > 0) {  // Gray step: digit q = ctz(t) flips to (gray(t) >> q) & 1
             const int q = __ffs(t) - 1;
             const bool on = ((t ^ (t >> 1)) >> q) & 1;
-            double dx = 0.0, dy = 0.0, du[4] = {0.0, 0.0, 0.0, 0.0};
+            const int k = dir(q);
+            const double ak = apm[k];
+            const double dx = c_steps[b][k][0] * ak, dy = c_steps[b][k][1] * ak;  // v_q, as at the centre
+            double du[4];
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq)
-                if (qq == q) {
-                    dx = vx[qq];
-                    dy = vy[qq];
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) du[m] = cu[qq][m];
-                }
+            for (int m = 0; m < 4; ++m) du[m] = S.cls.normal[b][m].x * dx + S.cls.normal[b][m].y * dy;
             Dx = on ? Dx - dx : Dx + dx;  // exact
             Dy = on ? Dy - dy : Dy + dy;
 #pragma unroll
@@ -214,10 +201,12 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
         bool in = true;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const int f = (int)floor(U[m]) - (nx[m] * ix + ny[m] * iy) - km[m];
-            in = in && f >= 0 && f < rx[m];
+            const int2 nm = S.cls.normal[b][m];
+            const int rxm = S.cls.radix[b][m];
+            const int f = (int)floor(U[m]) - (nm.x * ix + nm.y * iy) - S.cls.kmin[b][m];
+            in = in && f >= 0 && f < rxm;
             idx += f * mul;
-            mul *= rx[m];
+            mul *= rxm;
         }
         int reg = in ? S.cls.table[b][idx] : -1;
         if (reg < 0) reg = cls_region(S.cls, b, fx, fy);  // exactly on a knot line
@@ -227,7 +216,7 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
         // loads); all other reads are inside the domain (reach checked)
         const dd F = by + wymin - 2 >= 0 ? gx1_tap<NMON, false>(S, Gt, b, v, reg, fx, fy, sdl, by, GW)
                                          : gx1_tap<NMON, true>(S, Gt, b, v, reg, fx, fy, sdl, by, GW);
-        macs += (unsigned long long)S.cnt[b][v][reg] * NMON;  // algorithmic: window x monomials
+        macs += S.cnt[b][v][reg] * NMON;  // algorithmic: window x monomials
         // compensated signed sum: TwoSum on the heads, small terms in e0
         const double fh = sgn > 0 ? F.hi : -F.hi, fl = sgn > 0 ? F.lo : -F.lo;
         const dd s = two_sum(h0, fh);
@@ -239,7 +228,7 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
     double norm = S.var[b][v].invL;  // 1 / L
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-        if (q < ns) norm /= ps.ap[dirs[q]];
+        if (q < ns) norm /= apm[dir(q)];
     const double Sd = dd_to_d(Ssum);
     // rounding of the Horner steps and of the sum: (2 ntap + 8) u^2 sum_j |F_j|
     erel = 2.5e-30 * (double)(2 * ntap + 8) * sumF / fabs(Sd);
@@ -403,13 +392,9 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
             const int p = s_order[32 * grp + lane];
             const int w = s_info[p];
             const bool valid = (w >> 5) & 1;
-            PixelScales ps;
-            ps.basis = w & 1;
-            ps.drop = ((w >> 1) & 7) - 1;
-            ps.clamped = (w >> 4) & 1;
-            ps.flags = w >> 8;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) ps.ap[q] = s_ap[p][q];
+            // the scales stay in shared memory (s_ap[p]): re-read where used,
+            // not held in registers across the tap loop
+            const int basis = w & 1, drop = ((w >> 1) & 7) - 1;
             int img, x, y;
             long long oidx;
             if (a.pts) {
@@ -424,7 +409,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
                 y = y0 + p / GX1_TW;
                 oidx = out_index(a, img, x, y);
             }
-            int flags = ps.flags;
+            int flags = w >> 8;
             const bool live = valid && !(flags & (FLAG_INFEASIBLE | FLAG_TWO_ZERO));
             double res = __longlong_as_double(0x7ff8000000000000LL), erel = 0.0;
             bool used_dd = false;
@@ -435,21 +420,30 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
                 double rx = 0.0, ry = 0.0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    rx += ps.ap[k] * abs(c_steps[ps.basis][k][0]);
-                    ry += ps.ap[k] * c_steps[ps.basis][k][1];
+                    rx += s_ap[p][k] * abs(c_steps[basis][k][0]);
+                    ry += s_ap[p][k] * c_steps[basis][k][1];
                 }
                 const int ex = (int)ceil(0.5 * rx) + 1, ey = (int)ceil(0.5 * ry) + 1;
-                const int4 E = S.ext[ps.basis];
+                const int4 E = S.ext[basis];
                 const bool in = x + a.gP - ex + E.x - 2 >= 0 && x + a.gP + ex + E.y + 2 < a.gGW &&
                                 y + ey + E.w < a.gGH;
                 if (!in) {
                     flags |= FLAG_RANGE;
                 } else {
-                    const long long *G = a.gglob[ps.basis] + (size_t)img * a.gGH * a.gGW;
-                    res = ps.drop < 0 ? gx1_mesh<6>(S, G, a.gGW, a.gP, ps, x, y, erel, macs)
-                                      : gx1_mesh<3>(S, G, a.gGW, a.gP, ps, x, y, erel, macs);
+                    const long long *G = a.gglob[basis] + (size_t)img * a.gGH * a.gGW;
+                    unsigned int pm = 0;
+                    res = drop < 0 ? gx1_mesh<6>(S, G, a.gGW, a.gP, basis, drop, s_ap[p], x, y, erel, pm)
+                                   : gx1_mesh<3>(S, G, a.gGW, a.gP, basis, drop, s_ap[p], x, y, erel, pm);
+                    macs += pm;
                     if (!(erel <= a.split_tol)) {  // NaN-safe: the double-double mesh on the same sums
-                        res = gx1_fallback(G, a.gP, a.gGW, a.gGH, luts[ps.basis], ps, x, y, &flags);
+                        PixelScales ps;
+                        ps.basis = basis;
+                        ps.drop = drop;
+                        ps.clamped = (w >> 4) & 1;
+                        ps.flags = w >> 8;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) ps.ap[q] = s_ap[p][q];
+                        res = gx1_fallback(G, a.gP, a.gGW, a.gGH, luts[basis], ps, x, y, &flags);
                         used_dd = true;
                     }
                 }
@@ -457,11 +451,11 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
             if (valid) {
                 if (a.aux) {
                     double *ax = a.aux + BSF_AUX * oidx;
-                    ax[0] = ps.basis;
-                    ax[1] = ps.drop;
-                    ax[2] = ps.clamped;
+                    ax[0] = basis;
+                    ax[1] = drop;
+                    ax[2] = (w >> 4) & 1;
                     ax[3] = flags;
-                    for (int k = 0; k < 4; ++k) ax[4 + k] = ps.ap[k];
+                    for (int k = 0; k < 4; ++k) ax[4 + k] = s_ap[p][k];
                     ax[8] = used_dd;
                     ax[9] = erel;
                     ax[10] = ax[11] = 0.0;
@@ -473,9 +467,9 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
             }
             if (a.stats) {
                 warp_count(a.stats + 0, valid);
-                warp_count(a.stats + 1, valid && ps.clamped);
-                warp_count(a.stats + 2, valid && ps.drop >= 0);
-                warp_count(a.stats + 3, valid && ps.basis == BASIS_THETA_PRIME);
+                warp_count(a.stats + 1, valid && ((w >> 4) & 1));
+                warp_count(a.stats + 2, valid && drop >= 0);
+                warp_count(a.stats + 3, valid && basis == BASIS_THETA_PRIME);
                 warp_count(a.stats + 5, used_dd);
                 if (valid && flags) atomicOr(a.stats + 4, (unsigned long long)flags);
             }
