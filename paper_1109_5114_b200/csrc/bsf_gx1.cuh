@@ -167,15 +167,12 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
     const int ntap = 1 << ns;
     double h0 = 0.0, e0 = 0.0, sumF = 0.0;
     // taps in Gray-code order: consecutive taps differ in one digit j_q, so
-    // the displacement D and the knot-line coordinates U_m = n_m . D move by
-    // one exact step (R17: every value on the 2^-41 grid, |n_m| <= 2); the
-    // region key floor(n_m . phi) = floor(U_m) - n_m . floor(D) is then the
-    // same integer as cls_region's (the fused kernel's key pass does the same)
-    // the knot-line normals stay in shared memory and the per-step increments
-    // n_m . v_q are formed at the step (exact: |n_m| <= 2, R17)
-    double U[4];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) U[m] = S.cls.normal[b][m].x * cx + S.cls.normal[b][m].y * cy;
+    // the displacement D moves by one exact step (R17: every value on the
+    // 2^-41 grid).  The region key floor(n_m . phi) = floor(n_m . D) -
+    // n_m . floor(D) is then the same integer as cls_region's (the fused
+    // kernel's key pass does the same); n_m . D is formed per tap (exact:
+    // |n_m| <= 2, |n_m . D| < 2^11), the normals read from shared memory, so
+    // no per-line state lives across the taps
     double Dx = cx, Dy = cy;
     int sgn = 1;
     for (int t = 0; t < ntap; ++t) {
@@ -185,13 +182,8 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
             const int k = dir(q);
             const double ak = apm[k];
             const double dx = c_steps[b][k][0] * ak, dy = c_steps[b][k][1] * ak;  // v_q, as at the centre
-            double du[4];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) du[m] = S.cls.normal[b][m].x * dx + S.cls.normal[b][m].y * dy;
             Dx = on ? Dx - dx : Dx + dx;  // exact
             Dy = on ? Dy - dy : Dy + dy;
-#pragma unroll
-            for (int m = 0; m < 4; ++m) U[m] = on ? U[m] - du[m] : U[m] + du[m];
             sgn = -sgn;
         }
         const double flx = floor(Dx), fly = floor(Dy);
@@ -203,7 +195,8 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
         for (int m = 0; m < 4; ++m) {
             const int2 nm = S.cls.normal[b][m];
             const int rxm = S.cls.radix[b][m];
-            const int f = (int)floor(U[m]) - (nm.x * ix + nm.y * iy) - S.cls.kmin[b][m];
+            const double Um = nm.x * Dx + nm.y * Dy;  // exact
+            const int f = (int)floor(Um) - (nm.x * ix + nm.y * iy) - S.cls.kmin[b][m];
             in = in && f >= 0 && f < rxm;
             idx += f * mul;
             mul *= rxm;
