@@ -44,6 +44,7 @@ struct Gx1Var {
 
 struct Gx1Smem {
     ClsTables cls;
+    double2 nrm[2][4];                        // the knot-line normals as doubles (no per-tap conversions)
     Gx1Var var[2][NVAR];
     unsigned char cnt[2][NVAR][GX1_MAXREG];   // window slots of the region
     int4 ext[2];                              // window offset extents (wxmin, wxmax, wymin, wymax) per basis
@@ -168,11 +169,10 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
     double h0 = 0.0, e0 = 0.0, sumF = 0.0;
     // taps in Gray-code order: consecutive taps differ in one digit j_q, so
     // the displacement D moves by one exact step (R17: every value on the
-    // 2^-41 grid).  The region key floor(n_m . phi) = floor(n_m . D) -
-    // n_m . floor(D) is then the same integer as cls_region's (the fused
-    // kernel's key pass does the same); n_m . D is formed per tap (exact:
-    // |n_m| <= 2, |n_m . D| < 2^11), the normals read from shared memory, so
-    // no per-line state lives across the taps
+    // 2^-41 grid) and phi = D - floor(D) is exact.  The region key
+    // floor(n_m . phi) (cls_region's) is formed per tap from phi (exact:
+    // |n_m| <= 2), the normals read from shared memory, so no per-line state
+    // lives across the taps
     double Dx = cx, Dy = cy;
     int sgn = 1;
     for (int t = 0; t < ntap; ++t) {
@@ -193,10 +193,9 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
         bool in = true;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const int2 nm = S.cls.normal[b][m];
+            const double2 nm = S.nrm[b][m];
             const int rxm = S.cls.radix[b][m];
-            const double Um = nm.x * Dx + nm.y * Dy;  // exact
-            const int f = (int)floor(Um) - (nm.x * ix + nm.y * iy) - S.cls.kmin[b][m];
+            const int f = (int)floor(nm.x * fx + nm.y * fy) - S.cls.kmin[b][m];  // n_m . phi: exact
             in = in && f >= 0 && f < rxm;
             idx += f * mul;
             mul *= rxm;
@@ -248,6 +247,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
         const LutBasis &L = luts[tid];
         for (int k = 0; k < 4; ++k) {
             S.cls.normal[tid][k] = L.normal[k];
+            S.nrm[tid][k] = make_double2(L.normal[k].x, L.normal[k].y);
             S.cls.kmin[tid][k] = L.kmin[k];
             S.cls.radix[tid][k] = L.radix[k];
         }
