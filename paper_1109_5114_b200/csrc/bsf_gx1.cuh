@@ -49,7 +49,7 @@ struct Gx1Smem {
     unsigned char cnt[2][NVAR][GX1_MAXREG];   // window slots of the region
     int4 ext[2];                              // window offset extents (wxmin, wxmax, wymin, wymax) per basis
     // per (basis, variant, region, slot), flat: the window offset as a linear
-    // index dy GW + dx into the running sums, and the numerators n_mu
+    // byte offset 8 (dy GW + dx) into the running sums, and the numerators n_mu
     // (monomials in gen_lut order, int8, padded to 8 bytes); padding slots
     // have offset 0 and zero numerators
     int off[GX1_SLOTS];
@@ -77,23 +77,28 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
         for (int m = 0; m < NMON; ++m) acc[l][m] = 0;
     const int n4 = (S.cnt[b][v][reg] + 3) & ~3;
     const int row = S.var[b][v].base + reg * S.var[b][v].nmax4;
-    const int *off = S.off + row;
+    const int *off = S.off + row;  // byte offsets (8 x element offsets): one 64-bit add per load address
+    const char *Gb = reinterpret_cast<const char *>(Gt);
+    const char *Gv = reinterpret_cast<const char *>(Gt - sdl);  // the variant's lattice-shifted reads
     const uint2 *num = S.num + row;
     for (int s0 = 0; s0 < n4; s0 += 4) {
         long long g[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int o = off[s0 + i];
+            const int ob = off[s0 + i];
+            const long long *p0 = reinterpret_cast<const long long *>(Gb + ob);
+            const long long *p1 = reinterpret_cast<const long long *>(Gv + ob);
             if constexpr (TOP) {
                 // the tap's window reaches above the domain: zero state there
                 // (row of a read = row0 + floor((o + GW/2) / GW), GW > 2 |dx|)
+                const int o = ob >> 3;
                 const int ry = row0 + (o + (GW >> 1) + 16 * GW) / GW - 16;
                 const int ryv = ry - (sdl + (GW >> 1) + 16 * GW) / GW + 16;
-                g[i] = ry >= 0 ? __ldg(Gt + o) : 0ll;
-                if (NMON == 3) g[i] -= ryv >= 0 ? __ldg(Gt + (o - sdl)) : 0ll;
+                g[i] = ry >= 0 ? __ldg(p0) : 0ll;
+                if (NMON == 3) g[i] -= ryv >= 0 ? __ldg(p1) : 0ll;
             } else {
-                g[i] = __ldg(Gt + o);
-                if (NMON == 3) g[i] -= __ldg(Gt + (o - sdl));
+                g[i] = __ldg(p0);
+                if (NMON == 3) g[i] -= __ldg(p1);
             }
         }
 #pragma unroll
@@ -267,7 +272,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
             const int r = i / nmax4, sl = i % nmax4;
             const bool real = sl < __ldg(V.counts + r);
             const int2 o = real ? __ldg(V.offs + r * V.nmax + sl) : make_int2(0, 0);
-            S.off[base + i] = o.y * a.gGW + o.x;
+            S.off[base + i] = 8 * (o.y * a.gGW + o.x);  // bytes
             S.num[base + i] = real ? __ldg(reinterpret_cast<const uint2 *>(V.n8) + r * V.nmax + sl) : make_uint2(0u, 0u);
         }
         base += nreg * nmax4;
