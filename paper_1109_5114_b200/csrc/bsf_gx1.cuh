@@ -56,8 +56,13 @@ struct Gx1Smem {
     uint2 num[GX1_SLOTS];
 };
 
-__device__ __forceinline__ int gx1_byte(unsigned w, int k) {  // signed byte k of w
-    return (int)((signed char)(unsigned char)(w >> (8 * k)));
+template <int K>
+__device__ __forceinline__ int gx1_byte(unsigned w) {  // signed byte K of w: one PRMT
+    // prmt selector nibbles: byte K, then three copies of its sign (K | 8)
+    // (PTX prmt default mode; __byte_perm ignores the nibbles' sign bit)
+    int r;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "n"(K | ((8 | K) << 4) | ((8 | K) << 8) | ((8 | K) << 12)));
+    return r;
 }
 
 // One tap: F(b + phi) for the region's window, exact integer contraction then
@@ -105,9 +110,16 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
         for (int i = 0; i < 4; ++i) {
             const uint2 nw = num[s0 + i];
             const int v0 = (int)(g[i] & 0x1FFFFF), v1 = (int)((g[i] >> 21) & 0x1FFFFF), v2 = (int)(g[i] >> 42);
+            int cm[6];  // the monomials' numerators, sign-extended (gen_lut order)
+            cm[0] = gx1_byte<0>(nw.x);
+            cm[1] = gx1_byte<1>(nw.x);
+            cm[2] = gx1_byte<2>(nw.x);
+            cm[3] = gx1_byte<3>(nw.x);
+            cm[4] = gx1_byte<0>(nw.y);
+            cm[5] = gx1_byte<1>(nw.y);
 #pragma unroll
             for (int m = 0; m < NMON; ++m) {
-                const int c = gx1_byte(m < 4 ? nw.x : nw.y, m & 3);
+                const int c = cm[m];
                 acc[0][m] += v0 * c;
                 acc[1][m] += v1 * c;
                 acc[2][m] += v2 * c;
