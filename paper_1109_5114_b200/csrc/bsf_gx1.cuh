@@ -234,10 +234,11 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
         sumF += fabs(F.hi);
     }
     const dd Ssum = fast_two_sum(h0, e0);
-    double norm = S.var[b][v].invL;  // 1 / L
+    double den = 1.0;  // prod_k a'_k over the directions in use (one division below)
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-        if (q < ns) norm /= apm[dir(q)];
+        if (q < ns) den *= apm[dir(q)];
+    const double norm = S.var[b][v].invL / den;  // 1 / (L prod a'_k)
     const double Sd = dd_to_d(Ssum);
     // rounding of the Horner steps and of the sum: (2 ntap + 8) u^2 sum_j |F_j|
     erel = 2.5e-30 * (double)(2 * ntap + 8) * sumF / fabs(Sd);
