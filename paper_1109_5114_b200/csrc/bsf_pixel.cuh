@@ -66,7 +66,7 @@ __device__ __forceinline__ int solve_scales(int basis, double C11, double C12, d
         if (lo - hi > 1e-12 * scale) return FLAG_INFEASIBLE;
         lo = hi = 0.5 * (lo + hi);
     }
-    auto dJ = [&](double t, double *d2) -> double {
+    auto dJ = [&](double t, double *d2, double *mag) -> double {
         double K11, K12, K22, k11, k12, k22;
         if (basis == BASIS_THETA) {
             double x1 = A1 - 0.5 * t, x3 = A3 - 0.5 * t;
@@ -87,15 +87,17 @@ __device__ __forceinline__ int solve_scales(int basis, double C11, double C12, d
             k12 = 0.4 * (P - Q);
         }
         *d2 = 2.0 * k11 * k11 + 2.0 * K11 + 4.0 * k12 * k12 + 2.0 * k22 * k22 + 2.0 * K22;
+        // magnitude of the terms: |J'| below 16 u of it is rounding noise
+        *mag = fabs(2.0 * K11 * k11) + fabs(4.0 * K12 * k12) + fabs(2.0 * K22 * k22);
         return 2.0 * K11 * k11 + 4.0 * K12 * k12 + 2.0 * K22 * k22;
     };
-    double t, d2;
+    double t, d2, mag;
     int flags = 0;
     if (lo == hi) {
         t = lo;
-    } else if (dJ(lo, &d2) >= 0.0) {
+    } else if (dJ(lo, &d2, &mag) >= 0.0) {
         t = lo;
-    } else if (dJ(hi, &d2) <= 0.0) {
+    } else if (dJ(hi, &d2, &mag) <= 0.0) {
         t = hi;
     } else {
         double a = lo, b = hi;
@@ -103,8 +105,10 @@ __device__ __forceinline__ int solve_scales(int basis, double C11, double C12, d
         double tol = 4e-16 * fmax(fabs(lo), fabs(hi));
         int it = 0;
         for (; it < 100; ++it) {
-            double g = dJ(t, &d2);
-            if (g == 0.0) break;
+            double g = dJ(t, &d2, &mag);
+            // converged to the rounding noise of J' (a tighter step tolerance
+            // alone would bisect down to it: ~50 steps instead of ~5)
+            if (fabs(g) <= 16.0 * 1.1102230246251565e-16 * mag) break;
             if (g < 0.0)
                 a = t;
             else
