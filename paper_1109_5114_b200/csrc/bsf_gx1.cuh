@@ -52,8 +52,8 @@ struct Gx1Smem {
     // byte offset 8 (dy GW + dx) into the running sums, and the numerators n_mu
     // (monomials in gen_lut order, int8, padded to 8 bytes); padding slots
     // have offset 0 and zero numerators
-    int off[GX1_SLOTS];
-    uint2 num[GX1_SLOTS];
+    alignas(16) int off[GX1_SLOTS];     // groups of four slots are read as one 16-byte word
+    alignas(16) uint2 num[GX1_SLOTS];
 };
 
 template <int K>
@@ -88,9 +88,14 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
     const uint2 *num = S.num + row;
     for (int s0 = 0; s0 < n4; s0 += 4) {
         long long g[4];
+        // rows start on multiples of four slots: one 16-byte shared load for
+        // the group's four offsets, two for its numerators
+        const int4 ob4 = *reinterpret_cast<const int4 *>(off + s0);
+        const uint4 nwa = *reinterpret_cast<const uint4 *>(num + s0);
+        const uint4 nwb = *reinterpret_cast<const uint4 *>(num + s0 + 2);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int ob = off[s0 + i];
+            const int ob = i == 0 ? ob4.x : i == 1 ? ob4.y : i == 2 ? ob4.z : ob4.w;
             const long long *p0 = reinterpret_cast<const long long *>(Gb + ob);
             const long long *p1 = reinterpret_cast<const long long *>(Gv + ob);
             if constexpr (TOP) {
@@ -108,7 +113,8 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const uint2 nw = num[s0 + i];
+            const uint2 nw = i == 0 ? make_uint2(nwa.x, nwa.y) : i == 1 ? make_uint2(nwa.z, nwa.w)
+                             : i == 2 ? make_uint2(nwb.x, nwb.y) : make_uint2(nwb.z, nwb.w);
             const int v0 = (int)(g[i] & 0x1FFFFF), v1 = (int)((g[i] >> 21) & 0x1FFFFF), v2 = (int)(g[i] >> 42);
             int cm[6];  // the monomials' numerators, sign-extended (gen_lut order)
             cm[0] = gx1_byte<0>(nw.x);
