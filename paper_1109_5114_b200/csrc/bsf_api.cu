@@ -124,6 +124,7 @@ struct bsf_plan_s {
     // sums of the whole image, read by the fused kernel's taps
     bool global_ok = false;              // every sum of every basis stays below 2^62
     int gshift[2] = {0, 0};              // limb split G = 2^k G1 + G0 per basis
+    int gvw[2] = {0, 0};                 // order-1 gather: two-limb width for the variants (TileArgs.gvw)
     int stile_global = 32;
     long long *gx_ws = nullptr;          // [nbases][nimg][GH][GW] int64
     // row strips (nranks > 1): own rows [y0, y1), block [b0, b1), halo; GLOBAL-mode
@@ -380,6 +381,15 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
         }
         // order 1: int8 numerators for the global-mode gather (bsf_gx1.cuh)
         V.n8 = nullptr;
+        V.nabs = 0.0;
+        if (exact) {
+            for (uint32_t r = 0; r < nreg; ++r)
+                for (int m = 0; m < V.nmon; ++m) {
+                    double sa = 0.0;
+                    for (int s2 = 0; s2 < V.nmax; ++s2) sa += fabs(num[((size_t)r * V.nmax + s2) * V.nmon + m]);
+                    V.nabs = sa > V.nabs ? sa : V.nabs;
+                }
+        }
         if (exact && p->d.order == 1 && V.nmon <= 8) {
             std::vector<signed char> n8((size_t)nreg * V.nmax * 8, 0);
             bool fits = true;
@@ -560,6 +570,19 @@ extern "C" bsf_status bsf_plan_create(const bsf_plan_desc *desc, const char *lut
             const int k = std::max(1, bits - kb);
             if (bits > 62 || k > kb) ok = false;
             p->gshift[b] = k;
+            // the order-1 gather's zero-scale variants: G(q) - G(q - s_k) is the
+            // three-level sum without direction k, at most 255 x the product of
+            // the other three line lengths; with sum_s |n| <= nabs the
+            // contraction fits two w-bit limbs in int32 when nabs 2^w < 2^31 and
+            // the sum stays below 2^2w, and E_mu (below 2^53) is exact in fp64
+            double lmin = 1e300, nv = 0.0;
+            for (int lv = 0; lv < 4; ++lv)
+                lmin = std::min(lmin, sy_order[b][lv] == 0 ? (double)g.GW : (double)(g.GH / sy_order[b][lv] + 1));
+            for (int v = 1; v < NVAR; ++v) nv = std::max(nv, host[b].var[v].nabs);
+            const double bvar = bound / 2.0 / lmin;
+            int w = 0;
+            while (w < 30 && ldexp(nv, w + 1) < 0x1p31) ++w;
+            p->gvw[b] = (nv > 0.0 && bvar < ldexp(1.0, 2 * w) && bvar * nv < 0x1p53) ? w : 0;
         }
         // the order-1 gather stages every table in use in shared memory
         int slots = 0;
@@ -1055,6 +1078,7 @@ static bsf_status filter_global(bsf_plan_s *p, const void *g, const void *cov, v
     for (int sl = 0; sl < geo.nbases; ++sl) {  // slot sl of the int64 buffer holds basis bases[sl]
         a.gglob[p->bases[sl]] = (const long long *)g + sl * slot;
         a.gshift[p->bases[sl]] = p->gshift[p->bases[sl]];
+        a.gvw[p->bases[sl]] = p->gvw[p->bases[sl]];
     }
     if (pts) {
         a.pts = pts;
@@ -1087,6 +1111,7 @@ static bsf_status filter_global_window(bsf_plan_s *p, const void *g, const void 
     for (int sl = 0; sl < geo.nbases; ++sl) {
         a.gglob[p->bases[sl]] = (const long long *)g + sl * slot;
         a.gshift[p->bases[sl]] = p->gshift[p->bases[sl]];
+        a.gvw[p->bases[sl]] = p->gvw[p->bases[sl]];
     }
     CUDA_TRY(launch_gx1(a, st, p->luts_dev, &p->nlaunch));
     return BSF_OK;

@@ -48,6 +48,7 @@ struct Gx1Smem {
     Gx1Var var[2][NVAR];
     unsigned char cnt[2][NVAR][GX1_MAXREG];   // window slots of the region
     int4 ext[2];                              // window offset extents (wxmin, wxmax, wymin, wymax) per basis
+    int vw[2];                                // TileArgs.gvw: two-limb width of the variants (0: three limbs)
     // per (basis, variant, region, slot), flat: the window offset as a linear
     // byte offset 8 (dy GW + dx) into the running sums, and the numerators n_mu
     // (monomials in gen_lut order, int8, padded to 8 bytes); padding slots
@@ -72,12 +73,14 @@ __device__ __forceinline__ int gx1_byte(unsigned w) {  // signed byte K of w: on
 // the domain (and the buffer has zero rows above it), so no read is bounds
 // checked.  Slots go in groups of four with all loads of a group issued before
 // its multiply-adds.
-template <int NMON, bool TOP>
+// NL = 2 (zero-scale variants where the plan proved it safe, TileArgs.gvw):
+// two limbs G' = 2^w v1 + v0, and E_mu (below 2^53) exact as one double.
+template <int NMON, bool TOP, int NL = 3>
 __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restrict__ Gt, int b, int v, int reg,
-                                      double fx, double fy, int sdl, int row0, int GW) {
-    int acc[3][NMON];
+                                      double fx, double fy, int sdl, int row0, int GW, int w = 21) {
+    int acc[NL][NMON];
 #pragma unroll
-    for (int l = 0; l < 3; ++l)
+    for (int l = 0; l < NL; ++l)
 #pragma unroll
         for (int m = 0; m < NMON; ++m) acc[l][m] = 0;
     const int n4 = (S.cnt[b][v][reg] + 3) & ~3;
@@ -115,7 +118,15 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
         for (int i = 0; i < 4; ++i) {
             const uint2 nw = i == 0 ? make_uint2(nwa.x, nwa.y) : i == 1 ? make_uint2(nwa.z, nwa.w)
                              : i == 2 ? make_uint2(nwb.x, nwb.y) : make_uint2(nwb.z, nwb.w);
-            const int v0 = (int)(g[i] & 0x1FFFFF), v1 = (int)((g[i] >> 21) & 0x1FFFFF), v2 = (int)(g[i] >> 42);
+            int vl[NL];
+            if constexpr (NL == 3) {
+                vl[0] = (int)(g[i] & 0x1FFFFF);
+                vl[1] = (int)((g[i] >> 21) & 0x1FFFFF);
+                vl[NL - 1] = (int)(g[i] >> 42);
+            } else {
+                vl[0] = (int)(g[i] & ((1ll << w) - 1));
+                vl[NL - 1] = (int)(g[i] >> w);
+            }
             int cm[6];  // the monomials' numerators, sign-extended (gen_lut order)
             cm[0] = gx1_byte<0>(nw.x);
             cm[1] = gx1_byte<1>(nw.x);
@@ -126,9 +137,8 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
 #pragma unroll
             for (int m = 0; m < NMON; ++m) {
                 const int c = cm[m];
-                acc[0][m] += v0 * c;
-                acc[1][m] += v1 * c;
-                acc[2][m] += v2 * c;
+#pragma unroll
+                for (int l = 0; l < NL; ++l) acc[l][m] += vl[l] * c;
             }
         }
     }
@@ -138,8 +148,13 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
     dd E[NMON];
 #pragma unroll
     for (int m = 0; m < NMON; ++m) {
-        const long long hi = ((long long)acc[2][m] << 21) + acc[1][m];
-        E[m] = two_sum((double)hi * 0x1p21, (double)acc[0][m]);
+        if constexpr (NL == 3) {
+            const long long hi = ((long long)acc[NL - 1][m] << 21) + acc[1][m];
+            E[m] = two_sum((double)hi * 0x1p21, (double)acc[0][m]);
+        } else {  // an integer below 2^53: exact (the scaling by 2^w is exact)
+            E[m].hi = fma((double)acc[NL - 1][m], (double)(1ll << w), (double)acc[0][m]);
+            E[m].lo = 0.0;
+        }
     }
     // Horner: rows i (x power) in phi_y, then phi_x; monomial order (i, j):
     // i = deg..0, j = deg - i..0 (lut/gen_lut.py)
@@ -229,8 +244,14 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
         const long long *Gt = G + ((ptrdiff_t)by * GW + (x + ix + P));
         // windows that reach above row 0 read the zero state there (checked
         // loads); all other reads are inside the domain (reach checked)
-        const dd F = by + wymin - 2 >= 0 ? gx1_tap<NMON, false>(S, Gt, b, v, reg, fx, fy, sdl, by, GW)
-                                         : gx1_tap<NMON, true>(S, Gt, b, v, reg, fx, fy, sdl, by, GW);
+        dd F;
+        const int vw = NMON == 3 ? S.vw[b] : 0;
+        if (by + wymin - 2 < 0)
+            F = gx1_tap<NMON, true>(S, Gt, b, v, reg, fx, fy, sdl, by, GW);
+        else if (NMON == 3 && vw)
+            F = gx1_tap<NMON, false, 2>(S, Gt, b, v, reg, fx, fy, sdl, by, GW, vw);
+        else
+            F = gx1_tap<NMON, false>(S, Gt, b, v, reg, fx, fy, sdl, by, GW);
         macs += S.cnt[b][v][reg] * NMON;  // algorithmic: window x monomials
         // compensated signed sum: TwoSum on the heads, small terms in e0
         const double fh = sgn > 0 ? F.hi : -F.hi, fl = sgn > 0 ? F.lo : -F.lo;
@@ -286,6 +307,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
         const int nmax4 = (V.nmax + 3) & ~3;
         if (tid == 0) S.var[b][v] = Gx1Var{nmax4, base, 1.0 / V.L};
         if (tid == 0 && v == 0) S.ext[b] = make_int4(luts[b].wxmin, luts[b].wxmax, luts[b].wymin, luts[b].wymax);
+        if (tid == 0 && v == 0) S.vw[b] = a.gvw[b];
         for (int i = tid; i < nreg; i += GX1_BLOCK) S.cnt[b][v][i] = (unsigned char)__ldg(V.counts + i);
         for (int i = tid; i < nreg * nmax4; i += GX1_BLOCK) {
             const int r = i / nmax4, sl = i % nmax4;

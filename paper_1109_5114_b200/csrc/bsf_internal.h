@@ -108,6 +108,7 @@ struct LutVar {
     const signed char *n8; // order 1 (global-mode gather, bsf_gx1.cuh): [nreg][nmax][8] numerators n as int8
                            // (monomials in gen_lut order, zero padded); null when some |n| > 127
     float mean_count;      // window slots averaged over the regions (work-item cost estimate)
+    double nabs;           // max over (region, monomial) of sum_s |n| (order 1: the gather's limb widths)
     double bnd;            // bound on |F - F^| (units 2^e) of the split contraction: gamma_{n+1} 0.5 max_reg sum_s,mu |n|
     double L;              // common denominator
 };
@@ -192,6 +193,8 @@ struct TileArgs {
                                 // bsf_preintegrate_exact sums [nimg][gGH][gGW] of that basis
     int gP, gGW, gGH;
     int gshift[2];
+    int gvw[2];                 // order-1 gather, per basis id: limb width w of the two-limb contraction
+                                // of zero-scale variant differences (0: three 21-bit limbs)
 };
 constexpr int SCHED_NBIN = 128;
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per device
