@@ -78,7 +78,10 @@ static bsf_status set_err(bsf_status s, const std::string &msg) {
             return set_err(BSF_ECUDA, std::string(#expr ": ") + cudaGetErrorString(e_));      \
     } while (0)
 
-constexpr int BSF_HOST_BANDS = 8;  // bsf_run_host (global mode): row bands of the copy / compute pipeline
+#ifndef BSF_HOST_BANDS_T
+#define BSF_HOST_BANDS_T 16
+#endif
+constexpr int BSF_HOST_BANDS = BSF_HOST_BANDS_T;  // bsf_run_host (global mode): row bands of the copy / compute pipeline
 
 struct bsf_plan_s {
     bsf_plan_desc d;
