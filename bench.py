@@ -369,10 +369,12 @@ def roofline(w, r, mode, plan, stats, npx, kms, pms, ms):
         # exact contraction of Eq. (11): window x monomials multiply-adds per
         # tap (counted by the kernel, bsf_stats.macs), each an int64 x int8
         # product done as 3 int32 limb multiply-adds (no rounding).  Peak: the
-        # int32 multiply-add issue rate, 128 lanes/clk/SM (IMAD on the FMA pipe).
+        # int32 multiply-add rate: IMAD issues on the FMA pipe at a reciprocal
+        # throughput of 2 cycles per warp instruction per SMSP
+        # (B300_MICROARCH.md, 'Pipe rates'), i.e. 64 lanes/clk/SM.
         imad = 3.0 * stats["macs"] / max(stats["pixels"], 1) * npx
         achieved = imad / (kms * 1e-3) / 1e12
-        peak = nsm * 128 * sm_mhz * 1e6 / 1e12
+        peak = nsm * 64 * sm_mhz * 1e6 / 1e12
         g_bytes = geo.nbases * geo.g_height * geo.g_width * 8 * (npx // (w.width * w.height))
         pre_bytes = npx * in_b + g_bytes  # read f once, write g once
         gat_bytes = g_bytes + npx * (12 + 8)  # read g once (taps from L2), cov 3 x f32, out f64
@@ -381,7 +383,8 @@ def roofline(w, r, mode, plan, stats, npx, kms, pms, ms):
         return {"bound": "alu", "kernel": "gx1_kernel (order-1 exact integer gather)",
                 "achieved": achieved, "peak": peak, "unit": "Tintop/s", "frac": achieved / peak,
                 "traffic": _traffic(w.name, r, "gx1_kernel"),
-                "peak_source": "%d SM x 128 int32 multiply-add lanes/clk x %.0f MHz (sm_max, %s)" % (nsm, sm_mhz, src),
+                "peak_source": "%d SM x 64 int32 multiply-adds/clk (IMAD on the FMA pipe, 2 cycles per warp "
+                               "instruction per SMSP: B300_MICROARCH.md) x %.0f MHz (sm_max, %s)" % (nsm, sm_mhz, src),
                 "algorithmic": "3 int32 limb multiply-adds per (tap, window slot, monomial): %.0f per px" % (
                     imad / npx),
                 "kernel_ms": kms, "share_of_step": kms / ms if ms else None,
