@@ -140,6 +140,7 @@ struct bsf_plan_s {
     bool opt_fused = true;
     bool opt_order = true;
     int opt_global_kernel = 1;  // global mode: 1 the order-1 integer gather (bsf_gx1.cuh), 0 the fused kernel
+    int opt_gx1_dp4a = 0;       // order-1 gather: 1 byte-plane dp4a contraction, 0 three 21-bit IMAD limbs
     double opt_split_tol = BSF_SPLIT_TOL_DEFAULT;
 };
 
@@ -1083,6 +1084,7 @@ static bsf_status filter_global(bsf_plan_s *p, const void *g, const void *cov, v
         a.gshift[p->bases[sl]] = p->gshift[p->bases[sl]];
         a.gvw[p->bases[sl]] = p->gvw[p->bases[sl]];
     }
+    a.gdp4a = p->opt_gx1_dp4a;
     if (pts) {
         a.pts = pts;
         a.npts = npts;
@@ -1116,6 +1118,7 @@ static bsf_status filter_global_window(bsf_plan_s *p, const void *g, const void 
         a.gshift[p->bases[sl]] = p->gshift[p->bases[sl]];
         a.gvw[p->bases[sl]] = p->gvw[p->bases[sl]];
     }
+    a.gdp4a = p->opt_gx1_dp4a;
     CUDA_TRY(launch_gx1(a, st, p->luts_dev, &p->nlaunch));
     return BSF_OK;
 }
@@ -1597,6 +1600,8 @@ extern "C" bsf_status bsf_debug_option(bsf_plan_t p, const char *name, double va
         set_scan_tma(value != 0.0);
     } else if (n == "global_kernel") {
         p->opt_global_kernel = value != 0.0 ? 1 : 0;
+    } else if (n == "gx1_dp4a") {
+        p->opt_gx1_dp4a = value != 0.0 ? 1 : 0;
     } else if (n == "split_tol") {
         if (!(value >= 0.0)) return set_err(BSF_EINVAL, "split_tol must be >= 0");
         p->opt_split_tol = value;

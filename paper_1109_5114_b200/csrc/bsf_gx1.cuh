@@ -179,10 +179,122 @@ __device__ __forceinline__ dd gx1_tap(const Gx1Smem &S, const long long *__restr
     return fast_two_sum(h, l);
 }
 
+// The same exact contraction on byte planes with the 4-way int8 dot product
+// (IDP.4A): G' = sum_j 2^{8j} B_j with B_0..B_6 unsigned bytes and B_7 the
+// signed top byte (two's complement), so
+//   E_mu = sum_j 2^{8j} sum_s B_j(G'_s) n_{s,mu},
+// and one dp4a takes four window slots of one plane against the four slots'
+// numerators of one monomial.  The numerators are staged TRANSPOSED per group
+// of four slots (word mu of a group = the four slots' n_mu as int8), so no
+// sign extension is needed; the four values' bytes are transposed into eight
+// plane words by 16 PRMTs.  Per plane and monomial |sum| <= 255 sum_s |n| <
+// 2^18, so the pair p = acc_j + 2^8 acc_{j+1} fits int32 and
+// E = 2^32 (p45 + 2^16 p67) + (p01 + 2^16 p23) is exact as a double-double
+// (both brackets are integers below 2^53).
+__device__ __forceinline__ int gx1_dp4a_us(unsigned a, unsigned b, int c) {  // unsigned a bytes x signed b bytes
+    int d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int gx1_dp4a_ss(unsigned a, unsigned b, int c) {  // signed x signed (top plane)
+    int d;
+    asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+template <int NMON, bool TOP>
+__device__ __forceinline__ dd gx1_tap_dp(const Gx1Smem &S, const long long *__restrict__ Gt, int b, int v, int reg,
+                                         double fx, double fy, int sdl, int row0, int GW) {
+    int acc[8][NMON];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int m = 0; m < NMON; ++m) acc[j][m] = 0;
+    const int n4 = (S.cnt[b][v][reg] + 3) & ~3;
+    const int row = S.var[b][v].base + reg * S.var[b][v].nmax4;
+    const int *off = S.off + row;
+    const char *Gb = reinterpret_cast<const char *>(Gt);
+    const char *Gv = reinterpret_cast<const char *>(Gt - sdl);
+    const uint2 *num = S.num + row;  // transposed per group of four slots (gx1_kernel staging)
+    for (int s0 = 0; s0 < n4; s0 += 4) {
+        long long g[4];
+        const int4 ob4 = *reinterpret_cast<const int4 *>(off + s0);
+        const uint4 nwa = *reinterpret_cast<const uint4 *>(num + s0);
+        uint4 nwb = make_uint4(0u, 0u, 0u, 0u);
+        if constexpr (NMON > 4) nwb = *reinterpret_cast<const uint4 *>(num + s0 + 2);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int ob = i == 0 ? ob4.x : i == 1 ? ob4.y : i == 2 ? ob4.z : ob4.w;
+            const long long *p0 = reinterpret_cast<const long long *>(Gb + ob);
+            const long long *p1 = reinterpret_cast<const long long *>(Gv + ob);
+            if constexpr (TOP) {
+                const int o = ob >> 3;
+                const int ry = row0 + (o + (GW >> 1) + 16 * GW) / GW - 16;
+                const int ryv = ry - (sdl + (GW >> 1) + 16 * GW) / GW + 16;
+                g[i] = ry >= 0 ? __ldg(p0) : 0ll;
+                if (NMON == 3) g[i] -= ryv >= 0 ? __ldg(p1) : 0ll;
+            } else {
+                g[i] = __ldg(p0);
+                if (NMON == 3) g[i] -= __ldg(p1);
+            }
+        }
+        // byte transpose: plane j = byte j of the four values
+        unsigned pl[8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const unsigned w0 = (unsigned)((unsigned long long)g[0] >> (32 * h));
+            const unsigned w1 = (unsigned)((unsigned long long)g[1] >> (32 * h));
+            const unsigned w2 = (unsigned)((unsigned long long)g[2] >> (32 * h));
+            const unsigned w3 = (unsigned)((unsigned long long)g[3] >> (32 * h));
+            const unsigned a01 = __byte_perm(w0, w1, 0x5140), a23 = __byte_perm(w2, w3, 0x5140);
+            const unsigned b01 = __byte_perm(w0, w1, 0x7362), b23 = __byte_perm(w2, w3, 0x7362);
+            pl[4 * h + 0] = __byte_perm(a01, a23, 0x5410);
+            pl[4 * h + 1] = __byte_perm(a01, a23, 0x7632);
+            pl[4 * h + 2] = __byte_perm(b01, b23, 0x5410);
+            pl[4 * h + 3] = __byte_perm(b01, b23, 0x7632);
+        }
+        const unsigned nw[8] = {nwa.x, nwa.y, nwa.z, nwa.w, nwb.x, nwb.y, nwb.z, nwb.w};
+#pragma unroll
+        for (int m = 0; m < NMON; ++m) {
+#pragma unroll
+            for (int j = 0; j < 7; ++j) acc[j][m] = gx1_dp4a_us(pl[j], nw[m], acc[j][m]);
+            acc[7][m] = gx1_dp4a_ss(pl[7], nw[m], acc[7][m]);
+        }
+    }
+    dd E[NMON];
+#pragma unroll
+    for (int m = 0; m < NMON; ++m) {
+        const int p01 = acc[0][m] + acc[1][m] * 256, p23 = acc[2][m] + acc[3][m] * 256;
+        const int p45 = acc[4][m] + acc[5][m] * 256, p67 = acc[6][m] + acc[7][m] * 256;
+        const double lo = fma((double)p23, 0x1p16, (double)p01);  // exact: integers below 2^53
+        const double hi = fma((double)p67, 0x1p16, (double)p45);
+        E[m] = two_sum(hi * 0x1p32, lo);
+    }
+    double h, l;
+    if constexpr (NMON == 6) {  // (2,0) | (1,1) (1,0) | (0,2) (0,1) (0,0)
+        double r1h = E[1].hi, r1l = E[1].lo;
+        comp_step(r1h, r1l, fy, E[2].hi, E[2].lo);
+        double r0h = E[3].hi, r0l = E[3].lo;
+        comp_step(r0h, r0l, fy, E[4].hi, E[4].lo);
+        comp_step(r0h, r0l, fy, E[5].hi, E[5].lo);
+        h = E[0].hi;
+        l = E[0].lo;
+        comp_step(h, l, fx, r1h, r1l);
+        comp_step(h, l, fx, r0h, r0l);
+    } else {  // (1,0) | (0,1) (0,0)
+        double r0h = E[1].hi, r0l = E[1].lo;
+        comp_step(r0h, r0l, fy, E[2].hi, E[2].lo);
+        h = E[0].hi;
+        l = E[0].lo;
+        comp_step(h, l, fx, r0h, r0l);
+    }
+    return fast_two_sum(h, l);
+}
+
 // The pixel's (r+1)^ns = 2^ns taps (Table 1, generalised to
 // both bases; shift of Eq. (10) absorbed in the uncentred interpolant, DESIGN.md
 // R3): D_j = sum_k (1/2 - j_k) a'_k s_k, sign (-1)^{sum j}.
-template <int NMON>
+template <int NMON, bool DP>
 __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__restrict__ G, int GW, int P,
                                            int b, int drop, const double *apm, int x, int y, double &erel,
                                            unsigned int &macs) {
@@ -246,7 +358,14 @@ __device__ __forceinline__ double gx1_mesh(const Gx1Smem &S, const long long *__
         // loads); all other reads are inside the domain (reach checked)
         dd F;
         const int vw = NMON == 3 ? S.vw[b] : 0;
-        if (by + wymin - 2 < 0)
+        // DP: byte-plane dp4a contraction on the transposed tables (full
+        // taps, and variants without the two-limb form); see gx1_kernel staging
+        if (DP && !(NMON == 3 && vw)) {
+            if (by + wymin - 2 < 0)
+                F = gx1_tap_dp<NMON, true>(S, Gt, b, v, reg, fx, fy, sdl, by, GW);
+            else
+                F = gx1_tap_dp<NMON, false>(S, Gt, b, v, reg, fx, fy, sdl, by, GW);
+        } else if (by + wymin - 2 < 0)
             F = gx1_tap<NMON, true>(S, Gt, b, v, reg, fx, fy, sdl, by, GW);
         else if (NMON == 3 && vw)
             F = gx1_tap<NMON, false, 2>(S, Gt, b, v, reg, fx, fy, sdl, by, GW, vw);
@@ -284,6 +403,7 @@ __device__ __noinline__ double gx1_fallback(const long long *G, int P, int GW, i
 #ifndef GX1_MINB
 #define GX1_MINB 2
 #endif
+template <bool DP>
 __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
     __shared__ Gx1Smem S;
     const int tid = threadIdx.x;
@@ -314,7 +434,18 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
             const bool real = sl < __ldg(V.counts + r);
             const int2 o = real ? __ldg(V.offs + r * V.nmax + sl) : make_int2(0, 0);
             S.off[base + i] = 8 * (o.y * a.gGW + o.x);  // bytes
-            S.num[base + i] = real ? __ldg(reinterpret_cast<const uint2 *>(V.n8) + r * V.nmax + sl) : make_uint2(0u, 0u);
+            const uint2 nv = real ? __ldg(reinterpret_cast<const uint2 *>(V.n8) + r * V.nmax + sl) : make_uint2(0u, 0u);
+            if (DP && (v == 0 || !a.gvw[b])) {
+                // transposed per group of four slots (rows start on multiples
+                // of four): byte 4 mu + (slot & 3) of the group holds n_mu
+                unsigned char *g8 = reinterpret_cast<unsigned char *>(S.num + ((base + i) & ~3));
+                const int q = (base + i) & 3;
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+                    g8[4 * m + q] = (unsigned char)((m < 4 ? nv.x >> (8 * m) : nv.y >> (8 * (m - 4))) & 0xFFu);
+            } else {
+                S.num[base + i] = nv;
+            }
         }
         base += nreg * nmax4;
     }
@@ -471,8 +602,8 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
                 } else {
                     const long long *G = a.gglob[basis] + (size_t)img * a.gGH * a.gGW;
                     unsigned int pm = 0;
-                    res = drop < 0 ? gx1_mesh<6>(S, G, a.gGW, a.gP, basis, drop, s_ap[p], x, y, erel, pm)
-                                   : gx1_mesh<3>(S, G, a.gGW, a.gP, basis, drop, s_ap[p], x, y, erel, pm);
+                    res = drop < 0 ? gx1_mesh<6, DP>(S, G, a.gGW, a.gP, basis, drop, s_ap[p], x, y, erel, pm)
+                                   : gx1_mesh<3, DP>(S, G, a.gGW, a.gP, basis, drop, s_ap[p], x, y, erel, pm);
                     macs += pm;
                     if (!(erel <= a.split_tol)) {  // NaN-safe: the double-double mesh on the same sums
                         PixelScales ps;
@@ -525,19 +656,23 @@ int gx1_slots() {
     int dev = 0, sms = 148, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gx1_kernel, GX1_BLOCK, GX1_DYN_SMEM) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gx1_kernel<false>, GX1_BLOCK, GX1_DYN_SMEM) != cudaSuccess ||
         per < 1)
         per = 1;
     return sms * per;
 }
 
 cudaError_t launch_gx1(const TileArgs &a, cudaStream_t st, const LutBasis *luts, long long *nl) {
-    static std::atomic<unsigned long long> attr{0ull};
-    cudaError_t e = set_smem_attr(gx1_kernel, (int)GX1_DYN_SMEM, attr);
+    static std::atomic<unsigned long long> attr[2] = {{0ull}, {0ull}};
+    cudaError_t e = a.gdp4a ? set_smem_attr(gx1_kernel<true>, (int)GX1_DYN_SMEM, attr[1])
+                            : set_smem_attr(gx1_kernel<false>, (int)GX1_DYN_SMEM, attr[0]);
     if (e != cudaSuccess) return e;
     static int slots = 0;
     if (!slots) slots = gx1_slots();
-    gx1_kernel<<<slots, GX1_BLOCK, GX1_DYN_SMEM, st>>>(a, luts);
+    if (a.gdp4a)
+        gx1_kernel<true><<<slots, GX1_BLOCK, GX1_DYN_SMEM, st>>>(a, luts);
+    else
+        gx1_kernel<false><<<slots, GX1_BLOCK, GX1_DYN_SMEM, st>>>(a, luts);
     ++*nl;
     return cudaGetLastError();
 }

@@ -195,6 +195,7 @@ struct TileArgs {
     int gshift[2];
     int gvw[2];                 // order-1 gather, per basis id: limb width w of the two-limb contraction
                                 // of zero-scale variant differences (0: three 21-bit limbs)
+    int gdp4a;                  // order-1 gather: byte-plane dp4a contraction (bsf_gx1.cuh gx1_tap_dp)
 };
 constexpr int SCHED_NBIN = 128;
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per device

@@ -136,3 +136,39 @@ def test_run_host_pipeline_global_mode(out_f32):
         plan.run_host(f_h, c_h, o_h)
     torch.cuda.synchronize()
     assert torch.equal(o_h, dev)
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2])
+def test_gx1_dp4a_contraction_is_bit_identical(policy):
+    """The byte-plane dp4a contraction (bsf_gx1.cuh gx1_tap_dp) and the
+    three-limb IMAD contraction both form E_mu exactly, so the outputs agree
+    bit for bit (ragged 150 x 97 image with sums reaching above row 0,
+    zero-scale variants, both bases), and both match the oracle at 1e-9."""
+    w = synth.workload(3, width=150, height=97, max_sigma=40.0, extra={"grid_span": 300})
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    outs = []
+    for dp in (0, 1):
+        plan = make_plan(w, policy=policy, anchor=bsf.BSF_ANCHOR_GLOBAL)
+        plan.debug_option("gx1_dp4a", dp)
+        outs.append(gpu_full(plan, img[None], cov))
+        st = plan.stats(reset=True)
+        assert st["status"] == 0 and st["double_double"] == 0
+    assert torch.equal(outs[0], outs[1])
+    ys, xs = np.mgrid[0:w.height:5, 0:w.width:5]
+    pts = torch.tensor(np.stack([0 * xs.ravel(), xs.ravel(), ys.ravel()], 1), dtype=torch.int32)
+    err, _ = _check(w, img, cov, pts, outs[1], policy=policy)
+    assert err <= 1e-9, err
+
+
+def test_gx1_dp4a_config3_full_size_bit_identical():
+    """Config 3 at full size (sums up to 2^57: all eight byte planes live):
+    the dp4a and IMAD contractions give the same image bit for bit."""
+    w = synth.workload(3)
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    outs = []
+    for dp in (0, 1):
+        plan = make_plan(w, anchor=bsf.BSF_ANCHOR_AUTO)
+        assert plan.geometry.global_mode == 1
+        plan.debug_option("gx1_dp4a", dp)
+        outs.append(gpu_full(plan, img[None], cov))
+    assert torch.equal(outs[0], outs[1])
