@@ -82,6 +82,10 @@ static bsf_status set_err(bsf_status s, const std::string &msg) {
 #define BSF_HOST_BANDS_T 16
 #endif
 constexpr int BSF_HOST_BANDS = BSF_HOST_BANDS_T;  // bsf_run_host (global mode): row bands of the copy / compute pipeline
+#ifndef BSF_SCAN_BANDS_T
+#define BSF_SCAN_BANDS_T 4
+#endif
+constexpr int BSF_SCAN_BANDS = BSF_SCAN_BANDS_T;  // bsf_run_host (global mode): image row bands of the banded scans
 
 struct bsf_plan_s {
     bsf_plan_desc d;
@@ -118,6 +122,10 @@ struct bsf_plan_s {
     cudaStream_t s_in = nullptr, s_out = nullptr;  // bsf_run_host pipeline (global mode): copy streams
     cudaStream_t s_c2 = nullptr;                   // second compute stream (odd bands fill the even bands' tails)
     cudaEvent_t ev[2 * BSF_HOST_BANDS + 5] = {};
+    cudaEvent_t ev_fb[BSF_SCAN_BANDS] = {};          // bsf_run_host: image band k is on the device
+    cudaEvent_t ev_sb[2][BSF_SCAN_BANDS] = {};       // bsf_run_host: image band k of basis slot sl pre-integrated
+    cudaStream_t s_scan[2] = {nullptr, nullptr};     // bsf_run_host: banded scans, one stream per basis slot
+    unsigned long long *hcarry = nullptr;            // bsf_run_host banded scans: [2 parity][2 slots][levels][nimg][2][GW]
     // the two bases' running sums are independent: basis 1 runs on a side
     // stream forked from (and joined back into) the caller's stream
     cudaStream_t s_side = nullptr;
@@ -708,8 +716,18 @@ extern "C" bsf_status bsf_plan_destroy(bsf_plan_t p) {
         cudaStreamDestroy(p->s_in);
         cudaStreamDestroy(p->s_out);
         cudaStreamDestroy(p->s_c2);
+        for (cudaStream_t q : p->s_scan)
+            if (q) {
+                cudaStreamSynchronize(q);
+                cudaStreamDestroy(q);
+            }
         for (cudaEvent_t e : p->ev)
             if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : p->ev_fb)
+            if (e) cudaEventDestroy(e);
+        for (auto &row : p->ev_sb)
+            for (cudaEvent_t e : row)
+                if (e) cudaEventDestroy(e);
     }
     if (p->s_side) {
         cudaStreamSynchronize(p->s_side);
@@ -1079,6 +1097,7 @@ static bsf_status filter_global(bsf_plan_s *p, const void *g, const void *cov, v
     a.gP = geo.P;
     a.gGW = geo.GW;
     a.gGH = geo.GH;
+    a.gGHv = geo.GH;
     for (int sl = 0; sl < geo.nbases; ++sl) {  // slot sl of the int64 buffer holds basis bases[sl]
         a.gglob[p->bases[sl]] = (const long long *)g + sl * slot;
         a.gshift[p->bases[sl]] = p->gshift[p->bases[sl]];
@@ -1101,7 +1120,7 @@ static bsf_status filter_global(bsf_plan_s *p, const void *g, const void *cov, v
 // the order-1 gather on output rows [y0, y0 + h) only (cov and out hold those
 // rows: [batch][3][h][W] and [nimg][h][W]); y0 a multiple of 32
 static bsf_status filter_global_window(bsf_plan_s *p, const void *g, const void *cov, void *out, int y0, int h,
-                                       cudaStream_t st) {
+                                       int rows_ready, cudaStream_t st) {
     bsf_status s = ensure_tile_ws(p, false);
     if (s != BSF_OK) return s;
     const Geometry &geo = p->geo;
@@ -1111,6 +1130,7 @@ static bsf_status filter_global_window(bsf_plan_s *p, const void *g, const void 
     a.gP = geo.P;
     a.gGW = geo.GW;
     a.gGH = geo.GH;
+    a.gGHv = rows_ready;
     a.oy0 = y0;
     a.oH = h;
     for (int sl = 0; sl < geo.nbases; ++sl) {
@@ -1417,6 +1437,53 @@ extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov,
 // band as each band's covariance lands (its output row window), and each
 // finished band of the output goes back on a copy-out stream (the H2D and
 // D2H engines work in parallel).  The caller's stream waits for the last copy.
+// The single global pre-integration of bsf_run_host's staged image in row
+// bands (Alg. 3 step 2): band k of every image is scanned
+// once its rows are on the device (event ev_fb[k]), level by level, each level
+// with a vertical step starting from the level's last s_y rows of band k - 1
+// (the scan carry, copied out right after that level ran: the levels run in
+// place).  The same arithmetic as preintegrate_exact_strip's rank chain, so
+// the sums equal bsf_preintegrate_exact's bit for bit.  Each basis runs on its
+// own scan stream and records ev_sb[slot][k] after band k: a gather band waits
+// only for the scan bands its footprint reaches.
+// bsf_run_host's staged images (u8, global mode) start on 16-byte boundaries:
+// the scans read image i's band through its own base pointer, and the u8 row
+// loads assume a 4-byte aligned base
+static size_t host_f_pitch(const Geometry &g) { return ((size_t)g.H * g.W + 15) / 16 * 16; }
+
+static bsf_status banded_scans_basis(bsf_plan_s *p, int sl, int k, int srows, int nsb, cudaStream_t ss) {
+    const Geometry &g = p->geo;
+    const int nlev = 4 * p->d.order;
+    const size_t GW = g.GW, rowset = (size_t)g.nimg * 2 * GW;  // one level's carry: [nimg][2][GW]
+    unsigned long long *gsl = (unsigned long long *)p->gx_ws + sl * (size_t)g.nimg * g.GH * GW;
+    const int y0 = k * srows;
+    const bool last = k == nsb - 1;
+    Geometry gs = g;
+    gs.nimg = 1;
+    gs.H = std::min(srows, g.H - y0);
+    gs.Pb = last ? g.Pb : 0;
+    gs.GH = gs.H + gs.Pb;
+    CUDA_TRY(cudaStreamWaitEvent(ss, p->ev_fb[k], 0));
+    for (int lv = 0; lv < nlev; ++lv) {
+        int sx, sy;
+        scan_step(p->bases[sl], lv, &sx, &sy);
+        unsigned long long *cin = p->hcarry + (((size_t)((k + 1) & 1) * 2 + sl) * nlev + lv) * rowset;
+        unsigned long long *cout = p->hcarry + (((size_t)(k & 1) * 2 + sl) * nlev + lv) * rowset;
+        for (int i = 0; i < g.nimg; ++i) {
+            const uint8_t *fi = (const uint8_t *)p->f_stage + (size_t)i * host_f_pitch(g) + (size_t)y0 * g.W;
+            unsigned long long *gi = gsl + ((size_t)i * g.GH + y0) * GW;
+            CUDA_TRY(launch_scan_level(fi, 1, gi, 1, gs, p->bases[sl], lv,
+                                       (sy > 0 && k > 0) ? cin + (size_t)i * 2 * GW : nullptr, ss));
+            ++p->nlaunch;
+            if (sy > 0 && !last)  // this band's last sy rows of the level: the next band's carry
+                CUDA_TRY(cudaMemcpyAsync(cout + (size_t)i * 2 * GW, gi + (size_t)(gs.GH - sy) * GW,
+                                         (size_t)sy * GW * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, ss));
+        }
+    }
+    CUDA_TRY(cudaEventRecord(p->ev_sb[sl][k], ss));
+    return BSF_OK;
+}
+
 static bsf_status run_host_global(bsf_plan_s *p, const void *f_host, const void *cov_host, void *out_host,
                                   cudaStream_t st) {
     const Geometry &g = p->geo;
@@ -1425,36 +1492,18 @@ static bsf_status run_host_global(bsf_plan_s *p, const void *f_host, const void 
         CUDA_TRY(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&p->s_c2, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&p->s_scan[i], cudaStreamNonBlocking));
         for (int i = 0; i < 2 * BSF_HOST_BANDS + 5; ++i)
             CUDA_TRY(cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming));
+        for (int i = 0; i < BSF_SCAN_BANDS; ++i) {
+            CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fb[i], cudaEventDisableTiming));
+            for (int sl = 0; sl < 2; ++sl) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_sb[sl][i], cudaEventDisableTiming));
+        }
     }
-    cudaEvent_t ev_start = p->ev[0], ev_f = p->ev[1], ev_end = p->ev[2], ev_pre = p->ev[3], ev_c2 = p->ev[4];
+    cudaEvent_t ev_start = p->ev[0], ev_end = p->ev[2], ev_c2 = p->ev[4];
     cudaEvent_t *ev_cov = p->ev + 5, *ev_band = p->ev + 5 + BSF_HOST_BANDS;
     p->last = st;
-    const size_t plane = (size_t)g.H * g.W, fes = p->d.in_dtype == BSF_U8 ? 1 : 4,
-                 oes = p->d.out_dtype == BSF_F32 ? 4 : 8;
-    // bands of whole gather tiles (rows multiple of 32)
-    const int rows = ((g.H + nb - 1) / nb + 31) / 32 * 32;
-    CUDA_TRY(cudaEventRecord(ev_start, st));  // earlier work on the caller's stream comes first
-    CUDA_TRY(cudaStreamWaitEvent(p->s_in, ev_start, 0));
-    CUDA_TRY(cudaMemcpyAsync(p->f_stage, f_host, (size_t)g.nimg * plane * fes, cudaMemcpyHostToDevice, p->s_in));
-    CUDA_TRY(cudaEventRecord(ev_f, p->s_in));
-    int nband = 0;
-    for (int y0 = 0; y0 < g.H; y0 += rows, ++nband) {
-        const int h = std::min(rows, g.H - y0);
-        // the band's covariance as planes [batch][3][h][W], stored contiguously at
-        // float offset batch 3 y0 W of cov_stage (the bands tile the buffer)
-        float *cb = (float *)p->cov_stage + (size_t)p->d.batch * 3 * (size_t)y0 * g.W;
-        for (int b = 0; b < p->d.batch; ++b)
-            for (int c = 0; c < 3; ++c)
-                CUDA_TRY(cudaMemcpyAsync(cb + ((size_t)b * 3 + c) * (size_t)h * g.W,
-                                         (const float *)cov_host + ((size_t)b * 3 + c) * plane + (size_t)y0 * g.W,
-                                         (size_t)h * g.W * sizeof(float), cudaMemcpyHostToDevice, p->s_in));
-        CUDA_TRY(cudaEventRecord(ev_cov[nband], p->s_in));
-    }
-    // pre-integration on the caller's stream once the image is in
-    CUDA_TRY(cudaStreamWaitEvent(st, ev_f, 0));
-    const size_t slot = (size_t)g.nimg * g.GH * g.GW;
+    const size_t plane = (size_t)g.H * g.W, oes = p->d.out_dtype == BSF_F32 ? 4 : 8;
     if (!p->gx_ws) {
         void *q;
         const size_t bytes = g_bytes(p) / 2;
@@ -1462,33 +1511,77 @@ static bsf_status run_host_global(bsf_plan_s *p, const void *f_host, const void 
         p->dev_allocs.push_back(q);
         p->gx_ws = (long long *)q;
     }
-    {
-        const bsf_status e = preint_bases(p, st, [&](int b, cudaStream_t ss) {
-            return launch_preint_i64((const uint8_t *)p->f_stage, (unsigned long long *)p->gx_ws + b * slot, g,
-                                     p->bases[b], p->d.order, ss, &p->nlaunch);
-        });
-        if (e != BSF_OK) return e;
+    if (!p->hcarry) {
+        const size_t n = 2 * 2 * (size_t)(4 * p->d.order) * g.nimg * 2 * g.GW;
+        void *q;
+        if (cudaMalloc(&q, n * sizeof(unsigned long long)) != cudaSuccess)
+            return set_err(BSF_ENOMEM, "banded scan carries");
+        p->dev_allocs.push_back(q);
+        p->hcarry = (unsigned long long *)q;
     }
-    CUDA_TRY(cudaEventRecord(ev_pre, st));
-    CUDA_TRY(cudaStreamWaitEvent(p->s_c2, ev_pre, 0));
+    // gather bands of whole tiles (rows multiple of 32); image (scan) bands of
+    // whole gather bands
+    const int rows = ((g.H + nb - 1) / nb + 31) / 32 * 32;
+    const int per = std::max(1, ((g.H + BSF_SCAN_BANDS - 1) / BSF_SCAN_BANDS + rows - 1) / rows);
+    const int srows = per * rows;
+    const int nsb = (g.H + srows - 1) / srows;
+    CUDA_TRY(cudaEventRecord(ev_start, st));  // earlier work on the caller's stream comes first
+    CUDA_TRY(cudaStreamWaitEvent(p->s_in, ev_start, 0));
+    for (int sl = 0; sl < g.nbases; ++sl) CUDA_TRY(cudaStreamWaitEvent(p->s_scan[sl], ev_start, 0));
+    // copy-in order: image band k, then the covariance bands of its rows; each
+    // image band is scanned as soon as it is in (both bases concurrently)
     int band = 0;
-    for (int y0 = 0; y0 < g.H; y0 += rows, ++band) {
-        const int h = std::min(rows, g.H - y0);
+    for (int k = 0; k < nsb; ++k) {
+        const int y0 = k * srows, h = std::min(srows, g.H - y0);
+        for (int i = 0; i < g.nimg; ++i)
+            CUDA_TRY(cudaMemcpyAsync((char *)p->f_stage + (size_t)i * host_f_pitch(g) + (size_t)y0 * g.W,
+                                     (const char *)f_host + (size_t)i * plane + (size_t)y0 * g.W, (size_t)h * g.W,
+                                     cudaMemcpyHostToDevice, p->s_in));
+        CUDA_TRY(cudaEventRecord(p->ev_fb[k], p->s_in));
+        for (int sl = 0; sl < g.nbases; ++sl) {
+            const bsf_status e = banded_scans_basis(p, sl, k, srows, nsb, p->s_scan[sl]);
+            if (e != BSF_OK) return e;
+        }
+        for (int yb = y0; yb < y0 + h; yb += rows, ++band) {
+            const int hb = std::min(rows, g.H - yb);
+            // the band's covariance as planes [batch][3][hb][W], stored contiguously at
+            // float offset batch 3 yb W of cov_stage (the bands tile the buffer)
+            float *cb = (float *)p->cov_stage + (size_t)p->d.batch * 3 * (size_t)yb * g.W;
+            for (int b = 0; b < p->d.batch; ++b)
+                for (int c = 0; c < 3; ++c)
+                    CUDA_TRY(cudaMemcpyAsync(cb + ((size_t)b * 3 + c) * (size_t)hb * g.W,
+                                             (const float *)cov_host + ((size_t)b * 3 + c) * plane + (size_t)yb * g.W,
+                                             (size_t)hb * g.W * sizeof(float), cudaMemcpyHostToDevice, p->s_in));
+            CUDA_TRY(cudaEventRecord(ev_cov[band], p->s_in));
+        }
+    }
+    // the gather band by band on two alternating streams, each band after its
+    // covariance and the scan bands its footprint reaches (every read of a
+    // pixel of rows [yb, yb + hb) lies above domain row yb + hb - 1 + Pb)
+    CUDA_TRY(cudaStreamWaitEvent(p->s_c2, ev_start, 0));
+    band = 0;
+    for (int yb = 0; yb < g.H; yb += rows, ++band) {
+        const int hb = std::min(rows, g.H - yb);
         cudaStream_t sc = (band & 1) ? p->s_c2 : st;  // alternate: a band's blocks fill the previous band's tail
+        const int kneed = std::min(nsb - 1, (yb + hb - 1 + g.Pb) / srows);
         CUDA_TRY(cudaStreamWaitEvent(sc, ev_cov[band], 0));
-        const size_t obase = (size_t)g.nimg * (size_t)y0 * g.W;  // band output: [nimg][h][W] at nimg y0 W
-        bsf_status s = filter_global_window(p, p->gx_ws, (const float *)p->cov_stage + (size_t)p->d.batch * 3 * y0 * g.W,
-                                            (char *)p->out_stage + obase * oes, y0, h, sc);
+        for (int sl = 0; sl < g.nbases; ++sl) CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_sb[sl][kneed], 0));
+        const size_t obase = (size_t)g.nimg * (size_t)yb * g.W;  // band output: [nimg][hb][W] at nimg yb W
+        // domain rows pre-integrated once scan band kneed is done (the last band holds the bottom margin)
+        const int ready = kneed == nsb - 1 ? g.GH : (kneed + 1) * srows;
+        bsf_status s = filter_global_window(p, p->gx_ws, (const float *)p->cov_stage + (size_t)p->d.batch * 3 * yb * g.W,
+                                            (char *)p->out_stage + obase * oes, yb, hb, ready, sc);
         if (s != BSF_OK) return s;
         CUDA_TRY(cudaEventRecord(ev_band[band], sc));
         CUDA_TRY(cudaStreamWaitEvent(p->s_out, ev_band[band], 0));
         for (int i = 0; i < g.nimg; ++i)
-            CUDA_TRY(cudaMemcpyAsync((char *)out_host + ((size_t)i * plane + (size_t)y0 * g.W) * oes,
-                                     (char *)p->out_stage + (obase + (size_t)i * h * g.W) * oes, (size_t)h * g.W * oes,
+            CUDA_TRY(cudaMemcpyAsync((char *)out_host + ((size_t)i * plane + (size_t)yb * g.W) * oes,
+                                     (char *)p->out_stage + (obase + (size_t)i * hb * g.W) * oes, (size_t)hb * g.W * oes,
                                      cudaMemcpyDeviceToHost, p->s_out));
     }
     CUDA_TRY(cudaEventRecord(ev_c2, p->s_c2));
     CUDA_TRY(cudaStreamWaitEvent(st, ev_c2, 0));
+    for (int sl = 0; sl < g.nbases; ++sl) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_sb[sl][nsb - 1], 0));
     CUDA_TRY(cudaEventRecord(ev_end, p->s_out));
     CUDA_TRY(cudaStreamWaitEvent(st, ev_end, 0));
     return BSF_OK;
@@ -1502,6 +1595,7 @@ extern "C" bsf_status bsf_run_host(bsf_plan_t p, const void *f_host, const void 
     if (p->d.margin_y == -1) return set_err(BSF_EINVAL, "row-strip plan (margin_y = -1): pre-integration only");
     const Geometry &g = p->geo;
     size_t fb = (size_t)g.nimg * g.H * g.W * (p->d.in_dtype == BSF_U8 ? 1 : 4);
+    if (p->d.in_dtype == BSF_U8) fb = std::max(fb, (size_t)g.nimg * host_f_pitch(g));  // global mode's staging pitch
     size_t cb = (size_t)p->d.batch * 3 * g.H * g.W * 4;
     size_t ob = (size_t)g.nimg * g.H * g.W * (p->d.out_dtype == BSF_F32 ? 4 : 8);
     if (!p->f_stage) {

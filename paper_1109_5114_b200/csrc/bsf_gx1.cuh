@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(GX1_BLOCK, GX1_MINB) gx1_kernel(TileArgs a, co
                 const int ex = (int)ceil(0.5 * rx) + 1, ey = (int)ceil(0.5 * ry) + 1;
                 const int4 E = S.ext[basis];
                 const bool in = x + a.gP - ex + E.x - 2 >= 0 && x + a.gP + ex + E.y + 2 < a.gGW &&
-                                y + ey + E.w < a.gGH;
+                                y + ey + E.w < a.gGHv;
                 if (!in) {
                     flags |= FLAG_RANGE;
                 } else {

@@ -192,6 +192,8 @@ struct TileArgs {
     const long long *gglob[2];  // per basis id (null: basis not in the plan / not global mode): the
                                 // bsf_preintegrate_exact sums [nimg][gGH][gGW] of that basis
     int gP, gGW, gGH;
+    int gGHv;                   // order-1 gather: domain rows already pre-integrated (bsf_run_host's banded
+                                // scans; gGH otherwise): a pixel reading below is flagged FLAG_RANGE
     int gshift[2];
     int gvw[2];                 // order-1 gather, per basis id: limb width w of the two-limb contraction
                                 // of zero-scale variant differences (0: three 21-bit limbs)

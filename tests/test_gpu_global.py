@@ -111,6 +111,24 @@ def test_filter_exact_is_run_split_in_two_calls():
         tp.filter_exact(g, cov.to(dev).contiguous(), out)
 
 
+def test_run_host_banded_scans_config3_full_size():
+    """bsf_run_host at config 3's full size (one 4096^2 u8 image): the image
+    arrives in row bands and each band is pre-integrated as soon as it is in
+    (scan carries between bands, TMA-fed rows); the output equals the
+    device-resident run bit for bit."""
+    w = synth.workload(3)
+    img, cov = synth.make_image(w), synth.make_cov(w)
+    plan = make_plan(w, anchor=bsf.BSF_ANCHOR_AUTO)
+    assert plan.geometry.global_mode == 1
+    dev = gpu_full(plan, img[None], cov)
+    f_h = img[None].contiguous().pin_memory()
+    c_h = cov.contiguous().pin_memory()
+    o_h = torch.full((1, w.height, w.width), float("nan"), dtype=torch.float64).pin_memory()
+    plan.run_host(f_h, c_h, o_h)
+    torch.cuda.synchronize()
+    assert torch.equal(o_h, dev)
+
+
 @pytest.mark.parametrize("out_f32", [False, True])
 def test_run_host_pipeline_global_mode(out_f32):
     """bsf_run_host in global mode overlaps the copies with the compute (image,
@@ -136,6 +154,15 @@ def test_run_host_pipeline_global_mode(out_f32):
         plan.run_host(f_h, c_h, o_h)
     torch.cuda.synchronize()
     assert torch.equal(o_h, dev)
+    # one image (H = 301: image bands of 96 rows, the last one shorter and
+    # holding the bottom margin)
+    p1 = bsf.Plan(W, H, in_dtype=bsf.BSF_U8, out_dtype=bsf.BSF_F32 if out_f32 else bsf.BSF_F64, order=1, basis=2,
+                  max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_AUTO)
+    d1 = gpu_full(p1, img[:1], cov[0], out_dtype=dt)
+    o1 = torch.full((1, H, W), float("nan"), dtype=dt).pin_memory()
+    p1.run_host(img[:1].contiguous().pin_memory(), cov[0].contiguous().pin_memory(), o1)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, d1)
 
 
 @pytest.mark.parametrize("policy", [0, 1, 2])
