@@ -17,9 +17,10 @@ HBM:
     finite difference with an exact integer contraction of Eq. (11));
   * orders 2-3: bsf_run on the tile-anchored fused kernel (running sums per
     super-tile, exact split contraction on the FP64 tensor cores);
-  * order 4: bsf_run_tiles on a fixed stratified sample of whole anchoring
-    tiles (the double-double tile kernel: a full 4096^2 image takes tens of
-    minutes at order 4 -- PAPER.md:161-166; the sample is stated in the line).
+  * order 4: bsf_run_tiles on a fixed sample of whole anchoring tiles (16 per
+    SM: the four corners + uniform; the double-double tile kernel: a full
+    4096^2 image takes ~200 s at order 4, profiles/r02_order4_full.json --
+    PAPER.md:161-166; the sample is stated in the line).
 Orders 3 and 4 take min(K, 2) and 1 timed steps after one warm-up step (their
 steps take seconds); orders 1-2 take K steps after W >= 3 warm-ups.  The L2
 (126 MB) is flushed between timed steps (256 MB write, untimed); each step is
@@ -535,7 +536,7 @@ def main():
     ap.add_argument("--impl", default="bsf")
     ap.add_argument("--ref-points", type=int, default=0, help="oracle pixels per reference step (0: ~0.5 s of work)")
     ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds of oracle time per order")
-    ap.add_argument("--r4-tiles", type=int, default=148)
+    ap.add_argument("--r4-tiles", type=int, default=2368, help="order 4: anchoring tiles sampled (16 per SM)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--frames", type=int, default=64, help="config 4: frames in total (BASELINE.json: 64)")
     ap.add_argument("--frames-per-gpu", type=int, default=0, help="config 4: frames per rank (weak scaling)")
