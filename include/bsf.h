@@ -350,7 +350,14 @@ bsf_status bsf_run_normalized(bsf_plan_t plan, const void *f_dev, const void *co
 
 /* End to end from HOST buffers (pinned for overlap): copies f and cov to the
  * device, runs bsf_run, copies out back, all on `stream`.  Returns after
- * enqueueing; synchronise the stream before reading out_host.               */
+ * enqueueing; synchronise the stream before reading out_host.  Global mode
+ * (order 1, u8) pipelines the call on the plan's own streams, joined into
+ * `stream`: the image goes up in row bands, each pre-integrated as soon as it
+ * is in (scan carries passed band to band), the covariance in row bands, each
+ * gather band starts once its covariance and the sums its footprint reaches
+ * are ready, and its output band goes back while the next one computes; the
+ * output is bit-identical to bsf_run.  Host buffers are read and written in
+ * the layouts of bsf_run; the plan keeps device staging buffers.            */
 bsf_status bsf_run_host(bsf_plan_t plan, const void *f_host, const void *cov_host, void *out_host, void *stream);
 
 /* Statistics since the last reset (synchronises the plan's last stream). */
@@ -394,7 +401,9 @@ int bsf_uses_fused(bsf_plan_t plan);
  * gathers with the order-1 integer kernel (1, default) or the fused kernel's
  * DMMA groups (0); "scan_tma" 0/1 (process-wide) -- the running-sum strip
  * kernels stream their rows by TMA (1, default when the row pitch allows) or
- * by cp.async (0).  BSF_EINVAL for an unknown name.                          */
+ * by cp.async (0); "gx1_dp4a" 0/1 -- the order-1 gather contracts byte planes
+ * of the sums with dp4a (1) instead of three 21-bit IMAD limbs (0, default;
+ * both exact, outputs bit-identical).  BSF_EINVAL for an unknown name.     */
 bsf_status bsf_debug_option(bsf_plan_t plan, const char *name, double value);
 
 const char *bsf_status_str(bsf_status s);

@@ -2,8 +2,8 @@
 the CUDA sources the captures were taken on) from ncu --set full raw CSV
 exports: dram__bytes_read.sum + dram__bytes_write.sum per kernel family.
 
-python tools/traffic_json.py  (after tools/gpu/r02_final.sh copied the
-r02_r1_full_raw.csv / r02_r2_fused_raw.csv exports into profiles/)."""
+python tools/traffic_json.py  (after tools/gpu/r02_final2.sh's r02_r1_full_raw.csv /
+r02_r{2,3}_fused_raw.csv exports were copied into profiles/)."""
 import csv
 import json
 import os
@@ -37,12 +37,14 @@ def main():
                                          "file": "profiles/r02_r1_full_raw.csv"}
     caps["c3_4096_u8_grid32/r1/gx1_kernel"] = {"dram_bytes": gx[0], "src_hash": sh,
                                                "file": "profiles/r02_r1_full_raw.csv"}
-    r2 = per_kernel("profiles/r02_r2_fused_raw.csv")
-    caps["c3_4096_u8_grid32/r2/fused_kernel"] = {"dram_bytes": r2[0][1], "src_hash": sh,
-                                                 "file": "profiles/r02_r2_fused_raw.csv"}
+    for r in (2, 3):
+        path = "profiles/r02_r%d_fused_raw.csv" % r
+        if os.path.exists(os.path.join(ROOT, path)):
+            rr = per_kernel(path)
+            caps["c3_4096_u8_grid32/r%d/fused_kernel" % r] = {"dram_bytes": rr[0][1], "src_hash": sh, "file": path}
     doc = {"what": "dram__bytes_read.sum + dram__bytes_write.sum per launch (per step for the 8 scan launches of "
                    "order 1), one ncu --set full --clock-control none capture of tools/step_probe.py on config 3 "
-                   "(tools/gpu/r02_final.sh); bench.py reports them only while src_hash matches the CUDA sources",
+                   "(tools/gpu/r02_final2.sh); bench.py reports them only while src_hash matches the CUDA sources",
            "src_hash": sh, "captures": caps}
     with open(os.path.join(ROOT, "profiles", "r02_traffic.json"), "w") as fh:
         json.dump(doc, fh, indent=1)
