@@ -21,6 +21,7 @@
 // over groups; thread 0 issues the MMAs, tcgen05.commit -> mbarrier.
 //
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o i8_contract i8_contract.cu
+// library: add -DI8TC_LIB -shared -Xcompiler -fPIC -o libi8tc.so (tools/i8_tc/build.py)
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -310,6 +311,67 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
 }
 
+// Host entry (tests, tools/i8_tc/libi8tc.so): E = n^T G exactly, group g with
+// table g % ntab.  n: int64 [ntab][K][66], |n| < 2^55 (seven bytes, two's
+// complement); G: int64 [ngroups][32][K]; E: int64 [ngroups][66][32][2]
+// (low, high word of the int128).  K a multiple of 32, at most 4096 (so no
+// class sum can reach 2^31).  Returns 0, or -1 for bad arguments, -2 for a
+// CUDA error; *ms = the best kernel time of `reps` timed launches.
+extern "C" int i8tc_contract(const long long *n, int ntab, const long long *G, int ngroups, int K, long long *E,
+                             int reps, float *ms) {
+    if (!n || !G || !E || ntab < 1 || ngroups < 1 || K < KC || K % KC || K > 4096) return -1;
+    const int nchunk = K / KC;
+    std::vector<uint8_t> as((size_t)ntab * nchunk * A_CHUNK, 0);
+    for (int g = 0; g < ntab; ++g)
+        for (int ch = 0; ch < nchunk; ++ch)
+            for (int a = 0; a < NA; ++a)
+                for (int m = 0; m < MREAL; ++m)
+                    for (int k = 0; k < KC; ++k) {
+                        const long long v = n[((size_t)g * K + ch * KC + k) * MREAL + m];
+                        as[((size_t)g * nchunk + ch) * A_CHUNK + a * (M * KC) + canon(m, k)] =
+                            (uint8_t)((unsigned long long)v >> (8 * a));
+                    }
+    uint8_t *d_as = nullptr;
+    long long *d_G = nullptr, *d_E = nullptr;
+    int rc = 0;
+    int sms = 0;
+    const int smem = NS * STAGE;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaMalloc(&d_as, as.size()) != cudaSuccess || cudaMalloc(&d_G, (size_t)ngroups * N * K * 8) != cudaSuccess ||
+        cudaMalloc(&d_E, (size_t)ngroups * MREAL * N * 16) != cudaSuccess ||
+        cudaMemcpy(d_as, as.data(), as.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d_G, G, (size_t)ngroups * N * K * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaFuncSetAttribute(i8_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess ||
+        cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+        rc = -2;
+    } else {
+        float best = 1e30f;
+        for (int rep = 0; rep <= reps; ++rep) {  // launch 0 is a warm-up
+            cudaEventRecord(e0);
+            i8_contract_kernel<<<sms, KTHREADS, smem>>>(d_as, d_G, d_E, ngroups, K, ntab, 0);
+            cudaEventRecord(e1);
+            if (cudaEventSynchronize(e1) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+                rc = -2;
+                break;
+            }
+            float t = 0.f;
+            cudaEventElapsedTime(&t, e0, e1);
+            if (rep > 0 && t < best) best = t;
+        }
+        if (ms) *ms = reps > 0 ? best : 0.f;
+        if (rc == 0 && cudaMemcpy(E, d_E, (size_t)ngroups * MREAL * N * 16, cudaMemcpyDeviceToHost) != cudaSuccess)
+            rc = -2;
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(d_as);
+    cudaFree(d_G);
+    cudaFree(d_E);
+    return rc;
+}
+
+#ifndef I8TC_LIB
 int main(int argc, char **argv) {
     const int ngroups = argc > 1 ? atoi(argv[1]) : 148 * 32;
     const int K = argc > 2 ? atoi(argv[2]) : 224;  // Theta' order-3 window, padded to the k-step
@@ -390,3 +452,4 @@ int main(int argc, char **argv) {
            (double)ngroups * N * K * M * NA * NB * 2 / (best * 1e-3) / 1e12, dmma_ms, checked, bad);
     return (bad && !mode) ? 2 : 0;
 }
+#endif  // I8TC_LIB
