@@ -36,6 +36,7 @@ constexpr int N = 32;         // items per group
 constexpr int KC = 32;        // slots per chunk (one UMMA K step for int8)
 constexpr int NA = 7, NB = 8, NCLS = NA + NB - 1;
 constexpr int A_CHUNK = NA * M * KC;  // bytes of one chunk of all A slices (28 KB)
+constexpr int A_LIVE = ((MREAL + 7) / 8) * 8 * KC;  // bytes of a slice holding real rows (9 row groups: 2304)
 constexpr int B_CHUNK = NB * N * KC;  // 8 KB
 constexpr int THREADS = 128;
 
@@ -94,9 +95,22 @@ __device__ __forceinline__ bool elect_one() {  // one lane of a converged warp (
 // The chunk's 56 slice products, issued by one elected lane of warp 0 (the
 // whole warp runs this code, so the descriptors live in uniform registers);
 // a product overwrites its class when it is the group's first into it.
+// A in TMEM: the chunk's seven A slices (128 rows x 32 bytes each) are copied
+// shared -> tensor memory once (tcgen05.cp 128x256b, columns ACOL + 8a) and
+// every product reads A from there, so the shared-memory operand traffic per
+// UMMA is B only (1 KB instead of 5 KB: at N = 32 the A reads would bound
+// the MMAs by shared-memory bandwidth).  tcgen05.cp and tcgen05.mma issued by
+// one thread execute in issue order.
+constexpr uint32_t ACOL = NCLS * N;  // 448: first TMEM column of the A slices (7 x 8 columns)
 __device__ __forceinline__ void mma_chunk(uint32_t tbase, uint32_t a_addr, uint32_t b_addr, bool first_chunk,
                                           bool leader) {
     const uint64_t da0 = smem_desc(a_addr), db0 = smem_desc(b_addr);
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+        if (leader)
+            asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tbase + ACOL + 8u * a),
+                         "l"(da0 + (uint64_t)((a * M * KC) >> 4))
+                         : "memory");
 #pragma unroll
     for (int a = 0; a < NA; ++a)
 #pragma unroll
@@ -109,11 +123,12 @@ __device__ __forceinline__ void mma_chunk(uint32_t tbase, uint32_t a_addr, uint3
             const uint32_t idesc = a == NA - 1 ? (b == NB - 1 ? id_ss : id_su) : (b == NB - 1 ? id_us : id_uu);
             const uint32_t acc = first ? 0u : 1u;
             const uint32_t dt = tbase + (uint32_t)(c * N);
+            (void)da;
             if (leader)
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dt),
-                    "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dt),
+                    "r"(tbase + ACOL + 8u * a), "l"(db), "r"(idesc), "r"(acc)
                     : "memory");
         }
 }
@@ -191,6 +206,9 @@ __global__ void __launch_bounds__(KTHREADS, 1)
         mbar_init(btfree, THREADS);   // the epilogue threads have read TMEM
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int i = tid; i < NS * STAGE / 16; i += blockDim.x)  // zero padding rows of every stage
+        reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (warp == 0) {  // 512 TMEM columns (14 classes x 32)
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&tmem_base);
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
@@ -227,29 +245,35 @@ __global__ void __launch_bounds__(KTHREADS, 1)
         // ---- producers (stages ahead) + epilogue
         const int pt = tid - 32;  // 0..127
         int kp = 0;               // next chunk to produce
-        BRegs cur, nxt;  // chunk kq's values, and chunk kq + 1's in flight
+        BRegs cur, nxt, nxt2;  // chunk kq's values; chunks kq + 1 and kq + 2 in flight
         if (total > 0) load_b(cur, G, blockIdx.x, 0, K, pt);
+        if (total > 1) load_b(nxt, G, blockIdx.x + (1 / nchunk) * gridDim.x, 1 % nchunk, K, pt);
         auto produce = [&](int kq) {
             const int st = kq % NS, ch = kq % nchunk;
             const int pgrp = blockIdx.x + (kq / nchunk) * gridDim.x;
-            if (kq + 1 < total)
-                load_b(nxt, G, blockIdx.x + ((kq + 1) / nchunk) * gridDim.x, (kq + 1) % nchunk, K, pt);
+            if (kq + 2 < total)
+                load_b(nxt2, G, blockIdx.x + ((kq + 2) / nchunk) * gridDim.x, (kq + 2) % nchunk, K, pt);
             if (kq >= NS) mbar_wait(be0 + 8 * st, ((kq / NS) - 1) & 1);  // the MMAs of chunk kq - NS are done
             if (pt == 0) {
                 const uint32_t bar = bf0 + 8 * st;
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(A_CHUNK)
+                // only the row groups holding real monomials: rows 72..127 of
+                // every stage stay zero from the kernel's start
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(NA * A_LIVE)
                              : "memory");
                 const uint8_t *src = aslices + ((size_t)(pgrp % ntab) * nchunk + ch) * A_CHUNK;
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        s_addr + st * STAGE),
-                    "l"(src), "r"(A_CHUNK), "r"(bar)
-                    : "memory");
+#pragma unroll
+                for (int a = 0; a < NA; ++a)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            s_addr + st * STAGE + a * (M * KC)),
+                        "l"(src + a * (M * KC)), "r"(A_LIVE), "r"(bar)
+                        : "memory");
             }
             store_b(smem + st * STAGE + A_CHUNK, cur, pt);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             if (pt != 0) mbar_arrive(bf0 + 8 * st);
             cur = nxt;
+            nxt = nxt2;
         };
         for (int gi = 0; gi < my_groups; ++gi) {
             const int grp = blockIdx.x + gi * gridDim.x;
@@ -268,38 +292,30 @@ __global__ void __launch_bounds__(KTHREADS, 1)
             const int q = warp & 3;  // TMEM lane quadrant this warp may read
             const int m = q * 32 + lane;
 #pragma unroll 1
-            for (int i0 = 0; i0 < N; i0 += 8) {
-                unsigned long long lo[8], hi[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) lo[i] = hi[i] = 0ull;
+            for (int i0 = 0; i0 < N; i0 += 4) {
+                // all 14 classes of four items: 14 loads in flight, one wait
+                uint32_t r[NCLS][4];
 #pragma unroll
                 for (int c = 0; c < NCLS; ++c) {
-                    uint32_t r[8];
                     const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * N + i0);
-                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                                   "=r"(r[7])
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(r[c][0]), "=r"(r[c][1]), "=r"(r[c][2]), "=r"(r[c][3])
                                  : "r"(taddr));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {  // (hi, lo) += sign-extended r << 8c, 128-bit
-                        const long long v = (int)r[i];
-                        const int sh = 8 * c;
-                        const unsigned long long vlo = sh < 64 ? (unsigned long long)v << sh : 0ull;
-                        const unsigned long long vhi = sh == 0 ? (unsigned long long)(v >> 63)
-                                                       : sh < 64 ? (unsigned long long)(v >> (64 - sh))
-                                                                 : (unsigned long long)(v << (sh - 64));
-                        const unsigned long long t = lo[i] + vlo;
-                        hi[i] += vhi + (t < lo[i] ? 1ull : 0ull);
-                        lo[i] = t;
-                    }
                 }
-                if (m < MREAL) {
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        long long *e = E + (((size_t)grp * MREAL + m) * N + i0 + i) * 2;
-                        e[0] = (long long)lo[i];
-                        e[1] = (long long)hi[i];
+                for (int i = 0; i < 4; ++i) {
+                    // four classes at a time exactly in int64 (|sum| < 4 x 2^31 x 2^24 = 2^57),
+                    // then E = P0 + 2^32 P1 + 2^64 P2 + 2^96 P3 in 128-bit arithmetic
+                    long long P[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int c = 0; c < NCLS; ++c) P[c >> 2] += (long long)(int)r[c][i] * (1ll << (8 * (c & 3)));
+                    const __int128 e = (__int128)P[0] + ((__int128)P[1] << 32) + ((__int128)P[2] << 64) +
+                                       ((__int128)P[3] << 96);
+                    if (m < MREAL) {
+                        long long *o = E + (((size_t)grp * MREAL + m) * N + i0 + i) * 2;
+                        o[0] = (long long)(unsigned long long)e;
+                        o[1] = (long long)(e >> 64);
                     }
                 }
             }
