@@ -17,9 +17,10 @@ MREAL, N = 66, 32
 
 
 def _lib():
-    import sys
-    sys.path.insert(0, os.path.join(ROOT, "tools", "i8_tc"))
-    import build as B  # tools/i8_tc/build.py
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("i8tc_build", os.path.join(ROOT, "tools", "i8_tc", "build.py"))
+    B = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(B)
     L = ctypes.CDLL(B.build())
     L.i8tc_contract.restype = ctypes.c_int
     L.i8tc_contract.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
