@@ -149,6 +149,7 @@ struct bsf_plan_s {
     bool opt_order = true;
     int opt_global_kernel = 1;  // global mode: 1 the order-1 integer gather (bsf_gx1.cuh), 0 the fused kernel
     int opt_gx1_dp4a = 0;       // order-1 gather: 1 byte-plane dp4a contraction, 0 three 21-bit IMAD limbs
+    int opt_i8_tc = 0;          // order 3: 1 the exact limbs on tcgen05 kind::i8 (bsf_fused.cuh i8_tile), 0 DMMA
     double opt_split_tol = BSF_SPLIT_TOL_DEFAULT;
 };
 
@@ -418,6 +419,46 @@ static bsf_status load_lut(bsf_plan_s *p, const char *dir, int basis, LutBasis *
                 p->dev_allocs.push_back(d8);
                 CUDA_TRY(cudaMemcpy(d8, n8.data(), n8.size(), cudaMemcpyHostToDevice));
                 V.n8 = (const signed char *)d8;
+            }
+        }
+        // order 3, tcgen05 kind::i8 route (plan option "i8_tc", bsf_fused.cuh
+        // i8_tile): the integer numerators as byte slices in the UMMA canonical
+        // K-major layout, [region][32-slot chunk][slice][128 rows = table
+        // columns][32 slots] (row r, slot k at (r / 8) 256 + (k / 16) 128 +
+        // (r % 8) 16 + k % 16), slices A_0.. unsigned and the top one signed
+        V.i8tab = nullptr;
+        V.i8na = 0;
+        V.i8nchunk = 0;
+        // (the tile's window values G1 2^k + G2 are below 2^(2k+1): int64, 8 byte
+        // slices, for kbits <= 31; tables with wider limbs keep the DMMA path)
+        if (exact && p->d.order == 3 && V.nmonp <= 128 && V.kbits <= 31) {
+            double nmax_abs = 0.0;
+            for (double v : nump) nmax_abs = std::max(nmax_abs, fabs(v));
+            int na = 1;
+            while (na < 7 && !(nmax_abs < ldexp(1.0, 8 * na - 1))) ++na;
+            if (nmax_abs < ldexp(1.0, 8 * na - 1)) {
+                const int nch = (V.nslot4 + 31) / 32;
+                std::vector<uint8_t> t8((size_t)nreg * nch * na * 4096, 0);
+                for (uint32_t r = 0; r < nreg; ++r)
+                    for (int ch = 0; ch < nch; ++ch)
+                        for (int k = 0; k < 32; ++k) {
+                            const int sl = ch * 32 + k;
+                            if (sl >= V.nslot4) continue;
+                            for (int m = 0; m < V.nmonp; ++m) {
+                                const long long v = (long long)nump[((size_t)r * V.nslot4 + sl) * V.nmonp + m];
+                                const int off = (m >> 3) * 256 + (k >> 4) * 128 + (m & 7) * 16 + (k & 15);
+                                for (int a = 0; a < na; ++a)
+                                    t8[(((size_t)r * nch + ch) * na + a) * 4096 + off] =
+                                        (uint8_t)((unsigned long long)v >> (8 * a));
+                            }
+                        }
+                void *d8;
+                CUDA_TRY(cudaMalloc(&d8, t8.size()));
+                p->dev_allocs.push_back(d8);
+                CUDA_TRY(cudaMemcpy(d8, t8.data(), t8.size(), cudaMemcpyHostToDevice));
+                V.i8tab = (const uint8_t *)d8;
+                V.i8na = na;
+                V.i8nchunk = nch;
             }
         }
         // order >= 3: the B operand tables in fp32 when every value is exact there
@@ -1062,6 +1103,7 @@ static TileArgs tile_args(bsf_plan_s *p, const void *f, const void *cov, void *o
         a.order_cap = p->sched_cap;
     }
     a.split_tol = p->opt_split_tol;  // BSF_SPLIT_TOL_DEFAULT unless a diagnostics option changed it
+    a.i8 = p->opt_i8_tc;
     a.cov_layout = p->d.cov_layout;
     return a;
 }
@@ -1694,6 +1736,8 @@ extern "C" bsf_status bsf_debug_option(bsf_plan_t p, const char *name, double va
         set_scan_tma(value != 0.0);
     } else if (n == "global_kernel") {
         p->opt_global_kernel = value != 0.0 ? 1 : 0;
+    } else if (n == "i8_tc") {
+        p->opt_i8_tc = value != 0.0 ? 1 : 0;
     } else if (n == "gx1_dp4a") {
         p->opt_gx1_dp4a = value != 0.0 ? 1 : 0;
     } else if (n == "split_tol") {

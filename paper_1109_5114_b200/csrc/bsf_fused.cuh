@@ -76,6 +76,13 @@ constexpr size_t fused_smem_bytes() {
     return chunk > FUSED_SMEM_MIN ? chunk : FUSED_SMEM_MIN;
 }
 
+// order 3, i8 route (bsf_i8_gather.cuh): after the chunk buffers, 1 KB
+// aligned: seven A slices (4 KB each), eight B slices (1 KB each), the E12
+// tile (32 items x E12S columns, double-double)
+constexpr size_t I8_SMEM = 7 * 4096 + 8 * 1024 + 32 * 72 * 16;
+template <int R>
+constexpr size_t i8_smem_off() { return (fused_smem_bytes<R>() + 1023) / 1024 * 1024; }
+
 // pixel info word: bit0 basis, bits1-3 variant (drop + 1), bit4 live, bit5 clamped, bits 8.. flags
 __device__ __forceinline__ int info_basis(int w) { return w & 1; }
 __device__ __forceinline__ int info_var(int w) { return (w >> 1) & 7; }
@@ -571,13 +578,18 @@ __device__ __forceinline__ void fused_group(const Src &src, const int (&bxt)[MT]
 // conditioning of r = 3 needs it).  With split numerators (NSPLIT 2) the two
 // exact limbs each meet n1 and n0.  The N dimension is taken in passes of NP
 // n-tiles (bounded registers); the lock-step row Horner resumes across passes.
-template <int DEG, int NSPLIT, int NP, int MT, bool PRE>
+// I8 (plan option "i8_tc", PRE planes only): the exact part sum_s (G1 2^k + G2) n
+// was formed on the tcgen05 tensor cores (i8_tile) and is read from shared
+// memory (e12: this group's 8 items, row stride E12S, already scaled by 2^-k);
+// only the rounded G0 limb is contracted here on DMMA.
+constexpr int E12S = 72;  // E12 row stride (degree-10 tables: 9 n-tiles)
+template <int DEG, int NSPLIT, int NP, int MT, bool PRE, bool I8 = false>
 __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, int NX, int NY, const int (&bxt)[MT],
                                                const int (&byt)[MT], double fxo, double fyo,
                                                const int2 *__restrict__ offs, const float *__restrict__ numc,
                                                int nmonp, int n4, int shift, const double *__restrict__ G0,
                                                double sc_e, int kbits, double (&Fh)[MT], double (&Fl)[MT],
-                                               int &flags) {
+                                               int &flags, const double2 *e12 = nullptr) {
     constexpr int NT = DegCfg<DEG>::NT, NL = NSPLIT == 1 ? 3 : 5, QMAX = RowCfg<DEG>::QMAX;
     const int lane = threadIdx.x & 31, kq = lane & 3, gq = lane >> 2;
     // fractional offsets of this lane's items (gq + 8t), from the lanes that set them up
@@ -627,6 +639,11 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
                 // bypass L1 so that it keeps the region's coefficient table
                 // (an L1 prefetch of the next step's sums evicted the table: +32 %)
                 const size_t gi = inside ? (size_t)ly * NX + lx : 0;
+                if constexpr (I8) {  // the exact limbs are in e12: only G0
+                    g1[t] = g2[t] = 0.0;
+                    g0[t] = inside ? __ldcg(G0 + gi) : 0.0;
+                    continue;
+                }
                 const double2 g = __ldcg(G + gi);
                 if constexpr (PRE) {  // (G1, G2) and G0 split once per plane
                     const double gz = __ldcg(G0 + gi);
@@ -661,6 +678,10 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
                 }
 #pragma unroll
                 for (int t = 0; t < MT; ++t) {
+                    if constexpr (I8) {
+                        dmma(C[t][2][j], g0[t], NSPLIT == 1 ? bA : bF);
+                        continue;
+                    }
                     dmma(C[t][0][j], g1[t], bA);  // exact
                     dmma(C[t][1][j], g2[t], bA);  // exact
                     if constexpr (NSPLIT == 1) {
@@ -684,7 +705,10 @@ __device__ __forceinline__ void fused_group_g3(const double2 *__restrict__ G, in
 #pragma unroll
                 for (int t = 0; t < MT; ++t) {
                     dd e;
-                    if constexpr (NSPLIT == 1) {
+                    if constexpr (I8) {
+                        const double2 x = e12[(gq + 8 * t) * E12S + 8 * (j0 + j) + 2 * kq + h2];
+                        e = dd_add_d(dd{x.x, x.y}, C[t][2][j][h2] * iS);
+                    } else if constexpr (NSPLIT == 1) {
                         e = dd_add_d(two_sum(C[t][0][j][h2], C[t][1][j][h2] * iS), C[t][2][j][h2] * iS);
                     } else {
                         const dd x = two_sum(C[t][0][j][h2] * ssh, C[t][3][j][h2]);
@@ -937,7 +961,7 @@ __device__ bool sweep_plane(double2 *__restrict__ G, int NX, int NY, int X0, int
 // read the paper's single global pre-integration (Alg. 3
 // step 2), the exact int64 running sums of bsf_preintegrate_exact, through
 // GlobSrc; phases 2-3 are skipped and both contraction limbs are exact.
-template <int R, bool SPLIT, bool GLOBAL = false>
+template <int R, bool SPLIT, bool GLOBAL = false, bool I8 = false>
 __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis *__restrict__ luts) {
     constexpr int NTAP = FusedCfg<R>::NTAP, P = FusedCfg<R>::P, ITEMS = P * NTAP;
     constexpr int MT = FusedCfg<R>::MT, GS = 8 * MT;
@@ -971,7 +995,29 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
         }
         for (int i = 0; i < 81; ++i) s_cls.table[tid][i] = L.table[i];
     }
+    // order 3, i8 route: 512 TMEM columns (accumulator classes 0..447, the A
+    // slices 448..503) and the two mbarriers of i8_tile
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_i8bar[2];
+    uint32_t i8_pa = 0, i8_pm = 0;  // mbarrier phases (every thread tracks them)
+    if constexpr (I8) {
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_i8bar[0]))
+                         : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_i8bar[1]))
+                         : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(&s_tmem))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
     __syncthreads();
+    if constexpr (I8) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // optional phase timing (TileArgs::prof, diagnostics only): thread 0 adds
     // the SM cycles spent in each phase
     long long ph_t = clock64(), t_item = ph_t;
@@ -1523,7 +1569,9 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             FUSED_PHASE(3);
             // gather: groups of GS items sharing one key, one warp per group,
             // contraction on the FP64 tensor cores, polynomial from the fragments
-            {
+            if constexpr (I8 && R == 3) {
+#include "bsf_i8_gather.cuh"
+            } else {
                 const int ngroups = npad / GS;
                 int flags = 0;
                 for (int g = warp; g < ngroups; g += FT / 32) {
@@ -1833,6 +1881,11 @@ __global__ void __launch_bounds__(FT, 1) fused_kernel(TileArgs a, const LutBasis
             if (blockIdx.x < BSF_PROF_CTAS) atomicAdd(a.prof + 16 + BSF_PROF_ITEMS + blockIdx.x, dt);
         }
     }
+    if constexpr (I8) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -2041,13 +2094,13 @@ __global__ void __launch_bounds__(256) fused_order_kernel(TileArgs a, int nslots
     }
 }
 
-template <int R, bool SPLIT = false, bool GLOBAL = false>
+template <int R, bool SPLIT = false, bool GLOBAL = false, bool I8 = false>
 static cudaError_t launch_fused_r(const TileArgs &a, int slots, cudaStream_t st, const LutBasis *luts) {
-    constexpr size_t sm = fused_smem_bytes<R>();
+    constexpr size_t sm = I8 ? i8_smem_off<R>() + I8_SMEM : fused_smem_bytes<R>();
     static std::atomic<unsigned long long> attr{0ull};
-    cudaError_t e = set_smem_attr(fused_kernel<R, SPLIT, GLOBAL>, (int)sm, attr);
+    cudaError_t e = set_smem_attr(fused_kernel<R, SPLIT, GLOBAL, I8>, (int)sm, attr);
     if (e != cudaSuccess) return e;
-    fused_kernel<R, SPLIT, GLOBAL><<<slots, FT, sm, st>>>(a, luts);
+    fused_kernel<R, SPLIT, GLOBAL, I8><<<slots, FT, sm, st>>>(a, luts);
     return cudaGetLastError();
 }
 
@@ -2107,7 +2160,7 @@ cudaError_t launch_fused_impl(const TileArgs &a, int order, int slots, cudaStrea
         case 2:  // split mode only in its own instantiation (register allocation of the other plans untouched)
             e = b.order && S == 4 ? launch_fused_r<2, true>(b, slots, st, luts) : launch_fused_r<2>(b, slots, st, luts);
             break;
-        case 3: e = launch_fused_r<3>(b, slots, st, luts); break;
+        case 3: e = b.i8 ? launch_fused_r<3, false, false, true>(b, slots, st, luts) : launch_fused_r<3>(b, slots, st, luts); break;
         case 4: e = launch_fused_r<4>(b, slots, st, luts); break;
         default: return cudaErrorInvalidValue;
     }

@@ -107,6 +107,8 @@ struct LutVar {
                            // interleaved (n1, n0) pairs (nsplit 2) -- half the bytes of the MMA's B loads
     const signed char *n8; // order 1 (global-mode gather, bsf_gx1.cuh): [nreg][nmax][8] numerators n as int8
                            // (monomials in gen_lut order, zero padded); null when some |n| > 127
+    const uint8_t *i8tab;  // order 3: numerator byte slices, UMMA canonical layout (bsf_api.cu), or null
+    int i8na, i8nchunk;    // slices (the top one signed), 32-slot chunks per region
     float mean_count;      // window slots averaged over the regions (work-item cost estimate)
     double nabs;           // max over (region, monomial) of sum_s |n| (order 1: the gather's limb widths)
     double bnd;            // bound on |F - F^| (units 2^e) of the split contraction: gamma_{n+1} 0.5 max_reg sum_s,mu |n|
@@ -198,6 +200,7 @@ struct TileArgs {
     int gvw[2];                 // order-1 gather, per basis id: limb width w of the two-limb contraction
                                 // of zero-scale variant differences (0: three 21-bit limbs)
     int gdp4a;                  // order-1 gather: byte-plane dp4a contraction (bsf_gx1.cuh gx1_tap_dp)
+    int i8;                     // order 3: exact limbs on tcgen05 kind::i8 (bsf_fused.cuh i8_tile)
 };
 constexpr int SCHED_NBIN = 128;
 // Opt a kernel into more than 48 KB of dynamic shared memory, once per device
