@@ -403,7 +403,10 @@ int bsf_uses_fused(bsf_plan_t plan);
  * kernels stream their rows by TMA (1, default when the row pitch allows) or
  * by cp.async (0); "gx1_dp4a" 0/1 -- the order-1 gather contracts byte planes
  * of the sums with dp4a (1) instead of three 21-bit IMAD limbs (0, default;
- * both exact, outputs bit-identical).  BSF_EINVAL for an unknown name.     */
+ * both exact, outputs bit-identical); "i8_tc" 0/1 -- order 3: the exact limbs
+ * of Theta' full-kernel groups on the tcgen05 int8 tensor cores with TMEM
+ * accumulators (1) or on DMMA (0, default; outputs bit-identical, the DMMA
+ * path is faster today).  BSF_EINVAL for an unknown name.   */
 bsf_status bsf_debug_option(bsf_plan_t plan, const char *name, double value);
 
 const char *bsf_status_str(bsf_status s);
