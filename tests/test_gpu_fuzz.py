@@ -15,6 +15,18 @@ from gpu_util import max_rel, oracle_points
 pytestmark = pytest.mark.gpu
 
 
+def _rel_scale(img, cov, xs, ys, ref, u8, policy, r):
+    """Denominator of the relative error (R26).  u8 images: |ref|
+    (the box spline is non-negative, so outputs are positive).  Signed float
+    images: the same filter applied to |f| at the same pixels, sum_q |f(q)|
+    beta(p - q) >= |ref| -- the magnitude the pixel's sum is formed from, its
+    condition scale; equal to |ref| wherever f does not change sign under
+    the kernel's support.  No constant floor."""
+    if u8:
+        return np.abs(ref)
+    return oracle_points(np.abs(img), cov, xs, ys, policy=policy, r=r)[0]
+
+
 def _case(seed):
     rng = np.random.default_rng(1000 + seed)
     H, W = int(rng.integers(5, 90)), int(rng.integers(5, 90))
@@ -63,10 +75,7 @@ def test_fuzz_fused_vs_oracle(seed):
         ys, xs = idx // W, idx % W
         ref = oracle_points(c["img"][i], c["cov"][b], xs, ys, policy=c["policy"], r=c["r"])[0]
         tol = 1e-6 if c["out_f32"] else 1e-9
-        # u8 images: plain relative error (outputs are positive); signed float
-        # images only: against the larger of |ref| and 1e-3 of the output scale
-        # (outputs pass through zero, where a relative error is undefined)
-        scale = np.abs(ref) if c["u8"] else np.maximum(np.abs(ref), 1e-3 * np.max(np.abs(ref)))
+        scale = _rel_scale(c["img"][i], c["cov"][b], xs, ys, ref, c["u8"], c["policy"], c["r"])
         err = float(np.max(np.abs(got[i][ys, xs] - ref) / scale))
         assert err <= tol, (seed, i, err, {k: c[k] for k in ("H", "W", "r", "policy", "u8", "smax")})
 
@@ -112,7 +121,7 @@ def test_fuzz_large_images_vs_oracle(seed):
     idx = rng.choice(H * W, 24, replace=False)
     ys, xs = idx // W, idx % W
     ref = oracle_points(c["img"], c["cov"], xs, ys, policy=c["policy"], r=c["r"])[0]
-    scale = np.abs(ref) if c["u8"] else np.maximum(np.abs(ref), 1e-3 * np.max(np.abs(ref)))  # as above
+    scale = _rel_scale(c["img"], c["cov"], xs, ys, ref, c["u8"], c["policy"], c["r"])
     err = float(np.max(np.abs(got[ys, xs] - ref) / scale))
     assert err <= 1e-9, (seed, err, st, {k: c[k] for k in ("H", "W", "r", "policy", "u8", "smax")})
 
