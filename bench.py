@@ -381,7 +381,7 @@ def roofline(w, r, mode, plan, stats, npx, kms, pms, ms):
         gat_bytes = g_bytes + npx * (12 + 8)  # read g once (taps from L2), cov 3 x f32, out f64
         hbm = peaks.get("hbm_gbs", 6650.0)
         fma = stats["macs"] / max(stats["pixels"], 1)  # window x monomials per tap
-        return {"bound": "alu", "kernel": "gx1_kernel (order-1 exact integer gather)",
+        roof = {"bound": "alu", "kernel": "gx1_kernel (order-1 exact integer gather)",
                 "achieved": achieved, "peak": peak, "unit": "Tintop/s", "frac": achieved / peak,
                 "traffic": _traffic(w.name, r, "gx1_kernel"),
                 "peak_source": "%d SM x 64 int32 multiply-adds/clk (IMAD on the FMA pipe, 2 cycles per warp "
@@ -404,6 +404,11 @@ def roofline(w, r, mode, plan, stats, npx, kms, pms, ms):
                                    "achieved_gbs": pre_bytes / (pms * 1e-3) / 1e9, "peak_gbs": hbm,
                                    "frac": pre_bytes / (pms * 1e-3) / 1e9 / hbm,
                                    "traffic": _traffic(w.name, r, "scan")}}
+        pt = roof["preintegration"]["traffic"]
+        # the bytes the 8 level launches actually move (one read + one write
+        # of an int64 plane per level, ncu) over the same measured time
+        roof["preintegration"]["traffic_frac"] = pt / (pms * 1e-3) / 1e9 / hbm if pt else None
+        return roof
     if mode == "tile" and plan.uses_fused():
         fp = _json("profiles/r01_fp64_peak.json")
         macs_px = stats["macs"] / max(stats["pixels"], 1)
