@@ -271,18 +271,12 @@ def time_order(args, w, r, dev, rank, world, stream, flush, pg):
         tiles = _tile_sample(w, geo.tile_unit, args.r4_tiles).to(dev)
         npx = int(tiles.numel()) * geo.tile_unit * geo.tile_unit
 
-    def step(ev=None, split=False):
-        if mode == "global" and split:
-            # the two calls one after the other: the event between them
-            # times the gather kernel alone (the roofline's kernel duration)
+    def step(ev=None):
+        if mode == "global":
             plan.preintegrate_exact(img, g, stream)
             if ev is not None:
                 ev.record(stream)
             plan.filter_exact(g, cov, out, stream)
-        elif mode == "global":
-            # the product call: scans and gather in row bands, overlapped
-            # (bsf_run's global pipeline)
-            plan.run(img, cov, out, stream)
         elif mode == "tile":
             if ev is not None:
                 ev.record(stream)
@@ -314,26 +308,12 @@ def time_order(args, w, r, dev, rank, world, stream, flush, pg):
         pg.barrier()
     launches = plan.launch_count() - launches0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    stats = plan.stats(reset=True)
-    if mode == "global":
-        # kernel durations for the roofline: the same K steps as two calls
-        # (pre-integration, then the gather), an event between them
-        for _ in range(Wm):
-            step(split=True)
-            flush.zero_()
-        torch.cuda.synchronize()
-        for i in range(K):
-            starts[i].record(stream)
-            step(mids[i], split=True)
-            ends[i].record(stream)
-            flush.zero_()
-        torch.cuda.synchronize()
-        plan.stats(reset=True)
     kern_ms = [m.elapsed_time(e) for m, e in zip(mids, ends)]
     pre_ms = [s.elapsed_time(m) for s, m in zip(starts, mids)]
     ms = sum(step_ms) / K
     kms = sum(kern_ms) / K
     pms = sum(pre_ms) / K
+    stats = plan.stats(reset=True)
     if pg:
         t = torch.tensor([ms], device=dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)

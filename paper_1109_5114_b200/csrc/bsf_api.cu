@@ -149,7 +149,6 @@ struct bsf_plan_s {
     bool opt_order = true;
     int opt_global_kernel = 1;  // global mode: 1 the order-1 integer gather (bsf_gx1.cuh), 0 the fused kernel
     int opt_gx1_dp4a = 0;       // order-1 gather: 1 byte-plane dp4a contraction, 0 three 21-bit IMAD limbs
-    int opt_global_banded = 1;  // bsf_run, global mode: 1 scans and gather in row bands (overlapped), 0 one after the other
     int opt_i8_tc = 0;          // order 3: 1 the exact limbs on tcgen05 kind::i8 (bsf_fused.cuh i8_tile), 0 DMMA
     double opt_split_tol = BSF_SPLIT_TOL_DEFAULT;
 };
@@ -1163,7 +1162,7 @@ static bsf_status filter_global(bsf_plan_s *p, const void *g, const void *cov, v
 // the order-1 gather on output rows [y0, y0 + h) only (cov and out hold those
 // rows: [batch][3][h][W] and [nimg][h][W]); y0 a multiple of 32
 static bsf_status filter_global_window(bsf_plan_s *p, const void *g, const void *cov, void *out, int y0, int h,
-                                       int rows_ready, cudaStream_t st, int full = 0) {
+                                       int rows_ready, cudaStream_t st) {
     bsf_status s = ensure_tile_ws(p, false);
     if (s != BSF_OK) return s;
     const Geometry &geo = p->geo;
@@ -1176,7 +1175,6 @@ static bsf_status filter_global_window(bsf_plan_s *p, const void *g, const void 
     a.gGHv = rows_ready;
     a.oy0 = y0;
     a.oH = h;
-    a.ofull = full;  // 1: cov / out are the whole images, 0: they hold rows [y0, y0 + h) only
     for (int sl = 0; sl < geo.nbases; ++sl) {
         a.gglob[p->bases[sl]] = (const long long *)g + sl * slot;
         a.gshift[p->bases[sl]] = p->gshift[p->bases[sl]];
@@ -1187,10 +1185,8 @@ static bsf_status filter_global_window(bsf_plan_s *p, const void *g, const void 
     return BSF_OK;
 }
 
-static bsf_status run_global_banded(bsf_plan_s *p, const void *f, const void *cov, void *out, cudaStream_t st);
 static bsf_status run_global(bsf_plan_s *p, const void *f, const void *cov, void *out, const int *pts, int npts,
                              double *aux, cudaStream_t st) {
-    if (!pts && !aux && p->opt_global_banded && p->d.nranks <= 1) return run_global_banded(p, f, cov, out, st);
     if (!p->gx_ws) {
         void *q;
         const size_t bytes = g_bytes(p) / 2;  // int64 elements
@@ -1497,11 +1493,7 @@ extern "C" bsf_status bsf_run_alg1(bsf_plan_t p, const void *f, const void *cov,
 // loads assume a 4-byte aligned base
 static size_t host_f_pitch(const Geometry &g) { return ((size_t)g.H * g.W + 15) / 16 * 16; }
 
-// scan band k (image rows [k srows, ...)) of basis slot sl: every level, the
-// carries of the band above in, this band's out; fb / fpitch: the u8 images
-// and their pitch in bytes (staged host copy, or the caller's device images)
-static bsf_status banded_scans_basis(bsf_plan_s *p, int sl, int k, int srows, int nsb, cudaStream_t ss,
-                                     const uint8_t *fb, size_t fpitch) {
+static bsf_status banded_scans_basis(bsf_plan_s *p, int sl, int k, int srows, int nsb, cudaStream_t ss) {
     const Geometry &g = p->geo;
     const int nlev = 4 * p->d.order;
     const size_t GW = g.GW, rowset = (size_t)g.nimg * 2 * GW;  // one level's carry: [nimg][2][GW]
@@ -1520,7 +1512,7 @@ static bsf_status banded_scans_basis(bsf_plan_s *p, int sl, int k, int srows, in
         unsigned long long *cin = p->hcarry + (((size_t)((k + 1) & 1) * 2 + sl) * nlev + lv) * rowset;
         unsigned long long *cout = p->hcarry + (((size_t)(k & 1) * 2 + sl) * nlev + lv) * rowset;
         for (int i = 0; i < g.nimg; ++i) {
-            const uint8_t *fi = fb + (size_t)i * fpitch + (size_t)y0 * g.W;
+            const uint8_t *fi = (const uint8_t *)p->f_stage + (size_t)i * host_f_pitch(g) + (size_t)y0 * g.W;
             unsigned long long *gi = gsl + ((size_t)i * g.GH + y0) * GW;
             CUDA_TRY(launch_scan_level(fi, 1, gi, 1, gs, p->bases[sl], lv,
                                        (sy > 0 && k > 0) ? cin + (size_t)i * 2 * GW : nullptr, ss));
@@ -1534,10 +1526,10 @@ static bsf_status banded_scans_basis(bsf_plan_s *p, int sl, int k, int srows, in
     return BSF_OK;
 }
 
-// streams, events, the int64 sums and the banded scans' carry rows of the
-// global-mode pipelines (bsf_run_host, and bsf_run's banded form), once per plan
-static bsf_status ensure_pipeline(bsf_plan_s *p) {
+static bsf_status run_host_global(bsf_plan_s *p, const void *f_host, const void *cov_host, void *out_host,
+                                  cudaStream_t st) {
     const Geometry &g = p->geo;
+    const int nb = BSF_HOST_BANDS;
     if (!p->s_in) {
         CUDA_TRY(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
@@ -1550,6 +1542,10 @@ static bsf_status ensure_pipeline(bsf_plan_s *p) {
             for (int sl = 0; sl < 2; ++sl) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_sb[sl][i], cudaEventDisableTiming));
         }
     }
+    cudaEvent_t ev_start = p->ev[0], ev_end = p->ev[2], ev_c2 = p->ev[4];
+    cudaEvent_t *ev_cov = p->ev + 5, *ev_band = p->ev + 5 + BSF_HOST_BANDS;
+    p->last = st;
+    const size_t plane = (size_t)g.H * g.W, oes = p->d.out_dtype == BSF_F32 ? 4 : 8;
     if (!p->gx_ws) {
         void *q;
         const size_t bytes = g_bytes(p) / 2;
@@ -1565,69 +1561,6 @@ static bsf_status ensure_pipeline(bsf_plan_s *p) {
         p->dev_allocs.push_back(q);
         p->hcarry = (unsigned long long *)q;
     }
-    return BSF_OK;
-}
-
-// bsf_run in global mode with the inputs in device memory: the host
-// pipeline's schedule without its copies.  The images are pre-integrated in
-// BSF_SCAN_BANDS row bands (each level of a band starts from the carry rows
-// of the band above; one stream per basis), and the gather runs in
-// BSF_HOST_BANDS row bands on two alternating streams, each band as soon as
-// the scan bands its footprint reaches are done: the HBM-bound scans of the
-// lower bands overlap the compute-bound gather of the upper ones.  The
-// arithmetic is the unbanded path's (bit-identical int64 sums, same gather).
-static bsf_status run_global_banded(bsf_plan_s *p, const void *f, const void *cov, void *out, cudaStream_t st) {
-    const Geometry &g = p->geo;
-    const int nb = BSF_HOST_BANDS;
-    {
-        const bsf_status e = ensure_pipeline(p);
-        if (e != BSF_OK) return e;
-    }
-    cudaEvent_t ev_start = p->ev[0], ev_c2 = p->ev[4];
-    p->last = st;
-    const int rows = ((g.H + nb - 1) / nb + 31) / 32 * 32;
-    const int per = std::max(1, ((g.H + BSF_SCAN_BANDS - 1) / BSF_SCAN_BANDS + rows - 1) / rows);
-    const int srows = per * rows;
-    const int nsb = (g.H + srows - 1) / srows;
-    CUDA_TRY(cudaEventRecord(ev_start, st));  // earlier work on the caller's stream comes first
-    for (int k = 0; k < nsb; ++k) CUDA_TRY(cudaEventRecord(p->ev_fb[k], st));  // the images are in already
-    for (int sl = 0; sl < g.nbases; ++sl) {
-        CUDA_TRY(cudaStreamWaitEvent(p->s_scan[sl], ev_start, 0));
-        for (int k = 0; k < nsb; ++k) {
-            const bsf_status e = banded_scans_basis(p, sl, k, srows, nsb, p->s_scan[sl], (const uint8_t *)f,
-                                                    (size_t)g.H * g.W);
-            if (e != BSF_OK) return e;
-        }
-    }
-    CUDA_TRY(cudaStreamWaitEvent(p->s_c2, ev_start, 0));
-    int band = 0;
-    for (int yb = 0; yb < g.H; yb += rows, ++band) {
-        const int hb = std::min(rows, g.H - yb);
-        cudaStream_t sc = (band & 1) ? p->s_c2 : st;
-        const int kneed = std::min(nsb - 1, (yb + hb - 1 + g.Pb) / srows);
-        for (int sl = 0; sl < g.nbases; ++sl) CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_sb[sl][kneed], 0));
-        const int ready = kneed == nsb - 1 ? g.GH : (kneed + 1) * srows;
-        const bsf_status e = filter_global_window(p, p->gx_ws, cov, out, yb, hb, ready, sc, 1);
-        if (e != BSF_OK) return e;
-    }
-    CUDA_TRY(cudaEventRecord(ev_c2, p->s_c2));
-    CUDA_TRY(cudaStreamWaitEvent(st, ev_c2, 0));
-    for (int sl = 0; sl < g.nbases; ++sl) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_sb[sl][nsb - 1], 0));
-    return BSF_OK;
-}
-
-static bsf_status run_host_global(bsf_plan_s *p, const void *f_host, const void *cov_host, void *out_host,
-                                  cudaStream_t st) {
-    const Geometry &g = p->geo;
-    const int nb = BSF_HOST_BANDS;
-    {
-        const bsf_status e = ensure_pipeline(p);
-        if (e != BSF_OK) return e;
-    }
-    cudaEvent_t ev_start = p->ev[0], ev_end = p->ev[2], ev_c2 = p->ev[4];
-    cudaEvent_t *ev_cov = p->ev + 5, *ev_band = p->ev + 5 + BSF_HOST_BANDS;
-    p->last = st;
-    const size_t plane = (size_t)g.H * g.W, oes = p->d.out_dtype == BSF_F32 ? 4 : 8;
     // gather bands of whole tiles (rows multiple of 32); image (scan) bands of
     // whole gather bands
     const int rows = ((g.H + nb - 1) / nb + 31) / 32 * 32;
@@ -1648,8 +1581,7 @@ static bsf_status run_host_global(bsf_plan_s *p, const void *f_host, const void 
                                      cudaMemcpyHostToDevice, p->s_in));
         CUDA_TRY(cudaEventRecord(p->ev_fb[k], p->s_in));
         for (int sl = 0; sl < g.nbases; ++sl) {
-            const bsf_status e = banded_scans_basis(p, sl, k, srows, nsb, p->s_scan[sl], (const uint8_t *)p->f_stage,
-                                                    host_f_pitch(g));
+            const bsf_status e = banded_scans_basis(p, sl, k, srows, nsb, p->s_scan[sl]);
             if (e != BSF_OK) return e;
         }
         for (int yb = y0; yb < y0 + h; yb += rows, ++band) {
@@ -1808,8 +1740,6 @@ extern "C" bsf_status bsf_debug_option(bsf_plan_t p, const char *name, double va
         p->opt_i8_tc = value != 0.0 ? 1 : 0;
     } else if (n == "gx1_dp4a") {
         p->opt_gx1_dp4a = value != 0.0 ? 1 : 0;
-    } else if (n == "global_banded") {
-        p->opt_global_banded = value != 0.0 ? 1 : 0;
     } else if (n == "split_tol") {
         if (!(value >= 0.0)) return set_err(BSF_EINVAL, "split_tol must be >= 0");
         p->opt_split_tol = value;

@@ -197,23 +197,20 @@ __device__ __forceinline__ int out_rows(const TileArgs &a) { return a.oH ? a.oH 
 __device__ __forceinline__ bool out_row(const TileArgs &a, int y) {
     return y >= a.oy0 && y < a.oy0 + out_rows(a) && y < a.H;
 }
-// rows held by cov / out and the image row of their first row
-__device__ __forceinline__ int io_rows(const TileArgs &a) { return a.ofull ? a.H : out_rows(a); }
-__device__ __forceinline__ int io_row0(const TileArgs &a) { return a.ofull ? 0 : a.oy0; }
 __device__ __forceinline__ long long out_index(const TileArgs &a, int img, int x, int y) {
-    return ((long long)img * io_rows(a) + (y - io_row0(a))) * a.W + x;
+    return ((long long)img * out_rows(a) + (y - a.oy0)) * a.W + x;
 }
 
 __device__ __forceinline__ void load_cov(const TileArgs &a, int img, int x, int y, double &sx, double &sy,
                                          double &th) {
-    const size_t ipl = (size_t)io_rows(a) * a.W;
+    const size_t ipl = (size_t)out_rows(a) * a.W;
     const int b = img / a.channels;
     if (a.cov_mode == COV_ISO) {
         sx = sy = sqrt(a.sigma2[b] * a.sigma2_scale);
         th = 0.0;
         return;
     }
-    const float *cv = a.cov + (size_t)b * 3 * ipl + (size_t)(y - io_row0(a)) * a.W + x;
+    const float *cv = a.cov + (size_t)b * 3 * ipl + (size_t)(y - a.oy0) * a.W + x;
     sx = __ldg(cv);
     sy = __ldg(cv + ipl);
     th = __ldg(cv + 2 * ipl);

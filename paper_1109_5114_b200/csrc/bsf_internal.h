@@ -188,8 +188,6 @@ struct TileArgs {
     // [oy0, oy0 + oH) of the f block are filtered (oy0 a multiple of the
     // super-tile side); cov and out hold those rows only.  oH = 0: all rows.
     int oy0, oH;
-    int ofull;                  // 1: cov and out are whole images (rows [0, H)) although only the
-                                // window's rows are filtered (bsf_run's banded global pipeline)
     int cov_layout;             // BSF_COV_SIGMA_THETA / BSF_COV_C11_C12_C22
     const int *tiles;           // optional list of anchoring-tile indices to compute (bsf_run_tiles);
     int ntiles;                 // index = (img * tiles_y + ty) * tiles_x + tx in units of the plan's tile side

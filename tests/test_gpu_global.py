@@ -199,36 +199,3 @@ def test_gx1_dp4a_config3_full_size_bit_identical():
         plan.debug_option("gx1_dp4a", dp)
         outs.append(gpu_full(plan, img[None], cov))
     assert torch.equal(outs[0], outs[1])
-
-
-@pytest.mark.parametrize("shape", [(4096, 4096, 1, 1, False), (517, 333, 2, 2, False), (129, 70, 1, 3, True),
-                                   (40, 37, 2, 1, True)])
-def test_run_banded_equals_unbanded(shape):
-    """bsf_run in global mode with the inputs in HBM runs the scans and the
-    gather in row bands on several streams (plan option global_banded, the
-    default); the output equals the unbanded schedule (every scan, then the
-    gather) bit for bit: full config-3 size, ragged sizes, batch / channels,
-    f32 output, images smaller than one band."""
-    W, H, batch, channels, out_f32 = shape
-    w = synth.workload(3, width=W, height=H, extra={"grid_span": 4096})
-    dev = torch.device("cuda:0")
-    imgs = torch.stack([synth.make_image(w, frame=f, channel=c) for f in range(batch) for c in range(channels)])
-    covs = torch.stack([synth.make_cov(w, frame=f) for f in range(batch)])
-    outs = []
-    for banded in (0, 1):
-        plan = bsf.Plan(W, H, batch=batch, channels=channels, in_dtype=bsf.BSF_U8,
-                        out_dtype=bsf.BSF_F32 if out_f32 else bsf.BSF_F64, order=1, basis=w.basis,
-                        max_sigma=w.max_sigma, anchor=bsf.BSF_ANCHOR_GLOBAL)
-        assert plan.geometry.global_mode == 1
-        plan.debug_option("global_banded", banded)
-        out = torch.full((batch * channels, H, W), float("nan"), dtype=torch.float32 if out_f32 else torch.float64,
-                         device=dev)
-        n0 = plan.launch_count()
-        plan.run(imgs.to(dev).contiguous(), covs.to(dev).contiguous(), out)
-        torch.cuda.synchronize()
-        assert plan.stats(reset=True)["status"] == 0
-        if banded and H >= 1024:
-            assert plan.launch_count() - n0 > 9  # several scan and gather bands
-        outs.append(out.cpu())
-    assert not torch.isnan(outs[1]).any()
-    assert torch.equal(outs[0], outs[1])
