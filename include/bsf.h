@@ -80,7 +80,8 @@ typedef enum {
     BSF_ANCHOR_GLOBAL = 0, /* the paper's single pre-integration of the whole image.
                             * u8 input at order 1 with every running sum below 2^62 ("global mode",
                             * bsf_geometry.global_mode = 1): exact int64 sums (bsf_preintegrate_exact)
-                            * gathered by the fused kernel with an exact contraction.
+                            * gathered by gx1_kernel with an exact int32-limb contraction (DESIGN.md
+                            * §6.3; the fused kernel's DMMA groups as bsf_debug_option global_kernel 0).
                             * Otherwise double-double sums (bsf_preintegrate) + the per-pixel
                             * double-double gather (bsf_filter), whose rounding grows with the image
                             * size                                                      */
