@@ -42,6 +42,10 @@ def main():
         if os.path.exists(os.path.join(ROOT, path)):
             rr = per_kernel(path)
             caps["c3_4096_u8_grid32/r%d/fused_kernel" % r] = {"dram_bytes": rr[0][1], "src_hash": sh, "file": path}
+    path = "profiles/r02_r4_tile_raw.csv"
+    if os.path.exists(os.path.join(ROOT, path)):
+        rr = [b for k, b in per_kernel(path) if "tile_kernel" in k]
+        caps["c3_4096_u8_grid32/r4/tile_kernel"] = {"dram_bytes": rr[0], "src_hash": sh, "file": path}
     doc = {"what": "dram__bytes_read.sum + dram__bytes_write.sum per launch (per step for the 8 scan launches of "
                    "order 1), one ncu --set full --clock-control none capture of tools/step_probe.py on config 3 "
                    "(tools/gpu/r02_final2.sh); bench.py reports them only while src_hash matches the CUDA sources",
