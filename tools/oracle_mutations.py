@@ -48,6 +48,47 @@ MUTATIONS = [
     ("pre-integration: step sign",
      "int py = y - sy, pxi = xi - sx;",
      "int py = y - sy, pxi = xi + sx;"),
+    # second batch: the remaining terms of the covariance / kurtosis formulas,
+    # the gradient, the decode diagonal, the bounds and the sector choice
+    ("Theta covariance: C11 weight of u1 2 -> 1",
+     "C[0] = (2 * u1 + u2 + u4) / 24.0;",
+     "C[0] = (u1 + u2 + u4) / 24.0;"),
+    ("Theta covariance: C22 takes u1 for u3",
+     "C[2] = (2 * u3 + u2 + u4) / 24.0;",
+     "C[2] = (2 * u1 + u2 + u4) / 24.0;"),
+    ("Theta' covariance: C12 sign of u2",
+     "C[1] = 2 * (u1 + u2 - u3 - u4) / 60.0;",
+     "C[1] = 2 * (u1 - u2 - u3 - u4) / 60.0;"),
+    ("Theta' covariance: C22 weight of u3 4 -> 1",
+     "C[2] = (u1 + 4 * u2 + 4 * u3 + u4) / 60.0;",
+     "C[2] = (u1 + 4 * u2 + u3 + u4) / 60.0;"),
+    ("Theta' kurtosis: K12 sign of q3",
+     "K[1] = 2 * (q1 + q2 - q3 - q4) / 5.0;",
+     "K[1] = 2 * (q1 + q2 + q3 - q4) / 5.0;"),
+    ("Theta kurtosis: K11 weight of q2 1/2 -> 1",
+     "K[0] = q1 + q2 / 2 + q4 / 2;",
+     "K[0] = q1 + q2 + q4 / 2;"),
+    ("Theta kurtosis: K12 = (q2 + q4)/2",
+     "K[1] = (q2 - q4) / 2;",
+     "K[1] = (q2 + q4) / 2;"),
+    ("gradient: off-diagonal weight 2 -> 1",
+     "return 2 * (K[0] * dK[0] + 2 * K[1] * dK[1] + K[2] * dK[2]);",
+     "return 2 * (K[0] * dK[0] + K[1] * dK[1] + K[2] * dK[2]);"),
+    ("decode: C11 and C22 swapped trigonometry",
+     "C[0] = vx * c * c + vy * s * s;",
+     "C[0] = vx * s * s + vy * c * c;"),
+    ("Theta' bound: 4/5 -> 3/5 on sin",
+     "double b2 = s2 > 0 ? 0.8 / s2 : INFINITY;",
+     "double b2 = s2 > 0 ? 0.6 / s2 : INFINITY;"),
+    ("Theta bound: 1/(s2 + c2) -> 1/max",
+     "if (basis == OR_THETA) return 1.0 / (s2 + c2);",
+     "if (basis == OR_THETA) return 1.0 / (s2 > c2 ? s2 : c2);"),
+    ("orientation: minor axis not rotated by pi/2",
+     "p = th + M_PI / 2;",
+     "p = th;"),
+    ("select: sector comparison inverted",
+     "return or_bound_e(OR_THETA_PRIME, phi) > or_bound_e(OR_THETA, phi) ? OR_THETA_PRIME : OR_THETA;",
+     "return or_bound_e(OR_THETA_PRIME, phi) < or_bound_e(OR_THETA, phi) ? OR_THETA_PRIME : OR_THETA;"),
 ]
 
 
