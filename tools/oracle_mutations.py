@@ -3,7 +3,7 @@
 Applies plausible single-point mistakes to a copy of oracle/bsf_oracle.c in a
 temporary directory, rebuilds it there and runs the `-m "not gpu"` oracle pins
 against it; every mutation must make at least one pin fail.  Usage:
-    python tools/oracle_mutations.py
+    python tools/oracle_mutations.py [first]
 """
 import os
 import shutil
@@ -89,7 +89,32 @@ MUTATIONS = [
     ("select: sector comparison inverted",
      "return or_bound_e(OR_THETA_PRIME, phi) > or_bound_e(OR_THETA, phi) ? OR_THETA_PRIME : OR_THETA;",
      "return or_bound_e(OR_THETA_PRIME, phi) < or_bound_e(OR_THETA, phi) ? OR_THETA_PRIME : OR_THETA;"),
+    # third batch: the clamp branch, the support window, the image edge
+    ("clamp: rho bound (1 + e)/(1 - e) inverted",
+     "double rb = (1 + eb) / (1 - eb);",
+     "double rb = (1 - eb) / (1 + eb);"),
+    ("clamp: trace not preserved (T = sx^2)",
+     "double T = sx * sx + sy * sy;",
+     "double T = sx * sx;"),
+    ("clamp: eigenvalues swapped",
+     "double l1 = T * (1 + e) / 2, l2 = T * (1 - e) / 2;",
+     "double l1 = T * (1 - e) / 2, l2 = T * (1 + e) / 2;"),
+    ("clamp: C12 sign",
+     "C[1] = (l1 - l2) * c * s;",
+     "C[1] = -(l1 - l2) * c * s;"),
+    ("support: half extent r a/2 -> a/2",
+     "sx += 0.5 * r * a[k] * fabs(u[k][0]);",
+     "sx += 0.5 * a[k] * fabs(u[k][0]);"),
+    ("edge: pixels outside the image replicate instead of zero",
+     "if (x < 0 || y < 0 || x >= im->W || y >= im->H) return 0.0;",
+     "if (x < 0 || y < 0 || x >= im->W || y >= im->H) return 1.0;"),
+    ("direct sum: window clipped one column short",
+     "if (x1 > im->W - 1) x1 = im->W - 1;",
+     "if (x1 > im->W - 2) x1 = im->W - 2;"),
 ]
+
+
+FIRST = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # skip the first FIRST mutations
 
 
 def main() -> int:
@@ -99,7 +124,7 @@ def main() -> int:
         shutil.copytree(os.path.join(ROOT, "oracle"), os.path.join(tmp, "oracle"))
         shutil.copytree(os.path.join(ROOT, "tests"), os.path.join(tmp, "tests"))
         shutil.copy(os.path.join(ROOT, "pytest.ini"), tmp)
-        for name, old, new in MUTATIONS:
+        for name, old, new in MUTATIONS[FIRST:]:
             assert src.count(old) == 1, name
             with open(os.path.join(tmp, "oracle", "bsf_oracle.c"), "w") as fh:
                 fh.write(src.replace(old, new))
