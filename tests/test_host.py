@@ -117,3 +117,25 @@ def test_binding_validates_tensors_before_the_c_abi():
                  (t.view(2, 5).t(), "x", ["float32"], 10, "cpu"), (t, "x", ["float32"], 10, 0)):
         with pytest.raises(bsf.BsfError):
             bsf._want(*args)
+
+
+def test_oracle_mutation_sites_exist():
+    """tools/oracle_mutations.py (the mutation check of the pins): every
+    mutation's original text occurs exactly once in oracle/bsf_oracle.c and
+    differs from its replacement, so the tool keeps mutating what it names."""
+    import importlib.util
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("oracle_mutations", os.path.join(root, "tools", "oracle_mutations.py"))
+    m = importlib.util.module_from_spec(spec)
+    argv, sys_mod = None, __import__("sys")
+    argv, sys_mod.argv = sys_mod.argv, ["oracle_mutations.py"]
+    try:
+        spec.loader.exec_module(m)
+    finally:
+        sys_mod.argv = argv
+    src = open(os.path.join(root, "oracle", "bsf_oracle.c")).read()
+    assert len(m.MUTATIONS) >= 31
+    for name, old, new in m.MUTATIONS:
+        assert src.count(old) == 1, name
+        assert old != new, name
