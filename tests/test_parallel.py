@@ -75,7 +75,9 @@ def _worker(rank, world, port, H, W, q):
         ok_blk = torch.equal(blk, full[st.b0:st.b1])
         cov = torch.ones(3, st.y1 - st.y0, W)
         res = PL.filter_strip(_StandIn(st), own[None], cov, st, H)[0]
-        q.put((rank, ok_blk, st.y0, st.y1, res))
+        # by value (numpy): a torch tensor travels as a shared-memory handle
+        # that dies with this process if it exits before the parent reads it
+        q.put((rank, ok_blk, st.y0, st.y1, res.numpy().copy()))
     finally:
         dist.destroy_process_group()
 
@@ -107,7 +109,7 @@ def test_row_strips_reproduce_full_image(world):
     _StandIn().run(full, None, ref)
     for rank, ok_blk, y0, y1, res in got:
         assert ok_blk, rank
-        assert torch.equal(res, ref[0, y0:y1]), rank
+        assert torch.equal(torch.from_numpy(res), ref[0, y0:y1]), rank
 
 
 class _ScanStandIn:
@@ -162,7 +164,7 @@ def _global_worker(rank, world, port, H, W, P, Pb, q):
         plan = _ScanStandIn(W, P, st.Y1 - st.Y0, order=1)
         g = torch.zeros((st.Y1 - st.Y0) * (W + 2 * P), dtype=torch.int64)
         PL.preintegrate_global_strips(plan, img[st.Y0:st.Y0 + st.height], g, st)
-        q.put((rank, st.Y0, st.Y1, g.view(st.Y1 - st.Y0, W + 2 * P)))
+        q.put((rank, st.Y0, st.Y1, g.view(st.Y1 - st.Y0, W + 2 * P).numpy().copy()))
     finally:
         dist.destroy_process_group()
 
@@ -184,13 +186,13 @@ def test_global_mode_carry_chain_gloo():
     procs = [ctx.Process(target=_global_worker, args=(r, world, port, H, W, P, Pb, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=120) for _ in range(world)])
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res[0][1] == 0 and res[-1][2] == H + Pb
     for rank, Y0, Y1, g in res:
-        assert torch.equal(g, ref[Y0:Y1]), "rank %d rows [%d, %d) differ" % (rank, Y0, Y1)
+        assert torch.equal(torch.from_numpy(g), ref[Y0:Y1]), "rank %d rows [%d, %d) differ" % (rank, Y0, Y1)
 
 
 @pytest.mark.parametrize("H,unit,halo", [(1000, 32, 96), (4096, 64, 128), (352, 32, 32), (777, 16, 48)])
